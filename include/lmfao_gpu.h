@@ -1,0 +1,184 @@
+/* lmfao_gpu.h — C ABI of the B200-native LMFAO hot path.
+ *
+ * Evaluates a batch of group-by aggregates over the natural join of an acyclic
+ * schema, bottom-up over a join tree, without materialising the join
+ * (§3 "Problem Statement" P:336-347, §4):
+ *
+ *     Q(F_1..F_f; α_1..α_ℓ) += R_1(ω_1), …, R_m(ω_m)
+ *     α_i = Σ_j Π_k f_ijk,  f ∈ {constant, identity, Kronecker 1_{X op t}}
+ *
+ * Semantics (DESIGN.md §3 readings): bag semantics (duplicates multiply, tuples
+ * with dangling keys vanish); a query with no group-by attribute returns exactly
+ * one row, also over an empty join (value 0, count 0); a query with group-by
+ * attributes returns exactly the groups present in the join, in ascending
+ * lexicographic order of the group-key tuple (in the order the attributes were
+ * listed), together with each group's join multiplicity ("count").
+ *
+ * Conventions
+ *  - Every function returns lmfao_status.  No C++ exception, abort or CUDA error
+ *    crosses this boundary; after a non-OK status lmfao_last_error(ctx) returns a
+ *    message (valid until the next call on that ctx).
+ *  - Call order: create -> add_relation* -> set_join_tree -> prepare ->
+ *    add_query* -> plan -> run* -> (result_shape | fetch | result_device)*.
+ *    A call out of order returns LMFAO_ERR_STATE.  run may be repeated.
+ *  - One ctx per (process, GPU); a ctx is not thread-safe.
+ *  - Inputs are copied (the caller keeps ownership).  Host output buffers are
+ *    caller-owned; device views returned by lmfao_result_device are
+ *    library-owned and valid until the next run/destroy.
+ *  - Multi-GPU (world > 1): each rank passes the whole root relation; after the
+ *    global sort in lmfao_prepare the rank keeps its contiguous shard of the
+ *    sorted root (domain parallelism), dimension relations are
+ *    replicated, and lmfao_run combines the partial aggregates with an NCCL
+ *    all-reduce over NVLink, so every rank holds the full results.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one returns LMFAO_ERR_CUDA.
+ */
+#ifndef LMFAO_GPU_H
+#define LMFAO_GPU_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LMFAO_API __attribute__((visibility("default")))
+#else
+#define LMFAO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LMFAO_OK = 0,
+  LMFAO_ERR_INVALID_ARG = 1,        /* null pointer, negative size, bad enum, duplicate name */
+  LMFAO_ERR_STATE = 2,              /* call out of order */
+  LMFAO_ERR_UNKNOWN_ATTR = 3,       /* attribute / relation name or id does not exist */
+  LMFAO_ERR_TYPE = 4,               /* join or group-by attribute not int32; dtype mismatch */
+  LMFAO_ERR_CYCLIC_TREE = 5,        /* join tree has a cycle */
+  LMFAO_ERR_DISCONNECTED_TREE = 6,  /* join tree does not span all relations */
+  LMFAO_ERR_RUNNING_INTERSECTION = 7, /* ω_i ∩ ω_j ⊄ ω_k for some R_k on the path */
+  LMFAO_ERR_UNSUPPORTED = 8,        /* v1 limits: multi-attribute join keys, group-by on an attribute
+                                       not functionally determined by the root row (see lmfao_add_query) */
+  LMFAO_ERR_OOM = 9,                /* device allocation failed */
+  LMFAO_ERR_CUDA = 10,              /* CUDA runtime error / no device */
+  LMFAO_ERR_NCCL = 11               /* NCCL error (multi-GPU) */
+} lmfao_status;
+
+typedef enum { LMFAO_INT32 = 0, LMFAO_FP64 = 1 } lmfao_dtype;
+
+/* Per-attribute functions f of a product term: constant, identity, and
+ * the Kronecker delta 1_{X op t} for op in {<, <=, >, >=, =, !=}, compared in
+ * IEEE double (int32 attributes convert exactly). */
+typedef enum {
+  LMFAO_F_CONST = 0, LMFAO_F_IDENT = 1, LMFAO_F_LT = 2, LMFAO_F_LE = 3,
+  LMFAO_F_GT = 4, LMFAO_F_GE = 5, LMFAO_F_EQ = 6, LMFAO_F_NE = 7
+} lmfao_fkind;
+
+typedef struct {
+  int32_t kind;   /* lmfao_fkind */
+  int32_t attr;   /* attribute id (lmfao_attr_id); -1 for LMFAO_F_CONST */
+  double param;   /* CONST: the value; predicates: the threshold t */
+} lmfao_factor;
+
+typedef struct {
+  double coeff;                 /* multiplies the product */
+  int32_t n_factors;            /* >= 0; 0 means the product is just coeff */
+  const lmfao_factor* factors;
+} lmfao_product;
+
+typedef struct {
+  int32_t n_products;           /* α = Σ products; 0 means α ≡ 0 */
+  const lmfao_product* products;
+} lmfao_udaf;
+
+typedef struct lmfao_ctx lmfao_ctx;
+
+/* Size of the opaque id passed to lmfao_create for world > 1 (ncclUniqueId). */
+#define LMFAO_UNIQUE_ID_BYTES 128
+
+/* Fills `out` (LMFAO_UNIQUE_ID_BYTES bytes) with a fresh NCCL unique id; call on
+ * rank 0 and broadcast it (the Python harness uses a torch.distributed
+ * broadcast).  LMFAO_ERR_NCCL if NCCL cannot be loaded. */
+LMFAO_API lmfao_status lmfao_unique_id(void* out);
+
+/* Creates a context on CUDA device `device`.  world >= 1, 0 <= rank < world;
+ * unique_id must be non-NULL iff world > 1 (collective call across ranks). */
+LMFAO_API lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id, lmfao_ctx** out);
+LMFAO_API lmfao_status lmfao_destroy(lmfao_ctx* ctx);
+LMFAO_API const char* lmfao_last_error(const lmfao_ctx* ctx);
+
+/* Registers relation R(ω) (relations R_1..R_m over schemas ω_1..ω_m) as
+ * SoA columns: cols[i] points to nrows values of dtypes[i] (host memory, or
+ * device memory on this ctx's device if cols_on_device != 0).  Copied
+ * synchronously.  Attributes with the same name in different relations are the
+ * natural-join attributes (X = ∪ω).  *rel_id receives the relation id. */
+LMFAO_API lmfao_status lmfao_add_relation(lmfao_ctx* ctx, const char* name, int64_t nrows, int32_t ncols,
+                                const char* const* col_names, const lmfao_dtype* dtypes,
+                                const void* const* cols, int cols_on_device, int32_t* rel_id);
+
+/* Attribute id of a column name (ids are global over the schema X). */
+LMFAO_API lmfao_status lmfao_attr_id(lmfao_ctx* ctx, const char* attr_name, int32_t* attr_id);
+
+/* Registers the rooted join tree: n_edges = m-1 edges parent->child.
+ * Validates: connected, acyclic, each relation has at most one parent, the
+ * running-intersection property, and (v1) that every edge shares exactly
+ * one attribute, of type int32. */
+LMFAO_API lmfao_status lmfao_set_join_tree(lmfao_ctx* ctx, int32_t root_rel, int32_t n_edges,
+                                 const int32_t* parent_rel, const int32_t* child_rel);
+
+/* Simulated sharding for testing the multi-GPU partition on one device: keep
+ * part `part` of `nparts` contiguous parts of the sorted root (default: rank of
+ * world).  Must precede lmfao_prepare. */
+LMFAO_API lmfao_status lmfao_set_root_shard(lmfao_ctx* ctx, int32_t part, int32_t nparts);
+
+/* Load-time preprocessing, kernel (a) ("We sort S in this order";
+ * P:42 "We sort the relations once"): dense remap of every join key (rank
+ * among the child's distinct key values; dangling foreign keys drop the row,
+ * inner-join semantics), sort of each child by its key, and one composite LSD
+ * radix sort of the root by its foreign keys in increasing domain-size order
+ * (the MOO attribute order). Then sharding (see above). */
+LMFAO_API lmfao_status lmfao_prepare(lmfao_ctx* ctx);
+
+/* Adds Q(F; α_1..α_n) += R_1..R_m.  groupby_attrs: int32 attributes
+ * (LMFAO_ERR_TYPE otherwise) owned by the root or by a child of the root whose
+ * join key is unique in that child (v1; otherwise LMFAO_ERR_UNSUPPORTED).
+ * n_groupby may be 0.  Each product's factors must name existing attributes
+ * (CONST: attr = -1).  The batch is copied. */
+LMFAO_API lmfao_status lmfao_add_query(lmfao_ctx* ctx, int32_t n_groupby, const int32_t* groupby_attrs,
+                             int32_t n_udafs, const lmfao_udaf* udafs, int32_t* query_id);
+
+/* Host planner: pushes every product down the join tree, dedups
+ * view slots across the batch (view merging), picks the kernels and
+ * allocates all device buffers.  Freezes the batch. */
+LMFAO_API lmfao_status lmfao_plan(lmfao_ctx* ctx);
+
+/* Runs the planned batch asynchronously on `cuda_stream` (cudaStream_t; NULL =
+ * the ctx's own stream): view builds (b), the fused root scan (c) with its FP64
+ * Gram tiles (d) and histograms (e), dimension-side finishing, the NCCL
+ * all-reduce when world > 1, and compaction.  No host synchronisation. */
+LMFAO_API lmfao_status lmfao_run(lmfao_ctx* ctx, void* cuda_stream);
+
+/* Result shape of query_id after the last run (synchronises the stream). */
+LMFAO_API lmfao_status lmfao_result_shape(lmfao_ctx* ctx, int32_t query_id, int64_t* n_groups,
+                                int32_t* n_groupby, int32_t* n_udafs);
+
+/* Copies query_id's result to caller-owned HOST buffers (synchronises):
+ * keys_out [n_groups x n_groupby] int32 row-major (may be NULL if n_groupby = 0),
+ * vals_out [n_groups x n_udafs] double row-major, counts_out [n_groups] uint64
+ * join multiplicity of each group (nullable). Groups in ascending key order. */
+LMFAO_API lmfao_status lmfao_fetch(lmfao_ctx* ctx, int32_t query_id, int32_t* keys_out, double* vals_out,
+                         uint64_t* counts_out);
+
+/* Library-owned device views of query_id's result (same layout as fetch). */
+LMFAO_API lmfao_status lmfao_result_device(lmfao_ctx* ctx, int32_t query_id, const int32_t** keys,
+                                 const double** vals, const uint64_t** counts);
+
+/* Diagnostics: fills `out` (up to `cap` bytes) with a JSON object describing
+ * the plan (kernel path per query group, view widths, run counts per level after
+ * the last run, kernel launches per run). */
+LMFAO_API lmfao_status lmfao_plan_info(lmfao_ctx* ctx, char* out, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMFAO_GPU_H */

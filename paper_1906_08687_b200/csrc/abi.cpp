@@ -1,0 +1,825 @@
+// abi.cpp — the C ABI of liblmfao_gpu (include/lmfao_gpu.h): context, schema and
+// join-tree validation, load-time preprocessing (kernel (a)), the host planner
+// and the run orchestration.
+//
+// Planner (§4): every product term of the batch is pushed down the join
+// tree (aggregate pushdown: a view V_{C->S}(F_i; α_i) per child with
+// α_i the part of the product over the child's subtree); identical partial
+// products share one slot of the child's view (view merging cases (2)/(3),
+// P:961-1000); slot 0 of every view is the count, so multiplicities carry bag
+// semantics.  All queries are computed at one root (the user's), whose sorted
+// scan is the single shared pass over the largest relation (MOO).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <functional>
+#include <set>
+#include <sstream>
+#include <tuple>
+
+#include "comm.h"
+#include "ctx.h"
+
+using namespace lmfao;
+
+namespace {
+
+lmfao_status fail(lmfao_ctx* c, lmfao_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+lmfao_status cuda_fail(lmfao_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) return fail(c, LMFAO_ERR_OOM, "%s: out of device memory", where);
+  return fail(c, LMFAO_ERR_CUDA, "%s: CUDA error %s", where, cudaGetErrorString(e));
+}
+
+#define CTX_CUDA(c, x, where)                          \
+  do {                                                 \
+    cudaError_t e_ = (x);                              \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+  } while (0)
+
+// gather every column of relation r (and its fk_dense / dense_key) by `perm` of length n
+cudaError_t permute_rel(Rel& r, const uint32_t* perm, int64_t n, cudaStream_t st) {
+  for (auto& c : r.cols) {
+    DevBuf nb;
+    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * (c.dt == LMFAO_FP64 ? 8 : 4)));
+    CUDA_TRY(gather_bytes(c.buf.p, perm, nb.p, n, c.dt == LMFAO_FP64 ? 8 : 4, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    c.buf = std::move(nb);
+  }
+  for (auto& f : r.fk_dense) {
+    DevBuf nb;
+    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * 4));
+    CUDA_TRY(gather_bytes(f.p, perm, nb.p, n, 4, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    f = std::move(nb);
+  }
+  if (r.dense_key.p) {
+    DevBuf nb;
+    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * 4));
+    CUDA_TRY(gather_bytes(r.dense_key.p, perm, nb.p, n, 4, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    r.dense_key = std::move(nb);
+  }
+  r.nrows = n;
+  return cudaSuccess;
+}
+
+cudaError_t slice_rel(Rel& r, int64_t lo, int64_t hi, cudaStream_t st) {
+  int64_t n = hi - lo;
+  auto cut = [&](DevBuf& b, int es) -> cudaError_t {
+    DevBuf nb;
+    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * es));
+    if (n > 0) CUDA_TRY(cudaMemcpyAsync(nb.p, (char*)b.p + lo * es, n * es, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    b = std::move(nb);
+    return cudaSuccess;
+  };
+  for (auto& c : r.cols) CUDA_TRY(cut(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  for (auto& f : r.fk_dense) CUDA_TRY(cut(f, 4));
+  r.nrows = n;
+  return cudaSuccess;
+}
+
+NodeArgs node_args(const lmfao_ctx* c, int n) {
+  const Rel& r = c->rels[n];
+  NodeArgs a{};
+  a.nrows = r.nrows;
+  for (size_t i = 0; i < r.cols.size() && i < (size_t)MAX_COLS; i++) {
+    a.cols[i] = r.cols[i].buf.p;
+    a.col_is_int[i] = r.cols[i].dt == LMFAO_INT32;
+  }
+  a.nchild = (int)r.children.size();
+  for (int j = 0; j < a.nchild; j++) {
+    int ch = r.children[j];
+    a.fk[j] = r.fk_dense[j].as<int32_t>();
+    a.V[j] = c->nodes[ch].V.as<double>();
+    a.W[j] = (int)c->nodes[ch].slots.size();
+  }
+  return a;
+}
+
+}  // namespace
+
+// =====================================================================  ABI
+extern "C" {
+
+lmfao_status lmfao_unique_id(void* out) {
+  if (!out) return LMFAO_ERR_INVALID_ARG;
+  if (!nccl_available()) return LMFAO_ERR_NCCL;
+  return nccl_unique_id(out) == 0 ? LMFAO_OK : LMFAO_ERR_NCCL;
+}
+
+lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id, lmfao_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return LMFAO_ERR_INVALID_ARG;
+  if ((world > 1) != (unique_id != nullptr)) return LMFAO_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return LMFAO_ERR_CUDA;
+  if (device < 0 || device >= ndev) return LMFAO_ERR_INVALID_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return LMFAO_ERR_CUDA;
+  auto* c = new lmfao_ctx();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->shard_part = rank;
+  c->shard_nparts = world;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return LMFAO_ERR_CUDA;
+  }
+  if (world > 1) {
+    int e = nccl_init(&c->comm, world, unique_id, rank);
+    if (e != 0) {
+      cudaStreamDestroy(c->stream);
+      delete c;
+      return LMFAO_ERR_NCCL;
+    }
+  }
+  *out = c;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_destroy(lmfao_ctx* c) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->comm) nccl_destroy(c->comm);
+  cudaStream_t st = c->stream;
+  delete c;
+  cudaStreamDestroy(st);
+  return LMFAO_OK;
+}
+
+const char* lmfao_last_error(const lmfao_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, int32_t ncols,
+                                const char* const* col_names, const lmfao_dtype* dtypes, const void* const* cols,
+                                int cols_on_device, int32_t* rel_id) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_CREATED) return fail(c, LMFAO_ERR_STATE, "add_relation after set_join_tree");
+  if (!name || nrows < 0 || ncols < 1 || !col_names || !dtypes || (!cols && nrows > 0))
+    return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: bad arguments");
+  if (ncols > MAX_COLS) return fail(c, LMFAO_ERR_UNSUPPORTED, "add_relation: more than %d columns", MAX_COLS);
+  for (auto& r : c->rels)
+    if (r.name == name) return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate relation %s", name);
+  cudaSetDevice(c->device);
+  Rel r;
+  r.name = name;
+  r.nrows = nrows;
+  int rid = (int)c->rels.size();
+  std::set<std::string> seen;
+  for (int i = 0; i < ncols; i++) {
+    if (!col_names[i] || (dtypes[i] != LMFAO_INT32 && dtypes[i] != LMFAO_FP64))
+      return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: bad column %d", i);
+    if (!seen.insert(col_names[i]).second)
+      return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate column %s in %s", col_names[i], name);
+    auto it = c->attr_by_name.find(col_names[i]);
+    if (it != c->attr_by_name.end() && c->attrs[it->second].dt != dtypes[i])
+      return fail(c, LMFAO_ERR_TYPE, "attribute %s has conflicting dtypes", col_names[i]);
+  }
+  for (int i = 0; i < ncols; i++) {
+    Column col;
+    col.name = col_names[i];
+    col.dt = dtypes[i];
+    size_t es = col.dt == LMFAO_FP64 ? 8 : 4;
+    CTX_CUDA(c, col.buf.alloc(std::max<int64_t>(nrows, 1) * es), "add_relation");
+    if (nrows > 0) {
+      if (!cols[i]) return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: null column %d", i);
+      CTX_CUDA(c, cudaMemcpy(col.buf.p, cols[i], nrows * es, cols_on_device ? cudaMemcpyDeviceToDevice
+                                                                             : cudaMemcpyHostToDevice),
+               "add_relation copy");
+    }
+    auto it = c->attr_by_name.find(col.name);
+    int aid;
+    if (it == c->attr_by_name.end()) {
+      aid = (int)c->attrs.size();
+      c->attrs.push_back(Attr{col.name, col.dt, {}});
+      c->attr_by_name[col.name] = aid;
+    } else {
+      aid = it->second;
+    }
+    c->attrs[aid].occ.push_back({rid, i});
+    col.attr = aid;
+    r.cols.push_back(std::move(col));
+  }
+  c->rels.push_back(std::move(r));
+  if (rel_id) *rel_id = rid;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_attr_id(lmfao_ctx* c, const char* attr_name, int32_t* attr_id) {
+  if (!c || !attr_name || !attr_id) return LMFAO_ERR_INVALID_ARG;
+  auto it = c->attr_by_name.find(attr_name);
+  if (it == c->attr_by_name.end()) return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "unknown attribute %s", attr_name);
+  *attr_id = it->second;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_set_join_tree(lmfao_ctx* c, int32_t root_rel, int32_t n_edges, const int32_t* parent_rel,
+                                 const int32_t* child_rel) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_CREATED) return fail(c, LMFAO_ERR_STATE, "set_join_tree called twice or out of order");
+  int m = (int)c->rels.size();
+  if (m == 0) return fail(c, LMFAO_ERR_STATE, "no relations");
+  if (root_rel < 0 || root_rel >= m) return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "bad root relation id");
+  if (n_edges < 0 || (n_edges > 0 && (!parent_rel || !child_rel))) return fail(c, LMFAO_ERR_INVALID_ARG, "bad edges");
+  for (int e = 0; e < n_edges; e++)
+    if (parent_rel[e] < 0 || parent_rel[e] >= m || child_rel[e] < 0 || child_rel[e] >= m || parent_rel[e] == child_rel[e])
+      return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "edge %d names an unknown relation", e);
+  if (n_edges > m - 1) return fail(c, LMFAO_ERR_CYCLIC_TREE, "%d edges for %d relations: cycle", n_edges, m);
+  std::vector<int> parent(m, -1);
+  std::vector<std::vector<int>> children(m);
+  for (int e = 0; e < n_edges; e++) {
+    int p = parent_rel[e], ch = child_rel[e];
+    if (parent[ch] != -1 || ch == root_rel)
+      return fail(c, LMFAO_ERR_CYCLIC_TREE, "relation %s has two parents (cycle)", c->rels[ch].name.c_str());
+    parent[ch] = p;
+    children[p].push_back(ch);
+  }
+  // reachability from the root
+  std::vector<int> seen(m, 0), stack{root_rel};
+  int reached = 0;
+  while (!stack.empty()) {
+    int u = stack.back();
+    stack.pop_back();
+    if (seen[u]) return fail(c, LMFAO_ERR_CYCLIC_TREE, "cycle through %s", c->rels[u].name.c_str());
+    seen[u] = 1;
+    reached++;
+    for (int v : children[u]) stack.push_back(v);
+  }
+  if (reached != m) {
+    if (n_edges == m - 1) return fail(c, LMFAO_ERR_CYCLIC_TREE, "edges form a cycle disconnected from the root");
+    return fail(c, LMFAO_ERR_DISCONNECTED_TREE, "join tree does not reach every relation");
+  }
+  // running intersection: for every pair sharing an attribute, every
+  // relation on the path between them holds it.
+  auto path = [&](int a, int b) {
+    std::vector<int> pa, pb;
+    for (int u = a; u != -1; u = parent[u]) pa.push_back(u);
+    for (int u = b; u != -1; u = parent[u]) pb.push_back(u);
+    std::set<int> sa(pa.begin(), pa.end());
+    int lca = -1;
+    for (int u : pb)
+      if (sa.count(u)) { lca = u; break; }
+    std::vector<int> p;
+    for (int u = a; u != lca; u = parent[u]) p.push_back(u);
+    for (int u = b; u != lca; u = parent[u]) p.push_back(u);
+    p.push_back(lca);
+    return p;
+  };
+  for (auto& at : c->attrs) {
+    for (size_t i = 0; i < at.occ.size(); i++)
+      for (size_t j = i + 1; j < at.occ.size(); j++) {
+        for (int u : path(at.occ[i].first, at.occ[j].first)) {
+          bool has = false;
+          for (auto& o : at.occ) has |= o.first == u;
+          if (!has)
+            return fail(c, LMFAO_ERR_RUNNING_INTERSECTION,
+                        "running intersection violated: %s shared by %s and %s is missing from %s", at.name.c_str(),
+                        c->rels[at.occ[i].first].name.c_str(), c->rels[at.occ[j].first].name.c_str(),
+                        c->rels[u].name.c_str());
+        }
+      }
+  }
+  // v1: exactly one int32 join attribute per edge
+  for (int ch = 0; ch < m; ch++) {
+    if (parent[ch] < 0) continue;
+    Rel& C = c->rels[ch];
+    Rel& P = c->rels[parent[ch]];
+    int shared = 0, key = -1;
+    for (auto& col : C.cols)
+      if (P.find_attr(col.attr) >= 0) { shared++; key = col.attr; }
+    if (shared != 1)
+      return fail(c, LMFAO_ERR_UNSUPPORTED, "edge %s-%s shares %d attributes (v1 supports exactly one)",
+                  P.name.c_str(), C.name.c_str(), shared);
+    if (c->attrs[key].dt != LMFAO_INT32)
+      return fail(c, LMFAO_ERR_TYPE, "join attribute %s must be int32", c->attrs[key].name.c_str());
+    C.key_attr = key;
+    C.key_col = C.find_attr(key);
+  }
+  for (int u = 0; u < m; u++) {
+    c->rels[u].parent = parent[u];
+    c->rels[u].children = children[u];
+    c->rels[u].fk_col.clear();
+    for (int ch : children[u]) c->rels[u].fk_col.push_back(c->rels[u].find_attr(c->rels[ch].key_attr));
+  }
+  c->root = root_rel;
+  c->state = S_TREE;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_set_root_shard(lmfao_ctx* c, int32_t part, int32_t nparts) {
+  if (!c || nparts < 1 || part < 0 || part >= nparts) return LMFAO_ERR_INVALID_ARG;
+  if (c->state >= S_PREPARED) return fail(c, LMFAO_ERR_STATE, "set_root_shard after prepare");
+  c->shard_part = part;
+  c->shard_nparts = nparts;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_prepare(lmfao_ctx* c) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_TREE) return fail(c, LMFAO_ERR_STATE, "prepare needs a join tree (and runs once)");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  // post-order: children before parents
+  std::vector<int> post;
+  std::function<void(int)> dfs = [&](int u) {
+    for (int v : c->rels[u].children) dfs(v);
+    post.push_back(u);
+  };
+  dfs(c->root);
+  for (int u : post) {
+    Rel& r = c->rels[u];
+    // (1) dense remap of each child key: binary search in the child's dictionary
+    r.fk_dense.clear();
+    for (size_t j = 0; j < r.children.size(); j++) {
+      Rel& ch = c->rels[r.children[j]];
+      DevBuf d;
+      CTX_CUDA(c, d.alloc(std::max<int64_t>(r.nrows, 1) * 4), "prepare");
+      CTX_CUDA(c, lookup_dense(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.nrows, ch.dict.as<int32_t>(), ch.nkeys,
+                               d.as<int32_t>(), st),
+               "prepare remap");
+      r.fk_dense.push_back(std::move(d));
+    }
+    // (2) inner join: drop rows with a dangling foreign key
+    std::vector<const int32_t*> fks;
+    for (auto& f : r.fk_dense) fks.push_back(f.as<int32_t>());
+    DevBuf keep;
+    int64_t nkeep = r.nrows;
+    CTX_CUDA(c, keep_rows(fks, r.nrows, keep, nkeep, st), "prepare filter");
+    if (nkeep != r.nrows) CTX_CUDA(c, permute_rel(r, keep.as<uint32_t>(), nkeep, st), "prepare compact");
+    if (u != c->root) {
+      // (3) dictionary of the key to the parent, dense ids, sort by them
+      DevBuf codes;
+      CTX_CUDA(c, dict_encode_i32(r.cols[r.key_col].buf.as<int32_t>(), r.nrows, r.dict, r.nkeys, &codes, st),
+               "prepare dict");
+      r.dense_key = std::move(codes);
+      DevBuf perm;
+      CTX_CUDA(c, sort_perm_by_dense(r.dense_key.as<int32_t>(), r.nrows, r.nkeys, perm, st), "prepare sort");
+      CTX_CUDA(c, permute_rel(r, perm.as<uint32_t>(), r.nrows, st), "prepare permute");
+      r.unique_key = r.nkeys == r.nrows;
+    }
+  }
+  // (4) composite sort of the root by its children's dense keys, increasing
+  // domain size, then keep this rank's contiguous shard.
+  Rel& R = c->rels[c->root];
+  c->levels.clear();
+  for (size_t j = 0; j < R.children.size(); j++) c->levels.push_back((int)j);
+  std::stable_sort(c->levels.begin(), c->levels.end(), [&](int a, int b) {
+    return c->rels[R.children[a]].nkeys < c->rels[R.children[b]].nkeys;
+  });
+  if (!c->levels.empty() && R.nrows > 1) {
+    std::vector<const int32_t*> keys;
+    std::vector<int64_t> nk;
+    for (int j : c->levels) {
+      keys.push_back(R.fk_dense[j].as<int32_t>());
+      nk.push_back(c->rels[R.children[j]].nkeys);
+    }
+    DevBuf perm;
+    CTX_CUDA(c, sort_perm_composite(keys, nk, R.nrows, perm, st), "prepare root sort");
+    CTX_CUDA(c, permute_rel(R, perm.as<uint32_t>(), R.nrows, st), "prepare root permute");
+  }
+  if (c->shard_nparts > 1) {
+    int64_t N = R.nrows;
+    int64_t lo = N * c->shard_part / c->shard_nparts, hi = N * (c->shard_part + 1) / c->shard_nparts;
+    CTX_CUDA(c, slice_rel(R, lo, hi, st), "prepare shard");
+  }
+  // owners: the top-most relation holding each attribute (unique by P:720)
+  std::vector<int> depth(c->rels.size(), 0);
+  for (size_t u = 0; u < c->rels.size(); u++)
+    for (int v = c->rels[u].parent; v != -1; v = c->rels[v].parent) depth[u]++;
+  c->owner.assign(c->attrs.size(), -1);
+  for (size_t a = 0; a < c->attrs.size(); a++) {
+    int best = -1;
+    for (auto& o : c->attrs[a].occ)
+      if (best < 0 || depth[o.first] < depth[best]) best = o.first;
+    c->owner[a] = best;
+  }
+  c->postorder.clear();
+  for (int u : post)
+    if (u != c->root) c->postorder.push_back(u);
+  c->state = S_PREPARED;
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* groupby_attrs, int32_t n_udafs,
+                             const lmfao_udaf* udafs, int32_t* query_id) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PREPARED) return fail(c, LMFAO_ERR_STATE, "add_query needs prepare and must precede plan");
+  if (n_groupby < 0 || n_udafs < 0 || (n_groupby > 0 && !groupby_attrs) || (n_udafs > 0 && !udafs))
+    return fail(c, LMFAO_ERR_INVALID_ARG, "add_query: bad arguments");
+  if (n_groupby > 8) return fail(c, LMFAO_ERR_UNSUPPORTED, "more than 8 group-by attributes");
+  Query q;
+  int na = (int)c->attrs.size();
+  std::set<int> gbs;
+  for (int i = 0; i < n_groupby; i++) {
+    int a = groupby_attrs[i];
+    if (a < 0 || a >= na) return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "unknown group-by attribute id %d", a);
+    if (c->attrs[a].dt != LMFAO_INT32)
+      return fail(c, LMFAO_ERR_TYPE, "group-by attribute %s must be int32", c->attrs[a].name.c_str());
+    if (!gbs.insert(a).second) return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate group-by attribute");
+    int o = c->owner[a];
+    bool ok = o == c->root || (c->rels[o].parent == c->root && c->rels[o].unique_key);
+    if (!ok)
+      return fail(c, LMFAO_ERR_UNSUPPORTED,
+                  "group-by attribute %s is not functionally determined by a root row (v1: root or a unique-keyed "
+                  "child of the root)",
+                  c->attrs[a].name.c_str());
+    q.gb.push_back(a);
+  }
+  for (int j = 0; j < n_udafs; j++) {
+    const lmfao_udaf& u = udafs[j];
+    if (u.n_products < 0 || (u.n_products > 0 && !u.products))
+      return fail(c, LMFAO_ERR_INVALID_ARG, "udaf %d: bad products", j);
+    std::vector<QProduct> ps;
+    for (int p = 0; p < u.n_products; p++) {
+      const lmfao_product& pr = u.products[p];
+      if (pr.n_factors < 0 || (pr.n_factors > 0 && !pr.factors))
+        return fail(c, LMFAO_ERR_INVALID_ARG, "udaf %d product %d: bad factors", j, p);
+      QProduct qp{pr.coeff, {}};
+      for (int f = 0; f < pr.n_factors; f++) {
+        const lmfao_factor& fa = pr.factors[f];
+        if (fa.kind < LMFAO_F_CONST || fa.kind > LMFAO_F_NE) return fail(c, LMFAO_ERR_INVALID_ARG, "bad factor kind");
+        if (fa.kind == LMFAO_F_CONST) {
+          qp.f.push_back(QFactor{fa.kind, -1, fa.param});
+          continue;
+        }
+        if (fa.attr < 0 || fa.attr >= na) return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "unknown attribute id %d", fa.attr);
+        qp.f.push_back(QFactor{fa.kind, fa.attr, fa.param});
+      }
+      ps.push_back(qp);
+    }
+    q.udafs.push_back(ps);
+  }
+  c->queries.push_back(std::move(q));
+  if (query_id) *query_id = (int)c->queries.size() - 1;
+  return LMFAO_OK;
+}
+
+}  // extern "C"
+
+// ===================================================================== planner
+namespace {
+
+int child_toward(const lmfao_ctx* c, int node, int target) {
+  // the child of `node` whose subtree contains `target` (target != node)
+  int u = target;
+  while (c->rels[u].parent != node) u = c->rels[u].parent;
+  return u;
+}
+
+int slot_of(lmfao_ctx* c, int node, const std::vector<QFactor>& fs) {
+  const Rel& r = c->rels[node];
+  SlotKey key;
+  std::vector<std::vector<QFactor>> sub(r.children.size());
+  for (auto& f : fs) {
+    int o = c->owner[f.attr];
+    if (o == node) {
+      key.own.emplace_back(f.kind, f.attr, dbits(f.param));
+    } else {
+      int ch = child_toward(c, node, o);
+      for (size_t j = 0; j < r.children.size(); j++)
+        if (r.children[j] == ch) sub[j].push_back(f);
+    }
+  }
+  std::sort(key.own.begin(), key.own.end());
+  for (size_t j = 0; j < r.children.size(); j++) key.child_slots.push_back(slot_of(c, r.children[j], sub[j]));
+  NodePlan& np = c->nodes[node];
+  auto it = np.index.find(key);
+  if (it != np.index.end()) return it->second;
+  int s = (int)np.slots.size();
+  np.slots.push_back(key);
+  np.index[key] = s;
+  return s;
+}
+
+void emit_term(Program& p, const lmfao_ctx* c, int node, double coef, const std::vector<std::tuple<int, int, uint64_t>>& own,
+               const std::vector<int>& child_slots) {
+  const Rel& r = c->rels[node];
+  p.ip.push_back((int)own.size());
+  p.dp.push_back(coef);
+  for (auto& o : own) {
+    int kind = std::get<0>(o), attr = std::get<1>(o);
+    double prm;
+    uint64_t b = std::get<2>(o);
+    std::memcpy(&prm, &b, 8);
+    p.ip.push_back(kind);
+    p.ip.push_back(r.find_attr(attr));
+    p.dp.push_back(prm);
+  }
+  for (int s : child_slots) p.ip.push_back(s);
+}
+
+// root term of a product: own factors at the root, one slot per root child
+void root_term(lmfao_ctx* c, const QProduct& pr, double& coef, std::vector<std::tuple<int, int, uint64_t>>& own,
+               std::vector<int>& slots) {
+  const Rel& R = c->rels[c->root];
+  coef = pr.coeff;
+  std::vector<std::vector<QFactor>> sub(R.children.size());
+  for (auto& f : pr.f) {
+    if (f.kind == LMFAO_F_CONST) {
+      coef *= f.param;
+      continue;
+    }
+    int o = c->owner[f.attr];
+    if (o == c->root) {
+      own.emplace_back(f.kind, f.attr, dbits(f.param));
+    } else {
+      int ch = child_toward(c, c->root, o);
+      for (size_t j = 0; j < R.children.size(); j++)
+        if (R.children[j] == ch) sub[j].push_back(f);
+    }
+  }
+  for (size_t j = 0; j < R.children.size(); j++) slots.push_back(slot_of(c, R.children[j], sub[j]));
+}
+
+void append_udaf_program(lmfao_ctx* c, Program& p, const std::vector<QProduct>& u) {
+  p.out_ioff.push_back((int)p.ip.size());
+  p.out_doff.push_back((int)p.dp.size());
+  p.ip.push_back((int)u.size());
+  for (auto& pr : u) {
+    double coef;
+    std::vector<std::tuple<int, int, uint64_t>> own;
+    std::vector<int> slots;
+    root_term(c, pr, coef, own, slots);
+    emit_term(p, c, c->root, coef, own, slots);
+  }
+}
+
+}  // namespace
+
+extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PREPARED) return fail(c, LMFAO_ERR_STATE, "plan needs prepare (and runs once)");
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  c->nodes.clear();
+  c->nodes.resize(c->rels.size());
+  // slot 0 = count for every view (post-order: grandchildren first)
+  for (int u : c->postorder) slot_of(c, u, {});
+  // root programs (this also registers every view slot)
+  Program scal;
+  c->scalar_queries.clear();
+  c->scalar_off.clear();
+  c->query_kind.assign(c->queries.size(), 0);
+  c->query_slot.assign(c->queries.size(), 0);
+  std::vector<Program> gprogs;
+  c->groups.clear();
+  for (size_t q = 0; q < c->queries.size(); q++) {
+    const Query& Q = c->queries[q];
+    if (Q.gb.empty()) {
+      c->query_kind[q] = 0;
+      c->query_slot[q] = (int)c->scalar_queries.size();
+      c->scalar_queries.push_back((int)q);
+      c->scalar_off.push_back((int)scal.out_ioff.size());
+      for (auto& u : Q.udafs) append_udaf_program(c, scal, u);
+    } else {
+      c->query_kind[q] = 1;
+      c->query_slot[q] = (int)c->groups.size();
+      c->groups.emplace_back();
+      Program gp;
+      for (auto& u : Q.udafs) append_udaf_program(c, gp, u);
+      gprogs.push_back(std::move(gp));
+    }
+  }
+  // view programs: one output per slot
+  for (int u : c->postorder) {
+    NodePlan& np = c->nodes[u];
+    Program p;
+    for (auto& s : np.slots) {
+      p.out_ioff.push_back((int)p.ip.size());
+      p.out_doff.push_back((int)p.dp.size());
+      p.ip.push_back(1);
+      emit_term(p, c, u, 1.0, s.own, s.child_slots);
+    }
+    CTX_CUDA(c, np.prog.upload(p, st), "plan upload view program");
+    CTX_CUDA(c, np.V.alloc(std::max<int64_t>(c->rels[u].nkeys, 1) * np.slots.size() * 8), "plan alloc view");
+  }
+  // scalar outputs
+  CTX_CUDA(c, c->scalar_prog.upload(scal, st), "plan upload");
+  int nout = c->scalar_prog.nout;
+  c->scalar_grid = 148 * 4;
+  CTX_CUDA(c, c->partials.alloc((size_t)c->scalar_grid * std::max(nout, 1) * 8), "plan");
+  CTX_CUDA(c, c->cpart.alloc((size_t)c->scalar_grid * 8), "plan");
+  CTX_CUDA(c, c->scalar_out.alloc((size_t)std::max(nout, 1) * 8), "plan");
+  CTX_CUDA(c, c->scalar_count.alloc(8), "plan");
+  // group-by queries: dictionaries, codes, dense cell tables
+  for (size_t q = 0; q < c->queries.size(); q++) {
+    if (c->query_kind[q] != 1) continue;
+    GroupPlan& gp = c->groups[c->query_slot[q]];
+    const Query& Q = c->queries[q];
+    gp.q = (int)q;
+    gp.nudaf = (int)Q.udafs.size();
+    gp.g.ngb = gp.d.ngb = (int)Q.gb.size();
+    std::vector<int64_t> radix;
+    for (size_t i = 0; i < Q.gb.size(); i++) {
+      int a = Q.gb[i], o = c->owner[a];
+      const Rel& r = c->rels[o];
+      DevBuf dict, codes;
+      int64_t nd = 0;
+      CTX_CUDA(c, dict_encode_i32(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict, nd, &codes, st),
+               "plan dictionary");
+      gp.g.code[i] = codes.as<int32_t>();
+      gp.g.code_child[i] = -1;
+      if (o != c->root) {
+        const Rel& R = c->rels[c->root];
+        for (size_t j = 0; j < R.children.size(); j++)
+          if (R.children[j] == o) gp.g.code_child[i] = (int)j;
+      }
+      gp.d.dict[i] = dict.as<int32_t>();
+      gp.d.radix[i] = std::max<int64_t>(nd, 1);
+      radix.push_back(std::max<int64_t>(nd, 1));
+      gp.dicts.push_back(std::move(dict));
+      gp.codes.push_back(std::move(codes));
+    }
+    int64_t cells = 1;
+    for (int i = (int)radix.size() - 1; i >= 0; i--) {
+      gp.g.stride[i] = gp.d.stride[i] = cells;
+      cells *= radix[i];
+      if (cells > (int64_t)1 << 34) return fail(c, LMFAO_ERR_UNSUPPORTED, "group-by domain too large for v1");
+    }
+    gp.ncells = cells;
+    if ((double)cells * (gp.nudaf + 1) * 8 > 40e9)
+      return fail(c, LMFAO_ERR_UNSUPPORTED, "dense group-by table too large (%lld cells)", (long long)cells);
+    CTX_CUDA(c, gp.table.alloc(cells * std::max(gp.nudaf, 1) * 8), "plan group table");
+    CTX_CUDA(c, gp.counts.alloc(cells * 8), "plan group counts");
+    CTX_CUDA(c, gp.prog.upload(gprogs[c->query_slot[q]], st), "plan upload group");
+  }
+  // specialised kernels for recognised batch shapes (gram.cu / hist.cu)
+  c->fast.reset(plan_fast_paths(c));
+  c->state = S_PLANNED;
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
+  cudaSetDevice(c->device);
+  cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
+  launches_counter_reset();
+  // (b) views, bottom-up
+  for (int u : c->postorder) {
+    NodePlan& np = c->nodes[u];
+    const Rel& r = c->rels[u];
+    CTX_CUDA(c, cudaMemsetAsync(np.V.p, 0, np.V.bytes, st), "run memset view");
+    NodeArgs a = node_args(c, u);
+    CTX_CUDA(c, launch_view_build(a, r.dense_key.as<int32_t>(), np.prog.pi.as<int32_t>(), np.prog.pd.as<double>(),
+                                  np.prog.pio.as<int32_t>(), np.prog.pdo.as<int32_t>(), (int)np.slots.size(),
+                                  np.V.as<double>(), st),
+             "run view build");
+  }
+  NodeArgs ra = node_args(c, c->root);
+  bool scalar_done = false;
+  if (c->fast) {
+    int e = c->fast->run(c, ra, st, scalar_done);
+    if (e) return fail(c, LMFAO_ERR_CUDA, "fast path: %s", cudaGetErrorString((cudaError_t)e));
+  }
+  // (c) root scan, generic path
+  if (!c->scalar_queries.empty() && !scalar_done) {
+    int nout = c->scalar_prog.nout;
+    CTX_CUDA(c, launch_root_scalar(ra, c->scalar_prog.pi.as<int32_t>(), c->scalar_prog.pd.as<double>(),
+                                   c->scalar_prog.pio.as<int32_t>(), c->scalar_prog.pdo.as<int32_t>(), nout,
+                                   c->partials.as<double>(), c->cpart.as<unsigned long long>(), c->scalar_grid, st),
+             "run root scan");
+    CTX_CUDA(c, launch_combine_partials(c->partials.as<double>(), c->cpart.as<unsigned long long>(), c->scalar_grid,
+                                        nout, c->scalar_out.as<double>(), c->scalar_count.as<unsigned long long>(), st),
+             "run combine");
+  }
+  for (auto& gp : c->groups) {
+    if (c->fast && c->fast->handles_group(gp.q)) continue;
+    CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "run memset");
+    CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "run memset");
+    CTX_CUDA(c, launch_root_group(ra, gp.g, gp.prog.pi.as<int32_t>(), gp.prog.pd.as<double>(),
+                                  gp.prog.pio.as<int32_t>(), gp.prog.pdo.as<int32_t>(), gp.nudaf, gp.table.as<double>(),
+                                  gp.counts.as<unsigned long long>(), st),
+             "run group");
+  }
+  // combine across GPUs (domain parallelism)
+  if (c->world > 1) {
+    int e = 0;
+    if (!c->scalar_queries.empty()) {
+      e |= nccl_allreduce_f64(c->comm, c->scalar_out.as<double>(), c->scalar_prog.nout, st);
+      e |= nccl_allreduce_u64(c->comm, c->scalar_count.as<unsigned long long>(), 1, st);
+    }
+    for (auto& gp : c->groups) {
+      e |= nccl_allreduce_f64(c->comm, gp.table.as<double>(), gp.ncells * gp.nudaf, st);
+      e |= nccl_allreduce_u64(c->comm, gp.counts.as<unsigned long long>(), gp.ncells, st);
+    }
+    if (e) return fail(c, LMFAO_ERR_NCCL, "NCCL all-reduce failed: %s", nccl_error(e));
+  }
+  for (auto& gp : c->groups) gp.compacted = false;
+  c->ran = true;
+  c->launches_last_run = launches_counter_reset();
+  return LMFAO_OK;
+}
+
+namespace {
+lmfao_status ensure_compacted(lmfao_ctx* c, GroupPlan& gp) {
+  if (gp.compacted) return LMFAO_OK;
+  CTX_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
+  CTX_CUDA(c, cudaDeviceSynchronize(), "sync");
+  CTX_CUDA(c, launch_compact(gp.table.as<double>(), gp.counts.as<unsigned long long>(), gp.ncells, gp.nudaf, gp.d,
+                             gp.rkeys, gp.rvals, gp.rcnts, gp.ngroups, c->stream),
+           "compaction");
+  gp.compacted = true;
+  return LMFAO_OK;
+}
+}  // namespace
+
+extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_groups, int32_t* n_groupby,
+                                           int32_t* n_udafs) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
+  if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
+  cudaSetDevice(c->device);
+  const Query& Q = c->queries[q];
+  if (n_groupby) *n_groupby = (int)Q.gb.size();
+  if (n_udafs) *n_udafs = (int)Q.udafs.size();
+  if (c->query_kind[q] == 0) {
+    if (n_groups) *n_groups = 1;
+    return LMFAO_OK;
+  }
+  GroupPlan& gp = c->groups[c->query_slot[q]];
+  lmfao_status s = ensure_compacted(c, gp);
+  if (s != LMFAO_OK) return s;
+  if (n_groups) *n_groups = gp.ngroups;
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32_t** keys, const double** vals,
+                                            const uint64_t** counts) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
+  if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
+  cudaSetDevice(c->device);
+  if (c->query_kind[q] == 0) {
+    int off = c->scalar_off[c->query_slot[q]];
+    if (keys) *keys = nullptr;
+    if (vals) *vals = c->scalar_out.as<double>() + off;
+    if (counts) *counts = (const uint64_t*)c->scalar_count.p;
+    return LMFAO_OK;
+  }
+  GroupPlan& gp = c->groups[c->query_slot[q]];
+  lmfao_status s = ensure_compacted(c, gp);
+  if (s != LMFAO_OK) return s;
+  if (keys) *keys = gp.rkeys.as<int32_t>();
+  if (vals) *vals = gp.rvals.as<double>();
+  if (counts) *counts = (const uint64_t*)gp.rcnts.p;
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_fetch(lmfao_ctx* c, int32_t q, int32_t* keys_out, double* vals_out,
+                                    uint64_t* counts_out) {
+  int64_t ng = 0;
+  int32_t ngb = 0, nu = 0;
+  lmfao_status s = lmfao_result_shape(c, q, &ng, &ngb, &nu);
+  if (s != LMFAO_OK) return s;
+  const int32_t* dk = nullptr;
+  const double* dv = nullptr;
+  const uint64_t* dc = nullptr;
+  s = lmfao_result_device(c, q, &dk, &dv, &dc);
+  if (s != LMFAO_OK) return s;
+  if (ng > 0 && nu > 0 && !vals_out) return fail(c, LMFAO_ERR_INVALID_ARG, "vals_out is NULL");
+  if (ng > 0 && ngb > 0 && !keys_out) return fail(c, LMFAO_ERR_INVALID_ARG, "keys_out is NULL");
+  cudaStream_t st = c->stream;
+  CTX_CUDA(c, cudaDeviceSynchronize(), "fetch sync");
+  if (ng > 0 && ngb > 0) CTX_CUDA(c, cudaMemcpyAsync(keys_out, dk, ng * ngb * 4, cudaMemcpyDeviceToHost, st), "fetch");
+  if (ng > 0 && nu > 0) CTX_CUDA(c, cudaMemcpyAsync(vals_out, dv, ng * nu * 8, cudaMemcpyDeviceToHost, st), "fetch");
+  if (ng > 0 && counts_out) CTX_CUDA(c, cudaMemcpyAsync(counts_out, dc, ng * 8, cudaMemcpyDeviceToHost, st), "fetch");
+  CTX_CUDA(c, cudaStreamSynchronize(st), "fetch sync");
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
+  if (!c || !out || cap <= 0) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "plan_info needs plan");
+  std::ostringstream o;
+  o << "{\"root\": \"" << c->rels[c->root].name << "\", \"root_rows\": " << c->rels[c->root].nrows;
+  o << ", \"levels\": [";
+  for (size_t i = 0; i < c->levels.size(); i++) {
+    const Rel& ch = c->rels[c->rels[c->root].children[c->levels[i]]];
+    o << (i ? ", " : "") << "{\"rel\": \"" << ch.name << "\", \"nkeys\": " << ch.nkeys << "}";
+  }
+  o << "], \"views\": [";
+  bool first = true;
+  for (int u : c->postorder) {
+    o << (first ? "" : ", ") << "{\"rel\": \"" << c->rels[u].name << "\", \"width\": " << c->nodes[u].slots.size()
+      << ", \"rows\": " << c->rels[u].nrows << ", \"nkeys\": " << c->rels[u].nkeys << "}";
+    first = false;
+  }
+  o << "], \"scalar_outputs\": " << c->scalar_prog.nout << ", \"group_queries\": " << c->groups.size();
+  o << ", \"fast_path\": " << (c->fast ? c->fast->describe() : std::string("null"));
+  o << ", \"launches_last_run\": " << c->launches_last_run << "}";
+  std::string s = o.str();
+  if ((int64_t)s.size() + 1 > cap) return fail(c, LMFAO_ERR_INVALID_ARG, "plan_info buffer too small");
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return LMFAO_OK;
+}

@@ -1,0 +1,144 @@
+// ctx.h — the context behind the opaque lmfao_ctx handle (private).
+#pragma once
+#include <tuple>
+
+#include "internal.h"
+#include "paths.h"
+
+namespace lmfao {
+
+enum State { S_CREATED = 0, S_TREE, S_PREPARED, S_PLANNED };
+
+struct Column {
+  std::string name;
+  int attr = -1;
+  lmfao_dtype dt = LMFAO_INT32;
+  DevBuf buf;
+};
+
+struct Rel {
+  std::string name;
+  int64_t nrows = 0;
+  std::vector<Column> cols;
+  int parent = -1;
+  std::vector<int> children;
+  int key_attr = -1, key_col = -1;
+  std::vector<int> fk_col;  // per child: column of this relation holding the child's key
+  // prepared
+  int64_t nkeys = 0;
+  DevBuf dict;       // sorted distinct key values [nkeys]
+  DevBuf dense_key;  // dense key id per row (rows sorted by it)
+  bool unique_key = false;
+  std::vector<DevBuf> fk_dense;  // per child: dense id of the child key per row
+  int find_attr(int a) const {
+    for (size_t i = 0; i < cols.size(); i++)
+      if (cols[i].attr == a) return (int)i;
+    return -1;
+  }
+};
+
+struct Attr {
+  std::string name;
+  lmfao_dtype dt;
+  std::vector<std::pair<int, int>> occ;  // (relation, column)
+};
+
+struct QFactor {
+  int kind, attr;
+  double param;
+};
+struct QProduct {
+  double coeff;
+  std::vector<QFactor> f;
+};
+struct Query {
+  std::vector<int> gb;
+  std::vector<std::vector<QProduct>> udafs;
+};
+
+inline uint64_t dbits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
+struct SlotKey {
+  std::vector<std::tuple<int, int, uint64_t>> own;  // (kind, attr, param bits), sorted
+  std::vector<int> child_slots;
+  bool operator<(const SlotKey& o) const { return std::tie(own, child_slots) < std::tie(o.own, o.child_slots); }
+};
+
+struct DevProgram {
+  DevBuf pi, pd, pio, pdo;
+  int nout = 0;
+  cudaError_t upload(const Program& p, cudaStream_t st) {
+    nout = (int)p.out_ioff.size();
+    CUDA_TRY(pi.alloc(std::max<size_t>(p.ip.size(), 1) * 4));
+    CUDA_TRY(pd.alloc(std::max<size_t>(p.dp.size(), 1) * 8));
+    CUDA_TRY(pio.alloc(std::max<size_t>(p.out_ioff.size(), 1) * 4));
+    CUDA_TRY(pdo.alloc(std::max<size_t>(p.out_doff.size(), 1) * 4));
+    if (!p.ip.empty()) CUDA_TRY(cudaMemcpyAsync(pi.p, p.ip.data(), p.ip.size() * 4, cudaMemcpyHostToDevice, st));
+    if (!p.dp.empty()) CUDA_TRY(cudaMemcpyAsync(pd.p, p.dp.data(), p.dp.size() * 8, cudaMemcpyHostToDevice, st));
+    if (nout) {
+      CUDA_TRY(cudaMemcpyAsync(pio.p, p.out_ioff.data(), nout * 4, cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(pdo.p, p.out_doff.data(), nout * 4, cudaMemcpyHostToDevice, st));
+    }
+    return cudaStreamSynchronize(st);
+  }
+};
+
+struct NodePlan {
+  std::vector<SlotKey> slots;
+  std::map<SlotKey, int> index;
+  DevBuf V;
+  DevProgram prog;
+};
+
+struct GroupPlan {
+  int q = -1;
+  int nudaf = 0;
+  int64_t ncells = 0;
+  GroupArgs g{};
+  DecodeArgs d{};
+  std::vector<DevBuf> dicts, codes;
+  DevBuf table, counts;
+  DevProgram prog;
+  bool compacted = false;
+  DevBuf rkeys, rvals, rcnts;
+  int64_t ngroups = 0;
+};
+
+}  // namespace lmfao
+
+using namespace lmfao;
+struct lmfao_ctx {
+  int device = 0, rank = 0, world = 1;
+  int shard_part = 0, shard_nparts = 1;
+  cudaStream_t stream = nullptr;
+  void* comm = nullptr;
+  std::string err;
+  State state = S_CREATED;
+  std::vector<Rel> rels;
+  std::vector<Attr> attrs;
+  std::map<std::string, int> attr_by_name;
+  int root = -1;
+  std::vector<Query> queries;
+  // plan
+  std::vector<int> owner;      // per attr: top-most relation holding it
+  std::vector<NodePlan> nodes;  // per relation (non-root used)
+  std::vector<int> postorder;   // non-root nodes, children first
+  std::vector<int> levels;      // root children in increasing domain size (the sort order)
+  // scalar (no group-by) queries: one fused program over all their outputs
+  std::vector<int> scalar_queries;
+  std::vector<int> scalar_off;  // output offset per query (index into out)
+  DevProgram scalar_prog;
+  DevBuf partials, cpart, scalar_out, scalar_count;
+  int scalar_grid = 0;
+  std::vector<GroupPlan> groups;
+  std::vector<int> query_kind;  // 0 scalar, 1 group (index into groups)
+  std::vector<int> query_slot;
+  std::unique_ptr<FastPaths> fast;  // specialised kernels (gram / hist), if the batch matches
+  bool ran = false;
+  int64_t launches_last_run = 0;
+};
+

@@ -1,0 +1,262 @@
+// generic.cu — the general (interpreted) evaluation path for any batch the
+// planner accepts: view build (b) per non-root node and the root scan (c) for
+// no-group-by and dense group-by queries.  It is the coverage path; the
+// specialised kernels (gram.cu, hist.cu) are the performance path for the
+// BASELINE.json workloads.
+//
+// Decomposition (SURVEY §8 notation): for a product p split by the
+// planner into the root's own factors p_F and one view slot per child c,
+//     Σ_{joined t} p(t) = Σ_{f ∈ root} coef · p_F(f) · Π_c V_c[k_c(f)][slot_c(p)],
+//     V_c[k][s] = Σ_{d ∈ c, key(d)=k} p_{c,s}(d) · Π_e V_e[k_e(d)][slot_e(s)]   (Ex. 4.1).
+// Slot 0 of every view is the count (empty product), which gives bag semantics.
+#include "internal.h"
+
+namespace lmfao {
+
+__device__ __forceinline__ double load_col(const NodeArgs& a, int col, int64_t row) {
+  return a.col_is_int[col] ? (double)((const int32_t*)a.cols[col])[row] : ((const double*)a.cols[col])[row];
+}
+
+__device__ __forceinline__ double apply_factor(int kind, double x, double t) {
+  switch (kind) {
+    case LMFAO_F_IDENT: return x;
+    case LMFAO_F_LT: return x < t ? 1.0 : 0.0;
+    case LMFAO_F_LE: return x <= t ? 1.0 : 0.0;
+    case LMFAO_F_GT: return x > t ? 1.0 : 0.0;
+    case LMFAO_F_GE: return x >= t ? 1.0 : 0.0;
+    case LMFAO_F_EQ: return x == t ? 1.0 : 0.0;
+    case LMFAO_F_NE: return x != t ? 1.0 : 0.0;
+    default: return t;  // CONST
+  }
+}
+
+// Evaluates one output (sum of terms) at `row`; kk[c] = dense key of child c.
+__device__ double eval_output(const NodeArgs& a, int64_t row, const int32_t* kk, const int32_t* __restrict__ ip,
+                              const double* __restrict__ dp) {
+  int nt = *ip++;
+  double sum = 0.0;
+  for (int t = 0; t < nt; t++) {
+    int nown = *ip++;
+    double v = *dp++;
+    for (int f = 0; f < nown; f++) {
+      int kind = *ip++;
+      int col = *ip++;
+      double prm = *dp++;
+      double x = kind == LMFAO_F_CONST ? 0.0 : load_col(a, col, row);
+      v = v * apply_factor(kind, x, prm);
+    }
+    for (int c = 0; c < a.nchild; c++) {
+      int slot = *ip++;
+      v = v * a.V[c][(int64_t)kk[c] * a.W[c] + slot];
+    }
+    sum += v;
+  }
+  return sum;
+}
+
+__global__ void k_view_build(NodeArgs a, const int32_t* __restrict__ dense_key, const int32_t* __restrict__ prog_i,
+                             const double* __restrict__ prog_d, const int32_t* __restrict__ ioff,
+                             const int32_t* __restrict__ doff, int nslots, double* __restrict__ V) {
+  int32_t kk[MAX_CHILD];
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < a.nchild; c++) kk[c] = a.fk[c][row];
+    int64_t k = dense_key[row];
+    for (int s = 0; s < nslots; s++) {
+      double v = eval_output(a, row, kk, prog_i + ioff[s], prog_d + doff[s]);
+      atomicAdd(&V[k * nslots + s], v);
+    }
+  }
+}
+
+static unsigned grid_rows(int64_t n, int per_sm = 8) {
+  int64_t g = (n + 255) / 256;
+  g = std::min<int64_t>(g, 148 * per_sm);
+  return (unsigned)std::max<int64_t>(g, 1);
+}
+
+cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const int32_t* prog_i, const double* prog_d,
+                              const int32_t* ioff, const int32_t* doff, int nslots, double* V, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  k_view_build<<<grid_rows(a.nrows), 256, 0, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V);
+  launches_add(1);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// No-group-by outputs [o0, o0+nout): each warp reduces every output over its
+// rows with shuffles and lane 0 adds into the warp's smem row; the block then
+// sums its warps in fixed order.  No atomics, deterministic for a fixed grid.
+__global__ void k_root_scalar(NodeArgs a, const int32_t* __restrict__ prog_i, const double* __restrict__ prog_d,
+                              const int32_t* __restrict__ ioff, const int32_t* __restrict__ doff, int o0, int nout,
+                              int ld, double* __restrict__ partials, unsigned long long* __restrict__ cpart) {
+  extern __shared__ double wpart[];  // [nwarps][nout]
+  __shared__ unsigned long long wcnt[32];
+  int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < nw * nout; i += blockDim.x) wpart[i] = 0.0;
+  __syncthreads();
+  unsigned long long cnt = 0;
+  int32_t kk[MAX_CHILD];
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < a.nrows; base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t row = base + threadIdx.x;
+    bool valid = row < a.nrows;
+    double w = valid ? 1.0 : 0.0;
+    for (int c = 0; c < a.nchild; c++) {
+      kk[c] = valid ? a.fk[c][row] : 0;
+      if (valid) w *= a.V[c][(int64_t)kk[c] * a.W[c]];
+    }
+    cnt += (unsigned long long)w;
+    for (int o = 0; o < nout; o++) {
+      double v = valid ? eval_output(a, row, kk, prog_i + ioff[o0 + o], prog_d + doff[o0 + o]) : 0.0;
+      v = warp_sum(v);
+      if (lane == 0) wpart[warp * nout + o] += v;
+    }
+  }
+  cnt = warp_sum(cnt);
+  if (lane == 0) wcnt[warp] = cnt;
+  __syncthreads();
+  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < nw; w2++) s += wpart[w2 * nout + o];
+    partials[(int64_t)blockIdx.x * ld + o0 + o] = s;
+  }
+  if (threadIdx.x == 0 && cpart) {
+    unsigned long long s = 0;
+    for (int w2 = 0; w2 < nw; w2++) s += wcnt[w2];
+    cpart[blockIdx.x] = s;
+  }
+}
+
+cudaError_t launch_root_scalar(const NodeArgs& a, const int32_t* prog_i, const double* prog_d, const int32_t* ioff,
+                               const int32_t* doff, int nout, double* partials, unsigned long long* count_partials,
+                               int grid, cudaStream_t st) {
+  const int threads = 256, chunk = 1024;  // 8 warps x 1024 x 8 B = 64 KB smem per launch
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(k_root_scalar, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * chunk * 8));
+    attr_set = true;
+  }
+  if (nout == 0) {
+    k_root_scalar<<<grid, threads, 0, st>>>(a, prog_i, prog_d, ioff, doff, 0, 0, 1, partials, count_partials);
+    launches_add(1);
+    return cudaGetLastError();
+  }
+  for (int o0 = 0; o0 < nout; o0 += chunk) {
+    int n = std::min(chunk, nout - o0);
+    k_root_scalar<<<grid, threads, (size_t)(threads / 32) * n * 8, st>>>(a, prog_i, prog_d, ioff, doff, o0, n, nout,
+                                                                         partials, o0 == 0 ? count_partials : nullptr);
+    launches_add(1);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return cudaSuccess;
+}
+
+__global__ void k_combine(const double* __restrict__ partials, const unsigned long long* __restrict__ cpart, int grid,
+                          int nout, double* __restrict__ out, unsigned long long* __restrict__ cout_) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < grid; b++) s += partials[(int64_t)b * nout + o];
+    out[o] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && cout_) {
+    unsigned long long s = 0;
+    for (int b = 0; b < grid; b++) s += cpart[b];
+    *cout_ = s;
+  }
+}
+
+cudaError_t launch_combine_partials(const double* partials, const unsigned long long* cpart, int grid, int nout,
+                                    double* out, unsigned long long* count_out, cudaStream_t st) {
+  int blocks = std::max(1, std::min(64, (nout + 127) / 128));
+  k_combine<<<blocks, 128, 0, st>>>(partials, cpart, grid, nout, out, count_out);
+  launches_add(1);
+  return cudaGetLastError();
+}
+
+__global__ void k_root_group(NodeArgs a, GroupArgs g, const int32_t* __restrict__ prog_i,
+                             const double* __restrict__ prog_d, const int32_t* __restrict__ ioff,
+                             const int32_t* __restrict__ doff, int nudaf, double* __restrict__ table,
+                             unsigned long long* __restrict__ counts) {
+  int32_t kk[MAX_CHILD];
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    double w = 1.0;
+    for (int c = 0; c < a.nchild; c++) {
+      kk[c] = a.fk[c][row];
+      w *= a.V[c][(int64_t)kk[c] * a.W[c]];
+    }
+    if (w == 0.0) continue;
+    int64_t cell = 0;
+    for (int i = 0; i < g.ngb; i++) {
+      int cc = g.code_child[i];
+      int32_t code = cc < 0 ? g.code[i][row] : g.code[i][kk[cc]];
+      cell += (int64_t)code * g.stride[i];
+    }
+    atomicAdd(&counts[cell], (unsigned long long)w);
+    for (int j = 0; j < nudaf; j++) {
+      double v = eval_output(a, row, kk, prog_i + ioff[j], prog_d + doff[j]);
+      if (v != 0.0) atomicAdd(&table[cell * nudaf + j], v);
+    }
+  }
+}
+
+cudaError_t launch_root_group(const NodeArgs& a, const GroupArgs& g, const int32_t* prog_i, const double* prog_d,
+                              const int32_t* ioff, const int32_t* doff, int nudaf, double* table,
+                              unsigned long long* counts, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  k_root_group<<<grid_rows(a.nrows, 16), 256, 0, st>>>(a, g, prog_i, prog_d, ioff, doff, nudaf, table, counts);
+  launches_add(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- compaction
+__global__ void k_present(const unsigned long long* __restrict__ counts, int64_t n, uint32_t* flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = counts[i] > 0 ? 1u : 0u;
+}
+
+__global__ void k_scatter_groups(const double* __restrict__ table, const unsigned long long* __restrict__ counts,
+                                 const uint32_t* __restrict__ flags, const uint32_t* __restrict__ excl, int64_t n,
+                                 int nudaf, DecodeArgs d, int32_t* __restrict__ keys, double* __restrict__ vals,
+                                 unsigned long long* __restrict__ cnts) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!flags[i]) continue;
+    int64_t g = excl[i];
+    for (int a = 0; a < d.ngb; a++) keys[g * d.ngb + a] = d.dict[a][(i / d.stride[a]) % d.radix[a]];
+    for (int j = 0; j < nudaf; j++) vals[g * nudaf + j] = table[i * nudaf + j];
+    cnts[g] = counts[i];
+  }
+}
+
+cudaError_t launch_compact(const double* table, const unsigned long long* counts, int64_t ncells, int nudaf,
+                           const DecodeArgs& d, DevBuf& keys, DevBuf& vals, DevBuf& cnts, int64_t& ngroups,
+                           cudaStream_t st) {
+  ngroups = 0;
+  DevBuf flags, excl;
+  CUDA_TRY(flags.alloc(ncells * 4));
+  CUDA_TRY(excl.alloc(ncells * 4));
+  k_present<<<grid_rows(ncells, 16), 256, 0, st>>>(counts, ncells, flags.as<uint32_t>());
+  CUDA_TRY(exclusive_scan_u32(flags.as<uint32_t>(), excl.as<uint32_t>(), ncells, st));
+  uint32_t le = 0, lf = 0;
+  CUDA_TRY(cudaMemcpyAsync(&le, excl.as<uint32_t>() + ncells - 1, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&lf, flags.as<uint32_t>() + ncells - 1, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  ngroups = (int64_t)le + lf;
+  if (keys.bytes < (size_t)std::max<int64_t>(ngroups * d.ngb * 4, 16)) CUDA_TRY(keys.alloc(ngroups * d.ngb * 4));
+  if (vals.bytes < (size_t)std::max<int64_t>(ngroups * nudaf * 8, 16)) CUDA_TRY(vals.alloc(ngroups * nudaf * 8));
+  if (cnts.bytes < (size_t)std::max<int64_t>(ngroups * 8, 16)) CUDA_TRY(cnts.alloc(ngroups * 8));
+  k_scatter_groups<<<grid_rows(ncells, 16), 256, 0, st>>>(table, counts, flags.as<uint32_t>(), excl.as<uint32_t>(),
+                                                          ncells, nudaf, d, keys.as<int32_t>(), vals.as<double>(),
+                                                          cnts.as<unsigned long long>());
+  launches_add(3);
+  CUDA_TRY(cudaGetLastError());
+  return cudaStreamSynchronize(st);
+}
+
+}  // namespace lmfao

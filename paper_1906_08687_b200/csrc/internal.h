@@ -1,0 +1,131 @@
+// internal.h — private declarations of liblmfao_gpu (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/lmfao_gpu.h"
+
+#define CUDA_TRY(x)                          \
+  do {                                       \
+    cudaError_t e__ = (x);                   \
+    if (e__ != cudaSuccess) return e__;      \
+  } while (0)
+
+namespace lmfao {
+
+// Owning device buffer (cudaMalloc / cudaFree).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { reset(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t alloc(size_t b) {
+    reset();
+    if (b == 0) b = 16;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    else p = nullptr;
+    return e;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// ---- device primitives (prims.cu), all on stream st ----
+cudaError_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t st);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t st);
+cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st);
+cudaError_t iota_u32(uint32_t* a, int64_t n, cudaStream_t st);
+cudaError_t gather_bytes(const void* in, const uint32_t* perm, void* out, int64_t n, int elem_bytes, cudaStream_t st);
+cudaError_t dict_encode_i32(const int32_t* col, int64_t n, DevBuf& dict, int64_t& ndict, DevBuf* codes,
+                            cudaStream_t st);
+cudaError_t lookup_dense(const int32_t* vals, int64_t n, const int32_t* dict, int64_t nd, int32_t* out,
+                         cudaStream_t st);
+cudaError_t keep_rows(const std::vector<const int32_t*>& fks, int64_t n, DevBuf& idx, int64_t& nkeep,
+                      cudaStream_t st);
+cudaError_t sort_perm_by_dense(const int32_t* dense, int64_t n, int64_t nkeys, DevBuf& perm, cudaStream_t st);
+cudaError_t sort_perm_composite(const std::vector<const int32_t*>& keys, const std::vector<int64_t>& nkeys, int64_t n,
+                                DevBuf& perm, cudaStream_t st);
+cudaError_t segment_offsets(const int32_t* dkey, int64_t n, int64_t nkeys, DevBuf& off, cudaStream_t st);
+
+// ---- generic evaluation (generic.cu) ----
+constexpr int MAX_COLS = 48;
+constexpr int MAX_CHILD = 8;
+
+// A node's evaluation context: its columns, and per child the dense FK column
+// and the child's view V_c [nkeys_c x W_c] (row-major FP64).
+struct NodeArgs {
+  int64_t nrows;
+  const void* cols[MAX_COLS];
+  int32_t col_is_int[MAX_COLS];
+  int32_t nchild;
+  const int32_t* fk[MAX_CHILD];
+  const double* V[MAX_CHILD];
+  int32_t W[MAX_CHILD];
+};
+
+// Program encoding (int32 stream + double stream), interpreted per row:
+//   term   := n_own, (kind, col)*n_own, then one slot id per child (nchild ints); coef in dbl stream,
+//             followed by n_own params in dbl stream.
+//   output := n_terms, term*   (value = Σ terms)
+// Views: one output per slot; root: one output per (query, udaf).
+struct Program {
+  std::vector<int32_t> ip;
+  std::vector<double> dp;
+  std::vector<int32_t> out_ioff, out_doff;  // start offsets per output
+};
+
+cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const int32_t* prog_i, const double* prog_d,
+                              const int32_t* ioff, const int32_t* doff, int nslots, double* V, cudaStream_t st);
+
+// No-group-by outputs: per-block partial sums (deterministic fixed-order combine).
+cudaError_t launch_root_scalar(const NodeArgs& a, const int32_t* prog_i, const double* prog_d, const int32_t* ioff,
+                               const int32_t* doff, int nout, double* partials, unsigned long long* count_partials,
+                               int grid, cudaStream_t st);
+cudaError_t launch_combine_partials(const double* partials, const unsigned long long* cpart, int grid, int nout,
+                                    double* out, unsigned long long* count_out, cudaStream_t st);
+
+// Group-by outputs: dense cell table, FP64 atomics; counts u64.
+struct GroupArgs {
+  int32_t ngb;
+  const int32_t* code[8];   // per group attr: code column (root rows) or per-child-key code table
+  int32_t code_child[8];    // -1: code[] indexed by root row; else child index (code[] indexed by fk)
+  int64_t stride[8];        // mixed radix
+};
+cudaError_t launch_root_group(const NodeArgs& a, const GroupArgs& g, const int32_t* prog_i, const double* prog_d,
+                              const int32_t* ioff, const int32_t* doff, int nudaf, double* table,
+                              unsigned long long* counts, cudaStream_t st);
+
+// Compaction of a dense cell table: present cells (count > 0) in ascending order.
+struct DecodeArgs {
+  int32_t ngb;
+  const int32_t* dict[8];
+  int64_t radix[8];
+  int64_t stride[8];
+};
+cudaError_t launch_compact(const double* table, const unsigned long long* counts, int64_t ncells, int nudaf,
+                           const DecodeArgs& d, DevBuf& keys, DevBuf& vals, DevBuf& cnts, int64_t& ngroups,
+                           cudaStream_t st);
+
+int launches_counter_reset();
+void launches_add(int n);
+
+}  // namespace lmfao

@@ -1,0 +1,21 @@
+// paths.h — specialised kernels selected by the planner for recognised batch
+// shapes (the Gram path of the covariance batch, the histogram paths).
+#pragma once
+#include <string>
+
+#include "internal.h"
+
+struct lmfao_ctx;
+
+namespace lmfao {
+struct FastPaths {
+  virtual ~FastPaths() {}
+  // Launches the specialised root-scan work on `st`; sets scalar_done if it
+  // produced all no-group-by outputs.  Returns a cudaError_t value (0 = ok).
+  virtual int run(lmfao_ctx* c, const NodeArgs& root, cudaStream_t st, bool& scalar_done) = 0;
+  virtual bool handles_group(int query) const { return false; }
+  virtual std::string describe() const = 0;
+};
+// Returns nullptr when no specialised path applies (the generic path runs).
+FastPaths* plan_fast_paths(lmfao_ctx* c);
+}  // namespace lmfao

@@ -1,0 +1,247 @@
+"""Thin ctypes binding of liblmfao_gpu (include/lmfao_gpu.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+CUDA kernels.  There is no CPU fallback — if the shared library is missing the
+import fails loudly.  Function names follow the C ABI (lmfao_create,
+lmfao_add_relation, ...); `Engine` is a convenience wrapper over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblmfao_gpu.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1906_08687_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# status codes (lmfao_status)
+STATUS = {0: "LMFAO_OK", 1: "LMFAO_ERR_INVALID_ARG", 2: "LMFAO_ERR_STATE", 3: "LMFAO_ERR_UNKNOWN_ATTR",
+          4: "LMFAO_ERR_TYPE", 5: "LMFAO_ERR_CYCLIC_TREE", 6: "LMFAO_ERR_DISCONNECTED_TREE",
+          7: "LMFAO_ERR_RUNNING_INTERSECTION", 8: "LMFAO_ERR_UNSUPPORTED", 9: "LMFAO_ERR_OOM",
+          10: "LMFAO_ERR_CUDA", 11: "LMFAO_ERR_NCCL"}
+INT32, FP64 = 0, 1
+F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE = range(8)
+UNIQUE_ID_BYTES = 128
+
+
+class lmfao_factor(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("attr", ctypes.c_int32), ("param", ctypes.c_double)]
+
+
+class lmfao_product(ctypes.Structure):
+    _fields_ = [("coeff", ctypes.c_double), ("n_factors", ctypes.c_int32),
+                ("factors", ctypes.POINTER(lmfao_factor))]
+
+
+class lmfao_udaf(ctypes.Structure):
+    _fields_ = [("n_products", ctypes.c_int32), ("products", ctypes.POINTER(lmfao_product))]
+
+
+_P = ctypes.c_void_p
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_SIGS = {
+    "lmfao_unique_id": [_P],
+    "lmfao_create": [ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, ctypes.POINTER(_P)],
+    "lmfao_destroy": [_P],
+    "lmfao_add_relation": [_P, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_char_p),
+                           _i32p, ctypes.POINTER(_P), ctypes.c_int, _i32p],
+    "lmfao_attr_id": [_P, ctypes.c_char_p, _i32p],
+    "lmfao_set_join_tree": [_P, ctypes.c_int32, ctypes.c_int32, _i32p, _i32p],
+    "lmfao_set_root_shard": [_P, ctypes.c_int32, ctypes.c_int32],
+    "lmfao_prepare": [_P],
+    "lmfao_add_query": [_P, ctypes.c_int32, _i32p, ctypes.c_int32, ctypes.POINTER(lmfao_udaf), _i32p],
+    "lmfao_plan": [_P],
+    "lmfao_run": [_P, _P],
+    "lmfao_result_shape": [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _i32p, _i32p],
+    "lmfao_fetch": [_P, ctypes.c_int32, _P, _P, _P],
+    "lmfao_result_device": [_P, ctypes.c_int32, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
+    "lmfao_plan_info": [_P, ctypes.c_char_p, ctypes.c_int64],
+}
+for _name, _args in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = ctypes.c_int
+_lib.lmfao_last_error.argtypes = [_P]
+_lib.lmfao_last_error.restype = ctypes.c_char_p
+
+EXPORTED = list(_SIGS) + ["lmfao_last_error"]
+
+
+class LmfaoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+def lmfao_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(UNIQUE_ID_BYTES)
+    s = _lib.lmfao_unique_id(buf)
+    if s:
+        raise LmfaoError(s, "lmfao_unique_id failed")
+    return buf.raw
+
+
+def _udaf_structs(udafs, attr_id):
+    """udafs: list of products; product = (coeff, [(kind, attr_name|None, param), ...]) or an
+    object with .coeff/.factors whose factors have .kind/.attr/.param."""
+    keep = []
+    arr = (lmfao_udaf * max(1, len(udafs)))()
+    for j, u in enumerate(udafs):
+        parr = (lmfao_product * max(1, len(u)))()
+        for p_i, p in enumerate(u):
+            coeff, factors = (p.coeff, p.factors) if hasattr(p, "coeff") else p
+            farr = (lmfao_factor * max(1, len(factors)))()
+            for f_i, f in enumerate(factors):
+                kind, attr, param = (f.kind, f.attr, f.param) if hasattr(f, "kind") else f
+                farr[f_i].kind = int(kind)
+                farr[f_i].attr = -1 if attr is None else attr_id(attr)
+                farr[f_i].param = float(param)
+            keep.append(farr)
+            parr[p_i].coeff = float(coeff)
+            parr[p_i].n_factors = len(factors)
+            parr[p_i].factors = ctypes.cast(farr, ctypes.POINTER(lmfao_factor))
+        keep.append(parr)
+        arr[j].n_products = len(u)
+        arr[j].products = ctypes.cast(parr, ctypes.POINTER(lmfao_product))
+    return arr, keep
+
+
+class Engine:
+    """One lmfao_ctx (one process, one GPU)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+        h = _P()
+        uid = ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES) if unique_id is not None else None
+        s = _lib.lmfao_create(device, rank, world, uid, ctypes.byref(h))
+        if s:
+            raise LmfaoError(s, "lmfao_create failed (no CUDA device?)")
+        self.h = h
+        self.rel_ids = {}
+        self.query_ids = []
+
+    def _check(self, s):
+        if s:
+            raise LmfaoError(s, _lib.lmfao_last_error(self.h).decode())
+
+    def close(self):
+        if self.h:
+            _lib.lmfao_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def add_relation(self, name: str, cols: dict) -> int:
+        names = list(cols)
+        arrs, dtypes, ptrs, on_dev = [], [], [], None
+        for c in names:
+            v = cols[c]
+            if hasattr(v, "data_ptr"):  # torch tensor
+                dev = v.is_cuda
+                if on_dev is None:
+                    on_dev = dev
+                elif on_dev != dev:
+                    raise ValueError("all columns must be on the same side (host or device)")
+                v = v.contiguous()
+                dtypes.append(INT32 if str(v.dtype) == "torch.int32" else FP64)
+                ptrs.append(v.data_ptr())
+                arrs.append(v)
+            else:
+                a = np.ascontiguousarray(v)
+                if a.dtype == np.int32:
+                    dtypes.append(INT32)
+                elif a.dtype == np.float64:
+                    dtypes.append(FP64)
+                else:
+                    raise TypeError(f"column {c}: dtype {a.dtype} (int32 or float64 expected)")
+                on_dev = on_dev or False
+                arrs.append(a)
+                ptrs.append(a.ctypes.data)
+        n = len(arrs[0]) if arrs else 0
+        cn = (ctypes.c_char_p * len(names))(*[x.encode() for x in names])
+        dt = (ctypes.c_int32 * len(names))(*dtypes)
+        cp = (_P * len(names))(*ptrs)
+        rid = ctypes.c_int32()
+        self._check(_lib.lmfao_add_relation(self.h, name.encode(), n, len(names), cn, dt, cp, int(bool(on_dev)),
+                                            ctypes.byref(rid)))
+        self.rel_ids[name] = rid.value
+        return rid.value
+
+    def attr_id(self, name: str) -> int:
+        a = ctypes.c_int32()
+        self._check(_lib.lmfao_attr_id(self.h, name.encode(), ctypes.byref(a)))
+        return a.value
+
+    def set_join_tree(self, root: str, edges):
+        p = (ctypes.c_int32 * max(1, len(edges)))(*[self.rel_ids[e[0]] for e in edges])
+        c = (ctypes.c_int32 * max(1, len(edges)))(*[self.rel_ids[e[1]] for e in edges])
+        self._check(_lib.lmfao_set_join_tree(self.h, self.rel_ids[root], len(edges), p, c))
+
+    def set_root_shard(self, part: int, nparts: int):
+        self._check(_lib.lmfao_set_root_shard(self.h, part, nparts))
+
+    def prepare(self):
+        self._check(_lib.lmfao_prepare(self.h))
+
+    def add_query(self, groupby, udafs) -> int:
+        gb = (ctypes.c_int32 * max(1, len(groupby)))(*[self.attr_id(g) for g in groupby])
+        arr, keep = _udaf_structs(udafs, self.attr_id)
+        q = ctypes.c_int32()
+        self._check(_lib.lmfao_add_query(self.h, len(groupby), gb, len(udafs), arr, ctypes.byref(q)))
+        del keep
+        self.query_ids.append(q.value)
+        return q.value
+
+    def plan(self):
+        self._check(_lib.lmfao_plan(self.h))
+
+    def run(self, stream: int | None = None):
+        self._check(_lib.lmfao_run(self.h, _P(stream) if stream else None))
+
+    def result_shape(self, q: int):
+        ng, ngb, nu = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(_lib.lmfao_result_shape(self.h, q, ctypes.byref(ng), ctypes.byref(ngb), ctypes.byref(nu)))
+        return ng.value, ngb.value, nu.value
+
+    def fetch(self, q: int):
+        ng, ngb, nu = self.result_shape(q)
+        keys = np.zeros((ng, ngb), dtype=np.int32)
+        vals = np.zeros((ng, nu), dtype=np.float64)
+        counts = np.zeros(ng, dtype=np.uint64)
+        self._check(_lib.lmfao_fetch(self.h, q, keys.ctypes.data if keys.size else None,
+                                     vals.ctypes.data if vals.size else None, counts.ctypes.data if ng else None))
+        return keys, vals, counts
+
+    def result_device(self, q: int):
+        k, v, c = _P(), _P(), _P()
+        self._check(_lib.lmfao_result_device(self.h, q, ctypes.byref(k), ctypes.byref(v), ctypes.byref(c)))
+        return k.value, v.value, c.value
+
+    def plan_info(self) -> dict:
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._check(_lib.lmfao_plan_info(self.h, buf, 1 << 16))
+        return json.loads(buf.value.decode())
+
+
+def load(engine: Engine, db, batch, columns=None):
+    """Registers a database (relations with .name/.cols, .root, .edges) and a
+    batch (queries with .groupby/.udafs) on `engine`, through prepare; returns
+    the query ids.  `columns` optionally maps relation name -> dict of columns
+    (e.g. torch tensors already on the device) replacing rel.cols."""
+    for r in db.relations:
+        engine.add_relation(r.name, columns[r.name] if columns else r.cols)
+    engine.set_join_tree(db.root, list(db.edges))
+    engine.prepare()
+    return [engine.add_query(list(q.groupby), list(q.udafs)) for q in batch]

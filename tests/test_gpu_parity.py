@@ -1,0 +1,124 @@
+"""GPU parity: the CUDA path through the lmfao_gpu C-ABI vs the oracle, element
+by element on the same seeded inputs (keys and counts bit-exact, integral sums
+exact, floats within 1e-9 relative per DESIGN.md reading R14)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from _parity import assert_parity, run_gpu
+from _udaf import query
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _check(db, batch, **kw):
+    ref = oracle.evaluate(db, batch)
+    gpu = run_gpu(db, batch, **kw)
+    assert_parity(gpu, ref, batch)
+    return gpu, ref
+
+
+@pytest.mark.parametrize("name", ["h1", "h2", "h4", "h5"])
+def test_hand_databases_golden(name):
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    qs = g["queries"]
+    if qs == "same-as-h2":
+        qs = json.load(open(os.path.join(GOLD, "h2.json")))["queries"]
+    db = {"h1": synth.hand_h1, "h2": synth.hand_h2, "h4": synth.hand_h4, "h5": lambda: synth.hand_h2("S")}[name]()
+    batch = [query(q["groupby"], q["udafs"]) for q in qs]
+    if name == "h5":  # rooted at S: g is owned by the root; (g,b) needs b from F (non-unique child) -> skip
+        keep = [i for i, q in enumerate(qs) if "b" not in q["groupby"]]
+        qs = [qs[i] for i in keep]
+        batch = [batch[i] for i in keep]
+    gpu = run_gpu(db, batch)
+    for q, (k, v, c) in zip(qs, gpu):
+        assert k.tolist() == q["keys"] or (len(q["keys"]) == 0 and k.shape[0] == 0)
+        assert c.tolist() == q["counts"]
+        assert np.array_equal(v, np.array(q["vals"], dtype=np.float64).reshape(v.shape))
+
+
+@pytest.mark.parametrize("root,gbs", [("S1", ["X1", "X2"]), ("S2", ["X2", "X3"]), ("S3", ["X3", "X4"])])
+def test_chain_each_query_at_its_own_root(root, gbs):
+    """§4.3 chain: Q_i(X_i;1) evaluated with the root S_i (multi-root)."""
+    db = synth.hand_h3(root)
+    batch = [query([g], ["1"]) for g in gbs] + [query([], ["1"])]
+    _check(db, batch)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_star_pk_dims(seed):
+    db = synth.random_db(100 + seed, star=True, unique_child_keys=True, max_rows=800)
+    root = db.root
+    owners_ok = {a for r in db.relations for a, v in r.cols.items() if v.dtype == np.int32}
+    batch = synth.random_batch(seed, db, n_queries=4, groupby_ok=lambda a: a in owners_ok)
+    _check(db, batch)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_trees_duplicates_and_dangling(seed):
+    """General acyclic trees (depth > 1, duplicate and dangling keys): group-by only
+    on root attributes (v1 boundary)."""
+    db = synth.random_db(200 + seed, max_rows=500)
+    root_attrs = {a for a, v in db.rel(db.root).cols.items() if v.dtype == np.int32}
+    batch = synth.random_batch(seed, db, n_queries=4, groupby_ok=lambda a: a in root_attrs)
+    _check(db, batch)
+
+
+def test_config1_full():
+    w = synth.config1()
+    _check(w.db, w.batch)
+
+
+def test_config2_small_spans_tiles_and_ragged_tail():
+    w = synth.config2(fact_rows=123_457, dim_rows=(50, 400, 3000))
+    _check(w.db, w.batch)
+
+
+def test_config3_small():
+    w = synth.config3(fact_rows=40_001, dim_rows=(50, 400, 3000))
+    _check(w.db, w.batch)
+
+
+def test_config4_small():
+    w = synth.config4(fact_rows=60_003, dim_rows=(50, 400, 3000))
+    _check(w.db, w.batch)
+
+
+def test_config5_small():
+    w = synth.config5(fact_rows=50_011, dim_rows=(40, 300, 2000, 9000), cube_doms=(7, 30, 100))
+    _check(w.db, w.batch)
+
+
+@pytest.mark.parametrize("nparts", [2, 3])
+def test_simulated_sharding_partials_sum_to_oracle(nparts):
+    """Multi-GPU partition logic on one device: each contiguous shard of
+    the sorted root run separately; the partials summed in rank order equal the
+    oracle (counts exactly)."""
+    w = synth.config2(fact_rows=30_011, dim_rows=(30, 200, 1500))
+    batch = [synth.Query([], w.batch[0].udafs[:60])]
+    ref = oracle.evaluate(w.db, batch)[0]
+    parts = [run_gpu(w.db, batch, shard=(p, nparts))[0] for p in range(nparts)]
+    cnt = sum(int(p[2][0]) for p in parts)
+    assert cnt == int(ref.counts[0])
+    tot = sum(p[1] for p in parts)
+    assert np.allclose(tot, ref.vals, rtol=1e-9)
+
+
+def test_repeated_runs_identical():
+    w = synth.config2(fact_rows=20_000, dim_rows=(30, 200, 1500))
+    a = run_gpu(w.db, w.batch, runs=1)
+    b = run_gpu(w.db, w.batch, runs=3)
+    assert np.array_equal(a[0][1], b[0][1])
+
+
+def test_empty_root_and_empty_child():
+    db = synth.hand_h4()
+    _check(db, [query([], ["1", "x"]), query(["a"], ["x"])])
+    F = synth.Relation("F", {"a": np.zeros(0, np.int32), "x": np.zeros(0)})
+    S = synth.Relation("S", {"a": np.array([1], np.int32), "y": np.array([2.0])})
+    _check(synth.Database([F, S], "F", [("F", "S")]), [query([], ["1", "x*y"]), query(["a"], ["y"])])
