@@ -178,6 +178,13 @@ LMFAO_API lmfao_status lmfao_result_device(lmfao_ctx* ctx, int32_t query_id, con
  * the last run, kernel launches per run). */
 LMFAO_API lmfao_status lmfao_plan_info(lmfao_ctx* ctx, char* out, int64_t cap);
 
+/* Measurement: when enabled, lmfao_run records CUDA events on its stream around
+ * the dominant root-scan kernel (kernel (c)); lmfao_profile_read synchronises
+ * and returns the summed device time and the number of timed launches since
+ * the last lmfao_profile call. */
+LMFAO_API lmfao_status lmfao_profile(lmfao_ctx* ctx, int enable);
+LMFAO_API lmfao_status lmfao_profile_read(lmfao_ctx* ctx, double* total_ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -388,6 +388,14 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     CTX_CUDA(c, permute_rel(R, perm.as<uint32_t>(), R.nrows, st), "prepare root permute");
   }
   if (c->shard_nparts > 1) {
+    for (size_t i = 0; i < R.cols.size(); i++) {
+      if (R.cols[i].dt != LMFAO_INT32) continue;
+      DevBuf d;
+      int64_t nd = 0;
+      CTX_CUDA(c, dict_encode_i32(R.cols[i].buf.as<int32_t>(), R.nrows, d, nd, nullptr, st), "prepare dict");
+      R.full_dict_n[R.cols[i].attr] = nd;
+      R.full_dict[R.cols[i].attr] = std::move(d);
+    }
     int64_t N = R.nrows;
     int64_t lo = N * c->shard_part / c->shard_nparts, hi = N * (c->shard_part + 1) / c->shard_nparts;
     CTX_CUDA(c, slice_rel(R, lo, hi, st), "prepare shard");
@@ -625,8 +633,20 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       const Rel& r = c->rels[o];
       DevBuf dict, codes;
       int64_t nd = 0;
-      CTX_CUDA(c, dict_encode_i32(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict, nd, &codes, st),
-               "plan dictionary");
+      auto fd = r.full_dict.find(a);
+      if (fd != r.full_dict.end()) {  // sharded root: the global dictionary
+        nd = r.full_dict_n.at(a);
+        CTX_CUDA(c, dict.alloc(std::max<int64_t>(nd, 1) * 4), "plan dictionary");
+        CTX_CUDA(c, cudaMemcpyAsync(dict.p, fd->second.p, nd * 4, cudaMemcpyDeviceToDevice, st), "plan dictionary");
+        CTX_CUDA(c, codes.alloc(std::max<int64_t>(r.nrows, 1) * 4), "plan codes");
+        CTX_CUDA(c, lookup_dense(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict.as<int32_t>(), nd,
+                                 codes.as<int32_t>(), st),
+                 "plan codes");
+        CTX_CUDA(c, cudaStreamSynchronize(st), "plan codes");
+      } else {
+        CTX_CUDA(c, dict_encode_i32(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict, nd, &codes, st),
+                 "plan dictionary");
+      }
       gp.g.code[i] = codes.as<int32_t>();
       gp.g.code_child[i] = -1;
       if (o != c->root) {
@@ -667,6 +687,7 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   launches_counter_reset();
   // (b) views, bottom-up
   for (int u : c->postorder) {
+    if (c->fast && c->fast->skip_generic_views()) break;
     NodePlan& np = c->nodes[u];
     const Rel& r = c->rels[u];
     CTX_CUDA(c, cudaMemsetAsync(np.V.p, 0, np.V.bytes, st), "run memset view");
@@ -685,10 +706,12 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   // (c) root scan, generic path
   if (!c->scalar_queries.empty() && !scalar_done) {
     int nout = c->scalar_prog.nout;
+    scan_timer_begin(c, st);
     CTX_CUDA(c, launch_root_scalar(ra, c->scalar_prog.pi.as<int32_t>(), c->scalar_prog.pd.as<double>(),
                                    c->scalar_prog.pio.as<int32_t>(), c->scalar_prog.pdo.as<int32_t>(), nout,
                                    c->partials.as<double>(), c->cpart.as<unsigned long long>(), c->scalar_grid, st),
              "run root scan");
+    scan_timer_end(c, st);
     CTX_CUDA(c, launch_combine_partials(c->partials.as<double>(), c->cpart.as<unsigned long long>(), c->scalar_grid,
                                         nout, c->scalar_out.as<double>(), c->scalar_count.as<unsigned long long>(), st),
              "run combine");
@@ -821,5 +844,47 @@ extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   std::string s = o.str();
   if ((int64_t)s.size() + 1 > cap) return fail(c, LMFAO_ERR_INVALID_ARG, "plan_info buffer too small");
   std::memcpy(out, s.c_str(), s.size() + 1);
+  return LMFAO_OK;
+}
+
+namespace lmfao {
+void scan_timer_begin(lmfao_ctx* c, cudaStream_t st) {
+  if (!c->prof) return;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+  c->prof_events.push_back({a, b});
+}
+void scan_timer_end(lmfao_ctx* c, cudaStream_t st) {
+  if (!c->prof || c->prof_events.empty()) return;
+  cudaEventRecord(c->prof_events.back().second, st);
+}
+}  // namespace lmfao
+
+extern "C" lmfao_status lmfao_profile(lmfao_ctx* c, int enable) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  for (auto& e : c->prof_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->prof_events.clear();
+  c->prof = enable != 0;
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_profile_read(lmfao_ctx* c, double* total_ms, int64_t* launches) {
+  if (!c || !total_ms || !launches) return LMFAO_ERR_INVALID_ARG;
+  cudaSetDevice(c->device);
+  double t = 0;
+  for (auto& e : c->prof_events) {
+    if (cudaEventSynchronize(e.second) != cudaSuccess) return fail(c, LMFAO_ERR_CUDA, "profile: event sync failed");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    t += ms;
+  }
+  *total_ms = t;
+  *launches = (int64_t)c->prof_events.size();
   return LMFAO_OK;
 }

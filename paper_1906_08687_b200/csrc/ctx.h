@@ -30,6 +30,10 @@ struct Rel {
   DevBuf dense_key;  // dense key id per row (rows sorted by it)
   bool unique_key = false;
   std::vector<DevBuf> fk_dense;  // per child: dense id of the child key per row
+  // root only, sharded runs: dictionaries of every int32 column over the WHOLE root
+  // (before slicing), so group-by cells mean the same on every rank
+  std::map<int, DevBuf> full_dict;
+  std::map<int, int64_t> full_dict_n;
   int find_attr(int a) const {
     for (size_t i = 0; i < cols.size(); i++)
       if (cols[i].attr == a) return (int)i;
@@ -140,5 +144,14 @@ struct lmfao_ctx {
   std::unique_ptr<FastPaths> fast;  // specialised kernels (gram / hist), if the batch matches
   bool ran = false;
   int64_t launches_last_run = 0;
+  // optional timer around the dominant root-scan kernel (lmfao_profile)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::string prof_kernel;
 };
+
+namespace lmfao {
+void scan_timer_begin(lmfao_ctx* c, cudaStream_t st);
+void scan_timer_end(lmfao_ctx* c, cudaStream_t st);
+}
 

@@ -40,7 +40,8 @@ struct DevBuf {
   }
   cudaError_t alloc(size_t b) {
     reset();
-    if (b == 0) b = 16;
+    // 256 B of slack: TMA bulk copies round tail sizes up to 16 B
+    b += 256;
     cudaError_t e = cudaMalloc(&p, b);
     if (e == cudaSuccess) bytes = b;
     else p = nullptr;

@@ -14,8 +14,11 @@ struct FastPaths {
   // produced all no-group-by outputs.  Returns a cudaError_t value (0 = ok).
   virtual int run(lmfao_ctx* c, const NodeArgs& root, cudaStream_t st, bool& scalar_done) = 0;
   virtual bool handles_group(int query) const { return false; }
+  // true if the specialised path builds its own dimension tables (skip generic views)
+  virtual bool skip_generic_views() const { return false; }
   virtual std::string describe() const = 0;
 };
 // Returns nullptr when no specialised path applies (the generic path runs).
 FastPaths* plan_fast_paths(lmfao_ctx* c);
+FastPaths* plan_gram(lmfao_ctx* c);
 }  // namespace lmfao

@@ -64,6 +64,8 @@ _SIGS = {
     "lmfao_fetch": [_P, ctypes.c_int32, _P, _P, _P],
     "lmfao_result_device": [_P, ctypes.c_int32, ctypes.POINTER(_P), ctypes.POINTER(_P), ctypes.POINTER(_P)],
     "lmfao_plan_info": [_P, ctypes.c_char_p, ctypes.c_int64],
+    "lmfao_profile": [_P, ctypes.c_int],
+    "lmfao_profile_read": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -228,6 +230,14 @@ class Engine:
         k, v, c = _P(), _P(), _P()
         self._check(_lib.lmfao_result_device(self.h, q, ctypes.byref(k), ctypes.byref(v), ctypes.byref(c)))
         return k.value, v.value, c.value
+
+    def profile(self, enable: bool = True):
+        self._check(_lib.lmfao_profile(self.h, int(enable)))
+
+    def profile_read(self):
+        t, n = ctypes.c_double(), ctypes.c_int64()
+        self._check(_lib.lmfao_profile_read(self.h, ctypes.byref(t), ctypes.byref(n)))
+        return t.value, n.value
 
     def plan_info(self) -> dict:
         buf = ctypes.create_string_buffer(1 << 16)

@@ -109,11 +109,15 @@ def test_simulated_sharding_partials_sum_to_oracle(nparts):
     assert np.allclose(tot, ref.vals, rtol=1e-9)
 
 
-def test_repeated_runs_identical():
+def test_repeated_runs_consistent():
+    """Re-running a plan gives the same counts bit-exactly and the same sums up to
+    reassociation (the Gram path schedules work items dynamically, so the order of
+    FP64 additions may differ between runs; reading R14)."""
     w = synth.config2(fact_rows=20_000, dim_rows=(30, 200, 1500))
     a = run_gpu(w.db, w.batch, runs=1)
     b = run_gpu(w.db, w.batch, runs=3)
-    assert np.array_equal(a[0][1], b[0][1])
+    assert np.array_equal(a[0][2], b[0][2])
+    assert np.allclose(a[0][1], b[0][1], rtol=1e-12, atol=1e-12)
 
 
 def test_empty_root_and_empty_child():
