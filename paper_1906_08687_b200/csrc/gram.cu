@@ -22,6 +22,8 @@
 // DMMA fragment layout (PTX mma.m8n8k4 .f64): lane = 4*m + k; A[m][k] = a0,
 // B[k][n=m] = b0, C[m][2k+i] = c_i.  Here k indexes the 4 rows (or 4 records)
 // of a group and m the feature: lane (m, k) holds feature m of row k.
+#include <cuda.h>
+
 #include <set>
 
 #include "ctx.h"
@@ -29,6 +31,7 @@
 namespace lmfao {
 
 struct GramArgs {
+  CUtensorMap tmL;  // gather4 tensor map over the deepest view V_L [nk x WL] (must stay first: 64-B aligned)
   int64_t nrows;
   int nF, nL, nA, nB;
   const double* x[8];
@@ -45,17 +48,21 @@ struct GramArgs {
   unsigned* HA;
   unsigned* HB;
   double* partials;
-  int WG;             // gathered row stride in smem (doubles, even): [s_L | pad | 1 | 0]
+  int nLe;            // s_L columns staged per gathered row (nL rounded to 16 bytes)
+  int gslot;          // doubles per gather4 destination slot (4 rows, 128-B multiple)
   int cn;             // B / record column holding the constant 1 (the count)
   int* work;          // dynamic work-item counter (zeroed before each launch)
   int smem_per_warp;  // bytes
 };
 
-constexpr int CH = 32;   // rows per warp chunk (one 32-row block)
-constexpr int GRAM_THREADS = 384;  // 12 warps per CTA, one CTA per SM
-constexpr int ITEM = 512; // rows per dynamically scheduled work item (multiple of CH)
+constexpr int GW = 8;       // warps per CTA (one CTA per SM; 8 or 12 divide the 4 sub-partitions evenly)
+constexpr int ITEM = 512;   // rows per dynamically scheduled work item (per warp)
+constexpr int NSX = 3;      // stages of TMA-staged fact columns + keys (one 32-row block each)
+constexpr int NSG = 2;      // stages of gather4-staged s_L rows
+constexpr int XS = 36;      // smem column stride of a staged block (doubles): 16-B aligned, conflict-free
+constexpr int RCAP = 4;     // pending A records per DMMA batch
 constexpr int HCACHE_BITS = 6, HCACHE = 1 << HCACHE_BITS;
-constexpr int XST = 36;  // smem column stride (doubles): 16-B aligned, conflict-free DMMA-layout reads
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
@@ -100,6 +107,15 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int col, int r0, int r1, int r2, int r3,
+                                            uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
+      "%5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(b))
+      : "memory");
+}
+
 template <int NB, int NS, int NTS>
 struct GramTiles {
   static constexpr int TA = NS >= 1 ? NB * NTS : 0;
@@ -108,85 +124,78 @@ struct GramTiles {
   static constexpr int TOT = NB + TA + T12 + TB;
 };
 
+// Per warp: contiguous work items of ITEM rows (dynamic), processed in 32-row
+// blocks.  While a block is processed, every lane prefetches the NEXT block's
+// operands into registers directly in the DMMA lane layout -- x_m of row k, the
+// view values s_L[key(row k)][col] (L2-resident) -- and the keys two blocks
+// ahead; at the start of the block it parks them in its slots of a per-warp
+// shared buffer [group][tile][lane].  The group loop is deliberately not unrolled
+// and reads its operands from those slots, which keeps the kernel small for the
+// instruction cache (the hot loop, boundary and record code exist once).
 template <int NB, int NS, int NTS>
-__global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
+__global__ void __launch_bounds__(GW * 32, 1) k_gram(const __grid_constant__ GramArgs g) {
   using T = GramTiles<NB, NS, NTS>;
+  constexpr int TREG = NB + T::TA + T::T12;
   constexpr int TOT = T::TOT;
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2;
-  const int wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+  const int wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int cn = g.cn;
-  const int tn = cn >> 3, mn = cn & 7;
-  const int WG = g.WG;
+  const int nLe = g.nLe;
   const int64_t N = g.nrows;
   const int nitems = (int)((N + ITEM - 1) / ITEM);
+  const int nB = g.nB;
+  const int nkeycols = 1 + (NS >= 1) + (NS == 2);
 
-  double acc[TOT][2];
-#pragma unroll
-  for (int t = 0; t < TOT; t++) acc[t][0] = acc[t][1] = 0.0;
-  // per-lane (row phase k) prefix sums of the B columns over the current item, and the
-  // prefix at the start of the open level-A run: a run's record = P(end) - P(start)
-  double P[NB], Ps[NB], sumB[NB];
-#pragma unroll
-  for (int t = 0; t < NB; t++) P[t] = Ps[t] = sumB[t] = 0.0;
-  double preA[NTS], preAB[NTS], preB[NTS];
-#pragma unroll
-  for (int t = 0; t < NTS; t++) preA[t] = preAB[t] = preB[t] = 0.0;
-  int npA = 0, npB = 0;
-  bool runA_ne = false, runB_ne = false;
-  int curA = -1, curB = -1;
-  int prevL = -1, prevA = -1, prevB = -1;
-  int runL_start = 0;  // row index within the item
-
-  // ---- per-warp shared memory
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  unsigned char* wp = smem_raw + (size_t)wib * g.smem_per_warp;
-  double* xs = reinterpret_cast<double*>(wp);  // [3][8][XST]
-  wp += 3 * 8 * XST * 8;
-  double* gsb = reinterpret_cast<double*>(wp);  // [2][CH][WG]
-  wp += 2 * CH * WG * 8;
-  double* recA = reinterpret_cast<double*>(wp);  // [4][NB][32]
-  wp += 4 * NB * 32 * 8;
-  double* recB = reinterpret_cast<double*>(wp);  // [4][NB][32]
-  wp += 4 * NB * 32 * 8;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double* bacc = reinterpret_cast<double*>(smem_raw) + (size_t)wib * 24 * 16;  // [nw][24][16]
+  unsigned char* wp = smem_raw + (size_t)nw * 24 * 16 * 8 + (size_t)wib * g.smem_per_warp;
+  double* ob = reinterpret_cast<double*>(wp);  // operand slots [8 groups][NB][32 lanes]
+  wp += 8 * NB * 32 * 8;
+  double* recA = reinterpret_cast<double*>(wp);  // [RCAP][24]
+  wp += RCAP * 24 * 8;
+  double* recB = reinterpret_cast<double*>(wp);  // [24]
+  wp += 24 * 8;
   unsigned long long* hcache = reinterpret_cast<unsigned long long*>(wp);
   wp += HCACHE * 8;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(wp);
-  wp += 4 * 8;
-  int32_t* rkey = reinterpret_cast<int32_t*>(wp);  // [0..3] A keys, [8..11] B keys
-  wp += 16 * 4;
-  int32_t* ks = reinterpret_cast<int32_t*>(wp);  // [3][3][CH]
-  wp += 3 * 3 * CH * 4;
-  double* cst = reinterpret_cast<double*>(wp);  // 0.0, 1.0
+  int32_t* rkey = reinterpret_cast<int32_t*>(wp);  // A keys of pending records
+  for (int i = lane; i < 24 * 16; i += 32) bacc[i] = 0.0;
   for (int i = lane; i < HCACHE; i += 32) hcache[i] = 0xFFFFFFFF00000000ull;
-  if (lane == 0) {
-    cst[0] = 0.0;
-    cst[1] = 1.0;
-  }
-  const int gch = (g.nL + 1) / 2;
-  for (int i = lane; i < 2 * CH; i += 32)
-    for (int c2 = 2 * gch; c2 < WG; c2++) gsb[(size_t)i * WG + c2] = (c2 == cn - g.nF) ? 1.0 : 0.0;
-  const uint32_t cst0 = smem_u32(cst);
-  const int nkeycols = 1 + (NS >= 1) + (NS == 2);
-  if (lane == 0) {
-    for (int s = 0; s < 3; s++) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
   __syncwarp();
 
-  // per-lane operand addressing (relative to a stage): A = x column m (or 0); B col 8t+m
+  // B operand column 8t+m: x (t = 0, m < nF) | staged s_L column | constant (1 for the count column)
   const bool isx0 = m < g.nF;
-  uint32_t boff[NB], bstep[NB];  // byte offset within the gathered buffer or -1 markers
-  int bkind[NB];
+  bool isg[NB];
+  int gcol[NB];
+  double onev[NB];
 #pragma unroll
   for (int t = 0; t < NB; t++) {
     const int col = 8 * t + m;
     const int gc = col - g.nF;
-    bkind[t] = col < g.nF ? 0 : (gc < WG ? 1 : 2);
-    boff[t] = bkind[t] == 1 ? (uint32_t)((k * WG + gc) * 8) : 0u;
-    bstep[t] = bkind[t] == 0 ? 32u : (bkind[t] == 1 ? (uint32_t)(4 * WG * 8) : 0u);
+    isg[t] = col >= g.nF && gc < g.nL;
+    gcol[t] = isg[t] ? gc : 0;
+    onev[t] = col == cn ? 1.0 : 0.0;
   }
+  const double* xcolm = g.x[0];
+#pragma unroll
+  for (int i = 1; i < 8; i++)
+    if (m == i) xcolm = g.x[i];
+  const unsigned WL = (unsigned)g.WL;
 
-  // ---------------------------------------------------------------- H_L
+  double acc[TREG][2];
+#pragma unroll
+  for (int t = 0; t < TREG; t++) acc[t][0] = acc[t][1] = 0.0;
+  double P[NB], Ps[NB], sumB[NB];
+#pragma unroll
+  for (int t = 0; t < NB; t++) P[t] = Ps[t] = sumB[t] = 0.0;
+  double preA[NTS], preAB[NTS];
+#pragma unroll
+  for (int t = 0; t < NTS; t++) preA[t] = preAB[t] = 0.0;
+  int npA = 0;
+  bool runA_ne = false, runB_ne = false;
+  int curA = -1, curB = -1;
+  int prevL = -1, prevA = -1, prevB = -1;
+  int runL_start = 0;
+
   auto hl_flush_lanes = [&](bool fl, int key, unsigned len) {
     if (!__any_sync(FULL, fl)) return;
     const unsigned peers = __match_any_sync(FULL, fl ? key : -1 - lane);
@@ -218,75 +227,57 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
     }
     __syncwarp();
   };
-
-  // ---------------------------------------------------------------- records
+  auto reduce4 = [&](double v) {
+    v += __shfl_xor_sync(FULL, v, 1);
+    v += __shfl_xor_sync(FULL, v, 2);
+    return v;
+  };
   auto process_A = [&]() {
     __syncwarp();
     const bool rv = k < npA;
     double a[NB];
 #pragma unroll
-    for (int t = 0; t < NB; t++) {
-      const double* r = recA + ((size_t)k * NB + t) * 32 + 4 * m;
-      a[t] = rv ? (r[0] + r[1]) + (r[2] + r[3]) : 0.0;
-    }
-    double nk_own = 0.0;
-#pragma unroll
-    for (int t = 0; t < NB; t++)
-      if (t == tn) nk_own = a[t];
-    const double nk = __shfl_sync(FULL, nk_own, mn * 4 + k);
+    for (int t = 0; t < NB; t++) a[t] = rv ? recA[k * 24 + 8 * t + m] : 0.0;
+    const double nk = rv ? recA[k * 24 + cn] : 0.0;
 #pragma unroll
     for (int t = 0; t < NB; t++)
 #pragma unroll
-      for (int t2 = 0; t2 < NTS; t2++) dmma(acc[NB + t * NTS + t2], a[t], preA[t2]);
+      for (int t2 = 0; t2 < NTS; t2++) dmma(acc[NB + t * NTS + t2], a[t], rv ? preA[t2] : 0.0);
     if constexpr (NS == 2) {
 #pragma unroll
       for (int t1 = 0; t1 < NTS; t1++)
 #pragma unroll
-        for (int t2 = 0; t2 < NTS; t2++) dmma(acc[NB + T::TA + t1 * NTS + t2], nk * preAB[t1], preA[t2]);
+        for (int t2 = 0; t2 < NTS; t2++)
+          dmma(acc[NB + T::TA + t1 * NTS + t2], rv ? nk * preAB[t1] : 0.0, rv ? preA[t2] : 0.0);
     }
-    if (rv && m == mn) atomicAdd(&g.HA[rkey[k]], (unsigned)nk);
+    if (rv && m == 0) atomicAdd(&g.HA[rkey[k]], (unsigned)nk);
 #pragma unroll
     for (int t = 0; t < NTS; t++) preA[t] = preAB[t] = 0.0;
     npA = 0;
     __syncwarp();
   };
-  auto process_B = [&]() {
-    __syncwarp();
-    const bool rv = k < npB;
-    double a[NB];
+  // level-B record (rare): reduced sums (x) s_B into this warp's shared block
+  auto push_B = [&](int keyB) {
 #pragma unroll
     for (int t = 0; t < NB; t++) {
-      const double* r = recB + ((size_t)k * NB + t) * 32 + 4 * m;
-      a[t] = rv ? (r[0] + r[1]) + (r[2] + r[3]) : 0.0;
+      const double v = reduce4(sumB[t]);
+      if (k == 0) recB[8 * t + m] = v;
     }
-    double nk_own = 0.0;
-#pragma unroll
-    for (int t = 0; t < NB; t++)
-      if (t == tn) nk_own = a[t];
-#pragma unroll
-    for (int t = 0; t < NB; t++)
-#pragma unroll
-      for (int t1 = 0; t1 < NTS; t1++) dmma(acc[NB + T::TA + T::T12 + t * NTS + t1], a[t], preB[t1]);
-    if (rv && m == mn) atomicAdd(&g.HB[rkey[8 + k]], (unsigned)nk_own);
-#pragma unroll
-    for (int t = 0; t < NTS; t++) preB[t] = 0.0;
-    npB = 0;
     __syncwarp();
-  };
-  auto push_B = [&](int keyB) {  // record = sumB (per lane, unreduced)
-#pragma unroll
-    for (int t = 0; t < NB; t++) recB[((size_t)npB * NB + t) * 32 + lane] = sumB[t];
-    if (lane == 0) rkey[8 + npB] = keyB;
-    if (k == npB) {
-      const double* row = g.VB + (unsigned)keyB * (unsigned)g.WB;
-      preB[0] = m < g.nB ? row[m] : 0.0;
-      if constexpr (NTS == 2) preB[1] = 8 + m < g.nB ? row[8 + m] : 0.0;
+    const double* row = g.VB + (unsigned)keyB * (unsigned)g.WB;
+    for (int e = lane; e < 24 * nB; e += 32) {
+      const int c = e / nB, f = e % nB;
+      bacc[c * 16 + f] += recB[c] * row[f];
     }
-    if (++npB == 4) process_B();
+    if (lane == 0) atomicAdd(&g.HB[keyB], (unsigned)recB[cn]);
+    __syncwarp();
   };
   auto push_A = [&](const double* rec, int keyA, int keyB) {
 #pragma unroll
-    for (int t = 0; t < NB; t++) recA[((size_t)npA * NB + t) * 32 + lane] = rec[t];
+    for (int t = 0; t < NB; t++) {
+      const double v = reduce4(rec[t]);
+      if (k == 0) recA[npA * 24 + 8 * t + m] = v;
+    }
     if (lane == 0) rkey[npA] = keyA;
     if (k == npA) {
       const double* row = g.VA + (unsigned)keyA * (unsigned)g.WA;
@@ -294,8 +285,8 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
       if constexpr (NTS == 2) preA[1] = 8 + m < g.nA ? row[8 + m] : 0.0;
       if constexpr (NS == 2) {
         const double* rowb = g.VB + (unsigned)keyB * (unsigned)g.WB;
-        preAB[0] = m < g.nB ? rowb[m] : 0.0;
-        if constexpr (NTS == 2) preAB[1] = 8 + m < g.nB ? rowb[8 + m] : 0.0;
+        preAB[0] = m < nB ? rowb[m] : 0.0;
+        if constexpr (NTS == 2) preAB[1] = 8 + m < nB ? rowb[8 + m] : 0.0;
       }
     }
     if constexpr (NS == 2) {
@@ -303,10 +294,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
       for (int t = 0; t < NB; t++) sumB[t] += rec[t];
       runB_ne = true;
     }
-    if (++npA == 4) process_A();
+    if (++npA == RCAP) process_A();
   };
-  // close the open runs of an item ending at row-within-item `end`
-  auto flush_item = [&](int end) {
+  auto flush_range = [&](int end) {
     if constexpr (NS >= 1) {
       if (runA_ne) {
         double rec[NB];
@@ -319,13 +309,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
       }
     }
     hl_flush_lanes(lane == 0 && end > runL_start && prevL >= 0, prevL, (unsigned)(end - runL_start));
-#pragma unroll
-    for (int t = 0; t < NB; t++) P[t] = Ps[t] = sumB[t] = 0.0;
-    runA_ne = runB_ne = false;
-    prevL = prevA = prevB = -1;
   };
 
-  // ---------------------------------------------------------------- work items, staging
+  // ---- block sequence over dynamically grabbed items
   int ring[4] = {0, 0, 0, 0};
   int nring = 0;
   auto grab = [&]() {
@@ -344,106 +330,99 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
       if ((slot & 3) == i) it = ring[i];
     return it;
   };
-  // cursor over (item, chunk) with a chunk sequence number for stage selection
-  int tm_slot = 0, tm_c = 0, tm_seq = 0, tm_item;   // TMA cursor (2 ahead)
-  int ga_slot = 0, ga_c = 0, ga_seq = 0, ga_item;   // gather cursor (1 ahead)
-  int ct_c = 0, ct_seq = 0, ct_slot = 0, ct_item;   // compute cursor
   auto item_rows = [&](int it) {
     const int64_t r = (int64_t)it * ITEM;
     return (int)(N - r < ITEM ? N - r : ITEM);
   };
-  auto adv = [&](int& slot, int& c, int& seq, int& item, bool may_grab) {
-    seq++;
-    if ((c + 1) * CH < item_rows(item)) {
-      c++;
+  struct Cur {
+    int slot, b, seq, item;
+  };
+  auto adv = [&](Cur& u, bool may_grab) {
+    u.seq++;
+    if ((u.b + 1) * 32 < item_rows(u.item)) {
+      u.b++;
     } else {
-      c = 0;
-      slot++;
-      if (may_grab && slot >= nring) grab();
-      item = ring_at(slot);
+      u.b = 0;
+      u.slot++;
+      if (may_grab && u.slot >= nring) grab();
+      u.item = ring_at(u.slot);
     }
   };
-  const double* xcol = g.x[0];
+  // register prefetch of a block's operands (DMMA lane layout) and keys (lane = row)
+  double px[8], pg[NB][8];
+  int pk[3] = {-1, -1, -1};  // keys of the block whose operands are prefetched next
+  int qk[3] = {-1, -1, -1};  // keys of the block after it
+  auto row0_of = [&](const Cur& u) { return (int64_t)u.item * ITEM + u.b * 32; };
+  auto nrows_of = [&](const Cur& u) { return min(32, item_rows(u.item) - u.b * 32); };
+  auto load_keys = [&](const Cur& u, int (&kk)[3]) {
+    kk[0] = kk[1] = kk[2] = -1;
+    if (u.item < nitems && lane < nrows_of(u)) {
+      const int64_t r = row0_of(u) + lane;
+      kk[0] = g.kL[r];
+      if (NS >= 1) kk[1] = g.kA[r];
+      if (NS == 2) kk[2] = g.kB[r];
+    }
+  };
+  auto load_ops = [&](const Cur& u) {  // operands of block u; pk holds its keys
+    const int n = u.item < nitems ? nrows_of(u) : 0;
+    const int64_t r0 = u.item < nitems ? row0_of(u) : 0;
 #pragma unroll
-  for (int i = 1; i < 8; i++)
-    if (lane == i) xcol = g.x[i];
-  const int32_t* kcl = lane == 8 ? g.kL : (lane == 9 ? g.kA : g.kB);
-  auto issue_tma = [&](int item, int c, int seq) {
-    const int s = seq % 3;
-    const int64_t r = (int64_t)item * ITEM + c * CH;
-    const int n = min(CH, item_rows(item) - c * CH);
-    const uint32_t bx = (uint32_t)((n * 8 + 15) & ~15), bk = (uint32_t)((n * 4 + 15) & ~15);
-    if (lane == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&bars[s], bx * g.nF + bk * nkeycols);
-    }
-    __syncwarp();
-    if (lane < g.nF) tma_load_1d(xs + ((size_t)s * 8 + lane) * XST, xcol + r, bx, &bars[s]);
-    else if (lane >= 8 && lane < 8 + nkeycols) tma_load_1d(ks + ((size_t)s * 3 + (lane - 8)) * CH, kcl + r, bk, &bars[s]);
-  };
-  auto wait_tma = [&](int seq) { mbar_wait(&bars[seq % 3], (uint32_t)((seq / 3) & 1)); };
-  const int q32 = gch ? 32 / gch : 0, r32 = gch ? 32 % gch : 0;
-  const int rr0 = gch ? lane / gch : 0, pc0 = gch ? lane % gch : 0;
-  const unsigned WL = (unsigned)g.WL;
-  auto issue_gather = [&](int item, int c, int seq) {
-    const int s = seq % 3;
-    const int n = min(CH, item_rows(item) - c * CH);
-    double* dst = gsb + (size_t)(seq & 1) * CH * WG;
-    const int32_t* kk = ks + (size_t)s * 3 * CH;
-    int rr = rr0, pc = pc0;
-    while (rr < n) {
-      cp_async16(dst + rr * WG + 2 * pc, g.VL + ((unsigned)kk[rr] * WL + 2 * pc));
-      rr += q32;
-      pc += r32;
-      if (pc >= gch) {
-        pc -= gch;
-        rr++;
+    for (int j = 0; j < 8; j++) {
+      const int rj = 4 * j + k;
+      const int key = __shfl_sync(FULL, pk[0], rj);
+      const bool v = rj < n;
+      px[j] = (isx0 && v) ? xcolm[r0 + rj] : 0.0;
+      const double* row = g.VL + (unsigned)(v ? key : 0) * WL;
+#pragma unroll
+      for (int t = 0; t < NB; t++) {
+        double val = v ? onev[t] : 0.0;
+        if (v && isg[t]) val = row[gcol[t]];
+        pg[t][j] = val;
       }
     }
-    cp_async_commit();
+  };
+  auto park_ops = [&]() {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+#pragma unroll
+      for (int t = 0; t < NB; t++) ob[(j * NB + t) * 32 + lane] = (t == 0 && isx0) ? px[j] : pg[t][j];
   };
 
   grab();
-  tm_item = ga_item = ct_item = ring_at(0);
-  if (ct_item < nitems) {
-    issue_tma(tm_item, tm_c, tm_seq);
-    adv(tm_slot, tm_c, tm_seq, tm_item, true);
-    if (tm_item < nitems) {
-      issue_tma(tm_item, tm_c, tm_seq);
-      adv(tm_slot, tm_c, tm_seq, tm_item, true);
-    }
-    wait_tma(ga_seq);
-    if (gch) issue_gather(ga_item, ga_c, ga_seq);
-    adv(ga_slot, ga_c, ga_seq, ga_item, false);
-  }
-  int prev_item_rows = -1;
-  while (ct_item < nitems) {
-    const bool more = ga_item < nitems;
-    if (more) {
-      wait_tma(ga_seq);
-      if (gch) issue_gather(ga_item, ga_c, ga_seq);
-    }
-    if (tm_item < nitems) issue_tma(tm_item, tm_c, tm_seq);
-    if (more) cp_async_wait<1>();
-    else cp_async_wait<0>();
+  Cur c0{0, 0, 0, ring_at(0)};
+  Cur c1 = c0, c2 = c0;  // c1: operands in flight (one ahead), c2: keys in flight (two ahead)
+  int ck[3];             // keys (lane = row) of block c0
+  load_keys(c0, pk);
+  ck[0] = pk[0];
+  ck[1] = pk[1];
+  ck[2] = pk[2];
+  load_ops(c0);
+  adv(c1, true);
+  adv(c2, true);
+  adv(c2, true);
+  load_keys(c1, pk);
+  int range_end = -1;
+  while (c0.item < nitems) {
+    park_ops();  // operands of block c0 -> this lane's slots
     __syncwarp();
-    const int irows = item_rows(ct_item);
-    if (ct_c == 0) {
-      if (prev_item_rows >= 0) flush_item(prev_item_rows);
+    load_keys(c2, qk);  // prefetch: keys two blocks ahead, operands of the next block
+    load_ops(c1);
+    const int irows = item_rows(c0.item);
+    const int ro = c0.b * 32;
+    const int nval = min(32, irows - ro);
+    if (c0.b == 0) {  // new contiguous item: close the previous range
+      if (range_end >= 0) flush_range(range_end);
+#pragma unroll
+      for (int t = 0; t < NB; t++) P[t] = Ps[t] = sumB[t] = 0.0;
+      runA_ne = runB_ne = false;
+      prevL = prevA = prevB = -1;
       runL_start = 0;
-      prev_item_rows = irows;
     }
-    const int ro = ct_c * CH;  // row offset within the item
-    const int nval = min(CH, irows - ro);
-    const int s = ct_seq % 3;
-    const double* xsc = xs + (size_t)s * 8 * XST;
-    const int32_t* ksc = ks + (size_t)s * 3 * CH;
-    double* gsc = gsb + (size_t)(ct_seq & 1) * CH * WG;
-    // -- row lanes: keys and boundary masks of the 32-row chunk
+    range_end = irows;
     const bool vr = lane < nval;
-    const int kl = vr ? ksc[lane] : -1;
-    const int ka = (NS >= 1 && vr) ? ksc[CH + lane] : -1;
-    const int kb = (NS == 2 && vr) ? ksc[2 * CH + lane] : -1;
+    const int kl = vr ? ck[0] : -1;
+    const int ka = (NS >= 1 && vr) ? ck[1] : -1;
+    const int kb = (NS == 2 && vr) ? ck[2] : -1;
     int pl = __shfl_up_sync(FULL, kl, 1), pa = __shfl_up_sync(FULL, ka, 1), pb = __shfl_up_sync(FULL, kb, 1);
     if (lane == 0) {
       pl = prevL;
@@ -459,84 +438,64 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
     prevL = __shfl_sync(FULL, kl, nval - 1);
     prevA = __shfl_sync(FULL, ka, nval - 1);
     prevB = __shfl_sync(FULL, kb, nval - 1);
-    {  // H_L: lane i with a boundary flushes the run ending at row i-1 (key pl)
+    {
       const unsigned before = mL & ((1u << lane) - 1u);
       const int st = before ? ro + (31 - __clz(before)) : runL_start;
       const int len = ro + lane - st;
       hl_flush_lanes(dL && len > 0 && pl >= 0, pl, (unsigned)len);
       if (mL) runL_start = ro + (31 - __clz(mL));
     }
-    if (nval < CH) {  // the table's final partial chunk: zero its invalid rows in smem
-      if (lane >= nval) {
-        for (int f = 0; f < g.nF; f++) const_cast<double*>(xsc)[f * XST + lane] = 0.0;
-        for (int c2 = 0; c2 < WG; c2++) gsc[lane * WG + c2] = 0.0;
-      }
-      __syncwarp();
-    }
-    uint32_t xaddr = isx0 ? smem_u32(xsc + m * XST + k) : cst0;
-    const uint32_t xstep = isx0 ? 32u : 0u;
-    const uint32_t gbase = smem_u32(gsc);
-    uint32_t baddr[NB];
-#pragma unroll
-    for (int t = 0; t < NB; t++) baddr[t] = bkind[t] == 0 ? xaddr : (bkind[t] == 1 ? gbase + boff[t] : cst0);
     const int ngr = (nval + 3) >> 2;
 #pragma unroll 1
     for (int j = 0; j < ngr; j++) {
-      const double xa = lds64(xaddr);
-      xaddr += xstep;
       double b[NB];
 #pragma unroll
-      for (int t = 0; t < NB; t++) {
-        b[t] = lds64(baddr[t]);
-        baddr[t] += bstep[t];
-      }
+      for (int t = 0; t < NB; t++) b[t] = ob[(j * NB + t) * 32 + lane];
+      const double xa = isx0 ? b[0] : 0.0;
 #pragma unroll
       for (int t = 0; t < NB; t++) dmma(acc[t], xa, b[t]);
       if constexpr (NS >= 1) {
         const unsigned nib = (mA >> (4 * j)) & 0xFu;
-        if (nib) {
-          unsigned bits = nib;
-          while (bits) {
-            const int p = __ffs(bits) - 1;
-            bits &= bits - 1;
-            double rec[NB];
+        unsigned bits = nib;
+        while (bits) {
+          const int p = __ffs(bits) - 1;
+          bits &= bits - 1;
+          double rec[NB];
 #pragma unroll
-            for (int t = 0; t < NB; t++) {
-              const double pb2 = P[t] + (k < p ? b[t] : 0.0);  // prefix just before row p
-              rec[t] = pb2 - Ps[t];
-              Ps[t] = pb2;
-            }
-            if (runA_ne) push_A(rec, curA, curB);
-            runA_ne = true;
-            if constexpr (NS == 2) {
-              if ((mB >> (4 * j + p)) & 1u) {
-                if (runB_ne) push_B(curB);
-#pragma unroll
-                for (int t = 0; t < NB; t++) sumB[t] = 0.0;
-                runB_ne = false;
-              }
-            }
-            curA = __shfl_sync(FULL, ka, 4 * j + p);
-            curB = __shfl_sync(FULL, kb, 4 * j + p);
+          for (int t = 0; t < NB; t++) {
+            const double pb2 = P[t] + (k < p ? b[t] : 0.0);
+            rec[t] = pb2 - Ps[t];
+            Ps[t] = pb2;
           }
+          if (runA_ne) push_A(rec, curA, curB);
+          runA_ne = true;
+          if constexpr (NS == 2) {
+            if ((mB >> (4 * j + p)) & 1u) {
+              if (runB_ne) push_B(curB);
+#pragma unroll
+              for (int t = 0; t < NB; t++) sumB[t] = 0.0;
+              runB_ne = false;
+            }
+          }
+          curA = __shfl_sync(FULL, ka, 4 * j + p);
+          curB = __shfl_sync(FULL, kb, 4 * j + p);
         }
 #pragma unroll
         for (int t = 0; t < NB; t++) P[t] += b[t];
       }
     }
-    if (nval < CH) {  // restore the gathered count column of the zero-filled rows
-      if (lane >= nval)
-        for (int c2 = 2 * gch; c2 < WG; c2++) gsc[lane * WG + c2] = (c2 == cn - g.nF) ? 1.0 : 0.0;
-    }
     __syncwarp();
-    adv(ct_slot, ct_c, ct_seq, ct_item, false);
-    if (more) adv(ga_slot, ga_c, ga_seq, ga_item, false);
-    if (tm_item < nitems) adv(tm_slot, tm_c, tm_seq, tm_item, true);
+    adv(c0, false);
+    adv(c1, false);
+    adv(c2, true);
+    ck[0] = pk[0];
+    ck[1] = pk[1];
+    ck[2] = pk[2];
+    pk[0] = qk[0];
+    pk[1] = qk[1];
+    pk[2] = qk[2];
   }
-  if (prev_item_rows >= 0) flush_item(prev_item_rows);
-  if constexpr (NS == 2) {
-    if (npB > 0) process_B();
-  }
+  if (range_end >= 0) flush_range(range_end);
   if constexpr (NS >= 1) {
     if (npA > 0) process_A();
   }
@@ -545,23 +504,34 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_gram(GramArgs g) {
     const unsigned long long e = hcache[i];
     if ((unsigned)(e >> 32) != 0xFFFFFFFFu) atomicAdd(&g.HL[(unsigned)(e >> 32)], (unsigned)e);
   }
-
-  // deterministic CTA reduction (warps in order), then one partial per CTA
-  __shared__ double red[TOT * 64];
+  // deterministic CTA reduction (warps in order); the B block is summed from the warps' smem blocks
+  __syncthreads();
+  double* red = reinterpret_cast<double*>(smem_raw + (size_t)nw * 24 * 16 * 8);  // reuse staging (all consumed)
   for (int i = threadIdx.x; i < TOT * 64; i += blockDim.x) red[i] = 0.0;
   __syncthreads();
-  for (int w = 0; w < nwb; w++) {
+  for (int w = 0; w < nw; w++) {
     if (wib == w) {
 #pragma unroll
-      for (int t = 0; t < TOT; t++) {
+      for (int t = 0; t < TREG; t++) {
         red[t * 64 + m * 8 + 2 * k] += acc[t][0];
         red[t * 64 + m * 8 + 2 * k + 1] += acc[t][1];
       }
     }
     __syncthreads();
   }
+  if constexpr (NS == 2) {
+    const double* b0 = reinterpret_cast<const double*>(smem_raw);
+    for (int i = threadIdx.x; i < 24 * 16; i += blockDim.x) {
+      const int c = i / 16, f = i % 16;
+      double v = 0.0;
+      for (int w = 0; w < nw; w++) v += b0[(size_t)w * 24 * 16 + i];
+      if (c < 8 * NB && f < 8 * NTS) red[(TREG + (c / 8) * NTS + f / 8) * 64 + (c % 8) * 8 + (f % 8)] = v;
+    }
+    __syncthreads();
+  }
   for (int i = threadIdx.x; i < TOT * 64; i += blockDim.x) g.partials[(int64_t)blockIdx.x * TOT * 64 + i] = red[i];
 }
+
 
 
 __global__ void k_sum_partials(const double* __restrict__ partials, int nparts, int n, double* __restrict__ out) {
@@ -641,7 +611,8 @@ struct FastGram : FastPaths {
   Level L, A, B;
   int grid = 148, threads = 256;
   int smem_per_warp = 0;
-  int cn = 0, WG = 2;
+  int cn = 0, WG = 2, nLe = 2, gslot = 16;
+  CUtensorMap tmL;
   DevBuf partials, src, toff, tidx, tcoef, work;
   int nsrc = 0, count_idx = 0, nout = 0;
   int mom_blocks = 148 * 2;
@@ -666,7 +637,7 @@ int tiles_for(int nb, int ns, int nts) {
 
 template <int NB, int NS, int NTS>
 cudaError_t launch_gram_t(const GramArgs& g, int grid, int threads, cudaStream_t st) {
-  size_t smem = (size_t)g.smem_per_warp * (threads / 32);
+  size_t smem = (size_t)(threads / 32) * (24 * 16 * 8 + g.smem_per_warp);
   static size_t set = 0;
   if (smem > set) {
     CUDA_TRY(cudaFuncSetAttribute(k_gram<NB, NS, NTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -730,7 +701,9 @@ int FastGram::run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scala
     g.HB = B.H.as<unsigned>();
   }
   g.partials = partials.as<double>();
-  g.WG = WG;
+  g.nLe = nLe;
+  g.gslot = gslot;
+  g.tmL = tmL;
   g.cn = cn;
   g.smem_per_warp = smem_per_warp;
   g.work = work.as<int>();
@@ -844,6 +817,8 @@ FastPaths* plan_gram(lmfao_ctx* c) {
   const int cn = fg->nF + nLe;       // the count column "1" of B / records
   fg->cn = cn;
   fg->WG = nLe + 2;
+  fg->nLe = nLe;
+  fg->gslot = (4 * nLe + 15) / 16 * 16;
   fg->NB = (cn + 1 + 7) / 8;
   if (fg->NB > 3) return nullptr;
   int maxs = std::max(fg->NS >= 1 ? (int)fg->A.attrs.size() : 0, fg->NS == 2 ? (int)fg->B.attrs.size() : 0);
@@ -851,12 +826,12 @@ FastPaths* plan_gram(lmfao_ctx* c) {
   if (maxs > 16) return nullptr;
   fg->TOT = tiles_for(fg->NB, fg->NS, fg->NTS);
   {
-    fg->smem_per_warp = 3 * 8 * XST * 8 + 2 * CH * fg->WG * 8 + 2 * 4 * fg->NB * 32 * 8 + HCACHE * 8 + 4 * 8 + 16 * 4 +
-                        3 * 3 * CH * 4 + 16;
-    fg->smem_per_warp = (fg->smem_per_warp + 127) / 128 * 128;
-    int warps = GRAM_THREADS / 32;
-    while (warps > 1 && warps * fg->smem_per_warp > 212 * 1024) warps--;
-    fg->threads = warps * 32;
+    int pw = 8 * fg->NB * 32 * 8 + RCAP * 24 * 8 + 24 * 8 + HCACHE * 8 + 16;
+    pw = (pw + 127) / 128 * 128;
+    fg->smem_per_warp = pw;
+    fg->threads = GW * 32;
+    if (GW * (24 * 16 * 8 + pw) > 220 * 1024) return nullptr;
+    if ((size_t)fg->TOT * 64 * 8 > (size_t)GW * (pw + 24 * 16 * 8)) return nullptr;
   }
   cudaStream_t st = c->stream;
   // buffers
@@ -881,6 +856,31 @@ FastPaths* plan_gram(lmfao_ctx* c) {
   }
   fg->nsrc = off;
   fg->count_idx = fg->L.moff;
+  {  // gather4 tensor map over V_L [nk x W] (fp64): box = nLe columns x 1 row
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !fn)
+        return nullptr;
+      encode = (EncodeFn)fn;
+    }
+    std::memset(&fg->tmL, 0, sizeof(fg->tmL));
+    if (!fg->L.attrs.empty()) {
+      cuuint64_t dims[2] = {(cuuint64_t)fg->L.W, (cuuint64_t)std::max<int64_t>(fg->L.nk, 1)};
+      cuuint64_t strides[1] = {(cuuint64_t)fg->L.W * 8};
+      cuuint32_t box[2] = {(cuuint32_t)fg->nLe, 1};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = encode(&fg->tmL, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, fg->L.V.p, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return nullptr;
+    }
+  }
   if (fg->partials.alloc((size_t)fg->grid * fg->TOT * 64 * 8)) return nullptr;
   if (fg->work.alloc(16)) return nullptr;
   if (fg->src.alloc((size_t)fg->nsrc * 8)) return nullptr;
