@@ -193,6 +193,8 @@ def main():
     from paper_1906_08687_b200 import lmfao
 
     torch.cuda.set_device(local)
+    # a dedicated (non-default) stream: lmfao_run and the CUDA events share it
+    torch.cuda.set_stream(torch.cuda.Stream())
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args.config)
@@ -226,7 +228,6 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    eng.profile(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     with ClockSampler(local) as clk:
@@ -236,9 +237,13 @@ def main():
         ev1.record(stream)
         barrier()
     ms = ev0.elapsed_time(ev1)
+    info = eng.plan_info()
+    # dominant kernel: CUDA events around the root-scan launches (eager runs, same stream)
+    eng.profile(True)
+    for _ in range(min(args.steps, 200)):
+        eng.run(sptr)
     scan_ms, scan_n = eng.profile_read()
     eng.profile(False)
-    info = eng.plan_info()
     launches_per_run = info.get("launches_last_run", 0)
     if world > 1:
         t = torch.tensor([ms, scan_ms], dtype=torch.float64, device="cuda")

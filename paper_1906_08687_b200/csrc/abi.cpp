@@ -11,6 +11,7 @@
 // scan is the single shared pass over the largest relation (MOO).
 #include <cmath>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <functional>
 #include <set>
@@ -673,17 +674,70 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     CTX_CUDA(c, gp.counts.alloc(cells * 8), "plan group counts");
     CTX_CUDA(c, gp.prog.upload(gprogs[c->query_slot[q]], st), "plan upload group");
   }
+  // fused group-by scan: one combined program, one descriptor per group-by query
+  {
+    Program all;
+    std::vector<GroupDesc> descs;
+    for (size_t gi = 0; gi < c->groups.size(); gi++) {
+      GroupPlan& gp = c->groups[gi];
+      const Query& Q = c->queries[gp.q];
+      GroupDesc d{};
+      d.ngb = gp.g.ngb;
+      d.nudaf = gp.nudaf;
+      d.prog_base = (int)all.out_ioff.size();
+      for (int i = 0; i < d.ngb; i++) {
+        d.code[i] = gp.g.code[i];
+        d.code_child[i] = gp.g.code_child[i];
+        d.stride[i] = gp.g.stride[i];
+      }
+      d.table = gp.table.as<double>();
+      d.counts = gp.counts.as<unsigned long long>();
+      if (gp.nudaf > 64) return fail(c, LMFAO_ERR_UNSUPPORTED, "more than 64 UDAFs in a group-by query");
+      std::vector<double> cc(std::max(gp.nudaf, 1), std::nan(""));
+      for (int j = 0; j < gp.nudaf; j++) {
+        const auto& u = Q.udafs[j];
+        bool constant = u.size() == 1;
+        double coef = constant ? u[0].coeff : 0.0;
+        if (constant)
+          for (auto& f : u[0].f) {
+            if (f.kind != LMFAO_F_CONST) constant = false;
+            else coef *= f.param;
+          }
+        if (u.empty()) {
+          constant = true;
+          coef = 0.0;
+        }
+        d.countlike[j] = constant;
+        if (constant) cc[j] = coef;
+        all.out_ioff.push_back((int)all.ip.size());
+        all.out_doff.push_back((int)all.dp.size());
+        all.ip.push_back((int)u.size());
+        for (auto& pr : u) {
+          double coef2;
+          std::vector<std::tuple<int, int, uint64_t>> own;
+          std::vector<int> slots;
+          root_term(c, pr, coef2, own, slots);
+          emit_term(all, c, c->root, coef2, own, slots);
+        }
+      }
+      CTX_CUDA(c, gp.countcoef.alloc(cc.size() * 8), "plan");
+      CTX_CUDA(c, cudaMemcpy(gp.countcoef.p, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice), "plan");
+      gp.d.countcoef = gp.countcoef.as<double>();
+      descs.push_back(d);
+    }
+    CTX_CUDA(c, c->group_prog.upload(all, st), "plan upload groups");
+    CTX_CUDA(c, c->group_descs.alloc(std::max<size_t>(descs.size(), 1) * sizeof(GroupDesc)), "plan");
+    if (!descs.empty())
+      CTX_CUDA(c, cudaMemcpy(c->group_descs.p, descs.data(), descs.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice),
+               "plan");
+  }
   // specialised kernels for recognised batch shapes (gram.cu / hist.cu)
   c->fast.reset(plan_fast_paths(c));
   c->state = S_PLANNED;
   return LMFAO_OK;
 }
 
-extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
-  if (!c) return LMFAO_ERR_INVALID_ARG;
-  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
-  cudaSetDevice(c->device);
-  cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
+static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
   launches_counter_reset();
   // (b) views, bottom-up
   for (int u : c->postorder) {
@@ -716,14 +770,15 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
                                         nout, c->scalar_out.as<double>(), c->scalar_count.as<unsigned long long>(), st),
              "run combine");
   }
-  for (auto& gp : c->groups) {
-    if (c->fast && c->fast->handles_group(gp.q)) continue;
-    CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "run memset");
-    CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "run memset");
-    CTX_CUDA(c, launch_root_group(ra, gp.g, gp.prog.pi.as<int32_t>(), gp.prog.pd.as<double>(),
-                                  gp.prog.pio.as<int32_t>(), gp.prog.pdo.as<int32_t>(), gp.nudaf, gp.table.as<double>(),
-                                  gp.counts.as<unsigned long long>(), st),
-             "run group");
+  if (!c->groups.empty()) {
+    for (auto& gp : c->groups) {
+      CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "run memset");
+      CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "run memset");
+    }
+    CTX_CUDA(c, launch_groups_fused(ra, c->group_descs.as<GroupDesc>(), (int)c->groups.size(),
+                                    c->group_prog.pi.as<int32_t>(), c->group_prog.pd.as<double>(),
+                                    c->group_prog.pio.as<int32_t>(), c->group_prog.pdo.as<int32_t>(), st),
+             "run groups");
   }
   // combine across GPUs (domain parallelism)
   if (c->world > 1) {
@@ -741,6 +796,52 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   for (auto& gp : c->groups) gp.compacted = false;
   c->ran = true;
   c->launches_last_run = launches_counter_reset();
+  return LMFAO_OK;
+}
+
+// lmfao_run: the first run executes eagerly (lazy kernel attributes, validation);
+// the second captures the whole sequence into a CUDA Graph on the ctx stream and
+// every later run replays it on the caller's stream (one launch instead of ~a dozen).
+// Profiling runs and multi-GPU runs (NCCL) stay eager.
+extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
+  cudaSetDevice(c->device);
+  cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
+  const char* ng = std::getenv("LMFAO_NO_GRAPH");
+  bool use_graph = !c->prof && c->world == 1 && !(ng && ng[0] == '1');
+  if (!use_graph || c->graph_runs == 0) {
+    c->graph_runs++;
+    return run_body(c, st);
+  }
+  if (!c->graph_exec) {
+    cudaStream_t cs = c->stream;
+    if (st != cs) {  // order the capture stream after the caller's work
+      cudaEvent_t ev;
+      CTX_CUDA(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "graph");
+      CTX_CUDA(c, cudaEventRecord(ev, st), "graph");
+      CTX_CUDA(c, cudaStreamWaitEvent(cs, ev, 0), "graph");
+      cudaEventDestroy(ev);
+    }
+    CTX_CUDA(c, cudaStreamSynchronize(cs), "graph");
+    CTX_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "graph capture");
+    lmfao_status s = run_body(c, cs);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    if (s != LMFAO_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return s;
+    }
+    CTX_CUDA(c, e, "graph end capture");
+    e = cudaGraphInstantiate(&c->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CTX_CUDA(c, e, "graph instantiate");
+    c->graph_launches = c->launches_last_run;
+  }
+  CTX_CUDA(c, cudaGraphLaunch(c->graph_exec, st), "graph launch");
+  for (auto& gp : c->groups) gp.compacted = false;
+  c->launches_last_run = c->graph_launches;
+  c->graph_runs++;
   return LMFAO_OK;
 }
 

@@ -109,6 +109,7 @@ struct GroupPlan {
   DevProgram prog;
   bool compacted = false;
   DevBuf rkeys, rvals, rcnts;
+  DevBuf countcoef;
   int64_t ngroups = 0;
 };
 
@@ -139,6 +140,8 @@ struct lmfao_ctx {
   DevBuf partials, cpart, scalar_out, scalar_count;
   int scalar_grid = 0;
   std::vector<GroupPlan> groups;
+  DevProgram group_prog;  // all group-by UDAFs (fused scan)
+  DevBuf group_descs;     // GroupDesc per group-by query
   std::vector<int> query_kind;  // 0 scalar, 1 group (index into groups)
   std::vector<int> query_slot;
   std::unique_ptr<FastPaths> fast;  // specialised kernels (gram / hist), if the batch matches
@@ -148,6 +151,12 @@ struct lmfao_ctx {
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   std::string prof_kernel;
+  // CUDA Graph of lmfao_run (see abi.cpp)
+  cudaGraphExec_t graph_exec = nullptr;
+  int64_t graph_runs = 0, graph_launches = 0;
+  ~lmfao_ctx() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  }
 };
 
 namespace lmfao {

@@ -215,6 +215,64 @@ cudaError_t launch_root_group(const NodeArgs& a, const GroupArgs& g, const int32
   return cudaGetLastError();
 }
 
+// Fused group-by scan: one pass over the root for every group-by query of the
+// batch.  Lanes holding the same (query, cell) are found with __match_any_sync;
+// counts are aggregated per warp (popc of the peers when every multiplicity is 1)
+// so Zipf-hot cells take one atomic per warp instead of one per row.  UDAFs that
+// are constants (SUM(c), e.g. COUNT) are not accumulated at all: the compaction
+// derives them from the counts.
+__global__ void k_groups_fused(NodeArgs a, const GroupDesc* __restrict__ descs, int nq,
+                               const int32_t* __restrict__ prog_i, const double* __restrict__ prog_d,
+                               const int32_t* __restrict__ ioff, const int32_t* __restrict__ doff) {
+  int32_t kk[MAX_CHILD];
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; base < a.nrows;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = base + (threadIdx.x & ~31) + lane;
+    const bool valid = row < a.nrows;
+    double w = valid ? 1.0 : 0.0;
+    for (int c = 0; c < a.nchild; c++) {
+      kk[c] = valid ? a.fk[c][row] : 0;
+      if (valid) w *= a.V[c][(int64_t)kk[c] * a.W[c]];
+    }
+    const bool ones = __all_sync(0xffffffffu, !valid || w == 1.0);
+    for (int q = 0; q < nq; q++) {
+      const GroupDesc& d = descs[q];
+      long long cell = -1 - lane;
+      if (valid && w != 0.0) {
+        cell = 0;
+        for (int i = 0; i < d.ngb; i++) {
+          const int cc = d.code_child[i];
+          const int32_t code = cc < 0 ? d.code[i][row] : d.code[i][kk[cc]];
+          cell += (long long)code * d.stride[i];
+        }
+      }
+      if (ones) {
+        const unsigned peers = __match_any_sync(0xffffffffu, cell);
+        if (cell >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&d.counts[cell], (unsigned long long)__popc(peers));
+      } else if (cell >= 0) {
+        atomicAdd(&d.counts[cell], (unsigned long long)w);
+      }
+      if (cell >= 0) {
+        for (int j = 0; j < d.nudaf; j++) {
+          if (d.countlike[j]) continue;
+          const int o = d.prog_base + j;
+          const double v = eval_output(a, row, kk, prog_i + ioff[o], prog_d + doff[o]);
+          if (v != 0.0) atomicAdd(&d.table[cell * d.nudaf + j], v);
+        }
+      }
+    }
+  }
+}
+
+cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int nq, const int32_t* prog_i,
+                                const double* prog_d, const int32_t* ioff, const int32_t* doff, cudaStream_t st) {
+  if (a.nrows <= 0 || nq == 0) return cudaSuccess;
+  k_groups_fused<<<grid_rows(a.nrows, 16), 256, 0, st>>>(a, descs, nq, prog_i, prog_d, ioff, doff);
+  launches_add(1);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- compaction
 __global__ void k_present(const unsigned long long* __restrict__ counts, int64_t n, uint32_t* flags) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -229,7 +287,9 @@ __global__ void k_scatter_groups(const double* __restrict__ table, const unsigne
     if (!flags[i]) continue;
     int64_t g = excl[i];
     for (int a = 0; a < d.ngb; a++) keys[g * d.ngb + a] = d.dict[a][(i / d.stride[a]) % d.radix[a]];
-    for (int j = 0; j < nudaf; j++) vals[g * nudaf + j] = table[i * nudaf + j];
+    for (int j = 0; j < nudaf; j++)
+      vals[g * nudaf + j] = d.countcoef ? (isnan(d.countcoef[j]) ? table[i * nudaf + j] : d.countcoef[j] * (double)counts[i])
+                                        : table[i * nudaf + j];
     cnts[g] = counts[i];
   }
 }

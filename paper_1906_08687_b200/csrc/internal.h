@@ -115,12 +115,26 @@ cudaError_t launch_root_group(const NodeArgs& a, const GroupArgs& g, const int32
                               const int32_t* ioff, const int32_t* doff, int nudaf, double* table,
                               unsigned long long* counts, cudaStream_t st);
 
+// One group-by query of the fused group-by scan (device-resident array).
+struct GroupDesc {
+  int32_t ngb, nudaf, prog_base;
+  const int32_t* code[8];
+  int32_t code_child[8];
+  int64_t stride[8];
+  double* table;
+  unsigned long long* counts;
+  unsigned char countlike[64];  // UDAF j is a constant c (SUM(c)): derived from the counts
+};
+cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int nq, const int32_t* prog_i,
+                                const double* prog_d, const int32_t* ioff, const int32_t* doff, cudaStream_t st);
+
 // Compaction of a dense cell table: present cells (count > 0) in ascending order.
 struct DecodeArgs {
   int32_t ngb;
   const int32_t* dict[8];
   int64_t radix[8];
   int64_t stride[8];
+  const double* countcoef;  // per UDAF: c if the UDAF is the constant c (value = c * count), NaN otherwise
 };
 cudaError_t launch_compact(const double* table, const unsigned long long* counts, int64_t ncells, int nudaf,
                            const DecodeArgs& d, DevBuf& keys, DevBuf& vals, DevBuf& cnts, int64_t& ngroups,
