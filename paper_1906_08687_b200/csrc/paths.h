@@ -21,4 +21,5 @@ struct FastPaths {
 // Returns nullptr when no specialised path applies (the generic path runs).
 FastPaths* plan_fast_paths(lmfao_ctx* c);
 FastPaths* plan_gram(lmfao_ctx* c);
+FastPaths* plan_cov(lmfao_ctx* c);
 }  // namespace lmfao

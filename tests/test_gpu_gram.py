@@ -46,17 +46,31 @@ CASES = [
 ]
 
 
+FAST = ("cov", "gram")
+
+
+@pytest.fixture(params=["cov", "gram"])
+def kernel(request, monkeypatch):
+    """Run each case through the compile-time-specialised k_cov kernel (cov.cu) and,
+    with LMFAO_NO_COV=1, through the general gram.cu kernel."""
+    if request.param == "gram":
+        monkeypatch.setenv("LMFAO_NO_COV", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("case", range(len(CASES)))
-def test_gram_shapes(case):
+def test_gram_shapes(case, kernel):
     nF, df, dr = CASES[case]
     db, feats = star(case, 30_011 + 7 * case, nF, df, dr)
     batch = [synth.covar_batch(feats)]
     gpu, info = run_gpu(db, batch, info=True)
-    assert info["fast_path"] and info["fast_path"]["kind"] == "gram", info
+    fits_cov = nF <= 8 and max(df) <= 10 and sum(1 for f in df if f) <= 3
+    want = "cov" if kernel == "cov" and fits_cov else "gram"
+    assert info["fast_path"] and info["fast_path"]["kind"] == want, info
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
 
 
-def test_gram_coefficients_sums_and_repeated_factors():
+def test_gram_coefficients_sums_and_repeated_factors(kernel):
     db, feats = star(11, 20_003, 4, [3, 5], [30, 300])
     x0, x1, a, b = "x0", "x1", "d1_0", "d2_4"
     udafs = [
@@ -68,19 +82,19 @@ def test_gram_coefficients_sums_and_repeated_factors():
     ]
     batch = [Query([], udafs), synth.covar_batch(feats[:3])]
     gpu, info = run_gpu(db, batch, info=True)
-    assert info["fast_path"]["kind"] == "gram"
+    assert info["fast_path"]["kind"] == kernel
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
 
 
-def test_gram_uniform_and_extreme_skew():
+def test_gram_uniform_and_extreme_skew(kernel):
     for s in (0.0, 2.5):
         db, feats = star(21, 25_000, 6, [4, 4, 4], [30, 200, 3000], s=s)
         batch = [synth.covar_batch(feats)]
         assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 33, 129, 1001])
-def test_gram_tiny_and_ragged_row_counts(n):
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 33, 129, 511, 512, 513, 1001, 5000])
+def test_gram_tiny_and_ragged_row_counts(n, kernel):
     db, feats = star(31, n, 8, [10, 10, 10], [7, 9, 13])
     batch = [synth.covar_batch(feats)]
     assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
@@ -91,20 +105,20 @@ def test_gram_matches_generic_path(monkeypatch):
     g1, i1 = run_gpu(w.db, w.batch, info=True)
     monkeypatch.setenv("LMFAO_GENERIC_ONLY", "1")
     g2, i2 = run_gpu(w.db, w.batch, info=True)
-    assert i1["fast_path"]["kind"] == "gram" and i2["fast_path"] is None
+    assert i1["fast_path"]["kind"] in FAST and i2["fast_path"] is None
     assert np.array_equal(g1[0][2], g2[0][2])
     assert np.allclose(g1[0][1], g2[0][1], rtol=1e-11, atol=1e-9)
 
 
-def test_config5_covariance_uses_gram_with_cube_generic():
+def test_config5_covariance_uses_gram_with_cube_generic(kernel):
     w = synth.config5(fact_rows=30_011, dim_rows=(40, 300, 2000, 9000), cube_doms=(7, 30, 100))
     gpu, info = run_gpu(w.db, w.batch, info=True)
-    assert info["fast_path"]["kind"] == "gram"
+    assert info["fast_path"]["kind"] == kernel
     assert_parity(gpu, oracle.evaluate(w.db, w.batch), w.batch)
 
 
 @pytest.mark.parametrize("nparts", [2, 5])
-def test_gram_sharded_partials(nparts):
+def test_gram_sharded_partials(nparts, kernel):
     w = synth.config2(fact_rows=40_007, dim_rows=(30, 200, 1500))
     ref = oracle.evaluate(w.db, w.batch)[0]
     parts = [run_gpu(w.db, w.batch, shard=(p, nparts))[0] for p in range(nparts)]
