@@ -13,7 +13,7 @@
 //    features per dimension level (C1, C2, C5's covariance), so the hot loop has
 //    no runtime shape logic (the v12 kernel spent 45 warp-instructions per row);
 //  * every warp runs its own TMA pipeline: `cp.async.bulk` of the fact columns and
-//    keys of a 32-row block into a CS-deep shared-memory ring, and one
+//    keys of a 32-row block into a CF-deep shared-memory ring, and one
 //    `cp.async.bulk.tensor.2d ... tile::gather4` per 4 rows for the view rows
 //    s_L[k_L] (96-byte rows, L2-resident), issued one block ahead — no operand
 //    prefetch lives in registers;
@@ -27,6 +27,7 @@
 // run sums), so any row order is correct; the sort only makes runs long.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <set>
 
 #include "ctx.h"
@@ -34,42 +35,32 @@
 namespace lmfao {
 namespace {
 
-constexpr int CW = 8;        // warps per CTA (one CTA per SM)
-constexpr int CS = 4;        // pipeline stages per warp
-constexpr int CITEM = 512;   // rows per dynamically scheduled item
-constexpr int XSTR = 36;     // doubles per staged x column (32 rows + pad: conflict-free DMMA-layout reads)
-constexpr int GP = 12;       // doubles per view row (gather4 box width; cols >= n are 0)
-constexpr int HT = 2048;     // per-CTA H_L hash slots
-constexpr int PR = 97;       // doubles per pending record (3 x 32 lanes + 1: conflict-free transposed reads)
-constexpr int STG_X = 8 * XSTR * 8;            // 2304 B
-constexpr int STG_K = 3 * 32 * 4;              // 384 B
-constexpr int STG_G = 32 * GP * 8;             // 3072 B
-constexpr int STG = STG_X + STG_K + STG_G;     // 5760 B (45 x 128)
-constexpr int PEND_B = (4 * PR * 8 + 127) / 128 * 128;
-constexpr int WB = CS * STG + PEND_B + 128;    // per-warp shared bytes
-constexpr int SMEM = HT * 8 + CW * WB;
+constexpr int IB = 16;       // 32-row blocks per dynamically scheduled item
+constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
+constexpr int HT = 1024;     // per-CTA H_L hash slots
+constexpr int SBLK = 256 * 8 + 3 * 32 * 4;     // scan-layout bytes per 32-row block: x in DMMA order + 3 key rows
+constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows per block (2 slots)
 constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][10]
 constexpr int BRW = 36;      // doubles per B record
-constexpr int NFIN = 707;    // RB[34][10] | TOT[34] | MB[111] | ML[111] | MA[111]
+constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
 constexpr int FIN_BLOCKS = 148;
 constexpr unsigned FULL = 0xffffffffu;
 
-static_assert(SMEM <= 232448, "shared memory budget");
+static_assert(SBLK % 128 == 0 && STG_G % 128 == 0, "TMA / cp.async alignment");
 
 struct CovArgs {
-  CUtensorMap tmL;  // gather4 map over V_L [nkL x GP] fp64 (first: 64-B aligned)
-  int64_t nrows;
-  const double* x[8];
-  const int32_t* key[3];  // L, A, B dense key columns (A/B null if the level is absent)
-  const double* VA;       // [nkA x GP] (a zero row if absent)
+  int64_t nrows, nblk;
+  const unsigned char* scan;  // [nblk][SBLK] scan layout of the root
+  const double* VL;           // [nkL x GP]
+  const double* VA;           // [nkA x GP] (a zero row if absent)
   unsigned* HL;
   unsigned* HA;
   double* brec;
   int* bcount;
   int bcap;
-  int nx;
   double* partials;  // [grid][NPART]
   int* work;
+  int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -92,13 +83,12 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                "l"(src), "r"(bytes), "r"(sa(b))
                : "memory");
 }
-__device__ __forceinline__ void gather4(void* dst, const CUtensorMap* tm, int r0, int r1, int r2, int r3, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
-      "%5, %6}], [%7];" ::"r"(sa(dst)),
-      "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(sa(b))
-      : "memory");
+// 16-byte L1-allocating async copy; src_bytes = 0 writes zeros (ragged tail rows)
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -111,128 +101,160 @@ __device__ __forceinline__ double red4(double v) {
   return v;
 }
 
-// NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L).
-template <int NS>
-__global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
+// Scan layout of the root (built once at plan time, like the sort at prepare):
+// per 32-row block b, x in the DMMA lane order [group j][lane 4m+k] = x_m[32b+4j+k]
+// (0 for m >= nx or rows >= N), then the dense keys [level][32] of L, A, B.  One
+// contiguous bulk copy per block; conflict-free shared reads.
+struct LayoutArgs {
+  const double* x[8];
+  const int32_t* key[3];
+  int nx, nlev;
+  int64_t N, nblk;
+  unsigned char* out;
+};
+__global__ void k_cov_layout(LayoutArgs a) {
+  const int64_t tot = a.nblk * (SBLK / 8);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / (SBLK / 8);
+    const int o = (int)(i % (SBLK / 8));
+    if (o < 256) {
+      const int j = o >> 5, l = o & 31, m = l >> 2, kk = l & 3;
+      const int64_t row = 32 * b + 4 * j + kk;
+      reinterpret_cast<double*>(a.out)[i] = (m < a.nx && row < a.N) ? a.x[m][row] : 0.0;
+    } else {
+      const int e = 2 * (o - 256), lv = e >> 5, r = e & 31;
+      int2 v = make_int2(0, 0);
+      const int64_t row = 32 * b + r;
+      if (lv < a.nlev) {
+        if (row < a.N) v.x = a.key[lv][row];
+        if (row + 1 < a.N) v.y = a.key[lv][row + 1];
+      }
+      reinterpret_cast<int2*>(a.out)[i] = v;
+    }
+  }
+}
+
+constexpr int COV_W = 16;  // warps per CTA of the scan (one CTA per SM)
+
+template <int W>
+struct CovCfg {
+  static constexpr int CF = W >= 16 ? 3 : (W >= 12 ? 4 : 7);  // fact-block ring slots per warp
+  static constexpr int WB = CF * SBLK + 2 * STG_G + 512;       // + barriers, item ring, segment table
+  static constexpr int SMEM = HT * 8 + W * WB;
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+// NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L); W warps per CTA.
+//
+// Per 32-row block (lane = row for keys; DMMA layout lane = 4m + k for values):
+//  * x⊗x and x⊗s_L on the FP64 tensor pipe (DMMA m8n8k4 per 4-row group), x⊗s_L8/9 by DFMA;
+//  * the open level-A run's sums of v = [x, s_L0..7, (s_L8, s_L9, 1)] are carried per lane (C,
+//    DADD) across blocks in which no run ends (62% of C2's blocks: Zipf-hot keys make long runs);
+//  * in a block where runs end, the run ("segment") sums come from DMMA against a 0/1
+//    segment-indicator operand, D_t[f][s] += Σ_k v_t[f](row k) [seg(row k) = s], in windows of 8
+//    segments; each window's records (partial runs are exact by linearity) are two DMMA passes
+//    against the s_A rows (lane (m,k) holds segments 2k and 2k+1), DFMA for s_A8/9 and n·s_A,
+//    and H_A;
+//  * level-B records (run totals and Σ n·s_A) go to the device record list at B-run ends.
+template <int NS, int W>
+__global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
+  using Cfg = CovCfg<W>;
+  constexpr int CF = Cfg::CF;
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, wib = threadIdx.x >> 5;
   extern __shared__ __align__(1024) unsigned char sm[];
   int* hkey = reinterpret_cast<int*>(sm);
   unsigned* hcnt = reinterpret_cast<unsigned*>(sm + HT * 4);
-  unsigned char* wbase = sm + HT * 8 + wib * WB;
-  double* pend = reinterpret_cast<double*>(wbase + CS * STG);
-  uint64_t* bar_f = reinterpret_cast<uint64_t*>(wbase + CS * STG + PEND_B);
-  uint64_t* bar_g = bar_f + CS;
-  int* ring = reinterpret_cast<int*>(bar_g + CS);  // 8 grabbed item ids
+  unsigned char* wbase = sm + HT * 8 + wib * Cfg::WB;
+  unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
+  uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
+  int* ring = reinterpret_cast<int*>(bar_f + 8);  // 8 grabbed item ids
+  int* segst = ring + 8;                          // [34] segment start rows of the current block
+  int* segkey = segst + 40;                       // [33] their A keys
 
   for (int i = threadIdx.x; i < HT; i += blockDim.x) {
     hkey[i] = -1;
     hcnt[i] = 0;
   }
-  // x columns beyond nx stay zero for the whole kernel
-  for (int s = 0; s < CS; s++) {
-    double* xs = reinterpret_cast<double*>(wbase + s * STG);
-    for (int i = g.nx * XSTR + lane; i < 8 * XSTR; i += 32) xs[i] = 0.0;
-  }
   if (lane == 0) {
-    for (int s = 0; s < CS; s++) {
-      mbar_init(&bar_f[s], 1);
-      mbar_init(&bar_g[s], 1);
-    }
+    for (int s = 0; s < CF; s++) mbar_init(&bar_f[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  const int64_t N = g.nrows;
-  const int nitems = (int)((N + CITEM - 1) / CITEM);
-  auto item_rows = [&](int it) { const int64_t r = N - (int64_t)it * CITEM; return (int)(r < CITEM ? r : CITEM); };
-
-  // per-lane TMA source of the fact block: lanes 0..7 x columns, 8..10 key columns
-  const char* my_src = nullptr;
-  int my_es = 0, my_off = 0;
-  if (lane < 8) {
-    if (lane < g.nx) {
-      my_src = reinterpret_cast<const char*>(g.x[lane]);
-      my_es = 8;
-      my_off = lane * XSTR * 8;
-    }
-  } else if (lane < 8 + 1 + NS) {
-    my_src = reinterpret_cast<const char*>(g.key[lane - 8]);
-    my_es = 4;
-    my_off = STG_X + (lane - 8) * 128;
-  }
+  const int64_t N = g.nrows, NB = g.nblk;
+  const int nitems = (int)((NB + IB - 1) / IB);
 
   // cursors over this warp's block sequence (items grabbed dynamically, in order)
   int nring = 0;
+  int next_item = lane == 0 ? atomicAdd(g.work, 1) : 0;  // one grab in flight ahead of use
   auto grab = [&]() {
-    int it = 0;
-    if (lane == 0) it = atomicAdd(g.work, 1);
-    it = __shfl_sync(FULL, it, 0);
-    if (lane == 0) ring[nring & 7] = it;
-    __syncwarp();
+    const int it = __shfl_sync(FULL, next_item, 0);
+    if (lane == 0) {
+      ring[nring & 7] = it;
+      next_item = atomicAdd(g.work, 1);
+    }
     nring++;
+    __syncwarp();
   };
   struct Cur {
     int slot, b, item;
   };
-  auto item_at = [&](int slot) { return ring[slot & 7]; };
   auto advance = [&](Cur& c, bool may_grab) {
     if (c.item >= nitems) return;
-    if ((c.b + 1) * 32 < item_rows(c.item)) {
+    if (c.b + 1 < IB && (int64_t)c.item * IB + c.b + 1 < NB) {
       c.b++;
     } else {
       c.b = 0;
       c.slot++;
       if (may_grab && c.slot >= nring) grab();
-      c.item = item_at(c.slot);
+      c.item = ring[c.slot & 7];
     }
   };
-  auto block_rows = [&](const Cur& c) { return min(32, item_rows(c.item) - c.b * 32); };
-
+  auto gblock = [&](const Cur& c) { return (int64_t)c.item * IB + c.b; };
   auto issue_fact = [&](const Cur& c, int stage) {
+    __syncwarp();
     if (c.item >= nitems) return;
-    const int nv = block_rows(c);
-    const int64_t row0 = (int64_t)c.item * CITEM + c.b * 32;
-    const uint32_t bx = (uint32_t)((nv * 8 + 15) & ~15), bk = (uint32_t)((nv * 4 + 15) & ~15);
-    unsigned char* st = wbase + stage * STG;
-    __syncwarp();
-    fence_proxy_async();
-    if (lane == 0) mbar_expect(&bar_f[stage], bx * g.nx + bk * (1 + NS));
-    __syncwarp();
-    if (my_src) bulk_load(st + my_off, my_src + row0 * my_es, my_es == 8 ? bx : bk, &bar_f[stage]);
-  };
-  auto issue_gather = [&](const Cur& c, int stage) {
-    if (c.item >= nitems) return;
-    const int nv = block_rows(c);
-    const int ngr = (nv + 3) >> 2;
-    unsigned char* st = wbase + stage * STG;
-    const int* kl = reinterpret_cast<const int*>(st + STG_X);
-    __syncwarp();
-    fence_proxy_async();
-    if (lane == 0) mbar_expect(&bar_g[stage], (uint32_t)ngr * 4 * GP * 8);
-    __syncwarp();
-    if (lane < ngr) {
-      const int4 q = reinterpret_cast<const int4*>(kl)[lane];
-      const int r = 4 * lane;
-      gather4(st + STG_X + STG_K + lane * 4 * GP * 8, &g.tmL, q.x, r + 1 < nv ? q.y : 0, r + 2 < nv ? q.z : 0,
-              r + 3 < nv ? q.w : 0, &bar_g[stage]);
+    if (lane == 0) {  // the slot was only read (generic proxy) since its last fill: no proxy fence needed
+      mbar_expect(&bar_f[stage], SBLK);
+      bulk_load(wbase + stage * SBLK, g.scan + gblock(c) * SBLK, SBLK, &bar_f[stage]);
     }
+  };
+  // view rows s_L[k_L(row)] of a landed fact block -> gather slot [32 rows x 96 B]; 16-byte
+  // chunk c = 32 i + lane (row c / 6) so each instruction writes 512 contiguous bytes
+  int ch_row[6], ch_off[6];
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    const int c = 32 * i + lane;
+    ch_row[i] = c / 6;
+    ch_off[i] = (c % 6) * 16;
+  }
+  auto issue_gather = [&](const Cur& c, int fslot, int gslot) {
+    if (c.item < nitems && !(g.ablate & 1)) {
+      const int* kls = reinterpret_cast<const int*>(wbase + fslot * SBLK + 2048);
+      const int64_t r0 = 32 * gblock(c);
+      const uint32_t dst = sa(gbase + gslot * STG_G) + 16 * lane;
+#pragma unroll
+      for (int i = 0; i < 6; i++) {
+        const bool v = r0 + ch_row[i] < N;
+        const int key = v ? kls[ch_row[i]] : 0;
+        cp16(dst + 512 * i, reinterpret_cast<const char*>(g.VL + (size_t)(unsigned)key * GP) + ch_off[i], v ? 16u : 0u);
+      }
+    }
+    cp_commit();
   };
 
   // ---- accumulators
   double aXX[2] = {0, 0}, aXL[2] = {0, 0}, a8 = 0, a9 = 0;
   double aRA[3][2] = {{0, 0}, {0, 0}, {0, 0}}, r8[3] = {0, 0, 0}, r9[3] = {0, 0, 0};
   double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;
-  double Cx = 0, Cs = 0, Ct = 0;  // this lane's part of the open A run
-  double pbA = 0;
-  double2 pbA89 = make_double2(0, 0);
-  int pkey = 0, pn = 0, npend = 0;
-  bool openA = false, openB = false;
-  int curA = 0, curB = 0, startA = 0;
+  double C0 = 0, C1 = 0, C2 = 0;  // this lane's rows of the open level-A run (since its last fold)
+  bool openB = false;
+  int curB = 0;
   int prevL = -1, prevA = -1, prevB = -1;
-  const int tcol = 8 + min(m, 2);
+  const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
   auto hl_add = [&](int key, unsigned len) {
-    unsigned h = ((unsigned)key * 2654435761u) >> (32 - 11);
+    unsigned h = ((unsigned)key * 2654435761u) >> (32 - 10);
 #pragma unroll 1
     for (int probe = 0; probe < 2; probe++) {
       int t = hkey[h];
@@ -247,50 +269,6 @@ __global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovA
       h = (h + 1) & (HT - 1);
     }
     atomicAdd(&g.HL[key], len);
-  };
-  auto process_A = [&]() {
-    __syncwarp();
-    const bool rv = k < npend;
-    const double* pk = pend + k * PR + 4 * m;
-    double a0 = (pk[0] + pk[1]) + (pk[2] + pk[3]);
-    double a1 = (pk[32] + pk[33]) + (pk[34] + pk[35]);
-    double a2 = (pk[64] + pk[65]) + (pk[66] + pk[67]);
-    const double nk = rv ? (double)pn : 0.0;
-    if (m == 2) a2 = nk;
-    if (!rv) a0 = a1 = a2 = 0.0;
-    const double b0 = rv ? pbA : 0.0, b8 = rv ? pbA89.x : 0.0, b9 = rv ? pbA89.y : 0.0;
-    dmma(aRA[0], a0, b0);
-    dmma(aRA[1], a1, b0);
-    dmma(aRA[2], a2, b0);
-    r8[0] = fma(a0, b8, r8[0]);
-    r8[1] = fma(a1, b8, r8[1]);
-    r8[2] = fma(a2, b8, r8[2]);
-    r9[0] = fma(a0, b9, r9[0]);
-    r9[1] = fma(a1, b9, r9[1]);
-    r9[2] = fma(a2, b9, r9[2]);
-    SB0 += a0;
-    SB1 += a1;
-    SB2 += a2;
-    SBn = fma(nk, b0, SBn);
-    SBn8 = fma(nk, b8, SBn8);
-    SBn9 = fma(nk, b9, SBn9);
-    if (NS >= 1 && rv && m == 0) atomicAdd(&g.HA[pkey], (unsigned)pn);
-    npend = 0;
-    __syncwarp();
-  };
-  auto emit = [&](double rx, double rs, double rt, int n, int keyA) {
-    double* pr = pend + npend * PR + lane;
-    pr[0] = rx;
-    pr[32] = rs;
-    pr[64] = rt;
-    if (k == npend) {
-      pkey = keyA;
-      pn = n;
-      const double* row = g.VA + (size_t)(unsigned)keyA * GP;
-      pbA = row[m];
-      pbA89 = *reinterpret_cast<const double2*>(row + 8);
-    }
-    if (++npend == 4) process_A();
   };
   auto push_B = [&](int keyB) {
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
@@ -314,63 +292,38 @@ __global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovA
     }
     SB0 = SB1 = SB2 = SBn = SBn8 = SBn9 = 0.0;
   };
-  auto flush_item = [&](int irows) {
-    if (openA) emit(Cx, Cs, Ct, irows - startA, curA);
-    if (npend) process_A();
-    if (openB) push_B(curB);
-    openA = openB = false;
-    Cx = Cs = Ct = 0.0;
-    prevL = prevA = prevB = -1;
-  };
 
-  // ---- pipeline prologue
+  // ---- pipeline prologue: fact blocks 0..CF-1 in flight, gathers of block 0
   grab();
-  Cur cc{0, 0, item_at(0)};
+  Cur cc{0, 0, ring[0]};
   Cur cf = cc;
-  for (int s = 0; s < CS; s++) {
+  for (int s = 0; s < CF; s++) {
     issue_fact(cf, s);
     advance(cf, true);
   }
-  if (cc.item < nitems) {
-    mbar_wait(&bar_f[0], 0);
-    issue_gather(cc, 0);
-  }
-  int blk = 0;
-  int cur_item_rows = 0;
-  bool have_item = false;
+  if (cc.item < nitems) mbar_wait(&bar_f[0], 0);
+  issue_gather(cc, 0, 0);
+  int blk = 0, fs = 0, fph = 0;  // fs = blk % CF, fph = (blk / CF) & 1
   while (cc.item < nitems) {
-    const int s = blk % CS;
-    const uint32_t par = (uint32_t)(blk / CS) & 1u;
+    Cur cn = cc;
+    advance(cn, false);
+    const bool has_next = cn.item < nitems;
+    const int fs1 = fs + 1 == CF ? 0 : fs + 1;
     {  // gathers of the next block (its keys have landed)
-      Cur cn = cc;
-      advance(cn, false);
-      if (cn.item < nitems) {
-        const int s1 = (blk + 1) % CS;
-        mbar_wait(&bar_f[s1], (uint32_t)((blk + 1) / CS) & 1u);
-        issue_gather(cn, s1);
-      }
+      const int fph1 = fs + 1 == CF ? fph ^ 1 : fph;
+      if (has_next) mbar_wait(&bar_f[fs1], (uint32_t)fph1);
+      issue_gather(cn, fs1, (blk + 1) & 1);
     }
-    if (cc.b == 0) {
-      if (have_item) flush_item(cur_item_rows);
-      have_item = true;
-      cur_item_rows = item_rows(cc.item);
-    }
-    mbar_wait(&bar_g[s], par);
-    unsigned char* st = wbase + s * STG;
-    double* xs = reinterpret_cast<double*>(st);
-    const int* ks = reinterpret_cast<const int*>(st + STG_X);
-    double* gs = reinterpret_cast<double*>(st + STG_X + STG_K);
-    const int nv = block_rows(cc);
-    const int rowbase = cc.b * 32;
-    if (nv < 32) {  // ragged tail: zero the stale rows of the stage
-      if (lane >= nv) {
-#pragma unroll
-        for (int c = 0; c < 8; c++) xs[c * XSTR + lane] = 0.0;
-#pragma unroll
-        for (int c = 0; c < GP; c++) gs[lane * GP + c] = 0.0;
-      }
-      __syncwarp();
-    }
+    const int64_t gb = gblock(cc);
+    if (cc.b == 0) prevL = prevA = prevB = -1;  // a new item: row 0 starts runs at every level
+    cp_wait1();
+    __syncwarp();
+    const unsigned char* st = wbase + fs * SBLK;
+    const double* xs = reinterpret_cast<const double*>(st);
+    const int* ks = reinterpret_cast<const int*>(st + 2048);
+    const double* gs = reinterpret_cast<const double*>(gbase + (blk & 1) * STG_G);
+    const int64_t rleft = N - gb * 32;
+    const int nv = (int)(rleft < 32 ? rleft : 32);
     const bool vr = lane < nv;
     const int kl = vr ? ks[lane] : -1;
     const int ka = vr ? (NS >= 1 ? ks[32 + lane] : 0) : -1;
@@ -388,67 +341,187 @@ __global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovA
     prevL = __shfl_sync(FULL, kl, nv - 1);
     prevA = __shfl_sync(FULL, ka, nv - 1);
     prevB = __shfl_sync(FULL, kb, nv - 1);
-    if (lead) {
+    // does the run open at this block's end end here? (the next block is another item, or
+    // its row 0 has other A / B keys)
+    bool endA = true, endB = true;
+    if (has_next && cn.b != 0) {
+      const int* kn = reinterpret_cast<const int*>(wbase + fs1 * SBLK + 2048);
+      const int na = NS >= 1 ? kn[32] : 0, nb2 = NS == 2 ? kn[64] : 0;
+      endB = nb2 != prevB;
+      endA = endB || na != prevA;
+    }
+    if (lead && !(g.ablate & 8)) {
       const unsigned above = mLd & ~((2u << lane) - 1u);
       const int end = above ? __ffs(above) - 1 : nv;
       hl_add(kl, (unsigned)(end - lane));
     }
-    const double* xg = xs + m * XSTR + k;
-    const double* gg = gs + k * GP;
-    const int ngr = (nv + 3) >> 2;
-#pragma unroll 2
-    for (int j = 0; j < ngr; j++) {
-      const double xa = xg[4 * j];
-      const double* gr = gg + j * 4 * GP;
-      const double sv = gr[m];
-      const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
-      const double tv = gr[tcol];
-      dmma(aXX, xa, xa);
-      dmma(aXL, xa, sv);
-      a8 = fma(xa, s89.x, a8);
-      a9 = fma(xa, s89.y, a9);
-      unsigned nib = (mA >> (4 * j)) & 15u;
-      if (nib == 0) {
-        Cx += xa;
-        Cs += sv;
-        Ct += tv;
-        continue;
-      }
-      int lo = 0;
-      do {
-        const int q = __ffs(nib) - 1;
-        nib &= nib - 1;
-        const int p = 4 * j + q;
-        if (openA) {
-          const bool in = k >= lo && k < q;
-          emit(Cx + (in ? xa : 0.0), Cs + (in ? sv : 0.0), Ct + (in ? tv : 0.0), rowbase + p - startA, curA);
-        }
-        Cx = Cs = Ct = 0.0;
-        if ((mB >> p) & 1u) {
-          if (openB) {
-            if (npend) process_A();
-            push_B(curB);
-          }
-          openB = true;
-          curB = __shfl_sync(FULL, kb, p);
-        }
-        openA = true;
-        curA = __shfl_sync(FULL, ka, p);
-        startA = rowbase + p;
-        lo = q;
-      } while (nib);
-      const bool in = k >= lo;
-      Cx = in ? xa : 0.0;
-      Cs = in ? sv : 0.0;
-      Ct = in ? tv : 0.0;
+    if (mB & 1u) {  // a level-B run starts at row 0
+      openB = true;
+      curB = __shfl_sync(FULL, kb, 0);
     }
-    __syncwarp();
-    issue_fact(cf, s);  // the slot just consumed takes the block CS ahead
+    const unsigned mAx = mA & ~1u;  // run starts inside the block (row 0 always opens segment 0)
+    const double* gl = gs + k * GP;
+    if (mAx == 0 && !endA) {
+      // fast path: the open run continues through the block
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const double xa = xs[32 * j + lane];
+        const double* gr = gl + j * 4 * GP;
+        const double sv = gr[m];
+        const double tv = gr[tcol];
+        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
+        dmma(aXX, xa, xa);
+        dmma(aXL, xa, sv);
+        a8 = fma(xa, s89.x, a8);
+        a9 = fma(xa, s89.y, a9);
+        C0 += xa;
+        C1 += sv;
+        C2 += tv;
+      }
+    } else {
+      // segments of the block: segment 0 starts at row 0, segment s >= 1 at the s-th run start
+      const int R = __popc(mAx);
+      {
+        const int sr = __popc(mAx & ((2u << lane) - 1u));
+        if (lane == 0 || ((mAx >> lane) & 1u)) {
+          segst[sr] = lane;
+          segkey[sr] = ka;
+        }
+        if (lane == 0) segst[R + 1] = nv;
+        __syncwarp();
+      }
+      int sb = 0;  // first segment of the current window of 8
+      double D[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+      // this lane's record slots: segments s0 = sb + 2k (pass 0) and s0 + 1 (pass 1)
+      int key0 = 0, key1 = 0;
+      double b0 = 0, b1 = 0;
+      double2 b089 = make_double2(0, 0), b189 = make_double2(0, 0);
+      auto load_window = [&]() {  // keys and s_A rows of the window's segments
+        const int s0 = sb + 2 * k, s1 = s0 + 1;
+        const bool v0 = s0 <= R, v1 = s1 <= R;
+        key0 = v0 ? segkey[s0] : 0;
+        key1 = v1 ? segkey[s1] : 0;
+        const double* row0 = g.VA + (size_t)(unsigned)key0 * GP;
+        const double* row1 = g.VA + (size_t)(unsigned)key1 * GP;
+        b0 = v0 ? row0[m] : 0.0;
+        b1 = v1 ? row1[m] : 0.0;
+        b089 = v0 ? *reinterpret_cast<const double2*>(row0 + 8) : make_double2(0, 0);
+        b189 = v1 ? *reinterpret_cast<const double2*>(row1 + 8) : make_double2(0, 0);
+      };
+      // the window's (partial) level-A records ⊗ s_A, and level B; segments before s_end are
+      // complete here (s_end itself may continue into the next window)
+      auto flush_window = [&](int s_end) {
+        const int s0 = sb + 2 * k, s1 = s0 + 1;
+        // row counts of the slots (incl. rows carried from earlier blocks) = the t tile's "1" row
+        const double n0 = __shfl_sync(FULL, D[2][0], 8 + k), n1 = __shfl_sync(FULL, D[2][1], 8 + k);
+        if (!(g.ablate & 2)) {
+#pragma unroll
+          for (int t = 0; t < 3; t++) {
+            dmma(aRA[t], D[t][0], b0);
+            dmma(aRA[t], D[t][1], b1);
+            r8[t] = fma(D[t][0], b089.x, fma(D[t][1], b189.x, r8[t]));
+            r9[t] = fma(D[t][0], b089.y, fma(D[t][1], b189.y, r9[t]));
+          }
+          if (NS >= 1 && m == 0) {
+            if (n0 > 0.0) atomicAdd(&g.HA[key0], (unsigned)n0);
+            if (n1 > 0.0) atomicAdd(&g.HA[key1], (unsigned)n1);
+          }
+        }
+        auto add_segs = [&](int lo, int hi) {  // segments [lo, hi) of the window -> the open B run
+          const bool u0 = s0 >= lo && s0 < hi, u1 = s1 >= lo && s1 < hi;
+          const double d0 = u0 ? 1.0 : 0.0, d1 = u1 ? 1.0 : 0.0;
+          SB0 = fma(d0, D[0][0], fma(d1, D[0][1], SB0));
+          SB1 = fma(d0, D[1][0], fma(d1, D[1][1], SB1));
+          SB2 = fma(d0, D[2][0], fma(d1, D[2][1], SB2));
+          const double w0 = u0 ? n0 : 0.0, w1 = u1 ? n1 : 0.0;
+          SBn = fma(w0, b0, fma(w1, b1, SBn));
+          SBn8 = fma(w0, b089.x, fma(w1, b189.x, SBn8));
+          SBn9 = fma(w0, b089.y, fma(w1, b189.y, SBn9));
+        };
+        int lo = sb;
+        unsigned bb = mB & ~1u;
+        while (bb) {  // level-B run starts inside the block (rare)
+          const int p = __ffs(bb) - 1;
+          bb &= bb - 1;
+          const int sp = __popc(mAx & ((2u << p) - 1u));
+          if (sp <= sb || sp > s_end) continue;  // handled by the window that completes segment sp - 1
+          add_segs(lo, sp);
+          push_B(curB);
+          curB = __shfl_sync(FULL, kb, p);
+          lo = sp;
+        }
+        add_segs(lo, sb + 8);
+#pragma unroll
+        for (int t = 0; t < 3; t++) D[t][0] = D[t][1] = 0.0;
+      };
+      load_window();
+      {  // the carried part of segment 0 (rows of earlier blocks) -> slot 0
+        const double f0 = red4(C0), f1 = red4(C1), f2 = red4(C2);
+        if (k == 0) {
+          D[0][0] = f0;
+          D[1][0] = f1;
+          D[2][0] = f2;
+        }
+        C0 = C1 = C2 = 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        const double xa = xs[32 * j + lane];
+        const double* gr = gl + j * 4 * GP;
+        const double sv = gr[m];
+        const double tv = gr[tcol];
+        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
+        dmma(aXX, xa, xa);
+        dmma(aXL, xa, sv);
+        a8 = fma(xa, s89.x, a8);
+        a9 = fma(xa, s89.y, a9);
+        const int slast = __popc(mAx & ((2u << (4 * j + 3)) - 1u));
+        if (slast - sb >= 8) {  // the group reaches past the window: flush it, restart at the group's first segment
+          const int s4j = __popc(mAx & ((2u << (4 * j)) - 1u));
+          flush_window(s4j);
+          sb = s4j;
+          load_window();
+        }
+        const int sr = __popc(mAx & ((2u << (4 * j + k)) - 1u));
+        const double ind = (sr - sb == m) ? 1.0 : 0.0;
+        dmma(D[0], xa, ind);
+        dmma(D[1], sv, ind);
+        dmma(D[2], tv, ind);
+      }
+      if (endA) {
+        flush_window(64);
+      } else {  // the last segment continues into the next block: keep it open (carried in C)
+        const int sl = R - sb;  // its slot
+        {
+          // take it out of D before the flush: its value moves to lane (m, 0) of C
+          double e0 = 0, e1 = 0, e2 = 0;
+          if (k == (sl >> 1)) {
+            e0 = (sl & 1) ? D[0][1] : D[0][0];
+            e1 = (sl & 1) ? D[1][1] : D[1][0];
+            e2 = (sl & 1) ? D[2][1] : D[2][0];
+            if (sl & 1) D[0][1] = D[1][1] = D[2][1] = 0.0;
+            else D[0][0] = D[1][0] = D[2][0] = 0.0;
+          }
+          C0 = __shfl_sync(FULL, e0, 4 * m + (sl >> 1));
+          C1 = __shfl_sync(FULL, e1, 4 * m + (sl >> 1));
+          C2 = __shfl_sync(FULL, e2, 4 * m + (sl >> 1));
+          if (k != 0) C0 = C1 = C2 = 0.0;
+        }
+        flush_window(64);
+      }
+    }
+    if (endB && openB) {  // the level-B run ends with this block
+      push_B(curB);
+      openB = false;
+    }
+    issue_fact(cf, fs);  // the slot just consumed takes the block CF ahead
     advance(cf, true);
-    advance(cc, false);
+    cc = cn;
     blk++;
+    fs = fs1;
+    if (fs == 0) fph ^= 1;
   }
-  if (have_item) flush_item(cur_item_rows);
+  asm volatile("cp.async.wait_all;" ::: "memory");
 
   // ---- H_L table -> global
   __syncthreads();
@@ -468,7 +541,7 @@ __global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovA
   __syncthreads();
   for (int i = threadIdx.x; i < NPART; i += blockDim.x) red[i] = 0.0;
   __syncthreads();
-  for (int w = 0; w < CW; w++) {
+  for (int w = 0; w < W; w++) {
     if (wib == w) {
       red[m * 8 + 2 * k] += aXX[0];
       red[m * 8 + 2 * k + 1] += aXX[1];
@@ -493,7 +566,8 @@ __global__ void __launch_bounds__(CW * 32, 1) k_cov(const __grid_constant__ CovA
   for (int i = threadIdx.x; i < NPART; i += blockDim.x) g.partials[(size_t)blockIdx.x * NPART + i] = red[i];
 }
 
-// V[k][f] = col_f[k] for f < n, 0 for n <= f < GP (primary-key leaf: row k has dense key k).
+// V[k][f] = col_f[k] for f < n, 0 for n <= f < GP, except V[k][10] = 1 (the constant of the
+// scan's t tile; primary-key leaf: row k has dense key k).
 struct DimTables {
   const double* const* cols[3];
   int n[3];
@@ -516,13 +590,15 @@ __global__ void k_cov_dims(DimTables d) {
     }
     const int64_t kk = e / GP;
     const int f = (int)(e % GP);
-    d.V[l][e] = f < d.n[l] ? d.cols[l][f][kk] : 0.0;
+    d.V[l][e] = f < d.n[l] ? d.cols[l][f][kk] : (f == 10 ? 1.0 : 0.0);
   }
 }
 
-// Off-scan finishing, per block b of FIN_BLOCKS: B records in its range (R_B⊗s_B,
-// Σ R_B, B moments weighted by the record counts) and the L / A moments over its
-// key ranges weighted by H_L / H_A.  Output: partials [FIN_BLOCKS][NFIN].
+// Off-scan finishing with DMMA tiles (4 keys / records per m8n8k4), per warp over
+// contiguous ranges of: the L keys (weights H_L), the A keys (H_A), the B records
+// (R_B ⊗ [s_B, 1] and the B moments weighted by the record counts).  With
+// s' = [s_0..s_9, 1] (index 10 = the constant), a level's moments are the 16x16
+// matrix Σ_k w_k s'(k) s'(k)^T; the records give RBM[40][16] = Σ_rec rec ⊗ s'_B.
 struct FinArgs {
   const double* brec;
   const int* bcount;
@@ -534,62 +610,80 @@ struct FinArgs {
   const unsigned* HA;
   const double* VA;
   int64_t nkA;
-  double* partials;
+  double* partials;  // [grid][NFIN]
 };
-__device__ __forceinline__ void moment_ij(int o, int& f, int& g2) {
-  f = g2 = -1;
-  if (o >= 1 && o <= 10) f = o - 1;
-  if (o > 10) {
-    f = (o - 11) / 10;
-    g2 = (o - 11) % 10;
+__global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
+  const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + w, GW = (int64_t)gridDim.x * 8;
+  double mL[4][2] = {}, mA[4][2] = {}, mB[4][2] = {}, rb[5][2][2] = {};
+  auto srow = [&](const double* V, int64_t kk, bool v, double& s0, double& s1) {
+    const double* row = V + (size_t)kk * GP;
+    s0 = v ? row[m] : 0.0;
+    s1 = v ? (m < 2 ? row[8 + m] : (m == 2 ? 1.0 : 0.0)) : 0.0;
+  };
+  auto moments = [&](const unsigned* H, const double* V, int64_t nk, double (&acc)[4][2]) {
+    const int64_t ng = (nk + 3) / 4, g0 = gw * ng / GW, g1 = (gw + 1) * ng / GW;
+    for (int64_t gi = g0; gi < g1; gi++) {
+      const int64_t kk = gi * 4 + k;
+      const bool v = kk < nk;
+      const double h = v ? (double)H[kk] : 0.0;
+      double s0, s1;
+      srow(V, v ? kk : 0, v, s0, s1);
+      dmma(acc[0], h * s0, s0);
+      dmma(acc[1], h * s0, s1);
+      dmma(acc[2], h * s1, s0);
+      dmma(acc[3], h * s1, s1);
+    }
+  };
+  moments(a.HL, a.VL, a.nkL, mL);
+  moments(a.HA, a.VA, a.nkA, mA);
+  {
+    const int64_t nrec = min(*a.bcount, a.bcap);
+    const int64_t ng = (nrec + 3) / 4, g0 = gw * ng / GW, g1 = (gw + 1) * ng / GW;
+    for (int64_t gi = g0; gi < g1; gi++) {
+      const int64_t r = gi * 4 + k;
+      const bool v = r < nrec;
+      const double* rec = a.brec + (size_t)(v ? r : 0) * BRW;
+      const double n = v ? rec[18] : 0.0;
+      double s0, s1;
+      srow(a.VB, v ? (int64_t)(int)rec[34] : 0, v, s0, s1);
+#pragma unroll
+      for (int t = 0; t < 5; t++) {
+        const double av = (v && 8 * t + m < 34) ? rec[8 * t + m] : 0.0;
+        dmma(rb[t][0], av, s0);
+        dmma(rb[t][1], av, s1);
+      }
+      dmma(mB[0], n * s0, s0);
+      dmma(mB[1], n * s0, s1);
+      dmma(mB[2], n * s1, s0);
+      dmma(mB[3], n * s1, s1);
+    }
   }
-}
-__global__ void k_cov_fin(FinArgs a) {
-  const int b = blockIdx.x, P = gridDim.x;
-  const int nrec = min(*a.bcount, a.bcap);
-  const int r0 = (int)((int64_t)nrec * b / P), r1 = (int)((int64_t)nrec * (b + 1) / P);
-  const int64_t l0 = a.nkL * b / P, l1 = a.nkL * (b + 1) / P;
-  const int64_t q0 = a.nkA * b / P, q1 = a.nkA * (b + 1) / P;
-  for (int o = threadIdx.x; o < NFIN; o += blockDim.x) {
-    double s = 0.0;
-    if (o < 340) {
-      const int r = o / 10, c = o % 10;
-      for (int i = r0; i < r1; i++) {
-        const double* rec = a.brec + (size_t)i * BRW;
-        s = fma(rec[r], a.VB[(size_t)(unsigned)(int)rec[34] * GP + c], s);
+  __shared__ double red[NFIN];
+  for (int i = threadIdx.x; i < NFIN; i += blockDim.x) red[i] = 0.0;
+  __syncthreads();
+  auto put = [&](int base, int t1, int t2, const double (&c)[2]) {
+    const int i = base + (8 * t1 + m) * 16 + 8 * t2 + 2 * k;
+    red[i] += c[0];
+    red[i + 1] += c[1];
+  };
+  for (int ww = 0; ww < 8; ww++) {
+    if (w == ww) {
+#pragma unroll
+      for (int t = 0; t < 5; t++) {
+        put(0, t, 0, rb[t][0]);
+        put(0, t, 1, rb[t][1]);
       }
-    } else if (o < 374) {
-      const int r = o - 340;
-      for (int i = r0; i < r1; i++) s += a.brec[(size_t)i * BRW + r];
-    } else if (o < 485) {
-      int f, g2;
-      moment_ij(o - 374, f, g2);
-      for (int i = r0; i < r1; i++) {
-        const double* rec = a.brec + (size_t)i * BRW;
-        const double* v = a.VB + (size_t)(unsigned)(int)rec[34] * GP;
-        double t = rec[18];
-        if (f >= 0) t *= v[f];
-        if (g2 >= 0) t *= v[g2];
-        s += t;
-      }
-    } else {
-      const bool isL = o < 596;
-      int f, g2;
-      moment_ij(o - (isL ? 485 : 596), f, g2);
-      const unsigned* H = isL ? a.HL : a.HA;
-      const double* V = isL ? a.VL : a.VA;
-      const int64_t k0 = isL ? l0 : q0, k1 = isL ? l1 : q1;
-      for (int64_t kk = k0; kk < k1; kk++) {
-        const unsigned h = H[kk];
-        if (!h) continue;
-        double t = (double)h;
-        if (f >= 0) t *= V[kk * GP + f];
-        if (g2 >= 0) t *= V[kk * GP + g2];
-        s += t;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        put(640, q >> 1, q & 1, mL[q]);
+        put(896, q >> 1, q & 1, mA[q]);
+        put(1152, q >> 1, q & 1, mB[q]);
       }
     }
-    a.partials[(size_t)b * NFIN + o] = s;
+    __syncthreads();
   }
+  for (int i = threadIdx.x; i < NFIN; i += blockDim.x) a.partials[(size_t)blockIdx.x * NFIN + i] = red[i];
 }
 
 // src[0:NPART] = Σ_cta scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials (fixed order)
@@ -634,8 +728,9 @@ struct FastCov : FastPaths {
   DevBuf zbuf;   // [work | bcount | pad] [HA] [HL], cleared every run
   size_t off_HA = 0, off_HL = 0, zbytes = 0;
   DevBuf brec, partials, finp, src, toff, tidx, tcoef;
+  DevBuf scan;  // scan layout of the root (k_cov_layout), built at plan time
+  int64_t nblk = 0;
   int bcap = 0, grid = 148, nout = 0;
-  CUtensorMap tmL;
   bool only_scalar = true;
 
   std::string describe() const override {
@@ -643,26 +738,36 @@ struct FastCov : FastPaths {
     std::snprintf(b, sizeof b,
                   "{\"kind\": \"cov\", \"NS\": %d, \"nF\": %d, \"nL\": %zu, \"nA\": %zu, \"nB\": %zu, \"grid\": %d, "
                   "\"threads\": %d, \"stages\": %d, \"item\": %d}",
-                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, CW * 32, CS, CITEM);
+                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, COV_W * 32, CovCfg<COV_W>::CF, 32 * IB);
     return b;
   }
   bool skip_generic_views() const override { return only_scalar; }
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
 };
 
-cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
+int cov_warps() {  // LMFAO_COV_W (diagnostics): 12 or 16 warps per CTA
+  const char* e = std::getenv("LMFAO_COV_W");
+  return e && std::atoi(e) == 12 ? 12 : COV_W;
+}
+
+template <int W>
+cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
   static bool attr[3] = {false, false, false};
   auto go = [&](auto kern) -> cudaError_t {
+    constexpr int smem = CovCfg<W>::SMEM;
     if (!attr[NS]) {
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       attr[NS] = true;
     }
-    kern<<<grid, CW * 32, SMEM, st>>>(g);
+    kern<<<grid, W * 32, smem, st>>>(g);
     return cudaGetLastError();
   };
-  if (NS == 0) return go(k_cov<0>);
-  if (NS == 1) return go(k_cov<1>);
-  return go(k_cov<2>);
+  if (NS == 0) return go(k_cov<0, W>);
+  if (NS == 1) return go(k_cov<1, W>);
+  return go(k_cov<2, W>);
+}
+cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
+  return cov_warps() == 12 ? launch_cov_w<12>(NS, g, grid, st) : launch_cov_w<16>(NS, g, grid, st);
 }
 
 }  // namespace
@@ -687,19 +792,20 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
     }
   }
   CovArgs g{};
-  g.tmL = tmL;
   g.nrows = R.nrows;
-  g.nx = nF;
-  for (int i = 0; i < 8; i++) g.x[i] = i < nF ? (const double*)R.cols[R.find_attr(fattrs[i])].buf.p : nullptr;
-  g.key[0] = R.fk_dense[L.child].as<int32_t>();
-  g.key[1] = NS >= 1 ? R.fk_dense[A.child].as<int32_t>() : nullptr;
-  g.key[2] = NS == 2 ? R.fk_dense[B.child].as<int32_t>() : nullptr;
+  g.nblk = nblk;
+  g.scan = scan.as<unsigned char>();
+  g.VL = L.V.as<double>();
   g.VA = NS >= 1 ? A.V.as<double>() : zeros.as<double>();
   char* z = zbuf.as<char>();
   g.work = reinterpret_cast<int*>(z);
   g.bcount = reinterpret_cast<int*>(z + 4);
   g.HA = reinterpret_cast<unsigned*>(z + off_HA);
   g.HL = reinterpret_cast<unsigned*>(z + off_HL);
+  {
+    const char* ab = std::getenv("LMFAO_COV_ABLATE");
+    g.ablate = ab ? std::atoi(ab) : 0;
+  }
   g.brec = brec.as<double>();
   g.bcap = bcap;
   g.partials = partials.as<double>();
@@ -725,7 +831,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
                                                          src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                          tcoef.as<double>(), nout, c->scalar_out.as<double>(),
-                                                         NPART + 340 + 18, c->scalar_count.as<unsigned long long>());
+                                                         NPART + 18 * 16 + 10, c->scalar_count.as<unsigned long long>());
   launches_add(3);
   scalar_done = true;
   return cudaGetLastError();
@@ -823,34 +929,29 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   fc->off_HL = (fc->off_HA + (size_t)nkA * 4 + 15) / 16 * 16;
   fc->zbytes = fc->off_HL + (size_t)std::max<int64_t>(fc->L.nk, 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
-  const int64_t nitems = (R.nrows + CITEM - 1) / CITEM;
+  fc->nblk = (R.nrows + 31) / 32;
+  const int64_t nitems = (fc->nblk + IB - 1) / IB;
   fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + 2 * nitems + 64, INT32_MAX / BRW);
   if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
   if (fc->partials.alloc((size_t)fc->grid * NPART * 8)) return nullptr;
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
   if (fc->src.alloc((size_t)(NPART + NFIN) * 8)) return nullptr;
-  {  // gather4 tensor map over V_L [nk x GP] fp64, box GP x 1
-    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = nullptr;
-    if (!encode) {
-      cudaDriverEntryPointQueryResult q;
-      void* fn = nullptr;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-          q != cudaDriverEntryPointSuccess || !fn)
-        return nullptr;
-      encode = (EncodeFn)fn;
+  {  // scan layout of the root: x in DMMA lane order + dense keys, one 2432-byte block per 32 rows
+    if (fc->scan.alloc((size_t)std::max<int64_t>(fc->nblk, 1) * SBLK)) return nullptr;
+    LayoutArgs la{};
+    for (int i = 0; i < 8; i++) la.x[i] = i < fc->nF ? (const double*)R.cols[R.find_attr(fc->fattrs[i])].buf.p : nullptr;
+    la.key[0] = R.fk_dense[fc->L.child].as<int32_t>();
+    la.key[1] = fc->NS >= 1 ? R.fk_dense[fc->A.child].as<int32_t>() : nullptr;
+    la.key[2] = fc->NS == 2 ? R.fk_dense[fc->B.child].as<int32_t>() : nullptr;
+    la.nx = fc->nF;
+    la.nlev = 1 + fc->NS;
+    la.N = R.nrows;
+    la.nblk = fc->nblk;
+    la.out = fc->scan.as<unsigned char>();
+    if (fc->nblk > 0) {
+      k_cov_layout<<<148 * 8, 256, 0, c->stream>>>(la);
+      if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return nullptr;
     }
-    std::memset(&fc->tmL, 0, sizeof(fc->tmL));
-    cuuint64_t dims[2] = {(cuuint64_t)GP, (cuuint64_t)std::max<int64_t>(fc->L.nk, 1)};
-    cuuint64_t strides[1] = {(cuuint64_t)GP * 8};
-    cuuint32_t box[2] = {(cuuint32_t)GP, 1};
-    cuuint32_t estr[2] = {1, 1};
-    if (encode(&fc->tmL, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, fc->L.V.p, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return nullptr;
   }
   // source index of G[a][b] (a, b: attr id or -1 = "1"); see the layout above k_cov_sum
   auto fidx = [](const std::vector<int>& v, int a) {
@@ -858,7 +959,10 @@ FastPaths* plan_cov(lmfao_ctx* c) {
       if (v[i] == a) return (int)i;
     return -1;
   };
-  const int F0 = NPART, RB = F0, TOT = F0 + 340, MB = F0 + 374, ML = F0 + 485, MA = F0 + 596;
+  // fin layout (k_cov_fin): RBM[40][16] (rec row r x [s_B(0..9), 1 at col 10]), then 16x16 moment
+  // matrices of L, A, B over s' = [s_0..s_9, 1]
+  const int F0 = NPART, RBM = F0, MLM = F0 + 640, MAM = F0 + 896, MBM = F0 + 1152;
+  auto TOT = [&](int r) { return RBM + r * 16 + 10; };
   auto lvl = [&](int x) -> int {  // 0 = "1", 1 = fact, 2 = L, 3 = A, 4 = B
     if (x < 0) return 0;
     if (fidx(fc->fattrs, x) >= 0) return 1;
@@ -883,21 +987,21 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     }
     const int i = pos(a, la), j = pos(b, lb);
     switch (la * 5 + lb) {
-      case 0: return TOT + 18;                 // 1·1 = count
-      case 1: return TOT + j;                  // 1·x
-      case 2: return TOT + 8 + j;              // 1·s_L
-      case 3: return TOT + 24 + j;             // 1·s_A
-      case 4: return MB + 1 + j;               // 1·s_B
+      case 0: return TOT(18);                  // 1·1 = count
+      case 1: return TOT(j);                   // 1·x
+      case 2: return TOT(8 + j);               // 1·s_L
+      case 3: return TOT(24 + j);              // 1·s_A
+      case 4: return MBM + j * 16 + 10;        // 1·s_B
       case 6: return i * 8 + j;                // x·x
       case 7: return 64 + i * 10 + j;          // x·s_L
       case 8: return 144 + i * 10 + j;         // x·s_A
-      case 9: return RB + i * 10 + j;          // x·s_B
-      case 12: return ML + 11 + i * 10 + j;    // s_L·s_L
+      case 9: return RBM + i * 16 + j;         // x·s_B
+      case 12: return MLM + i * 16 + j;        // s_L·s_L
       case 13: return 144 + (8 + i) * 10 + j;  // s_L·s_A
-      case 14: return RB + (8 + i) * 10 + j;   // s_L·s_B
-      case 18: return MA + 11 + i * 10 + j;    // s_A·s_A
-      case 19: return RB + (24 + i) * 10 + j;  // s_A·s_B
-      case 24: return MB + 11 + i * 10 + j;    // s_B·s_B
+      case 14: return RBM + (8 + i) * 16 + j;  // s_L·s_B
+      case 18: return MAM + i * 16 + j;        // s_A·s_A
+      case 19: return RBM + (24 + i) * 16 + j; // s_A·s_B
+      case 24: return MBM + i * 16 + j;        // s_B·s_B
     }
     return -1;
   };
