@@ -60,7 +60,8 @@ struct CovArgs {
   int bcap;
   double* partials;  // [grid][NPART]
   int* work;
-  int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L
+  int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L,
+               // 16 no compute at all (pipeline only), 32 every block on the fast path
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -140,7 +141,7 @@ template <int W>
 struct CovCfg {
   static constexpr int CF = W >= 16 ? 3 : (W >= 12 ? 4 : 7);  // fact-block ring slots per warp
   static constexpr int WB = CF * SBLK + 2 * STG_G + 512;       // + barriers, item ring, segment table
-  static constexpr int SMEM = HT * 8 + W * WB;
+  static constexpr int SMEM = 128 + HT * 8 + W * WB;  // [CTA counters | H_L table | warps]
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -162,9 +163,10 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   constexpr int CF = Cfg::CF;
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, wib = threadIdx.x >> 5;
   extern __shared__ __align__(1024) unsigned char sm[];
-  int* hkey = reinterpret_cast<int*>(sm);
-  unsigned* hcnt = reinterpret_cast<unsigned*>(sm + HT * 4);
-  unsigned char* wbase = sm + HT * 8 + wib * Cfg::WB;
+  int* cta_done = reinterpret_cast<int*>(sm);
+  int* hkey = reinterpret_cast<int*>(sm + 128);
+  unsigned* hcnt = reinterpret_cast<unsigned*>(sm + 128 + HT * 4);
+  unsigned char* wbase = sm + 128 + HT * 8 + wib * Cfg::WB;
   unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
   uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
   int* ring = reinterpret_cast<int*>(bar_f + 8);  // 8 grabbed item ids
@@ -175,14 +177,24 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     hkey[i] = -1;
     hcnt[i] = 0;
   }
+  if (threadIdx.x == 0) *cta_done = 0;
   if (lane == 0) {
     for (int s = 0; s < CF; s++) mbar_init(&bar_f[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
+  // work items: blocks [0, NB) in items of IB blocks, the last ~10% in items of 2 blocks (a
+  // short tail for the dynamic schedule)
   const int64_t N = g.nrows, NB = g.nblk;
-  const int nitems = (int)((NB + IB - 1) / IB);
+  const int nbig = (int)(NB * 9 / 10 / IB);
+  const int nitems = nbig + (int)((NB - (int64_t)nbig * IB + 1) / 2);
+  auto item_first = [&](int it) { return it < nbig ? (int64_t)it * IB : (int64_t)nbig * IB + 2 * (int64_t)(it - nbig); };
+  auto item_blocks = [&](int it) {
+    const int64_t f = item_first(it), r = NB - f;
+    const int64_t cap = it < nbig ? IB : 2;
+    return (int)(r < cap ? r : cap);
+  };
 
   // cursors over this warp's block sequence (items grabbed dynamically, in order)
   int nring = 0;
@@ -197,20 +209,28 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     __syncwarp();
   };
   struct Cur {
-    int slot, b, item;
+    int slot, b, item, nb;  // nb: blocks of the item
+    int64_t gb0;            // its first block
+    int rows;               // rows of the item
+  };
+  auto set_item = [&](Cur& c) {
+    c.item = ring[c.slot & 7];
+    if (c.item < nitems) {
+      c.gb0 = item_first(c.item);
+      c.nb = item_blocks(c.item);
+      const int64_t r = N - c.gb0 * 32;
+      c.rows = (int)(r < 32 * c.nb ? r : 32 * c.nb);
+    }
   };
   auto advance = [&](Cur& c, bool may_grab) {
     if (c.item >= nitems) return;
-    if (c.b + 1 < IB && (int64_t)c.item * IB + c.b + 1 < NB) {
-      c.b++;
-    } else {
-      c.b = 0;
-      c.slot++;
-      if (may_grab && c.slot >= nring) grab();
-      c.item = ring[c.slot & 7];
-    }
+    if (++c.b < c.nb) return;
+    c.b = 0;
+    c.slot++;
+    if (may_grab && c.slot >= nring) grab();
+    set_item(c);
   };
-  auto gblock = [&](const Cur& c) { return (int64_t)c.item * IB + c.b; };
+  auto gblock = [&](const Cur& c) { return c.gb0 + c.b; };
   auto issue_fact = [&](const Cur& c, int stage) {
     __syncwarp();
     if (c.item >= nitems) return;
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     }
   };
   // view rows s_L[k_L(row)] of a landed fact block -> gather slot [32 rows x 96 B]; 16-byte
-  // chunk c = 32 i + lane (row c / 6) so each instruction writes 512 contiguous bytes
+  // chunk c = 32 i + lane (row c / 6), so each instruction covers ~5 whole rows (coalesced)
   int ch_row[6], ch_off[6];
 #pragma unroll
   for (int i = 0; i < 6; i++) {
@@ -231,13 +251,14 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   auto issue_gather = [&](const Cur& c, int fslot, int gslot) {
     if (c.item < nitems && !(g.ablate & 1)) {
       const int* kls = reinterpret_cast<const int*>(wbase + fslot * SBLK + 2048);
-      const int64_t r0 = 32 * gblock(c);
+      const int left = c.rows - c.b * 32;
+      const char* vl = reinterpret_cast<const char*>(g.VL);
       const uint32_t dst = sa(gbase + gslot * STG_G) + 16 * lane;
 #pragma unroll
       for (int i = 0; i < 6; i++) {
-        const bool v = r0 + ch_row[i] < N;
-        const int key = v ? kls[ch_row[i]] : 0;
-        cp16(dst + 512 * i, reinterpret_cast<const char*>(g.VL + (size_t)(unsigned)key * GP) + ch_off[i], v ? 16u : 0u);
+        const bool v = ch_row[i] < left;
+        const unsigned off = (unsigned)kls[ch_row[i]] * (unsigned)(GP * 8) + (unsigned)ch_off[i];
+        cp16(dst + 512 * i, vl + (v ? off : 0u), v ? 16u : 0u);
       }
     }
     cp_commit();
@@ -295,7 +316,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
 
   // ---- pipeline prologue: fact blocks 0..CF-1 in flight, gathers of block 0
   grab();
-  Cur cc{0, 0, ring[0]};
+  Cur cc{0, 0, 0, 0, 0, 0};
+  set_item(cc);
   Cur cf = cc;
   for (int s = 0; s < CF; s++) {
     issue_fact(cf, s);
@@ -314,16 +336,24 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       if (has_next) mbar_wait(&bar_f[fs1], (uint32_t)fph1);
       issue_gather(cn, fs1, (blk + 1) & 1);
     }
-    const int64_t gb = gblock(cc);
     if (cc.b == 0) prevL = prevA = prevB = -1;  // a new item: row 0 starts runs at every level
     cp_wait1();
     __syncwarp();
+    if (g.ablate & 16) {
+      issue_fact(cf, fs);
+      advance(cf, true);
+      cc = cn;
+      blk++;
+      fs = fs1;
+      if (fs == 0) fph ^= 1;
+      continue;
+    }
     const unsigned char* st = wbase + fs * SBLK;
     const double* xs = reinterpret_cast<const double*>(st);
     const int* ks = reinterpret_cast<const int*>(st + 2048);
     const double* gs = reinterpret_cast<const double*>(gbase + (blk & 1) * STG_G);
-    const int64_t rleft = N - gb * 32;
-    const int nv = (int)(rleft < 32 ? rleft : 32);
+    const int rleft = cc.rows - cc.b * 32;
+    const int nv = rleft < 32 ? rleft : 32;
     const bool vr = lane < nv;
     const int kl = vr ? ks[lane] : -1;
     const int ka = vr ? (NS >= 1 ? ks[32 + lane] : 0) : -1;
@@ -361,7 +391,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     }
     const unsigned mAx = mA & ~1u;  // run starts inside the block (row 0 always opens segment 0)
     const double* gl = gs + k * GP;
-    if (mAx == 0 && !endA) {
+    if ((mAx == 0 && !endA) || (g.ablate & 32)) {
       // fast path: the open run continues through the block
 #pragma unroll
       for (int j = 0; j < 8; j++) {
@@ -523,13 +553,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 
-  // ---- H_L table -> global
-  __syncthreads();
-  for (int i = threadIdx.x; i < HT; i += blockDim.x) {
-    const int key = hkey[i];
-    if (key != -1 && hcnt[i]) atomicAdd(&g.HL[key], hcnt[i]);
-  }
-  // ---- CTA reduction (warps in order) -> partials
+  // ---- this warp's partial -> partials[CTA * W + warp] (no CTA barrier: warps finish unevenly)
   a8 = red4(a8);
   a9 = red4(a9);
 #pragma unroll
@@ -537,33 +561,36 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     r8[t] = red4(r8[t]);
     r9[t] = red4(r9[t]);
   }
-  double* red = reinterpret_cast<double*>(sm + HT * 8);  // stage memory is free now
-  __syncthreads();
-  for (int i = threadIdx.x; i < NPART; i += blockDim.x) red[i] = 0.0;
-  __syncthreads();
-  for (int w = 0; w < W; w++) {
-    if (wib == w) {
-      red[m * 8 + 2 * k] += aXX[0];
-      red[m * 8 + 2 * k + 1] += aXX[1];
-      red[64 + m * 10 + 2 * k] += aXL[0];
-      red[64 + m * 10 + 2 * k + 1] += aXL[1];
-      if (k == 0) {
-        red[64 + m * 10 + 8] += a8;
-        red[64 + m * 10 + 9] += a9;
-      }
-#pragma unroll
-      for (int t = 0; t < 3; t++) {
-        red[144 + (8 * t + m) * 10 + 2 * k] += aRA[t][0];
-        red[144 + (8 * t + m) * 10 + 2 * k + 1] += aRA[t][1];
-        if (k == 0) {
-          red[144 + (8 * t + m) * 10 + 8] += r8[t];
-          red[144 + (8 * t + m) * 10 + 9] += r9[t];
-        }
-      }
-    }
-    __syncthreads();
+  double* out = g.partials + ((size_t)blockIdx.x * W + wib) * NPART;
+  out[m * 8 + 2 * k] = aXX[0];
+  out[m * 8 + 2 * k + 1] = aXX[1];
+  out[64 + m * 10 + 2 * k] = aXL[0];
+  out[64 + m * 10 + 2 * k + 1] = aXL[1];
+  if (k == 0) {
+    out[64 + m * 10 + 8] = a8;
+    out[64 + m * 10 + 9] = a9;
   }
-  for (int i = threadIdx.x; i < NPART; i += blockDim.x) g.partials[(size_t)blockIdx.x * NPART + i] = red[i];
+#pragma unroll
+  for (int t = 0; t < 3; t++) {
+    out[144 + (8 * t + m) * 10 + 2 * k] = aRA[t][0];
+    out[144 + (8 * t + m) * 10 + 2 * k + 1] = aRA[t][1];
+    if (k == 0) {
+      out[144 + (8 * t + m) * 10 + 8] = r8[t];
+      out[144 + (8 * t + m) * 10 + 9] = r9[t];
+    }
+  }
+  // ---- the CTA's last warp to finish moves the H_L table to global
+  __threadfence_block();
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(cta_done, 1);
+  ticket = __shfl_sync(FULL, ticket, 0);
+  if (ticket == W - 1) {
+    __threadfence_block();
+    for (int i = lane; i < HT; i += 32) {
+      const int key = hkey[i];
+      if (key != -1 && hcnt[i]) atomicAdd(&g.HL[key], hcnt[i]);
+    }
+  }
 }
 
 // V[k][f] = col_f[k] for f < n, 0 for n <= f < GP, except V[k][10] = 1 (the constant of the
@@ -686,19 +713,24 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
   for (int i = threadIdx.x; i < NFIN; i += blockDim.x) a.partials[(size_t)blockIdx.x * NFIN + i] = red[i];
 }
 
-// src[0:NPART] = Σ_cta scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials (fixed order)
-__global__ void k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2, int n2,
-                          double* __restrict__ src) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < NPART) {
-    double s = 0.0;
-    for (int b = 0; b < n1; b++) s += p1[(size_t)b * NPART + e];
-    src[e] = s;
-  } else if (e < NPART + NFIN) {
-    double s = 0.0;
-    for (int b = 0; b < n2; b++) s += p2[(size_t)b * NFIN + e - NPART];
-    src[e] = s;
+// src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  One CTA per
+// output element, fixed-order strided sums and tree (deterministic).
+__global__ void __launch_bounds__(256) k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2,
+                                                 int n2, double* __restrict__ src) {
+  const int e = blockIdx.x;
+  const bool first = e < NPART;
+  const double* p = first ? p1 + e : p2 + (e - NPART);
+  const int n = first ? n1 : n2, stride = first ? NPART : NFIN;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < n; b += blockDim.x) s += p[(size_t)b * stride];
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) src[e] = red[0];
 }
 
 __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __restrict__ toff,
@@ -827,8 +859,8 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
   k_cov_fin<<<FIN_BLOCKS, 256, 0, st>>>(f);
-  k_cov_sum<<<(NPART + NFIN + 127) / 128, 128, 0, st>>>(partials.as<double>(), grid, finp.as<double>(), FIN_BLOCKS,
-                                                         src.as<double>());
+  k_cov_sum<<<NPART + NFIN, 256, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(), FIN_BLOCKS,
+                                          src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                          tcoef.as<double>(), nout, c->scalar_out.as<double>(),
                                                          NPART + 18 * 16 + 10, c->scalar_count.as<unsigned long long>());
@@ -907,6 +939,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   };
   setup(fc->L, featured.back());
   fc->NS = (int)featured.size() - 1;
+  if (fc->L.nk * GP * 8 >= ((int64_t)1 << 32)) return nullptr;  // 32-bit view-row offsets in the scan
   if (fc->NS >= 1) setup(fc->A, featured[featured.size() - 2]);
   if (fc->NS == 2) setup(fc->B, featured[0]);
   // buffers
@@ -933,7 +966,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   const int64_t nitems = (fc->nblk + IB - 1) / IB;
   fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + 2 * nitems + 64, INT32_MAX / BRW);
   if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
-  if (fc->partials.alloc((size_t)fc->grid * NPART * 8)) return nullptr;
+  if (fc->partials.alloc((size_t)fc->grid * 16 * NPART * 8)) return nullptr;  // one partial per warp
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
   if (fc->src.alloc((size_t)(NPART + NFIN) * 8)) return nullptr;
   {  // scan layout of the root: x in DMMA lane order + dense keys, one 2432-byte block per 32 rows
