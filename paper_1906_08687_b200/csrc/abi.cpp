@@ -770,7 +770,7 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
                                         nout, c->scalar_out.as<double>(), c->scalar_count.as<unsigned long long>(), st),
              "run combine");
   }
-  if (!c->groups.empty()) {
+  if (!c->groups.empty() && !(c->fast && c->fast->handles_all_groups())) {
     for (auto& gp : c->groups) {
       CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "run memset");
       CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "run memset");

@@ -14,6 +14,8 @@ struct FastPaths {
   // produced all no-group-by outputs.  Returns a cudaError_t value (0 = ok).
   virtual int run(lmfao_ctx* c, const NodeArgs& root, cudaStream_t st, bool& scalar_done) = 0;
   virtual bool handles_group(int query) const { return false; }
+  // true if run() fills every group-by table of the batch (the generic group scan is skipped)
+  virtual bool handles_all_groups() const { return false; }
   // true if the specialised path builds its own dimension tables (skip generic views)
   virtual bool skip_generic_views() const { return false; }
   virtual std::string describe() const = 0;
@@ -22,4 +24,5 @@ struct FastPaths {
 FastPaths* plan_fast_paths(lmfao_ctx* c);
 FastPaths* plan_gram(lmfao_ctx* c);
 FastPaths* plan_cov(lmfao_ctx* c);
+FastPaths* plan_rt(lmfao_ctx* c);
 }  // namespace lmfao

@@ -1,0 +1,687 @@
+// rt.cu — the histogram path (§8 row (e)) for regression-tree node batches
+// (§3 "Regression trees" P:528-555; BASELINE.json configs[2]):
+//   Q_cat(X; Σ w_p)                  one single-attribute group-by per categorical X,
+//   Q(Σ w_p · 1[A op t])             a Kronecker-delta predicate per (attribute, threshold),
+// with w_p = y^p (p ∈ {0, 1, 2}: SUM(1), SUM(y), SUM(y²)) for one root attribute y.
+//
+// Every such aggregate is a linear functional of a histogram of w:
+//  * a predicate A op t only depends on which "cell" A falls in among the sorted distinct
+//    thresholds used with A (cell 2i: t_{i-1} < A < t_i, cell 2i+1: A = t_i), so
+//    Σ w_p 1[A op t] = Σ_{cells c ⊨ op t} H_A[c][p] — a prefix/suffix sum of H_A
+//    (the paper's 20 buckets; the comparison is exact in IEEE double);
+//  * for a root attribute A, H_A is accumulated over the root rows (k_rt_fact);
+//  * for an attribute of a primary-key leaf D, Σ over the join = Σ_{k ∈ D} V_D[k] · f(A(k))
+//    with the fact→dimension view V_D[k][p] = Σ_{root rows with key k} w_p ("each aggregate
+//    to its own root") — V_D by segmented warp scans over the sorted root
+//    (k_rt_views), then H_A / group tables at the dimension (k_rt_dims);
+//  * group-bys on a root attribute accumulate w per cell (k_rt_fact), on a dimension
+//    attribute through V_D (k_rt_dims).
+// Assembly (k_rt_assemble) maps histogram cells to the batch's UDAFs with term lists.
+#include <cmath>
+#include <cstdlib>
+#include <map>
+#include <set>
+
+#include "ctx.h"
+
+namespace lmfao {
+namespace {
+
+constexpr unsigned RFULL = 0xffffffffu;
+constexpr int RT_MAX_FACT = 24;   // root attributes with histograms (predicates + small group-bys)
+constexpr int RT_MAX_DIM = 64;    // dimension attributes with histograms
+constexpr int RT_MAX_LEVELS = 8;  // root children with views
+constexpr int RT_HT = 1024;       // per-CTA hash slots per view level (Zipf-hot keys)
+
+// A histogram over the root rows: predicate cells of a column, or the codes of a group-by.
+struct FactHist {
+  const void* col;  // root column (fp64 or int32) for predicates, int32 codes for group-bys
+  int is_int;       // predicate column dtype
+  int is_code;      // group-by codes (cell = code) instead of threshold cells
+  int nthr;         // thresholds (predicates)
+  int thr_off;      // into the threshold array
+  int ncell;
+  int soff;         // shared-memory offset (doubles) of the per-warp table, -1: global
+  int64_t goff;     // global offset (doubles) of the [ncell][3] table in the output buffer
+};
+struct RtFactArgs {
+  int64_t nrows;
+  const double* y;  // null: w = (1, 0, 0)
+  int nh;
+  FactHist h[RT_MAX_FACT];
+  const double* thr;  // thresholds, all attributes
+  int nthr_all;
+  int warp_doubles;  // per-warp shared table size
+  double* out;       // global accumulators (TOT at 0)
+};
+
+__device__ __forceinline__ int rt_cell(double x, const double* t, int n) {
+  int lo = 0, hi = n;  // lower bound: first t >= x
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (t[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < n && t[lo] == x) ? 2 * lo + 1 : 2 * lo;
+}
+
+// Root rows: TOT = Σ w and the histograms of the root attributes.  Tables of small cell
+// counts live per warp in shared memory (smem atomics, contention only within the warp),
+// large ones go to global atomics; at the end the CTA's warps are summed into global.
+__global__ void __launch_bounds__(256) k_rt_fact(const __grid_constant__ RtFactArgs a) {
+  extern __shared__ double rsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* thr = rsm;
+  double* tab = rsm + ((a.nthr_all + 1) & ~1) + wib * a.warp_doubles;
+  for (int i = threadIdx.x; i < a.nthr_all; i += blockDim.x) thr[i] = a.thr[i];
+  for (int i = threadIdx.x; i < nw * a.warp_doubles; i += blockDim.x) rsm[((a.nthr_all + 1) & ~1) + i] = 0.0;
+  __syncthreads();
+  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows; row += stride) {
+    const double y = a.y ? a.y[row] : 0.0;
+    const double y2 = y * y;
+    t0 += 1.0;
+    t1 += y;
+    t2 += y2;
+    for (int i = 0; i < a.nh; i++) {
+      const FactHist& h = a.h[i];
+      int c;
+      if (h.is_code) {
+        c = reinterpret_cast<const int32_t*>(h.col)[row];
+      } else {
+        const double x = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
+                                  : reinterpret_cast<const double*>(h.col)[row];
+        c = rt_cell(x, thr + h.thr_off, h.nthr);
+      }
+      if (h.soff >= 0) {
+        double* e = tab + h.soff + 3 * c;
+        atomicAdd(e, 1.0);
+        if (a.y) {
+          atomicAdd(e + 1, y);
+          atomicAdd(e + 2, y2);
+        }
+      } else {
+        double* e = a.out + h.goff + 3 * (int64_t)c;
+        atomicAdd(e, 1.0);
+        if (a.y) {
+          atomicAdd(e + 1, y);
+          atomicAdd(e + 2, y2);
+        }
+      }
+    }
+  }
+  // TOT
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t0 += __shfl_xor_sync(RFULL, t0, o);
+    t1 += __shfl_xor_sync(RFULL, t1, o);
+    t2 += __shfl_xor_sync(RFULL, t2, o);
+  }
+  if (lane == 0) {
+    atomicAdd(a.out, t0);
+    atomicAdd(a.out + 1, t1);
+    atomicAdd(a.out + 2, t2);
+  }
+  __syncthreads();
+  // per-warp tables -> global (sum over the CTA's warps first)
+  const double* base = rsm + ((a.nthr_all + 1) & ~1);
+  for (int i = 0; i < a.nh; i++) {
+    const FactHist& h = a.h[i];
+    if (h.soff < 0) continue;
+    for (int e = threadIdx.x; e < 3 * h.ncell; e += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < nw; w++) s += base[w * a.warp_doubles + h.soff + e];
+      if (s != 0.0) atomicAdd(a.out + h.goff + e, s);
+    }
+  }
+}
+
+// Fact -> dimension views V_j[k][p] = Σ_{root rows with key k} w_p, for the root children
+// that carry predicate or group-by attributes.  Each warp takes a contiguous row range,
+// lane = row; runs of equal keys are summed by a segmented warp scan (the root is sorted
+// by its keys, so runs are long at the outer levels) and a run's total is carried across
+// blocks until it ends.  Run totals go to a per-CTA open-addressing table in shared
+// memory (Zipf-hot keys), to global atomics when a probe misses twice.
+struct RtViewArgs {
+  int64_t nrows;
+  const double* y;
+  int nlev;
+  const int32_t* fk[RT_MAX_LEVELS];
+  double* V[RT_MAX_LEVELS];  // [nk][3]
+};
+__global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtViewArgs a) {
+  extern __shared__ unsigned char vsm[];
+  const int lane = threadIdx.x & 31;
+  int* hkey = reinterpret_cast<int*>(vsm);                                     // [nlev][RT_HT]
+  double* hval = reinterpret_cast<double*>(vsm + a.nlev * RT_HT * 4 + 16);  // [nlev][RT_HT][3]
+  hval = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(hval) + 15) & ~(uintptr_t)15);
+  for (int i = threadIdx.x; i < a.nlev * RT_HT; i += blockDim.x) {
+    hkey[i] = -1;
+    hval[3 * i] = hval[3 * i + 1] = hval[3 * i + 2] = 0.0;
+  }
+  __syncthreads();
+  auto add = [&](int l, int key, double v0, double v1, double v2) {
+    unsigned h = ((unsigned)key * 2654435761u) >> 22;  // 10 bits
+#pragma unroll 1
+    for (int probe = 0; probe < 2; probe++) {
+      int* slot = hkey + l * RT_HT + h;
+      int t = *slot;
+      if (t == -1) {
+        const int old = atomicCAS(slot, -1, key);
+        t = old == -1 ? key : old;
+      }
+      if (t == key) {
+        double* e = hval + 3 * (l * RT_HT + h);
+        atomicAdd(e, v0);
+        atomicAdd(e + 1, v1);
+        atomicAdd(e + 2, v2);
+        return;
+      }
+      h = (h + 1) & (RT_HT - 1);
+    }
+    double* e = a.V[l] + 3 * (int64_t)key;
+    atomicAdd(e, v0);
+    atomicAdd(e + 1, v1);
+    atomicAdd(e + 2, v2);
+  };
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t nblk = (a.nrows + 31) / 32;
+  const int64_t b0 = nblk * gw / nwarps, b1 = nblk * (gw + 1) / nwarps;
+  int ckey[RT_MAX_LEVELS];
+  double c0[RT_MAX_LEVELS], c1[RT_MAX_LEVELS], c2[RT_MAX_LEVELS];
+  for (int l = 0; l < RT_MAX_LEVELS; l++) {
+    ckey[l] = -1;
+    c0[l] = c1[l] = c2[l] = 0.0;
+  }
+  for (int64_t b = b0; b < b1; b++) {
+    const int64_t row = 32 * b + lane;
+    const bool vr = row < a.nrows;
+    const int64_t nrem = a.nrows - 32 * b;
+    const int nv = nrem < 32 ? (int)nrem : 32;
+    const double y = (vr && a.y) ? a.y[row] : 0.0;
+    const double w0 = vr ? 1.0 : 0.0, w1 = y, w2 = y * y;
+#pragma unroll 1
+    for (int l = 0; l < a.nlev; l++) {
+      const int key = vr ? a.fk[l][row] : -2;
+      int prev = __shfl_up_sync(RFULL, key, 1);
+      if (lane == 0) prev = ckey[l];
+      const unsigned heads = __ballot_sync(RFULL, vr && key != prev);
+      double v0 = w0, v1 = w1, v2 = w2;
+      if (heads == 0) {  // the carried run goes on through the block
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          v0 += __shfl_xor_sync(RFULL, v0, o);
+          v1 += __shfl_xor_sync(RFULL, v1, o);
+          v2 += __shfl_xor_sync(RFULL, v2, o);
+        }
+        c0[l] += v0;
+        c1[l] += v1;
+        c2[l] += v2;
+        continue;
+      }
+      // segmented inclusive scan; segment s0 = the run containing the lane
+      const unsigned upto = heads & ((2u << lane) - 1u);
+      const int s0 = upto ? 31 - __clz(upto) : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double o0 = __shfl_up_sync(RFULL, v0, d), o1 = __shfl_up_sync(RFULL, v1, d),
+                     o2 = __shfl_up_sync(RFULL, v2, d);
+        if (lane - d >= s0) {
+          v0 += o0;
+          v1 += o1;
+          v2 += o2;
+        }
+      }
+      if (!upto) {  // lanes of the carried run (before the first head)
+        v0 += c0[l];
+        v1 += c1[l];
+        v2 += c2[l];
+      }
+      // run ends: the lane before a head, and the carried run if the block starts a new one
+      const bool ends = vr && lane < 31 && ((heads >> (lane + 1)) & 1u);  // the next row starts a run
+      if (ends) add(l, upto ? key : ckey[l], v0, v1, v2);
+      if ((heads & 1u) && lane == 0 && ckey[l] >= 0 && (c0[l] != 0.0 || c1[l] != 0.0 || c2[l] != 0.0))
+        add(l, ckey[l], c0[l], c1[l], c2[l]);  // the carried run ended with the previous block
+      // the last run continues: its total (at lane nv-1) becomes the carry
+      c0[l] = __shfl_sync(RFULL, v0, nv - 1);
+      c1[l] = __shfl_sync(RFULL, v1, nv - 1);
+      c2[l] = __shfl_sync(RFULL, v2, nv - 1);
+      ckey[l] = __shfl_sync(RFULL, key, nv - 1);
+    }
+  }
+  for (int l = 0; l < a.nlev; l++)
+    if (lane == 0 && ckey[l] >= 0) add(l, ckey[l], c0[l], c1[l], c2[l]);
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.nlev * RT_HT; i += blockDim.x) {
+    const int key = hkey[i];
+    if (key < 0) continue;
+    const int l = i / RT_HT;
+    double* e = a.V[l] + 3 * (int64_t)key;
+    atomicAdd(e, hval[3 * i]);
+    atomicAdd(e + 1, hval[3 * i + 1]);
+    atomicAdd(e + 2, hval[3 * i + 2]);
+  }
+}
+
+// Dimension side: for every dimension row k of a view level, its V[k] goes to the
+// histogram cell of each of its predicate attributes and to the group cell of each of its
+// group-by attributes.
+struct DimHist {
+  int level;
+  const void* col;  // dimension column (predicates) or codes per dense key (group-bys)
+  int is_int, is_code;
+  int nthr, thr_off, ncell;
+  int64_t goff;
+};
+struct RtDimArgs {
+  int nh;
+  DimHist h[RT_MAX_DIM];
+  const double* V[RT_MAX_LEVELS];
+  int64_t nk[RT_MAX_LEVELS];
+  const double* thr;
+  double* out;
+};
+__global__ void k_rt_dims(const __grid_constant__ RtDimArgs a) {
+  const int i = blockIdx.y;
+  const DimHist& h = a.h[i];
+  const double* V = a.V[h.level];
+  const int64_t nk = a.nk[h.level];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nk; k += (int64_t)gridDim.x * blockDim.x) {
+    const double v0 = V[3 * k];
+    if (v0 == 0.0) continue;
+    int c;
+    if (h.is_code) {
+      c = reinterpret_cast<const int32_t*>(h.col)[k];
+    } else {
+      const double x = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[k]
+                                : reinterpret_cast<const double*>(h.col)[k];
+      c = rt_cell(x, a.thr + h.thr_off, h.nthr);
+    }
+    double* e = a.out + h.goff + 3 * (int64_t)c;
+    atomicAdd(e, v0);
+    atomicAdd(e + 1, V[3 * k + 1]);
+    atomicAdd(e + 2, V[3 * k + 2]);
+  }
+}
+
+// Scalar outputs: out[o] = Σ_t coef_t · acc[idx_t]; group tables: per (query, cell)
+// table[cell][j] = Σ_p coef_{j,p} G[cell][p], counts[cell] = G[cell][0].
+struct RtGroupOut {
+  int64_t ncell, goff;
+  int nudaf, coff;  // coefficients [nudaf][3] at coef + coff
+  double* table;
+  unsigned long long* counts;
+};
+__global__ void k_rt_scalar(const double* __restrict__ acc, const int32_t* __restrict__ toff,
+                            const int32_t* __restrict__ tidx, const double* __restrict__ tcoef, int nout,
+                            double* __restrict__ out, unsigned long long* __restrict__ count) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * acc[tidx[t]];
+    out[o] = s;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)acc[0];
+}
+__global__ void k_rt_groups(const double* __restrict__ acc, const RtGroupOut* __restrict__ gq,
+                            const double* __restrict__ coef) {
+  const RtGroupOut g = gq[blockIdx.y];
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.ncell; c += (int64_t)gridDim.x * blockDim.x) {
+    const double* e = acc + g.goff + 3 * c;
+    g.counts[c] = (unsigned long long)e[0];
+    for (int j = 0; j < g.nudaf; j++) {
+      const double* cf = coef + g.coff + 3 * j;
+      g.table[c * g.nudaf + j] = cf[0] * e[0] + cf[1] * e[1] + cf[2] * e[2];
+    }
+  }
+}
+
+// ======================================================================= host
+struct FastRT : FastPaths {
+  std::vector<int> handled;  // group indices (c->groups) computed here
+  std::vector<FactHist> fh;
+  std::vector<DimHist> dh;
+  std::vector<double> thr;
+  DevBuf dthr, acc, V, toff, tidx, tcoef, gq, gcoef;
+  int64_t nacc = 0;
+  int nlev = 0;
+  int64_t vnk[RT_MAX_LEVELS];
+  int64_t voff[RT_MAX_LEVELS];
+  const int32_t* vfk[RT_MAX_LEVELS];
+  const double* y = nullptr;
+  int warp_doubles = 0, nout = 0, ngq = 0;
+  size_t fact_smem = 0, view_smem = 0;
+  int64_t vtotal = 0;
+  std::string describe() const override {
+    char b[200];
+    std::snprintf(b, sizeof b, "{\"kind\": \"rt\", \"fact_hists\": %zu, \"dim_hists\": %zu, \"views\": %d, \"groups\": %zu}",
+                  fh.size(), dh.size(), nlev, handled.size());
+    return b;
+  }
+  bool handles_group(int g) const override {
+    for (int h : handled)
+      if (h == g) return true;
+    return false;
+  }
+  bool handles_all_groups() const override { return true; }
+  bool skip_generic_views() const override { return true; }
+  int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
+};
+
+int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_done) {
+  const Rel& R = c->rels[c->root];
+  CUDA_TRY(cudaMemsetAsync(acc.p, 0, nacc * 8, st));
+  if (vtotal) CUDA_TRY(cudaMemsetAsync(V.p, 0, vtotal * 24, st));
+  RtFactArgs fa{};
+  fa.nrows = R.nrows;
+  fa.y = y;
+  fa.nh = (int)fh.size();
+  for (size_t i = 0; i < fh.size(); i++) fa.h[i] = fh[i];
+  fa.thr = dthr.as<double>();
+  fa.nthr_all = (int)thr.size();
+  fa.warp_doubles = warp_doubles;
+  fa.out = acc.as<double>();
+  scan_timer_begin(c, st);
+  if (R.nrows > 0) {
+    k_rt_fact<<<148 * 2, 256, fact_smem, st>>>(fa);
+    launches_add(1);
+  }
+  scan_timer_end(c, st);
+  if (nlev > 0 && R.nrows > 0) {
+    RtViewArgs va{};
+    va.nrows = R.nrows;
+    va.y = y;
+    va.nlev = nlev;
+    for (int l = 0; l < nlev; l++) {
+      va.fk[l] = vfk[l];
+      va.V[l] = V.as<double>() + 3 * voff[l];
+    }
+    k_rt_views<<<148 * 2, 256, view_smem, st>>>(va);
+    launches_add(1);
+  }
+  if (!dh.empty()) {
+    RtDimArgs da{};
+    da.nh = (int)dh.size();
+    for (size_t i = 0; i < dh.size(); i++) da.h[i] = dh[i];
+    for (int l = 0; l < nlev; l++) {
+      da.V[l] = V.as<double>() + 3 * voff[l];
+      da.nk[l] = vnk[l];
+    }
+    da.thr = dthr.as<double>();
+    da.out = acc.as<double>();
+    k_rt_dims<<<dim3(64, (unsigned)dh.size()), 256, 0, st>>>(da);
+    launches_add(1);
+  }
+  if (nout > 0) {
+    k_rt_scalar<<<(nout + 255) / 256, 256, 0, st>>>(acc.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
+                                                    tcoef.as<double>(), nout, c->scalar_out.as<double>(),
+                                                    c->scalar_count.as<unsigned long long>());
+    launches_add(1);
+    scalar_done = true;
+  }
+  if (ngq > 0) {
+    k_rt_groups<<<dim3(64, (unsigned)ngq), 256, 0, st>>>(acc.as<double>(), gq.as<RtGroupOut>(), gcoef.as<double>());
+    launches_add(1);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Planner hook: every product is coeff · y^p · [at most one predicate on one attribute]
+// (p <= 2, y one fp64 root attribute), every group-by query has one group-by attribute
+// and predicate-free products; attributes belong to the root or to primary-key leaves
+// of the root.  Otherwise nullptr.
+FastPaths* plan_rt(lmfao_ctx* c) {
+  const Rel& R = c->rels[c->root];
+  for (int ch : R.children)
+    if (!c->rels[ch].children.empty() || !c->rels[ch].unique_key) return nullptr;
+  auto level_of = [&](int attr) -> int {  // -1 root, j child index, -2 unsupported
+    const int o = c->owner[attr];
+    if (o == c->root) return -1;
+    for (size_t j = 0; j < R.children.size(); j++)
+      if (R.children[j] == o) return (int)j;
+    return -2;
+  };
+  struct P {
+    double coef;
+    int pw;
+    int pattr;  // -1: none
+    int kind;
+    double t;
+  };
+  int yattr = -1;
+  bool any_pred = false;
+  auto parse = [&](const QProduct& pr, P& out, bool allow_pred) -> bool {
+    out = P{pr.coeff, 0, -1, 0, 0.0};
+    for (auto& f : pr.f) {
+      if (f.kind == LMFAO_F_CONST) {
+        out.coef *= f.param;
+      } else if (f.kind == LMFAO_F_IDENT) {
+        if (yattr < 0) yattr = f.attr;
+        if (f.attr != yattr) return false;
+        if (++out.pw > 2) return false;
+      } else {
+        if (!allow_pred || out.pattr >= 0) return false;
+        out.pattr = f.attr;
+        out.kind = f.kind;
+        out.t = f.param;
+      }
+    }
+    return true;
+  };
+  std::vector<std::vector<std::vector<P>>> sq;  // scalar: per query, per udaf, products
+  for (int q : c->scalar_queries) {
+    std::vector<std::vector<P>> us;
+    for (auto& u : c->queries[q].udafs) {
+      std::vector<P> ps;
+      for (auto& pr : u) {
+        P p;
+        if (!parse(pr, p, true)) return nullptr;
+        if (p.pattr >= 0) any_pred = true;
+        ps.push_back(p);
+      }
+      us.push_back(ps);
+    }
+    sq.push_back(us);
+  }
+  std::vector<std::vector<std::vector<P>>> gqp(c->groups.size());
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    const Query& Q = c->queries[c->groups[gi].q];
+    if (Q.gb.size() != 1) return nullptr;
+    if (level_of(Q.gb[0]) == -2) return nullptr;
+    for (auto& u : Q.udafs) {
+      std::vector<P> ps;
+      for (auto& pr : u) {
+        P p;
+        if (!parse(pr, p, false)) return nullptr;
+        ps.push_back(p);
+      }
+      gqp[gi].push_back(ps);
+    }
+  }
+  if (!any_pred && c->groups.empty()) return nullptr;
+  if (yattr >= 0 && (level_of(yattr) != -1 || c->attrs[yattr].dt != LMFAO_FP64)) return nullptr;
+  std::unique_ptr<FastRT> rt(new FastRT());
+  if (yattr >= 0) rt->y = (const double*)R.cols[R.find_attr(yattr)].buf.p;
+  // predicate attributes and their sorted distinct thresholds
+  std::map<int, std::set<double>> thr_of;
+  for (auto& us : sq)
+    for (auto& ps : us)
+      for (auto& p : ps)
+        if (p.pattr >= 0) {
+          if (level_of(p.pattr) == -2) return nullptr;
+          if (std::isnan(p.t)) return nullptr;
+          thr_of[p.pattr].insert(p.t);
+        }
+  // accumulator layout: [TOT 3] [fact / dim histograms] [group tables]
+  int64_t nacc = 3;
+  std::map<int, int64_t> hoff;  // predicate attr -> offset of its [ncell][3]
+  std::map<int, int> hthr;      // attr -> thr offset
+  std::vector<int> levels_used(R.children.size(), 0);
+  int soff = 0;
+  for (auto& kv : thr_of) {
+    const int a = kv.first, lv = level_of(a);
+    const int thr_off = (int)rt->thr.size();
+    for (double t : kv.second) rt->thr.push_back(t);
+    const int nthr = (int)kv.second.size(), ncell = 2 * nthr + 1;
+    hoff[a] = nacc;
+    hthr[a] = thr_off;
+    if (lv == -1) {
+      FactHist h{};
+      h.col = R.cols[R.find_attr(a)].buf.p;
+      h.is_int = c->attrs[a].dt == LMFAO_INT32;
+      h.is_code = 0;
+      h.nthr = nthr;
+      h.thr_off = thr_off;
+      h.ncell = ncell;
+      h.soff = -1;
+      if (ncell <= 256) {
+        h.soff = soff;
+        soff += 3 * ncell;
+      }
+      h.goff = nacc;
+      rt->fh.push_back(h);
+    } else {
+      const Rel& D = c->rels[R.children[lv]];
+      DimHist h{};
+      h.level = lv;
+      h.col = D.cols[D.find_attr(a)].buf.p;
+      h.is_int = c->attrs[a].dt == LMFAO_INT32;
+      h.is_code = 0;
+      h.nthr = nthr;
+      h.thr_off = thr_off;
+      h.ncell = ncell;
+      h.goff = nacc;
+      rt->dh.push_back(h);
+      levels_used[lv] = 1;
+    }
+    nacc += 3 * (int64_t)ncell;
+  }
+  // group-by queries
+  std::vector<RtGroupOut> gouts;
+  std::vector<double> gcoef;
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    GroupPlan& gp = c->groups[gi];
+    const Query& Q = c->queries[gp.q];
+    const int a = Q.gb[0], lv = level_of(a);
+    const int64_t ncell = gp.ncells;
+    if (lv == -1) {
+      FactHist h{};
+      h.col = gp.g.code[0];
+      h.is_code = 1;
+      h.ncell = (int)std::min<int64_t>(ncell, INT32_MAX);
+      h.soff = -1;
+      if (ncell <= 256) {
+        h.soff = soff;
+        soff += 3 * (int)ncell;
+      }
+      h.goff = nacc;
+      rt->fh.push_back(h);
+    } else {
+      DimHist h{};
+      h.level = lv;
+      h.col = gp.g.code[0];  // codes indexed by the child's dense key
+      h.is_code = 1;
+      h.ncell = (int)std::min<int64_t>(ncell, INT32_MAX);
+      h.goff = nacc;
+      rt->dh.push_back(h);
+      levels_used[lv] = 1;
+    }
+    RtGroupOut go{};
+    go.ncell = ncell;
+    go.goff = nacc;
+    go.nudaf = gp.nudaf;
+    go.coff = (int)gcoef.size();
+    go.table = gp.table.as<double>();
+    go.counts = gp.counts.as<unsigned long long>();
+    for (auto& ps : gqp[gi]) {
+      double cf[3] = {0, 0, 0};
+      for (auto& p : ps) cf[p.pw] += p.coef;
+      gcoef.insert(gcoef.end(), cf, cf + 3);
+    }
+    gouts.push_back(go);
+    rt->handled.push_back((int)gi);
+    nacc += 3 * ncell;
+  }
+  if ((int)rt->fh.size() > RT_MAX_FACT || (int)rt->dh.size() > RT_MAX_DIM) return nullptr;
+  rt->nacc = nacc;
+  rt->warp_doubles = (soff + 1) & ~1;
+  rt->fact_smem = (size_t)(((int)rt->thr.size() + 1) & ~1) * 8 + (size_t)8 * rt->warp_doubles * 8;
+  if (rt->fact_smem > 200 * 1024) {  // too many per-warp tables: all global
+    for (auto& h : rt->fh) h.soff = -1;
+    rt->warp_doubles = 0;
+    rt->fact_smem = (size_t)(((int)rt->thr.size() + 1) & ~1) * 8;
+  }
+  // views
+  int64_t vt = 0;
+  for (size_t j = 0; j < R.children.size(); j++) {
+    if (!levels_used[j]) continue;
+    if (rt->nlev == RT_MAX_LEVELS) return nullptr;
+    const int l = rt->nlev++;
+    rt->vfk[l] = R.fk_dense[j].as<int32_t>();
+    rt->vnk[l] = c->rels[R.children[j]].nkeys;
+    rt->voff[l] = vt;
+    vt += rt->vnk[l];
+    for (auto& h : rt->dh)
+      if (h.level == (int)j) h.level = l;
+  }
+  rt->vtotal = vt;
+  rt->view_smem = (size_t)rt->nlev * RT_HT * 4 + 32 + (size_t)rt->nlev * RT_HT * 24;
+  if (rt->view_smem > 200 * 1024) return nullptr;
+  // scalar outputs: term lists over the accumulators
+  std::vector<int32_t> toff{0}, tidx;
+  std::vector<double> tcoef;
+  auto truth = [](int kind, int q, int cell) -> bool {  // predicate `op t_q` on cell
+    switch (kind) {
+      case LMFAO_F_LT: return cell <= 2 * q;
+      case LMFAO_F_LE: return cell <= 2 * q + 1;
+      case LMFAO_F_GT: return cell >= 2 * q + 2;
+      case LMFAO_F_GE: return cell >= 2 * q + 1;
+      case LMFAO_F_EQ: return cell == 2 * q + 1;
+      default: return cell != 2 * q + 1;  // NE
+    }
+  };
+  for (auto& us : sq)
+    for (auto& ps : us) {
+      for (auto& p : ps) {
+        if (p.pattr < 0) {
+          tidx.push_back(p.pw);
+          tcoef.push_back(p.coef);
+          continue;
+        }
+        const std::set<double>& ts = thr_of[p.pattr];
+        const int q = (int)std::distance(ts.begin(), ts.find(p.t));
+        const int ncell = 2 * (int)ts.size() + 1;
+        for (int cell = 0; cell < ncell; cell++)
+          if (truth(p.kind, q, cell)) {
+            tidx.push_back((int32_t)(hoff[p.pattr] + 3 * cell + p.pw));
+            tcoef.push_back(p.coef);
+          }
+      }
+      toff.push_back((int32_t)tidx.size());
+    }
+  rt->nout = (int)toff.size() - 1;
+  rt->ngq = (int)gouts.size();
+  cudaStream_t st = c->stream;
+  auto up = [&](DevBuf& b, const void* src, size_t bytes) -> bool {
+    if (b.alloc(std::max<size_t>(bytes, 16))) return false;
+    if (bytes && cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, st)) return false;
+    return true;
+  };
+  if (!up(rt->dthr, rt->thr.data(), rt->thr.size() * 8) || !up(rt->toff, toff.data(), toff.size() * 4) ||
+      !up(rt->tidx, tidx.data(), tidx.size() * 4) || !up(rt->tcoef, tcoef.data(), tcoef.size() * 8) ||
+      !up(rt->gq, gouts.data(), gouts.size() * sizeof(RtGroupOut)) ||
+      !up(rt->gcoef, gcoef.data(), gcoef.size() * 8))
+    return nullptr;
+  if (rt->acc.alloc(nacc * 8)) return nullptr;
+  if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) return nullptr;
+  if (cudaStreamSynchronize(st)) return nullptr;
+  if (cudaFuncSetAttribute(k_rt_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(rt->fact_smem, 16)) ||
+      cudaFuncSetAttribute(k_rt_views, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->view_smem))
+    return nullptr;
+  return rt.release();
+}
+
+}  // namespace lmfao
