@@ -41,18 +41,19 @@ struct FactHist {
   int nthr;         // thresholds (predicates)
   int thr_off;      // into the threshold array
   int ncell;
-  int soff;         // shared-memory offset (doubles) of the per-warp table, -1: global
+  int uniform;      // thresholds t_i = t_0 + i h exactly (cell estimate + exact fix-up)
+  double t0, inv_h;
   int64_t goff;     // global offset (doubles) of the [ncell][3] table in the output buffer
 };
+constexpr int RT_SMALL = 41;  // cells of a histogram kept in per-lane private tables
 struct RtFactArgs {
   int64_t nrows;
   const double* y;  // null: w = (1, 0, 0)
-  int nh;
+  int nh;           // histograms; CTA (part, h) does histogram h over row part `part`
+  int nparts;
   FactHist h[RT_MAX_FACT];
   const double* thr;  // thresholds, all attributes
-  int nthr_all;
-  int warp_doubles;  // per-warp shared table size
-  double* out;       // global accumulators (TOT at 0)
+  double* out;        // global accumulators (TOT at 0)
 };
 
 __device__ __forceinline__ int rt_cell(double x, const double* t, int n) {
@@ -64,76 +65,158 @@ __device__ __forceinline__ int rt_cell(double x, const double* t, int n) {
   }
   return (lo < n && t[lo] == x) ? 2 * lo + 1 : 2 * lo;
 }
+// lower bound from an arithmetic-progression estimate, corrected by exact comparisons
+__device__ __forceinline__ int rt_cell_uniform(double x, const double* t, int n, double t0, double inv_h) {
+  double e = (x - t0) * inv_h + 1.0;
+  e = e < 0.0 ? 0.0 : (e > (double)n ? (double)n : e);  // NaN-free inputs
+  int lo = (int)e;
+  while (lo > 0 && t[lo - 1] >= x) lo--;
+  while (lo < n && t[lo] < x) lo++;
+  return (lo < n && t[lo] == x) ? 2 * lo + 1 : 2 * lo;
+}
 
-// Root rows: TOT = Σ w and the histograms of the root attributes.  Tables of small cell
-// counts live per warp in shared memory (smem atomics, contention only within the warp),
-// large ones go to global atomics; at the end the CTA's warps are summed into global.
+// Root rows: one histogram per CTA (blockIdx = part * nh + h: the CTAs of one row part run
+// side by side, so y is read from HBM once and from L2 by the others).  Small histograms
+// (<= RT_SMALL cells) use per-lane private tables in shared memory — plain conflict-free
+// read-modify-write, no atomics — summed over the CTA at the end; TOT is accumulated by
+// the CTAs of histogram 0.
 __global__ void __launch_bounds__(256) k_rt_fact(const __grid_constant__ RtFactArgs a) {
   extern __shared__ double rsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int hi = blockIdx.x % a.nh, part = blockIdx.x / a.nh;
+  const FactHist& h = a.h[hi];
+  const int nc = h.ncell;
+  // per warp: [nc][32] u32 counts, [nc][32] y, [nc][32] y^2
   double* thr = rsm;
-  double* tab = rsm + ((a.nthr_all + 1) & ~1) + wib * a.warp_doubles;
-  for (int i = threadIdx.x; i < a.nthr_all; i += blockDim.x) thr[i] = a.thr[i];
-  for (int i = threadIdx.x; i < nw * a.warp_doubles; i += blockDim.x) rsm[((a.nthr_all + 1) & ~1) + i] = 0.0;
+  const int tslot = (h.nthr + 1) & ~1;
+  unsigned char* wt = reinterpret_cast<unsigned char*>(rsm + tslot) + (size_t)wib * nc * 32 * 20;
+  unsigned* tc = reinterpret_cast<unsigned*>(wt);
+  double* ty = reinterpret_cast<double*>(wt + nc * 32 * 4);
+  double* ty2 = ty + nc * 32;
+  for (int i = threadIdx.x; i < h.nthr; i += blockDim.x) thr[i] = a.thr[h.thr_off + i];
+  for (int i = lane; i < nc * 32; i += 32) {
+    tc[i] = 0;
+    ty[i] = 0.0;
+    ty2[i] = 0.0;
+  }
   __syncthreads();
+  const int64_t r0 = a.nrows * part / a.nparts, r1 = a.nrows * (part + 1) / a.nparts;
   double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows; row += stride) {
-    const double y = a.y ? a.y[row] : 0.0;
-    const double y2 = y * y;
-    t0 += 1.0;
-    t1 += y;
-    t2 += y2;
-    for (int i = 0; i < a.nh; i++) {
-      const FactHist& h = a.h[i];
-      int c;
-      if (h.is_code) {
-        c = reinterpret_cast<const int32_t*>(h.col)[row];
-      } else {
-        const double x = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
-                                  : reinterpret_cast<const double*>(h.col)[row];
-        c = rt_cell(x, thr + h.thr_off, h.nthr);
+  constexpr int U = 16;  // rows per lane per step: all loads issued before the table updates
+  for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
+    double yv[U], xv[U];
+    int cv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t row = base + 32 * u;
+      const bool v = row < r1;
+      yv[u] = (v && a.y) ? a.y[row] : 0.0;
+      cv[u] = -1;
+      xv[u] = 0.0;
+      if (v) {
+        if (h.is_code) cv[u] = reinterpret_cast<const int32_t*>(h.col)[row];
+        else xv[u] = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
+                              : reinterpret_cast<const double*>(h.col)[row];
       }
-      if (h.soff >= 0) {
-        double* e = tab + h.soff + 3 * c;
-        atomicAdd(e, 1.0);
-        if (a.y) {
-          atomicAdd(e + 1, y);
-          atomicAdd(e + 2, y2);
-        }
-      } else {
-        double* e = a.out + h.goff + 3 * (int64_t)c;
-        atomicAdd(e, 1.0);
-        if (a.y) {
-          atomicAdd(e + 1, y);
-          atomicAdd(e + 2, y2);
-        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (base + 32 * u >= r1) continue;
+      const double y = yv[u];
+      int c = cv[u];
+      if (!h.is_code) c = h.uniform ? rt_cell_uniform(xv[u], thr, h.nthr, h.t0, h.inv_h) : rt_cell(xv[u], thr, h.nthr);
+      const int e = c * 32 + lane;
+      tc[e] += 1u;
+      ty[e] += y;
+      ty2[e] += y * y;
+      if (hi == 0) {
+        t0 += 1.0;
+        t1 += y;
+        t2 += y * y;
       }
     }
   }
-  // TOT
+  if (hi == 0) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t0 += __shfl_xor_sync(RFULL, t0, o);
-    t1 += __shfl_xor_sync(RFULL, t1, o);
-    t2 += __shfl_xor_sync(RFULL, t2, o);
-  }
-  if (lane == 0) {
-    atomicAdd(a.out, t0);
-    atomicAdd(a.out + 1, t1);
-    atomicAdd(a.out + 2, t2);
+    for (int o = 16; o > 0; o >>= 1) {
+      t0 += __shfl_xor_sync(RFULL, t0, o);
+      t1 += __shfl_xor_sync(RFULL, t1, o);
+      t2 += __shfl_xor_sync(RFULL, t2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(a.out, t0);
+      atomicAdd(a.out + 1, t1);
+      atomicAdd(a.out + 2, t2);
+    }
   }
   __syncthreads();
-  // per-warp tables -> global (sum over the CTA's warps first)
-  const double* base = rsm + ((a.nthr_all + 1) & ~1);
-  for (int i = 0; i < a.nh; i++) {
-    const FactHist& h = a.h[i];
-    if (h.soff < 0) continue;
-    for (int e = threadIdx.x; e < 3 * h.ncell; e += blockDim.x) {
-      double s = 0.0;
-      for (int w = 0; w < nw; w++) s += base[w * a.warp_doubles + h.soff + e];
-      if (s != 0.0) atomicAdd(a.out + h.goff + e, s);
+  // Σ over the CTA's warps and lanes -> global
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(rsm + tslot);
+  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+    const int cell = i / 3, v = i % 3;
+    double s = 0.0;
+    for (int w = 0; w < nw; w++) {
+      const unsigned char* ww = base + (size_t)w * nc * 32 * 20;
+      if (v == 0) {
+        unsigned long long cs = 0;
+        for (int l = 0; l < 32; l++) cs += reinterpret_cast<const unsigned*>(ww)[cell * 32 + l];
+        s += (double)cs;
+      } else {
+        const double* tv = reinterpret_cast<const double*>(ww + nc * 32 * 4) + (v - 1) * nc * 32 + cell * 32;
+        for (int l = 0; l < 32; l++) s += tv[l];
+      }
     }
+    if (s != 0.0) atomicAdd(a.out + h.goff + i, s);
+  }
+}
+
+// Root histograms with more than RT_SMALL cells (group-bys on large root domains): one
+// table per CTA in shared memory ([ncell] u32 counts, [ncell][2] sums) updated with shared
+// atomics when it fits, global atomics otherwise.
+struct RtBigArgs {
+  int64_t nrows;
+  const double* y;
+  const int32_t* code;
+  int ncell;
+  int in_smem;
+  double* out;  // [ncell][3] at its goff
+};
+__global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArgs a) {
+  extern __shared__ unsigned char bsm[];
+  unsigned* cnt = reinterpret_cast<unsigned*>(bsm);
+  double* sums = reinterpret_cast<double*>(bsm + ((a.ncell * 4 + 15) & ~15));
+  if (a.in_smem) {
+    for (int i = threadIdx.x; i < a.ncell; i += blockDim.x) {
+      cnt[i] = 0;
+      sums[2 * i] = sums[2 * i + 1] = 0.0;
+    }
+    __syncthreads();
+  }
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    const double y = a.y ? a.y[row] : 0.0;
+    const int c = a.code[row];
+    if (a.in_smem) {
+      atomicAdd(&cnt[c], 1u);
+      if (a.y) {
+        atomicAdd(&sums[2 * c], y);
+        atomicAdd(&sums[2 * c + 1], y * y);
+      }
+    } else {
+      atomicAdd(a.out + 3 * (int64_t)c, 1.0);
+      if (a.y) {
+        atomicAdd(a.out + 3 * (int64_t)c + 1, y);
+        atomicAdd(a.out + 3 * (int64_t)c + 2, y * y);
+      }
+    }
+  }
+  if (!a.in_smem) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.ncell; i += blockDim.x) {
+    if (!cnt[i]) continue;
+    atomicAdd(a.out + 3 * (int64_t)i, (double)cnt[i]);
+    atomicAdd(a.out + 3 * (int64_t)i + 1, sums[2 * i]);
+    atomicAdd(a.out + 3 * (int64_t)i + 2, sums[2 * i + 1]);
   }
 }
 
@@ -150,6 +233,7 @@ struct RtViewArgs {
   const int32_t* fk[RT_MAX_LEVELS];
   double* V[RT_MAX_LEVELS];  // [nk][3]
 };
+template <int NLEV>
 __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtViewArgs a) {
   extern __shared__ unsigned char vsm[];
   const int lane = threadIdx.x & 31;
@@ -189,22 +273,38 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t nblk = (a.nrows + 31) / 32;
   const int64_t b0 = nblk * gw / nwarps, b1 = nblk * (gw + 1) / nwarps;
-  int ckey[RT_MAX_LEVELS];
-  double c0[RT_MAX_LEVELS], c1[RT_MAX_LEVELS], c2[RT_MAX_LEVELS];
-  for (int l = 0; l < RT_MAX_LEVELS; l++) {
+  int ckey[NLEV];
+  double c0[NLEV], c1[NLEV], c2[NLEV];
+#pragma unroll
+  for (int l = 0; l < NLEV; l++) {
     ckey[l] = -1;
     c0[l] = c1[l] = c2[l] = 0.0;
   }
+  // software pipeline: the next block's y and keys are loaded while this block is scanned
+  double ny = 0.0;
+  int nkey[NLEV];
+  auto load = [&](int64_t b) {
+    const int64_t row = 32 * b + lane;
+    const bool v = b < b1 && row < a.nrows;
+    ny = (v && a.y) ? a.y[row] : 0.0;
+#pragma unroll
+    for (int l = 0; l < NLEV; l++) nkey[l] = v ? a.fk[l][row] : -2;
+  };
+  load(b0);
   for (int64_t b = b0; b < b1; b++) {
     const int64_t row = 32 * b + lane;
     const bool vr = row < a.nrows;
     const int64_t nrem = a.nrows - 32 * b;
     const int nv = nrem < 32 ? (int)nrem : 32;
-    const double y = (vr && a.y) ? a.y[row] : 0.0;
+    const double y = ny;
+    int keys[NLEV];
+#pragma unroll
+    for (int l = 0; l < NLEV; l++) keys[l] = nkey[l];
+    load(b + 1);
     const double w0 = vr ? 1.0 : 0.0, w1 = y, w2 = y * y;
-#pragma unroll 1
-    for (int l = 0; l < a.nlev; l++) {
-      const int key = vr ? a.fk[l][row] : -2;
+#pragma unroll
+    for (int l = 0; l < NLEV; l++) {
+      const int key = keys[l];
       int prev = __shfl_up_sync(RFULL, key, 1);
       if (lane == 0) prev = ckey[l];
       const unsigned heads = __ballot_sync(RFULL, vr && key != prev);
@@ -251,7 +351,8 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
       ckey[l] = __shfl_sync(RFULL, key, nv - 1);
     }
   }
-  for (int l = 0; l < a.nlev; l++)
+#pragma unroll
+  for (int l = 0; l < NLEV; l++)
     if (lane == 0 && ckey[l] >= 0) add(l, ckey[l], c0[l], c1[l], c2[l]);
   __syncthreads();
   for (int i = threadIdx.x; i < a.nlev * RT_HT; i += blockDim.x) {
@@ -340,7 +441,9 @@ __global__ void k_rt_groups(const double* __restrict__ acc, const RtGroupOut* __
 // ======================================================================= host
 struct FastRT : FastPaths {
   std::vector<int> handled;  // group indices (c->groups) computed here
-  std::vector<FactHist> fh;
+  std::vector<FactHist> fh;  // small root histograms (k_rt_fact)
+  std::vector<FactHist> fbig;  // large root group-bys (k_rt_big)
+  int nparts = 1;
   std::vector<DimHist> dh;
   std::vector<double> thr;
   DevBuf dthr, acc, V, toff, tidx, tcoef, gq, gcoef;
@@ -350,7 +453,7 @@ struct FastRT : FastPaths {
   int64_t voff[RT_MAX_LEVELS];
   const int32_t* vfk[RT_MAX_LEVELS];
   const double* y = nullptr;
-  int warp_doubles = 0, nout = 0, ngq = 0;
+  int nout = 0, ngq = 0;
   size_t fact_smem = 0, view_smem = 0;
   int64_t vtotal = 0;
   std::string describe() const override {
@@ -377,17 +480,29 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
   fa.nrows = R.nrows;
   fa.y = y;
   fa.nh = (int)fh.size();
+  fa.nparts = nparts;
   for (size_t i = 0; i < fh.size(); i++) fa.h[i] = fh[i];
   fa.thr = dthr.as<double>();
-  fa.nthr_all = (int)thr.size();
-  fa.warp_doubles = warp_doubles;
   fa.out = acc.as<double>();
   scan_timer_begin(c, st);
   if (R.nrows > 0) {
-    k_rt_fact<<<148 * 2, 256, fact_smem, st>>>(fa);
+    k_rt_fact<<<nparts * fa.nh, 256, fact_smem, st>>>(fa);
     launches_add(1);
   }
   scan_timer_end(c, st);
+  for (auto& h : fbig) {
+    if (R.nrows <= 0) break;
+    RtBigArgs ba{};
+    ba.nrows = R.nrows;
+    ba.y = y;
+    ba.code = reinterpret_cast<const int32_t*>(h.col);
+    ba.ncell = h.ncell;
+    const size_t smem = (size_t)((h.ncell * 4 + 15) & ~15) + (size_t)h.ncell * 16;
+    ba.in_smem = smem <= 200 * 1024;
+    ba.out = acc.as<double>() + h.goff;
+    k_rt_big<<<148, 512, ba.in_smem ? smem : 0, st>>>(ba);
+    launches_add(1);
+  }
   if (nlev > 0 && R.nrows > 0) {
     RtViewArgs va{};
     va.nrows = R.nrows;
@@ -397,7 +512,14 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
       va.fk[l] = vfk[l];
       va.V[l] = V.as<double>() + 3 * voff[l];
     }
-    k_rt_views<<<148 * 2, 256, view_smem, st>>>(va);
+    switch (nlev) {
+#define VIEWS(n)                                               \
+  case n:                                                      \
+    k_rt_views<n><<<148 * 2, 256, view_smem, st>>>(va);        \
+    break;
+      VIEWS(1) VIEWS(2) VIEWS(3) VIEWS(4) VIEWS(5) VIEWS(6) VIEWS(7) VIEWS(8)
+#undef VIEWS
+    }
     launches_add(1);
   }
   if (!dh.empty()) {
@@ -520,7 +642,6 @@ FastPaths* plan_rt(lmfao_ctx* c) {
   std::map<int, int64_t> hoff;  // predicate attr -> offset of its [ncell][3]
   std::map<int, int> hthr;      // attr -> thr offset
   std::vector<int> levels_used(R.children.size(), 0);
-  int soff = 0;
   for (auto& kv : thr_of) {
     const int a = kv.first, lv = level_of(a);
     const int thr_off = (int)rt->thr.size();
@@ -536,13 +657,21 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       h.nthr = nthr;
       h.thr_off = thr_off;
       h.ncell = ncell;
-      h.soff = -1;
-      if (ncell <= 256) {
-        h.soff = soff;
-        soff += 3 * ncell;
-      }
       h.goff = nacc;
-      rt->fh.push_back(h);
+      if (nthr >= 2) {  // near-arithmetic thresholds: O(1) cell estimate (exact fix-up either way)
+        const double t0 = *kv.second.begin(), tl = *kv.second.rbegin();
+        const double step = (tl - t0) / (nthr - 1);
+        bool ok = step > 0.0 && std::isfinite(step);
+        int i = 0;
+        for (double t : kv.second) ok = ok && std::fabs(t - (t0 + i++ * step)) <= step;
+        if (ok) {
+          h.uniform = 1;
+          h.t0 = t0;
+          h.inv_h = 1.0 / step;
+        }
+      }
+      if (ncell <= RT_SMALL) rt->fh.push_back(h);
+      else rt->fbig.push_back(h);  // (predicate with > 20 thresholds: not expected; handled below)
     } else {
       const Rel& D = c->rels[R.children[lv]];
       DimHist h{};
@@ -572,13 +701,9 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       h.col = gp.g.code[0];
       h.is_code = 1;
       h.ncell = (int)std::min<int64_t>(ncell, INT32_MAX);
-      h.soff = -1;
-      if (ncell <= 256) {
-        h.soff = soff;
-        soff += 3 * (int)ncell;
-      }
       h.goff = nacc;
-      rt->fh.push_back(h);
+      if (ncell <= RT_SMALL) rt->fh.push_back(h);
+      else rt->fbig.push_back(h);
     } else {
       DimHist h{};
       h.level = lv;
@@ -606,13 +731,24 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     nacc += 3 * ncell;
   }
   if ((int)rt->fh.size() > RT_MAX_FACT || (int)rt->dh.size() > RT_MAX_DIM) return nullptr;
+  for (auto& h : rt->fbig)
+    if (!h.is_code) return nullptr;  // predicates with more than 20 distinct thresholds: generic path
+  if (rt->fh.empty()) {  // TOT still comes from k_rt_fact: a one-cell histogram of the first root column
+    FactHist h{};
+    h.col = R.cols.empty() ? nullptr : R.cols[0].buf.p;
+    if (!h.col) return nullptr;
+    h.is_int = R.cols[0].dt == LMFAO_INT32;
+    h.ncell = 1;
+    h.goff = nacc;
+    nacc += 3;
+    rt->fh.push_back(h);
+  }
   rt->nacc = nacc;
-  rt->warp_doubles = (soff + 1) & ~1;
-  rt->fact_smem = (size_t)(((int)rt->thr.size() + 1) & ~1) * 8 + (size_t)8 * rt->warp_doubles * 8;
-  if (rt->fact_smem > 200 * 1024) {  // too many per-warp tables: all global
-    for (auto& h : rt->fh) h.soff = -1;
-    rt->warp_doubles = 0;
-    rt->fact_smem = (size_t)(((int)rt->thr.size() + 1) & ~1) * 8;
+  rt->nparts = std::max(1, (148 * 2 + (int)rt->fh.size() - 1) / (int)rt->fh.size());
+  {
+    int maxthr = 0;
+    for (auto& h : rt->fh) maxthr = std::max(maxthr, h.nthr);
+    rt->fact_smem = (size_t)((maxthr + 1) & ~1) * 8 + (size_t)8 * RT_SMALL * 32 * 20;
   }
   // views
   int64_t vt = 0;
@@ -678,9 +814,17 @@ FastPaths* plan_rt(lmfao_ctx* c) {
   if (rt->acc.alloc(nacc * 8)) return nullptr;
   if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) return nullptr;
   if (cudaStreamSynchronize(st)) return nullptr;
-  if (cudaFuncSetAttribute(k_rt_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(rt->fact_smem, 16)) ||
-      cudaFuncSetAttribute(k_rt_views, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->view_smem))
+  if (cudaFuncSetAttribute(k_rt_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->fact_smem) ||
+      cudaFuncSetAttribute(k_rt_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
     return nullptr;
+  {
+    cudaError_t e = cudaSuccess;
+#define VATTR(n) \
+  if (!e) e = cudaFuncSetAttribute(k_rt_views<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->view_smem);
+    VATTR(1) VATTR(2) VATTR(3) VATTR(4) VATTR(5) VATTR(6) VATTR(7) VATTR(8)
+#undef VATTR
+    if (e) return nullptr;
+  }
   return rt.release();
 }
 
