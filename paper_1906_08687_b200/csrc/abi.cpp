@@ -708,6 +708,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
           coef = 0.0;
         }
         d.countlike[j] = constant;
+        if (!constant) d.nsum++;
         if (constant) cc[j] = coef;
         all.out_ioff.push_back((int)all.ip.size());
         all.out_doff.push_back((int)all.dp.size());

@@ -253,13 +253,27 @@ __global__ void k_groups_fused(NodeArgs a, const GroupDesc* __restrict__ descs, 
       } else if (cell >= 0) {
         atomicAdd(&d.counts[cell], (unsigned long long)w);
       }
-      if (cell >= 0) {
-        for (int j = 0; j < d.nudaf; j++) {
-          if (d.countlike[j]) continue;
-          const int o = d.prog_base + j;
-          const double v = eval_output(a, row, kk, prog_i + ioff[o], prog_d + doff[o]);
-          if (v != 0.0) atomicAdd(&d.table[cell * d.nudaf + j], v);
+      // non-constant UDAFs: the root is sorted by its keys, so equal cells mostly sit in
+      // runs of adjacent lanes; a segmented warp scan sums each run and its last lane
+      // issues one atomic (cells repeated in non-adjacent runs just get several atomics)
+      if (d.nsum == 0) continue;
+      long long pc = __shfl_up_sync(0xffffffffu, cell, 1);
+      const bool head = lane == 0 || pc != cell;
+      const unsigned heads = __ballot_sync(0xffffffffu, head);
+      const unsigned upto = heads & ((2u << lane) - 1u);
+      const int s0 = 31 - __clz(upto);
+      long long nc = __shfl_down_sync(0xffffffffu, cell, 1);
+      const bool tail = lane == 31 || nc != cell;
+      for (int j = 0; j < d.nudaf; j++) {
+        if (d.countlike[j]) continue;
+        const int o = d.prog_base + j;
+        double v = cell >= 0 ? eval_output(a, row, kk, prog_i + ioff[o], prog_d + doff[o]) : 0.0;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const double u = __shfl_up_sync(0xffffffffu, v, dd);
+          if (lane - dd >= s0) v += u;
         }
+        if (tail && cell >= 0 && v != 0.0) atomicAdd(&d.table[cell * d.nudaf + j], v);
       }
     }
   }

@@ -124,6 +124,7 @@ struct GroupDesc {
   double* table;
   unsigned long long* counts;
   unsigned char countlike[64];  // UDAF j is a constant c (SUM(c)): derived from the counts
+  int32_t nsum;                 // UDAFs that are not countlike
 };
 cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int nq, const int32_t* prog_i,
                                 const double* prog_d, const int32_t* ioff, const int32_t* doff, cudaStream_t st);
