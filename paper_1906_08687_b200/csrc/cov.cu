@@ -37,9 +37,10 @@ namespace {
 
 constexpr int IB = 16;       // 32-row blocks per dynamically scheduled item
 constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
+constexpr int HT = 1024;     // per-CTA H_L hash slots
 constexpr int SBLK = 256 * 8 + 3 * 32 * 4;     // scan-layout bytes per 32-row block: x in DMMA order + 3 key rows
 constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows per block (2 slots)
-constexpr int NPART = 484;   // per-warp partial: XX[8][8] | XL[8][10] | RA[24][10] | LL[10][10]
+constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][10]
 constexpr int BRW = 36;      // doubles per B record
 constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
 constexpr int FIN_BLOCKS = 148;
@@ -134,13 +135,13 @@ __global__ void k_cov_layout(LayoutArgs a) {
   }
 }
 
-constexpr int COV_W = 12;  // warps per CTA of the scan (one CTA per SM; 168 registers, no spills)
+constexpr int COV_W = 16;  // warps per CTA of the scan (one CTA per SM)
 
 template <int W>
 struct CovCfg {
-  static constexpr int CF = W >= 16 ? 3 : (W >= 12 ? 5 : 7);  // fact-block ring slots per warp
+  static constexpr int CF = W >= 16 ? 3 : (W >= 12 ? 4 : 7);  // fact-block ring slots per warp
   static constexpr int WB = CF * SBLK + 2 * STG_G + 512;       // + barriers, item ring, segment table
-  static constexpr int SMEM = W * WB;
+  static constexpr int SMEM = 128 + HT * 8 + W * WB;  // [CTA counters | H_L table | warps]
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -162,13 +163,21 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   constexpr int CF = Cfg::CF;
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, wib = threadIdx.x >> 5;
   extern __shared__ __align__(1024) unsigned char sm[];
-  unsigned char* wbase = sm + wib * Cfg::WB;
+  int* cta_done = reinterpret_cast<int*>(sm);
+  int* hkey = reinterpret_cast<int*>(sm + 128);
+  unsigned* hcnt = reinterpret_cast<unsigned*>(sm + 128 + HT * 4);
+  unsigned char* wbase = sm + 128 + HT * 8 + wib * Cfg::WB;
   unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
   uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
   int* ring = reinterpret_cast<int*>(bar_f + 8);  // 8 grabbed item ids
   int* segst = ring + 8;                          // [34] segment start rows of the current block
   int* segkey = segst + 40;                       // [33] their A keys
 
+  for (int i = threadIdx.x; i < HT; i += blockDim.x) {
+    hkey[i] = -1;
+    hcnt[i] = 0;
+  }
+  if (threadIdx.x == 0) *cta_done = 0;
   if (lane == 0) {
     for (int s = 0; s < CF; s++) mbar_init(&bar_f[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -257,15 +266,31 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
 
   // ---- accumulators
   double aXX[2] = {0, 0}, aXL[2] = {0, 0}, a8 = 0, a9 = 0;
-  double aLL[2] = {0, 0}, aTL[2] = {0, 0}, aTT[2] = {0, 0};  // s_L⊗s_L per row (t = [s_L8, s_L9, 1, 0..])
   double aRA[3][2] = {{0, 0}, {0, 0}, {0, 0}}, r8[3] = {0, 0, 0}, r9[3] = {0, 0, 0};
   double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;
   double C0 = 0, C1 = 0, C2 = 0;  // this lane's rows of the open level-A run (since its last fold)
   bool openB = false;
   int curB = 0;
-  int prevA = -1, prevB = -1;
+  int prevL = -1, prevA = -1, prevB = -1;
   const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
+  auto hl_add = [&](int key, unsigned len) {
+    unsigned h = ((unsigned)key * 2654435761u) >> (32 - 10);
+#pragma unroll 1
+    for (int probe = 0; probe < 2; probe++) {
+      int t = hkey[h];
+      if (t == -1) {
+        const int old = atomicCAS(&hkey[h], -1, key);
+        t = old == -1 ? key : old;
+      }
+      if (t == key) {
+        atomicAdd(&hcnt[h], len);
+        return;
+      }
+      h = (h + 1) & (HT - 1);
+    }
+    atomicAdd(&g.HL[key], len);
+  };
   auto push_B = [&](int keyB) {
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
     int slot = 0;
@@ -311,7 +336,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       if (has_next) mbar_wait(&bar_f[fs1], (uint32_t)fph1);
       issue_gather(cn, fs1, (blk + 1) & 1);
     }
-    if (cc.b == 0) prevA = prevB = -1;  // a new item: row 0 starts runs at every level
+    if (cc.b == 0) prevL = prevA = prevB = -1;  // a new item: row 0 starts runs at every level
     cp_wait1();
     __syncwarp();
     if (g.ablate & 16) {
@@ -330,16 +355,20 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     const int rleft = cc.rows - cc.b * 32;
     const int nv = rleft < 32 ? rleft : 32;
     const bool vr = lane < nv;
+    const int kl = vr ? ks[lane] : -1;
     const int ka = vr ? (NS >= 1 ? ks[32 + lane] : 0) : -1;
     const int kb = vr ? (NS == 2 ? ks[64 + lane] : 0) : -1;
-    int pa = __shfl_up_sync(FULL, ka, 1), pb = __shfl_up_sync(FULL, kb, 1);
+    int pl = __shfl_up_sync(FULL, kl, 1), pa = __shfl_up_sync(FULL, ka, 1), pb = __shfl_up_sync(FULL, kb, 1);
     if (lane == 0) {
+      pl = prevL;
       pa = prevA;
       pb = prevB;
     }
     const bool dB = vr && kb != pb;
     const bool dA = vr && (dB || ka != pa);
-    const unsigned mB = __ballot_sync(FULL, dB), mA = __ballot_sync(FULL, dA);
+    const bool lead = vr && (dA || kl != pl || lane == 0);
+    const unsigned mB = __ballot_sync(FULL, dB), mA = __ballot_sync(FULL, dA), mLd = __ballot_sync(FULL, lead);
+    prevL = __shfl_sync(FULL, kl, nv - 1);
     prevA = __shfl_sync(FULL, ka, nv - 1);
     prevB = __shfl_sync(FULL, kb, nv - 1);
     // does the run open at this block's end end here? (the next block is another item, or
@@ -350,6 +379,11 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       const int na = NS >= 1 ? kn[32] : 0, nb2 = NS == 2 ? kn[64] : 0;
       endB = nb2 != prevB;
       endA = endB || na != prevA;
+    }
+    if (lead && !(g.ablate & 8)) {
+      const unsigned above = mLd & ~((2u << lane) - 1u);
+      const int end = above ? __ffs(above) - 1 : nv;
+      hl_add(kl, (unsigned)(end - lane));
     }
     if (mB & 1u) {  // a level-B run starts at row 0
       openB = true;
@@ -368,9 +402,6 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        dmma(aLL, sv, sv);
-        dmma(aTL, tv, sv);
-        dmma(aTT, tv, tv);
         a8 = fma(xa, s89.x, a8);
         a9 = fma(xa, s89.y, a9);
         C0 += xa;
@@ -472,9 +503,6 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        dmma(aLL, sv, sv);
-        dmma(aTL, tv, sv);
-        dmma(aTT, tv, tv);
         a8 = fma(xa, s89.x, a8);
         a9 = fma(xa, s89.y, a9);
         const int slast = __popc(mAx & ((2u << (4 * j + 3)) - 1u));
@@ -551,21 +579,17 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       out[144 + (8 * t + m) * 10 + 9] = r9[t];
     }
   }
-  // LL[10][10] = Σ s_L s_L^T: rows 0..7 from aLL, rows 8/9 (s_L8, s_L9 against s_L0..7) from
-  // aTL, the (8|9)x(8|9) block from aTT; columns 8/9 of rows 0..7 are read by symmetry
-  out[384 + m * 10 + 2 * k] = aLL[0];
-  out[384 + m * 10 + 2 * k + 1] = aLL[1];
-  if (m < 2) {
-    out[384 + (8 + m) * 10 + 2 * k] = aTL[0];
-    out[384 + (8 + m) * 10 + 2 * k + 1] = aTL[1];
-    if (k == 0) {
-      out[384 + (8 + m) * 10 + 8] = aTT[0];
-      out[384 + (8 + m) * 10 + 9] = aTT[1];
+  // ---- the CTA's last warp to finish moves the H_L table to global
+  __threadfence_block();
+  int ticket = 0;
+  if (lane == 0) ticket = atomicAdd(cta_done, 1);
+  ticket = __shfl_sync(FULL, ticket, 0);
+  if (ticket == W - 1) {
+    __threadfence_block();
+    for (int i = lane; i < HT; i += 32) {
+      const int key = hkey[i];
+      if (key != -1 && hcnt[i]) atomicAdd(&g.HL[key], hcnt[i]);
     }
-  }
-  if (k == 0) {  // columns 8/9 of rows 0..7: read through rows 8/9 (symmetry), kept zero here
-    out[384 + m * 10 + 8] = 0.0;
-    out[384 + m * 10 + 9] = 0.0;
   }
 }
 
@@ -733,7 +757,7 @@ struct FastCov : FastPaths {
   std::vector<int> fattrs;
   CovLevel L, A, B;
   DevBuf zeros;  // one zero view row (absent levels)
-  DevBuf zbuf;   // [work | bcount | pad] [HA], cleared every run
+  DevBuf zbuf;   // [work | bcount | pad] [HA] [HL], cleared every run
   size_t off_HA = 0, off_HL = 0, zbytes = 0;
   DevBuf brec, partials, finp, src, toff, tidx, tcoef;
   DevBuf scan;  // scan layout of the root (k_cov_layout), built at plan time
@@ -755,8 +779,7 @@ struct FastCov : FastPaths {
 
 int cov_warps() {  // LMFAO_COV_W (diagnostics): 12 or 16 warps per CTA
   const char* e = std::getenv("LMFAO_COV_W");
-  if (e && (std::atoi(e) == 12 || std::atoi(e) == 16)) return std::atoi(e);
-  return COV_W;
+  return e && std::atoi(e) == 12 ? 12 : COV_W;
 }
 
 template <int W>
@@ -776,7 +799,7 @@ cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
   return go(k_cov<2, W>);
 }
 cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
-  return cov_warps() == 16 ? launch_cov_w<16>(NS, g, grid, st) : launch_cov_w<12>(NS, g, grid, st);
+  return cov_warps() == 12 ? launch_cov_w<12>(NS, g, grid, st) : launch_cov_w<16>(NS, g, grid, st);
 }
 
 }  // namespace
@@ -810,6 +833,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   g.work = reinterpret_cast<int*>(z);
   g.bcount = reinterpret_cast<int*>(z + 4);
   g.HA = reinterpret_cast<unsigned*>(z + off_HA);
+  g.HL = reinterpret_cast<unsigned*>(z + off_HL);
   {
     const char* ab = std::getenv("LMFAO_COV_ABLATE");
     g.ablate = ab ? std::atoi(ab) : 0;
@@ -827,9 +851,9 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.bcount = g.bcount;
   f.bcap = bcap;
   f.VB = NS == 2 ? B.V.as<double>() : zeros.as<double>();
-  f.HL = nullptr;
+  f.HL = g.HL;
   f.VL = L.V.as<double>();
-  f.nkL = 0;  // s_L⊗s_L comes from the scan (LL block)
+  f.nkL = L.nk;
   f.HA = g.HA;
   f.VA = g.VA;
   f.nkA = NS >= 1 ? A.nk : 0;
@@ -936,7 +960,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   const int64_t nkA = fc->NS >= 1 ? fc->A.nk : 0;
   fc->off_HA = 16;
   fc->off_HL = (fc->off_HA + (size_t)nkA * 4 + 15) / 16 * 16;
-  fc->zbytes = fc->off_HL;
+  fc->zbytes = fc->off_HL + (size_t)std::max<int64_t>(fc->L.nk, 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
   fc->nblk = (R.nrows + 31) / 32;
   const int64_t nitems = (fc->nblk + IB - 1) / IB;
@@ -1005,8 +1029,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
       case 7: return 64 + i * 10 + j;          // x·s_L
       case 8: return 144 + i * 10 + j;         // x·s_A
       case 9: return RBM + i * 16 + j;         // x·s_B
-      case 12: return i < 8 && j < 8 ? 384 + i * 10 + j   // s_L·s_L (LL block of the scan)
-                                     : 384 + std::max(i, j) * 10 + std::min(i, j);
+      case 12: return MLM + i * 16 + j;        // s_L·s_L
       case 13: return 144 + (8 + i) * 10 + j;  // s_L·s_A
       case 14: return RBM + (8 + i) * 16 + j;  // s_L·s_B
       case 18: return MAM + i * 16 + j;        // s_A·s_A
