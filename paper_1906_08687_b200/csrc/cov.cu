@@ -43,7 +43,7 @@ constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows p
 constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][10]
 constexpr int BRW = 36;      // doubles per B record
 constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
-constexpr int FIN_BLOCKS = 148;
+constexpr int FIN_BLOCKS = 296;
 constexpr unsigned FULL = 0xffffffffu;
 
 static_assert(SBLK % 128 == 0 && STG_G % 128 == 0, "TMA / cp.async alignment");
@@ -58,7 +58,7 @@ struct CovArgs {
   double* brec;
   int* bcount;
   int bcap;
-  double* partials;  // [grid][NPART]
+  double* partials;  // [grid * W][NPART] per-warp partials
   int* work;
   int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L,
                // 16 no compute at all (pipeline only), 32 every block on the fast path
@@ -602,22 +602,18 @@ struct DimTables {
   double* V[3];
 };
 __global__ void k_cov_dims(DimTables d) {
-  const int64_t tot0 = d.nk[0] * GP, tot1 = d.nk[1] * GP, tot2 = d.nk[2] * GP;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot0 + tot1 + tot2;
+  const int64_t n0 = d.nk[0], n1 = d.nk[1], n2 = d.nk[2];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1 + n2;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int l = 0;
-    int64_t e = i;
-    if (e >= tot0) {
-      e -= tot0;
-      l = 1;
-      if (e >= tot1) {
-        e -= tot1;
-        l = 2;
-      }
-    }
-    const int64_t kk = e / GP;
-    const int f = (int)(e % GP);
-    d.V[l][e] = f < d.n[l] ? d.cols[l][f][kk] : (f == 10 ? 1.0 : 0.0);
+    const int l = i < n0 ? 0 : (i < n0 + n1 ? 1 : 2);
+    const int64_t kk = i - (l == 0 ? 0 : (l == 1 ? n0 : n0 + n1));
+    const int n = d.n[l];
+    double v[GP];
+#pragma unroll
+    for (int f = 0; f < GP; f++) v[f] = f < n ? d.cols[l][f][kk] : (f == 10 ? 1.0 : 0.0);
+    double2* out = reinterpret_cast<double2*>(d.V[l] + kk * GP);
+#pragma unroll
+    for (int f = 0; f < GP / 2; f++) out[f] = make_double2(v[2 * f], v[2 * f + 1]);
   }
 }
 
@@ -650,16 +646,23 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
   };
   auto moments = [&](const unsigned* H, const double* V, int64_t nk, double (&acc)[4][2]) {
     const int64_t ng = (nk + 3) / 4, g0 = gw * ng / GW, g1 = (gw + 1) * ng / GW;
-    for (int64_t gi = g0; gi < g1; gi++) {
-      const int64_t kk = gi * 4 + k;
-      const bool v = kk < nk;
-      const double h = v ? (double)H[kk] : 0.0;
-      double s0, s1;
-      srow(V, v ? kk : 0, v, s0, s1);
-      dmma(acc[0], h * s0, s0);
-      dmma(acc[1], h * s0, s1);
-      dmma(acc[2], h * s1, s0);
-      dmma(acc[3], h * s1, s1);
+    constexpr int U = 4;  // groups whose loads are in flight together
+    for (int64_t gb = g0; gb < g1; gb += U) {
+      double h[U], s0[U], s1[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t kk = (gb + u) * 4 + k;
+        const bool v = gb + u < g1 && kk < nk;
+        h[u] = v ? (double)H[kk] : 0.0;
+        srow(V, v ? kk : 0, v, s0[u], s1[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        dmma(acc[0], h[u] * s0[u], s0[u]);
+        dmma(acc[1], h[u] * s0[u], s1[u]);
+        dmma(acc[2], h[u] * s1[u], s0[u]);
+        dmma(acc[3], h[u] * s1[u], s1[u]);
+      }
     }
   };
   moments(a.HL, a.VL, a.nkL, mL);
@@ -713,24 +716,28 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
   for (int i = threadIdx.x; i < NFIN; i += blockDim.x) a.partials[(size_t)blockIdx.x * NFIN + i] = red[i];
 }
 
-// src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  One CTA per
-// output element, fixed-order strided sums and tree (deterministic).
-__global__ void __launch_bounds__(256) k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2,
-                                                 int n2, double* __restrict__ src) {
-  const int e = blockIdx.x;
-  const bool first = e < NPART;
-  const double* p = first ? p1 + e : p2 + (e - NPART);
-  const int n = first ? n1 : n2, stride = first ? NPART : NFIN;
+// src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  A CTA per 32
+// consecutive outputs: lane = output (coalesced rows), warp r of 32 sums rows r, r + 32, ...;
+// then a fixed-order sum over the warps (deterministic).
+__global__ void __launch_bounds__(1024) k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2,
+                                                  int n2, double* __restrict__ src) {
+  const int e = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5;
   double s = 0.0;
-  for (int b = threadIdx.x; b < n; b += blockDim.x) s += p[(size_t)b * stride];
-  __shared__ double red[256];
-  red[threadIdx.x] = s;
-  __syncthreads();
-  for (int h = 128; h > 0; h >>= 1) {
-    if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
-    __syncthreads();
+  if (e < NPART) {
+#pragma unroll 4
+    for (int b = r; b < n1; b += 32) s += p1[(size_t)b * NPART + e];
+  } else if (e < NPART + NFIN) {
+#pragma unroll 4
+    for (int b = r; b < n2; b += 32) s += p2[(size_t)b * NFIN + e - NPART];
   }
-  if (threadIdx.x == 0) src[e] = red[0];
+  __shared__ double red[32][33];
+  red[r][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (r == 0 && e < NPART + NFIN) {
+    double t = 0.0;
+    for (int i = 0; i < 32; i++) t += red[i][threadIdx.x];
+    src[e] = t;
+  }
 }
 
 __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __restrict__ toff,
@@ -819,7 +826,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
       tot += d.nk[i] * GP;
     }
     if (tot > 0) {
-      k_cov_dims<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(d);
+      k_cov_dims<<<(unsigned)std::min<int64_t>((tot / GP + 255) / 256, 148 * 16), 256, 0, st>>>(d);
       launches_add(1);
     }
   }
@@ -859,8 +866,8 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
   k_cov_fin<<<FIN_BLOCKS, 256, 0, st>>>(f);
-  k_cov_sum<<<NPART + NFIN, 256, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(), FIN_BLOCKS,
-                                          src.as<double>());
+  k_cov_sum<<<(NPART + NFIN + 31) / 32, 1024, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(),
+                                                      FIN_BLOCKS, src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                          tcoef.as<double>(), nout, c->scalar_out.as<double>(),
                                                          NPART + 18 * 16 + 10, c->scalar_count.as<unsigned long long>());
