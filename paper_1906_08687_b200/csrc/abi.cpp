@@ -582,6 +582,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   c->query_slot.assign(c->queries.size(), 0);
   std::vector<Program> gprogs;
   c->groups.clear();
+  c->code_cache.clear();
   for (size_t q = 0; q < c->queries.size(); q++) {
     const Query& Q = c->queries[q];
     if (Q.gb.empty()) {
@@ -632,22 +633,30 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     for (size_t i = 0; i < Q.gb.size(); i++) {
       int a = Q.gb[i], o = c->owner[a];
       const Rel& r = c->rels[o];
-      DevBuf dict, codes;
-      int64_t nd = 0;
-      auto fd = r.full_dict.find(a);
-      if (fd != r.full_dict.end()) {  // sharded root: the global dictionary
-        nd = r.full_dict_n.at(a);
-        CTX_CUDA(c, dict.alloc(std::max<int64_t>(nd, 1) * 4), "plan dictionary");
-        CTX_CUDA(c, cudaMemcpyAsync(dict.p, fd->second.p, nd * 4, cudaMemcpyDeviceToDevice, st), "plan dictionary");
-        CTX_CUDA(c, codes.alloc(std::max<int64_t>(r.nrows, 1) * 4), "plan codes");
-        CTX_CUDA(c, lookup_dense(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict.as<int32_t>(), nd,
-                                 codes.as<int32_t>(), st),
-                 "plan codes");
-        CTX_CUDA(c, cudaStreamSynchronize(st), "plan codes");
-      } else {
-        CTX_CUDA(c, dict_encode_i32(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict, nd, &codes, st),
-                 "plan dictionary");
+      std::shared_ptr<CodeSet>& cs = c->code_cache[a];
+      if (!cs) {
+        cs = std::make_shared<CodeSet>();
+        DevBuf& dict = cs->dict;
+        DevBuf& codes = cs->codes;
+        int64_t& nd = cs->nd;
+        auto fd = r.full_dict.find(a);
+        if (fd != r.full_dict.end()) {  // sharded root: the global dictionary
+          nd = r.full_dict_n.at(a);
+          CTX_CUDA(c, dict.alloc(std::max<int64_t>(nd, 1) * 4), "plan dictionary");
+          CTX_CUDA(c, cudaMemcpyAsync(dict.p, fd->second.p, nd * 4, cudaMemcpyDeviceToDevice, st), "plan dictionary");
+          CTX_CUDA(c, codes.alloc(std::max<int64_t>(r.nrows, 1) * 4), "plan codes");
+          CTX_CUDA(c, lookup_dense(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict.as<int32_t>(), nd,
+                                   codes.as<int32_t>(), st),
+                   "plan codes");
+          CTX_CUDA(c, cudaStreamSynchronize(st), "plan codes");
+        } else {
+          CTX_CUDA(c, dict_encode_i32(r.cols[r.find_attr(a)].buf.as<int32_t>(), r.nrows, dict, nd, &codes, st),
+                   "plan dictionary");
+        }
       }
+      const DevBuf& dict = cs->dict;
+      const DevBuf& codes = cs->codes;
+      const int64_t nd = cs->nd;
       gp.g.code[i] = codes.as<int32_t>();
       gp.g.code_child[i] = -1;
       if (o != c->root) {
@@ -658,8 +667,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       gp.d.dict[i] = dict.as<int32_t>();
       gp.d.radix[i] = std::max<int64_t>(nd, 1);
       radix.push_back(std::max<int64_t>(nd, 1));
-      gp.dicts.push_back(std::move(dict));
-      gp.codes.push_back(std::move(codes));
+      gp.sets.push_back(cs);
     }
     int64_t cells = 1;
     for (int i = (int)radix.size() - 1; i >= 0; i--) {

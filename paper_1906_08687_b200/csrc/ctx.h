@@ -98,13 +98,20 @@ struct NodePlan {
   DevProgram prog;
 };
 
+// Dictionary (sorted distinct values) and per-row (root) or per-dense-key (child) codes of a
+// group-by attribute; shared by every query that groups by the attribute.
+struct CodeSet {
+  DevBuf dict, codes;
+  int64_t nd = 0;
+};
+
 struct GroupPlan {
   int q = -1;
   int nudaf = 0;
   int64_t ncells = 0;
   GroupArgs g{};
   DecodeArgs d{};
-  std::vector<DevBuf> dicts, codes;
+  std::vector<std::shared_ptr<CodeSet>> sets;
   DevBuf table, counts;
   DevProgram prog;
   bool compacted = false;
@@ -140,6 +147,7 @@ struct lmfao_ctx {
   DevBuf partials, cpart, scalar_out, scalar_count;
   int scalar_grid = 0;
   std::vector<GroupPlan> groups;
+  std::map<int, std::shared_ptr<CodeSet>> code_cache;  // per group-by attribute
   DevProgram group_prog;  // all group-by UDAFs (fused scan)
   DevBuf group_descs;     // GroupDesc per group-by query
   std::vector<int> query_kind;  // 0 scalar, 1 group (index into groups)

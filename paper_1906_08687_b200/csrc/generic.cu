@@ -221,9 +221,19 @@ cudaError_t launch_root_group(const NodeArgs& a, const GroupArgs& g, const int32
 // so Zipf-hot cells take one atomic per warp instead of one per row.  UDAFs that
 // are constants (SUM(c), e.g. COUNT) are not accumulated at all: the compaction
 // derives them from the counts.
-__global__ void k_groups_fused(NodeArgs a, const GroupDesc* __restrict__ descs, int nq,
+__global__ void k_groups_fused(NodeArgs a, const GroupDesc* descs, int nq,
                                const int32_t* __restrict__ prog_i, const double* __restrict__ prog_d,
                                const int32_t* __restrict__ ioff, const int32_t* __restrict__ doff) {
+  // the query descriptors live in shared memory (read for every row and query)
+  extern __shared__ __align__(16) unsigned char dsm[];
+  {
+    const int4* src = reinterpret_cast<const int4*>(descs);
+    int4* dst = reinterpret_cast<int4*>(dsm);
+    const int n16 = (int)((nq * sizeof(GroupDesc) + 15) / 16);
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+  }
+  descs = reinterpret_cast<const GroupDesc*>(dsm);
   int32_t kk[MAX_CHILD];
   const int lane = threadIdx.x & 31;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; base < a.nrows;
@@ -282,7 +292,15 @@ __global__ void k_groups_fused(NodeArgs a, const GroupDesc* __restrict__ descs, 
 cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int nq, const int32_t* prog_i,
                                 const double* prog_d, const int32_t* ioff, const int32_t* doff, cudaStream_t st) {
   if (a.nrows <= 0 || nq == 0) return cudaSuccess;
-  k_groups_fused<<<grid_rows(a.nrows, 16), 256, 0, st>>>(a, descs, nq, prog_i, prog_d, ioff, doff);
+  const size_t smem = ((size_t)nq * sizeof(GroupDesc) + 15) / 16 * 16;
+  if (smem > 48 * 1024) {
+    static size_t set = 0;
+    if (smem > set) {
+      CUDA_TRY(cudaFuncSetAttribute(k_groups_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      set = smem;
+    }
+  }
+  k_groups_fused<<<grid_rows(a.nrows, 16), 256, smem, st>>>(a, descs, nq, prog_i, prog_d, ioff, doff);
   launches_add(1);
   return cudaGetLastError();
 }
