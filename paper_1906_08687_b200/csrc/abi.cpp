@@ -704,17 +704,18 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       std::vector<double> cc(std::max(gp.nudaf, 1), std::nan(""));
       for (int j = 0; j < gp.nudaf; j++) {
         const auto& u = Q.udafs[j];
-        bool constant = u.size() == 1;
-        double coef = constant ? u[0].coeff : 0.0;
-        if (constant)
-          for (auto& f : u[0].f) {
+        // a UDAF whose products are all constants is c * COUNT, c = Σ_p coeff_p Π params
+        bool constant = true;
+        double coef = 0.0;
+        for (auto& pr : u) {
+          double v = pr.coeff;
+          for (auto& f : pr.f) {
             if (f.kind != LMFAO_F_CONST) constant = false;
-            else coef *= f.param;
+            else v *= f.param;
           }
-        if (u.empty()) {
-          constant = true;
-          coef = 0.0;
+          coef += v;
         }
+        if (!constant) coef = 0.0;
         d.countlike[j] = constant;
         if (!constant) d.nsum++;
         if (constant) cc[j] = coef;

@@ -1,0 +1,308 @@
+// counts.cu — the histogram path (§8 row (e)) for count batches: COUNT GROUP BY over at
+// most two attributes per query (§3 "Mutual information" / Chow-Liu trees
+// Q_S for S ⊆ {i, j}; BASELINE.json configs[3]).  Every UDAF of the batch is a
+// constant (SUM(c) = c · COUNT), so only the per-cell row counts of the join are needed
+// (the compaction multiplies by c).  With primary-key leaves and no dangling rows every
+// root row joins exactly one row per child, so
+//  * a query over attributes of one dimension D only is finished at the dimension:
+//    count[cell(D row k)] += H_D[k] with H_D[k] = root rows with key k ("each aggregate to
+//    its own root");
+//  * every other query (a root attribute, or attributes of two relations) is counted per
+//    root row: its cell from the codes of the row (root attributes) and of the rows it
+//    joins (dimension attributes through the foreign keys), lanes holding the same cell
+//    merged with __match_any_sync so a Zipf-hot cell takes one atomic per warp.
+// The attribute codes of a row are loaded once (not once per query).
+#include <cstdlib>
+#include <map>
+#include <set>
+
+#include "ctx.h"
+
+namespace lmfao {
+namespace {
+
+constexpr int CN_ATTR = 24;   // attributes with codes
+constexpr int CN_LEV = 8;     // root children
+constexpr unsigned CFULL = 0xffffffffu;
+
+struct CntQuery {
+  int8_t a, b;      // attribute slots (b = -1: one attribute)
+  int32_t sa;       // cell = code_a * sa + code_b
+  unsigned long long* counts;
+};
+struct CntArgs {
+  int64_t nrows;
+  int nattr, nlev, nq;
+  const int32_t* code[CN_ATTR];  // root: per row; child: per dense key
+  int8_t lev[CN_ATTR];           // -1 root, else child index (into fk)
+  const int32_t* fk[CN_LEV];
+  unsigned* H[CN_LEV];           // rows per key of the children with dimension-only queries (null: none)
+  const CntQuery* q;             // [nq] per-row queries
+  unsigned long long* total;     // COUNT
+};
+
+// Per root row: the codes of every attribute, then each per-row query's cell.
+__global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArgs a) {
+  extern __shared__ CntQuery sq[];
+  __shared__ int scode[8][CN_ATTR][32];  // this warp's codes (attribute x lane)
+  for (int i = threadIdx.x; i < a.nq; i += blockDim.x) sq[i] = a.q[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned long long tot = 0;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; base < a.nrows;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = base + (threadIdx.x & ~31) + lane;
+    const bool v = row < a.nrows;
+    tot += v ? 1 : 0;
+    int key[CN_LEV];
+#pragma unroll
+    for (int l = 0; l < CN_LEV; l++)
+      if (l < a.nlev) key[l] = v ? a.fk[l][row] : 0;
+#pragma unroll
+    for (int i = 0; i < CN_ATTR; i++) {
+      if (i >= a.nattr) break;
+      const int l = a.lev[i];
+      int kk = 0;
+#pragma unroll
+      for (int j = 0; j < CN_LEV; j++)
+        if (j == l) kk = key[j];
+      scode[wib][i][lane] = v ? (l < 0 ? a.code[i][row] : a.code[i][kk]) : 0;
+    }
+    __syncwarp();
+    // rows per key of the children that have dimension-only queries
+#pragma unroll
+    for (int l = 0; l < CN_LEV; l++) {
+      if (l >= a.nlev) break;
+      if (!a.H[l]) continue;
+      const int k = v ? key[l] : -1 - lane;
+      const unsigned peers = __match_any_sync(CFULL, k);
+      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&a.H[l][k], (unsigned)__popc(peers));
+    }
+    for (int qi = 0; qi < a.nq; qi++) {
+      const CntQuery q = sq[qi];
+      const int ca = scode[wib][q.a][lane], cb = q.b >= 0 ? scode[wib][q.b][lane] : 0;
+      const int cell = v ? ca * q.sa + cb : -1 - lane;
+      const unsigned peers = __match_any_sync(CFULL, cell);
+      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&q.counts[cell], (unsigned long long)__popc(peers));
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(CFULL, tot, o);
+  if (lane == 0 && a.total) atomicAdd(a.total, tot);
+}
+
+// Scalar queries of the batch: every UDAF is a constant c, value = c * COUNT.
+__global__ void k_cnt_scalar(const double* __restrict__ coef, int nout, const unsigned long long* __restrict__ total,
+                             double* __restrict__ out) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x)
+    out[o] = coef[o] * (double)*total;
+}
+
+// Dimension-only queries: count[cell(k)] += H[k] over the child's dense keys.
+struct CntDimQuery {
+  const int32_t* ca;
+  const int32_t* cb;  // null: one attribute
+  int32_t sa;
+  int lev;
+  unsigned long long* counts;
+};
+struct CntDimArgs {
+  int nq;
+  const CntDimQuery* q;
+  const unsigned* H[CN_LEV];
+  int64_t nk[CN_LEV];
+};
+__global__ void k_cnt_dims(const __grid_constant__ CntDimArgs a) {
+  const CntDimQuery q = a.q[blockIdx.y];
+  const unsigned* H = a.H[q.lev];
+  const int64_t nk = a.nk[q.lev];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nk; k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned h = H[k];
+    if (!h) continue;
+    const int cell = q.ca[k] * q.sa + (q.cb ? q.cb[k] : 0);
+    atomicAdd(&q.counts[cell], (unsigned long long)h);
+  }
+}
+
+struct FastCounts : FastPaths {
+  CntArgs ra{};
+  CntDimArgs da{};
+  DevBuf dq, ddq, Hbuf, scoef;
+  int nscalar = 0;
+  int64_t hwords = 0;
+  int nrowq = 0, ndimq = 0;
+  bool scalar = false;
+  std::string describe() const override {
+    char b[160];
+    std::snprintf(b, sizeof b, "{\"kind\": \"counts\", \"attrs\": %d, \"row_queries\": %d, \"dim_queries\": %d}",
+                  ra.nattr, nrowq, ndimq);
+    return b;
+  }
+  bool handles_group(int) const override { return true; }
+  bool handles_all_groups() const override { return true; }
+  bool skip_generic_views() const override { return true; }
+  int run(lmfao_ctx* c, const NodeArgs& root, cudaStream_t st, bool& scalar_done) override;
+};
+
+int FastCounts::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_done) {
+  for (auto& gp : c->groups) CUDA_TRY(cudaMemsetAsync(gp.counts.p, 0, gp.ncells * 8, st));
+  if (hwords) CUDA_TRY(cudaMemsetAsync(Hbuf.p, 0, hwords * 4, st));
+  CntArgs a = ra;
+  a.nrows = c->rels[c->root].nrows;
+  a.total = nullptr;
+  if (scalar) {
+    CUDA_TRY(cudaMemsetAsync(c->scalar_count.p, 0, 8, st));
+    a.total = c->scalar_count.as<unsigned long long>();
+  }
+  scan_timer_begin(c, st);
+  if (a.nrows > 0) {
+    k_cnt_rows<<<148 * 8, 256, std::max<size_t>((size_t)nrowq * sizeof(CntQuery), 16), st>>>(a);
+    launches_add(1);
+  }
+  scan_timer_end(c, st);
+  if (ndimq > 0) {
+    k_cnt_dims<<<dim3(64, (unsigned)ndimq), 256, 0, st>>>(da);
+    launches_add(1);
+  }
+  if (scalar) {  // every scalar UDAF is a constant c: value = c * COUNT
+    k_cnt_scalar<<<(nscalar + 127) / 128 + 1, 128, 0, st>>>(scoef.as<double>(), nscalar,
+                                                           c->scalar_count.as<unsigned long long>(),
+                                                           c->scalar_out.as<double>());
+    launches_add(1);
+    scalar_done = true;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Planner hook: every UDAF of every query is a constant (SUM(c)), every group-by query has
+// one or two attributes, scalar queries only count, and the root's children are
+// primary-key leaves.  Otherwise nullptr.
+FastPaths* plan_counts(lmfao_ctx* c) {
+  if (c->groups.empty()) return nullptr;
+  const Rel& R = c->rels[c->root];
+  if (R.children.size() > (size_t)CN_LEV) return nullptr;
+  for (int ch : R.children)
+    if (!c->rels[ch].children.empty() || !c->rels[ch].unique_key) return nullptr;
+  auto constant_udaf = [](const std::vector<QProduct>& u) {
+    for (auto& p : u)
+      for (auto& f : p.f)
+        if (f.kind != LMFAO_F_CONST) return false;
+    return true;
+  };
+  for (auto& Q : c->queries)
+    for (auto& u : Q.udafs)
+      if (!constant_udaf(u)) return nullptr;
+  auto level_of = [&](int attr) -> int {
+    const int o = c->owner[attr];
+    if (o == c->root) return -1;
+    for (size_t j = 0; j < R.children.size(); j++)
+      if (R.children[j] == o) return (int)j;
+    return -2;
+  };
+  std::unique_ptr<FastCounts> fc(new FastCounts());
+  CntArgs& a = fc->ra;
+  a.nlev = (int)R.children.size();
+  for (int j = 0; j < a.nlev; j++) a.fk[j] = R.fk_dense[j].as<int32_t>();
+  std::map<int, int> slot;  // attr -> code slot
+  std::vector<CntQuery> rq;
+  std::vector<CntDimQuery> dq;
+  std::vector<int> needH(a.nlev, 0);
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    GroupPlan& gp = c->groups[gi];
+    const Query& Q = c->queries[gp.q];
+    if (Q.gb.empty() || Q.gb.size() > 2) return nullptr;
+    int lv[2] = {0, 0};
+    for (size_t i = 0; i < Q.gb.size(); i++) {
+      lv[i] = level_of(Q.gb[i]);
+      if (lv[i] == -2) return nullptr;
+    }
+    if (gp.ncells > INT32_MAX) return nullptr;
+    const bool dim_only = lv[0] >= 0 && (Q.gb.size() == 1 || lv[1] == lv[0]);
+    if (dim_only) {
+      CntDimQuery d{};
+      d.ca = gp.g.code[0];
+      d.cb = Q.gb.size() == 2 ? gp.g.code[1] : nullptr;
+      d.sa = (int32_t)gp.g.stride[0];
+      d.lev = lv[0];
+      d.counts = gp.counts.as<unsigned long long>();
+      dq.push_back(d);
+      needH[lv[0]] = 1;
+      continue;
+    }
+    CntQuery q{};
+    for (size_t i = 0; i < Q.gb.size(); i++) {
+      auto it = slot.find(Q.gb[i]);
+      if (it == slot.end()) {
+        if ((int)slot.size() == CN_ATTR) return nullptr;
+        const int s = (int)slot.size();
+        slot[Q.gb[i]] = s;
+        a.code[s] = gp.g.code[i];
+        a.lev[s] = (int8_t)lv[i];
+        it = slot.find(Q.gb[i]);
+      }
+      if (i == 0) q.a = (int8_t)it->second;
+      else q.b = (int8_t)it->second;
+    }
+    if (Q.gb.size() == 1) q.b = -1;
+    q.sa = (int32_t)gp.g.stride[0];
+    q.counts = gp.counts.as<unsigned long long>();
+    rq.push_back(q);
+  }
+  a.nattr = (int)slot.size();
+  a.nq = (int)rq.size();
+  fc->nrowq = (int)rq.size();
+  fc->ndimq = (int)dq.size();
+  // H buffers
+  int64_t off = 0;
+  std::vector<int64_t> hoff(a.nlev, -1);
+  for (int j = 0; j < a.nlev; j++)
+    if (needH[j]) {
+      hoff[j] = off;
+      off += std::max<int64_t>(c->rels[R.children[j]].nkeys, 1);
+    }
+  fc->hwords = off;
+  if (fc->Hbuf.alloc(std::max<int64_t>(off, 1) * 4)) return nullptr;
+  for (int j = 0; j < a.nlev; j++) {
+    a.H[j] = hoff[j] >= 0 ? fc->Hbuf.as<unsigned>() + hoff[j] : nullptr;
+    fc->da.H[j] = a.H[j];
+    fc->da.nk[j] = c->rels[R.children[j]].nkeys;
+  }
+  // scalar outputs (constants times COUNT), in the order of the scalar program
+  std::vector<double> sc;
+  for (int qi : c->scalar_queries)
+    for (auto& u : c->queries[qi].udafs) {
+      double cf = 0.0;
+      for (auto& p : u) {
+        double v = p.coeff;
+        for (auto& f : p.f) v *= f.param;
+        cf += v;
+      }
+      sc.push_back(cf);
+    }
+  fc->scalar = !c->scalar_queries.empty();
+  fc->nscalar = (int)sc.size();
+  cudaStream_t st = c->stream;
+  if (fc->scoef.alloc(std::max<size_t>(sc.size(), 1) * 8)) return nullptr;
+  if (!sc.empty() && cudaMemcpyAsync(fc->scoef.p, sc.data(), sc.size() * 8, cudaMemcpyHostToDevice, st)) return nullptr;
+  if (fc->dq.alloc(std::max<size_t>(rq.size(), 1) * sizeof(CntQuery)) ||
+      fc->ddq.alloc(std::max<size_t>(dq.size(), 1) * sizeof(CntDimQuery)))
+    return nullptr;
+  if (!rq.empty() && cudaMemcpyAsync(fc->dq.p, rq.data(), rq.size() * sizeof(CntQuery), cudaMemcpyHostToDevice, st))
+    return nullptr;
+  if (!dq.empty() &&
+      cudaMemcpyAsync(fc->ddq.p, dq.data(), dq.size() * sizeof(CntDimQuery), cudaMemcpyHostToDevice, st))
+    return nullptr;
+  a.q = fc->dq.as<CntQuery>();
+  fc->da.nq = (int)dq.size();
+  fc->da.q = fc->ddq.as<CntDimQuery>();
+  if (cudaStreamSynchronize(st)) return nullptr;
+  if ((size_t)rq.size() * sizeof(CntQuery) > 48 * 1024 &&
+      cudaFuncSetAttribute(k_cnt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(rq.size() * sizeof(CntQuery))))
+    return nullptr;
+  return fc.release();
+}
+
+}  // namespace lmfao

@@ -11,6 +11,7 @@ FastPaths* plan_fast_paths(lmfao_ctx* c) {
   const char* ng = std::getenv("LMFAO_NO_COV");  // tests: force the gram.cu kernel
   if (!(ng && ng[0] == '1'))
     if (FastPaths* f = plan_cov(c)) return f;
+  if (FastPaths* f = plan_counts(c)) return f;
   if (FastPaths* f = plan_rt(c)) return f;
   if (FastPaths* f = plan_gram(c)) return f;
   return nullptr;

@@ -25,4 +25,5 @@ FastPaths* plan_fast_paths(lmfao_ctx* c);
 FastPaths* plan_gram(lmfao_ctx* c);
 FastPaths* plan_cov(lmfao_ctx* c);
 FastPaths* plan_rt(lmfao_ctx* c);
+FastPaths* plan_counts(lmfao_ctx* c);
 }  // namespace lmfao
