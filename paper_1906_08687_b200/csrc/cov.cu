@@ -61,7 +61,7 @@ struct CovArgs {
   double* partials;  // [grid * W][NPART] per-warp partials
   int* work;
   int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L,
-               // 16 no compute at all (pipeline only), 32 every block on the fast path
+               // 16 no compute at all (pipeline only), 32 every block on the fast path, 64 no wait for gathers
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       issue_gather(cn, fs1, (blk + 1) & 1);
     }
     if (cc.b == 0) prevL = prevA = prevB = -1;  // a new item: row 0 starts runs at every level
-    cp_wait1();
+    if (!(g.ablate & 64)) cp_wait1();
     __syncwarp();
     if (g.ablate & 16) {
       issue_fact(cf, fs);
