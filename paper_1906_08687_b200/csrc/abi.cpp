@@ -46,45 +46,40 @@ lmfao_status cuda_fail(lmfao_ctx* c, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
   } while (0)
 
-// gather every column of relation r (and its fk_dense / dense_key) by `perm` of length n
+// gather every column of relation r (and its fk_dense / dense_key) by `perm` of length n;
+// all gathers are queued, then one synchronisation releases the old buffers
 cudaError_t permute_rel(Rel& r, const uint32_t* perm, int64_t n, cudaStream_t st) {
-  for (auto& c : r.cols) {
+  std::vector<DevBuf> old;
+  auto regather = [&](DevBuf& b, int es) -> cudaError_t {
     DevBuf nb;
-    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * (c.dt == LMFAO_FP64 ? 8 : 4)));
-    CUDA_TRY(gather_bytes(c.buf.p, perm, nb.p, n, c.dt == LMFAO_FP64 ? 8 : 4, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    c.buf = std::move(nb);
-  }
-  for (auto& f : r.fk_dense) {
-    DevBuf nb;
-    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * 4));
-    CUDA_TRY(gather_bytes(f.p, perm, nb.p, n, 4, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    f = std::move(nb);
-  }
-  if (r.dense_key.p) {
-    DevBuf nb;
-    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * 4));
-    CUDA_TRY(gather_bytes(r.dense_key.p, perm, nb.p, n, 4, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    r.dense_key = std::move(nb);
-  }
+    CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * es));
+    CUDA_TRY(gather_bytes(b.p, perm, nb.p, n, es, st));
+    old.push_back(std::move(b));
+    b = std::move(nb);
+    return cudaSuccess;
+  };
+  for (auto& c : r.cols) CUDA_TRY(regather(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  for (auto& f : r.fk_dense) CUDA_TRY(regather(f, 4));
+  if (r.dense_key.p) CUDA_TRY(regather(r.dense_key, 4));
+  CUDA_TRY(cudaStreamSynchronize(st));
   r.nrows = n;
   return cudaSuccess;
 }
 
 cudaError_t slice_rel(Rel& r, int64_t lo, int64_t hi, cudaStream_t st) {
   int64_t n = hi - lo;
+  std::vector<DevBuf> old;
   auto cut = [&](DevBuf& b, int es) -> cudaError_t {
     DevBuf nb;
     CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * es));
     if (n > 0) CUDA_TRY(cudaMemcpyAsync(nb.p, (char*)b.p + lo * es, n * es, cudaMemcpyDeviceToDevice, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
+    old.push_back(std::move(b));
     b = std::move(nb);
     return cudaSuccess;
   };
   for (auto& c : r.cols) CUDA_TRY(cut(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
   for (auto& f : r.fk_dense) CUDA_TRY(cut(f, 4));
+  CUDA_TRY(cudaStreamSynchronize(st));
   r.nrows = n;
   return cudaSuccess;
 }

@@ -132,24 +132,54 @@ __global__ void k_scan_add(T* __restrict__ out, int64_t n, const T* __restrict__
     if (base + i < n) out[base + i] += add;
 }
 
+// Load-time scratch (sort / scan temporaries): grow-only per thread and device, reused in
+// stream order, so the sort passes need no allocation or synchronisation of their own.
+struct Arena {
+  int dev = -1;
+  DevBuf buf[6];
+  void* get(int i, size_t bytes) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d != dev) {
+      for (auto& b : buf) b.reset();
+      dev = d;
+    }
+    if (buf[i].bytes < bytes + 256 && buf[i].alloc(bytes + bytes / 4)) return nullptr;
+    return buf[i].p;
+  }
+};
+static thread_local Arena g_arena;
+
 template <typename T>
-cudaError_t exclusive_scan_t(const T* in, T* out, int64_t n, cudaStream_t st) {
+size_t scan_scratch_elems(int64_t n) {  // sums + offs of every recursion level
+  size_t tot = 0;
+  for (int64_t t = (n + SCAN_TILE - 1) / SCAN_TILE; t > 1; t = (t + SCAN_TILE - 1) / SCAN_TILE) tot += 2 * t;
+  return tot;
+}
+
+template <typename T>
+cudaError_t exclusive_scan_rec(const T* in, T* out, int64_t n, T* scratch, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles == 1) {
     k_scan_tiles<T><<<1, SCAN_THREADS, 0, st>>>(in, out, n, nullptr);
     return cudaGetLastError();
   }
-  DevBuf sums, offs;
-  CUDA_TRY(sums.alloc(tiles * sizeof(T)));
-  CUDA_TRY(offs.alloc(tiles * sizeof(T)));
-  k_scan_tiles<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums.as<T>());
+  T* sums = scratch;
+  T* offs = scratch + tiles;
+  k_scan_tiles<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(exclusive_scan_t<T>(sums.as<T>(), offs.as<T>(), tiles, st));
-  k_scan_add<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(out, n, offs.as<T>());
-  CUDA_TRY(cudaGetLastError());
-  // sums/offs freed at scope exit: make sure the stream is done with them
-  return cudaStreamSynchronize(st);
+  CUDA_TRY(exclusive_scan_rec<T>(sums, offs, tiles, scratch + 2 * tiles, st));
+  k_scan_add<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(out, n, offs);
+  return cudaGetLastError();
+}
+
+// stream-ordered: the scratch lives in the arena slot `slot`
+template <typename T>
+cudaError_t exclusive_scan_t(const T* in, T* out, int64_t n, cudaStream_t st, int slot = 5) {
+  T* scratch = (T*)g_arena.get(slot, std::max<size_t>(scan_scratch_elems<T>(n), 1) * sizeof(T));
+  if (!scratch) return cudaErrorMemoryAllocation;
+  return exclusive_scan_rec<T>(in, out, n, scratch, st);
 }
 
 cudaError_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t st) {
@@ -162,20 +192,19 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaS
 cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st) {
   if (n <= 1 || key_bits <= 0) return cudaSuccess;
   int64_t nblocks = (n + SORT_TILE - 1) / SORT_TILE;
-  DevBuf k2, v2, hist, offs;
-  CUDA_TRY(k2.alloc(n * 4));
-  CUDA_TRY(v2.alloc(n * 4));
-  CUDA_TRY(hist.alloc(256 * nblocks * 4));
-  CUDA_TRY(offs.alloc(256 * nblocks * 4));
-  uint32_t *ka = keys, *va = vals, *kb = k2.as<uint32_t>(), *vb = v2.as<uint32_t>();
+  uint32_t* k2 = (uint32_t*)g_arena.get(0, n * 4);
+  uint32_t* v2 = (uint32_t*)g_arena.get(1, n * 4);
+  uint32_t* hist = (uint32_t*)g_arena.get(2, 256 * nblocks * 4);
+  uint32_t* offs = (uint32_t*)g_arena.get(3, 256 * nblocks * 4);
+  if (!k2 || !v2 || !hist || !offs) return cudaErrorMemoryAllocation;
+  uint32_t *ka = keys, *va = vals, *kb = k2, *vb = v2;
   int passes = 0;
   for (int shift = 0; shift < key_bits; shift += 8) {
     int bits = std::min(8, key_bits - shift);
-    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, shift, bits, hist.as<uint32_t>(), (int)nblocks);
+    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, shift, bits, hist, (int)nblocks);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(exclusive_scan_u32(hist.as<uint32_t>(), offs.as<uint32_t>(), (int64_t)(1 << bits) * nblocks, st));
-    k_radix_scatter<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, va, kb, vb, n, shift, bits, offs.as<uint32_t>(),
-                                                                 (int)nblocks);
+    CUDA_TRY(exclusive_scan_t<uint32_t>(hist, offs, (int64_t)(1 << bits) * nblocks, st, 4));
+    k_radix_scatter<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, va, kb, vb, n, shift, bits, offs, (int)nblocks);
     CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb);
     std::swap(va, vb);
@@ -185,7 +214,7 @@ cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_
     CUDA_TRY(cudaMemcpyAsync(keys, ka, n * 4, cudaMemcpyDeviceToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(vals, va, n * 4, cudaMemcpyDeviceToDevice, st));
   }
-  return cudaStreamSynchronize(st);
+  return cudaSuccess;  // stream-ordered; callers synchronise before reading results on the host
 }
 
 // ---------------------------------------------------------------- small kernels
