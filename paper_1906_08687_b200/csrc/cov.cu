@@ -970,8 +970,11 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   fc->zbytes = fc->off_HL + (size_t)std::max<int64_t>(fc->L.nk, 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
   fc->nblk = (R.nrows + 31) / 32;
-  const int64_t nitems = (fc->nblk + IB - 1) / IB;
-  fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + 2 * nitems + 64, INT32_MAX / BRW);
+  // work items as k_cov defines them: IB-block items, then 2-block items for the last ~10 %
+  const int64_t nbig = fc->nblk * 9 / 10 / IB;
+  const int64_t nitems = nbig + (fc->nblk - nbig * IB + 1) / 2;
+  // level-B records: one per (B run, item) pair <= B runs + items
+  fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + nitems + 64, INT32_MAX / BRW);
   if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
   if (fc->partials.alloc((size_t)fc->grid * 16 * NPART * 8)) return nullptr;  // one partial per warp
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
