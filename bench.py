@@ -274,17 +274,31 @@ def main():
         h2d = sum(t.numel() * t.element_size() for d in pinned.values() for t in d.values())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         times = []
+        phases = {k: [] for k in ("create", "add_relation", "prepare", "plan", "run", "fetch")}
         for i in range(args.e2e_steps + 1):
             barrier()
-            t0 = time.perf_counter()
+            t = [time.perf_counter()]
             e = new_engine()
-            lmfao.load(e, w.db, w.batch, columns=pinned)
+            t.append(time.perf_counter())
+            for r in w.db.relations:
+                e.add_relation(r.name, pinned[r.name])
+            t.append(time.perf_counter())
+            e.set_join_tree(w.db.root, list(w.db.edges))
+            e.prepare()
+            t.append(time.perf_counter())
+            qids_e = [e.add_query(list(q.groupby), list(q.udafs)) for q in w.batch]
             e.plan()
+            t.append(time.perf_counter())
             e.run(sptr)
-            k, v, c = e.fetch(0)
+            torch.cuda.current_stream().synchronize()
+            t.append(time.perf_counter())
+            k, v, c = e.fetch(qids_e[0])
             barrier()
+            t.append(time.perf_counter())
             if i > 0:
-                times.append(time.perf_counter() - t0)
+                times.append(t[-1] - t[0])
+                for name, a, b in zip(phases, t[:-1], t[1:]):
+                    phases[name].append(1e3 * (b - a))
             e.close()
         tt = max(times) if world == 1 else None
         if world > 1:
@@ -294,7 +308,8 @@ def main():
         else:
             tt = sum(times) / len(times)
         e2e = {"value": N / tt, "unit": "rows/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(res_bytes),
-               "s_per_step": tt, "what": "add_relation from pinned host + prepare (sort) + plan + run + fetch"}
+               "s_per_step": tt, "what": "add_relation from pinned host + prepare (sort) + plan + run + fetch",
+               "phases_ms": {k: round(statistics.median(v), 2) for k, v in phases.items()}}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -1,6 +1,6 @@
 """Wall-clock phases of the end-to-end path (bench.py's e2e) on C2: add_relation from
 pinned host memory, prepare (remap + sort), add_query + plan, run, fetch.
-usage: python tools/e2e_phases.py"""
+usage: python tools/e2e_phases.py [--keep]"""
 import os
 import sys
 import time
@@ -13,6 +13,13 @@ import synth  # noqa: E402
 from paper_1906_08687_b200 import lmfao  # noqa: E402
 
 w = synth.config2()
+keep = None
+if "--keep" in sys.argv:  # like bench.py: a first engine with the same data stays alive
+    keep = lmfao.Engine()
+    lmfao.load(keep, w.db, w.batch)
+    keep.plan()
+    keep.run()
+    torch.cuda.synchronize()
 pinned = {r.name: {c: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for c, v in r.cols.items()}
           for r in w.db.relations}
 for it in range(3):
