@@ -607,6 +607,28 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     }
     CTX_CUDA(c, np.prog.upload(p, st), "plan upload view program");
     CTX_CUDA(c, np.V.alloc(std::max<int64_t>(c->rels[u].nkeys, 1) * np.slots.size() * 8), "plan alloc view");
+    {  // leaf child with slots of <= 2 identity factors: the linear view kernel
+      const Rel& r = c->rels[u];
+      bool lin = r.children.empty() && np.slots.size() <= 64;
+      for (auto& sl : np.slots) {
+        if (sl.own.size() > 2) lin = false;
+        for (auto& o : sl.own)
+          if (std::get<0>(o) != LMFAO_F_IDENT) lin = false;
+      }
+      np.linear = lin;
+      if (lin) {
+        np.lin = ViewLinArgs{};
+        np.lin.nslots = (int)np.slots.size();
+        for (size_t i = 0; i < np.slots.size(); i++) {
+          const auto& own = np.slots[i].own;
+          for (size_t f = 0; f < own.size(); f++) {
+            const Column& col = r.cols[r.find_attr(std::get<1>(own[f]))];
+            (f == 0 ? np.lin.ca[i] : np.lin.cb[i]) = col.buf.p;
+            (f == 0 ? np.lin.ia[i] : np.lin.ib[i]) = col.dt == LMFAO_INT32;
+          }
+        }
+      }
+    }
   }
   // scalar outputs
   CTX_CUDA(c, c->scalar_prog.upload(scal, st), "plan upload");
@@ -750,6 +772,12 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
     NodePlan& np = c->nodes[u];
     const Rel& r = c->rels[u];
     CTX_CUDA(c, cudaMemsetAsync(np.V.p, 0, np.V.bytes, st), "run memset view");
+    if (np.linear) {
+      ViewLinArgs la = np.lin;
+      la.nrows = r.nrows;
+      CTX_CUDA(c, launch_view_lin(la, r.dense_key.as<int32_t>(), np.V.as<double>(), st), "run view build");
+      continue;
+    }
     NodeArgs a = node_args(c, u);
     CTX_CUDA(c, launch_view_build(a, r.dense_key.as<int32_t>(), np.prog.pi.as<int32_t>(), np.prog.pd.as<double>(),
                                   np.prog.pio.as<int32_t>(), np.prog.pdo.as<int32_t>(), (int)np.slots.size(),

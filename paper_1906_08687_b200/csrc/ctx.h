@@ -96,6 +96,8 @@ struct NodePlan {
   std::map<SlotKey, int> index;
   DevBuf V;
   DevProgram prog;
+  bool linear = false;  // leaf with identity-only slots: k_view_lin
+  ViewLinArgs lin{};
 };
 
 // Dictionary (sorted distinct values) and per-row (root) or per-dense-key (child) codes of a

@@ -54,19 +54,113 @@ __device__ double eval_output(const NodeArgs& a, int64_t row, const int32_t* kk,
   return sum;
 }
 
-__global__ void k_view_build(NodeArgs a, const int32_t* __restrict__ dense_key, const int32_t* __restrict__ prog_i,
-                             const double* __restrict__ prog_d, const int32_t* __restrict__ ioff,
-                             const int32_t* __restrict__ doff, int nslots, double* __restrict__ V) {
-  int32_t kk[MAX_CHILD];
-  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    for (int c = 0; c < a.nchild; c++) kk[c] = a.fk[c][row];
-    int64_t k = dense_key[row];
+// View build (b): V[k][s] = Σ_{rows d with dense key k} slot_s(d).  The child is sorted by
+// its dense key (prepare), so a key's rows are contiguous.  Each warp takes a contiguous range
+// of 32-row blocks (lane = row) and sums every slot over the runs of equal keys with a
+// segmented warp scan; a run that reaches the end of a block is carried (per slot, in shared
+// memory) into the next block, so a Zipf-hot key with thousands of rows costs one update, not
+// one per row or per block.  Runs that start and end inside the warp's range are stored
+// plainly (no other warp has rows of their key); runs touching the range's edges are added
+// atomically.  VAL(row, slot, lane) gives a slot's value for a row (interpreted or linear).
+constexpr int VB_WARPS = 8;
+constexpr int VB_MAXSLOT = 64;
+
+template <typename Val>
+__device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __restrict__ dense_key, int nslots,
+                                              double* __restrict__ V, double* carry, Val&& val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nblk = (nrows + 31) / 32;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t b0 = nblk * gw / nw, b1 = nblk * (gw + 1) / nw;
+  const int64_t rend = min(nrows, 32 * b1);
+  bool cstart = false;  // the carried run (if any) started inside this warp's range
+  int last = b0 > 0 ? dense_key[32 * b0 - 1] : -2;  // key of the row before the current block
+  for (int s = lane; s < nslots; s += 32) carry[s] = 0.0;  // (a run entering the range starts from 0)
+  __syncwarp();
+  for (int64_t b = b0; b < b1; b++) {
+    const int64_t row = 32 * b + lane;
+    const bool v = row < rend;
+    const int key = v ? dense_key[row] : -1;
+    int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    if (lane == 0) prev = last;
+    const int next = __shfl_down_sync(0xffffffffu, key, 1);
+    const unsigned heads = __ballot_sync(0xffffffffu, v && key != prev);  // rows that start a run
+    const unsigned upto = heads & ((2u << lane) - 1u);
+    const int s0 = upto ? 31 - __clz(upto) : 0;
+    const int64_t nrem = rend - 32 * b;
+    const int nv = nrem < 32 ? (int)nrem : 32;
+    const bool lastlane = lane == nv - 1;
+    const bool tail = v && (lastlane || next != key);
+    // the block's last run goes on past this block (into this range: carry; past it: atomic)
+    const bool cont = tail && lastlane && row + 1 < nrows && dense_key[row + 1] == key;
+    const bool carry_on = cont && row + 1 < rend;
+    const bool first_seg = upto == 0;          // the run carried from the previous block
+    const bool started_in = first_seg ? cstart : true;
     for (int s = 0; s < nslots; s++) {
-      double v = eval_output(a, row, kk, prog_i + ioff[s], prog_d + doff[s]);
-      atomicAdd(&V[k * nslots + s], v);
+      double x = v ? val(row, s) : 0.0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane - d >= s0) x += u;
+      }
+      if (tail) {
+        if (first_seg) x += carry[s];
+        if (carry_on) {
+          carry[s] = x;
+        } else {
+          double* dst = &V[(int64_t)key * nslots + s];
+          if (started_in && !cont) *dst = x;  // the run lies inside this warp's range
+          else atomicAdd(dst, x);
+        }
+      }
+      __syncwarp();
     }
+    // the carried run of the next block: the last run of this one, if it goes on
+    const unsigned cm = __ballot_sync(0xffffffffu, carry_on);
+    if (cm) {
+      const unsigned up_l = __shfl_sync(0xffffffffu, upto, __ffs(cm) - 1);
+      cstart = up_l ? true : cstart;
+    } else {
+      cstart = false;
+    }
+    last = __shfl_sync(0xffffffffu, key, nv - 1);
   }
+}
+
+__global__ void __launch_bounds__(VB_WARPS * 32) k_view_build(NodeArgs a, const int32_t* __restrict__ dense_key,
+                                                              const int32_t* __restrict__ prog_i,
+                                                              const double* __restrict__ prog_d,
+                                                              const int32_t* __restrict__ ioff,
+                                                              const int32_t* __restrict__ doff, int nslots,
+                                                              double* __restrict__ V) {
+  extern __shared__ double vcarry[];  // [VB_WARPS][nslots]
+  double* carry = vcarry + (threadIdx.x >> 5) * nslots;
+  int32_t kk[MAX_CHILD];
+  int64_t krow = -1;
+  view_seg_warp(a.nrows, dense_key, nslots, V, carry, [&](int64_t row, int s) {
+    if (row != krow) {
+      for (int c = 0; c < a.nchild; c++) kk[c] = a.fk[c][row];
+      krow = row;
+    }
+    return eval_output(a, row, kk, prog_i + ioff[s], prog_d + doff[s]);
+  });
+}
+
+// Linear slots of a leaf child (every slot a product of at most two identity factors on the
+// child's own columns): the same segmented pass with the slot values read straight from the
+// columns (no interpreter).
+__global__ void __launch_bounds__(VB_WARPS * 32) k_view_lin(const __grid_constant__ ViewLinArgs a,
+                                                            const int32_t* __restrict__ dense_key,
+                                                            double* __restrict__ V) {
+  __shared__ double carry[VB_WARPS][VB_MAXSLOT];
+  auto col = [&](const void* p, int is_int, int64_t row) -> double {
+    if (!p) return 1.0;
+    return is_int ? (double)reinterpret_cast<const int32_t*>(p)[row] : reinterpret_cast<const double*>(p)[row];
+  };
+  view_seg_warp(a.nrows, dense_key, a.nslots, V, carry[threadIdx.x >> 5], [&](int64_t row, int s) {
+    return col(a.ca[s], a.ia[s], row) * col(a.cb[s], a.ib[s], row);
+  });
 }
 
 static unsigned grid_rows(int64_t n, int per_sm = 8) {
@@ -75,10 +169,27 @@ static unsigned grid_rows(int64_t n, int per_sm = 8) {
   return (unsigned)std::max<int64_t>(g, 1);
 }
 
+cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, double* V, cudaStream_t st) {
+  if (a.nrows <= 0) return cudaSuccess;
+  if (a.nslots > VB_MAXSLOT) return cudaErrorInvalidValue;
+  k_view_lin<<<grid_rows(a.nrows), VB_WARPS * 32, 0, st>>>(a, dense_key, V);
+  launches_add(1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const int32_t* prog_i, const double* prog_d,
                               const int32_t* ioff, const int32_t* doff, int nslots, double* V, cudaStream_t st) {
   if (a.nrows <= 0) return cudaSuccess;
-  k_view_build<<<grid_rows(a.nrows), 256, 0, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V);
+  const size_t smem = (size_t)VB_WARPS * std::max(nslots, 1) * 8;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    static size_t set = 0;
+    if (smem > set) {
+      CUDA_TRY(cudaFuncSetAttribute(k_view_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      set = smem;
+    }
+  }
+  k_view_build<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V);
   launches_add(1);
   return cudaGetLastError();
 }

@@ -94,6 +94,17 @@ struct Program {
   std::vector<int32_t> out_ioff, out_doff;  // start offsets per output
 };
 
+// A leaf child whose slots are products of <= 2 identity factors on its own columns
+// (ca/cb null: factor 1).
+struct ViewLinArgs {
+  int64_t nrows;
+  int nslots;
+  const void* ca[64];
+  const void* cb[64];
+  unsigned char ia[64], ib[64];
+};
+cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, double* V, cudaStream_t st);
+
 cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const int32_t* prog_i, const double* prog_d,
                               const int32_t* ioff, const int32_t* doff, int nslots, double* V, cudaStream_t st);
 
