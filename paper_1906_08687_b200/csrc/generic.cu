@@ -65,9 +65,11 @@ __device__ double eval_output(const NodeArgs& a, int64_t row, const int32_t* kk,
 constexpr int VB_WARPS = 8;
 constexpr int VB_MAXSLOT = 64;
 
+// lacc (optional, [nslots][32] per warp): lane-private sums of the carried run in blocks where
+// no run starts, so a long run costs one add per row and slot, reduced once when it ends.
 template <typename Val>
 __device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __restrict__ dense_key, int nslots,
-                                              double* __restrict__ V, double* carry, Val&& val) {
+                                              double* __restrict__ V, double* carry, double* lacc, Val&& val) {
   const int lane = threadIdx.x & 31;
   const int64_t nblk = (nrows + 31) / 32;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -77,7 +79,15 @@ __device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __re
   bool cstart = false;  // the carried run (if any) started inside this warp's range
   int last = b0 > 0 ? dense_key[32 * b0 - 1] : -2;  // key of the row before the current block
   for (int s = lane; s < nslots; s += 32) carry[s] = 0.0;  // (a run entering the range starts from 0)
+  if (lacc)
+    for (int s = 0; s < nslots; s++) lacc[s * 32 + lane] = 0.0;
+  bool ldirty = false;  // lacc holds part of the carried run
   __syncwarp();
+  auto wsum = [&](double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  };
   for (int64_t b = b0; b < b1; b++) {
     const int64_t row = 32 * b + lane;
     const bool v = row < rend;
@@ -97,6 +107,37 @@ __device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __re
     const bool carry_on = cont && row + 1 < rend;
     const bool first_seg = upto == 0;          // the run carried from the previous block
     const bool started_in = first_seg ? cstart : true;
+    if (lacc && heads == 0) {  // the carried run goes on through the block: lane-private sums
+      const bool c_on = __any_sync(0xffffffffu, carry_on), c_any = __any_sync(0xffffffffu, cont);
+      for (int s = 0; s < nslots; s++) lacc[s * 32 + lane] += v ? val(row, s) : 0.0;
+      ldirty = true;
+      if (!c_on) {  // the run ends with this block (or leaves the range): emit it
+        for (int s = 0; s < nslots; s++) {
+          const double t = wsum(lacc[s * 32 + lane]) + carry[s];
+          lacc[s * 32 + lane] = 0.0;
+          if (lane == nv - 1) {
+            double* dst = &V[(int64_t)key * nslots + s];
+            if (cstart && !c_any) *dst = t;
+            else atomicAdd(dst, t);
+            carry[s] = 0.0;
+          }
+        }
+        ldirty = false;
+        cstart = false;
+      }
+      __syncwarp();
+      last = __shfl_sync(0xffffffffu, key, nv - 1);
+      continue;
+    }
+    if (ldirty) {  // a run starts in this block: fold the lane-private sums into the carry
+      for (int s = 0; s < nslots; s++) {
+        const double t = wsum(lacc[s * 32 + lane]);
+        lacc[s * 32 + lane] = 0.0;
+        if (lane == 0) carry[s] += t;
+      }
+      ldirty = false;
+      __syncwarp();
+    }
     for (int s = 0; s < nslots; s++) {
       double x = v ? val(row, s) : 0.0;
 #pragma unroll
@@ -133,12 +174,13 @@ __global__ void __launch_bounds__(VB_WARPS * 32) k_view_build(NodeArgs a, const 
                                                               const double* __restrict__ prog_d,
                                                               const int32_t* __restrict__ ioff,
                                                               const int32_t* __restrict__ doff, int nslots,
-                                                              double* __restrict__ V) {
-  extern __shared__ double vcarry[];  // [VB_WARPS][nslots]
+                                                              double* __restrict__ V, int use_lacc) {
+  extern __shared__ double vcarry[];  // [VB_WARPS][nslots] (+ [VB_WARPS][nslots][32] lane sums)
   double* carry = vcarry + (threadIdx.x >> 5) * nslots;
+  double* lacc = use_lacc ? vcarry + VB_WARPS * nslots + (threadIdx.x >> 5) * nslots * 32 : nullptr;
   int32_t kk[MAX_CHILD];
   int64_t krow = -1;
-  view_seg_warp(a.nrows, dense_key, nslots, V, carry, [&](int64_t row, int s) {
+  view_seg_warp(a.nrows, dense_key, nslots, V, carry, lacc, [&](int64_t row, int s) {
     if (row != krow) {
       for (int c = 0; c < a.nchild; c++) kk[c] = a.fk[c][row];
       krow = row;
@@ -153,12 +195,14 @@ __global__ void __launch_bounds__(VB_WARPS * 32) k_view_build(NodeArgs a, const 
 __global__ void __launch_bounds__(VB_WARPS * 32) k_view_lin(const __grid_constant__ ViewLinArgs a,
                                                             const int32_t* __restrict__ dense_key,
                                                             double* __restrict__ V) {
-  __shared__ double carry[VB_WARPS][VB_MAXSLOT];
+  extern __shared__ double lsm[];  // [VB_WARPS][nslots] carries, [VB_WARPS][nslots][32] lane sums
+  double* carry = lsm + (threadIdx.x >> 5) * a.nslots;
+  double* lacc = lsm + VB_WARPS * a.nslots + (threadIdx.x >> 5) * a.nslots * 32;
   auto col = [&](const void* p, int is_int, int64_t row) -> double {
     if (!p) return 1.0;
     return is_int ? (double)reinterpret_cast<const int32_t*>(p)[row] : reinterpret_cast<const double*>(p)[row];
   };
-  view_seg_warp(a.nrows, dense_key, a.nslots, V, carry[threadIdx.x >> 5], [&](int64_t row, int s) {
+  view_seg_warp(a.nrows, dense_key, a.nslots, V, carry, lacc, [&](int64_t row, int s) {
     return col(a.ca[s], a.ia[s], row) * col(a.cb[s], a.ib[s], row);
   });
 }
@@ -172,7 +216,15 @@ static unsigned grid_rows(int64_t n, int per_sm = 8) {
 cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, double* V, cudaStream_t st) {
   if (a.nrows <= 0) return cudaSuccess;
   if (a.nslots > VB_MAXSLOT) return cudaErrorInvalidValue;
-  k_view_lin<<<grid_rows(a.nrows), VB_WARPS * 32, 0, st>>>(a, dense_key, V);
+  const size_t smem = (size_t)VB_WARPS * a.nslots * 8 * 33;
+  if (smem > 48 * 1024) {
+    static size_t set = 0;
+    if (smem > set) {
+      CUDA_TRY(cudaFuncSetAttribute(k_view_lin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      set = smem;
+    }
+  }
+  k_view_lin<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, V);
   launches_add(1);
   return cudaGetLastError();
 }
@@ -180,7 +232,12 @@ cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, doub
 cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const int32_t* prog_i, const double* prog_d,
                               const int32_t* ioff, const int32_t* doff, int nslots, double* V, cudaStream_t st) {
   if (a.nrows <= 0) return cudaSuccess;
-  const size_t smem = (size_t)VB_WARPS * std::max(nslots, 1) * 8;
+  size_t smem = (size_t)VB_WARPS * std::max(nslots, 1) * 8 * 33;  // carries + lane sums
+  int use_lacc = 1;
+  if (smem > 200 * 1024) {  // many slots: carries only
+    use_lacc = 0;
+    smem = (size_t)VB_WARPS * std::max(nslots, 1) * 8;
+  }
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     static size_t set = 0;
@@ -189,7 +246,8 @@ cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const
       set = smem;
     }
   }
-  k_view_build<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V);
+  k_view_build<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V,
+                                                                use_lacc);
   launches_add(1);
   return cudaGetLastError();
 }
