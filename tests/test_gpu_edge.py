@@ -1,0 +1,57 @@
+"""Degenerate inputs through every specialised path (cov.cu, gram.cu, rt.cu, counts.cu) and
+the view kernels: a root whose rows all dangle (empty join), a single-row root, dimensions
+with a single key, and a root that shrinks to one 32-row block after dropping dangling rows."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from _parity import assert_parity, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def star(n, dim_rows, dangle_all=False, seed=0, nf=3, df=(2, 3, 4)):
+    rng = np.random.default_rng(seed)
+    F, dims = {}, []
+    for r, (nr, f) in enumerate(zip(dim_rows, df), start=1):
+        keys = np.arange(nr, dtype=np.int32) * 3
+        cols = {f"k{r}": keys, f"c{r}": rng.integers(0, 4, nr).astype(np.int32)}
+        for j in range(f):
+            cols[f"d{r}_{j}"] = rng.standard_normal(nr)
+        dims.append(synth.Relation(f"D{r}", cols))
+        fk = keys[rng.integers(0, nr, n)] if nr else np.zeros(n, np.int32)
+        F[f"k{r}"] = (fk + 1 if dangle_all else fk).astype(np.int32)
+    for j in range(nf):
+        F[f"x{j}"] = rng.standard_normal(n)
+    F["y"] = rng.standard_normal(n)
+    F["g"] = rng.integers(0, 3, n).astype(np.int32)
+    db = synth.Database([synth.Relation("F", F)] + dims, "F", [("F", d.name) for d in dims])
+    feats = [f"x{j}" for j in range(nf)] + [f"d{r}_{j}" for r, f in enumerate(df, 1) for j in range(f)]
+    return db, feats
+
+
+def batches(feats):
+    return {
+        "cov": [synth.covar_batch(feats)],
+        "rt": synth.rt_batch(feats[:4], "y", ["g", "c1", "c3"], synth.thresholds_c3()[::5]),
+        "counts": [synth.Query(["g", "c2"], [[synth.Product(1.0, ())]]), synth.Query(["c1"], [[synth.Product(1.0, ())]]),
+                   synth.Query([], [[synth.Product(1.0, ())]])],
+    }
+
+
+@pytest.mark.parametrize("kind", ["cov", "rt", "counts"])
+@pytest.mark.parametrize("case", ["all_dangling", "one_row", "single_keys", "one_block"])
+def test_degenerate(kind, case):
+    if case == "all_dangling":
+        db, feats = star(5000, (20, 30, 40), dangle_all=True)
+    elif case == "one_row":
+        db, feats = star(1, (20, 30, 40))
+    elif case == "single_keys":
+        db, feats = star(3000, (1, 1, 1))
+    else:
+        db, feats = star(29, (20, 30, 40), seed=3)
+    batch = batches(feats)[kind]
+    gpu, info = run_gpu(db, batch, info=True)
+    ref = oracle.evaluate(db, batch)
+    assert_parity(gpu, ref, batch)
