@@ -127,6 +127,15 @@ lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id
   c->world = world;
   c->shard_part = rank;
   c->shard_nparts = world;
+  static bool pool_ready[64] = {};
+  if (device < 64 && !pool_ready[device]) {  // keep freed blocks cached in the device pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_ready[device] = true;
+  }
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     return LMFAO_ERR_CUDA;
@@ -146,6 +155,7 @@ lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id
 lmfao_status lmfao_destroy(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   cudaStreamSynchronize(c->stream);
   if (c->comm) nccl_destroy(c->comm);
   cudaStream_t st = c->stream;
@@ -167,6 +177,7 @@ lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, i
   for (auto& r : c->rels)
     if (r.name == name) return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate relation %s", name);
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   Rel r;
   r.name = name;
   r.nrows = nrows;
@@ -189,8 +200,8 @@ lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, i
     CTX_CUDA(c, col.buf.alloc(std::max<int64_t>(nrows, 1) * es), "add_relation");
     if (nrows > 0) {
       if (!cols[i]) return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: null column %d", i);
-      CTX_CUDA(c, cudaMemcpy(col.buf.p, cols[i], nrows * es, cols_on_device ? cudaMemcpyDeviceToDevice
-                                                                             : cudaMemcpyHostToDevice),
+      CTX_CUDA(c, cudaMemcpyAsync(col.buf.p, cols[i], nrows * es,
+                                  cols_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream),
                "add_relation copy");
     }
     auto it = c->attr_by_name.find(col.name);
@@ -206,6 +217,8 @@ lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, i
     col.attr = aid;
     r.cols.push_back(std::move(col));
   }
+  // the caller may release its buffers on return
+  CTX_CUDA(c, cudaStreamSynchronize(c->stream), "add_relation copy");
   c->rels.push_back(std::move(r));
   if (rel_id) *rel_id = rid;
   return LMFAO_OK;
@@ -324,7 +337,9 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_TREE) return fail(c, LMFAO_ERR_STATE, "prepare needs a join tree (and runs once)");
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   cudaStream_t st = c->stream;
+  PhaseTrace tr("prepare");
   // post-order: children before parents
   std::vector<int> post;
   std::function<void(int)> dfs = [&](int u) {
@@ -363,6 +378,7 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       CTX_CUDA(c, permute_rel(r, perm.as<uint32_t>(), r.nrows, st), "prepare permute");
       r.unique_key = r.nkeys == r.nrows;
     }
+    tr.mark(r.name.c_str(), st);
   }
   // (4) composite sort of the root by its children's dense keys, increasing
   // domain size, then keep this rank's contiguous shard.
@@ -381,7 +397,9 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     }
     DevBuf perm;
     CTX_CUDA(c, sort_perm_composite(keys, nk, R.nrows, perm, st), "prepare root sort");
+    tr.mark("root sort", st);
     CTX_CUDA(c, permute_rel(R, perm.as<uint32_t>(), R.nrows, st), "prepare root permute");
+    tr.mark("root permute", st);
   }
   if (c->shard_nparts > 1) {
     for (size_t i = 0; i < R.cols.size(); i++) {
@@ -564,7 +582,9 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PREPARED) return fail(c, LMFAO_ERR_STATE, "plan needs prepare (and runs once)");
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   cudaStream_t st = c->stream;
+  PhaseTrace tr("plan");
   c->nodes.clear();
   c->nodes.resize(c->rels.size());
   // slot 0 = count for every view (post-order: grandchildren first)
@@ -595,6 +615,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       gprogs.push_back(std::move(gp));
     }
   }
+  tr.mark("root programs");
   // view programs: one output per slot
   for (int u : c->postorder) {
     NodePlan& np = c->nodes[u];
@@ -630,6 +651,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       }
     }
   }
+  tr.mark("view programs", st);
   // scalar outputs
   CTX_CUDA(c, c->scalar_prog.upload(scal, st), "plan upload");
   int nout = c->scalar_prog.nout;
@@ -748,18 +770,20 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
         }
       }
       CTX_CUDA(c, gp.countcoef.alloc(cc.size() * 8), "plan");
-      CTX_CUDA(c, cudaMemcpy(gp.countcoef.p, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice), "plan");
+      CTX_CUDA(c, cudaMemcpyAsync(gp.countcoef.p, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice, st), "plan");
       gp.d.countcoef = gp.countcoef.as<double>();
       descs.push_back(d);
     }
     CTX_CUDA(c, c->group_prog.upload(all, st), "plan upload groups");
     CTX_CUDA(c, c->group_descs.alloc(std::max<size_t>(descs.size(), 1) * sizeof(GroupDesc)), "plan");
     if (!descs.empty())
-      CTX_CUDA(c, cudaMemcpy(c->group_descs.p, descs.data(), descs.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice),
+      CTX_CUDA(c, cudaMemcpyAsync(c->group_descs.p, descs.data(), descs.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice, st),
                "plan");
   }
+  tr.mark("group plans", st);
   // specialised kernels for recognised batch shapes (gram.cu / hist.cu)
   c->fast.reset(plan_fast_paths(c));
+  tr.mark("fast paths", st);
   c->state = S_PLANNED;
   return LMFAO_OK;
 }
@@ -840,6 +864,7 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
   const char* ng = std::getenv("LMFAO_NO_GRAPH");
   bool use_graph = !c->prof && c->world == 1 && !(ng && ng[0] == '1');
@@ -897,6 +922,7 @@ extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_g
   if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
   if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   const Query& Q = c->queries[q];
   if (n_groupby) *n_groupby = (int)Q.gb.size();
   if (n_udafs) *n_udafs = (int)Q.udafs.size();
@@ -917,6 +943,7 @@ extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32
   if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
   if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   if (c->query_kind[q] == 0) {
     int off = c->scalar_off[c->query_slot[q]];
     if (keys) *keys = nullptr;
@@ -999,6 +1026,7 @@ void scan_timer_end(lmfao_ctx* c, cudaStream_t st) {
 extern "C" lmfao_status lmfao_profile(lmfao_ctx* c, int enable) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   for (auto& e : c->prof_events) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -1011,6 +1039,7 @@ extern "C" lmfao_status lmfao_profile(lmfao_ctx* c, int enable) {
 extern "C" lmfao_status lmfao_profile_read(lmfao_ctx* c, double* total_ms, int64_t* launches) {
   if (!c || !total_ms || !launches) return LMFAO_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
   double t = 0;
   for (auto& e : c->prof_events) {
     if (cudaEventSynchronize(e.second) != cudaSuccess) return fail(c, LMFAO_ERR_CUDA, "profile: event sync failed");

@@ -912,6 +912,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
       outs.push_back(ts);
     }
   }
+  PhaseTrace tr("plan_cov");
   std::unique_ptr<FastCov> fc(new FastCov());
   fc->only_scalar = c->groups.empty();
   std::vector<std::vector<int>> lf(R.children.size());
@@ -951,7 +952,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   if (fc->NS == 2) setup(fc->B, featured[0]);
   // buffers
   if (fc->zeros.alloc(GP * 8)) return nullptr;
-  if (cudaMemset(fc->zeros.p, 0, fc->zeros.bytes)) return nullptr;
+  if (cudaMemsetAsync(fc->zeros.p, 0, fc->zeros.bytes, c->stream)) return nullptr;
   CovLevel* lv[3] = {&fc->L, &fc->A, &fc->B};
   for (int i = 0; i < 3; i++) {
     CovLevel& l = *lv[i];
@@ -961,7 +962,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     const Rel& D = c->rels[l.rel];
     for (int a : l.attrs) cp.push_back((const double*)D.cols[D.find_attr(a)].buf.p);
     if (l.colptrs.alloc(std::max<size_t>(cp.size(), 1) * sizeof(void*))) return nullptr;
-    if (!cp.empty() && cudaMemcpy(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice))
+    if (!cp.empty() && cudaMemcpyAsync(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream))
       return nullptr;
   }
   const int64_t nkA = fc->NS >= 1 ? fc->A.nk : 0;
@@ -969,6 +970,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   fc->off_HL = (fc->off_HA + (size_t)nkA * 4 + 15) / 16 * 16;
   fc->zbytes = fc->off_HL + (size_t)std::max<int64_t>(fc->L.nk, 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
+  tr.mark("terms + buffers", c->stream);
   fc->nblk = (R.nrows + 31) / 32;
   // work items as k_cov defines them: IB-block items, then 2-block items for the last ~10 %
   const int64_t nbig = fc->nblk * 9 / 10 / IB;
@@ -996,6 +998,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
       if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return nullptr;
     }
   }
+  tr.mark("scan layout", c->stream);
   // source index of G[a][b] (a, b: attr id or -1 = "1"); see the layout above k_cov_sum
   auto fidx = [](const std::vector<int>& v, int a) {
     for (size_t i = 0; i < v.size(); i++)

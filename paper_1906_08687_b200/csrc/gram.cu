@@ -847,7 +847,7 @@ FastPaths* plan_gram(lmfao_ctx* c) {
     const Rel& D = c->rels[l.rel];
     for (int a : l.attrs) cp.push_back((const double*)D.cols[D.find_attr(a)].buf.p);
     if (l.colptrs.alloc(std::max<size_t>(cp.size(), 1) * sizeof(void*))) return nullptr;
-    if (!cp.empty() && cudaMemcpy(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice))
+    if (!cp.empty() && cudaMemcpyAsync(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, st))
       return nullptr;
     l.nmom = 1 + n + n * n;
     l.moff = off;

@@ -1,6 +1,9 @@
 // internal.h — private declarations of liblmfao_gpu (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cstdint>
@@ -20,21 +23,70 @@
 
 namespace lmfao {
 
-// Owning device buffer (cudaMalloc / cudaFree).
+// LMFAO_TRACE=1: wall-clock checkpoints of the host-side phases on stderr (tools/e2e_phases.py).
+struct PhaseTrace {
+  bool on;
+  const char* name;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTrace(const char* n) : name(n), t(std::chrono::steady_clock::now()) {
+    const char* e = std::getenv("LMFAO_TRACE");
+    on = e && e[0] == '1';
+  }
+  void mark(const char* what, cudaStream_t st = nullptr) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lmfao] %s/%s %.3f ms\n", name, what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
+// Stream the owning buffers below are ordered on.  Every ABI entry point sets it to its
+// context's stream (StreamScope); allocations then come from the device's stream-ordered
+// memory pool (cudaMallocAsync / cudaFreeAsync, release threshold raised in lmfao_create),
+// which keeps freed memory cached instead of handing it back to the driver with an implicit
+// device-wide synchronisation on every cudaFree.  Outside a scope (pooled == false) the
+// buffers use plain cudaMalloc / cudaFree.
+struct AllocScope {
+  cudaStream_t st = nullptr;
+  bool pooled = false;
+};
+inline AllocScope& alloc_scope() {
+  static thread_local AllocScope s;
+  return s;
+}
+struct StreamScope {
+  AllocScope prev;
+  StreamScope(cudaStream_t st, bool pooled = true) : prev(alloc_scope()) { alloc_scope() = AllocScope{st, pooled}; }
+  ~StreamScope() { alloc_scope() = prev; }
+  StreamScope(const StreamScope&) = delete;
+  StreamScope& operator=(const StreamScope&) = delete;
+};
+
+// Owning device buffer.
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t st = nullptr;  // stream it was allocated on (pooled buffers are freed there)
+  bool pooled = false;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), pooled(o.pooled) { o.p = nullptr; o.bytes = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { reset(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    if (this != &o) {
+      reset();
+      p = o.p; bytes = o.bytes; st = o.st; pooled = o.pooled;
+      o.p = nullptr; o.bytes = 0;
+    }
     return *this;
   }
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) cudaFreeAsync(p, st);
+      else cudaFree(p);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -42,7 +94,10 @@ struct DevBuf {
     reset();
     // 256 B of slack: TMA bulk copies round tail sizes up to 16 B
     b += 256;
-    cudaError_t e = cudaMalloc(&p, b);
+    const AllocScope& sc = alloc_scope();
+    pooled = sc.pooled;
+    st = sc.st;
+    cudaError_t e = pooled ? cudaMallocAsync(&p, b, st) : cudaMalloc(&p, b);
     if (e == cudaSuccess) bytes = b;
     else p = nullptr;
     return e;

@@ -138,6 +138,7 @@ struct Arena {
   int dev = -1;
   DevBuf buf[6];
   void* get(int i, size_t bytes) {
+    StreamScope plain(nullptr, false);  // outlives any one context's stream
     int d = 0;
     cudaGetDevice(&d);
     if (d != dev) {

@@ -92,29 +92,53 @@ def lmfao_unique_id() -> bytes:
     return buf.raw
 
 
+def _struct_dtype(cls):
+    """numpy dtype with the same field offsets as a ctypes Structure (pointers as uint64)."""
+    names, formats, offsets = [], [], []
+    for name, ct in cls._fields_:
+        names.append(name)
+        formats.append({ctypes.c_int32: np.int32, ctypes.c_double: np.float64}.get(ct, np.uint64))
+        offsets.append(getattr(cls, name).offset)
+    return np.dtype({"names": names, "formats": formats, "offsets": offsets, "itemsize": ctypes.sizeof(cls)})
+
+
+_FACTOR_DT, _PRODUCT_DT, _UDAF_DT = (_struct_dtype(c) for c in (lmfao_factor, lmfao_product, lmfao_udaf))
+
+
 def _udaf_structs(udafs, attr_id):
     """udafs: list of products; product = (coeff, [(kind, attr_name|None, param), ...]) or an
-    object with .coeff/.factors whose factors have .kind/.attr/.param."""
-    keep = []
-    arr = (lmfao_udaf * max(1, len(udafs)))()
-    for j, u in enumerate(udafs):
-        parr = (lmfao_product * max(1, len(u)))()
-        for p_i, p in enumerate(u):
+    object with .coeff/.factors whose factors have .kind/.attr/.param.  Returns the lmfao_udaf
+    array (three flat numpy buffers laid out as the C structs) and the buffers to keep alive."""
+    ids = {}
+    fk, fa, fp, pc, pn, ps, un, us = [], [], [], [], [], [], [], []
+    for u in udafs:
+        us.append(len(pc))
+        un.append(len(u))
+        for p in u:
             coeff, factors = (p.coeff, p.factors) if hasattr(p, "coeff") else p
-            farr = (lmfao_factor * max(1, len(factors)))()
-            for f_i, f in enumerate(factors):
+            ps.append(len(fk))
+            pn.append(len(factors))
+            pc.append(float(coeff))
+            for f in factors:
                 kind, attr, param = (f.kind, f.attr, f.param) if hasattr(f, "kind") else f
-                farr[f_i].kind = int(kind)
-                farr[f_i].attr = -1 if attr is None else attr_id(attr)
-                farr[f_i].param = float(param)
-            keep.append(farr)
-            parr[p_i].coeff = float(coeff)
-            parr[p_i].n_factors = len(factors)
-            parr[p_i].factors = ctypes.cast(farr, ctypes.POINTER(lmfao_factor))
-        keep.append(parr)
-        arr[j].n_products = len(u)
-        arr[j].products = ctypes.cast(parr, ctypes.POINTER(lmfao_product))
-    return arr, keep
+                fk.append(int(kind))
+                if attr is None:
+                    fa.append(-1)
+                else:
+                    a = ids.get(attr)
+                    if a is None:
+                        a = ids[attr] = attr_id(attr)
+                    fa.append(a)
+                fp.append(float(param))
+    F = np.zeros(max(1, len(fk)), _FACTOR_DT)
+    F["kind"][:len(fk)], F["attr"][:len(fk)], F["param"][:len(fk)] = fk, fa, fp
+    P = np.zeros(max(1, len(pc)), _PRODUCT_DT)
+    P["coeff"][:len(pc)], P["n_factors"][:len(pc)] = pc, pn
+    P["factors"][:len(pc)] = F.ctypes.data + np.asarray(ps, np.uint64) * np.uint64(F.itemsize)
+    U = np.zeros(max(1, len(un)), _UDAF_DT)
+    U["n_products"][:len(un)] = un
+    U["products"][:len(un)] = P.ctypes.data + np.asarray(us, np.uint64) * np.uint64(P.itemsize)
+    return ctypes.cast(U.ctypes.data, ctypes.POINTER(lmfao_udaf)), (F, P, U)
 
 
 class Engine:

@@ -49,3 +49,26 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h")):
                 src = open(os.path.join(dp, f), errors="ignore").read()
                 assert "import oracle" not in src and "from oracle" not in src and "oracle.cpp" not in src, f
+
+
+def test_udaf_marshalling_matches_c_layout():
+    """The binding lays the UDAF batch out as the lmfao_udaf / lmfao_product / lmfao_factor
+    structs of include/lmfao_gpu.h; read it back through the ctypes struct view."""
+    import synth
+    from paper_1906_08687_b200 import lmfao
+    udafs = [[synth.Product(1.0, ())],
+             [synth.Product(2.5, (synth.ident("a"), synth.Factor(synth.F_LE, "b", 0.25)))],
+             [synth.Product(-1.0, (synth.ident("b"),)), synth.Product(3.0, (synth.Factor(lmfao.F_CONST, None, 4.0),))],
+             [(0.5, [(lmfao.F_EQ, "a", 7.0)])]]
+    ids = {"a": 3, "b": 9}
+    arr, keep = lmfao._udaf_structs(udafs, ids.__getitem__)
+    for j, u in enumerate(udafs):
+        assert arr[j].n_products == len(u)
+        for i, p in enumerate(u):
+            coeff, factors = (p.coeff, p.factors) if hasattr(p, "coeff") else p
+            pr = arr[j].products[i]
+            assert pr.coeff == coeff and pr.n_factors == len(factors)
+            for k, f in enumerate(factors):
+                kind, attr, param = (f.kind, f.attr, f.param) if hasattr(f, "kind") else f
+                got = pr.factors[k]
+                assert (got.kind, got.attr, got.param) == (int(kind), -1 if attr is None else ids[attr], float(param))
