@@ -108,10 +108,19 @@ LMFAO_API lmfao_status lmfao_destroy(lmfao_ctx* ctx);
 LMFAO_API const char* lmfao_last_error(const lmfao_ctx* ctx);
 
 /* Registers relation R(ω) (relations R_1..R_m over schemas ω_1..ω_m) as
- * SoA columns: cols[i] points to nrows values of dtypes[i] (host memory, or
- * device memory on this ctx's device if cols_on_device != 0).  Copied
- * synchronously.  Attributes with the same name in different relations are the
- * natural-join attributes (X = ∪ω).  *rel_id receives the relation id. */
+ * SoA columns: cols[i] points to nrows values of dtypes[i].  cols_on_device:
+ *   LMFAO_COLS_HOST   (0) host memory, copied before the call returns;
+ *   LMFAO_COLS_DEVICE (1) device memory on this ctx's device, copied before return;
+ *   LMFAO_COLS_HOST_DEFERRED (2) host memory (pinned for full speed) that the caller
+ *       keeps valid and unchanged until lmfao_prepare returns: prepare streams the
+ *       columns in on a copy stream in the order it consumes them (dimension
+ *       relations, then the root's foreign keys, then its other columns), so the
+ *       host->device transfer overlaps the remap, the sort and the root permutation.
+ * Attributes with the same name in different relations are the natural-join
+ * attributes (X = ∪ω).  *rel_id receives the relation id. */
+#define LMFAO_COLS_HOST 0
+#define LMFAO_COLS_DEVICE 1
+#define LMFAO_COLS_HOST_DEFERRED 2
 LMFAO_API lmfao_status lmfao_add_relation(lmfao_ctx* ctx, const char* name, int64_t nrows, int32_t ncols,
                                 const char* const* col_names, const lmfao_dtype* dtypes,
                                 const void* const* cols, int cols_on_device, int32_t* rel_id);

@@ -48,20 +48,35 @@ lmfao_status cuda_fail(lmfao_ctx* c, cudaError_t e, const char* where) {
 
 // gather every column of relation r (and its fk_dense / dense_key) by `perm` of length n;
 // all gathers are queued, then one synchronisation releases the old buffers
+// Orders stream st after the deferred host->device copy of column col (if any).
+cudaError_t column_ready(Column& col, cudaStream_t st) {
+  if (!col.ready) return cudaSuccess;
+  CUDA_TRY(cudaStreamWaitEvent(st, col.ready, 0));
+  cudaEventDestroy(col.ready);  // the wait above is already enqueued
+  col.ready = nullptr;
+  return cudaSuccess;
+}
+
+// Pooled buffers are freed in stream order, so replaced buffers need no synchronisation.
 cudaError_t permute_rel(Rel& r, const uint32_t* perm, int64_t n, cudaStream_t st) {
   std::vector<DevBuf> old;
+  bool sync = false;
   auto regather = [&](DevBuf& b, int es) -> cudaError_t {
     DevBuf nb;
     CUDA_TRY(nb.alloc(std::max<int64_t>(n, 1) * es));
     CUDA_TRY(gather_bytes(b.p, perm, nb.p, n, es, st));
+    sync |= !b.pooled || !nb.pooled || b.st != st;
     old.push_back(std::move(b));
     b = std::move(nb);
     return cudaSuccess;
   };
-  for (auto& c : r.cols) CUDA_TRY(regather(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  for (auto& c : r.cols) {
+    CUDA_TRY(column_ready(c, st));
+    CUDA_TRY(regather(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  }
   for (auto& f : r.fk_dense) CUDA_TRY(regather(f, 4));
   if (r.dense_key.p) CUDA_TRY(regather(r.dense_key, 4));
-  CUDA_TRY(cudaStreamSynchronize(st));
+  if (sync) CUDA_TRY(cudaStreamSynchronize(st));
   r.nrows = n;
   return cudaSuccess;
 }
@@ -77,7 +92,10 @@ cudaError_t slice_rel(Rel& r, int64_t lo, int64_t hi, cudaStream_t st) {
     b = std::move(nb);
     return cudaSuccess;
   };
-  for (auto& c : r.cols) CUDA_TRY(cut(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  for (auto& c : r.cols) {
+    CUDA_TRY(column_ready(c, st));
+    CUDA_TRY(cut(c.buf, c.dt == LMFAO_FP64 ? 8 : 4));
+  }
   for (auto& f : r.fk_dense) CUDA_TRY(cut(f, 4));
   CUDA_TRY(cudaStreamSynchronize(st));
   r.nrows = n;
@@ -159,6 +177,13 @@ lmfao_status lmfao_destroy(lmfao_ctx* c) {
   cudaStreamSynchronize(c->stream);
   if (c->comm) nccl_destroy(c->comm);
   cudaStream_t st = c->stream;
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+  }
+  for (auto& r : c->rels)
+    for (auto& col : r.cols)
+      if (col.ready) cudaEventDestroy(col.ready);
   delete c;
   cudaStreamDestroy(st);
   return LMFAO_OK;
@@ -171,7 +196,8 @@ lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, i
                                 int cols_on_device, int32_t* rel_id) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_CREATED) return fail(c, LMFAO_ERR_STATE, "add_relation after set_join_tree");
-  if (!name || nrows < 0 || ncols < 1 || !col_names || !dtypes || (!cols && nrows > 0))
+  if (!name || nrows < 0 || ncols < 1 || !col_names || !dtypes || (!cols && nrows > 0) || cols_on_device < 0 ||
+      cols_on_device > LMFAO_COLS_HOST_DEFERRED)
     return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: bad arguments");
   if (ncols > MAX_COLS) return fail(c, LMFAO_ERR_UNSUPPORTED, "add_relation: more than %d columns", MAX_COLS);
   for (auto& r : c->rels)
@@ -200,9 +226,12 @@ lmfao_status lmfao_add_relation(lmfao_ctx* c, const char* name, int64_t nrows, i
     CTX_CUDA(c, col.buf.alloc(std::max<int64_t>(nrows, 1) * es), "add_relation");
     if (nrows > 0) {
       if (!cols[i]) return fail(c, LMFAO_ERR_INVALID_ARG, "add_relation: null column %d", i);
-      CTX_CUDA(c, cudaMemcpyAsync(col.buf.p, cols[i], nrows * es,
-                                  cols_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream),
-               "add_relation copy");
+      if (cols_on_device == LMFAO_COLS_HOST_DEFERRED)
+        col.host_src = cols[i];
+      else
+        CTX_CUDA(c, cudaMemcpyAsync(col.buf.p, cols[i], nrows * es,
+                                    cols_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream),
+                 "add_relation copy");
     }
     auto it = c->attr_by_name.find(col.name);
     int aid;
@@ -347,12 +376,44 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     post.push_back(u);
   };
   dfs(c->root);
+  {  // deferred host columns: stream them in in the order they are consumed below
+    std::vector<std::pair<const Rel*, Column*>> order;
+    for (int u : post) {
+      Rel& r = c->rels[u];
+      for (int j : r.fk_col) order.push_back({&r, &r.cols[j]});
+      if (r.key_col >= 0) order.push_back({&r, &r.cols[r.key_col]});
+    }
+    for (int u : post)
+      for (auto& col : c->rels[u].cols) order.push_back({&c->rels[u], &col});
+    bool first = true;
+    for (auto& rc : order) {
+      Column* col = rc.second;
+      if (!col->host_src) continue;
+      if (first) {  // the column buffers were allocated on the ctx stream: copy after that
+        first = false;
+        if (!c->copy_stream) CTX_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "prepare");
+        cudaEvent_t alloc_done;
+        CTX_CUDA(c, cudaEventCreateWithFlags(&alloc_done, cudaEventDisableTiming), "prepare");
+        CTX_CUDA(c, cudaEventRecord(alloc_done, st), "prepare");
+        CTX_CUDA(c, cudaStreamWaitEvent(c->copy_stream, alloc_done, 0), "prepare");
+        cudaEventDestroy(alloc_done);
+      }
+      size_t es = col->dt == LMFAO_FP64 ? 8 : 4;
+      CTX_CUDA(c, cudaMemcpyAsync(col->buf.p, col->host_src, rc.first->nrows * es, cudaMemcpyHostToDevice,
+                                  c->copy_stream),
+               "prepare copy");
+      col->host_src = nullptr;
+      CTX_CUDA(c, cudaEventCreateWithFlags(&col->ready, cudaEventDisableTiming), "prepare");
+      CTX_CUDA(c, cudaEventRecord(col->ready, c->copy_stream), "prepare");
+    }
+  }
   for (int u : post) {
     Rel& r = c->rels[u];
     // (1) dense remap of each child key: binary search in the child's dictionary
     r.fk_dense.clear();
     for (size_t j = 0; j < r.children.size(); j++) {
       Rel& ch = c->rels[r.children[j]];
+      CTX_CUDA(c, column_ready(r.cols[r.fk_col[j]], st), "prepare copy");
       DevBuf d;
       CTX_CUDA(c, d.alloc(std::max<int64_t>(r.nrows, 1) * 4), "prepare");
       CTX_CUDA(c, lookup_dense(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.nrows, ch.dict.as<int32_t>(), ch.nkeys,
@@ -369,6 +430,7 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     if (nkeep != r.nrows) CTX_CUDA(c, permute_rel(r, keep.as<uint32_t>(), nkeep, st), "prepare compact");
     if (u != c->root) {
       // (3) dictionary of the key to the parent, dense ids, sort by them
+      CTX_CUDA(c, column_ready(r.cols[r.key_col], st), "prepare copy");
       DevBuf codes;
       CTX_CUDA(c, dict_encode_i32(r.cols[r.key_col].buf.as<int32_t>(), r.nrows, r.dict, r.nkeys, &codes, st),
                "prepare dict");
@@ -401,6 +463,9 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     CTX_CUDA(c, permute_rel(R, perm.as<uint32_t>(), R.nrows, st), "prepare root permute");
     tr.mark("root permute", st);
   }
+  for (auto& r : c->rels)  // columns no permutation consumed
+    for (auto& col : r.cols) CTX_CUDA(c, column_ready(col, st), "prepare copy");
+  if (c->copy_stream) CTX_CUDA(c, cudaStreamSynchronize(c->copy_stream), "prepare copy");  // host buffers released
   if (c->shard_nparts > 1) {
     for (size_t i = 0; i < R.cols.size(); i++) {
       if (R.cols[i].dt != LMFAO_INT32) continue;

@@ -14,6 +14,8 @@ struct Column {
   int attr = -1;
   lmfao_dtype dt = LMFAO_INT32;
   DevBuf buf;
+  const void* host_src = nullptr;  // LMFAO_COLS_HOST_DEFERRED: copied in by prepare
+  cudaEvent_t ready = nullptr;     // copy-stream event the column's consumers wait on
 };
 
 struct Rel {
@@ -129,6 +131,7 @@ struct lmfao_ctx {
   int device = 0, rank = 0, world = 1;
   int shard_part = 0, shard_nparts = 1;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // deferred host->device column copies (prepare)
   void* comm = nullptr;
   std::string err;
   State state = S_CREATED;

@@ -30,6 +30,7 @@ STATUS = {0: "LMFAO_OK", 1: "LMFAO_ERR_INVALID_ARG", 2: "LMFAO_ERR_STATE", 3: "L
 INT32, FP64 = 0, 1
 F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE = range(8)
 UNIQUE_ID_BYTES = 128
+COLS_HOST, COLS_DEVICE, COLS_HOST_DEFERRED = 0, 1, 2
 
 
 class lmfao_factor(ctypes.Structure):
@@ -153,6 +154,7 @@ class Engine:
         self.h = h
         self.rel_ids = {}
         self.query_ids = []
+        self._deferred = []  # host buffers of LMFAO_COLS_HOST_DEFERRED relations, until prepare
 
     def _check(self, s):
         if s:
@@ -162,6 +164,7 @@ class Engine:
         if self.h:
             _lib.lmfao_destroy(self.h)
             self.h = None
+        self._deferred = []
 
     def __del__(self):
         try:
@@ -169,7 +172,11 @@ class Engine:
         except Exception:
             pass
 
-    def add_relation(self, name: str, cols: dict) -> int:
+    def add_relation(self, name: str, cols: dict, deferred: bool | None = None) -> int:
+        """cols: name -> numpy array or torch tensor (all host or all on this device).
+        deferred (default: True for pinned host tensors): LMFAO_COLS_HOST_DEFERRED — the
+        copies happen inside prepare(), overlapped with it; the Engine keeps the buffers
+        alive until then."""
         names = list(cols)
         arrs, dtypes, ptrs, on_dev = [], [], [], None
         for c in names:
@@ -196,12 +203,17 @@ class Engine:
                 arrs.append(a)
                 ptrs.append(a.ctypes.data)
         n = len(arrs[0]) if arrs else 0
+        if deferred is None:
+            deferred = not on_dev and all(hasattr(a, "is_pinned") and a.is_pinned() for a in arrs)
+        mode = COLS_DEVICE if on_dev else (COLS_HOST_DEFERRED if deferred else COLS_HOST)
         cn = (ctypes.c_char_p * len(names))(*[x.encode() for x in names])
         dt = (ctypes.c_int32 * len(names))(*dtypes)
         cp = (_P * len(names))(*ptrs)
         rid = ctypes.c_int32()
-        self._check(_lib.lmfao_add_relation(self.h, name.encode(), n, len(names), cn, dt, cp, int(bool(on_dev)),
+        self._check(_lib.lmfao_add_relation(self.h, name.encode(), n, len(names), cn, dt, cp, mode,
                                             ctypes.byref(rid)))
+        if mode == COLS_HOST_DEFERRED:
+            self._deferred.append(arrs)
         self.rel_ids[name] = rid.value
         return rid.value
 
@@ -220,6 +232,7 @@ class Engine:
 
     def prepare(self):
         self._check(_lib.lmfao_prepare(self.h))
+        self._deferred = []  # prepare has consumed the deferred host columns (else close() drops them)
 
     def add_query(self, groupby, udafs) -> int:
         gb = (ctypes.c_int32 * max(1, len(groupby)))(*[self.attr_id(g) for g in groupby])

@@ -7,12 +7,13 @@ import synth
 from _udaf import float_close
 
 
-def run_gpu(db, batch, shard=None, engine_kw=None, runs=1, info=False):
+def run_gpu(db, batch, shard=None, engine_kw=None, runs=1, info=False, cols=None):
+    """cols: optional relation -> columns override (e.g. pinned torch tensors: deferred load)."""
     from paper_1906_08687_b200 import lmfao
     e = lmfao.Engine(**(engine_kw or {}))
     try:
         for r in db.relations:
-            e.add_relation(r.name, r.cols)
+            e.add_relation(r.name, cols[r.name] if cols else r.cols)
         e.set_join_tree(db.root, db.edges)
         if shard is not None:
             e.set_root_shard(*shard)
