@@ -932,7 +932,7 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   StreamScope scope_(c->stream);
   cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
   const char* ng = std::getenv("LMFAO_NO_GRAPH");
-  bool use_graph = !c->prof && c->world == 1 && !(ng && ng[0] == '1');
+  bool use_graph = !c->prof && c->world == 1 && !(ng && ng[0] == '1') && !(c->fast && !c->fast->graph_ok());
   if (!use_graph || c->graph_runs == 0) {
     c->graph_runs++;
     return run_body(c, st);
@@ -970,7 +970,7 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
 
 namespace {
 lmfao_status ensure_compacted(lmfao_ctx* c, GroupPlan& gp) {
-  if (gp.compacted) return LMFAO_OK;
+  if (gp.compacted || gp.direct) return LMFAO_OK;
   CTX_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
   CTX_CUDA(c, cudaDeviceSynchronize(), "sync");
   CTX_CUDA(c, launch_compact(gp.table.as<double>(), gp.counts.as<unsigned long long>(), gp.ncells, gp.nudaf, gp.d,

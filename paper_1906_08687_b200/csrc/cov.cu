@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       }
       h = (h + 1) & (HT - 1);
     }
-    atomicAdd(&g.HL[key], len);
+    gred_add(&g.HL[key], len);
   };
   auto push_B = [&](int keyB) {
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
@@ -453,8 +453,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
             r9[t] = fma(D[t][0], b089.y, fma(D[t][1], b189.y, r9[t]));
           }
           if (NS >= 1 && m == 0) {
-            if (n0 > 0.0) atomicAdd(&g.HA[key0], (unsigned)n0);
-            if (n1 > 0.0) atomicAdd(&g.HA[key1], (unsigned)n1);
+            if (n0 > 0.0) gred_add(&g.HA[key0], (unsigned)n0);
+            if (n1 > 0.0) gred_add(&g.HA[key1], (unsigned)n1);
           }
         }
         auto add_segs = [&](int lo, int hi) {  // segments [lo, hi) of the window -> the open B run
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     __threadfence_block();
     for (int i = lane; i < HT; i += 32) {
       const int key = hkey[i];
-      if (key != -1 && hcnt[i]) atomicAdd(&g.HL[key], hcnt[i]);
+      if (key != -1 && hcnt[i]) gred_add(&g.HL[key], hcnt[i]);
     }
   }
 }

@@ -119,6 +119,7 @@ struct GroupPlan {
   DevBuf table, counts;
   DevProgram prog;
   bool compacted = false;
+  bool direct = false;  // a fast path writes rkeys/rvals/rcnts/ngroups itself at run (no dense table)
   DevBuf rkeys, rvals, rcnts;
   DevBuf countcoef;
   int64_t ngroups = 0;

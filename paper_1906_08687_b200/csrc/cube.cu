@@ -1,0 +1,632 @@
+// cube.cu — the histogram path (§8 row (e)(iii)) for group-by batches whose aggregates are
+// linear in root measures: SUM(c_0 + Σ_j c_j · m_j) GROUP BY attributes of the root and of
+// its primary-key children (§3 "Data cubes": one query per subset of
+// the cube dimensions, each with SUM(m) for every measure; BASELINE.json configs[4]).
+//
+// The root is sorted by its children's dense keys in increasing domain order (levels
+// 0..R-1), so for a cuboid whose deepest group-by attribute lives at level d, every
+// maximal run of rows with equal keys at levels 0..d ("level-d run") falls into one cell.
+// Per 32-row block a warp takes segmented sums of (1, m_1..m_M) over the level-d runs of
+// every level d some cuboid needs, carries a run that continues into the next block, and at
+// each run end adds the run's totals once to each of the level's cuboids (one atomic per
+// UDAF and one for the count) — "cuboid cells updated once per run at the level of their
+// deepest group-by attribute", instead of once per row.  Cuboids
+// with root attributes use level R: runs of equal keys and equal root group-by codes.
+// With primary-key leaves and no dangling rows (dropped at prepare) every root row joins
+// exactly one row per child, so the join multiplicity of a row is 1.
+#include <cstdlib>
+#include <map>
+#include <set>
+
+#include "ctx.h"
+
+namespace lmfao {
+namespace {
+
+constexpr int CB_LEV = 8;     // root children
+constexpr int CB_MEAS = 8;    // distinct measure attributes
+constexpr int CB_GB = 8;      // group-by attributes per cuboid
+constexpr int CB_ATTR = 8;    // distinct group-by attributes of the batch
+constexpr int CB_TERMS = 512; // UDAF terms of the batch (shared memory)
+constexpr int CB_QD = 16;     // cuboids per level
+constexpr int CB_ITEMS = 1024;  // (cuboid, non-constant UDAF) pairs of the batch
+constexpr int CB_WARPS = 8;
+constexpr unsigned BFULL = 0xffffffffu;
+
+struct Cuboid {
+  long long stride[CB_GB];
+  int8_t aslot[CB_GB];          // group-by attribute i -> batch attribute slot
+  int ngb, nudaf;
+  int sparse, pad0_;
+  double* table;                // [cells][nudaf]; constant UDAFs are left to the compaction (countcoef)
+  unsigned long long* counts;
+  // sparse cuboid (too many cells for a dense table): one record per run end, sorted and
+  // reduced after the scan: rkey[slot] = cell, rval[j * rcap + slot] = S_j
+  unsigned* rkey;
+  double* rval;
+  unsigned long long* rn;
+  long long rcap;
+  long long pad_;
+};
+static_assert(sizeof(Cuboid) % 16 == 0, "cuboids are copied to shared memory in 16-byte units");
+// (cuboid, UDAF) pair of a level: value = Σ_{t in [t0, t1)} tc[t] · S_{tj[t]}
+struct CubeItem {
+  int16_t qk;  // cuboid within its level
+  int16_t u;
+  int16_t t0, t1;
+};
+struct CubeArgs {
+  int64_t nrows;
+  int R, M, nattr, nq, nterm, nitem;
+  unsigned dmask;               // levels (0..R) with cuboids
+  int64_t chunk;                // rows per work unit (multiple of 32), taken dynamically
+  int* work;                    // chunk counter (zeroed per run)
+  const int32_t* key[CB_LEV];   // dense keys, level order
+  const void* meas[CB_MEAS];
+  int meas_i32[CB_MEAS];
+  const int32_t* acode[CB_ATTR];  // codes per child dense key (level < R) or per root row (level R)
+  int alvl[CB_ATTR];
+  int qbeg[CB_LEV + 2];         // cuboids sorted by depth: depth d = [qbeg[d], qbeg[d + 1])
+  int ibeg[CB_LEV + 2];         // items sorted by depth
+  const Cuboid* q;
+  const CubeItem* items;
+  const int8_t* tj;             // [nterm] S index (0 = count, 1 + measure)
+  const double* tc;             // [nterm] coefficient
+  int ablate;                   // LMFAO_CUBE_ABLATE (profiling): 1 no flush, 2 counts only
+};
+
+unsigned cgrid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+__device__ __forceinline__ double seg_scan(double v, int lane, int s0) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const double u = __shfl_up_sync(BFULL, v, d);
+    if (lane - d >= s0) v += u;
+  }
+  return v;
+}
+
+// shared memory: [cuboids | items | tj | tc | per warp: S[32][CB_MEAS+1], carry[CB_LEV+1][CB_MEAS+1],
+// cells[32][CB_QD], codes[32][CB_ATTR]]
+struct CubeSmem {
+  size_t q, items, tj, tc, warps, per_warp;
+  __host__ __device__ CubeSmem(int nq, int nitem, int nterm) {
+    q = 0;
+    items = (nq * sizeof(Cuboid) + 15) / 16 * 16;
+    tj = items + (nitem * sizeof(CubeItem) + 15) / 16 * 16;
+    tc = tj + (nterm + 15) / 16 * 16;
+    warps = tc + (size_t)nterm * 8;
+    per_warp = (32 * (CB_MEAS + 1) + (CB_LEV + 1) * (CB_MEAS + 1) + 32 * CB_QD) * 8 + 32 * CB_ATTR * 4;
+  }
+  size_t total() const { return warps + CB_WARPS * per_warp; }
+};
+
+__global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ CubeArgs a) {
+  extern __shared__ __align__(16) unsigned char csm[];
+  const CubeSmem L(a.nq, a.nitem, a.nterm);
+  const Cuboid* sq = reinterpret_cast<const Cuboid*>(csm + L.q);
+  const CubeItem* items = reinterpret_cast<const CubeItem*>(csm + L.items);
+  const int8_t* tj = reinterpret_cast<const int8_t*>(csm + L.tj);
+  const double* tc = reinterpret_cast<const double*>(csm + L.tc);
+  {
+    const int4* src = reinterpret_cast<const int4*>(a.q);
+    int4* dst = reinterpret_cast<int4*>(csm + L.q);
+    for (int i = threadIdx.x; i < (int)(a.nq * sizeof(Cuboid) / 16); i += blockDim.x) dst[i] = src[i];
+    for (int i = threadIdx.x; i < a.nitem; i += blockDim.x) reinterpret_cast<CubeItem*>(csm + L.items)[i] = a.items[i];
+    for (int i = threadIdx.x; i < a.nterm; i += blockDim.x) {
+      reinterpret_cast<int8_t*>(csm + L.tj)[i] = a.tj[i];
+      reinterpret_cast<double*>(csm + L.tc)[i] = a.tc[i];
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int M1 = a.M + 1;
+  unsigned char* wsm = csm + L.warps + (size_t)wib * L.per_warp;
+  double* S = reinterpret_cast<double*>(wsm);               // run totals of the level's run ends [tail][j]
+  double* carry = S + 32 * (CB_MEAS + 1);                   // the run open at the previous block's end [d][j]
+  long long* cells = reinterpret_cast<long long*>(carry + (CB_LEV + 1) * (CB_MEAS + 1));  // [tail][cuboid]
+  int* codes = reinterpret_cast<int*>(cells + 32 * CB_QD);  // [tail][attr]
+  const int64_t nchunks = (a.nrows + a.chunk - 1) / a.chunk;
+  for (;;) {
+    int ch = 0;
+    if (lane == 0) ch = atomicAdd(a.work, 1);
+    ch = __shfl_sync(BFULL, ch, 0);
+    if (ch >= nchunks) break;
+    const int64_t r0 = (int64_t)ch * a.chunk;
+    const int64_t r1 = r0 + a.chunk < a.nrows ? r0 + a.chunk : a.nrows;
+    for (int i = lane; i < (CB_LEV + 1) * (CB_MEAS + 1); i += 32) carry[i] = 0.0;
+    __syncwarp();
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int64_t row = base + lane;
+      const bool v = row < r1;
+      const bool vn = row + 1 < r1;  // the next row exists in this chunk
+      // level-d run starts of this row (st) and of the next row (stn); a row beyond the
+      // chunk starts runs everywhere
+      unsigned st = 0, stn = 0;  // bit d
+      int key[CB_LEV];
+      {
+        bool chg = false, chgn = false;
+#pragma unroll
+        for (int l = 0; l < CB_LEV; l++) {
+          if (l >= a.R) break;
+          const int k = v ? a.key[l][row] : -1;
+          key[l] = k;
+          int kp = __shfl_up_sync(BFULL, k, 1);
+          if (lane == 0) kp = base > r0 ? a.key[l][base - 1] : -2;
+          int kn = __shfl_down_sync(BFULL, k, 1);
+          if (lane == 31) kn = vn ? a.key[l][row + 1] : -3;
+          chg |= kp != k;
+          chgn |= !vn || kn != k;
+          if (chg) st |= 1u << l;
+          if (chgn) stn |= 1u << l;
+        }
+        if (a.dmask >> a.R & 1u) {  // level R: equal keys and equal root group-by codes
+#pragma unroll
+          for (int i = 0; i < CB_ATTR; i++) {
+            if (i >= a.nattr) break;
+            if (a.alvl[i] != a.R) continue;
+            const int c = v ? a.acode[i][row] : -1;
+            int cp = __shfl_up_sync(BFULL, c, 1);
+            if (lane == 0) cp = base > r0 ? a.acode[i][base - 1] : -2;
+            int cn = __shfl_down_sync(BFULL, c, 1);
+            if (lane == 31) cn = vn ? a.acode[i][row + 1] : -3;
+            chg |= cp != c;
+            chgn |= !vn || cn != c;
+          }
+          if (chg) st |= 1u << a.R;
+          if (chgn) stn |= 1u << a.R;
+        }
+        if (!v) st = stn = ~0u;
+      }
+      // the row's values: S_0 = 1 (count), S_j = m_j
+      double xm[CB_MEAS + 1];
+      xm[0] = v ? 1.0 : 0.0;
+#pragma unroll
+      for (int j = 0; j < CB_MEAS; j++) {
+        xm[j + 1] = 0.0;
+        if (j < a.M && v)
+          xm[j + 1] = a.meas_i32[j] ? (double)reinterpret_cast<const int32_t*>(a.meas[j])[row]
+                                    : reinterpret_cast<const double*>(a.meas[j])[row];
+      }
+      for (int d = a.R; d >= 0; d--) {
+        if (!(a.dmask >> d & 1u)) continue;
+        const bool s = st >> d & 1u, tail = v && (stn >> d & 1u);
+        const unsigned starts = __ballot_sync(BFULL, s) | 1u;
+        const int s0 = 31 - __clz(starts & ((2u << lane) - 1u));
+        const bool cont0 = !__shfl_sync(BFULL, (int)s, 0);  // lane 0 continues the carried run
+        const bool carry_out = !__shfl_sync(BFULL, (int)(stn >> d & 1u), 31);
+        const unsigned T = __ballot_sync(BFULL, tail);  // run ends, compacted by rank
+        const int nt = __popc(T), rank = __popc(T & ((1u << lane) - 1u));
+        double* cd = carry + d * (CB_MEAS + 1);
+#pragma unroll
+        for (int j = 0; j <= CB_MEAS; j++) {
+          if (j >= M1) break;
+          double x = xm[j];
+          if (lane == 0 && cont0) x += cd[j];
+          x = seg_scan(x, lane, s0);
+          if (tail) S[rank * (CB_MEAS + 1) + j] = x;
+          __syncwarp();
+          if (lane == 31) cd[j] = carry_out ? x : 0.0;
+        }
+        __syncwarp();
+        if (nt && !(a.ablate & 1)) {
+          // (0) each run end's group-by codes (attributes at levels <= d), loaded once
+          if (tail) {
+            int* cl = codes + rank * CB_ATTR;
+#pragma unroll
+            for (int i = 0; i < CB_ATTR; i++) {
+              if (i >= a.nattr) break;
+              const int l = a.alvl[i];
+              if (l > d) continue;
+              int idx = 0;
+#pragma unroll
+              for (int t = 0; t < CB_LEV; t++)
+                if (t == l) idx = key[t];
+              cl[i] = l >= a.R ? a.acode[i][row] : a.acode[i][idx];
+            }
+          }
+          __syncwarp();
+          // (1) per (run end, cuboid): the cell, the count, or a record of a sparse cuboid;
+          // lanes split as tp run ends x nqd cuboids
+          const int q0 = a.qbeg[d], nqd = a.qbeg[d + 1] - q0;
+          {
+            const int tp = 32 / nqd, sub = lane / nqd, qk = lane - sub * nqd;
+            for (int tb = 0; tb < nt; tb += tp) {
+              const int t = tb + sub;
+              const bool act = sub < tp && t < nt;
+              const Cuboid& q = sq[q0 + (act ? qk : 0)];
+              long long cell = 0;
+              if (act) {
+                for (int i = 0; i < q.ngb; i++) cell += (long long)codes[t * CB_ATTR + q.aslot[i]] * q.stride[i];
+                cells[t * CB_QD + qk] = cell;
+                if (!q.sparse) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
+              }
+              const bool rec = act && q.sparse;
+              if (__any_sync(BFULL, rec)) {  // warp-aggregated record slots per cuboid
+                const unsigned grp = __match_any_sync(BFULL, rec ? qk : -1);
+                const int leader = __ffs(grp) - 1;
+                unsigned long long b0 = 0;
+                if (rec && lane == leader) b0 = atomicAdd(q.rn, (unsigned long long)__popc(grp));
+                b0 = __shfl_sync(BFULL, b0, leader);
+                const long long slot = (long long)b0 + __popc(grp & ((1u << lane) - 1u));
+                if (rec && slot < q.rcap) {
+                  q.rkey[slot] = (unsigned)cell;
+                  for (int j = 0; j < M1; j++) q.rval[j * q.rcap + slot] = S[t * (CB_MEAS + 1) + j];
+                }
+              }
+            }
+          }
+          __syncwarp();
+          // (2) per (run end, non-constant UDAF of a dense cuboid): one reduction each
+          if (!(a.ablate & 2)) {
+            const int i0 = a.ibeg[d], nid = a.ibeg[d + 1] - i0;
+            if (nid > 0 && nid <= 32) {
+              const int tp = 32 / nid, sub = lane / nid, it = lane - sub * nid;
+              const CubeItem e = items[i0 + it];
+              const Cuboid& q = sq[q0 + e.qk];
+              for (int tb = 0; tb < nt; tb += tp) {
+                const int t = tb + sub;
+                if (sub < tp && t < nt) {
+                  double val = 0.0;
+                  for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
+                  if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
+                }
+              }
+            } else if (nid > 32) {
+              for (int t = 0; t < nt; t++)
+                for (int it = lane; it < nid; it += 32) {
+                  const CubeItem e = items[i0 + it];
+                  const Cuboid& q = sq[q0 + e.qk];
+                  double val = 0.0;
+                  for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
+                  if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
+                }
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// sorted records of a sparse cuboid -> its groups in canonical (ascending cell) order
+__global__ void k_rec_heads(const unsigned* __restrict__ key, int64_t n, uint32_t* __restrict__ head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || key[i] != key[i - 1]) ? 1u : 0u;
+}
+struct RecReduce {
+  const unsigned* key;
+  const uint32_t* perm;
+  const uint32_t* head;
+  const uint32_t* excl;
+  const double* rval;
+  long long rcap;
+  int64_t n;
+  int M1, nudaf;
+  const double* coef;  // [nudaf][M1]
+  DecodeArgs d;
+  int32_t* okeys;
+  double* ovals;
+  unsigned long long* ocnts;
+};
+__global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!r.head[i]) continue;
+    double S[CB_MEAS + 1];
+    for (int j = 0; j < r.M1; j++) S[j] = 0.0;
+    int64_t t = i;
+    do {
+      const uint32_t p = r.perm[t];
+      for (int j = 0; j < r.M1; j++) S[j] += r.rval[j * r.rcap + p];
+      t++;
+    } while (t < r.n && !r.head[t]);
+    const int64_t g = r.excl[i];
+    const long long cell = r.key[i];
+    for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][(cell / r.d.stride[a]) % r.d.radix[a]];
+    for (int u = 0; u < r.nudaf; u++) {
+      double v = 0.0;
+      for (int j = 0; j < r.M1; j++) v = fma(r.coef[u * r.M1 + j], S[j], v);
+      r.ovals[g * r.nudaf + u] = v;
+    }
+    r.ocnts[g] = (unsigned long long)S[0];
+  }
+}
+
+struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
+  int gi = -1, coff = 0, bits = 1;
+  long long cap = 0;
+  DevBuf key, val, n, perm, head, excl;
+};
+
+struct FastCube : FastPaths {
+  CubeArgs ca{};
+  DevBuf dq, dcoef, ditems, dtj, dtc, dwork;
+  std::vector<SparseOut> sparse;
+  int nq = 0, grid = 148;
+  size_t smem = 0;
+  bool graph_ok() const override { return sparse.empty(); }
+  std::string describe() const override {
+    char b[160];
+    std::snprintf(b, sizeof b, "{\"kind\": \"cube\", \"cuboids\": %d, \"sparse\": %d, \"measures\": %d, \"levels\": %d}",
+                  nq, (int)sparse.size(), ca.M, ca.R);
+    return b;
+  }
+  bool handles_group(int) const override { return true; }
+  bool handles_all_groups() const override { return true; }
+  bool skip_generic_views() const override { return true; }
+  int run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool&) override {
+    for (auto& gp : c->groups) {
+      if (gp.direct) continue;
+      CUDA_TRY(cudaMemsetAsync(gp.counts.p, 0, gp.ncells * 8, st));
+      CUDA_TRY(cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st));
+    }
+    for (auto& sp : sparse) CUDA_TRY(cudaMemsetAsync(sp.n.p, 0, 8, st));
+    CUDA_TRY(cudaMemsetAsync(dwork.p, 0, 4, st));
+    CubeArgs a = ca;
+    a.nrows = c->rels[c->root].nrows;
+    if (a.nrows > 0) {
+      const int64_t nch = (a.nrows + a.chunk - 1) / a.chunk;
+      const int64_t g = std::min<int64_t>((nch + CB_WARPS - 1) / CB_WARPS, grid);
+      k_cube<<<(unsigned)g, CB_WARPS * 32, smem, st>>>(a);
+      launches_add(1);
+    }
+    CUDA_TRY(cudaGetLastError());
+    for (auto& sp : sparse) CUDA_TRY(finish_sparse(c, sp, st));
+    return cudaSuccess;
+  }
+  // sort the records by cell, reduce equal cells, decode: the groups in canonical order
+  cudaError_t finish_sparse(lmfao_ctx* c, SparseOut& sp, cudaStream_t st) {
+    GroupPlan& gp = c->groups[sp.gi];
+    unsigned long long n = 0;
+    CUDA_TRY(cudaMemcpyAsync(&n, sp.n.p, 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if ((long long)n > sp.cap) return cudaErrorIllegalAddress;  // cannot happen: records <= runs + chunks
+    gp.ngroups = 0;
+    if (n > 0) {
+      CUDA_TRY(iota_u32(sp.perm.as<uint32_t>(), (int64_t)n, st));
+      CUDA_TRY(radix_sort_pairs(sp.key.as<uint32_t>(), sp.perm.as<uint32_t>(), (int64_t)n, sp.bits, st));
+      k_rec_heads<<<cgrid((int64_t)n), 256, 0, st>>>(sp.key.as<unsigned>(), (int64_t)n, sp.head.as<uint32_t>());
+      CUDA_TRY(exclusive_scan_u32(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), (int64_t)n, st));
+      uint32_t le = 0, lf = 0;
+      CUDA_TRY(cudaMemcpyAsync(&le, sp.excl.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaMemcpyAsync(&lf, sp.head.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      gp.ngroups = (int64_t)le + lf;
+    }
+    const int64_t ng = gp.ngroups;
+    if (gp.rkeys.bytes < (size_t)std::max<int64_t>(ng * gp.d.ngb * 4, 16)) CUDA_TRY(gp.rkeys.alloc(ng * gp.d.ngb * 4));
+    if (gp.rvals.bytes < (size_t)std::max<int64_t>(ng * gp.nudaf * 8, 16)) CUDA_TRY(gp.rvals.alloc(ng * gp.nudaf * 8));
+    if (gp.rcnts.bytes < (size_t)std::max<int64_t>(ng * 8, 16)) CUDA_TRY(gp.rcnts.alloc(ng * 8));
+    if (n > 0) {
+      RecReduce r{};
+      r.key = sp.key.as<unsigned>();
+      r.perm = sp.perm.as<uint32_t>();
+      r.head = sp.head.as<uint32_t>();
+      r.excl = sp.excl.as<uint32_t>();
+      r.rval = sp.val.as<double>();
+      r.rcap = sp.cap;
+      r.n = (int64_t)n;
+      r.M1 = ca.M + 1;
+      r.nudaf = gp.nudaf;
+      r.coef = dcoef.as<double>() + sp.coff;
+      r.d = gp.d;
+      r.okeys = gp.rkeys.as<int32_t>();
+      r.ovals = gp.rvals.as<double>();
+      r.ocnts = gp.rcnts.as<unsigned long long>();
+      k_rec_reduce<<<cgrid((int64_t)n), 256, 0, st>>>(r);
+      launches_add(3);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return cudaSuccess;
+  }
+};
+
+}  // namespace
+
+// Planner hook: every group-by query's UDAFs are sums of products of constants and at most
+// one identity factor on a root attribute, the root's children are primary-key leaves, and
+// the batch's measures, levels and attributes fit the kernel's limits.  Otherwise nullptr.
+FastPaths* plan_cube(lmfao_ctx* c) {
+  if (c->groups.empty()) return nullptr;
+  const Rel& R = c->rels[c->root];
+  const int nlev = (int)R.children.size();
+  if (nlev > CB_LEV) return nullptr;
+  for (int ch : R.children)
+    if (!c->rels[ch].children.empty() || !c->rels[ch].unique_key) return nullptr;
+  std::vector<int> lvl_of_child(nlev, -1);
+  for (size_t p = 0; p < c->levels.size(); p++) lvl_of_child[c->levels[p]] = (int)p;
+  std::unique_ptr<FastCube> fc(new FastCube());
+  CubeArgs& a = fc->ca;
+  a.R = nlev;
+  for (int l = 0; l < nlev; l++) a.key[l] = R.fk_dense[c->levels[l]].as<int32_t>();
+  std::vector<int> meas;  // attr ids
+  auto meas_slot = [&](int attr) -> int {
+    for (size_t i = 0; i < meas.size(); i++)
+      if (meas[i] == attr) return (int)i;
+    if (meas.size() == (size_t)CB_MEAS) return -1;
+    meas.push_back(attr);
+    return (int)meas.size() - 1;
+  };
+  for (auto& gp : c->groups)
+    for (auto& u : c->queries[gp.q].udafs)
+      for (auto& p : u) {
+        int nid = 0;
+        for (auto& f : p.f) {
+          if (f.kind == LMFAO_F_CONST) continue;
+          if (f.kind != LMFAO_F_IDENT || c->owner[f.attr] != c->root || ++nid > 1) return nullptr;
+          if (meas_slot(f.attr) < 0) return nullptr;
+        }
+      }
+  const int M = (int)meas.size(), M1 = M + 1;
+  std::map<int, int> aslot;  // group-by attribute -> slot
+  struct QInfo {
+    Cuboid q;
+    int gi, depth;
+    std::vector<std::vector<std::pair<int, double>>> terms;  // per UDAF (j, coef), empty: constant
+    std::vector<double> dense;                               // [nudaf][M1] (sparse reduce)
+  };
+  std::vector<QInfo> qs;
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    GroupPlan& gp = c->groups[gi];
+    const Query& Q = c->queries[gp.q];
+    if (Q.gb.size() > (size_t)CB_GB || gp.nudaf > 64) return nullptr;
+    QInfo qi{};
+    qi.gi = (int)gi;
+    Cuboid& q = qi.q;
+    q.ngb = (int)Q.gb.size();
+    for (int i = 0; i < q.ngb; i++) {
+      const int cc = gp.g.code_child[i];
+      const int l = cc < 0 ? nlev : lvl_of_child[cc];
+      auto it = aslot.find(Q.gb[i]);
+      if (it == aslot.end()) {
+        if ((int)aslot.size() == CB_ATTR) return nullptr;
+        const int sl = (int)aslot.size();
+        aslot[Q.gb[i]] = sl;
+        a.acode[sl] = gp.g.code[i];
+        a.alvl[sl] = l;
+        it = aslot.find(Q.gb[i]);
+      }
+      q.aslot[i] = (int8_t)it->second;
+      q.stride[i] = gp.g.stride[i];
+      qi.depth = std::max(qi.depth, l);
+    }
+    q.nudaf = gp.nudaf;
+    q.table = gp.table.as<double>();
+    q.counts = gp.counts.as<unsigned long long>();
+    for (int u = 0; u < gp.nudaf; u++) {
+      std::vector<double> row(M1, 0.0);
+      bool constant = true;
+      for (auto& p : Q.udafs[u]) {
+        double v = p.coeff;
+        int j = 0;
+        for (auto& f : p.f) {
+          if (f.kind == LMFAO_F_CONST) v *= f.param;
+          else j = 1 + meas_slot(f.attr), constant = false;
+        }
+        row[j] += v;
+      }
+      std::vector<std::pair<int, double>> t;
+      if (!constant)
+        for (int j = 0; j < M1; j++)
+          if (row[j] != 0.0) t.push_back({j, row[j]});
+      qi.terms.push_back(t);
+      qi.dense.insert(qi.dense.end(), row.begin(), row.end());
+    }
+    a.dmask |= 1u << qi.depth;
+    qs.push_back(std::move(qi));
+  }
+  std::stable_sort(qs.begin(), qs.end(), [](const QInfo& x, const QInfo& y) { return x.depth < y.depth; });
+  for (int d = 0, k = 0; d <= CB_LEV + 1; d++) {
+    while (k < (int)qs.size() && qs[k].depth < d) k++;
+    a.qbeg[d] = k;
+  }
+  a.M = M;
+  for (int j = 0; j < M; j++) {
+    const Column& col = R.cols[R.find_attr(meas[j])];
+    a.meas[j] = col.buf.p;
+    a.meas_i32[j] = col.dt == LMFAO_INT32;
+  }
+  a.nattr = (int)aslot.size();
+  a.nq = (int)qs.size();
+  a.chunk = 32 * 32;
+  if (const char* ab = std::getenv("LMFAO_CUBE_ABLATE")) a.ablate = std::atoi(ab);
+  for (int d = 0; d <= CB_LEV; d++)
+    if (a.qbeg[d + 1] - a.qbeg[d] > CB_QD) return nullptr;
+  // cuboids with more cells than 2^25 (C5's {A,B,C}: 5·10^8) keep no dense table: their
+  // run records are sorted and reduced after the scan (single GPU; LMFAO_CUBE_DENSE=1: off)
+  const char* dn = std::getenv("LMFAO_CUBE_DENSE");
+  const bool allow_sparse = c->world == 1 && !(dn && dn[0] == '1');
+  const int64_t nrows = R.nrows, nchunks = (nrows + a.chunk - 1) / a.chunk;
+  const char* smin = std::getenv("LMFAO_CUBE_SPARSE_CELLS");  // tests: lower the threshold
+  const int64_t sparse_min = smin ? std::atoll(smin) : ((int64_t)1 << 25);
+  std::vector<Cuboid> hq;
+  std::vector<double> dense;
+  for (size_t k = 0; k < qs.size(); k++) {
+    hq.push_back(qs[k].q);
+    const int coff = (int)dense.size();
+    dense.insert(dense.end(), qs[k].dense.begin(), qs[k].dense.end());
+    GroupPlan& gp = c->groups[qs[k].gi];
+    if (!allow_sparse || gp.ncells <= sparse_min || gp.ncells > ((int64_t)1 << 32)) continue;
+    SparseOut sp;
+    sp.gi = qs[k].gi;
+    sp.coff = coff;
+    sp.cap = nrows + nchunks + 64;
+    while (sp.bits < 32 && ((int64_t)1 << sp.bits) < gp.ncells) sp.bits++;
+    if (sp.key.alloc(sp.cap * 4) || sp.val.alloc((size_t)sp.cap * M1 * 8) || sp.n.alloc(8) || sp.perm.alloc(sp.cap * 4) ||
+        sp.head.alloc(sp.cap * 4) || sp.excl.alloc(sp.cap * 4))
+      return nullptr;
+    Cuboid& q = hq[k];
+    q.sparse = 1;
+    q.rkey = sp.key.as<unsigned>();
+    q.rval = sp.val.as<double>();
+    q.rn = sp.n.as<unsigned long long>();
+    q.rcap = sp.cap;
+    fc->sparse.push_back(std::move(sp));
+  }
+  // items: (cuboid, non-constant UDAF) pairs of the dense cuboids, by level, with their terms
+  std::vector<CubeItem> items;
+  std::vector<int8_t> tj;
+  std::vector<double> tc;
+  for (int d = 0; d <= CB_LEV; d++) {
+    a.ibeg[d] = (int)items.size();
+    for (int k = a.qbeg[d]; k < a.qbeg[d + 1]; k++) {
+      if (hq[k].sparse) continue;
+      for (size_t u = 0; u < qs[k].terms.size(); u++) {
+        const auto& t = qs[k].terms[u];
+        if (t.empty()) continue;  // constant UDAF: from the count at compaction
+        CubeItem e{(int16_t)(k - a.qbeg[d]), (int16_t)u, (int16_t)tj.size(), 0};
+        for (auto& jt : t) {
+          tj.push_back((int8_t)jt.first);
+          tc.push_back(jt.second);
+        }
+        e.t1 = (int16_t)tj.size();
+        items.push_back(e);
+      }
+    }
+  }
+  a.ibeg[CB_LEV + 1] = (int)items.size();
+  if ((int)tj.size() > CB_TERMS || (int)items.size() > CB_ITEMS) return nullptr;
+  a.nterm = (int)tj.size();
+  a.nitem = (int)items.size();
+  fc->nq = a.nq;
+  cudaStream_t st = c->stream;
+  if (fc->dq.alloc(hq.size() * sizeof(Cuboid)) || fc->dcoef.alloc(std::max<size_t>(dense.size(), 1) * 8) ||
+      fc->ditems.alloc(std::max<size_t>(items.size(), 1) * sizeof(CubeItem)) || fc->dtj.alloc(std::max<size_t>(tj.size(), 1)) ||
+      fc->dtc.alloc(std::max<size_t>(tc.size(), 1) * 8) || fc->dwork.alloc(16))
+    return nullptr;
+  if (cudaMemcpyAsync(fc->dq.p, hq.data(), hq.size() * sizeof(Cuboid), cudaMemcpyHostToDevice, st)) return nullptr;
+  if (!items.empty() &&
+      cudaMemcpyAsync(fc->ditems.p, items.data(), items.size() * sizeof(CubeItem), cudaMemcpyHostToDevice, st))
+    return nullptr;
+  if (!dense.empty() && cudaMemcpyAsync(fc->dcoef.p, dense.data(), dense.size() * 8, cudaMemcpyHostToDevice, st))
+    return nullptr;
+  if (!tj.empty() && (cudaMemcpyAsync(fc->dtj.p, tj.data(), tj.size(), cudaMemcpyHostToDevice, st) ||
+                      cudaMemcpyAsync(fc->dtc.p, tc.data(), tc.size() * 8, cudaMemcpyHostToDevice, st)))
+    return nullptr;
+  a.q = fc->dq.as<Cuboid>();
+  a.items = fc->ditems.as<CubeItem>();
+  a.tj = fc->dtj.as<int8_t>();
+  a.tc = fc->dtc.as<double>();
+  a.work = fc->dwork.as<int>();
+  fc->smem = CubeSmem(a.nq, a.nitem, a.nterm).total();
+  if (fc->smem > 227 * 1024) return nullptr;
+  if (fc->smem > 48 * 1024 &&
+      cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc->smem))
+    return nullptr;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cube, CB_WARPS * 32, fc->smem) || per_sm < 1) per_sm = 1;
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+  fc->grid = nsm * per_sm;
+  if (cudaStreamSynchronize(st)) return nullptr;
+  for (auto& sp : fc->sparse) {  // no dense table for these
+    GroupPlan& gp = c->groups[sp.gi];
+    gp.direct = true;
+    gp.table.reset();
+    gp.counts.reset();
+  }
+  return fc.release();
+}
+
+}  // namespace lmfao

@@ -118,7 +118,7 @@ __device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __re
           if (lane == nv - 1) {
             double* dst = &V[(int64_t)key * nslots + s];
             if (cstart && !c_any) *dst = t;
-            else atomicAdd(dst, t);
+            else gred_add(dst, t);
             carry[s] = 0.0;
           }
         }
@@ -152,7 +152,7 @@ __device__ __forceinline__ void view_seg_warp(int64_t nrows, const int32_t* __re
         } else {
           double* dst = &V[(int64_t)key * nslots + s];
           if (started_in && !cont) *dst = x;  // the run lies inside this warp's range
-          else atomicAdd(dst, x);
+          else gred_add(dst, x);
         }
       }
       __syncwarp();
@@ -367,10 +367,10 @@ __global__ void k_root_group(NodeArgs a, GroupArgs g, const int32_t* __restrict_
       int32_t code = cc < 0 ? g.code[i][row] : g.code[i][kk[cc]];
       cell += (int64_t)code * g.stride[i];
     }
-    atomicAdd(&counts[cell], (unsigned long long)w);
+    gred_add(&counts[cell], (unsigned long long)w);
     for (int j = 0; j < nudaf; j++) {
       double v = eval_output(a, row, kk, prog_i + ioff[j], prog_d + doff[j]);
-      if (v != 0.0) atomicAdd(&table[cell * nudaf + j], v);
+      if (v != 0.0) gred_add(&table[cell * nudaf + j], v);
     }
   }
 }
@@ -428,9 +428,9 @@ __global__ void k_groups_fused(NodeArgs a, const GroupDesc* descs, int nq,
       }
       if (ones) {
         const unsigned peers = __match_any_sync(0xffffffffu, cell);
-        if (cell >= 0 && (__ffs(peers) - 1) == lane) atomicAdd(&d.counts[cell], (unsigned long long)__popc(peers));
+        if (cell >= 0 && (__ffs(peers) - 1) == lane) gred_add(&d.counts[cell], (unsigned long long)__popc(peers));
       } else if (cell >= 0) {
-        atomicAdd(&d.counts[cell], (unsigned long long)w);
+        gred_add(&d.counts[cell], (unsigned long long)w);
       }
       // non-constant UDAFs: the root is sorted by its keys, so equal cells mostly sit in
       // runs of adjacent lanes; a segmented warp scan sums each run and its last lane
@@ -452,7 +452,7 @@ __global__ void k_groups_fused(NodeArgs a, const GroupDesc* descs, int nq,
           const double u = __shfl_up_sync(0xffffffffu, v, dd);
           if (lane - dd >= s0) v += u;
         }
-        if (tail && cell >= 0 && v != 0.0) atomicAdd(&d.table[cell * d.nudaf + j], v);
+        if (tail && cell >= 0 && v != 0.0) gred_add(&d.table[cell * d.nudaf + j], v);
       }
     }
   }

@@ -23,6 +23,25 @@
 
 namespace lmfao {
 
+#ifdef __CUDACC__
+// Reductions without a return value on a known state space.  Pointers that come from
+// kernel-argument structs or shared-memory descriptors are generic to the compiler, which
+// then emits a generic ATOM that waits for its result (to branch to a shared-memory CAS
+// loop); these emit RED, which the SM issues and forgets.
+__device__ __forceinline__ void gred_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void gred_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void gred_add(unsigned* p, unsigned v) {
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sred_add(double* p, double v) {
+  asm volatile("red.shared.add.f64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "d"(v) : "memory");
+}
+#endif
+
 // LMFAO_TRACE=1: wall-clock checkpoints of the host-side phases on stderr (tools/e2e_phases.py).
 struct PhaseTrace {
   bool on;

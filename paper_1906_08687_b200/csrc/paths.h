@@ -18,6 +18,8 @@ struct FastPaths {
   virtual bool handles_all_groups() const { return false; }
   // true if the specialised path builds its own dimension tables (skip generic views)
   virtual bool skip_generic_views() const { return false; }
+  // false if run() synchronises with the host (data-dependent sizes): no CUDA Graph capture
+  virtual bool graph_ok() const { return true; }
   virtual std::string describe() const = 0;
 };
 // Returns nullptr when no specialised path applies (the generic path runs).
@@ -26,4 +28,5 @@ FastPaths* plan_gram(lmfao_ctx* c);
 FastPaths* plan_cov(lmfao_ctx* c);
 FastPaths* plan_rt(lmfao_ctx* c);
 FastPaths* plan_counts(lmfao_ctx* c);
+FastPaths* plan_cube(lmfao_ctx* c);  // group-by queries only (scalar queries: another path)
 }  // namespace lmfao

@@ -144,9 +144,9 @@ __global__ void __launch_bounds__(256) k_rt_fact(const __grid_constant__ RtFactA
       t2 += __shfl_xor_sync(RFULL, t2, o);
     }
     if (lane == 0) {
-      atomicAdd(a.out, t0);
-      atomicAdd(a.out + 1, t1);
-      atomicAdd(a.out + 2, t2);
+      gred_add(a.out, t0);
+      gred_add(a.out + 1, t1);
+      gred_add(a.out + 2, t2);
     }
   }
   __syncthreads();
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256) k_rt_fact(const __grid_constant__ RtFactA
         for (int l = 0; l < 32; l++) s += tv[l];
       }
     }
-    if (s != 0.0) atomicAdd(a.out + h.goff + i, s);
+    if (s != 0.0) gred_add(a.out + h.goff + i, s);
   }
 }
 
@@ -199,14 +199,14 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
     if (a.in_smem) {
       atomicAdd(&cnt[c], 1u);
       if (a.y) {
-        atomicAdd(&sums[2 * c], y);
-        atomicAdd(&sums[2 * c + 1], y * y);
+        sred_add(&sums[2 * c], y);
+        sred_add(&sums[2 * c + 1], y * y);
       }
     } else {
-      atomicAdd(a.out + 3 * (int64_t)c, 1.0);
+      gred_add(a.out + 3 * (int64_t)c, 1.0);
       if (a.y) {
-        atomicAdd(a.out + 3 * (int64_t)c + 1, y);
-        atomicAdd(a.out + 3 * (int64_t)c + 2, y * y);
+        gred_add(a.out + 3 * (int64_t)c + 1, y);
+        gred_add(a.out + 3 * (int64_t)c + 2, y * y);
       }
     }
   }
@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
   __syncthreads();
   for (int i = threadIdx.x; i < a.ncell; i += blockDim.x) {
     if (!cnt[i]) continue;
-    atomicAdd(a.out + 3 * (int64_t)i, (double)cnt[i]);
-    atomicAdd(a.out + 3 * (int64_t)i + 1, sums[2 * i]);
-    atomicAdd(a.out + 3 * (int64_t)i + 2, sums[2 * i + 1]);
+    gred_add(a.out + 3 * (int64_t)i, (double)cnt[i]);
+    gred_add(a.out + 3 * (int64_t)i + 1, sums[2 * i]);
+    gred_add(a.out + 3 * (int64_t)i + 2, sums[2 * i + 1]);
   }
 }
 
@@ -257,17 +257,17 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
       }
       if (t == key) {
         double* e = hval + 3 * (l * RT_HT + h);
-        atomicAdd(e, v0);
-        atomicAdd(e + 1, v1);
-        atomicAdd(e + 2, v2);
+        sred_add(e, v0);
+        sred_add(e + 1, v1);
+        sred_add(e + 2, v2);
         return;
       }
       h = (h + 1) & (RT_HT - 1);
     }
     double* e = a.V[l] + 3 * (int64_t)key;
-    atomicAdd(e, v0);
-    atomicAdd(e + 1, v1);
-    atomicAdd(e + 2, v2);
+    gred_add(e, v0);
+    gred_add(e + 1, v1);
+    gred_add(e + 2, v2);
   };
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -360,9 +360,9 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     if (key < 0) continue;
     const int l = i / RT_HT;
     double* e = a.V[l] + 3 * (int64_t)key;
-    atomicAdd(e, hval[3 * i]);
-    atomicAdd(e + 1, hval[3 * i + 1]);
-    atomicAdd(e + 2, hval[3 * i + 2]);
+    gred_add(e, hval[3 * i]);
+    gred_add(e + 1, hval[3 * i + 1]);
+    gred_add(e + 2, hval[3 * i + 2]);
   }
 }
 
@@ -401,9 +401,9 @@ __global__ void k_rt_dims(const __grid_constant__ RtDimArgs a) {
       c = rt_cell(x, a.thr + h.thr_off, h.nthr);
     }
     double* e = a.out + h.goff + 3 * (int64_t)c;
-    atomicAdd(e, v0);
-    atomicAdd(e + 1, V[3 * k + 1]);
-    atomicAdd(e + 2, V[3 * k + 2]);
+    gred_add(e, v0);
+    gred_add(e + 1, V[3 * k + 1]);
+    gred_add(e + 2, V[3 * k + 2]);
   }
 }
 

@@ -110,10 +110,18 @@ def test_gram_matches_generic_path(monkeypatch):
     assert np.allclose(g1[0][1], g2[0][1], rtol=1e-11, atol=1e-9)
 
 
-def test_config5_covariance_uses_gram_with_cube_generic(kernel):
+@pytest.mark.parametrize("cube", [True, False])
+def test_config5_covariance_uses_gram_with_cube(kernel, cube, monkeypatch):
+    """C5: the covariance scan next to the cube path (cube.cu), or next to the generic group scan."""
+    if not cube:
+        monkeypatch.setenv("LMFAO_NO_CUBE", "1")
     w = synth.config5(fact_rows=30_011, dim_rows=(40, 300, 2000, 9000), cube_doms=(7, 30, 100))
     gpu, info = run_gpu(w.db, w.batch, info=True)
-    assert info["fast_path"]["kind"] == kernel
+    fp = info["fast_path"]
+    if cube:
+        assert fp["kind"] == "combo" and fp["scalar"]["kind"] == kernel and fp["groups"]["kind"] == "cube", fp
+    else:
+        assert fp["kind"] == kernel, fp
     assert_parity(gpu, oracle.evaluate(w.db, w.batch), w.batch)
 
 
