@@ -648,6 +648,12 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   if (c->state != S_PREPARED) return fail(c, LMFAO_ERR_STATE, "plan needs prepare (and runs once)");
   cudaSetDevice(c->device);
   StreamScope scope_(c->stream);
+  // LMFAO_PLAIN_SITES (A/B): plan-time allocations from plain cudaMalloc instead of the pool,
+  // bit 1 group tables, 2 code sets, 4 specialised paths, 8 views and programs
+  const int plain_sites = [] {
+    const char* e = std::getenv("LMFAO_PLAIN_SITES");
+    return e ? std::atoi(e) : 0;
+  }();
   cudaStream_t st = c->stream;
   PhaseTrace tr("plan");
   c->nodes.clear();
@@ -691,6 +697,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       p.ip.push_back(1);
       emit_term(p, c, u, 1.0, s.own, s.child_slots);
     }
+    StreamScope vs(st, !(plain_sites & 8));
     CTX_CUDA(c, np.prog.upload(p, st), "plan upload view program");
     CTX_CUDA(c, np.V.alloc(std::max<int64_t>(c->rels[u].nkeys, 1) * np.slots.size() * 8), "plan alloc view");
     {  // leaf child with slots of <= 2 identity factors: the linear view kernel
@@ -739,6 +746,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       const Rel& r = c->rels[o];
       std::shared_ptr<CodeSet>& cs = c->code_cache[a];
       if (!cs) {
+        StreamScope cs_scope(st, !(plain_sites & 2));
         cs = std::make_shared<CodeSet>();
         DevBuf& dict = cs->dict;
         DevBuf& codes = cs->codes;
@@ -782,8 +790,11 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     gp.ncells = cells;
     if ((double)cells * (gp.nudaf + 1) * 8 > 40e9)
       return fail(c, LMFAO_ERR_UNSUPPORTED, "dense group-by table too large (%lld cells)", (long long)cells);
-    CTX_CUDA(c, gp.table.alloc(cells * std::max(gp.nudaf, 1) * 8), "plan group table");
-    CTX_CUDA(c, gp.counts.alloc(cells * 8), "plan group counts");
+    {
+      StreamScope ts(st, !(plain_sites & 1));
+      CTX_CUDA(c, gp.table.alloc(cells * std::max(gp.nudaf, 1) * 8), "plan group table");
+      CTX_CUDA(c, gp.counts.alloc(cells * 8), "plan group counts");
+    }
     CTX_CUDA(c, gp.prog.upload(gprogs[c->query_slot[q]], st), "plan upload group");
   }
   // fused group-by scan: one combined program, one descriptor per group-by query
@@ -847,7 +858,10 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   }
   tr.mark("group plans", st);
   // specialised kernels for recognised batch shapes (gram.cu / hist.cu)
-  c->fast.reset(plan_fast_paths(c));
+  {
+    StreamScope fs(st, !(plain_sites & 4));
+    c->fast.reset(plan_fast_paths(c));
+  }
   tr.mark("fast paths", st);
   c->state = S_PLANNED;
   return LMFAO_OK;

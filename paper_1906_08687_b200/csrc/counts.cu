@@ -76,14 +76,14 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
       if (!a.H[l]) continue;
       const int k = v ? key[l] : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, k);
-      if (v && (__ffs(peers) - 1) == lane) gred_add(&a.H[l][k], (unsigned)__popc(peers));
+      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&a.H[l][k], (unsigned)__popc(peers));
     }
     for (int qi = 0; qi < a.nq; qi++) {
       const CntQuery q = sq[qi];
       const int ca = scode[wib][q.a][lane], cb = q.b >= 0 ? scode[wib][q.b][lane] : 0;
       const int cell = v ? ca * q.sa + cb : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, cell);
-      if (v && (__ffs(peers) - 1) == lane) gred_add(&q.counts[cell], (unsigned long long)__popc(peers));
+      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&q.counts[cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
     }
     __syncwarp();
   }

@@ -76,7 +76,13 @@ inline AllocScope& alloc_scope() {
 }
 struct StreamScope {
   AllocScope prev;
-  StreamScope(cudaStream_t st, bool pooled = true) : prev(alloc_scope()) { alloc_scope() = AllocScope{st, pooled}; }
+  StreamScope(cudaStream_t st, bool pooled = true) : prev(alloc_scope()) {
+    static const bool off = [] {  // LMFAO_NO_POOL=1: plain cudaMalloc / cudaFree (A/B measurements)
+      const char* e = std::getenv("LMFAO_NO_POOL");
+      return e && e[0] == '1';
+    }();
+    alloc_scope() = AllocScope{st, pooled && !off};
+  }
   ~StreamScope() { alloc_scope() = prev; }
   StreamScope(const StreamScope&) = delete;
   StreamScope& operator=(const StreamScope&) = delete;

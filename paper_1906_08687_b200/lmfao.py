@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblmfao_gpu.so")
+LIB_PATH = os.environ.get("LMFAO_LIB") or os.path.join(_HERE, "liblmfao_gpu.so")  # LMFAO_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1906_08687_b200.build` "
