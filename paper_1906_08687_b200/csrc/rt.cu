@@ -43,9 +43,11 @@ struct FactHist {
   int ncell;
   int uniform;      // thresholds t_i = t_0 + i h exactly (cell estimate + exact fix-up)
   double t0, inv_h;
+  double margin;    // max_i |t_i - (t_0 + i h)| / h + 1e-9: estimates farther than this from an integer are exact
   int64_t goff;     // global offset (doubles) of the [ncell][3] table in the output buffer
 };
-constexpr int RT_SMALL = 41;  // cells of a histogram kept in per-lane private tables
+constexpr int RT_SMALL = 21;  // lane cells of a histogram kept in per-lane private tables
+constexpr int RT_FACT_WARPS = 16;
 struct RtFactArgs {
   int64_t nrows;
   const double* y;  // null: w = (1, 0, 0)
@@ -54,6 +56,7 @@ struct RtFactArgs {
   FactHist h[RT_MAX_FACT];
   const double* thr;  // thresholds, all attributes
   double* out;        // global accumulators (TOT at 0)
+  int eq_off, tab_off;  // shared memory (doubles): thresholds | equality cells | lane tables
 };
 
 __device__ __forceinline__ int rt_cell(double x, const double* t, int n) {
@@ -75,98 +78,157 @@ __device__ __forceinline__ int rt_cell_uniform(double x, const double* t, int n,
   return (lo < n && t[lo] == x) ? 2 * lo + 1 : 2 * lo;
 }
 
-// Root rows: one histogram per CTA (blockIdx = part * nh + h: the CTAs of one row part run
-// side by side, so y is read from HBM once and from L2 by the others).  Small histograms
-// (<= RT_SMALL cells) use per-lane private tables in shared memory — plain conflict-free
-// read-modify-write, no atomics — summed over the CTA at the end; TOT is accumulated by
-// the CTAs of histogram 0.
-__global__ void __launch_bounds__(256) k_rt_fact(const __grid_constant__ RtFactArgs a) {
+// Threshold cell without memory traffic when the estimate is safely between two thresholds:
+// with g = (x - t_0) / h and |t_i - (t_0 + i h)| <= μ h, t_i < x iff i < g whenever g is more
+// than μ from every integer, so #{t_i < x} = clamp(floor(g + 1), 0, n) and x equals no t_i.
+// Rounding of e is ~1e-15 absolute for |e| <= n + 1 (the margin adds 1e-9); the rest take
+// the exact fix-up.
+__device__ __forceinline__ int rt_cell_fast(double x, const double* t, int n, double t0, double inv_h,
+                                            double margin) {
+  const double e = (x - t0) * inv_h + 1.0;
+  if (fabs(e - rint(e)) > margin && fabs(e) < 1e9) {  // NaN compares false: exact path
+    const double f = floor(e);
+    const int lo = f < 0.0 ? 0 : (f > (double)n ? n : (int)f);
+    return 2 * lo;
+  }
+  return rt_cell_uniform(x, t, n, t0, inv_h);
+}
+
+// Root rows, all histograms: the (histogram, row) space is cut into equal contiguous pieces,
+// one per CTA (so every CTA has the same work and at most a few histogram switches, each a
+// flush of its tables).  Small histograms (<= RT_SMALL cells) use per-lane private tables in
+// shared memory — plain conflict-free read-modify-write, no atomics — with one spare cell for
+// rows past the end; rows are taken in pairs whose table updates are issued together (a pair
+// in the same cell is merged first), summed over the CTA at each flush.  TOT comes from the
+// pieces of histogram 0.
+__global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_constant__ RtFactArgs a) {
   extern __shared__ double rsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int hi = blockIdx.x % a.nh, part = blockIdx.x / a.nh;
-  const FactHist& h = a.h[hi];
-  const int nc = h.ncell;
-  // per warp: [nc][32] u32 counts, [nc][32] y, [nc][32] y^2
   double* thr = rsm;
-  const int tslot = (h.nthr + 1) & ~1;
-  unsigned char* wt = reinterpret_cast<unsigned char*>(rsm + tslot) + (size_t)wib * nc * 32 * 20;
-  unsigned* tc = reinterpret_cast<unsigned*>(wt);
-  double* ty = reinterpret_cast<double*>(wt + nc * 32 * 4);
-  double* ty2 = ty + nc * 32;
-  for (int i = threadIdx.x; i < h.nthr; i += blockDim.x) thr[i] = a.thr[h.thr_off + i];
-  for (int i = lane; i < nc * 32; i += 32) {
-    tc[i] = 0;
-    ty[i] = 0.0;
-    ty2[i] = 0.0;
-  }
-  __syncthreads();
-  const int64_t r0 = a.nrows * part / a.nparts, r1 = a.nrows * (part + 1) / a.nparts;
-  double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-  constexpr int U = 16;  // rows per lane per step: all loads issued before the table updates
-  for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
-    double yv[U], xv[U];
-    int cv[U];
+  double* eqt = rsm + a.eq_off;  // [nthr][3] rows equal to a threshold (rare: shared atomics)
+  const int64_t N = a.nrows, W = (a.nh * N + gridDim.x - 1) / gridDim.x;
+  const int64_t L0 = (int64_t)blockIdx.x * W, L1 = L0 + W < a.nh * N ? L0 + W : a.nh * N;
+  for (int64_t L = L0; L < L1;) {
+    const int hi = (int)(L / N);
+    const int64_t r0 = L - (int64_t)hi * N;
+    const int64_t r1 = L1 - (int64_t)hi * N < N ? L1 - (int64_t)hi * N : N;
+    L = (int64_t)hi * N + r1;
+    const FactHist& h = a.h[hi];
+    // lane cells: the group-by codes, or the nthr + 1 intervals between thresholds (cell 2b
+    // of the histogram); a row equal to threshold i (cell 2i + 1) goes to eqt
+    const int nc = h.is_code ? h.ncell : h.nthr + 1, ncp = nc + 1;  // + the spare cell
+    // per warp: [ncp][32] u32 counts, [ncp][32] y, [ncp][32] y^2
+    unsigned char* wt = reinterpret_cast<unsigned char*>(rsm + a.tab_off) + (size_t)wib * ncp * 32 * 20;
+    unsigned* tc = reinterpret_cast<unsigned*>(wt);
+    double* ty = reinterpret_cast<double*>(wt + ncp * 32 * 4);
+    double* ty2 = ty + ncp * 32;
+    __syncthreads();  // the previous piece's flush is done with the tables
+    for (int i = threadIdx.x; i < h.nthr; i += blockDim.x) thr[i] = a.thr[h.thr_off + i];
+    for (int i = threadIdx.x; i < 3 * h.nthr; i += blockDim.x) eqt[i] = 0.0;
+    for (int i = lane; i < ncp * 32; i += 32) {
+      tc[i] = 0;
+      ty[i] = 0.0;
+      ty2[i] = 0.0;
+    }
+    __syncthreads();
+    double t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    constexpr int U = 16;  // rows per lane per step: all loads issued before the table updates
+    for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
+      double yv[U], xv[U];
+      int cv[U];
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int64_t row = base + 32 * u;
-      const bool v = row < r1;
-      yv[u] = (v && a.y) ? a.y[row] : 0.0;
-      cv[u] = -1;
-      xv[u] = 0.0;
-      if (v) {
-        if (h.is_code) cv[u] = reinterpret_cast<const int32_t*>(h.col)[row];
-        else xv[u] = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
-                              : reinterpret_cast<const double*>(h.col)[row];
+      for (int u = 0; u < U; u++) {
+        const int64_t row = base + 32 * u;
+        const bool v = row < r1;
+        yv[u] = (v && a.y) ? a.y[row] : 0.0;
+        cv[u] = -1;
+        xv[u] = 0.0;
+        if (v) {
+          if (h.is_code) cv[u] = reinterpret_cast<const int32_t*>(h.col)[row];
+          else xv[u] = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
+                                : reinterpret_cast<const double*>(h.col)[row];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        int e[2];
+        double n[2], yy[2], q[2];
+#pragma unroll
+        for (int z = 0; z < 2; z++) {
+          const bool v = base + 32 * (u + z) < r1;
+          int c = cv[u + z];
+          bool eq = false;
+          if (v && !h.is_code) {
+            c = h.uniform ? rt_cell_fast(xv[u + z], thr, h.nthr, h.t0, h.inv_h, h.margin) : rt_cell(xv[u + z], thr, h.nthr);
+            eq = c & 1;
+            c >>= 1;
+          }
+          n[z] = v ? 1.0 : 0.0;
+          yy[z] = yv[u + z];
+          q[z] = yy[z] * yy[z];
+          t0 += n[z];
+          t1 += yy[z];
+          t2 += q[z];
+          if (eq) {  // x equals threshold c: rare for continuous data
+            double* et = eqt + 3 * c;
+            sred_add(et, 1.0);
+            sred_add(et + 1, yy[z]);
+            sred_add(et + 2, q[z]);
+            n[z] = yy[z] = q[z] = 0.0;
+          }
+          e[z] = (v && !eq ? c : nc) * 32 + lane;
+        }
+        if (e[0] == e[1]) {  // merge into the first; the second writes its old value back
+          n[0] += n[1];
+          yy[0] += yy[1];
+          q[0] += q[1];
+          n[1] = yy[1] = q[1] = 0.0;
+        }
+        const unsigned c0 = tc[e[0]], c1 = tc[e[1]];
+        const double y0 = ty[e[0]], y1 = ty[e[1]], s0 = ty2[e[0]], s1 = ty2[e[1]];
+        tc[e[1]] = c1 + (unsigned)n[1];
+        ty[e[1]] = y1 + yy[1];
+        ty2[e[1]] = s1 + q[1];
+        tc[e[0]] = c0 + (unsigned)n[0];
+        ty[e[0]] = y0 + yy[0];
+        ty2[e[0]] = s0 + q[0];
       }
     }
+    if (hi == 0) {
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      if (base + 32 * u >= r1) continue;
-      const double y = yv[u];
-      int c = cv[u];
-      if (!h.is_code) c = h.uniform ? rt_cell_uniform(xv[u], thr, h.nthr, h.t0, h.inv_h) : rt_cell(xv[u], thr, h.nthr);
-      const int e = c * 32 + lane;
-      tc[e] += 1u;
-      ty[e] += y;
-      ty2[e] += y * y;
-      if (hi == 0) {
-        t0 += 1.0;
-        t1 += y;
-        t2 += y * y;
+      for (int o = 16; o > 0; o >>= 1) {
+        t0 += __shfl_xor_sync(RFULL, t0, o);
+        t1 += __shfl_xor_sync(RFULL, t1, o);
+        t2 += __shfl_xor_sync(RFULL, t2, o);
+      }
+      if (lane == 0) {
+        gred_add(a.out, t0);
+        gred_add(a.out + 1, t1);
+        gred_add(a.out + 2, t2);
       }
     }
-  }
-  if (hi == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      t0 += __shfl_xor_sync(RFULL, t0, o);
-      t1 += __shfl_xor_sync(RFULL, t1, o);
-      t2 += __shfl_xor_sync(RFULL, t2, o);
-    }
-    if (lane == 0) {
-      gred_add(a.out, t0);
-      gred_add(a.out + 1, t1);
-      gred_add(a.out + 2, t2);
-    }
-  }
-  __syncthreads();
-  // Σ over the CTA's warps and lanes -> global
-  const unsigned char* base = reinterpret_cast<const unsigned char*>(rsm + tslot);
-  for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
-    const int cell = i / 3, v = i % 3;
-    double s = 0.0;
-    for (int w = 0; w < nw; w++) {
-      const unsigned char* ww = base + (size_t)w * nc * 32 * 20;
-      if (v == 0) {
-        unsigned long long cs = 0;
-        for (int l = 0; l < 32; l++) cs += reinterpret_cast<const unsigned*>(ww)[cell * 32 + l];
-        s += (double)cs;
-      } else {
-        const double* tv = reinterpret_cast<const double*>(ww + nc * 32 * 4) + (v - 1) * nc * 32 + cell * 32;
-        for (int l = 0; l < 32; l++) s += tv[l];
+    __syncthreads();
+    // Σ over the CTA's warps and lanes -> global (the spare cell is dropped)
+    for (int i = threadIdx.x; i < 3 * h.nthr; i += blockDim.x)
+      if (eqt[i] != 0.0) gred_add(a.out + h.goff + 3 * (2 * (i / 3) + 1) + i % 3, eqt[i]);
+    const unsigned char* tb = reinterpret_cast<const unsigned char*>(rsm + a.tab_off);
+    for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) {
+      const int cell = i / 3, v = i % 3;
+      double sum = 0.0;
+      for (int w = 0; w < nw; w++) {
+        const unsigned char* ww = tb + (size_t)w * ncp * 32 * 20;
+        if (v == 0) {
+          unsigned long long cs = 0;
+          for (int l = 0; l < 32; l++) cs += reinterpret_cast<const unsigned*>(ww)[cell * 32 + l];
+          sum += (double)cs;
+        } else {
+          const double* tv = reinterpret_cast<const double*>(ww + ncp * 32 * 4) + (v - 1) * ncp * 32 + cell * 32;
+          for (int l = 0; l < 32; l++) sum += tv[l];
+        }
       }
+      const int oc = h.is_code ? cell : 2 * cell;
+      if (sum != 0.0) gred_add(a.out + h.goff + 3 * oc + v, sum);
     }
-    if (s != 0.0) gred_add(a.out + h.goff + i, s);
   }
 }
 
@@ -455,6 +517,7 @@ struct FastRT : FastPaths {
   const double* y = nullptr;
   int nout = 0, ngq = 0;
   size_t fact_smem = 0, view_smem = 0;
+  int eq_off = 0, tab_off = 0;
   int64_t vtotal = 0;
   std::string describe() const override {
     char b[200];
@@ -483,10 +546,12 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
   fa.nparts = nparts;
   for (size_t i = 0; i < fh.size(); i++) fa.h[i] = fh[i];
   fa.thr = dthr.as<double>();
+  fa.eq_off = eq_off;
+  fa.tab_off = tab_off;
   fa.out = acc.as<double>();
   scan_timer_begin(c, st);
   if (R.nrows > 0) {
-    k_rt_fact<<<nparts * fa.nh, 256, fact_smem, st>>>(fa);
+    k_rt_fact<<<nparts, RT_FACT_WARPS * 32, fact_smem, st>>>(fa);
     launches_add(1);
   }
   scan_timer_end(c, st);
@@ -663,14 +728,17 @@ FastPaths* plan_rt(lmfao_ctx* c) {
         const double step = (tl - t0) / (nthr - 1);
         bool ok = step > 0.0 && std::isfinite(step);
         int i = 0;
-        for (double t : kv.second) ok = ok && std::fabs(t - (t0 + i++ * step)) <= step;
+        double mu = 0.0;
+        for (double t : kv.second) mu = std::max(mu, std::fabs(t - (t0 + i++ * step)) / step);
+        ok = ok && mu <= 0.25;
         if (ok) {
           h.uniform = 1;
           h.t0 = t0;
           h.inv_h = 1.0 / step;
+          h.margin = mu + 1e-9;
         }
       }
-      if (ncell <= RT_SMALL) rt->fh.push_back(h);
+      if (nthr + 1 <= RT_SMALL) rt->fh.push_back(h);
       else rt->fbig.push_back(h);  // (predicate with > 20 thresholds: not expected; handled below)
     } else {
       const Rel& D = c->rels[R.children[lv]];
@@ -744,11 +812,17 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     rt->fh.push_back(h);
   }
   rt->nacc = nacc;
-  rt->nparts = std::max(1, (148 * 2 + (int)rt->fh.size() - 1) / (int)rt->fh.size());
+  {  // one CTA per SM over equal pieces of the (histogram, row) space (the tables fill shared memory)
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    rt->nparts = nsm;
+  }
   {
     int maxthr = 0;
     for (auto& h : rt->fh) maxthr = std::max(maxthr, h.nthr);
-    rt->fact_smem = (size_t)((maxthr + 1) & ~1) * 8 + (size_t)8 * RT_SMALL * 32 * 20;
+    rt->eq_off = (maxthr + 1) & ~1;
+    rt->tab_off = rt->eq_off + ((3 * maxthr + 1) & ~1);
+    rt->fact_smem = (size_t)rt->tab_off * 8 + (size_t)RT_FACT_WARPS * (RT_SMALL + 1) * 32 * 20;
   }
   // views
   int64_t vt = 0;
