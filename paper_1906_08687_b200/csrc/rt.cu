@@ -337,10 +337,15 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
   const int64_t b0 = nblk * gw / nwarps, b1 = nblk * (gw + 1) / nwarps;
   int ckey[NLEV];
   double c0[NLEV], c1[NLEV], c2[NLEV];
+  // lane-private sums of the carried run over blocks it goes on through (folded when it ends)
+  double p0[NLEV], p1[NLEV], p2[NLEV];
+  bool dirty[NLEV];
 #pragma unroll
   for (int l = 0; l < NLEV; l++) {
     ckey[l] = -1;
     c0[l] = c1[l] = c2[l] = 0.0;
+    p0[l] = p1[l] = p2[l] = 0.0;
+    dirty[l] = false;
   }
   // software pipeline: the next block's y and keys are loaded while this block is scanned
   double ny = 0.0;
@@ -371,17 +376,26 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
       if (lane == 0) prev = ckey[l];
       const unsigned heads = __ballot_sync(RFULL, vr && key != prev);
       double v0 = w0, v1 = w1, v2 = w2;
-      if (heads == 0) {  // the carried run goes on through the block
+      if (heads == 0) {  // the carried run goes on through the block: lane-private sums
+        p0[l] += v0;
+        p1[l] += v1;
+        p2[l] += v2;
+        dirty[l] = true;
+        continue;
+      }
+      if (dirty[l]) {  // a run starts here: fold the lane-private sums into the carried run
+        double q0 = p0[l], q1 = p1[l], q2 = p2[l];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          v0 += __shfl_xor_sync(RFULL, v0, o);
-          v1 += __shfl_xor_sync(RFULL, v1, o);
-          v2 += __shfl_xor_sync(RFULL, v2, o);
+          q0 += __shfl_xor_sync(RFULL, q0, o);
+          q1 += __shfl_xor_sync(RFULL, q1, o);
+          q2 += __shfl_xor_sync(RFULL, q2, o);
         }
-        c0[l] += v0;
-        c1[l] += v1;
-        c2[l] += v2;
-        continue;
+        c0[l] += q0;
+        c1[l] += q1;
+        c2[l] += q2;
+        p0[l] = p1[l] = p2[l] = 0.0;
+        dirty[l] = false;
       }
       // segmented inclusive scan; segment s0 = the run containing the lane
       const unsigned upto = heads & ((2u << lane) - 1u);
@@ -414,8 +428,20 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     }
   }
 #pragma unroll
-  for (int l = 0; l < NLEV; l++)
+  for (int l = 0; l < NLEV; l++) {
+    if (dirty[l]) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p0[l] += __shfl_xor_sync(RFULL, p0[l], o);
+        p1[l] += __shfl_xor_sync(RFULL, p1[l], o);
+        p2[l] += __shfl_xor_sync(RFULL, p2[l], o);
+      }
+      c0[l] += p0[l];
+      c1[l] += p1[l];
+      c2[l] += p2[l];
+    }
     if (lane == 0 && ckey[l] >= 0) add(l, ckey[l], c0[l], c1[l], c2[l]);
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < a.nlev * RT_HT; i += blockDim.x) {
     const int key = hkey[i];
