@@ -472,26 +472,67 @@ struct RtDimArgs {
   const double* thr;
   double* out;
 };
-__global__ void k_rt_dims(const __grid_constant__ RtDimArgs a) {
+constexpr int RT_DIM_CELLS = 64;  // histograms up to this many cells: per-warp shared tables
+__global__ void __launch_bounds__(256) k_rt_dims(const __grid_constant__ RtDimArgs a) {
+  __shared__ double wtab[8][RT_DIM_CELLS * 3];
   const int i = blockIdx.y;
   const DimHist& h = a.h[i];
   const double* V = a.V[h.level];
   const int64_t nk = a.nk[h.level];
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nk; k += (int64_t)gridDim.x * blockDim.x) {
-    const double v0 = V[3 * k];
-    if (v0 == 0.0) continue;
-    int c;
-    if (h.is_code) {
-      c = reinterpret_cast<const int32_t*>(h.col)[k];
-    } else {
-      const double x = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[k]
-                                : reinterpret_cast<const double*>(h.col)[k];
-      c = rt_cell(x, a.thr + h.thr_off, h.nthr);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool small = h.ncell <= RT_DIM_CELLS;  // CTA-uniform
+  double* tab = wtab[wib];
+  if (small) {
+    for (int k = lane; k < h.ncell * 3; k += 32) tab[k] = 0.0;
+    __syncwarp();
+  }
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); base < nk; base += stride) {
+    const int64_t k = base + lane;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    int c = -1;
+    if (k < nk) {
+      v0 = V[3 * k];
+      if (v0 != 0.0) {
+        v1 = V[3 * k + 1];
+        v2 = V[3 * k + 2];
+        if (h.is_code) {
+          c = reinterpret_cast<const int32_t*>(h.col)[k];
+        } else {
+          const double x = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[k]
+                                    : reinterpret_cast<const double*>(h.col)[k];
+          c = rt_cell(x, a.thr + h.thr_off, h.nthr);
+        }
+      }
     }
-    double* e = a.out + h.goff + 3 * (int64_t)c;
-    gred_add(e, v0);
-    gred_add(e + 1, V[3 * k + 1]);
-    gred_add(e + 2, V[3 * k + 2]);
+    if (!small) {  // large domains: few collisions, fire-and-forget global reductions
+      if (c >= 0) {
+        double* e = a.out + h.goff + 3 * (int64_t)c;
+        gred_add(e, v0);
+        gred_add(e + 1, v1);
+        gred_add(e + 2, v2);
+      }
+      continue;
+    }
+    // lanes with the same cell take turns (rank among their peers): plain read-modify-write
+    const unsigned peers = __match_any_sync(RFULL, c);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    const int rounds = __reduce_max_sync(RFULL, c >= 0 ? rank + 1 : 0);
+    for (int r = 0; r < rounds; r++) {
+      if (c >= 0 && rank == r) {
+        tab[3 * c] += v0;
+        tab[3 * c + 1] += v1;
+        tab[3 * c + 2] += v2;
+      }
+      __syncwarp();
+    }
+  }
+  if (!small) return;
+  __syncthreads();
+  for (int k = threadIdx.x; k < h.ncell * 3; k += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < 8; w++) s += wtab[w][k];
+    if (s != 0.0) gred_add(a.out + h.goff + k, s);
   }
 }
 
@@ -623,7 +664,7 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
     }
     da.thr = dthr.as<double>();
     da.out = acc.as<double>();
-    k_rt_dims<<<dim3(64, (unsigned)dh.size()), 256, 0, st>>>(da);
+    k_rt_dims<<<dim3(16, (unsigned)dh.size()), 256, 0, st>>>(da);
     launches_add(1);
   }
   if (nout > 0) {
