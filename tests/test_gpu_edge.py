@@ -1,4 +1,4 @@
-"""Degenerate inputs through every specialised path (cov.cu, gram.cu, rt.cu, counts.cu) and
+"""Degenerate inputs through every specialised path (cov.cu, gram.cu, rt.cu, counts.cu, cube.cu) and
 the view kernels: a root whose rows all dangle (empty join), a single-row root, dimensions
 with a single key, and a root that shrinks to one 32-row block after dropping dangling rows."""
 import numpy as np
@@ -37,10 +37,14 @@ def batches(feats):
         "rt": synth.rt_batch(feats[:4], "y", ["g", "c1", "c3"], synth.thresholds_c3()[::5]),
         "counts": [synth.Query(["g", "c2"], [[synth.Product(1.0, ())]]), synth.Query(["c1"], [[synth.Product(1.0, ())]]),
                    synth.Query([], [[synth.Product(1.0, ())]])],
+        "cube": [synth.Query(["c1"], [[synth.Product(1.0, (synth.ident("x0"),))], [synth.Product(1.0, ())]]),
+                 synth.Query(["c1", "c3"], [[synth.Product(2.0, (synth.ident("y"),))]]),
+                 synth.Query(["g", "c2"], [[synth.Product(1.0, (synth.ident("x1"),)), synth.Product(-3.0, ())]]),
+                 synth.Query([], [[synth.Product(1.0, (synth.ident("y"),))]])],
     }
 
 
-@pytest.mark.parametrize("kind", ["cov", "rt", "counts"])
+@pytest.mark.parametrize("kind", ["cov", "rt", "counts", "cube"])
 @pytest.mark.parametrize("case", ["all_dangling", "one_row", "single_keys", "one_block"])
 def test_degenerate(kind, case):
     if case == "all_dangling":
