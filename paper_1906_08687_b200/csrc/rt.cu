@@ -51,6 +51,7 @@ constexpr int RT_FACT_WARPS = 16;
 struct RtFactArgs {
   int64_t nrows;
   const double* y;  // null: w = (1, 0, 0)
+  const uint8_t* filt;  // path condition per root row (null: every row)
   int nh;           // histograms; CTA (part, h) does histogram h over row part `part`
   int nparts;
   FactHist h[RT_MAX_FACT];
@@ -143,11 +144,14 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
     for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
       double yv[U], xv[U];
       int cv[U];
+      bool pv[U];
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int64_t row = base + 32 * u;
         const bool v = row < r1;
-        yv[u] = (v && a.y) ? a.y[row] : 0.0;
+        const bool pass = v && (!a.filt || a.filt[row]);
+        yv[u] = (pass && a.y) ? a.y[row] : 0.0;
+        pv[u] = pass;
         cv[u] = -1;
         xv[u] = 0.0;
         if (v) {
@@ -167,10 +171,10 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
           bool eq = false;
           if (v && !h.is_code) {
             c = h.uniform ? rt_cell_fast(xv[u + z], thr, h.nthr, h.t0, h.inv_h, h.margin) : rt_cell(xv[u + z], thr, h.nthr);
-            eq = c & 1;
+            eq = (c & 1) && pv[u + z];
             c >>= 1;
           }
-          n[z] = v ? 1.0 : 0.0;
+          n[z] = pv[u + z] ? 1.0 : 0.0;  // rows failing the path condition weigh 0
           yy[z] = yv[u + z];
           q[z] = yy[z] * yy[z];
           t0 += n[z];
@@ -245,6 +249,7 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
 struct RtBigArgs {
   int64_t nrows;
   const double* y;
+  const uint8_t* filt;
   const int32_t* code;
   int ncell;
   int in_smem;
@@ -263,6 +268,7 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
   }
   for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
        row += (int64_t)gridDim.x * blockDim.x) {
+    if (a.filt && !a.filt[row]) continue;
     const double y = a.y ? a.y[row] : 0.0;
     const int c = a.code[row];
     if (a.in_smem) {
@@ -298,6 +304,7 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
 struct RtViewArgs {
   int64_t nrows;
   const double* y;
+  const uint8_t* filt;
   int nlev;
   const int32_t* fk[RT_MAX_LEVELS];
   double* V[RT_MAX_LEVELS];  // [nk][3]
@@ -356,11 +363,14 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
   }
   // software pipeline: the next block's y and keys are loaded while this block is scanned
   double ny = 0.0;
+  bool npass = false;
   int nkey[NLEV];
   auto load = [&](int64_t b) {
     const int64_t row = 32 * b + lane;
     const bool v = b < b1 && row < a.nrows;
-    ny = (v && a.y) ? a.y[row] : 0.0;
+    const bool pass = v && (!a.filt || a.filt[row]);
+    ny = pass ? (a.y ? a.y[row] : 0.0) : 0.0;
+    npass = pass;
 #pragma unroll
     for (int l = 0; l < NLEV; l++) nkey[l] = v ? a.fk[l][row] : -2;
   };
@@ -371,11 +381,12 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     const int64_t nrem = a.nrows - 32 * b;
     const int nv = nrem < 32 ? (int)nrem : 32;
     const double y = ny;
+    const bool rp = npass;
     int keys[NLEV];
 #pragma unroll
     for (int l = 0; l < NLEV; l++) keys[l] = nkey[l];
     load(b + 1);
-    const double w0 = vr ? 1.0 : 0.0, w1 = y, w2 = y * y;
+    const double w0 = rp ? 1.0 : 0.0, w1 = y, w2 = y * y;
 #pragma unroll
     for (int l = 0; l < NLEV; l++) {
       const int key = keys[l];
@@ -545,28 +556,73 @@ __global__ void __launch_bounds__(256) k_rt_dims(const __grid_constant__ RtDimAr
 
 // Scalar outputs: out[o] = Σ_t coef_t · acc[idx_t]; group tables: per (query, cell)
 // table[cell][j] = Σ_p coef_{j,p} G[cell][p], counts[cell] = G[cell][0].
+// Path condition φ = Π_i 1[A_i op_i t_i] shared by every product of the batch (a tree node's
+// condition, §3 "Regression trees" P:528-555: α = Π of Kronecker deltas along the
+// path): one byte per root row, dimension attributes read through the foreign keys.
+constexpr int RT_MAX_PHI = 8;
+struct RtPhi {
+  const void* col;  // root column, or dimension column indexed by dense key
+  const int32_t* fk;  // null: root attribute
+  int is_int, kind;
+  double t;
+};
+struct RtFilterArgs {
+  int64_t nrows;
+  int n;
+  RtPhi p[RT_MAX_PHI];
+  uint8_t* out;
+};
+__device__ __forceinline__ bool rt_pred(int kind, double x, double t) {
+  switch (kind) {
+    case LMFAO_F_LT: return x < t;
+    case LMFAO_F_LE: return x <= t;
+    case LMFAO_F_GT: return x > t;
+    case LMFAO_F_GE: return x >= t;
+    case LMFAO_F_EQ: return x == t;
+    default: return x != t;
+  }
+}
+__global__ void k_rt_filter(const __grid_constant__ RtFilterArgs a) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    for (int i = 0; i < a.n; i++) {
+      const RtPhi& p = a.p[i];
+      const int64_t k = p.fk ? (int64_t)p.fk[r] : r;
+      const double x = p.is_int ? (double)reinterpret_cast<const int32_t*>(p.col)[k]
+                                : reinterpret_cast<const double*>(p.col)[k];
+      ok = ok && rt_pred(p.kind, x, p.t);
+    }
+    a.out[r] = ok ? 1 : 0;
+  }
+}
+
 struct RtGroupOut {
   int64_t ncell, goff;
   int nudaf, coff;  // coefficients [nudaf][3] at coef + coff
   double* table;
   unsigned long long* counts;
 };
-__global__ void k_rt_scalar(const double* __restrict__ acc, const int32_t* __restrict__ toff,
-                            const int32_t* __restrict__ tidx, const double* __restrict__ tcoef, int nout,
-                            double* __restrict__ out, unsigned long long* __restrict__ count) {
+// acc: the sums (under the path condition); cnt: the unconditioned accumulators, whose TOT[0]
+// is the join size (the count of the scalar queries)
+__global__ void k_rt_scalar(const double* __restrict__ acc, const double* __restrict__ cnt,
+                            const int32_t* __restrict__ toff, const int32_t* __restrict__ tidx,
+                            const double* __restrict__ tcoef, int nout, double* __restrict__ out,
+                            unsigned long long* __restrict__ count) {
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * acc[tidx[t]];
     out[o] = s;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)acc[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)cnt[0];
 }
-__global__ void k_rt_groups(const double* __restrict__ acc, const RtGroupOut* __restrict__ gq,
-                            const double* __restrict__ coef) {
+// group presence and counts are the join multiplicities (unconditioned, cnt), the UDAF values
+// the sums under the path condition (acc)
+__global__ void k_rt_groups(const double* __restrict__ acc, const double* __restrict__ cnt,
+                            const RtGroupOut* __restrict__ gq, const double* __restrict__ coef) {
   const RtGroupOut g = gq[blockIdx.y];
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < g.ncell; c += (int64_t)gridDim.x * blockDim.x) {
     const double* e = acc + g.goff + 3 * c;
-    g.counts[c] = (unsigned long long)e[0];
+    g.counts[c] = (unsigned long long)cnt[g.goff + 3 * c];
     for (int j = 0; j < g.nudaf; j++) {
       const double* cf = coef + g.coff + 3 * j;
       g.table[c * g.nudaf + j] = cf[0] * e[0] + cf[1] * e[1] + cf[2] * e[2];
@@ -583,6 +639,12 @@ struct FastRT : FastPaths {
   std::vector<DimHist> dh;
   std::vector<double> thr;
   DevBuf dthr, acc, V, toff, tidx, tcoef, gq, gcoef;
+  // path condition: the filter, and the unconditioned pass for the join multiplicities
+  int nphi = 0;
+  RtFilterArgs phi{};
+  DevBuf filt, acc_all, V_all;
+  std::vector<FactHist> fh_cnt;  // TOT + root group histograms
+  std::vector<DimHist> dh_cnt;   // dimension group histograms
   int64_t nacc = 0;
   int nlev = 0;
   int64_t vnk[RT_MAX_LEVELS];
@@ -595,8 +657,10 @@ struct FastRT : FastPaths {
   int64_t vtotal = 0;
   std::string describe() const override {
     char b[200];
-    std::snprintf(b, sizeof b, "{\"kind\": \"rt\", \"fact_hists\": %zu, \"dim_hists\": %zu, \"views\": %d, \"groups\": %zu}",
-                  fh.size(), dh.size(), nlev, handled.size());
+    std::snprintf(b, sizeof b,
+                  "{\"kind\": \"rt\", \"fact_hists\": %zu, \"dim_hists\": %zu, \"views\": %d, \"groups\": %zu, "
+                  "\"path_preds\": %d}",
+                  fh.size(), dh.size(), nlev, handled.size(), nphi);
     return b;
   }
   bool handles_group(int g) const override {
@@ -607,52 +671,92 @@ struct FastRT : FastPaths {
   bool handles_all_groups() const override { return true; }
   bool skip_generic_views() const override { return true; }
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
+  cudaError_t pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const double* yp, double* accp, double* Vp,
+                   const std::vector<FactHist>& fhl, const std::vector<DimHist>& dhl, bool timed);
 };
 
 int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_done) {
   const Rel& R = c->rels[c->root];
-  CUDA_TRY(cudaMemsetAsync(acc.p, 0, nacc * 8, st));
-  if (vtotal) CUDA_TRY(cudaMemsetAsync(V.p, 0, vtotal * 24, st));
+  const uint8_t* fp = nullptr;
+  if (nphi > 0 && R.nrows > 0) {
+    RtFilterArgs f = phi;
+    f.nrows = R.nrows;
+    f.out = filt.as<uint8_t>();
+    k_rt_filter<<<148 * 8, 256, 0, st>>>(f);
+    launches_add(1);
+    fp = filt.as<uint8_t>();
+  }
+  CUDA_TRY(pass(c, st, fp, y, acc.as<double>(), V.as<double>(), fh, dh, true));
+  const double* cnt = acc.as<double>();
+  if (nphi > 0) {  // the join multiplicities do not depend on the path condition
+    CUDA_TRY(pass(c, st, nullptr, nullptr, acc_all.as<double>(), V_all.as<double>(), fh_cnt, dh_cnt, false));
+    cnt = acc_all.as<double>();
+  }
+  if (nout > 0) {
+    k_rt_scalar<<<(nout + 255) / 256, 256, 0, st>>>(acc.as<double>(), cnt, toff.as<int32_t>(), tidx.as<int32_t>(),
+                                                    tcoef.as<double>(), nout, c->scalar_out.as<double>(),
+                                                    c->scalar_count.as<unsigned long long>());
+    launches_add(1);
+    scalar_done = true;
+  }
+  if (ngq > 0) {
+    k_rt_groups<<<dim3(64, (unsigned)ngq), 256, 0, st>>>(acc.as<double>(), cnt, gq.as<RtGroupOut>(),
+                                                        gcoef.as<double>());
+    launches_add(1);
+  }
+  return cudaGetLastError();
+}
+
+// One pass of the histogram kernels over the root: fp = path-condition filter (null: every
+// row), yp = target (null: w = (1, 0, 0)), into the accumulators accp and views Vp.
+cudaError_t FastRT::pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const double* yp, double* accp,
+                         double* Vp, const std::vector<FactHist>& fhl, const std::vector<DimHist>& dhl, bool timed) {
+  const Rel& R = c->rels[c->root];
+  CUDA_TRY(cudaMemsetAsync(accp, 0, nacc * 8, st));
+  if (vtotal && !dhl.empty()) CUDA_TRY(cudaMemsetAsync(Vp, 0, vtotal * 24, st));
   RtFactArgs fa{};
   fa.nrows = R.nrows;
-  fa.y = y;
-  fa.nh = (int)fh.size();
+  fa.y = yp;
+  fa.filt = fp;
+  fa.nh = (int)fhl.size();
   fa.nparts = nparts;
-  for (size_t i = 0; i < fh.size(); i++) {
-    fa.h[i] = fh[i];
-    fa.wgt[i] = fh[i].is_code ? 6 : 11;  // measured: a code row costs ~0.55 of a threshold row
+  for (size_t i = 0; i < fhl.size(); i++) {
+    fa.h[i] = fhl[i];
+    fa.wgt[i] = fhl[i].is_code ? 6 : 11;  // measured: a code row costs ~0.55 of a threshold row
   }
   fa.thr = dthr.as<double>();
   fa.eq_off = eq_off;
   fa.tab_off = tab_off;
-  fa.out = acc.as<double>();
-  scan_timer_begin(c, st);
-  if (R.nrows > 0) {
+  fa.out = accp;
+  if (timed) scan_timer_begin(c, st);
+  if (R.nrows > 0 && fa.nh > 0) {
     k_rt_fact<<<nparts, RT_FACT_WARPS * 32, fact_smem, st>>>(fa);
     launches_add(1);
   }
-  scan_timer_end(c, st);
+  if (timed) scan_timer_end(c, st);
   for (auto& h : fbig) {
     if (R.nrows <= 0) break;
     RtBigArgs ba{};
     ba.nrows = R.nrows;
-    ba.y = y;
+    ba.y = yp;
+    ba.filt = fp;
     ba.code = reinterpret_cast<const int32_t*>(h.col);
     ba.ncell = h.ncell;
     const size_t smem = (size_t)((h.ncell * 4 + 15) & ~15) + (size_t)h.ncell * 16;
     ba.in_smem = smem <= 200 * 1024;
-    ba.out = acc.as<double>() + h.goff;
+    ba.out = accp + h.goff;
     k_rt_big<<<148, 512, ba.in_smem ? smem : 0, st>>>(ba);
     launches_add(1);
   }
-  if (nlev > 0 && R.nrows > 0) {
+  if (nlev > 0 && R.nrows > 0 && !dhl.empty()) {
     RtViewArgs va{};
     va.nrows = R.nrows;
-    va.y = y;
+    va.y = yp;
+    va.filt = fp;
     va.nlev = nlev;
     for (int l = 0; l < nlev; l++) {
       va.fk[l] = vfk[l];
-      va.V[l] = V.as<double>() + 3 * voff[l];
+      va.V[l] = Vp + 3 * voff[l];
     }
     switch (nlev) {
 #define VIEWS(n)                                               \
@@ -664,28 +768,17 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
     }
     launches_add(1);
   }
-  if (!dh.empty()) {
+  if (!dhl.empty()) {
     RtDimArgs da{};
-    da.nh = (int)dh.size();
-    for (size_t i = 0; i < dh.size(); i++) da.h[i] = dh[i];
+    da.nh = (int)dhl.size();
+    for (size_t i = 0; i < dhl.size(); i++) da.h[i] = dhl[i];
     for (int l = 0; l < nlev; l++) {
-      da.V[l] = V.as<double>() + 3 * voff[l];
+      da.V[l] = Vp + 3 * voff[l];
       da.nk[l] = vnk[l];
     }
     da.thr = dthr.as<double>();
-    da.out = acc.as<double>();
-    k_rt_dims<<<dim3(16, (unsigned)dh.size()), 256, 0, st>>>(da);
-    launches_add(1);
-  }
-  if (nout > 0) {
-    k_rt_scalar<<<(nout + 255) / 256, 256, 0, st>>>(acc.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
-                                                    tcoef.as<double>(), nout, c->scalar_out.as<double>(),
-                                                    c->scalar_count.as<unsigned long long>());
-    launches_add(1);
-    scalar_done = true;
-  }
-  if (ngq > 0) {
-    k_rt_groups<<<dim3(64, (unsigned)ngq), 256, 0, st>>>(acc.as<double>(), gq.as<RtGroupOut>(), gcoef.as<double>());
+    da.out = accp;
+    k_rt_dims<<<dim3(16, (unsigned)dhl.size()), 256, 0, st>>>(da);
     launches_add(1);
   }
   return cudaGetLastError();
@@ -735,12 +828,61 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     }
     return true;
   };
+  // path condition φ: the predicates that every product of the batch carries (a tree node's
+  // condition); each product is φ · (its own part), parsed below without φ
+  struct PR {
+    int attr, kind;
+    double t;
+    bool operator<(const PR& o) const {
+      return attr != o.attr ? attr < o.attr : (kind != o.kind ? kind < o.kind : t < o.t);
+    }
+  };
+  std::vector<PR> phi;
+  {
+    bool first = true;
+    auto visit = [&](const QProduct& pr) -> bool {
+      std::vector<PR> v;
+      for (auto& f : pr.f)
+        if (f.kind >= LMFAO_F_LT) {
+          if (std::isnan(f.param)) return false;
+          v.push_back(PR{f.attr, f.kind, f.param});
+        }
+      std::sort(v.begin(), v.end());
+      if (first) {
+        phi = v;
+        first = false;
+      } else {
+        std::vector<PR> o;
+        std::set_intersection(phi.begin(), phi.end(), v.begin(), v.end(), std::back_inserter(o));
+        phi = o;
+      }
+      return true;
+    };
+    for (auto& Q : c->queries)
+      for (auto& u : Q.udafs)
+        for (auto& pr : u)
+          if (!visit(pr)) return nullptr;
+  }
+  if ((int)phi.size() > RT_MAX_PHI) return nullptr;
+  auto strip = [&](const QProduct& pr) {  // the product without (one occurrence of each) φ predicate
+    QProduct o{pr.coeff, {}};
+    std::vector<bool> used(phi.size(), false);
+    for (auto& f : pr.f) {
+      bool drop = false;
+      if (f.kind >= LMFAO_F_LT)
+        for (size_t i = 0; i < phi.size() && !drop; i++)
+          if (!used[i] && phi[i].attr == f.attr && phi[i].kind == f.kind && phi[i].t == f.param) used[i] = drop = true;
+      if (!drop) o.f.push_back(f);
+    }
+    return o;
+  };
   std::vector<std::vector<std::vector<P>>> sq;  // scalar: per query, per udaf, products
   for (int q : c->scalar_queries) {
     std::vector<std::vector<P>> us;
     for (auto& u : c->queries[q].udafs) {
       std::vector<P> ps;
-      for (auto& pr : u) {
+      for (auto& pr0 : u) {
+        const QProduct pr = strip(pr0);
         P p;
         if (!parse(pr, p, true)) return nullptr;
         if (p.pattr >= 0) any_pred = true;
@@ -757,7 +899,8 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     if (level_of(Q.gb[0]) == -2) return nullptr;
     for (auto& u : Q.udafs) {
       std::vector<P> ps;
-      for (auto& pr : u) {
+      for (auto& pr0 : u) {
+        const QProduct pr = strip(pr0);
         P p;
         if (!parse(pr, p, false)) return nullptr;
         ps.push_back(p);
@@ -765,7 +908,9 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       gqp[gi].push_back(ps);
     }
   }
-  if (!any_pred && c->groups.empty()) return nullptr;
+  if (!any_pred && c->groups.empty() && phi.empty()) return nullptr;
+  for (auto& p : phi)
+    if (level_of(p.attr) == -2) return nullptr;
   if (yattr >= 0 && (level_of(yattr) != -1 || c->attrs[yattr].dt != LMFAO_FP64)) return nullptr;
   std::unique_ptr<FastRT> rt(new FastRT());
   if (yattr >= 0) rt->y = (const double*)R.cols[R.find_attr(yattr)].buf.p;
@@ -888,6 +1033,34 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     nacc += 3;
     rt->fh.push_back(h);
   }
+  // path condition: the filter's predicates, and the unconditioned pass (TOT + group histograms)
+  rt->nphi = (int)phi.size();
+  rt->phi.n = rt->nphi;
+  for (int i = 0; i < rt->nphi; i++) {
+    RtPhi& q = rt->phi.p[i];
+    const int lv = level_of(phi[i].attr);
+    const Rel& O = lv < 0 ? R : c->rels[R.children[lv]];
+    q.col = O.cols[O.find_attr(phi[i].attr)].buf.p;
+    q.fk = lv < 0 ? nullptr : R.fk_dense[lv].as<int32_t>();
+    q.is_int = c->attrs[phi[i].attr].dt == LMFAO_INT32;
+    q.kind = phi[i].kind;
+    q.t = phi[i].t;
+  }
+  if (rt->nphi > 0) {
+    for (auto& h : rt->fh)
+      if (h.is_code) rt->fh_cnt.push_back(h);
+    if (rt->fh_cnt.empty() || rt->fh_cnt[0].is_code) {  // TOT from a one-cell histogram in front
+      FactHist h{};
+      h.col = R.cols[0].buf.p;
+      h.is_int = R.cols[0].dt == LMFAO_INT32;
+      h.ncell = 1;
+      h.goff = nacc;
+      nacc += 3;
+      rt->fh_cnt.insert(rt->fh_cnt.begin(), h);
+    }
+    for (auto& h : rt->dh)
+      if (h.is_code) rt->dh_cnt.push_back(h);
+  }
   rt->nacc = nacc;
   {  // one CTA per SM over equal pieces of the (histogram, row) space (the tables fill shared memory)
     int nsm = 148;
@@ -912,6 +1085,8 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     rt->voff[l] = vt;
     vt += rt->vnk[l];
     for (auto& h : rt->dh)
+      if (h.level == (int)j) h.level = l;
+    for (auto& h : rt->dh_cnt)
       if (h.level == (int)j) h.level = l;
   }
   rt->vtotal = vt;
@@ -964,6 +1139,9 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     return nullptr;
   if (rt->acc.alloc(nacc * 8)) return nullptr;
   if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) return nullptr;
+  if (rt->nphi > 0 && (rt->filt.alloc(std::max<int64_t>(R.nrows, 1)) || rt->acc_all.alloc(nacc * 8) ||
+                       rt->V_all.alloc(std::max<int64_t>(vt, 1) * 24)))
+    return nullptr;
   if (cudaStreamSynchronize(st)) return nullptr;
   if (cudaFuncSetAttribute(k_rt_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->fact_smem) ||
       cudaFuncSetAttribute(k_rt_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
