@@ -1,0 +1,158 @@
+"""Downstream consumers of the batch results (host-side, cheap).
+
+* Ridge linear regression over the covar matrix (§3 "Ridge linear regression",
+  P:364-402; the optimiser of §6: batch gradient descent with Armijo
+  backtracking line search and Barzilai-Borwein step sizes).  The covar matrix
+  C[j][k] = Σ_{x ∈ D} X_j X_k (with X_0 ≡ 1 for the intercept) is the result of the covariance
+  batch; every gradient step is C-sized work, the data is never touched again.
+* Mutual information and the Chow-Liu tree: MI(X_i, X_j) from the count queries
+  Q_∅, Q_{i}, Q_{j}, Q_{i,j} of the Chow-Liu batch with the 4-ary function
+  f(α, β, γ, δ) = δ/α · log(αδ / (βγ)) summed over the groups (a, b) of Q_{i,j}; the tree is a
+  maximum-weight spanning tree over the MI weights (reading R16 in DESIGN.md).
+
+These run on the host over results that `lmfao_fetch` returned; they import nothing from
+the oracle.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+# ------------------------------------------------------------------ covar matrix
+def covar_matrix(features, values):
+    """The (n+1)x(n+1) covar matrix [1, x_1..x_n] from the values of a covariance batch laid out
+    as synth.covar_batch: COUNT, SUM(x_i), SUM(x_i x_j) for i <= j."""
+    n = len(features)
+    v = np.asarray(values, dtype=np.float64).ravel()
+    if v.size != (n + 1) * (n + 2) // 2:
+        raise ValueError(f"{v.size} values for {n} features")
+    C = np.empty((n + 1, n + 1))
+    C[0, 0] = v[0]
+    C[0, 1:] = C[1:, 0] = v[1:n + 1]
+    k = n + 1
+    for i in range(n):
+        for j in range(i, n):
+            C[i + 1, j + 1] = C[j + 1, i + 1] = v[k]
+            k += 1
+    return C
+
+
+# ------------------------------------------------------------------ ridge regression by BGD
+def ridge_objective(C, label, theta, lam):
+    """J(θ) = 1/(2|D|) Σ_x (Σ_j θ_j X_j − X_label)^2 + λ/2 ||θ||^2, from C alone:
+    with θ' = θ and θ'_label = −1, Σ_x (θ'·X)^2 = θ'ᵀ C θ'.  θ ranges over the columns other
+    than `label` (the intercept column 0 included)."""
+    tp = _extend(theta, label, C.shape[0])
+    return 0.5 * tp @ C @ tp / C[0, 0] + 0.5 * lam * theta @ theta
+
+
+def ridge_gradient(C, label, theta, lam):
+    """∇_k J = (1/|D|) Σ_j θ'_j C[j][k] + λ θ_k for k ≠ label."""
+    tp = _extend(theta, label, C.shape[0])
+    g = C @ tp / C[0, 0]
+    return np.delete(g, label) + lam * theta
+
+
+def _extend(theta, label, m):
+    tp = np.empty(m)
+    tp[:label] = theta[:label]
+    tp[label] = -1.0
+    tp[label + 1:] = theta[label:]
+    return tp
+
+
+def ridge_bgd(C, label, lam=1e-3, tol=1e-10, max_iter=100_000, armijo_c=1e-4, shrink=0.5):
+    """Batch gradient descent with Armijo backtracking and Barzilai-Borwein step sizes over the
+    covar matrix.  Returns (θ, iterations, converged)."""
+    m = C.shape[0]
+    theta = np.zeros(m - 1)
+    g = ridge_gradient(C, label, theta, lam)
+    J = ridge_objective(C, label, theta, lam)
+    s = 1.0
+    prev = None
+    for it in range(1, max_iter + 1):
+        gg = g @ g
+        if math.sqrt(gg) <= tol * max(1.0, abs(J)):
+            return theta, it - 1, True
+        if prev is not None:  # Barzilai-Borwein: s = Δθ·Δθ / Δθ·Δg
+            dt, dg = theta - prev[0], g - prev[1]
+            den = dt @ dg
+            s = (dt @ dt) / den if den > 0 else 1.0
+        while True:  # Armijo: sufficient decrease along −g
+            cand = theta - s * g
+            Jc = ridge_objective(C, label, cand, lam)
+            if Jc <= J - armijo_c * s * gg or s < 1e-300:
+                break
+            s *= shrink
+        prev = (theta, g)
+        theta, J = cand, Jc
+        g = ridge_gradient(C, label, theta, lam)
+    return theta, max_iter, False
+
+
+def ridge_closed_form(C, label, lam):
+    """The minimiser of J: (C_ff/|D| + λI) θ = C_{f,label}/|D| (normal equations)."""
+    keep = [j for j in range(C.shape[0]) if j != label]
+    A = C[np.ix_(keep, keep)] / C[0, 0] + lam * np.eye(len(keep))
+    b = C[keep, label] / C[0, 0]
+    return np.linalg.solve(A, b)
+
+
+# ------------------------------------------------------------------ MI and Chow-Liu
+def mutual_information(total, marg_i, marg_j, pair):
+    """MI(X_i, X_j) = Σ_{(a,b)} f(α, β_a, γ_b, δ_ab), f = δ/α · log(αδ/(βγ)).
+    total = α = |D|; marg_i / marg_j: value -> count (Q_{i}, Q_{j}); pair: (a, b) -> count."""
+    a = float(total)
+    mi = 0.0
+    for (u, v), d in pair.items():
+        if d > 0:
+            mi += d / a * math.log(a * d / (marg_i[u] * marg_j[v]))
+    return mi
+
+
+def mi_matrix(attrs, results):
+    """MI for every pair from the results of synth.mi_batch(attrs): the pair queries in
+    itertools.combinations order, then the single-attribute queries, then COUNT; each result
+    is (keys, values, counts) as lmfao_fetch returns it."""
+    n = len(attrs)
+    npair = n * (n - 1) // 2
+    marg = []
+    for q in range(npair, npair + n):
+        keys, _, counts = results[q]
+        marg.append({int(k[0]): int(c) for k, c in zip(keys, counts)})
+    total = int(results[npair + n][2][0])
+    M = np.zeros((n, n))
+    q = 0
+    for i in range(n):
+        for j in range(i + 1, n):
+            keys, _, counts = results[q]
+            pair = {(int(k[0]), int(k[1])): int(c) for k, c in zip(keys, counts)}
+            M[i, j] = M[j, i] = mutual_information(total, marg[i], marg[j], pair)
+            q += 1
+    return M
+
+
+def chow_liu_tree(M):
+    """Maximum-weight spanning tree over the MI matrix (Kruskal: heaviest edges first, skipping
+    those that close a cycle); returns the n-1 edges (i, j), i < j, in the order they were added."""
+    n = M.shape[0]
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    edges = sorted(((M[i, j], i, j) for i in range(n) for j in range(i + 1, n)), key=lambda e: (-e[0], e[1], e[2]))
+    tree = []
+    for w, i, j in edges:
+        ri, rj = find(i), find(j)
+        if ri != rj:
+            parent[ri] = rj
+            tree.append((i, j))
+            if len(tree) == n - 1:
+                break
+    return tree

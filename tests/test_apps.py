@@ -1,0 +1,165 @@
+"""Downstream consumers (paper_1906_08687_b200/apps.py): ridge
+regression by BGD over the covar matrix, mutual information and the Chow-Liu tree.  Pinned to
+a pandas materialisation of the join (least squares / empirical MI on the joined rows), closed
+forms, and brute force over all spanning trees; the GPU test feeds lmfao_fetch results."""
+import itertools
+import math
+
+import numpy as np
+import pandas as pd
+import pytest
+
+import oracle
+import synth
+from paper_1906_08687_b200 import apps
+
+
+def _join(db):
+    frames = {r.name: pd.DataFrame({c: v for c, v in r.cols.items()}) for r in db.relations}
+    J = frames[db.root]
+    for p, c in db.edges:
+        f = frames[c]
+        J = J.merge(f, on=[x for x in f.columns if x in J.columns], how="inner")
+    return J
+
+
+def _small_star(seed=0, n=3000):
+    w = synth.config2(seed=seed, fact_rows=n, dim_rows=(20, 60, 200))
+    feats = w.meta["features"][:5] + ["d1_1", "d3_2"]
+    return w.db, feats
+
+
+@pytest.mark.parametrize("lam", [0.0, 1e-2, 1.0])
+def test_ridge_bgd_matches_lstsq_on_materialised_join(lam):
+    db, feats = _small_star()
+    label = len(feats)  # the last feature is the label; column 0 is the intercept
+    res = oracle.evaluate(db, [synth.covar_batch(feats)])[0]
+    C = apps.covar_matrix(feats, res.vals[0])
+    J = _join(db)
+    X = np.concatenate([np.ones((len(J), 1)), J[feats[:-1]].to_numpy()], axis=1)
+    y = J[feats[-1]].to_numpy()
+    assert np.allclose(C, np.concatenate([X, y[:, None]], axis=1).T @ np.concatenate([X, y[:, None]], axis=1),
+                       rtol=1e-10)
+    N = len(J)
+    exp = np.linalg.solve(X.T @ X / N + lam * np.eye(X.shape[1]), X.T @ y / N)
+    theta, it, ok = apps.ridge_bgd(C, label, lam=lam, tol=1e-12)
+    assert ok, it
+    assert np.allclose(theta, exp, rtol=1e-6, atol=1e-8), (theta, exp)
+    assert np.allclose(apps.ridge_closed_form(C, label, lam), exp, rtol=1e-9, atol=1e-12)
+    # the objective from C equals the objective on the rows
+    J_rows = 0.5 * np.mean((X @ theta - y) ** 2) + 0.5 * lam * theta @ theta
+    assert math.isclose(apps.ridge_objective(C, label, theta, lam), J_rows, rel_tol=1e-9)
+
+
+def test_ridge_gradient_is_the_derivative():
+    db, feats = _small_star(1, 800)
+    C = apps.covar_matrix(feats, oracle.evaluate(db, [synth.covar_batch(feats)])[0].vals[0])
+    rng = np.random.default_rng(0)
+    th = rng.standard_normal(len(feats))
+    g = apps.ridge_gradient(C, 3, th, 0.1)
+    h = 1e-6
+    num = np.array([(apps.ridge_objective(C, 3, th + h * e, 0.1) - apps.ridge_objective(C, 3, th - h * e, 0.1)) / (2 * h)
+                    for e in np.eye(len(th))])
+    assert np.allclose(g, num, rtol=1e-5, atol=1e-7)
+
+
+def _mi_db(seed=0, n=4000):
+    rng = np.random.default_rng(seed)
+    keys = np.arange(50, dtype=np.int32)
+    D = {"k": keys, "b": rng.integers(0, 4, 50).astype(np.int32), "c": rng.integers(0, 3, 50).astype(np.int32)}
+    k = rng.integers(0, 50, n).astype(np.int32)
+    a = rng.integers(0, 5, n).astype(np.int32)
+    e = ((a + D["b"][k]) % 3).astype(np.int32)  # e depends on a and b: high MI
+    return synth.Database([synth.Relation("F", {"k": k, "a": a, "e": e}), synth.Relation("D", D)], "F", [("F", "D")])
+
+
+def _results(db, batch):
+    return [(r.keys, r.vals, r.counts) for r in oracle.evaluate(db, batch)]
+
+
+def test_mi_matches_empirical_mi_of_the_join():
+    db = _mi_db()
+    attrs = ["a", "b", "c", "e"]
+    M = apps.mi_matrix(attrs, _results(db, synth.mi_batch(attrs)))
+    J = _join(db)
+    for i, j in itertools.combinations(range(4), 2):
+        p = pd.crosstab(J[attrs[i]], J[attrs[j]]).to_numpy() / len(J)
+        pi, pj = p.sum(1, keepdims=True), p.sum(0, keepdims=True)
+        nz = p > 0
+        exp = float((p[nz] * np.log(p[nz] / (pi @ pj)[nz])).sum())
+        assert math.isclose(M[i, j], exp, rel_tol=1e-12, abs_tol=1e-15), (attrs[i], attrs[j])
+    assert np.all(M >= -1e-15) and np.array_equal(M, M.T)
+
+
+def test_mi_of_independent_and_identical_attributes():
+    # identical attributes: MI = entropy; a constant attribute: MI = 0
+    total = 8
+    marg = {0: 2, 1: 6}
+    pair_same = {(0, 0): 2, (1, 1): 6}
+    H = -(0.25 * math.log(0.25) + 0.75 * math.log(0.75))
+    assert math.isclose(apps.mutual_information(total, marg, marg, pair_same), H, rel_tol=1e-15)
+    assert apps.mutual_information(total, marg, {7: 8}, {(0, 7): 2, (1, 7): 6}) == 0.0
+
+
+def _brute_max_spanning(M):
+    n = M.shape[0]
+    best, arg = -1.0, None
+    edges = [(i, j) for i in range(n) for j in range(i + 1, n)]
+    for sub in itertools.combinations(edges, n - 1):
+        parent = list(range(n))
+
+        def find(x):
+            while parent[x] != x:
+                x = parent[x]
+            return x
+        ok = True
+        for i, j in sub:
+            ri, rj = find(i), find(j)
+            if ri == rj:
+                ok = False
+                break
+            parent[ri] = rj
+        if ok:
+            w = sum(M[i, j] for i, j in sub)
+            if w > best:
+                best, arg = w, set(sub)
+    return best, arg
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_chow_liu_is_a_maximum_spanning_tree(seed):
+    rng = np.random.default_rng(seed)
+    n = 6
+    A = rng.random((n, n))
+    M = np.triu(A, 1) + np.triu(A, 1).T
+    tree = apps.chow_liu_tree(M)
+    best, arg = _brute_max_spanning(M)
+    assert len(tree) == n - 1 and math.isclose(sum(M[i, j] for i, j in tree), best, rel_tol=1e-12)
+    assert set(tree) == arg
+
+
+def test_chow_liu_on_mi_of_the_join():
+    db = _mi_db(3)
+    attrs = ["a", "b", "c", "e"]
+    M = apps.mi_matrix(attrs, _results(db, synth.mi_batch(attrs)))
+    tree = apps.chow_liu_tree(M)
+    assert len(tree) == 3
+    assert (0, 3) in tree or (1, 3) in tree  # e = (a + b) mod 3 hangs off a or b
+
+
+@pytest.mark.gpu
+def test_consumers_on_gpu_results():
+    from _parity import run_gpu
+    db, feats = _small_star(4, 20_000)
+    gpu = run_gpu(db, [synth.covar_batch(feats)])
+    C = apps.covar_matrix(feats, gpu[0][1][0])
+    Cref = apps.covar_matrix(feats, oracle.evaluate(db, [synth.covar_batch(feats)])[0].vals[0])
+    th, _, ok = apps.ridge_bgd(C, len(feats), lam=1e-2, tol=1e-12)
+    assert ok and np.allclose(th, apps.ridge_closed_form(Cref, len(feats), 1e-2), rtol=1e-6, atol=1e-8)
+    mdb = _mi_db(5, 30_000)
+    attrs = ["a", "b", "c", "e"]
+    b = synth.mi_batch(attrs)
+    Mg = apps.mi_matrix(attrs, run_gpu(mdb, b))
+    Mo = apps.mi_matrix(attrs, _results(mdb, b))
+    assert np.allclose(Mg, Mo, rtol=1e-12, atol=1e-15)
+    assert apps.chow_liu_tree(Mg) == apps.chow_liu_tree(Mo)
