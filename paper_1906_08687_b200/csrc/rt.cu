@@ -560,6 +560,7 @@ __global__ void __launch_bounds__(256) k_rt_dims(const __grid_constant__ RtDimAr
 // condition, §3 "Regression trees" P:528-555: α = Π of Kronecker deltas along the
 // path): one byte per root row, dimension attributes read through the foreign keys.
 constexpr int RT_MAX_PHI = 8;
+constexpr int RT_MAX_CLASSES = 16;  // classes of a classification node's group-by attribute
 struct RtPhi {
   const void* col;  // root column, or dimension column indexed by dense key
   const int32_t* fk;  // null: root attribute
@@ -630,6 +631,26 @@ __global__ void k_rt_groups(const double* __restrict__ acc, const double* __rest
   }
 }
 
+// Classification node outputs CT(X; α·...): per (query, UDAF) a term list over the
+// accumulators of class c's pass (acc + c·nacc); counts from the unconditioned histogram of X.
+struct RtCtOut {
+  double* table;
+  unsigned long long* counts;
+  int ncell, nudaf, u;
+  int64_t cnt_goff;
+};
+__global__ void k_rt_ct(const double* __restrict__ acc, int64_t nacc, const double* __restrict__ cnt,
+                        const RtCtOut* __restrict__ outs, const int32_t* __restrict__ toff,
+                        const int32_t* __restrict__ tidx, const double* __restrict__ tcoef) {
+  const RtCtOut o = outs[blockIdx.x];
+  for (int c = threadIdx.x; c < o.ncell; c += blockDim.x) {
+    double v = 0.0;
+    for (int t = toff[blockIdx.x]; t < toff[blockIdx.x + 1]; t++) v += tcoef[t] * acc[c * nacc + tidx[t]];
+    o.table[(int64_t)c * o.nudaf + o.u] = v;
+    if (o.u == 0) o.counts[c] = (unsigned long long)cnt[o.cnt_goff + 3 * c];
+  }
+}
+
 // ======================================================================= host
 struct FastRT : FastPaths {
   std::vector<int> handled;  // group indices (c->groups) computed here
@@ -645,6 +666,12 @@ struct FastRT : FastPaths {
   DevBuf filt, acc_all, V_all;
   std::vector<FactHist> fh_cnt;  // TOT + root group histograms
   std::vector<DimHist> dh_cnt;   // dimension group histograms
+  // classification node: one conditioned pass per class of ct_code
+  int ncls = 0, nct = 0;
+  RtPhi ct_code{};
+  std::vector<FactHist> fh_ct;
+  std::vector<DimHist> dh_ct;
+  DevBuf acc_cls, ct_outs, ct_toff, ct_tidx, ct_tcoef;
   int64_t nacc = 0;
   int nlev = 0;
   int64_t vnk[RT_MAX_LEVELS];
@@ -659,8 +686,8 @@ struct FastRT : FastPaths {
     char b[200];
     std::snprintf(b, sizeof b,
                   "{\"kind\": \"rt\", \"fact_hists\": %zu, \"dim_hists\": %zu, \"views\": %d, \"groups\": %zu, "
-                  "\"path_preds\": %d}",
-                  fh.size(), dh.size(), nlev, handled.size(), nphi);
+                  "\"path_preds\": %d, \"classes\": %d}",
+                  fh.size(), dh.size(), nlev, handled.size(), nphi, ncls);
     return b;
   }
   bool handles_group(int g) const override {
@@ -691,6 +718,25 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
   if (nphi > 0) {  // the join multiplicities do not depend on the path condition
     CUDA_TRY(pass(c, st, nullptr, nullptr, acc_all.as<double>(), V_all.as<double>(), fh_cnt, dh_cnt, false));
     cnt = acc_all.as<double>();
+  }
+  if (ncls > 0 && R.nrows == 0) CUDA_TRY(cudaMemsetAsync(acc_cls.p, 0, (size_t)ncls * nacc * 8, st));
+  if (ncls > 0 && R.nrows > 0) {  // classification: the node's condition and X = class, per class
+    for (int k = 0; k < ncls; k++) {
+      RtFilterArgs f = phi;
+      f.n = nphi + 1;
+      f.p[nphi] = ct_code;
+      f.p[nphi].t = (double)k;
+      f.nrows = R.nrows;
+      f.out = filt.as<uint8_t>();
+      k_rt_filter<<<148 * 8, 256, 0, st>>>(f);
+      launches_add(1);
+      CUDA_TRY(pass(c, st, filt.as<uint8_t>(), y, acc_cls.as<double>() + k * nacc, V.as<double>(), fh_ct, dh_ct, false));
+    }
+  }
+  if (nct > 0) {
+    k_rt_ct<<<nct, 128, 0, st>>>(acc_cls.as<double>(), nacc, cnt, ct_outs.as<RtCtOut>(), ct_toff.as<int32_t>(),
+                                 ct_tidx.as<int32_t>(), ct_tcoef.as<double>());
+    launches_add(1);
   }
   if (nout > 0) {
     k_rt_scalar<<<(nout + 255) / 256, 256, 0, st>>>(acc.as<double>(), cnt, toff.as<int32_t>(), tidx.as<int32_t>(),
@@ -790,10 +836,17 @@ cudaError_t FastRT::pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const
 // (p <= 2, y one fp64 root attribute), every group-by query has one group-by attribute
 // and predicate-free products; attributes belong to the root or to primary-key leaves
 // of the root.  Otherwise nullptr.
+// LMFAO_PLAN_DEBUG=1: report where the planner declines a batch
+#define RT_DECLINE()                                                                             \
+  do {                                                                                           \
+    if (const char* e__ = std::getenv("LMFAO_PLAN_DEBUG"))                                       \
+      if (e__[0] == '1') std::fprintf(stderr, "[lmfao] plan_rt declines (rt.cu:%d)\n", __LINE__); \
+    return nullptr;                                                                              \
+  } while (0)
 FastPaths* plan_rt(lmfao_ctx* c) {
   const Rel& R = c->rels[c->root];
   for (int ch : R.children)
-    if (!c->rels[ch].children.empty() || !c->rels[ch].unique_key) return nullptr;
+    if (!c->rels[ch].children.empty() || !c->rels[ch].unique_key) RT_DECLINE();
   auto level_of = [&](int attr) -> int {  // -1 root, j child index, -2 unsupported
     const int o = c->owner[attr];
     if (o == c->root) return -1;
@@ -861,9 +914,9 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     for (auto& Q : c->queries)
       for (auto& u : Q.udafs)
         for (auto& pr : u)
-          if (!visit(pr)) return nullptr;
+          if (!visit(pr)) RT_DECLINE();
   }
-  if ((int)phi.size() > RT_MAX_PHI) return nullptr;
+  if ((int)phi.size() > RT_MAX_PHI) RT_DECLINE();
   auto strip = [&](const QProduct& pr) {  // the product without (one occurrence of each) φ predicate
     QProduct o{pr.coeff, {}};
     std::vector<bool> used(phi.size(), false);
@@ -884,7 +937,7 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       for (auto& pr0 : u) {
         const QProduct pr = strip(pr0);
         P p;
-        if (!parse(pr, p, true)) return nullptr;
+        if (!parse(pr, p, true)) RT_DECLINE();
         if (p.pattr >= 0) any_pred = true;
         ps.push_back(p);
       }
@@ -893,25 +946,33 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     sq.push_back(us);
   }
   std::vector<std::vector<std::vector<P>>> gqp(c->groups.size());
+  std::vector<char> ct(c->groups.size(), 0);  // classification queries: a predicate inside a group-by
+  int ct_attr = -1;
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     const Query& Q = c->queries[c->groups[gi].q];
-    if (Q.gb.size() != 1) return nullptr;
-    if (level_of(Q.gb[0]) == -2) return nullptr;
+    if (Q.gb.size() != 1) RT_DECLINE();
+    if (level_of(Q.gb[0]) == -2) RT_DECLINE();
     for (auto& u : Q.udafs) {
       std::vector<P> ps;
       for (auto& pr0 : u) {
         const QProduct pr = strip(pr0);
         P p;
-        if (!parse(pr, p, false)) return nullptr;
+        if (!parse(pr, p, true)) RT_DECLINE();
+        if (p.pattr >= 0) ct[gi] = 1;
         ps.push_back(p);
       }
       gqp[gi].push_back(ps);
     }
+    if (ct[gi]) {  // CT(X; α·1[A op t]): one conditioned pass per class of X
+      if (ct_attr >= 0 && ct_attr != Q.gb[0]) RT_DECLINE();
+      ct_attr = Q.gb[0];
+      if (c->groups[gi].ncells > RT_MAX_CLASSES) RT_DECLINE();
+    }
   }
-  if (!any_pred && c->groups.empty() && phi.empty()) return nullptr;
+  if (!any_pred && c->groups.empty() && phi.empty()) RT_DECLINE();
   for (auto& p : phi)
-    if (level_of(p.attr) == -2) return nullptr;
-  if (yattr >= 0 && (level_of(yattr) != -1 || c->attrs[yattr].dt != LMFAO_FP64)) return nullptr;
+    if (level_of(p.attr) == -2) RT_DECLINE();
+  if (yattr >= 0 && (level_of(yattr) != -1 || c->attrs[yattr].dt != LMFAO_FP64)) RT_DECLINE();
   std::unique_ptr<FastRT> rt(new FastRT());
   if (yattr >= 0) rt->y = (const double*)R.cols[R.find_attr(yattr)].buf.p;
   // predicate attributes and their sorted distinct thresholds
@@ -920,9 +981,17 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     for (auto& ps : us)
       for (auto& p : ps)
         if (p.pattr >= 0) {
-          if (level_of(p.pattr) == -2) return nullptr;
-          if (std::isnan(p.t)) return nullptr;
+          if (level_of(p.pattr) == -2) RT_DECLINE();
+          if (std::isnan(p.t)) RT_DECLINE();
           thr_of[p.pattr].insert(p.t);
+        }
+  for (size_t gi = 0; gi < gqp.size(); gi++)
+    if (ct[gi])
+      for (auto& ps : gqp[gi])
+        for (auto& p : ps)
+          if (p.pattr >= 0) {
+            if (level_of(p.pattr) == -2 || std::isnan(p.t)) RT_DECLINE();
+            thr_of[p.pattr].insert(p.t);
         }
   // accumulator layout: [TOT 3] [fact / dim histograms] [group tables]
   int64_t nacc = 3;
@@ -980,13 +1049,20 @@ FastPaths* plan_rt(lmfao_ctx* c) {
   }
   // group-by queries
   std::vector<RtGroupOut> gouts;
+  std::vector<std::pair<int, int64_t>> ct_goff;  // classification queries: (group, offset of its count histogram)
+  std::map<int, int64_t> code_goff;  // group-by attribute -> offset of its histogram
   std::vector<double> gcoef;
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     GroupPlan& gp = c->groups[gi];
     const Query& Q = c->queries[gp.q];
     const int a = Q.gb[0], lv = level_of(a);
     const int64_t ncell = gp.ncells;
-    if (lv == -1) {
+    // one histogram of w per group-by attribute, shared by the queries grouping by it
+    auto seen = code_goff.find(a);
+    const bool fresh = seen == code_goff.end();
+    const int64_t goff = fresh ? nacc : seen->second;
+    if (!fresh) {
+    } else if (lv == -1) {
       FactHist h{};
       h.col = gp.g.code[0];
       h.is_code = 1;
@@ -1004,9 +1080,18 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       rt->dh.push_back(h);
       levels_used[lv] = 1;
     }
+    if (fresh) {
+      code_goff[a] = nacc;
+      nacc += 3 * ncell;
+    }
+    if (ct[gi]) {  // classification query: values from the per-class passes, counts from here
+      rt->handled.push_back((int)gi);
+      ct_goff.push_back({(int)gi, goff});
+      continue;
+    }
     RtGroupOut go{};
     go.ncell = ncell;
-    go.goff = nacc;
+    go.goff = goff;
     go.nudaf = gp.nudaf;
     go.coff = (int)gcoef.size();
     go.table = gp.table.as<double>();
@@ -1018,15 +1103,14 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     }
     gouts.push_back(go);
     rt->handled.push_back((int)gi);
-    nacc += 3 * ncell;
   }
-  if ((int)rt->fh.size() > RT_MAX_FACT || (int)rt->dh.size() > RT_MAX_DIM) return nullptr;
+  if ((int)rt->fh.size() > RT_MAX_FACT || (int)rt->dh.size() > RT_MAX_DIM) RT_DECLINE();
   for (auto& h : rt->fbig)
-    if (!h.is_code) return nullptr;  // predicates with more than 20 distinct thresholds: generic path
+    if (!h.is_code) RT_DECLINE();  // predicates with more than 20 distinct thresholds: generic path
   if (rt->fh.empty()) {  // TOT still comes from k_rt_fact: a one-cell histogram of the first root column
     FactHist h{};
     h.col = R.cols.empty() ? nullptr : R.cols[0].buf.p;
-    if (!h.col) return nullptr;
+    if (!h.col) RT_DECLINE();
     h.is_int = R.cols[0].dt == LMFAO_INT32;
     h.ncell = 1;
     h.goff = nacc;
@@ -1061,6 +1145,30 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     for (auto& h : rt->dh)
       if (h.is_code) rt->dh_cnt.push_back(h);
   }
+  if (!ct_goff.empty()) {  // classification: the class code per row, and the predicate histograms
+    if (rt->nphi + 1 > RT_MAX_PHI) RT_DECLINE();
+    const GroupPlan& gp = c->groups[ct_goff[0].first];
+    const int lv = level_of(ct_attr);
+    rt->ct_code.col = gp.g.code[0];  // codes: per root row, or per dense key of the child
+    rt->ct_code.fk = lv < 0 ? nullptr : R.fk_dense[lv].as<int32_t>();
+    rt->ct_code.is_int = 1;
+    rt->ct_code.kind = LMFAO_F_EQ;
+    rt->ncls = (int)gp.ncells;
+    {
+      FactHist h{};  // TOT of the class pass, in front
+      h.col = R.cols[0].buf.p;
+      h.is_int = R.cols[0].dt == LMFAO_INT32;
+      h.ncell = 1;
+      h.goff = nacc;
+      nacc += 3;
+      rt->fh_ct.push_back(h);
+    }
+    for (auto& h : rt->fh)
+      if (!h.is_code && h.ncell > 1) rt->fh_ct.push_back(h);
+    for (auto& h : rt->dh)
+      if (!h.is_code) rt->dh_ct.push_back(h);
+    if ((int)rt->fh_ct.size() > RT_MAX_FACT) RT_DECLINE();
+  }
   rt->nacc = nacc;
   {  // one CTA per SM over equal pieces of the (histogram, row) space (the tables fill shared memory)
     int nsm = 148;
@@ -1078,7 +1186,7 @@ FastPaths* plan_rt(lmfao_ctx* c) {
   int64_t vt = 0;
   for (size_t j = 0; j < R.children.size(); j++) {
     if (!levels_used[j]) continue;
-    if (rt->nlev == RT_MAX_LEVELS) return nullptr;
+    if (rt->nlev == RT_MAX_LEVELS) RT_DECLINE();
     const int l = rt->nlev++;
     rt->vfk[l] = R.fk_dense[j].as<int32_t>();
     rt->vnk[l] = c->rels[R.children[j]].nkeys;
@@ -1088,10 +1196,12 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       if (h.level == (int)j) h.level = l;
     for (auto& h : rt->dh_cnt)
       if (h.level == (int)j) h.level = l;
+    for (auto& h : rt->dh_ct)
+      if (h.level == (int)j) h.level = l;
   }
   rt->vtotal = vt;
   rt->view_smem = (size_t)rt->nlev * RT_HT * 4 + 32 + (size_t)rt->nlev * RT_HT * 24;
-  if (rt->view_smem > 200 * 1024) return nullptr;
+  if (rt->view_smem > 200 * 1024) RT_DECLINE();
   // scalar outputs: term lists over the accumulators
   std::vector<int32_t> toff{0}, tidx;
   std::vector<double> tcoef;
@@ -1126,6 +1236,33 @@ FastPaths* plan_rt(lmfao_ctx* c) {
     }
   rt->nout = (int)toff.size() - 1;
   rt->ngq = (int)gouts.size();
+  // classification outputs: per (query, UDAF) term lists over a class pass's accumulators
+  std::vector<RtCtOut> couts;
+  std::vector<int32_t> ctoff{0}, ctidx;
+  std::vector<double> ctcoef;
+  for (auto& cg : ct_goff) {
+    GroupPlan& gp = c->groups[cg.first];
+    for (int u = 0; u < gp.nudaf; u++) {
+      for (auto& p : gqp[cg.first][u]) {
+        if (p.pattr < 0) {
+          ctidx.push_back(p.pw);
+          ctcoef.push_back(p.coef);
+          continue;
+        }
+        const std::set<double>& ts = thr_of[p.pattr];
+        const int q = (int)std::distance(ts.begin(), ts.find(p.t));
+        for (int cell = 0; cell < 2 * (int)ts.size() + 1; cell++)
+          if (truth(p.kind, q, cell)) {
+            ctidx.push_back((int32_t)(hoff[p.pattr] + 3 * cell + p.pw));
+            ctcoef.push_back(p.coef);
+          }
+      }
+      ctoff.push_back((int32_t)ctidx.size());
+      couts.push_back(RtCtOut{gp.table.as<double>(), gp.counts.as<unsigned long long>(), (int)gp.ncells, gp.nudaf, u,
+                              cg.second});
+    }
+  }
+  rt->nct = (int)couts.size();
   cudaStream_t st = c->stream;
   auto up = [&](DevBuf& b, const void* src, size_t bytes) -> bool {
     if (b.alloc(std::max<size_t>(bytes, 16))) return false;
@@ -1135,24 +1272,26 @@ FastPaths* plan_rt(lmfao_ctx* c) {
   if (!up(rt->dthr, rt->thr.data(), rt->thr.size() * 8) || !up(rt->toff, toff.data(), toff.size() * 4) ||
       !up(rt->tidx, tidx.data(), tidx.size() * 4) || !up(rt->tcoef, tcoef.data(), tcoef.size() * 8) ||
       !up(rt->gq, gouts.data(), gouts.size() * sizeof(RtGroupOut)) ||
-      !up(rt->gcoef, gcoef.data(), gcoef.size() * 8))
-    return nullptr;
-  if (rt->acc.alloc(nacc * 8)) return nullptr;
-  if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) return nullptr;
-  if (rt->nphi > 0 && (rt->filt.alloc(std::max<int64_t>(R.nrows, 1)) || rt->acc_all.alloc(nacc * 8) ||
-                       rt->V_all.alloc(std::max<int64_t>(vt, 1) * 24)))
-    return nullptr;
-  if (cudaStreamSynchronize(st)) return nullptr;
+      !up(rt->gcoef, gcoef.data(), gcoef.size() * 8) ||
+      !up(rt->ct_outs, couts.data(), couts.size() * sizeof(RtCtOut)) || !up(rt->ct_toff, ctoff.data(), ctoff.size() * 4) ||
+      !up(rt->ct_tidx, ctidx.data(), ctidx.size() * 4) || !up(rt->ct_tcoef, ctcoef.data(), ctcoef.size() * 8))
+    RT_DECLINE();
+  if (rt->ncls > 0 && rt->acc_cls.alloc((size_t)rt->ncls * nacc * 8)) RT_DECLINE();
+  if (rt->acc.alloc(nacc * 8)) RT_DECLINE();
+  if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) RT_DECLINE();
+  if (rt->nphi > 0 && (rt->acc_all.alloc(nacc * 8) || rt->V_all.alloc(std::max<int64_t>(vt, 1) * 24))) RT_DECLINE();
+  if ((rt->nphi > 0 || rt->ncls > 0) && rt->filt.alloc(std::max<int64_t>(R.nrows, 1))) RT_DECLINE();
+  if (cudaStreamSynchronize(st)) RT_DECLINE();
   if (cudaFuncSetAttribute(k_rt_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->fact_smem) ||
       cudaFuncSetAttribute(k_rt_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
-    return nullptr;
+    RT_DECLINE();
   {
     cudaError_t e = cudaSuccess;
 #define VATTR(n) \
   if (!e) e = cudaFuncSetAttribute(k_rt_views<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rt->view_smem);
     VATTR(1) VATTR(2) VATTR(3) VATTR(4) VATTR(5) VATTR(6) VATTR(7) VATTR(8)
 #undef VATTR
-    if (e) return nullptr;
+    if (e) RT_DECLINE();
   }
   return rt.release();
 }

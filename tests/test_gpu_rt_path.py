@@ -108,3 +108,36 @@ def test_path_sharded_partials():
     parts = [run_gpu(db, batch, shard=(p, 3))[0] for p in range(3)]
     assert sum(int(p[2][0]) for p in parts) == int(ref.counts[0])
     assert np.allclose(sum(p[1] for p in parts), ref.vals, rtol=1e-9, atol=1e-9)
+
+
+def ct_batch(path, cls, splits, ts=(-0.5, 0.0, 0.75)):
+    """A classification node: CT(X; α) and CT(X; α·1[A op t]) for the class X, plus
+    CT(α); here also y-weighted variants and the node's regression totals."""
+    P = tuple(path)
+    qs = [Query([cls], [[Product(1.0, P)], [Product(1.0, P + (ident("y"),))]])]
+    for a, op in splits:
+        qs.append(Query([cls], [[Product(1.0, P + (Factor(op, a, t),))] for t in ts] +
+                        [[Product(0.5, P + (Factor(op, a, ts[0]), ident("y")))]]))
+    qs.append(Query([], [[Product(1.0, P)], [Product(1.0, P + (Factor(F_LE, "x2", 0.0),))]]))
+    return qs
+
+
+@pytest.mark.parametrize("cls", ["c1", "g1"])
+@pytest.mark.parametrize("with_path", [False, True])
+def test_classification_node(cls, with_path):
+    db = rt_db(6, 25_000)
+    path = PATH[:2] if with_path else []
+    batch = ct_batch(path, cls, [("x2", F_LE), ("d3", F_GT), ("i1", F_EQ), ("e2", F_NE)])
+    gpu, info = run_gpu(db, batch, info=True)
+    fp = info["fast_path"]
+    assert fp["kind"] == "rt" and fp["classes"] > 0 and fp["path_preds"] == len(path), fp
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("n", [1, 31, 2_049])
+def test_classification_node_small(n):
+    db = rt_db(7, n)
+    batch = ct_batch(PATH, "c1", [("x1", F_GE), ("d1", F_LT)]) + [Query(["g2"], [[Product(1.0, tuple(PATH))]])]
+    gpu, info = run_gpu(db, batch, info=True)
+    assert info["fast_path"]["kind"] == "rt", info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
