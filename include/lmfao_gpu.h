@@ -161,6 +161,13 @@ LMFAO_API lmfao_status lmfao_add_query(lmfao_ctx* ctx, int32_t n_groupby, const 
  * allocates all device buffers.  Freezes the batch. */
 LMFAO_API lmfao_status lmfao_plan(lmfao_ctx* ctx);
 
+/* Drops the batch and its plan (queries, selected kernels, results) but keeps the loaded and
+ * prepared relations, so that another batch over the same data — the next node of a decision
+ * tree, whose aggregates carry a different path condition — needs only
+ * add_query + plan.  Valid after prepare (state PREPARED or PLANNED), returns to PREPARED;
+ * query ids restart at 0.  LMFAO_ERR_STATE otherwise. */
+LMFAO_API lmfao_status lmfao_reset_batch(lmfao_ctx* ctx);
+
 /* Runs the planned batch asynchronously on `cuda_stream` (cudaStream_t; NULL =
  * the ctx's own stream): view builds (b), the fused root scan (c) with its FP64
  * Gram tiles (d) and histograms (e), dimension-side finishing, the NCCL

@@ -8,7 +8,8 @@
 * Mutual information and the Chow-Liu tree: MI(X_i, X_j) from the count queries
   Q_∅, Q_{i}, Q_{j}, Q_{i,j} of the Chow-Liu batch with the 4-ary function
   f(α, β, γ, δ) = δ/α · log(αδ / (βγ)) summed over the groups (a, b) of Q_{i,j}; the tree is a
-  maximum-weight spanning tree over the MI weights (reading R16 in DESIGN.md).
+  maximum-weight spanning tree over the MI weights (reading R19 in DESIGN.md).
+* A CART regression tree grown with node batches over the prepared relations (NEXT-1).
 
 These run on the host over results that `lmfao_fetch` returned; they import nothing from
 the oracle.
@@ -156,3 +157,57 @@ def chow_liu_tree(M):
             if len(tree) == n - 1:
                 break
     return tree
+
+
+# ------------------------------------------------------------------ CART regression tree
+F_LE, F_GT, F_IDENT = 3, 4, 1  # lmfao_fkind
+
+
+def regression_tree(engine, features, target, thresholds, max_depth=4, min_split=1000):
+    """A CART regression tree (§3 "Decision trees" P:480-555; §6: depth 4, min split
+    1000, 20 buckets) grown over the prepared relations of `engine`.
+
+    Each node runs one batch (lmfao_reset_batch + add_query + plan + run): with α the node's
+    path condition, RT(α, y·α, y²·α) for the node and for every candidate condition A ≤ t
+    (the rt.cu path takes α as a row filter).  The split with the largest variance reduction
+    SSE(node) − SSE(A ≤ t) − SSE(A > t), SSE = Σy² − (Σy)²/n, is taken; the right child's sums
+    are the node's minus the left's.  A node with fewer than `min_split` rows, at `max_depth`,
+    or without a split that reduces SSE is a leaf.  Returns nested dicts."""
+    y = [(F_IDENT, target, 0.0)]
+
+    def node(path, depth):
+        engine.reset_batch()
+        udafs = [[(1.0, path + y * p)] for p in range(3)]
+        for a in features:
+            for t in thresholds:
+                cond = path + [(F_LE, a, float(t))]
+                udafs += [[(1.0, cond + y * p)] for p in range(3)]
+        q = engine.add_query([], udafs)
+        engine.plan()
+        engine.run()
+        v = engine.fetch(q)[1][0]
+        n, s, s2 = v[0], v[1], v[2]
+        out = {"n": int(round(n)), "mean": s / n if n > 0 else 0.0, "path": [tuple(c) for c in path]}
+        if depth == max_depth or n < min_split:
+            return out
+        sse = s2 - s * s / n
+        best = None
+        k = 3
+        for a in features:
+            for t in thresholds:
+                nl, sl, s2l = v[k], v[k + 1], v[k + 2]
+                k += 3
+                nr, sr, s2r = n - nl, s - sl, s2 - s2l
+                if nl < 0.5 or nr < 0.5:
+                    continue
+                gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
+                if best is None or gain > best[0]:
+                    best = (gain, a, float(t))
+        if best is None or best[0] <= 0.0:
+            return out
+        _, a, t = best
+        out.update(feature=a, threshold=t,
+                   left=node(path + [(F_LE, a, t)], depth + 1), right=node(path + [(F_GT, a, t)], depth + 1))
+        return out
+
+    return node([], 0)

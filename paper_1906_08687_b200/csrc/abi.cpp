@@ -939,6 +939,32 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
 // the second captures the whole sequence into a CUDA Graph on the ctx stream and
 // every later run replays it on the caller's stream (one launch instead of ~a dozen).
 // Profiling runs and multi-GPU runs (NCCL) stay eager.
+// Drops the batch and its plan (queries, kernels selected, results) and keeps the loaded,
+// prepared relations: the next batch over the same data (a tree learner's next node) needs
+// add_query + plan only.
+extern "C" lmfao_status lmfao_reset_batch(lmfao_ctx* c) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PREPARED && c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "reset_batch needs prepare");
+  cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
+  CTX_CUDA(c, cudaStreamSynchronize(c->stream), "reset_batch");
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  c->graph_exec = nullptr;
+  c->graph_runs = c->graph_launches = 0;
+  c->fast.reset();
+  c->queries.clear();
+  c->nodes.clear();
+  c->scalar_queries.clear();
+  c->scalar_off.clear();
+  c->groups.clear();
+  c->code_cache.clear();
+  c->query_kind.clear();
+  c->query_slot.clear();
+  c->ran = false;
+  c->state = S_PREPARED;
+  return LMFAO_OK;
+}
+
 extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");

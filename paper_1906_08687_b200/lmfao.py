@@ -60,6 +60,7 @@ _SIGS = {
     "lmfao_prepare": [_P],
     "lmfao_add_query": [_P, ctypes.c_int32, _i32p, ctypes.c_int32, ctypes.POINTER(lmfao_udaf), _i32p],
     "lmfao_plan": [_P],
+    "lmfao_reset_batch": [_P],
     "lmfao_run": [_P, _P],
     "lmfao_result_shape": [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), _i32p, _i32p],
     "lmfao_fetch": [_P, ctypes.c_int32, _P, _P, _P],
@@ -245,6 +246,11 @@ class Engine:
 
     def plan(self):
         self._check(_lib.lmfao_plan(self.h))
+
+    def reset_batch(self):
+        """Drop the batch and plan, keep the prepared relations (lmfao_reset_batch)."""
+        self._check(_lib.lmfao_reset_batch(self.h))
+        self.query_ids = []
 
     def run(self, stream: int | None = None):
         self._check(_lib.lmfao_run(self.h, _P(stream) if stream else None))

@@ -163,3 +163,64 @@ def test_consumers_on_gpu_results():
     Mo = apps.mi_matrix(attrs, _results(mdb, b))
     assert np.allclose(Mg, Mo, rtol=1e-12, atol=1e-15)
     assert apps.chow_liu_tree(Mg) == apps.chow_liu_tree(Mo)
+
+
+def _cart_numpy(J, features, target, thresholds, max_depth, min_split):
+    """The same CART over the materialised join (numpy masks)."""
+    y = J[target].to_numpy()
+    cols = {a: J[a].to_numpy().astype(np.float64) for a in features}
+
+    def node(mask, depth):
+        n = mask.sum()
+        s, s2 = y[mask].sum(), (y[mask] ** 2).sum()
+        out = {"n": int(n), "mean": s / n if n else 0.0}
+        if depth == max_depth or n < min_split:
+            return out
+        sse = s2 - s * s / n
+        best = None
+        for a in features:
+            for t in thresholds:
+                lm = mask & (cols[a] <= t)
+                nl = lm.sum()
+                nr = n - nl
+                if nl == 0 or nr == 0:
+                    continue
+                sl, s2l = y[lm].sum(), (y[lm] ** 2).sum()
+                sr, s2r = s - sl, s2 - s2l
+                gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
+                if best is None or gain > best[0]:
+                    best = (gain, a, t)
+        if best is None or best[0] <= 0:
+            return out
+        _, a, t = best
+        out.update(feature=a, threshold=t, left=node(mask & (cols[a] <= t), depth + 1),
+                   right=node(mask & (cols[a] > t), depth + 1))
+        return out
+
+    return node(np.ones(len(J), bool), 0)
+
+
+def _same_tree(g, r):
+    assert g["n"] == r["n"] and math.isclose(g["mean"], r["mean"], rel_tol=1e-9, abs_tol=1e-12)
+    assert ("feature" in g) == ("feature" in r), (g.get("feature"), r.get("feature"))
+    if "feature" in g:
+        assert (g["feature"], g["threshold"]) == (r["feature"], r["threshold"])
+        _same_tree(g["left"], r["left"])
+        _same_tree(g["right"], r["right"])
+
+
+@pytest.mark.gpu
+def test_regression_tree_matches_numpy_cart():
+    from paper_1906_08687_b200 import lmfao
+    w = synth.config3(seed=2, fact_rows=30_000, dim_rows=(40, 300, 2000))
+    feats = ["x1", "x2", "x5", "d1_1", "d2_3", "d3_2"]
+    ts = synth.thresholds_c3()
+    e = lmfao.Engine()
+    try:
+        lmfao.load(e, w.db, [])
+        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=2_000)
+    finally:
+        e.close()
+    ref = _cart_numpy(_join(w.db), feats, "y", ts, 3, 2_000)
+    _same_tree(tree, ref)
+    assert "feature" in tree and "feature" in tree["left"]  # a non-trivial tree
