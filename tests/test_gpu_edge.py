@@ -59,3 +59,30 @@ def test_degenerate(kind, case):
     gpu, info = run_gpu(db, batch, info=True)
     ref = oracle.evaluate(db, batch)
     assert_parity(gpu, ref, batch)
+
+
+def test_reset_batch_reuses_prepared_relations():
+    """lmfao_reset_batch: STATE error before prepare; afterwards batches of different shapes
+    (covariance, counts, cube, rt) over the same prepared data all match the oracle."""
+    from paper_1906_08687_b200 import lmfao
+    db, feats = star(4000, (20, 30, 40), seed=5)
+    e = lmfao.Engine()
+    try:
+        for r in db.relations:
+            e.add_relation(r.name, r.cols)
+        with pytest.raises(lmfao.LmfaoError) as ei:
+            e.reset_batch()
+        assert ei.value.name == "LMFAO_ERR_STATE"
+        e.set_join_tree(db.root, db.edges)
+        e.prepare()
+        for kind in ["cov", "counts", "cube", "rt", "cov"]:
+            batch = batches(feats)[kind]
+            qids = [e.add_query(q.groupby, q.udafs) for q in batch]
+            e.plan()
+            e.run()
+            e.run()
+            got = [e.fetch(q) for q in qids]
+            assert_parity(got, oracle.evaluate(db, batch), batch)
+            e.reset_batch()
+    finally:
+        e.close()
