@@ -30,6 +30,8 @@
 #include <cstdlib>
 #include <set>
 
+#include <functional>
+
 #include "ctx.h"
 
 namespace lmfao {
@@ -597,6 +599,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
 // scan's t tile; primary-key leaf: row k has dense key k).
 struct DimTables {
   const double* const* cols[3];
+  const int32_t* const* idx[3];  // per feature: row of its relation per dimension key (null: the key's own row)
   int n[3];
   int64_t nk[3];
   double* V[3];
@@ -610,7 +613,14 @@ __global__ void k_cov_dims(DimTables d) {
     const int n = d.n[l];
     double v[GP];
 #pragma unroll
-    for (int f = 0; f < GP; f++) v[f] = f < n ? d.cols[l][f][kk] : (f == 10 ? 1.0 : 0.0);
+    for (int f = 0; f < GP; f++) {
+      if (f < n) {
+        const int32_t* ix = d.idx[l][f];
+        v[f] = d.cols[l][f][ix ? (int64_t)ix[kk] : kk];
+      } else {
+        v[f] = f == 10 ? 1.0 : 0.0;
+      }
+    }
     double2* out = reinterpret_cast<double2*>(d.V[l] + kk * GP);
 #pragma unroll
     for (int f = 0; f < GP / 2; f++) out[f] = make_double2(v[2 * f], v[2 * f + 1]);
@@ -756,7 +766,8 @@ struct CovLevel {
   int child = -1, rel = -1;
   std::vector<int> attrs;
   int64_t nk = 0;
-  DevBuf V, colptrs;
+  DevBuf V, colptrs, idxptrs;
+  std::vector<DevBuf> idx;  // composed foreign-key chains to the features of deeper relations
 };
 
 struct FastCov : FastPaths {
@@ -820,6 +831,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
     int64_t tot = 0;
     for (int i = 0; i < 3; i++) {
       d.cols[i] = (const double* const*)lv[i]->colptrs.p;
+      d.idx[i] = (const int32_t* const*)lv[i]->idxptrs.p;
       d.n[i] = (int)lv[i]->attrs.size();
       d.nk[i] = lv[i]->rel >= 0 ? lv[i]->nk : 0;
       d.V[i] = lv[i]->V.as<double>();
@@ -883,10 +895,14 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   if (c->scalar_queries.empty()) return nullptr;
   const Rel& R = c->rels[c->root];
   if (R.children.empty()) return nullptr;
-  for (int ch : R.children) {
-    const Rel& D = c->rels[ch];
-    if (!D.children.empty() || !D.unique_key) return nullptr;
-  }
+  // every non-root relation unique-keyed: a root row joins one row of each (snowflake PK chains,
+  // dangling rows dropped at prepare), so a dimension key determines its subtree's features
+  for (size_t u = 0; u < c->rels.size(); u++)
+    if ((int)u != c->root && !c->rels[u].unique_key) return nullptr;
+  auto root_child_of = [&](int rel) {  // the root child whose subtree holds rel
+    while (c->rels[rel].parent != c->root) rel = c->rels[rel].parent;
+    return rel;
+  };
   struct Term {
     double coef;
     int a, b;
@@ -925,7 +941,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     }
     bool found = false;
     for (size_t j = 0; j < R.children.size(); j++)
-      if (R.children[j] == o) {
+      if (R.children[j] == root_child_of(o)) {
         lf[j].push_back(a);
         found = true;
       }
@@ -959,10 +975,43 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     if (l.rel < 0) continue;
     if (l.V.alloc((size_t)std::max<int64_t>(l.nk, 1) * GP * 8)) return nullptr;
     std::vector<const double*> cp;
-    const Rel& D = c->rels[l.rel];
-    for (int a : l.attrs) cp.push_back((const double*)D.cols[D.find_attr(a)].buf.p);
-    if (l.colptrs.alloc(std::max<size_t>(cp.size(), 1) * sizeof(void*))) return nullptr;
-    if (!cp.empty() && cudaMemcpyAsync(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream))
+    std::vector<const int32_t*> ip;
+    std::map<int, const int32_t*> chain;  // relation -> row per dimension key (composed foreign keys)
+    std::function<const int32_t*(int)> row_of = [&](int rel) -> const int32_t* {
+      if (rel == l.rel) return nullptr;
+      auto it = chain.find(rel);
+      if (it != chain.end()) return it->second;
+      const int par = c->rels[rel].parent;
+      const Rel& P = c->rels[par];
+      int j = 0;
+      while (P.children[j] != rel) j++;
+      const int32_t* fk = P.fk_dense[j].as<int32_t>();  // the parent's rows -> this relation's rows
+      const int32_t* up = row_of(par);
+      const int32_t* out = fk;
+      if (up) {  // compose: key -> parent row -> this relation's row
+        l.idx.emplace_back();
+        DevBuf& b = l.idx.back();
+        if (b.alloc((size_t)std::max<int64_t>(l.nk, 1) * 4)) return nullptr;
+        if (l.nk > 0 && gather_bytes(fk, reinterpret_cast<const uint32_t*>(up), b.p, l.nk, 4, c->stream)) return nullptr;
+        out = b.as<int32_t>();
+      }
+      chain[rel] = out;
+      return out;
+    };
+    for (int a : l.attrs) {
+      const int o = c->owner[a];
+      const Rel& O = c->rels[o];
+      cp.push_back((const double*)O.cols[O.find_attr(a)].buf.p);
+      const int32_t* ix = row_of(o);
+      if (o != l.rel && !ix) return nullptr;
+      ip.push_back(ix);
+    }
+    if (l.colptrs.alloc(std::max<size_t>(cp.size(), 1) * sizeof(void*)) ||
+        l.idxptrs.alloc(std::max<size_t>(ip.size(), 1) * sizeof(void*)))
+      return nullptr;
+    if (!cp.empty() &&
+        (cudaMemcpyAsync(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream) ||
+         cudaMemcpyAsync(l.idxptrs.p, ip.data(), ip.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream)))
       return nullptr;
   }
   const int64_t nkA = fc->NS >= 1 ? fc->A.nk : 0;
