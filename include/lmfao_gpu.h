@@ -130,8 +130,9 @@ LMFAO_API lmfao_status lmfao_attr_id(lmfao_ctx* ctx, const char* attr_name, int3
 
 /* Registers the rooted join tree: n_edges = m-1 edges parent->child.
  * Validates: connected, acyclic, each relation has at most one parent, the
- * running-intersection property, and (v1) that every edge shares exactly
- * one attribute, of type int32. */
+ * running-intersection property, and that every edge shares one or two
+ * attributes, of type int32 (a two-attribute key such as Favorita's (date, store),
+ * P:1408-1411, is matched as the pair); otherwise LMFAO_ERR_UNSUPPORTED / _TYPE. */
 LMFAO_API lmfao_status lmfao_set_join_tree(lmfao_ctx* ctx, int32_t root_rel, int32_t n_edges,
                                  const int32_t* parent_rel, const int32_t* child_rel);
 

@@ -327,27 +327,36 @@ lmfao_status lmfao_set_join_tree(lmfao_ctx* c, int32_t root_rel, int32_t n_edges
         }
       }
   }
-  // v1: exactly one int32 join attribute per edge
+  // one or two int32 join attributes per edge (a two-attribute key — Favorita's (date, store),
+  // is matched as the pair)
   for (int ch = 0; ch < m; ch++) {
     if (parent[ch] < 0) continue;
     Rel& C = c->rels[ch];
     Rel& P = c->rels[parent[ch]];
-    int shared = 0, key = -1;
+    std::vector<int> keys;
     for (auto& col : C.cols)
-      if (P.find_attr(col.attr) >= 0) { shared++; key = col.attr; }
-    if (shared != 1)
-      return fail(c, LMFAO_ERR_UNSUPPORTED, "edge %s-%s shares %d attributes (v1 supports exactly one)",
-                  P.name.c_str(), C.name.c_str(), shared);
-    if (c->attrs[key].dt != LMFAO_INT32)
-      return fail(c, LMFAO_ERR_TYPE, "join attribute %s must be int32", c->attrs[key].name.c_str());
-    C.key_attr = key;
-    C.key_col = C.find_attr(key);
+      if (P.find_attr(col.attr) >= 0) keys.push_back(col.attr);
+    std::sort(keys.begin(), keys.end());
+    if (keys.empty() || keys.size() > 2)
+      return fail(c, LMFAO_ERR_UNSUPPORTED, "edge %s-%s shares %zu attributes (one or two supported)",
+                  P.name.c_str(), C.name.c_str(), keys.size());
+    for (int key : keys)
+      if (c->attrs[key].dt != LMFAO_INT32)
+        return fail(c, LMFAO_ERR_TYPE, "join attribute %s must be int32", c->attrs[key].name.c_str());
+    C.key_attr = keys[0];
+    C.key_col = C.find_attr(keys[0]);
+    C.key_attr2 = keys.size() > 1 ? keys[1] : -1;
+    C.key_col2 = keys.size() > 1 ? C.find_attr(keys[1]) : -1;
   }
   for (int u = 0; u < m; u++) {
     c->rels[u].parent = parent[u];
     c->rels[u].children = children[u];
     c->rels[u].fk_col.clear();
-    for (int ch : children[u]) c->rels[u].fk_col.push_back(c->rels[u].find_attr(c->rels[ch].key_attr));
+    c->rels[u].fk_col2.clear();
+    for (int ch : children[u]) {
+      c->rels[u].fk_col.push_back(c->rels[u].find_attr(c->rels[ch].key_attr));
+      c->rels[u].fk_col2.push_back(c->rels[ch].key_attr2 >= 0 ? c->rels[u].find_attr(c->rels[ch].key_attr2) : -1);
+    }
   }
   c->root = root_rel;
   c->state = S_TREE;
@@ -381,7 +390,10 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
     for (int u : post) {
       Rel& r = c->rels[u];
       for (int j : r.fk_col) order.push_back({&r, &r.cols[j]});
+      for (int j : r.fk_col2)
+        if (j >= 0) order.push_back({&r, &r.cols[j]});
       if (r.key_col >= 0) order.push_back({&r, &r.cols[r.key_col]});
+      if (r.key_col2 >= 0) order.push_back({&r, &r.cols[r.key_col2]});
     }
     for (int u : post)
       for (auto& col : c->rels[u].cols) order.push_back({&c->rels[u], &col});
@@ -416,9 +428,16 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       CTX_CUDA(c, column_ready(r.cols[r.fk_col[j]], st), "prepare copy");
       DevBuf d;
       CTX_CUDA(c, d.alloc(std::max<int64_t>(r.nrows, 1) * 4), "prepare");
-      CTX_CUDA(c, lookup_dense(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.nrows, ch.dict.as<int32_t>(), ch.nkeys,
-                               d.as<int32_t>(), st),
-               "prepare remap");
+      if (r.fk_col2[j] >= 0) {  // two-attribute key
+        CTX_CUDA(c, column_ready(r.cols[r.fk_col2[j]], st), "prepare copy");
+        CTX_CUDA(c, lookup_dense_pair(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.cols[r.fk_col2[j]].buf.as<int32_t>(),
+                                      r.nrows, ch.dict.as<uint64_t>(), ch.nkeys, d.as<int32_t>(), st),
+                 "prepare remap");
+      } else {
+        CTX_CUDA(c, lookup_dense(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.nrows, ch.dict.as<int32_t>(), ch.nkeys,
+                                 d.as<int32_t>(), st),
+                 "prepare remap");
+      }
       r.fk_dense.push_back(std::move(d));
     }
     // (2) inner join: drop rows with a dangling foreign key
@@ -432,8 +451,15 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       // (3) dictionary of the key to the parent, dense ids, sort by them
       CTX_CUDA(c, column_ready(r.cols[r.key_col], st), "prepare copy");
       DevBuf codes;
-      CTX_CUDA(c, dict_encode_i32(r.cols[r.key_col].buf.as<int32_t>(), r.nrows, r.dict, r.nkeys, &codes, st),
-               "prepare dict");
+      if (r.key_col2 >= 0) {
+        CTX_CUDA(c, column_ready(r.cols[r.key_col2], st), "prepare copy");
+        CTX_CUDA(c, dict_encode_pair(r.cols[r.key_col].buf.as<int32_t>(), r.cols[r.key_col2].buf.as<int32_t>(), r.nrows,
+                                     r.dict, r.nkeys, &codes, st),
+                 "prepare dict");
+      } else {
+        CTX_CUDA(c, dict_encode_i32(r.cols[r.key_col].buf.as<int32_t>(), r.nrows, r.dict, r.nkeys, &codes, st),
+                 "prepare dict");
+      }
       r.dense_key = std::move(codes);
       DevBuf perm;
       CTX_CUDA(c, sort_perm_by_dense(r.dense_key.as<int32_t>(), r.nrows, r.nkeys, perm, st), "prepare sort");

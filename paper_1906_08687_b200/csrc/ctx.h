@@ -25,10 +25,12 @@ struct Rel {
   int parent = -1;
   std::vector<int> children;
   int key_attr = -1, key_col = -1;
-  std::vector<int> fk_col;  // per child: column of this relation holding the child's key
+  int key_attr2 = -1, key_col2 = -1;  // second attribute of a two-attribute join key (-1: one attribute)
+  std::vector<int> fk_col;   // per child: column of this relation holding the child's key
+  std::vector<int> fk_col2;  // per child: the second key column (-1: one attribute)
   // prepared
   int64_t nkeys = 0;
-  DevBuf dict;       // sorted distinct key values [nkeys]
+  DevBuf dict;       // sorted distinct key values [nkeys] (int32; u64 pair images for two-attribute keys)
   DevBuf dense_key;  // dense key id per row (rows sorted by it)
   bool unique_key = false;
   std::vector<DevBuf> fk_dense;  // per child: dense id of the child key per row

@@ -140,6 +140,11 @@ cudaError_t dict_encode_i32(const int32_t* col, int64_t n, DevBuf& dict, int64_t
                             cudaStream_t st);
 cudaError_t lookup_dense(const int32_t* vals, int64_t n, const int32_t* dict, int64_t nd, int32_t* out,
                          cudaStream_t st);
+// two-attribute join keys: dictionary over the distinct (a, b) pairs (order-preserving u64 images)
+cudaError_t dict_encode_pair(const int32_t* a, const int32_t* b, int64_t n, DevBuf& dict, int64_t& ndict, DevBuf* codes,
+                             cudaStream_t st);
+cudaError_t lookup_dense_pair(const int32_t* a, const int32_t* b, int64_t n, const uint64_t* dict, int64_t nd,
+                              int32_t* out, cudaStream_t st);
 cudaError_t keep_rows(const std::vector<const int32_t*>& fks, int64_t n, DevBuf& idx, int64_t& nkeep,
                       cudaStream_t st);
 cudaError_t sort_perm_by_dense(const int32_t* dense, int64_t n, int64_t nkeys, DevBuf& perm, cudaStream_t st);

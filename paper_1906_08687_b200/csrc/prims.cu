@@ -359,6 +359,95 @@ cudaError_t dict_encode_i32(const int32_t* col, int64_t n, DevBuf& dict, int64_t
   return cudaStreamSynchronize(st);
 }
 
+// ---- two-attribute join keys (a, b): order-preserving u64 images, dictionary over the pairs
+__global__ void k_pair_key(const int32_t* __restrict__ a, const int32_t* __restrict__ b, uint64_t* __restrict__ out,
+                           int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ((uint64_t)((uint32_t)a[i] ^ 0x80000000u) << 32) | (uint64_t)((uint32_t)b[i] ^ 0x80000000u);
+}
+__global__ void k_split_u64(const uint64_t* __restrict__ in, const uint32_t* __restrict__ perm, uint32_t* __restrict__ lo,
+                            uint32_t* __restrict__ hi, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = in[perm ? perm[i] : i];
+    if (lo) lo[i] = (uint32_t)v;
+    if (hi) hi[i] = (uint32_t)(v >> 32);
+  }
+}
+__global__ void k_pair_heads(const uint64_t* __restrict__ in, const uint32_t* __restrict__ perm, uint32_t* flags,
+                             int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || in[perm[i]] != in[perm[i - 1]]) ? 1u : 0u;
+}
+__global__ void k_pair_dict(const uint64_t* __restrict__ in, const uint32_t* __restrict__ perm,
+                            const uint32_t* __restrict__ flags, const uint32_t* __restrict__ excl, uint64_t* dict,
+                            int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (flags[i]) dict[excl[i]] = in[perm[i]];
+}
+__global__ void k_lookup_u64(const uint64_t* __restrict__ vals, int64_t n, const uint64_t* __restrict__ dict, int64_t nd,
+                             int32_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = vals[i];
+    int64_t lo = 0, hi = nd;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (dict[mid] < v) lo = mid + 1;
+      else hi = mid;
+    }
+    out[i] = (lo < nd && dict[lo] == v) ? (int32_t)lo : -1;
+  }
+}
+
+cudaError_t dict_encode_pair(const int32_t* a, const int32_t* b, int64_t n, DevBuf& dict, int64_t& ndict, DevBuf* codes,
+                             cudaStream_t st) {
+  ndict = 0;
+  if (n <= 0) {
+    CUDA_TRY(dict.alloc(8));
+    if (codes) CUDA_TRY(codes->alloc(4));
+    return cudaSuccess;
+  }
+  DevBuf key, k32, perm, flags, excl;
+  CUDA_TRY(key.alloc(n * 8));
+  CUDA_TRY(k32.alloc(n * 4));
+  CUDA_TRY(perm.alloc(n * 4));
+  CUDA_TRY(flags.alloc(n * 4));
+  CUDA_TRY(excl.alloc(n * 4));
+  k_pair_key<<<grid_for(n), 256, 0, st>>>(a, b, key.as<uint64_t>(), n);
+  CUDA_TRY(iota_u32(perm.as<uint32_t>(), n, st));
+  // LSD over the two 32-bit halves: low word, then (stably) high word
+  k_split_u64<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), nullptr, k32.as<uint32_t>(), nullptr, n);
+  CUDA_TRY(radix_sort_pairs(k32.as<uint32_t>(), perm.as<uint32_t>(), n, 32, st));
+  k_split_u64<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), perm.as<uint32_t>(), nullptr, k32.as<uint32_t>(), n);
+  CUDA_TRY(radix_sort_pairs(k32.as<uint32_t>(), perm.as<uint32_t>(), n, 32, st));
+  k_pair_heads<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), perm.as<uint32_t>(), flags.as<uint32_t>(), n);
+  CUDA_TRY(exclusive_scan_u32(flags.as<uint32_t>(), excl.as<uint32_t>(), n, st));
+  uint32_t last_ex = 0, last_f = 0;
+  CUDA_TRY(cudaMemcpyAsync(&last_ex, excl.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&last_f, flags.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  ndict = (int64_t)last_ex + last_f;
+  CUDA_TRY(dict.alloc(ndict * 8));
+  k_pair_dict<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), perm.as<uint32_t>(), flags.as<uint32_t>(),
+                                           excl.as<uint32_t>(), dict.as<uint64_t>(), n);
+  CUDA_TRY(cudaGetLastError());
+  if (codes) {
+    CUDA_TRY(codes->alloc(n * 4));
+    k_lookup_u64<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), n, dict.as<uint64_t>(), ndict, codes->as<int32_t>());
+    CUDA_TRY(cudaGetLastError());
+  }
+  return cudaStreamSynchronize(st);
+}
+
+cudaError_t lookup_dense_pair(const int32_t* a, const int32_t* b, int64_t n, const uint64_t* dict, int64_t nd,
+                              int32_t* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  DevBuf key;
+  CUDA_TRY(key.alloc(n * 8));
+  k_pair_key<<<grid_for(n), 256, 0, st>>>(a, b, key.as<uint64_t>(), n);
+  k_lookup_u64<<<grid_for(n), 256, 0, st>>>(key.as<uint64_t>(), n, dict, nd, out);
+  return cudaGetLastError();
+}
+
 cudaError_t lookup_dense(const int32_t* vals, int64_t n, const int32_t* dict, int64_t nd, int32_t* out,
                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
