@@ -64,6 +64,7 @@ struct CubeArgs {
   const int32_t* key[CB_LEV];   // dense keys, level order
   const void* meas[CB_MEAS];
   int meas_i32[CB_MEAS];
+  const int32_t* midx[CB_MEAS];  // dimension measure: its row per root row (the dense foreign key); null: root
   const int32_t* acode[CB_ATTR];  // codes per child dense key (level < R) or per root row (level R)
   int alvl[CB_ATTR];
   int qbeg[CB_LEV + 2];         // cuboids sorted by depth: depth d = [qbeg[d], qbeg[d + 1])
@@ -184,9 +185,11 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
 #pragma unroll
       for (int j = 0; j < CB_MEAS; j++) {
         xm[j + 1] = 0.0;
-        if (j < a.M && v)
-          xm[j + 1] = a.meas_i32[j] ? (double)reinterpret_cast<const int32_t*>(a.meas[j])[row]
-                                    : reinterpret_cast<const double*>(a.meas[j])[row];
+        if (j < a.M && v) {
+          const int64_t mr = a.midx[j] ? (int64_t)a.midx[j][row] : row;
+          xm[j + 1] = a.meas_i32[j] ? (double)reinterpret_cast<const int32_t*>(a.meas[j])[mr]
+                                    : reinterpret_cast<const double*>(a.meas[j])[mr];
+        }
       }
       for (int d = a.R; d >= 0; d--) {
         if (!(a.dmask >> d & 1u)) continue;
@@ -454,7 +457,9 @@ FastPaths* plan_cube(lmfao_ctx* c) {
         int nid = 0;
         for (auto& f : p.f) {
           if (f.kind == LMFAO_F_CONST) continue;
-          if (f.kind != LMFAO_F_IDENT || c->owner[f.attr] != c->root || ++nid > 1) return nullptr;
+          if (f.kind != LMFAO_F_IDENT || ++nid > 1) return nullptr;
+          const int o = c->owner[f.attr];
+          if (o != c->root && c->rels[o].parent != c->root) return nullptr;  // root or a (primary-key leaf) child
           if (meas_slot(f.attr) < 0) return nullptr;
         }
       }
@@ -523,9 +528,15 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   }
   a.M = M;
   for (int j = 0; j < M; j++) {
-    const Column& col = R.cols[R.find_attr(meas[j])];
+    const int o = c->owner[meas[j]];
+    const Rel& O = c->rels[o];
+    const Column& col = O.cols[O.find_attr(meas[j])];
     a.meas[j] = col.buf.p;
     a.meas_i32[j] = col.dt == LMFAO_INT32;
+    a.midx[j] = nullptr;
+    if (o != c->root)  // a dimension measure: read through the dense foreign key
+      for (size_t ch = 0; ch < R.children.size(); ch++)
+        if (R.children[ch] == o) a.midx[j] = R.fk_dense[ch].as<int32_t>();
   }
   a.nattr = (int)aslot.size();
   a.nq = (int)qs.size();

@@ -139,3 +139,15 @@ def test_c5_cube_sparse_abc():
     gpu, info = run_gpu(w.db, w.batch, info=True)
     assert info["fast_path"]["groups"]["sparse"] == 1, info["fast_path"]
     assert_parity(gpu, oracle.evaluate(w.db, w.batch), w.batch)
+
+
+def test_cube_dimension_measures():
+    """Measures owned by primary-key dimensions (Covar(X_j; X_k) with X_j a dimension feature,
+    NEXT-2): read through the dense foreign keys."""
+    db = cube_db(8, 20_000)
+    batch = [Query(["a1"], [S((1, "x2")), S((1, "m1")), S((2, "x3"), (1, None))]),
+             Query(["g", "a3"], [S((1, "x1"))]),
+             Query(["a2", "b2"], [S((-1, "x3"))])]
+    gpu, info = run_gpu(db, batch, info=True)
+    assert info["fast_path"]["groups"]["kind"] == "cube", info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
