@@ -57,8 +57,8 @@ typedef enum {
   LMFAO_ERR_CYCLIC_TREE = 5,        /* join tree has a cycle */
   LMFAO_ERR_DISCONNECTED_TREE = 6,  /* join tree does not span all relations */
   LMFAO_ERR_RUNNING_INTERSECTION = 7, /* ω_i ∩ ω_j ⊄ ω_k for some R_k on the path */
-  LMFAO_ERR_UNSUPPORTED = 8,        /* v1 limits: multi-attribute join keys, group-by on an attribute
-                                       not functionally determined by the root row (see lmfao_add_query) */
+  LMFAO_ERR_UNSUPPORTED = 8,        /* limits: join keys of more than two attributes, group-by
+                                       attributes the engine cannot place (see lmfao_add_query) */
   LMFAO_ERR_OOM = 9,                /* device allocation failed */
   LMFAO_ERR_CUDA = 10,              /* CUDA runtime error / no device */
   LMFAO_ERR_NCCL = 11               /* NCCL error (multi-GPU) */
@@ -150,10 +150,13 @@ LMFAO_API lmfao_status lmfao_set_root_shard(lmfao_ctx* ctx, int32_t part, int32_
 LMFAO_API lmfao_status lmfao_prepare(lmfao_ctx* ctx);
 
 /* Adds Q(F; α_1..α_n) += R_1..R_m.  groupby_attrs: int32 attributes
- * (LMFAO_ERR_TYPE otherwise) owned by the root or by a child of the root whose
- * join key is unique in that child (v1; otherwise LMFAO_ERR_UNSUPPORTED).
- * n_groupby may be 0.  Each product's factors must name existing attributes
- * (CONST: attr = -1).  The batch is copied. */
+ * (LMFAO_ERR_TYPE otherwise) owned by the root or by children of the root; when a
+ * child's join key is not unique in it (a root row joins several of its rows) all the
+ * query's group-by attributes must belong to that child — the query is then finished
+ * at the child ("each aggregate to its own root") — otherwise, and for
+ * attributes deeper in the tree, LMFAO_ERR_UNSUPPORTED.  n_groupby may be 0.  Each
+ * product's factors must name existing attributes (CONST: attr = -1).  The batch is
+ * copied. */
 LMFAO_API lmfao_status lmfao_add_query(lmfao_ctx* ctx, int32_t n_groupby, const int32_t* groupby_attrs,
                              int32_t n_udafs, const lmfao_udaf* udafs, int32_t* query_id);
 

@@ -540,13 +540,28 @@ lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* gro
       return fail(c, LMFAO_ERR_TYPE, "group-by attribute %s must be int32", c->attrs[a].name.c_str());
     if (!gbs.insert(a).second) return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate group-by attribute");
     int o = c->owner[a];
-    bool ok = o == c->root || (c->rels[o].parent == c->root && c->rels[o].unique_key);
+    // the root, a unique-keyed child (determined by a root row), or a child with a
+    // non-unique key (the query is then finished at that child: all its group-by
+    // attributes must belong to it, checked below)
+    bool ok = o == c->root || c->rels[o].parent == c->root;
     if (!ok)
       return fail(c, LMFAO_ERR_UNSUPPORTED,
-                  "group-by attribute %s is not functionally determined by a root row (v1: root or a unique-keyed "
-                  "child of the root)",
-                  c->attrs[a].name.c_str());
+                  "group-by attribute %s belongs to neither the root nor a child of the root", c->attrs[a].name.c_str());
     q.gb.push_back(a);
+  }
+  {
+    int T = -1;
+    bool mixed = false;
+    for (int a : q.gb) {
+      const int o = c->owner[a];
+      if (o != c->root && !c->rels[o].unique_key) T = o;
+    }
+    if (T >= 0)
+      for (int a : q.gb) mixed |= c->owner[a] != T;
+    if (mixed)
+      return fail(c, LMFAO_ERR_UNSUPPORTED,
+                  "group-by attributes of %s (a non-unique key) mixed with attributes of other relations",
+                  c->rels[T].name.c_str());
   }
   for (int j = 0; j < n_udafs; j++) {
     const lmfao_udaf& u = udafs[j];
@@ -667,6 +682,69 @@ void append_udaf_program(lmfao_ctx* c, Program& p, const std::vector<QProduct>& 
   }
 }
 
+// Programs of a query finished at the non-unique-keyed root child T (see RevPlan): per
+// product, the root side (root factors, the other children's view slots, T left out as
+// slot -1) and the T side (T's factors, its children's view slots); a last output each for
+// the multiplicities.
+void build_rev(lmfao_ctx* c, const Query& Q, int T, RevPlan& rv, Program& rp, Program& tp, std::vector<int32_t>& pu) {
+  const Rel& R = c->rels[c->root];
+  const Rel& TR = c->rels[T];
+  int jT = 0;
+  while (R.children[jT] != T) jT++;
+  rv.T = T;
+  rv.j = jT;
+  auto out = [](Program& p) {
+    p.out_ioff.push_back((int)p.ip.size());
+    p.out_doff.push_back((int)p.dp.size());
+    p.ip.push_back(1);  // one term
+  };
+  for (size_t u = 0; u < Q.udafs.size(); u++)
+    for (auto& pr : Q.udafs[u]) {
+      double coef = pr.coeff;
+      std::vector<std::tuple<int, int, uint64_t>> own, ownT;
+      std::vector<std::vector<QFactor>> sub(R.children.size()), subT(TR.children.size());
+      for (auto& f : pr.f) {
+        if (f.kind == LMFAO_F_CONST) {
+          coef *= f.param;
+          continue;
+        }
+        const int o = c->owner[f.attr];
+        if (o == c->root) {
+          own.emplace_back(f.kind, f.attr, dbits(f.param));
+          continue;
+        }
+        const int ch = child_toward(c, c->root, o);
+        if (ch != T) {
+          for (size_t j = 0; j < R.children.size(); j++)
+            if (R.children[j] == ch) sub[j].push_back(f);
+        } else if (o == T) {
+          ownT.emplace_back(f.kind, f.attr, dbits(f.param));
+        } else {
+          const int cT = child_toward(c, T, o);
+          for (size_t k = 0; k < TR.children.size(); k++)
+            if (TR.children[k] == cT) subT[k].push_back(f);
+        }
+      }
+      std::sort(own.begin(), own.end());
+      std::sort(ownT.begin(), ownT.end());
+      std::vector<int> slots, slotsT;
+      for (size_t j = 0; j < R.children.size(); j++)
+        slots.push_back((int)j == jT ? -1 : slot_of(c, R.children[j], sub[j]));
+      for (size_t k = 0; k < TR.children.size(); k++) slotsT.push_back(slot_of(c, TR.children[k], subT[k]));
+      out(rp);
+      emit_term(rp, c, c->root, coef, own, slots);
+      out(tp);
+      emit_term(tp, c, T, 1.0, ownT, slotsT);
+      pu.push_back((int32_t)u);
+    }
+  std::vector<int> cs, csT(TR.children.size(), 0);  // the count terms
+  for (size_t j = 0; j < R.children.size(); j++) cs.push_back((int)j == jT ? -1 : 0);
+  out(rp);
+  emit_term(rp, c, c->root, 1.0, {}, cs);
+  out(tp);
+  emit_term(tp, c, T, 1.0, {}, csT);
+}
+
 }  // namespace
 
 extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
@@ -694,6 +772,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   c->query_slot.assign(c->queries.size(), 0);
   std::vector<Program> gprogs;
   c->groups.clear();
+  c->revs.clear();
   c->code_cache.clear();
   for (size_t q = 0; q < c->queries.size(); q++) {
     const Query& Q = c->queries[q];
@@ -708,7 +787,26 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       c->query_slot[q] = (int)c->groups.size();
       c->groups.emplace_back();
       Program gp;
-      for (auto& u : Q.udafs) append_udaf_program(c, gp, u);
+      int T = -1;
+      for (int a : Q.gb)
+        if (c->owner[a] != c->root && !c->rels[c->owner[a]].unique_key) T = c->owner[a];
+      if (T >= 0) {  // finished at T (k_rev_*); no fused-scan program
+        c->groups.back().rev = (int)c->revs.size();
+        c->revs.emplace_back();
+        RevPlan& rv = c->revs.back();
+        rv.gi = (int)c->groups.size() - 1;
+        Program rp, tp;
+        std::vector<int32_t> pu;
+        build_rev(c, Q, T, rv, rp, tp, pu);
+        CTX_CUDA(c, rv.rp.upload(rp, st), "plan rev");
+        CTX_CUDA(c, rv.tp.upload(tp, st), "plan rev");
+        CTX_CUDA(c, rv.pu.alloc(std::max<size_t>(pu.size(), 1) * 4), "plan rev");
+        if (!pu.empty())
+          CTX_CUDA(c, cudaMemcpyAsync(rv.pu.p, pu.data(), pu.size() * 4, cudaMemcpyHostToDevice, st), "plan rev");
+        CTX_CUDA(c, rv.A.alloc((size_t)std::max<int64_t>(c->rels[T].nkeys, 1) * rv.rp.nout * 8), "plan rev");
+      } else {
+        for (auto& u : Q.udafs) append_udaf_program(c, gp, u);
+      }
       gprogs.push_back(std::move(gp));
     }
   }
@@ -830,6 +928,8 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     for (size_t gi = 0; gi < c->groups.size(); gi++) {
       GroupPlan& gp = c->groups[gi];
       const Query& Q = c->queries[gp.q];
+      const bool rev = gp.rev >= 0;  // finished at its child: no fused-scan outputs (and no new view slots:
+                                     // the views are laid out already)
       GroupDesc d{};
       d.ngb = gp.g.ngb;
       d.nudaf = gp.nudaf;
@@ -860,6 +960,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
         d.countlike[j] = constant;
         if (!constant) d.nsum++;
         if (constant) cc[j] = coef;
+        if (rev) continue;
         all.out_ioff.push_back((int)all.ip.size());
         all.out_doff.push_back((int)all.dp.size());
         all.ip.push_back((int)u.size());
@@ -874,9 +975,14 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       CTX_CUDA(c, gp.countcoef.alloc(cc.size() * 8), "plan");
       CTX_CUDA(c, cudaMemcpyAsync(gp.countcoef.p, cc.data(), cc.size() * 8, cudaMemcpyHostToDevice, st), "plan");
       gp.d.countcoef = gp.countcoef.as<double>();
+      if (gp.rev >= 0) {  // finished at its child, not by the fused scan
+        c->revs[gp.rev].d = d;
+        continue;
+      }
       descs.push_back(d);
     }
     CTX_CUDA(c, c->group_prog.upload(all, st), "plan upload groups");
+    c->ndescs = (int)descs.size();
     CTX_CUDA(c, c->group_descs.alloc(std::max<size_t>(descs.size(), 1) * sizeof(GroupDesc)), "plan");
     if (!descs.empty())
       CTX_CUDA(c, cudaMemcpyAsync(c->group_descs.p, descs.data(), descs.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice, st),
@@ -937,10 +1043,22 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
       CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "run memset");
       CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "run memset");
     }
-    CTX_CUDA(c, launch_groups_fused(ra, c->group_descs.as<GroupDesc>(), (int)c->groups.size(),
-                                    c->group_prog.pi.as<int32_t>(), c->group_prog.pd.as<double>(),
-                                    c->group_prog.pio.as<int32_t>(), c->group_prog.pdo.as<int32_t>(), st),
-             "run groups");
+    if (c->ndescs > 0)
+      CTX_CUDA(c, launch_groups_fused(ra, c->group_descs.as<GroupDesc>(), c->ndescs, c->group_prog.pi.as<int32_t>(),
+                                      c->group_prog.pd.as<double>(), c->group_prog.pio.as<int32_t>(),
+                                      c->group_prog.pdo.as<int32_t>(), st),
+               "run groups");
+    for (auto& rv : c->revs) {  // group-bys finished at a non-unique-keyed child
+      const Rel& R = c->rels[c->root];
+      const Rel& T = c->rels[rv.T];
+      auto pp = [](const DevProgram& p) {
+        return ProgPtrs{p.pi.as<int32_t>(), p.pd.as<double>(), p.pio.as<int32_t>(), p.pdo.as<int32_t>(), p.nout};
+      };
+      CTX_CUDA(c, launch_rev(ra, R.fk_dense[rv.j].as<int32_t>(), pp(rv.rp), node_args(c, rv.T),
+                             T.dense_key.as<int32_t>(), pp(rv.tp), rv.pu.as<int32_t>(), rv.A.as<double>(), T.nkeys,
+                             rv.d, st),
+               "run groups at a child");
+    }
   }
   // combine across GPUs (domain parallelism)
   if (c->world > 1) {
@@ -983,6 +1101,7 @@ extern "C" lmfao_status lmfao_reset_batch(lmfao_ctx* c) {
   c->scalar_queries.clear();
   c->scalar_off.clear();
   c->groups.clear();
+  c->revs.clear();
   c->code_cache.clear();
   c->query_kind.clear();
   c->query_slot.clear();

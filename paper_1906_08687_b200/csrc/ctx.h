@@ -125,6 +125,17 @@ struct GroupPlan {
   DevBuf rkeys, rvals, rcnts;
   DevBuf countcoef;
   int64_t ngroups = 0;
+  int rev = -1;  // index into lmfao_ctx::revs: finished at a non-unique-keyed root child
+};
+
+// A group-by query over the attributes of a root child T with a non-unique key (generic.cu
+// k_rev_root / k_rev_child): per product, its root side summed per key of T, then its T side.
+struct RevPlan {
+  int gi = -1, j = -1, T = -1;  // group, index of T among the root's children, relation
+  DevProgram rp, tp;            // one output per product + the count term
+  DevBuf pu;                    // product -> UDAF
+  DevBuf A;                     // [keys of T][products + 1]
+  GroupDesc d{};
 };
 
 }  // namespace lmfao
@@ -155,6 +166,8 @@ struct lmfao_ctx {
   DevBuf partials, cpart, scalar_out, scalar_count;
   int scalar_grid = 0;
   std::vector<GroupPlan> groups;
+  std::vector<RevPlan> revs;
+  int ndescs = 0;  // group-by queries of the fused generic scan
   std::map<int, std::shared_ptr<CodeSet>> code_cache;  // per group-by attribute
   DevProgram group_prog;  // all group-by UDAFs (fused scan)
   DevBuf group_descs;     // GroupDesc per group-by query

@@ -47,7 +47,7 @@ __device__ double eval_output(const NodeArgs& a, int64_t row, const int32_t* kk,
     }
     for (int c = 0; c < a.nchild; c++) {
       int slot = *ip++;
-      v = v * a.V[c][(int64_t)kk[c] * a.W[c] + slot];
+      if (slot >= 0) v = v * a.V[c][(int64_t)kk[c] * a.W[c] + slot];  // -1: the child is left out
     }
     sum += v;
   }
@@ -471,6 +471,83 @@ cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int n
   }
   k_groups_fused<<<grid_rows(a.nrows, 16), 256, smem, st>>>(a, descs, nq, prog_i, prog_d, ioff, doff);
   launches_add(1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- group-bys at a child
+// Group-by attributes of a root child T with a non-unique key (a row of T is not determined
+// by a root row): "each aggregate to its own root" — the root side of every
+// product is summed per key of T, A[k][p] = Σ_{root rows with T-key k} root_side_p(row)
+// (the other children through their views, T left out), and the query is finished at T:
+// Σ over T rows t of A[key(t)][p] · T_side_p(t) into the cell of t's group-by codes.
+// Output nout-1 of both programs is the count term (multiplicities).
+__global__ void k_rev_root(NodeArgs a, const int32_t* __restrict__ fkT, int nout, const int32_t* __restrict__ prog_i,
+                           const double* __restrict__ prog_d, const int32_t* __restrict__ ioff,
+                           const int32_t* __restrict__ doff, double* __restrict__ A) {
+  int32_t kk[MAX_CHILD];
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; base < a.nrows;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = base + (threadIdx.x & ~31) + lane;
+    const bool valid = row < a.nrows;
+    for (int c = 0; c < a.nchild; c++) kk[c] = valid ? a.fk[c][row] : 0;
+    const int key = valid ? fkT[row] : -1 - lane;
+    // runs of equal T keys (the root is sorted by its keys): a segmented scan per output,
+    // the run's last lane adds it
+    const int pk = __shfl_up_sync(0xffffffffu, key, 1);
+    const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || pk != key);
+    const int s0 = 31 - __clz(heads & ((2u << lane) - 1u));
+    const int nk = __shfl_down_sync(0xffffffffu, key, 1);
+    const bool tail = lane == 31 || nk != key;
+    for (int o = 0; o < nout; o++) {
+      double v = valid ? eval_output(a, row, kk, prog_i + ioff[o], prog_d + doff[o]) : 0.0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane - d >= s0) v += u;
+      }
+      if (tail && valid && v != 0.0) gred_add(&A[(int64_t)key * nout + o], v);
+    }
+  }
+}
+
+__global__ void k_rev_child(NodeArgs t, const int32_t* __restrict__ tkey, int nout, const int32_t* __restrict__ prog_i,
+                            const double* __restrict__ prog_d, const int32_t* __restrict__ ioff,
+                            const int32_t* __restrict__ doff, const int32_t* __restrict__ pu,
+                            const double* __restrict__ A, GroupDesc d) {
+  int32_t kk[MAX_CHILD];
+  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < t.nrows;
+       row += (int64_t)gridDim.x * blockDim.x) {
+    for (int c = 0; c < t.nchild; c++) kk[c] = t.fk[c][row];
+    const int64_t k = tkey[row];
+    long long cell = 0;
+    for (int i = 0; i < d.ngb; i++) cell += (long long)d.code[i][row] * d.stride[i];
+    const double* Ak = A + k * nout;
+    const double cnt = Ak[nout - 1] * eval_output(t, row, kk, prog_i + ioff[nout - 1], prog_d + doff[nout - 1]);
+    if (cnt == 0.0) continue;  // no root row joins this T row (or its subtree is empty)
+    gred_add(&d.counts[cell], (unsigned long long)cnt);
+    for (int p = 0; p < nout - 1; p++) {
+      const int u = pu[p];
+      if (d.countlike[u]) continue;
+      const double v = Ak[p] * eval_output(t, row, kk, prog_i + ioff[p], prog_d + doff[p]);
+      if (v != 0.0) gred_add(&d.table[cell * d.nudaf + u], v);
+    }
+  }
+}
+
+cudaError_t launch_rev(const NodeArgs& root, const int32_t* fkT, const ProgPtrs& rp, const NodeArgs& t,
+                       const int32_t* tkey, const ProgPtrs& tp, const int32_t* pu, double* A, int64_t nkT,
+                       const GroupDesc& d, cudaStream_t st) {
+  const int nout = rp.nout;
+  CUDA_TRY(cudaMemsetAsync(A, 0, (size_t)std::max<int64_t>(nkT, 1) * nout * 8, st));
+  if (root.nrows > 0) {
+    k_rev_root<<<grid_rows(root.nrows, 16), 256, 0, st>>>(root, fkT, nout, rp.pi, rp.pd, rp.io, rp.dofs, A);
+    launches_add(1);
+  }
+  if (t.nrows > 0) {
+    k_rev_child<<<grid_rows(t.nrows, 16), 256, 0, st>>>(t, tkey, nout, tp.pi, tp.pd, tp.io, tp.dofs, pu, A, d);
+    launches_add(1);
+  }
   return cudaGetLastError();
 }
 

@@ -224,6 +224,17 @@ struct GroupDesc {
 };
 cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int nq, const int32_t* prog_i,
                                 const double* prog_d, const int32_t* ioff, const int32_t* doff, cudaStream_t st);
+// group-by queries finished at a root child T with a non-unique key (generic.cu k_rev_*)
+struct ProgPtrs {
+  const int32_t* pi;
+  const double* pd;
+  const int32_t* io;
+  const int32_t* dofs;
+  int nout;
+};
+cudaError_t launch_rev(const NodeArgs& root, const int32_t* fkT, const ProgPtrs& rp, const NodeArgs& t,
+                       const int32_t* tkey, const ProgPtrs& tp, const int32_t* pu, double* A, int64_t nkT,
+                       const GroupDesc& d, cudaStream_t st);
 
 // Compaction of a dense cell table: present cells (count > 0) in ascending order.
 struct DecodeArgs {

@@ -42,6 +42,7 @@ FastPaths* plan_fast_paths(lmfao_ctx* c) {
   // LMFAO_GENERIC_ONLY=1 forces the interpreted path (used by tests to cross-check the two)
   const char* env = std::getenv("LMFAO_GENERIC_ONLY");
   if (env && env[0] == '1') return nullptr;
+  if (!c->revs.empty()) return nullptr;  // group-bys finished at a non-unique child: the generic scan
   const char* ng = std::getenv("LMFAO_NO_COV");  // tests: force the gram.cu kernel
   const char* nc = std::getenv("LMFAO_NO_CUBE");  // tests: keep group-bys on the generic scan
   const bool cube = !(nc && nc[0] == '1');
