@@ -211,3 +211,47 @@ def regression_tree(engine, features, target, thresholds, max_depth=4, min_split
         return out
 
     return node([], 0)
+
+
+# ------------------------------------------------------------------ root assignment
+def assign_roots(schemas, sizes, batch):
+    """LMFAO's root choice per query (§4): every query gives each relation the
+    fraction of its group-by attributes that the relation holds (a query without group-by
+    attributes gives every relation 1/m); relations are then taken in decreasing total weight
+    (ties: the larger relation) and each becomes the root of every still-unassigned query
+    that gave it a positive weight.  schemas: relation -> set of attribute names; sizes:
+    relation -> row count; batch: queries with .groupby.  Returns one relation per query."""
+    names = list(schemas)
+    m = len(names)
+    w = []
+    for q in batch:
+        gb = list(q.groupby)
+        if gb:
+            w.append({r: sum(a in schemas[r] for a in gb) / len(gb) for r in names})
+        else:
+            w.append({r: 1.0 / m for r in names})
+    total = {r: sum(x[r] for x in w) for r in names}
+    order = sorted(names, key=lambda r: (-total[r], -sizes[r], names.index(r)))
+    root = [None] * len(batch)
+    for r in order:
+        for i in range(len(batch)):
+            if root[i] is None and w[i][r] > 0:
+                root[i] = r
+    return root
+
+
+def reroot(edges, root):
+    """The edges (parent, child) of the same undirected join tree re-oriented away from root."""
+    adj = {}
+    for p, c in edges:
+        adj.setdefault(p, []).append(c)
+        adj.setdefault(c, []).append(p)
+    out, seen, stack = [], {root}, [root]
+    while stack:
+        u = stack.pop()
+        for v in adj.get(u, []):
+            if v not in seen:
+                seen.add(v)
+                out.append((u, v))
+                stack.append(v)
+    return out

@@ -224,3 +224,49 @@ def test_regression_tree_matches_numpy_cart():
     ref = _cart_numpy(_join(w.db), feats, "y", ts, 3, 2_000)
     _same_tree(tree, ref)
     assert "feature" in tree and "feature" in tree["left"]  # a non-trivial tree
+
+
+def test_assign_roots_follows_the_weights():
+    schemas = {"F": {"k1", "k2", "x"}, "D1": {"k1", "a", "b"}, "D2": {"k2", "c"}}
+    sizes = {"F": 1000, "D1": 10, "D2": 20}
+    Q = synth.Query
+    batch = [Q(["a", "b"], []), Q(["a"], []), Q(["c"], []), Q([], []), Q(["k1"], []), Q(["x", "c"], [])]
+    # weights: D1 1+1+1/3+1 (k1 is in F and D1) = 3.33, F 1/3+1+1/2 = 1.83, D2 1+1/3+1/2 = 1.83;
+    # order D1, F (larger than D2), D2
+    roots = apps.assign_roots(schemas, sizes, batch)
+    assert roots == ["D1", "D1", "D2", "D1", "D1", "F"]  # F beats D2 on size for the tie
+    # ties break towards the larger relation
+    assert apps.assign_roots({"A": {"u"}, "B": {"u"}}, {"A": 5, "B": 9}, [Q([], [])]) == ["B"]
+
+
+def test_reroot_keeps_the_tree():
+    edges = [("F", "D1"), ("F", "D2"), ("D2", "E")]
+    e = apps.reroot(edges, "E")
+    assert set(map(frozenset, e)) == set(map(frozenset, edges))
+    assert e[0] == ("E", "D2") and len(e) == 3
+
+
+@pytest.mark.gpu
+def test_batch_over_assigned_roots_matches_oracle():
+    """Results do not depend on the root (reading R16): run each query at the root the
+    heuristic assigns and compare with the oracle at the original root."""
+    from _parity import assert_parity, run_gpu
+    db = synth.random_db(21, max_rels=4, max_rows=600, unique_child_keys=True)
+    batch = synth.random_batch(5, db, n_queries=5, groupby_ok=lambda a: True)
+    schemas = {r.name: set(r.cols) for r in db.relations}
+    sizes = {r.name: len(next(iter(r.cols.values()))) for r in db.relations}
+    roots = apps.assign_roots(schemas, sizes, batch)
+    ref = oracle.evaluate(db, batch)
+    ran = 0
+    for r in set(roots):
+        sub = [q for q, rr in zip(batch, roots) if rr == r]
+        rdb = synth.Database(db.relations, r, apps.reroot(db.edges, r))
+        try:
+            got = run_gpu(rdb, sub)
+        except Exception as e:  # a shape the engine does not place at this root (e.g. deep group-bys)
+            if "UNSUPPORTED" in str(e):
+                continue
+            raise
+        assert_parity(got, [x for x, rr in zip(ref, roots) if rr == r], sub)
+        ran += 1
+    assert ran >= 1, roots
