@@ -46,6 +46,7 @@ constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][1
 constexpr int BRW = 36;      // doubles per B record
 constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
 constexpr int FIN_BLOCKS = 296;
+constexpr int SUM_SPLIT = 8;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
 constexpr unsigned FULL = 0xffffffffu;
 
 static_assert(SBLK % 128 == 0 && STG_G % 128 == 0, "TMA / cp.async alignment");
@@ -729,16 +730,19 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
 // src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  A CTA per 32
 // consecutive outputs: lane = output (coalesced rows), warp r of 32 sums rows r, r + 32, ...;
 // then a fixed-order sum over the warps (deterministic).
+// src[g][e] = Σ of chunk g (of SUM_SPLIT) of the partial rows of element e, fixed order
 __global__ void __launch_bounds__(1024) k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2,
                                                   int n2, double* __restrict__ src) {
-  const int e = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5, g = blockIdx.y;
   double s = 0.0;
   if (e < NPART) {
+    const int b0 = n1 * g / SUM_SPLIT, b1 = n1 * (g + 1) / SUM_SPLIT;
 #pragma unroll 4
-    for (int b = r; b < n1; b += 32) s += p1[(size_t)b * NPART + e];
+    for (int b = b0 + r; b < b1; b += 32) s += p1[(size_t)b * NPART + e];
   } else if (e < NPART + NFIN) {
+    const int b0 = n2 * g / SUM_SPLIT, b1 = n2 * (g + 1) / SUM_SPLIT;
 #pragma unroll 4
-    for (int b = r; b < n2; b += 32) s += p2[(size_t)b * NFIN + e - NPART];
+    for (int b = b0 + r; b < b1; b += 32) s += p2[(size_t)b * NFIN + e - NPART];
   }
   __shared__ double red[32][33];
   red[r][threadIdx.x & 31] = s;
@@ -746,8 +750,14 @@ __global__ void __launch_bounds__(1024) k_cov_sum(const double* __restrict__ p1,
   if (r == 0 && e < NPART + NFIN) {
     double t = 0.0;
     for (int i = 0; i < 32; i++) t += red[i][threadIdx.x];
-    src[e] = t;
+    src[(size_t)g * (NPART + NFIN) + e] = t;
   }
+}
+__device__ __forceinline__ double cov_src(const double* __restrict__ src, int e) {
+  double t = 0.0;
+#pragma unroll
+  for (int g = 0; g < SUM_SPLIT; g++) t += src[(size_t)g * (NPART + NFIN) + e];
+  return t;
 }
 
 __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __restrict__ toff,
@@ -755,10 +765,10 @@ __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __
                                double* __restrict__ out, int count_idx, unsigned long long* __restrict__ count) {
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * src[tidx[t]];
+    for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * cov_src(src, tidx[t]);
     out[o] = s;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)src[count_idx];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)cov_src(src, count_idx);
 }
 
 // ======================================================================= host
@@ -878,7 +888,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
   k_cov_fin<<<FIN_BLOCKS, 256, 0, st>>>(f);
-  k_cov_sum<<<(NPART + NFIN + 31) / 32, 1024, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(),
+  k_cov_sum<<<dim3((NPART + NFIN + 31) / 32, SUM_SPLIT), 1024, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(),
                                                       FIN_BLOCKS, src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                          tcoef.as<double>(), nout, c->scalar_out.as<double>(),
@@ -1029,7 +1039,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
   if (fc->partials.alloc((size_t)fc->grid * 16 * NPART * 8)) return nullptr;  // one partial per warp
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
-  if (fc->src.alloc((size_t)(NPART + NFIN) * 8)) return nullptr;
+  if (fc->src.alloc((size_t)SUM_SPLIT * (NPART + NFIN) * 8)) return nullptr;
   {  // scan layout of the root: x in DMMA lane order + dense keys, one 2432-byte block per 32 rows
     if (fc->scan.alloc((size_t)std::max<int64_t>(fc->nblk, 1) * SBLK)) return nullptr;
     LayoutArgs la{};
