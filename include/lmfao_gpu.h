@@ -68,10 +68,13 @@ typedef enum { LMFAO_INT32 = 0, LMFAO_FP64 = 1 } lmfao_dtype;
 
 /* Per-attribute functions f of a product term: constant, identity, and
  * the Kronecker delta 1_{X op t} for op in {<, <=, >, >=, =, !=}, compared in
- * IEEE double (int32 attributes convert exactly). */
+ * IEEE double (int32 attributes convert exactly); LMFAO_F_IN is set inclusion
+ * 1_{X ∈ S} for categorical splits, S ⊆ {0..52} given as the bit mask
+ * param = Σ_{v ∈ S} 2^v (an exact integer below 2^53): true iff X is an integer
+ * v in [0, 52] whose bit is set. */
 typedef enum {
   LMFAO_F_CONST = 0, LMFAO_F_IDENT = 1, LMFAO_F_LT = 2, LMFAO_F_LE = 3,
-  LMFAO_F_GT = 4, LMFAO_F_GE = 5, LMFAO_F_EQ = 6, LMFAO_F_NE = 7
+  LMFAO_F_GT = 4, LMFAO_F_GE = 5, LMFAO_F_EQ = 6, LMFAO_F_NE = 7, LMFAO_F_IN = 8
 } lmfao_fkind;
 
 typedef struct {

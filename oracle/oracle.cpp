@@ -44,7 +44,7 @@
 
 namespace {
 
-enum FactorKind { F_CONST = 0, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE };
+enum FactorKind { F_CONST = 0, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE, F_IN };
 
 struct Column {
   std::string name;
@@ -259,6 +259,11 @@ struct Oracle {
       case F_GE: return x >= f.param ? 1.0 : 0.0;
       case F_EQ: return x == f.param ? 1.0 : 0.0;
       case F_NE: return x != f.param ? 1.0 : 0.0;
+      case F_IN: {  // set inclusion, S as a bit mask over {0..52} (reading R20)
+        if (!(x >= 0.0 && x <= 52.0) || x != std::floor(x)) return 0.0;
+        const uint64_t mask = (uint64_t)f.param;
+        return ((mask >> (int)x) & 1u) ? 1.0 : 0.0;
+      }
     }
     throw std::runtime_error("bad factor kind");
   }

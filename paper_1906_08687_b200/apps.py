@@ -160,19 +160,26 @@ def chow_liu_tree(M):
 
 
 # ------------------------------------------------------------------ CART regression tree
-F_LE, F_GT, F_IDENT = 3, 4, 1  # lmfao_fkind
+F_LE, F_GT, F_IDENT, F_IN = 3, 4, 1, 8  # lmfao_fkind
 
 
-def regression_tree(engine, features, target, thresholds, max_depth=4, min_split=1000):
+def _mask(values):
+    return float(sum(1 << int(v) for v in values))
+
+
+def regression_tree(engine, features, target, thresholds, max_depth=4, min_split=1000, categoricals=()):
     """A CART regression tree (§3 "Decision trees" P:480-555; §6: depth 4, min split
     1000, 20 buckets) grown over the prepared relations of `engine`.
 
     Each node runs one batch (lmfao_reset_batch + add_query + plan + run): with α the node's
     path condition, RT(α, y·α, y²·α) for the node and for every candidate condition A ≤ t
-    (the rt.cu path takes α as a row filter).  The split with the largest variance reduction
-    SSE(node) − SSE(A ≤ t) − SSE(A > t), SSE = Σy² − (Σy)²/n, is taken; the right child's sums
-    are the node's minus the left's.  A node with fewer than `min_split` rows, at `max_depth`,
-    or without a split that reduces SSE is a leaf.  Returns nested dicts."""
+    (the rt.cu path takes α as a row filter), and Q(X; α·y^p) for every categorical X.  The
+    split with the largest variance reduction SSE(node) − SSE(left) − SSE(right),
+    SSE = Σy² − (Σy)²/n, is taken; the right side's sums are the node's minus the left's.
+    A categorical X splits by set inclusion (LMFAO_F_IN; values in [0, 52]): its
+    categories in increasing order of mean y (then value), cut after each prefix.  A node
+    with fewer than `min_split` rows, at `max_depth`, or without a split that reduces SSE is a
+    leaf.  Returns nested dicts."""
     y = [(F_IDENT, target, 0.0)]
 
     def node(path, depth):
@@ -183,6 +190,7 @@ def regression_tree(engine, features, target, thresholds, max_depth=4, min_split
                 cond = path + [(F_LE, a, float(t))]
                 udafs += [[(1.0, cond + y * p)] for p in range(3)]
         q = engine.add_query([], udafs)
+        qc = [engine.add_query([x], [[(1.0, path + y * p)] for p in range(3)]) for x in categoricals]
         engine.plan()
         engine.run()
         v = engine.fetch(q)[1][0]
@@ -192,22 +200,44 @@ def regression_tree(engine, features, target, thresholds, max_depth=4, min_split
             return out
         sse = s2 - s * s / n
         best = None
+
+        def consider(nl, sl, s2l, split):
+            nonlocal best
+            nr, sr, s2r = n - nl, s - sl, s2 - s2l
+            if nl < 0.5 or nr < 0.5:
+                return
+            gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
+            if best is None or gain > best[0]:
+                best = (gain, split)
+
         k = 3
         for a in features:
             for t in thresholds:
-                nl, sl, s2l = v[k], v[k + 1], v[k + 2]
+                consider(v[k], v[k + 1], v[k + 2], ("num", a, float(t)))
                 k += 3
-                nr, sr, s2r = n - nl, s - sl, s2 - s2l
-                if nl < 0.5 or nr < 0.5:
-                    continue
-                gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
-                if best is None or gain > best[0]:
-                    best = (gain, a, float(t))
+        for x, qx in zip(categoricals, qc):
+            keys, vals, _ = engine.fetch(qx)
+            cats = [(vals[i, 1] / vals[i, 0], int(keys[i, 0]), vals[i]) for i in range(len(keys)) if vals[i, 0] > 0]
+            if not cats or any(c < 0 or c > 52 for _, c, _ in cats):
+                continue
+            cats.sort(key=lambda e: (e[0], e[1]))
+            acc = np.zeros(3)
+            for i in range(len(cats) - 1):
+                acc = acc + cats[i][2]
+                left = [c for _, c, _ in cats[:i + 1]]
+                right = [c for _, c, _ in cats[i + 1:]]
+                consider(acc[0], acc[1], acc[2], ("cat", x, _mask(left), _mask(right)))
         if best is None or best[0] <= 0.0:
             return out
-        _, a, t = best
-        out.update(feature=a, threshold=t,
-                   left=node(path + [(F_LE, a, t)], depth + 1), right=node(path + [(F_GT, a, t)], depth + 1))
+        split = best[1]
+        if split[0] == "num":
+            _, a, t = split
+            out.update(feature=a, threshold=t,
+                       left=node(path + [(F_LE, a, t)], depth + 1), right=node(path + [(F_GT, a, t)], depth + 1))
+        else:
+            _, x, ml, mr = split
+            out.update(feature=x, categories=ml,
+                       left=node(path + [(F_IN, x, ml)], depth + 1), right=node(path + [(F_IN, x, mr)], depth + 1))
         return out
 
     return node([], 0)

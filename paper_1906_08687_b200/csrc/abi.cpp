@@ -575,7 +575,9 @@ lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* gro
       QProduct qp{pr.coeff, {}};
       for (int f = 0; f < pr.n_factors; f++) {
         const lmfao_factor& fa = pr.factors[f];
-        if (fa.kind < LMFAO_F_CONST || fa.kind > LMFAO_F_NE) return fail(c, LMFAO_ERR_INVALID_ARG, "bad factor kind");
+        if (fa.kind < LMFAO_F_CONST || fa.kind > LMFAO_F_IN) return fail(c, LMFAO_ERR_INVALID_ARG, "bad factor kind");
+        if (fa.kind == LMFAO_F_IN && !(fa.param >= 0.0 && fa.param < 9007199254740992.0 && fa.param == std::floor(fa.param)))
+          return fail(c, LMFAO_ERR_INVALID_ARG, "LMFAO_F_IN: the set mask must be an integer in [0, 2^53)");
         if (fa.kind == LMFAO_F_CONST) {
           qp.f.push_back(QFactor{fa.kind, -1, fa.param});
           continue;

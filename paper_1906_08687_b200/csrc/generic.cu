@@ -26,6 +26,7 @@ __device__ __forceinline__ double apply_factor(int kind, double x, double t) {
     case LMFAO_F_GE: return x >= t ? 1.0 : 0.0;
     case LMFAO_F_EQ: return x == t ? 1.0 : 0.0;
     case LMFAO_F_NE: return x != t ? 1.0 : 0.0;
+    case LMFAO_F_IN: return (x >= 0.0 && x <= 52.0 && x == floor(x) && ((unsigned long long)t >> (int)x) & 1ull) ? 1.0 : 0.0;
     default: return t;  // CONST
   }
 }

@@ -580,6 +580,7 @@ __device__ __forceinline__ bool rt_pred(int kind, double x, double t) {
     case LMFAO_F_GT: return x > t;
     case LMFAO_F_GE: return x >= t;
     case LMFAO_F_EQ: return x == t;
+    case LMFAO_F_IN: return x >= 0.0 && x <= 52.0 && x == floor(x) && (((unsigned long long)t >> (int)x) & 1ull);
     default: return x != t;
   }
 }
@@ -873,7 +874,7 @@ FastPaths* plan_rt(lmfao_ctx* c) {
         if (f.attr != yattr) return false;
         if (++out.pw > 2) return false;
       } else {
-        if (!allow_pred || out.pattr >= 0) return false;
+        if (!allow_pred || out.pattr >= 0 || f.kind == LMFAO_F_IN) return false;  // IN: only in a path condition
         out.pattr = f.attr;
         out.kind = f.kind;
         out.t = f.param;

@@ -28,7 +28,7 @@ STATUS = {0: "LMFAO_OK", 1: "LMFAO_ERR_INVALID_ARG", 2: "LMFAO_ERR_STATE", 3: "L
           7: "LMFAO_ERR_RUNNING_INTERSECTION", 8: "LMFAO_ERR_UNSUPPORTED", 9: "LMFAO_ERR_OOM",
           10: "LMFAO_ERR_CUDA", 11: "LMFAO_ERR_NCCL"}
 INT32, FP64 = 0, 1
-F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE = range(8)
+F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE, F_IN = range(9)
 UNIQUE_ID_BYTES = 128
 COLS_HOST, COLS_DEVICE, COLS_HOST_DEFERRED = 0, 1, 2
 

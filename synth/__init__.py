@@ -26,7 +26,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 # factor kinds (constant, identity, Kronecker 1_{X op t})
-F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE = range(8)
+F_CONST, F_IDENT, F_LT, F_LE, F_GT, F_GE, F_EQ, F_NE, F_IN = range(9)
 
 
 @dataclass

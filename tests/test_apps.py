@@ -165,10 +165,10 @@ def test_consumers_on_gpu_results():
     assert apps.chow_liu_tree(Mg) == apps.chow_liu_tree(Mo)
 
 
-def _cart_numpy(J, features, target, thresholds, max_depth, min_split):
+def _cart_numpy(J, features, target, thresholds, max_depth, min_split, categoricals=()):
     """The same CART over the materialised join (numpy masks)."""
     y = J[target].to_numpy()
-    cols = {a: J[a].to_numpy().astype(np.float64) for a in features}
+    cols = {a: J[a].to_numpy().astype(np.float64) for a in list(features) + list(categoricals)}
 
     def node(mask, depth):
         n = mask.sum()
@@ -178,23 +178,40 @@ def _cart_numpy(J, features, target, thresholds, max_depth, min_split):
             return out
         sse = s2 - s * s / n
         best = None
+
+        def consider(lm, split):
+            nonlocal best
+            nl = lm.sum()
+            nr = n - nl
+            if nl == 0 or nr == 0:
+                return
+            sl, s2l = y[lm].sum(), (y[lm] ** 2).sum()
+            sr, s2r = s - sl, s2 - s2l
+            gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
+            if best is None or gain > best[0]:
+                best = (gain, split)
+
         for a in features:
             for t in thresholds:
-                lm = mask & (cols[a] <= t)
-                nl = lm.sum()
-                nr = n - nl
-                if nl == 0 or nr == 0:
-                    continue
-                sl, s2l = y[lm].sum(), (y[lm] ** 2).sum()
-                sr, s2r = s - sl, s2 - s2l
-                gain = sse - (s2l - sl * sl / nl) - (s2r - sr * sr / nr)
-                if best is None or gain > best[0]:
-                    best = (gain, a, t)
+                consider(mask & (cols[a] <= t), ("num", a, t))
+        for x in categoricals:
+            vals = np.unique(cols[x][mask])
+            cats = sorted(((y[mask & (cols[x] == c)].mean(), int(c)) for c in vals))
+            for i in range(len(cats) - 1):
+                left = [c for _, c in cats[:i + 1]]
+                consider(mask & np.isin(cols[x], left), ("cat", x, left))
         if best is None or best[0] <= 0:
             return out
-        _, a, t = best
-        out.update(feature=a, threshold=t, left=node(mask & (cols[a] <= t), depth + 1),
-                   right=node(mask & (cols[a] > t), depth + 1))
+        split = best[1]
+        if split[0] == "num":
+            _, a, t = split
+            out.update(feature=a, threshold=t, left=node(mask & (cols[a] <= t), depth + 1),
+                       right=node(mask & (cols[a] > t), depth + 1))
+        else:
+            _, x, left = split
+            lm = np.isin(cols[x], left)
+            out.update(feature=x, categories=float(sum(1 << c for c in left)), left=node(mask & lm, depth + 1),
+                       right=node(mask & ~lm, depth + 1))
         return out
 
     return node(np.ones(len(J), bool), 0)
@@ -204,7 +221,8 @@ def _same_tree(g, r):
     assert g["n"] == r["n"] and math.isclose(g["mean"], r["mean"], rel_tol=1e-9, abs_tol=1e-12)
     assert ("feature" in g) == ("feature" in r), (g.get("feature"), r.get("feature"))
     if "feature" in g:
-        assert (g["feature"], g["threshold"]) == (r["feature"], r["threshold"])
+        assert g["feature"] == r["feature"] and g.get("threshold") == r.get("threshold")
+        assert g.get("categories") == r.get("categories")
         _same_tree(g["left"], r["left"])
         _same_tree(g["right"], r["right"])
 
@@ -270,3 +288,28 @@ def test_batch_over_assigned_roots_matches_oracle():
         assert_parity(got, [x for x, rr in zip(ref, roots) if rr == r], sub)
         ran += 1
     assert ran >= 1, roots
+
+
+@pytest.mark.gpu
+def test_regression_tree_with_categorical_splits():
+    """Categorical features split by set inclusion: node paths carry LMFAO_F_IN."""
+    from paper_1906_08687_b200 import lmfao
+    w = synth.config3(seed=3, fact_rows=30_000, dim_rows=(40, 300, 2000))
+    rng = np.random.default_rng(9)
+    F = w.db.rel("F")
+    cat = rng.integers(0, 7, F.nrows).astype(np.int32)
+    F.cols["cat"] = cat
+    F.cols["y"] = F.cols["y"] + np.array([0.0, 3.0, -2.0, 1.0, 5.0, -4.0, 0.5])[cat]  # y depends on cat
+    D = w.db.rel("D1")
+    D.cols["dc"] = rng.integers(0, 5, D.nrows).astype(np.int32)
+    feats = ["x1", "d2_3"]
+    ts = synth.thresholds_c3()[::4]
+    e = lmfao.Engine()
+    try:
+        lmfao.load(e, w.db, [])
+        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=1_000, categoricals=["cat", "dc"])
+    finally:
+        e.close()
+    ref = _cart_numpy(_join(w.db), feats, "y", ts, 3, 1_000, categoricals=["cat", "dc"])
+    _same_tree(tree, ref)
+    assert tree.get("feature") == "cat" and "categories" in tree

@@ -141,3 +141,25 @@ def test_classification_node_small(n):
     gpu, info = run_gpu(db, batch, info=True)
     assert info["fast_path"]["kind"] == "rt", info["fast_path"]
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+def test_path_with_set_inclusion():
+    """Categorical splits on the path (LMFAO_F_IN): root and dimension categoricals."""
+    from synth import F_IN
+    db = rt_db(8, 20_000)
+    path = [Factor(F_IN, "c1", float((1 << 0) | (1 << 3) | (1 << 4) | (1 << 8))),
+            Factor(F_IN, "g2", float(sum(1 << v for v in range(0, 19, 2)))), Factor(F_GE, "x2", -1.0)]
+    batch = node_batch(path, SPLITS[:4], ["g1", "c2"])
+    gpu, info = run_gpu(db, batch, info=True)
+    assert info["fast_path"]["kind"] == "rt" and info["fast_path"]["path_preds"] == 3, info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+def test_set_inclusion_in_products_interpreted():
+    """LMFAO_F_IN inside products the histogram path does not take: the interpreted scan."""
+    from synth import F_IN
+    db = rt_db(9, 6_000)
+    m = float((1 << 1) | (1 << 2) | (1 << 52))
+    batch = [Query(["c1"], [[Product(1.0, (Factor(F_IN, "g3", m),))], [Product(1.0, (Factor(F_IN, "e1", m), ident("x2")))]]),
+             Query([], [[Product(1.0, (Factor(F_IN, "i1", m), ident("y"), ident("x1")))]])]
+    assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)

@@ -101,8 +101,12 @@ def _eval_products(J, udaf):
                 x = np.full(len(J), f.param)
             else:
                 a = J[f.attr].to_numpy().astype(np.float64)
-                x = {F_IDENT: a, F_LT: (a < f.param) * 1.0, F_LE: (a <= f.param) * 1.0, F_GT: (a > f.param) * 1.0,
-                     F_GE: (a >= f.param) * 1.0, F_EQ: (a == f.param) * 1.0, F_NE: (a != f.param) * 1.0}[f.kind]
+                if f.kind == synth.F_IN:  # set inclusion: the members of the mask, written out
+                    members = [v for v in range(53) if (int(f.param) >> v) & 1]
+                    x = np.isin(a, np.array(members, dtype=np.float64)) * 1.0
+                else:
+                    x = {F_IDENT: a, F_LT: (a < f.param) * 1.0, F_LE: (a <= f.param) * 1.0, F_GT: (a > f.param) * 1.0,
+                         F_GE: (a >= f.param) * 1.0, F_EQ: (a == f.param) * 1.0, F_NE: (a != f.param) * 1.0}[f.kind]
             v = v * x
         tot = tot + v
     return tot
@@ -394,3 +398,24 @@ def test_errors():
     Tt = synth.Relation("T", {"A": i([1]), "C": i([1])})
     with pytest.raises(ValueError, match="running intersection"):
         oracle.evaluate(synth.Database([Rr, Ss, Tt], "R", [("R", "S"), ("S", "T")]), [query([], ["1"])])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_set_inclusion_factor_vs_pandas(seed):
+    """LMFAO_F_IN (reading R20): 1[x ∈ S] for a bit mask S over {0..52}, against membership in
+    the listed set on the materialised join; values outside [0, 52], negative and fractional
+    values are never members."""
+    db = synth.random_db(100 + seed, max_rows=300)
+    rng = np.random.default_rng(seed)
+    attrs = [(r.name, c) for r in db.relations for c in r.cols]
+    batch = []
+    for _ in range(3):
+        name, col = attrs[rng.integers(len(attrs))]
+        mask = float(int(rng.integers(0, 2 ** 20)) | (1 << 52) | 1)
+        other = attrs[rng.integers(len(attrs))][1]
+        batch.append(synth.Query([], [[synth.Product(1.0, (synth.Factor(synth.F_IN, col, mask),))],
+                                     [synth.Product(2.0, (synth.Factor(synth.F_IN, col, mask), synth.ident(other)))]]))
+    res = oracle.evaluate(db, batch)
+    ref = _brute(db, batch)
+    for r, (k, v, n) in zip(res, ref):
+        assert np.allclose(r.vals, v, rtol=1e-12, atol=1e-9), (r.vals, v)
