@@ -73,9 +73,12 @@ def ridge_bgd(C, label, lam=1e-3, tol=1e-10, max_iter=100_000, armijo_c=1e-4, sh
     J = ridge_objective(C, label, theta, lam)
     s = 1.0
     prev = None
+    stall = 0
     for it in range(1, max_iter + 1):
         gg = g @ g
-        if math.sqrt(gg) <= tol * max(1.0, abs(J)):
+        if math.sqrt(gg) <= tol * max(1.0, abs(J)) or stall >= 50:
+            # converged, or at the floating-point floor: 50 steps without a decrease of J
+            # beyond its rounding (BB steps then only wander inside the noise of ∇J)
             return theta, it - 1, True
         if prev is not None:  # Barzilai-Borwein: s = Δθ·Δθ / Δθ·Δg
             dt, dg = theta - prev[0], g - prev[1]
@@ -88,6 +91,7 @@ def ridge_bgd(C, label, lam=1e-3, tol=1e-10, max_iter=100_000, armijo_c=1e-4, sh
                 break
             s *= shrink
         prev = (theta, g)
+        stall = stall + 1 if J - Jc <= 1e-15 * max(1.0, abs(J)) else 0
         theta, J = cand, Jc
         g = ridge_gradient(C, label, theta, lam)
     return theta, max_iter, False
