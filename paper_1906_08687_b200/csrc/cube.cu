@@ -54,6 +54,9 @@ struct CubeItem {
   int16_t qk;  // cuboid within its level
   int16_t u;
   int16_t t0, t1;
+  int32_t j1;  // single-term UDAF (t1 == t0 + 1): S index and coefficient, no term loop
+  int32_t pad_;
+  double c1;
 };
 struct CubeArgs {
   int64_t nrows;
@@ -271,7 +274,9 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                 const int t = tb + sub;
                 if (sub < tp && t < nt) {
                   double val = 0.0;
-                  for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
+                  if (e.t1 == e.t0 + 1) val = e.c1 * S[t * (CB_MEAS + 1) + e.j1];
+                  else
+                    for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
                   if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
                 }
               }
@@ -281,7 +286,9 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                   const CubeItem e = items[i0 + it];
                   const Cuboid& q = sq[q0 + e.qk];
                   double val = 0.0;
-                  for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
+                  if (e.t1 == e.t0 + 1) val = e.c1 * S[t * (CB_MEAS + 1) + e.j1];
+                  else
+                    for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
                   if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
                 }
             }
@@ -586,7 +593,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
       for (size_t u = 0; u < qs[k].terms.size(); u++) {
         const auto& t = qs[k].terms[u];
         if (t.empty()) continue;  // constant UDAF: from the count at compaction
-        CubeItem e{(int16_t)(k - a.qbeg[d]), (int16_t)u, (int16_t)tj.size(), 0};
+        CubeItem e{(int16_t)(k - a.qbeg[d]), (int16_t)u, (int16_t)tj.size(), 0, t[0].first, 0, t[0].second};
         for (auto& jt : t) {
           tj.push_back((int8_t)jt.first);
           tc.push_back(jt.second);
