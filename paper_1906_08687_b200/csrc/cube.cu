@@ -37,7 +37,7 @@ struct Cuboid {
   long long stride[CB_GB];
   int8_t aslot[CB_GB];          // group-by attribute i -> batch attribute slot
   int ngb, nudaf;
-  int sparse, pad0_;
+  int sparse, derived;          // derived: rolled up from a sparse cuboid's groups (finish_sparse), not flushed
   double* table;                // [cells][nudaf]; constant UDAFs are left to the compaction (countcoef)
   unsigned long long* counts;
   // sparse cuboid (too many cells for a dense table): one record per run end, sorted and
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
               const bool act = sub < tp && t < nt;
               const Cuboid& q = sq[q0 + (act ? qk : 0)];
               long long cell = 0;
-              if (act) {
+              if (act && !q.derived) {
                 for (int i = 0; i < q.ngb; i++) cell += (long long)codes[t * CB_ATTR + q.aslot[i]] * q.stride[i];
                 cells[t * CB_QD + qk] = cell;
                 if (!q.sparse) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
@@ -319,6 +319,20 @@ struct RecReduce {
   int32_t* okeys;
   double* ovals;
   unsigned long long* ocnts;
+  int nder;
+  const struct Rollup* der;
+};
+// A dense cuboid X at the sparse cuboid Y's level whose attributes are a subset of Y's: its
+// cells are sums of Y's groups (X = Σ over Y's other attributes), added per reduced group of Y
+// instead of per run end.
+struct Rollup {
+  double* table;
+  unsigned long long* counts;
+  const double* coef;  // [nudaf][M1]
+  int nudaf, ngb;
+  int pos[CB_GB];      // X's attribute i is Y's attribute pos[i]
+  long long stride[CB_GB];
+  unsigned long long cmask;
 };
 __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -340,6 +354,21 @@ __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
       r.ovals[g * r.nudaf + u] = v;
     }
     r.ocnts[g] = (unsigned long long)S[0];
+    for (int x = 0; x < r.nder; x++) {
+      const Rollup& X = r.der[x];
+      long long xc = 0;
+      for (int i = 0; i < X.ngb; i++) {
+        const int p = X.pos[i];
+        xc += (long long)((cell / r.d.stride[p]) % r.d.radix[p]) * X.stride[i];
+      }
+      gred_add(&X.counts[xc], (unsigned long long)S[0]);
+      for (int u = 0; u < X.nudaf; u++) {
+        if (X.cmask >> u & 1ull) continue;
+        double v = 0.0;
+        for (int j = 0; j < r.M1; j++) v = fma(X.coef[u * r.M1 + j], S[j], v);
+        if (v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
+      }
+    }
   }
 }
 
@@ -347,6 +376,8 @@ struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
   int gi = -1, coff = 0, bits = 1;
   long long cap = 0;
   DevBuf key, val, n, perm, head, excl;
+  std::vector<Rollup> der;  // dense cuboids rolled up from this one's groups
+  DevBuf dder;
 };
 
 struct FastCube : FastPaths {
@@ -424,6 +455,8 @@ struct FastCube : FastPaths {
       r.okeys = gp.rkeys.as<int32_t>();
       r.ovals = gp.rvals.as<double>();
       r.ocnts = gp.rcnts.as<unsigned long long>();
+      r.nder = (int)sp.der.size();
+      r.der = sp.dder.as<Rollup>();
       k_rec_reduce<<<cgrid((int64_t)n), 256, 0, st>>>(r);
       launches_add(3);
       CUDA_TRY(cudaGetLastError());
@@ -560,9 +593,11 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   const int64_t sparse_min = smin ? std::atoll(smin) : ((int64_t)1 << 25);
   std::vector<Cuboid> hq;
   std::vector<double> dense;
+  std::vector<int> coffs, sparse_of(qs.size(), -1);
   for (size_t k = 0; k < qs.size(); k++) {
     hq.push_back(qs[k].q);
     const int coff = (int)dense.size();
+    coffs.push_back(coff);
     dense.insert(dense.end(), qs[k].dense.begin(), qs[k].dense.end());
     GroupPlan& gp = c->groups[qs[k].gi];
     if (!allow_sparse || gp.ncells <= sparse_min || gp.ncells > ((int64_t)1 << 32)) continue;
@@ -580,8 +615,42 @@ FastPaths* plan_cube(lmfao_ctx* c) {
     q.rval = sp.val.as<double>();
     q.rn = sp.n.as<unsigned long long>();
     q.rcap = sp.cap;
+    sparse_of[k] = (int)fc->sparse.size();
     fc->sparse.push_back(std::move(sp));
   }
+  // dense cuboids at a sparse cuboid's level over a subset of its attributes: rolled up from
+  // its reduced groups (one update per group, not per run end; C5's {A,C}, {B,C}, {C} from
+  // {A,B,C}).  LMFAO_CUBE_ROLLUP=0: off.
+  std::vector<std::vector<int>> der_coff(fc->sparse.size());
+  const char* ru = std::getenv("LMFAO_CUBE_ROLLUP");
+  if (!(ru && ru[0] == '0'))
+    for (size_t k = 0; k < qs.size(); k++) {
+      if (hq[k].sparse) continue;
+      for (size_t y = 0; y < qs.size(); y++) {
+        if (sparse_of[y] < 0 || qs[y].depth != qs[k].depth) continue;
+        Rollup ro{};
+        bool sub = true;
+        for (int i = 0; i < hq[k].ngb && sub; i++) {
+          int p = -1;
+          for (int t = 0; t < hq[y].ngb; t++)
+            if (hq[y].aslot[t] == hq[k].aslot[i]) p = t;
+          sub = p >= 0;
+          ro.pos[i] = p;
+          ro.stride[i] = hq[k].stride[i];
+        }
+        if (!sub) continue;
+        ro.table = hq[k].table;
+        ro.counts = hq[k].counts;
+        ro.nudaf = hq[k].nudaf;
+        ro.ngb = hq[k].ngb;
+        for (int u = 0; u < hq[k].nudaf; u++)
+          if (qs[k].terms[u].empty()) ro.cmask |= 1ull << u;
+        hq[k].derived = 1;
+        fc->sparse[sparse_of[y]].der.push_back(ro);
+        der_coff[sparse_of[y]].push_back(coffs[k]);
+        break;
+      }
+    }
   // items: (cuboid, non-constant UDAF) pairs of the dense cuboids, by level, with their terms
   std::vector<CubeItem> items;
   std::vector<int8_t> tj;
@@ -589,7 +658,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   for (int d = 0; d <= CB_LEV; d++) {
     a.ibeg[d] = (int)items.size();
     for (int k = a.qbeg[d]; k < a.qbeg[d + 1]; k++) {
-      if (hq[k].sparse) continue;
+      if (hq[k].sparse || hq[k].derived) continue;
       for (size_t u = 0; u < qs[k].terms.size(); u++) {
         const auto& t = qs[k].terms[u];
         if (t.empty()) continue;  // constant UDAF: from the count at compaction
@@ -622,6 +691,14 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   if (!tj.empty() && (cudaMemcpyAsync(fc->dtj.p, tj.data(), tj.size(), cudaMemcpyHostToDevice, st) ||
                       cudaMemcpyAsync(fc->dtc.p, tc.data(), tc.size() * 8, cudaMemcpyHostToDevice, st)))
     return nullptr;
+  for (size_t y = 0; y < fc->sparse.size(); y++) {
+    SparseOut& sp = fc->sparse[y];
+    for (size_t x = 0; x < sp.der.size(); x++) sp.der[x].coef = fc->dcoef.as<double>() + der_coff[y][x];
+    if (sp.dder.alloc(std::max<size_t>(sp.der.size(), 1) * sizeof(Rollup))) return nullptr;
+    if (!sp.der.empty() &&
+        cudaMemcpyAsync(sp.dder.p, sp.der.data(), sp.der.size() * sizeof(Rollup), cudaMemcpyHostToDevice, st))
+      return nullptr;
+  }
   a.q = fc->dq.as<Cuboid>();
   a.items = fc->ditems.as<CubeItem>();
   a.tj = fc->dtj.as<int8_t>();
