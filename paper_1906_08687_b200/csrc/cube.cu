@@ -41,7 +41,7 @@ struct Cuboid {
   double* table;                // [cells][nudaf]; constant UDAFs are left to the compaction (countcoef)
   unsigned long long* counts;
   // sparse cuboid (too many cells for a dense table): one record per run end, sorted and
-  // reduced after the scan: rkey[slot] = cell, rval[j * rcap + slot] = S_j
+  // reduced after the scan: rkey[slot] = cell, rval[slot * (M + 1) + j] = S_j (a record's sums contiguous)
   unsigned* rkey;
   double* rval;
   unsigned long long* rn;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                 const long long slot = (long long)b0 + __popc(grp & ((1u << lane) - 1u));
                 if (rec && slot < q.rcap) {
                   q.rkey[slot] = (unsigned)cell;
-                  for (int j = 0; j < M1; j++) q.rval[j * q.rcap + slot] = S[t * (CB_MEAS + 1) + j];
+                  for (int j = 0; j < M1; j++) q.rval[slot * M1 + j] = S[t * (CB_MEAS + 1) + j];
                 }
               }
             }
@@ -342,7 +342,7 @@ __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
     int64_t t = i;
     do {
       const uint32_t p = r.perm[t];
-      for (int j = 0; j < r.M1; j++) S[j] += r.rval[j * r.rcap + p];
+      for (int j = 0; j < r.M1; j++) S[j] += r.rval[(int64_t)p * r.M1 + j];
       t++;
     } while (t < r.n && !r.head[t]);
     const int64_t g = r.excl[i];
