@@ -623,9 +623,11 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   // {A,B,C}).  LMFAO_CUBE_ROLLUP=0: off.
   std::vector<std::vector<int>> der_coff(fc->sparse.size());
   const char* ru = std::getenv("LMFAO_CUBE_ROLLUP");
+  const char* rmin = std::getenv("LMFAO_CUBE_ROLLUP_MIN");  // cuboids with fewer cells stay on the scan
+  const int64_t rollup_min = rmin ? std::atoll(rmin) : 0;
   if (!(ru && ru[0] == '0'))
     for (size_t k = 0; k < qs.size(); k++) {
-      if (hq[k].sparse) continue;
+      if (hq[k].sparse || c->groups[qs[k].gi].ncells < rollup_min) continue;
       for (size_t y = 0; y < qs.size(); y++) {
         if (sparse_of[y] < 0 || qs[y].depth != qs[k].depth) continue;
         Rollup ro{};
