@@ -65,6 +65,8 @@ struct CovArgs {
   int* work;
   int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L,
                // 16 no compute at all (pipeline only), 32 every block on the fast path, 64 no wait for gathers
+  int cold;    // blocks with at least this many level-A run starts (and no level-B start inside) take
+               // the per-row level-A path; 0: never (LMFAO_COV_COLD)
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -138,7 +140,8 @@ __global__ void k_cov_layout(LayoutArgs a) {
   }
 }
 
-constexpr int COV_W = 16;  // warps per CTA of the scan (one CTA per SM)
+constexpr int COV_W = 12;     // warps per CTA of the scan (one CTA per SM; 168 registers with the per-row path)
+constexpr int COV_COLD = 2;  // level-A run starts from which a block takes the per-row path (measured 2..6 alike)
 
 template <int W>
 struct CovCfg {
@@ -410,6 +413,85 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         C0 += xa;
         C1 += sv;
         C2 += tv;
+      }
+    } else if (NS >= 1 && g.cold > 0 && __popc(mAx) >= g.cold && !(mB & ~1u)) {
+      // cold block (many short level-A runs, no level-B run starting inside): instead of run
+      // ("segment") sums times the run's s_A row, every row's v = [x, s_L, (s_L8, s_L9, 1)]
+      // times its own s_A row — the same sum by linearity, Σ_run (Σ_rows v) ⊗ s_A =
+      // Σ_rows v ⊗ s_A(row) — without segment windows, records or their s_A loads.
+      const int* kas = ks + 32;
+      {  // the open run's rows from earlier blocks (carried in C) with its s_A row (row 0's key)
+        const int key0 = __shfl_sync(FULL, ka, 0);
+        const double* ar = g.VA + (size_t)(unsigned)key0 * GP;
+        const double b0 = ar[m];
+        const double2 b89 = *reinterpret_cast<const double2*>(ar + 8);
+        dmma(aRA[0], C0, b0);
+        dmma(aRA[1], C1, b0);
+        dmma(aRA[2], C2, b0);
+        r8[0] = fma(C0, b89.x, r8[0]);
+        r9[0] = fma(C0, b89.y, r9[0]);
+        r8[1] = fma(C1, b89.x, r8[1]);
+        r9[1] = fma(C1, b89.y, r9[1]);
+        r8[2] = fma(C2, b89.x, r8[2]);
+        r9[2] = fma(C2, b89.y, r9[2]);
+        SB0 += C0;
+        SB1 += C1;
+        SB2 += C2;
+        // carried rows: their count is the constant row (m == 2) of the t tile
+        const double nc = __shfl_sync(FULL, red4(C2), 8);
+        const double nq = k == 0 ? nc : 0.0;  // once per quad (SBn* are summed over k at push_B)
+        SBn = fma(nq, b0, SBn);
+        SBn8 = fma(nq, b89.x, SBn8);
+        SBn9 = fma(nq, b89.y, SBn9);
+        // H_A: each run's rows in this block (and the carried rows for row 0's run)
+        if (vr && (dA || lane == 0)) {
+          const unsigned above = mA & ~((2u << lane) - 1u);
+          const int end = above ? __ffs(above) - 1 : nv;
+          const unsigned len = (unsigned)(end - lane) + (lane == 0 ? (unsigned)nc : 0u);
+          if (!(g.ablate & 2)) gred_add(&g.HA[ka], len);
+        }
+        C0 = C1 = C2 = 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        double sam[4], s8[4], s9[4];  // the s_A rows of this lane's next 4 rows, loads in flight together
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          const int r = 4 * (4 * h + jj) + k;
+          const double* ar = g.VA + (size_t)(unsigned)(r < nv ? kas[r] : 0) * GP;
+          const double2 a89 = *reinterpret_cast<const double2*>(ar + 8);
+          sam[jj] = r < nv ? ar[m] : 0.0;
+          s8[jj] = r < nv ? a89.x : 0.0;
+          s9[jj] = r < nv ? a89.y : 0.0;
+        }
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        const int j = 4 * h + jj;
+        const double xa = xs[32 * j + lane];
+        const double* gr = gl + j * 4 * GP;
+        const double sv = gr[m];
+        const double tv = gr[tcol];
+        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
+        dmma(aXX, xa, xa);
+        dmma(aXL, xa, sv);
+        a8 = fma(xa, s89.x, a8);
+        a9 = fma(xa, s89.y, a9);
+        dmma(aRA[0], xa, sam[jj]);
+        dmma(aRA[1], sv, sam[jj]);
+        dmma(aRA[2], tv, sam[jj]);
+        r8[0] = fma(xa, s8[jj], r8[0]);
+        r9[0] = fma(xa, s9[jj], r9[0]);
+        r8[1] = fma(sv, s8[jj], r8[1]);
+        r9[1] = fma(sv, s9[jj], r9[1]);
+        r8[2] = fma(tv, s8[jj], r8[2]);
+        r9[2] = fma(tv, s9[jj], r9[2]);
+        SB0 += xa;
+        SB1 += sv;
+        SB2 += tv;
+        SBn += sam[jj];
+        SBn8 += s8[jj];
+        SBn9 += s9[jj];
+      }
       }
     } else {
       // segments of the block: segment 0 starts at row 0, segment s >= 1 at the s-th run start
@@ -807,7 +889,8 @@ struct FastCov : FastPaths {
 
 int cov_warps() {  // LMFAO_COV_W (diagnostics): 12 or 16 warps per CTA
   const char* e = std::getenv("LMFAO_COV_W");
-  return e && std::atoi(e) == 12 ? 12 : COV_W;
+  if (e) return std::atoi(e) == 12 ? 12 : 16;
+  return COV_W;
 }
 
 template <int W>
@@ -866,6 +949,8 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   {
     const char* ab = std::getenv("LMFAO_COV_ABLATE");
     g.ablate = ab ? std::atoi(ab) : 0;
+    const char* cd = std::getenv("LMFAO_COV_COLD");
+    g.cold = cd ? std::atoi(cd) : COV_COLD;
   }
   g.brec = brec.as<double>();
   g.bcap = bcap;

@@ -21,7 +21,7 @@ e.plan()
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
 for wv, mode in [(16, 0), (12, 0), (16, 1), (16, 2), (16, 8), (16, 11), (16, 16), (16, 17), (12, 17), (16, 32), (16, 43),
-                 (16, 64), (12, 64), (16, 0)]:
+                 (16, 64), (12, 64), (16, 128), (16, 0)]:
     os.environ["LMFAO_COV_ABLATE"] = str(mode)
     os.environ["LMFAO_COV_W"] = str(wv)
     for _ in range(3):
