@@ -420,7 +420,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
       // times its own s_A row — the same sum by linearity, Σ_run (Σ_rows v) ⊗ s_A =
       // Σ_rows v ⊗ s_A(row) — without segment windows, records or their s_A loads.
       const int* kas = ks + 32;
-      {  // the open run's rows from earlier blocks (carried in C) with its s_A row (row 0's key)
+      double nc = 0.0;
+      if (!(mA & 1u)) {  // row 0 continues the run open at the previous block's end: its rows from
+                         // earlier blocks (carried in C) with the run's s_A row (row 0's key)
         const int key0 = __shfl_sync(FULL, ka, 0);
         const double* ar = g.VA + (size_t)(unsigned)key0 * GP;
         const double b0 = ar[m];
@@ -438,19 +440,18 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         SB1 += C1;
         SB2 += C2;
         // carried rows: their count is the constant row (m == 2) of the t tile
-        const double nc = __shfl_sync(FULL, red4(C2), 8);
+        nc = __shfl_sync(FULL, red4(C2), 8);
         const double nq = k == 0 ? nc : 0.0;  // once per quad (SBn* are summed over k at push_B)
         SBn = fma(nq, b0, SBn);
         SBn8 = fma(nq, b89.x, SBn8);
         SBn9 = fma(nq, b89.y, SBn9);
-        // H_A: each run's rows in this block (and the carried rows for row 0's run)
-        if (vr && (dA || lane == 0)) {
-          const unsigned above = mA & ~((2u << lane) - 1u);
-          const int end = above ? __ffs(above) - 1 : nv;
-          const unsigned len = (unsigned)(end - lane) + (lane == 0 ? (unsigned)nc : 0u);
-          if (!(g.ablate & 2)) gred_add(&g.HA[ka], len);
-        }
         C0 = C1 = C2 = 0.0;
+      }
+      // H_A: each run's rows in this block (and the carried rows for row 0's run)
+      if (vr && (dA || lane == 0) && !(g.ablate & 2)) {
+        const unsigned above = mA & ~((2u << lane) - 1u);
+        const int end = above ? __ffs(above) - 1 : nv;
+        gred_add(&g.HA[ka], (unsigned)(end - lane) + (lane == 0 ? (unsigned)nc : 0u));
       }
 #pragma unroll
       for (int h = 0; h < 2; h++) {
