@@ -783,31 +783,32 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
       dmma(mB[3], n * s1, s1);
     }
   }
-  __shared__ double red[NFIN];
-  for (int i = threadIdx.x; i < NFIN; i += blockDim.x) red[i] = 0.0;
-  __syncthreads();
+  // each warp stores its fragments into its own slice (every element exactly once), then one
+  // barrier and a fixed-order sum over the 8 slices
+  extern __shared__ __align__(16) double fred[];  // [8][NFIN]
+  double* red = fred + (size_t)w * NFIN;
   auto put = [&](int base, int t1, int t2, const double (&c)[2]) {
     const int i = base + (8 * t1 + m) * 16 + 8 * t2 + 2 * k;
-    red[i] += c[0];
-    red[i + 1] += c[1];
+    *reinterpret_cast<double2*>(red + i) = make_double2(c[0], c[1]);
   };
-  for (int ww = 0; ww < 8; ww++) {
-    if (w == ww) {
 #pragma unroll
-      for (int t = 0; t < 5; t++) {
-        put(0, t, 0, rb[t][0]);
-        put(0, t, 1, rb[t][1]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        put(640, q >> 1, q & 1, mL[q]);
-        put(896, q >> 1, q & 1, mA[q]);
-        put(1152, q >> 1, q & 1, mB[q]);
-      }
-    }
-    __syncthreads();
+  for (int t = 0; t < 5; t++) {
+    put(0, t, 0, rb[t][0]);
+    put(0, t, 1, rb[t][1]);
   }
-  for (int i = threadIdx.x; i < NFIN; i += blockDim.x) a.partials[(size_t)blockIdx.x * NFIN + i] = red[i];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    put(640, q >> 1, q & 1, mL[q]);
+    put(896, q >> 1, q & 1, mA[q]);
+    put(1152, q >> 1, q & 1, mB[q]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NFIN; i += blockDim.x) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < 8; ww++) t += fred[(size_t)ww * NFIN + i];
+    a.partials[(size_t)blockIdx.x * NFIN + i] = t;
+  }
 }
 
 // src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  A CTA per 32
@@ -973,7 +974,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.VA = g.VA;
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
-  k_cov_fin<<<FIN_BLOCKS, 256, 0, st>>>(f);
+  k_cov_fin<<<FIN_BLOCKS, 256, 8 * NFIN * 8, st>>>(f);
   k_cov_sum<<<dim3((NPART + NFIN + 31) / 32, SUM_SPLIT), 1024, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(),
                                                       FIN_BLOCKS, src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
@@ -1218,6 +1219,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     cudaMemcpyAsync(fc->tcoef.p, tcoef.data(), tcoef.size() * 8, cudaMemcpyHostToDevice, st);
   }
   if (cudaStreamSynchronize(st)) return nullptr;
+  if (cudaFuncSetAttribute(k_cov_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * NFIN * 8)) return nullptr;
   return fc.release();
 }
 
