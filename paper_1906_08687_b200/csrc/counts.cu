@@ -29,7 +29,10 @@ struct CntQuery {
   int8_t a, b;      // attribute slots (b = -1: one attribute)
   int32_t sa;       // cell = code_a * sa + code_b
   unsigned long long* counts;
+  int32_t soff;     // >= 0: counted in the CTA's shared table at this offset (small tables)
+  int32_t ncell;
 };
+constexpr int CN_SMEM_CELLS = 12288;  // shared counters per CTA (48 KB) for the smallest tables
 struct CntArgs {
   int64_t nrows;
   int nattr, nlev, nq;
@@ -38,14 +41,18 @@ struct CntArgs {
   const int32_t* fk[CN_LEV];
   unsigned* H[CN_LEV];           // rows per key of the children with dimension-only queries (null: none)
   const CntQuery* q;             // [nq] per-row queries
+  int nsmall;                    // shared counters of the small tables
   unsigned long long* total;     // COUNT
 };
 
 // Per root row: the codes of every attribute, then each per-row query's cell.
 __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArgs a) {
-  extern __shared__ CntQuery sq[];
+  extern __shared__ __align__(16) unsigned char cnsm[];
+  CntQuery* sq = reinterpret_cast<CntQuery*>(cnsm);
+  unsigned* stab = reinterpret_cast<unsigned*>(cnsm + ((a.nq * sizeof(CntQuery) + 15) / 16) * 16);
   __shared__ int scode[8][CN_ATTR][32];  // this warp's codes (attribute x lane)
   for (int i = threadIdx.x; i < a.nq; i += blockDim.x) sq[i] = a.q[i];
+  for (int i = threadIdx.x; i < a.nsmall; i += blockDim.x) stab[i] = 0u;
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned long long tot = 0;
@@ -81,6 +88,10 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
     for (int qi = 0; qi < a.nq; qi++) {
       const CntQuery q = sq[qi];
       const int ca = scode[wib][q.a][lane], cb = q.b >= 0 ? scode[wib][q.b][lane] : 0;
+      if (q.soff >= 0) {  // a small table: the CTA's shared counters (native shared atomics)
+        if (v) atomicAdd(&stab[q.soff + ca * q.sa + cb], 1u);
+        continue;
+      }
       const int cell = v ? ca * q.sa + cb : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, cell);
       if (v && (__ffs(peers) - 1) == lane) atomicAdd(&q.counts[cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
@@ -90,6 +101,16 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(CFULL, tot, o);
   if (lane == 0 && a.total) atomicAdd(a.total, tot);
+  if (a.nsmall == 0) return;
+  __syncthreads();
+  for (int qi = 0; qi < a.nq; qi++) {  // the shared counters -> the global tables
+    const CntQuery q = sq[qi];
+    if (q.soff < 0) continue;
+    for (int c = threadIdx.x; c < q.ncell; c += blockDim.x) {
+      const unsigned n = stab[q.soff + c];
+      if (n) gred_add(&q.counts[c], (unsigned long long)n);
+    }
+  }
 }
 
 // Scalar queries of the batch: every UDAF is a constant c, value = c * COUNT.
@@ -131,7 +152,8 @@ struct FastCounts : FastPaths {
   DevBuf dq, ddq, Hbuf, scoef;
   int nscalar = 0;
   int64_t hwords = 0;
-  int nrowq = 0, ndimq = 0;
+  int nrowq = 0, ndimq = 0, grid = 148 * 8;
+  size_t smem = 0;
   bool scalar = false;
   std::string describe() const override {
     char b[160];
@@ -157,7 +179,7 @@ int FastCounts::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar
   }
   scan_timer_begin(c, st);
   if (a.nrows > 0) {
-    k_cnt_rows<<<148 * 8, 256, std::max<size_t>((size_t)nrowq * sizeof(CntQuery), 16), st>>>(a);
+    k_cnt_rows<<<grid, 256, std::max<size_t>(smem, 16), st>>>(a);
     launches_add(1);
   }
   scan_timer_end(c, st);
@@ -249,10 +271,26 @@ FastPaths* plan_counts(lmfao_ctx* c) {
     if (Q.gb.size() == 1) q.b = -1;
     q.sa = (int32_t)gp.g.stride[0];
     q.counts = gp.counts.as<unsigned long long>();
+    q.soff = -1;
+    q.ncell = (int32_t)gp.ncells;
     rq.push_back(q);
   }
   a.nattr = (int)slot.size();
   a.nq = (int)rq.size();
+  {  // the smallest per-row tables get shared counters (no warp matching, no global atomics per row)
+    const char* sc = std::getenv("LMFAO_CNT_SMEM_CELLS");
+    const int budget = sc ? std::atoi(sc) : CN_SMEM_CELLS;
+    std::vector<int> order(rq.size());
+    for (size_t i = 0; i < rq.size(); i++) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rq[x].ncell < rq[y].ncell; });
+    int used = 0;
+    for (int i : order)
+      if (used + rq[i].ncell <= budget) {
+        rq[i].soff = used;
+        used += rq[i].ncell;
+      }
+    a.nsmall = used;
+  }
   fc->nrowq = (int)rq.size();
   fc->ndimq = (int)dq.size();
   // H buffers
@@ -299,9 +337,19 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   fc->da.nq = (int)dq.size();
   fc->da.q = fc->ddq.as<CntDimQuery>();
   if (cudaStreamSynchronize(st)) return nullptr;
-  if ((size_t)rq.size() * sizeof(CntQuery) > 48 * 1024 &&
-      cudaFuncSetAttribute(k_cnt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(rq.size() * sizeof(CntQuery))))
-    return nullptr;
+  fc->smem = ((rq.size() * sizeof(CntQuery) + 15) / 16) * 16 + (size_t)a.nsmall * 4;
+  // (static scode + dynamic above 48 KB needs the opt-in; the attribute is process-wide: keep the max)
+  static int set_smem = 0;
+  if ((int)fc->smem > set_smem) {
+    if (cudaFuncSetAttribute(k_cnt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc->smem)) return nullptr;
+    set_smem = (int)fc->smem;
+  }
+  {
+    int per_sm = 0, nsm = 148;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cnt_rows, 256, fc->smem) || per_sm < 1) per_sm = 1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
+    fc->grid = nsm * std::min(per_sm, 8);
+  }
   return fc.release();
 }
 
