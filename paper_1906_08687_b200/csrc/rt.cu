@@ -301,7 +301,9 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
 // by its keys, so runs are long at the outer levels) and a run's total is carried across
 // blocks until it ends.  Run totals go to a per-CTA open-addressing table in shared
 // memory (Zipf-hot keys), to global atomics when a probe misses twice.
+constexpr int RT_VCHUNK = 16;  // blocks of 32 rows per dynamically taken chunk (k_rt_views)
 struct RtViewArgs {
+  int* work;  // chunk counter (zeroed per launch)
   int64_t nrows;
   const double* y;
   const uint8_t* filt;
@@ -345,10 +347,10 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     gred_add(e + 1, v1);
     gred_add(e + 2, v2);
   };
-  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t nblk = (a.nrows + 31) / 32;
-  const int64_t b0 = nblk * gw / nwarps, b1 = nblk * (gw + 1) / nwarps;
+  // warps take chunks of RT_VCHUNK blocks dynamically (Zipf-hot and -cold regions cost very
+  // differently); a run crossing a chunk edge is added in parts (linear)
+  const int64_t nblk = (a.nrows + 31) / 32, nchunks = (nblk + RT_VCHUNK - 1) / RT_VCHUNK;
+  int64_t b0 = 0, b1 = 0;
   int ckey[NLEV];
   double c0[NLEV], c1[NLEV], c2[NLEV];
   // lane-private sums of the carried run over blocks it goes on through (folded when it ends)
@@ -362,6 +364,22 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     dirty[l] = false;
   }
   // software pipeline: the next block's y and keys are loaded while this block is scanned
+  for (;;) {
+  {
+    int chk = 0;
+    if (lane == 0) chk = atomicAdd(a.work, 1);
+    chk = __shfl_sync(RFULL, chk, 0);
+    if (chk >= nchunks) break;
+    b0 = (int64_t)chk * RT_VCHUNK;
+    b1 = b0 + RT_VCHUNK < nblk ? b0 + RT_VCHUNK : nblk;
+  }
+#pragma unroll
+  for (int l = 0; l < NLEV; l++) {
+    ckey[l] = -1;
+    c0[l] = c1[l] = c2[l] = 0.0;
+    p0[l] = p1[l] = p2[l] = 0.0;
+    dirty[l] = false;
+  }
   double ny = 0.0;
   bool npass = false;
   int nkey[NLEV];
@@ -460,6 +478,7 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     }
     if (lane == 0 && ckey[l] >= 0) add(l, ckey[l], c0[l], c1[l], c2[l]);
   }
+  }  // chunks
   __syncthreads();
   for (int i = threadIdx.x; i < a.nlev * RT_HT; i += blockDim.x) {
     const int key = hkey[i];
@@ -664,7 +683,7 @@ struct FastRT : FastPaths {
   // path condition: the filter, and the unconditioned pass for the join multiplicities
   int nphi = 0;
   RtFilterArgs phi{};
-  DevBuf filt, acc_all, V_all;
+  DevBuf filt, acc_all, V_all, vwork;
   std::vector<FactHist> fh_cnt;  // TOT + root group histograms
   std::vector<DimHist> dh_cnt;   // dimension group histograms
   // classification node: one conditioned pass per class of ct_code
@@ -797,6 +816,8 @@ cudaError_t FastRT::pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const
   }
   if (nlev > 0 && R.nrows > 0 && !dhl.empty()) {
     RtViewArgs va{};
+    CUDA_TRY(cudaMemsetAsync(vwork.p, 0, 16, st));
+    va.work = vwork.as<int>();
     va.nrows = R.nrows;
     va.y = yp;
     va.filt = fp;
@@ -1278,7 +1299,7 @@ FastPaths* plan_rt(lmfao_ctx* c) {
       !up(rt->ct_tidx, ctidx.data(), ctidx.size() * 4) || !up(rt->ct_tcoef, ctcoef.data(), ctcoef.size() * 8))
     RT_DECLINE();
   if (rt->ncls > 0 && rt->acc_cls.alloc((size_t)rt->ncls * nacc * 8)) RT_DECLINE();
-  if (rt->acc.alloc(nacc * 8)) RT_DECLINE();
+  if (rt->acc.alloc(nacc * 8) || rt->vwork.alloc(16)) RT_DECLINE();
   if (rt->V.alloc(std::max<int64_t>(vt, 1) * 24)) RT_DECLINE();
   if (rt->nphi > 0 && (rt->acc_all.alloc(nacc * 8) || rt->V_all.alloc(std::max<int64_t>(vt, 1) * 24))) RT_DECLINE();
   if ((rt->nphi > 0 || rt->ncls > 0) && rt->filt.alloc(std::max<int64_t>(R.nrows, 1))) RT_DECLINE();
