@@ -280,22 +280,23 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   int prevL = -1, prevA = -1, prevB = -1;
   const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
-  auto hl_add = [&](int key, unsigned len) {
+  auto hl_add = [&](int key, unsigned len) {  // two probes, straight-line; full: global RED
     unsigned h = ((unsigned)key * 2654435761u) >> (32 - 10);
-#pragma unroll 1
-    for (int probe = 0; probe < 2; probe++) {
-      int t = hkey[h];
+    int t = hkey[h];
+    if (t == -1) {
+      const int old = atomicCAS(&hkey[h], -1, key);
+      t = old == -1 ? key : old;
+    }
+    if (t != key) {
+      h = (h + 1) & (HT - 1);
+      t = hkey[h];
       if (t == -1) {
         const int old = atomicCAS(&hkey[h], -1, key);
         t = old == -1 ? key : old;
       }
-      if (t == key) {
-        atomicAdd(&hcnt[h], len);
-        return;
-      }
-      h = (h + 1) & (HT - 1);
     }
-    gred_add(&g.HL[key], len);
+    if (t == key) atomicAdd(&hcnt[h], len);
+    else gred_add(&g.HL[key], len);
   };
   auto push_B = [&](int keyB) {
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
