@@ -140,11 +140,9 @@ __global__ void __launch_bounds__(GW * 32, 1) k_gram(const __grid_constant__ Gra
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2;
   const int wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int cn = g.cn;
-  const int nLe = g.nLe;
   const int64_t N = g.nrows;
   const int nitems = (int)((N + ITEM - 1) / ITEM);
   const int nB = g.nB;
-  const int nkeycols = 1 + (NS >= 1) + (NS == 2);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double* bacc = reinterpret_cast<double*>(smem_raw) + (size_t)wib * 24 * 16;  // [nw][24][16]
