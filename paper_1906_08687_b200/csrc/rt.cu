@@ -128,15 +128,13 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
     // per warp: [ncp][32] u32 counts, [ncp][32] y, [ncp][32] y^2
     unsigned char* wt = reinterpret_cast<unsigned char*>(rsm + a.tab_off) + (size_t)wib * ncp * 32 * 20;
     unsigned* tc = reinterpret_cast<unsigned*>(wt);
-    double* ty = reinterpret_cast<double*>(wt + ncp * 32 * 4);
-    double* ty2 = ty + ncp * 32;
+    double2* ty = reinterpret_cast<double2*>(wt + ncp * 32 * 4);  // (Σ y, Σ y²) per (cell, lane)
     __syncthreads();  // the previous piece's flush is done with the tables
     for (int i = threadIdx.x; i < h.nthr; i += blockDim.x) thr[i] = a.thr[h.thr_off + i];
     for (int i = threadIdx.x; i < 3 * h.nthr; i += blockDim.x) eqt[i] = 0.0;
     for (int i = lane; i < ncp * 32; i += 32) {
       tc[i] = 0;
-      ty[i] = 0.0;
-      ty2[i] = 0.0;
+      ty[i] = make_double2(0.0, 0.0);
     }
     __syncthreads();
     double t0 = 0.0, t1 = 0.0, t2 = 0.0;
@@ -196,13 +194,11 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
           n[1] = yy[1] = q[1] = 0.0;
         }
         const unsigned c0 = tc[e[0]], c1 = tc[e[1]];
-        const double y0 = ty[e[0]], y1 = ty[e[1]], s0 = ty2[e[0]], s1 = ty2[e[1]];
+        const double2 w0 = ty[e[0]], w1 = ty[e[1]];
         tc[e[1]] = c1 + (unsigned)n[1];
-        ty[e[1]] = y1 + yy[1];
-        ty2[e[1]] = s1 + q[1];
+        ty[e[1]] = make_double2(w1.x + yy[1], w1.y + q[1]);
         tc[e[0]] = c0 + (unsigned)n[0];
-        ty[e[0]] = y0 + yy[0];
-        ty2[e[0]] = s0 + q[0];
+        ty[e[0]] = make_double2(w0.x + yy[0], w0.y + q[0]);
       }
     }
     if (hi == 0) {
@@ -233,8 +229,8 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
           for (int l = 0; l < 32; l++) cs += reinterpret_cast<const unsigned*>(ww)[cell * 32 + l];
           sum += (double)cs;
         } else {
-          const double* tv = reinterpret_cast<const double*>(ww + ncp * 32 * 4) + (v - 1) * ncp * 32 + cell * 32;
-          for (int l = 0; l < 32; l++) sum += tv[l];
+          const double* tv = reinterpret_cast<const double*>(ww + ncp * 32 * 4) + 2 * cell * 32 + (v - 1);
+          for (int l = 0; l < 32; l++) sum += tv[2 * l];
         }
       }
       const int oc = h.is_code ? cell : 2 * cell;
