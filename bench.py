@@ -258,7 +258,8 @@ def main():
     alg_bytes = BYTES_PER_ROW[args.config] * rows_rank + dim_feature_bytes(w)
     scan_avg_s = (scan_ms / max(scan_n, 1)) / 1e3
     achieved = alg_bytes / scan_avg_s / 1e9 if scan_n else None
-    traffic = committed_traffic(args.config)
+    # the committed ncu capture is of the 1-GPU launch; a shard's launch has no capture
+    traffic = committed_traffic(args.config) if world == 1 else None
 
     # result check (cheap): the count equals the fact rows
     keys, vals, counts = eng.fetch(qids[0])
