@@ -346,8 +346,12 @@ __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
       t++;
     } while (t < r.n && !r.head[t]);
     const int64_t g = r.excl[i];
-    const long long cell = r.key[i];
-    for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][(cell / r.d.stride[a]) % r.d.radix[a]];
+    const unsigned cell = r.key[i];  // sparse cuboids have < 2^32 cells: 32-bit decode
+    unsigned code[CB_GB];
+    for (int a = 0; a < r.d.ngb; a++) {
+      code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
+      r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
+    }
     for (int u = 0; u < r.nudaf; u++) {
       double v = 0.0;
       for (int j = 0; j < r.M1; j++) v = fma(r.coef[u * r.M1 + j], S[j], v);
@@ -357,10 +361,7 @@ __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
     for (int x = 0; x < r.nder; x++) {
       const Rollup& X = r.der[x];
       long long xc = 0;
-      for (int i = 0; i < X.ngb; i++) {
-        const int p = X.pos[i];
-        xc += (long long)((cell / r.d.stride[p]) % r.d.radix[p]) * X.stride[i];
-      }
+      for (int i = 0; i < X.ngb; i++) xc += (long long)code[X.pos[i]] * X.stride[i];
       gred_add(&X.counts[xc], (unsigned long long)S[0]);
       for (int u = 0; u < X.nudaf; u++) {
         if (X.cmask >> u & 1ull) continue;
