@@ -24,7 +24,8 @@ namespace lmfao {
 namespace {
 
 constexpr int CB_LEV = 8;     // root children
-constexpr int CB_MEAS = 8;    // distinct measure attributes
+constexpr int CB_MEAS = 8;    // measure attributes per scan (more: one scan per group of 8)
+constexpr int CB_MAXM = 64;   // distinct measure attributes of a batch
 constexpr int CB_GB = 8;      // group-by attributes per cuboid
 constexpr int CB_ATTR = 8;    // distinct group-by attributes of the batch
 constexpr int CB_TERMS = 512; // UDAF terms of the batch (shared memory)
@@ -77,6 +78,7 @@ struct CubeArgs {
   const int8_t* tj;             // [nterm] S index (0 = count, 1 + measure)
   const double* tc;             // [nterm] coefficient
   int ablate;                   // LMFAO_CUBE_ABLATE (profiling): 1 no flush, 2 counts only
+  int nocount;                  // a later measure group's scan: the counts come from the first
 };
 
 unsigned cgrid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
               if (act && !q.derived) {
                 for (int i = 0; i < q.ngb; i++) cell += (long long)codes[t * CB_ATTR + q.aslot[i]] * q.stride[i];
                 cells[t * CB_QD + qk] = cell;
-                if (!q.sparse) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
+                if (!q.sparse && !a.nocount) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
               }
               const bool rec = act && q.sparse;
               if (__any_sync(BFULL, rec)) {  // warp-aggregated record slots per cuboid
@@ -383,6 +385,8 @@ struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
 
 struct FastCube : FastPaths {
   CubeArgs ca{};
+  std::vector<CubeArgs> parts;  // one scan per group of up to CB_MEAS measures
+  std::vector<DevBuf> pbuf;     // per part: items, tj, tc
   DevBuf dq, dcoef, ditems, dtj, dtc, dwork;
   std::vector<SparseOut> sparse;
   int nq = 0, grid = 148;
@@ -390,8 +394,11 @@ struct FastCube : FastPaths {
   bool graph_ok() const override { return sparse.empty(); }
   std::string describe() const override {
     char b[160];
-    std::snprintf(b, sizeof b, "{\"kind\": \"cube\", \"cuboids\": %d, \"sparse\": %d, \"measures\": %d, \"levels\": %d}",
-                  nq, (int)sparse.size(), ca.M, ca.R);
+    int m = 0;
+    for (auto& p : parts) m += p.M;
+    std::snprintf(b, sizeof b,
+                  "{\"kind\": \"cube\", \"cuboids\": %d, \"sparse\": %d, \"measures\": %d, \"scans\": %d, \"levels\": %d}",
+                  nq, (int)sparse.size(), m, (int)parts.size(), ca.R);
     return b;
   }
   bool handles_group(int) const override { return true; }
@@ -404,14 +411,17 @@ struct FastCube : FastPaths {
       CUDA_TRY(cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st));
     }
     for (auto& sp : sparse) CUDA_TRY(cudaMemsetAsync(sp.n.p, 0, 8, st));
-    CUDA_TRY(cudaMemsetAsync(dwork.p, 0, 4, st));
-    CubeArgs a = ca;
-    a.nrows = c->rels[c->root].nrows;
-    if (a.nrows > 0) {
-      const int64_t nch = (a.nrows + a.chunk - 1) / a.chunk;
-      const int64_t g = std::min<int64_t>((nch + CB_WARPS - 1) / CB_WARPS, grid);
-      k_cube<<<(unsigned)g, CB_WARPS * 32, smem, st>>>(a);
-      launches_add(1);
+    for (size_t pi = 0; pi < parts.size(); pi++) {
+      CUDA_TRY(cudaMemsetAsync(dwork.as<int>() + pi, 0, 4, st));
+      CubeArgs a = parts[pi];
+      a.nrows = c->rels[c->root].nrows;
+      a.work = dwork.as<int>() + pi;
+      if (a.nrows > 0) {
+        const int64_t nch = (a.nrows + a.chunk - 1) / a.chunk;
+        const int64_t g = std::min<int64_t>((nch + CB_WARPS - 1) / CB_WARPS, grid);
+        k_cube<<<(unsigned)g, CB_WARPS * 32, smem, st>>>(a);
+        launches_add(1);
+      }
     }
     CUDA_TRY(cudaGetLastError());
     for (auto& sp : sparse) CUDA_TRY(finish_sparse(c, sp, st));
@@ -488,7 +498,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   auto meas_slot = [&](int attr) -> int {
     for (size_t i = 0; i < meas.size(); i++)
       if (meas[i] == attr) return (int)i;
-    if (meas.size() == (size_t)CB_MEAS) return -1;
+    if (meas.size() == (size_t)CB_MAXM) return -1;
     meas.push_back(attr);
     return (int)meas.size() - 1;
   };
@@ -567,18 +577,22 @@ FastPaths* plan_cube(lmfao_ctx* c) {
     while (k < (int)qs.size() && qs[k].depth < d) k++;
     a.qbeg[d] = k;
   }
-  a.M = M;
+  a.M = std::min(M, CB_MEAS);
+  std::vector<const void*> mptr(M);
+  std::vector<int> mi32(M);
+  std::vector<const int32_t*> midx(M);
   for (int j = 0; j < M; j++) {
     const int o = c->owner[meas[j]];
     const Rel& O = c->rels[o];
     const Column& col = O.cols[O.find_attr(meas[j])];
-    a.meas[j] = col.buf.p;
-    a.meas_i32[j] = col.dt == LMFAO_INT32;
-    a.midx[j] = nullptr;
+    mptr[j] = col.buf.p;
+    mi32[j] = col.dt == LMFAO_INT32;
+    midx[j] = nullptr;
     if (o != c->root)  // a dimension measure: read through the dense foreign key
       for (size_t ch = 0; ch < R.children.size(); ch++)
-        if (R.children[ch] == o) a.midx[j] = R.fk_dense[ch].as<int32_t>();
+        if (R.children[ch] == o) midx[j] = R.fk_dense[ch].as<int32_t>();
   }
+  const int nparts = std::max(1, (M + CB_MEAS - 1) / CB_MEAS);
   a.nattr = (int)aslot.size();
   a.nq = (int)qs.size();
   a.chunk = 32 * 32;
@@ -588,7 +602,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   // cuboids with more cells than 2^25 (C5's {A,B,C}: 5·10^8) keep no dense table: their
   // run records are sorted and reduced after the scan (single GPU; LMFAO_CUBE_DENSE=1: off)
   const char* dn = std::getenv("LMFAO_CUBE_DENSE");
-  const bool allow_sparse = c->world == 1 && !(dn && dn[0] == '1');
+  const bool allow_sparse = c->world == 1 && nparts == 1 && !(dn && dn[0] == '1');
   const int64_t nrows = R.nrows, nchunks = (nrows + a.chunk - 1) / a.chunk;
   const char* smin = std::getenv("LMFAO_CUBE_SPARSE_CELLS");  // tests: lower the threshold
   const int64_t sparse_min = smin ? std::atoll(smin) : ((int64_t)1 << 25);
@@ -654,46 +668,89 @@ FastPaths* plan_cube(lmfao_ctx* c) {
         break;
       }
     }
-  // items: (cuboid, non-constant UDAF) pairs of the dense cuboids, by level, with their terms
-  std::vector<CubeItem> items;
-  std::vector<int8_t> tj;
-  std::vector<double> tc;
-  for (int d = 0; d <= CB_LEV; d++) {
-    a.ibeg[d] = (int)items.size();
-    for (int k = a.qbeg[d]; k < a.qbeg[d + 1]; k++) {
-      if (hq[k].sparse || hq[k].derived) continue;
-      for (size_t u = 0; u < qs[k].terms.size(); u++) {
-        const auto& t = qs[k].terms[u];
-        if (t.empty()) continue;  // constant UDAF: from the count at compaction
-        CubeItem e{(int16_t)(k - a.qbeg[d]), (int16_t)u, (int16_t)tj.size(), 0, t[0].first, 0, t[0].second};
-        for (auto& jt : t) {
-          tj.push_back((int8_t)jt.first);
-          tc.push_back(jt.second);
+  // items: (cuboid, non-constant UDAF) pairs of the dense cuboids, by level, with their terms;
+  // with more than CB_MEAS measures one scan per group of CB_MEAS, each with the terms of its
+  // measures (the count term and the counts with the first)
+  std::vector<std::vector<CubeItem>> pitems(nparts);
+  std::vector<std::vector<int8_t>> ptj(nparts);
+  std::vector<std::vector<double>> ptc(nparts);
+  for (int pt = 0; pt < nparts; pt++) {
+    CubeArgs ap = a;
+    const int m0 = pt * CB_MEAS, m1 = std::min(M, m0 + CB_MEAS);
+    ap.M = m1 - m0;
+    for (int j = m0; j < m1; j++) {
+      ap.meas[j - m0] = mptr[j];
+      ap.meas_i32[j - m0] = mi32[j];
+      ap.midx[j - m0] = midx[j];
+    }
+    ap.nocount = pt > 0;
+    auto& items = pitems[pt];
+    auto& tj = ptj[pt];
+    auto& tc = ptc[pt];
+    for (int d = 0; d <= CB_LEV; d++) {
+      ap.ibeg[d] = (int)items.size();
+      for (int k = a.qbeg[d]; k < a.qbeg[d + 1]; k++) {
+        if (hq[k].sparse || hq[k].derived) continue;
+        for (size_t u = 0; u < qs[k].terms.size(); u++) {
+          const auto& t = qs[k].terms[u];
+          if (t.empty()) continue;  // constant UDAF: from the count at compaction
+          std::vector<std::pair<int, double>> lt;  // this part's terms, local S indices
+          for (auto& jt : t) {
+            if (jt.first == 0 && pt == 0) lt.push_back(jt);
+            else if (jt.first >= 1 + m0 && jt.first < 1 + m1) lt.push_back({jt.first - m0, jt.second});
+          }
+          if (lt.empty()) continue;
+          CubeItem e{(int16_t)(k - a.qbeg[d]), (int16_t)u, (int16_t)tj.size(), 0, lt[0].first, 0, lt[0].second};
+          for (auto& jt : lt) {
+            tj.push_back((int8_t)jt.first);
+            tc.push_back(jt.second);
+          }
+          e.t1 = (int16_t)tj.size();
+          items.push_back(e);
         }
-        e.t1 = (int16_t)tj.size();
-        items.push_back(e);
       }
     }
+    ap.ibeg[CB_LEV + 1] = (int)items.size();
+    if ((int)tj.size() > CB_TERMS || (int)items.size() > CB_ITEMS) return nullptr;
+    ap.nterm = (int)tj.size();
+    ap.nitem = (int)items.size();
+    fc->parts.push_back(ap);
   }
-  a.ibeg[CB_LEV + 1] = (int)items.size();
-  if ((int)tj.size() > CB_TERMS || (int)items.size() > CB_ITEMS) return nullptr;
-  a.nterm = (int)tj.size();
-  a.nitem = (int)items.size();
+  a = fc->parts[0];
   fc->nq = a.nq;
   cudaStream_t st = c->stream;
   if (fc->dq.alloc(hq.size() * sizeof(Cuboid)) || fc->dcoef.alloc(std::max<size_t>(dense.size(), 1) * 8) ||
-      fc->ditems.alloc(std::max<size_t>(items.size(), 1) * sizeof(CubeItem)) || fc->dtj.alloc(std::max<size_t>(tj.size(), 1)) ||
-      fc->dtc.alloc(std::max<size_t>(tc.size(), 1) * 8) || fc->dwork.alloc(16))
+      fc->dwork.alloc(16 * 4))
     return nullptr;
+  if (nparts > 16) return nullptr;
   if (cudaMemcpyAsync(fc->dq.p, hq.data(), hq.size() * sizeof(Cuboid), cudaMemcpyHostToDevice, st)) return nullptr;
-  if (!items.empty() &&
-      cudaMemcpyAsync(fc->ditems.p, items.data(), items.size() * sizeof(CubeItem), cudaMemcpyHostToDevice, st))
-    return nullptr;
   if (!dense.empty() && cudaMemcpyAsync(fc->dcoef.p, dense.data(), dense.size() * 8, cudaMemcpyHostToDevice, st))
     return nullptr;
-  if (!tj.empty() && (cudaMemcpyAsync(fc->dtj.p, tj.data(), tj.size(), cudaMemcpyHostToDevice, st) ||
-                      cudaMemcpyAsync(fc->dtc.p, tc.data(), tc.size() * 8, cudaMemcpyHostToDevice, st)))
-    return nullptr;
+  fc->pbuf.resize(3 * nparts);
+  int max_item = 0, max_term = 0;
+  for (int pt = 0; pt < nparts; pt++) {
+    DevBuf& bi = fc->pbuf[3 * pt];
+    DevBuf& bj = fc->pbuf[3 * pt + 1];
+    DevBuf& bc = fc->pbuf[3 * pt + 2];
+    const auto& items = pitems[pt];
+    const auto& tj = ptj[pt];
+    const auto& tc = ptc[pt];
+    if (bi.alloc(std::max<size_t>(items.size(), 1) * sizeof(CubeItem)) || bj.alloc(std::max<size_t>(tj.size(), 1)) ||
+        bc.alloc(std::max<size_t>(tc.size(), 1) * 8))
+      return nullptr;
+    if (!items.empty() && cudaMemcpyAsync(bi.p, items.data(), items.size() * sizeof(CubeItem), cudaMemcpyHostToDevice, st))
+      return nullptr;
+    if (!tj.empty() && (cudaMemcpyAsync(bj.p, tj.data(), tj.size(), cudaMemcpyHostToDevice, st) ||
+                        cudaMemcpyAsync(bc.p, tc.data(), tc.size() * 8, cudaMemcpyHostToDevice, st)))
+      return nullptr;
+    CubeArgs& ap = fc->parts[pt];
+    ap.q = fc->dq.as<Cuboid>();
+    ap.items = bi.as<CubeItem>();
+    ap.tj = bj.as<int8_t>();
+    ap.tc = bc.as<double>();
+    max_item = std::max(max_item, ap.nitem);
+    max_term = std::max(max_term, ap.nterm);
+  }
   for (size_t y = 0; y < fc->sparse.size(); y++) {
     SparseOut& sp = fc->sparse[y];
     for (size_t x = 0; x < sp.der.size(); x++) sp.der[x].coef = fc->dcoef.as<double>() + der_coff[y][x];
@@ -702,12 +759,8 @@ FastPaths* plan_cube(lmfao_ctx* c) {
         cudaMemcpyAsync(sp.dder.p, sp.der.data(), sp.der.size() * sizeof(Rollup), cudaMemcpyHostToDevice, st))
       return nullptr;
   }
-  a.q = fc->dq.as<Cuboid>();
-  a.items = fc->ditems.as<CubeItem>();
-  a.tj = fc->dtj.as<int8_t>();
-  a.tc = fc->dtc.as<double>();
-  a.work = fc->dwork.as<int>();
-  fc->smem = CubeSmem(a.nq, a.nitem, a.nterm).total();
+  fc->ca = fc->parts[0];
+  fc->smem = CubeSmem(a.nq, max_item, max_term).total();
   if (fc->smem > 227 * 1024) return nullptr;
   if (fc->smem > 48 * 1024 &&
       cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc->smem))

@@ -151,3 +151,23 @@ def test_cube_dimension_measures():
     gpu, info = run_gpu(db, batch, info=True)
     assert info["fast_path"]["groups"]["kind"] == "cube", info["fast_path"]
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+def test_cube_many_measures():
+    """More measures than one scan carries (8): one scan per group of 8, the counts with the
+    first; UDAFs mixing measures of different groups are added in parts."""
+    db = cube_db(10, 15_000)
+    rng = np.random.default_rng(3)
+    F = db.rel("F")
+    extra = []
+    for j in range(9):
+        F.cols[f"z{j}"] = rng.standard_normal(F.nrows)
+        extra.append(f"z{j}")
+    ms = ["m1", "m2", "i1", "x1", "x2"] + extra  # 14 measures (x* on dimensions)
+    batch = [Query(["a1"], [S((1, m)) for m in ms]),
+             Query(["g", "a3"], [S((1, "z0"), (2, "z8"), (-1, None)), S((1, "x2"), (1, "m1"))]),
+             Query(["a2"], [S((3, "z5"))] + [S((1, None))])]
+    gpu, info = run_gpu(db, batch, info=True)
+    fp = info["fast_path"]["groups"]
+    assert fp["kind"] == "cube" and fp["scans"] == 2 and fp["measures"] == 14, fp
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
