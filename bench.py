@@ -243,6 +243,12 @@ def main():
     for _ in range(min(args.steps, 200)):
         eng.run(sptr)
     scan_ms, scan_n = eng.profile_read()
+    collective = None
+    if world > 1:  # the all-reduce of the partial results, timed on the run stream
+        ci = eng.plan_info()
+        if "collective_ms" in ci:
+            collective = {"ms_per_step": ci["collective_ms"], "bytes_per_step": ci["collective_bytes"],
+                          "backend": "nccl"}
     eng.profile(False)
     launches_per_run = info.get("launches_last_run", 0)
     if world > 1:
@@ -331,6 +337,7 @@ def main():
                          "peak_kind": peak_kind, "kernel": "root scan (c)+(d)",
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": scan_avg_s * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_run) * args.steps,
+            **({"collective": collective} if collective else {}),
             "clocks": clk.summary(), "load_s": load_s, "plan": info.get("fast_path"),
         }
         print(json.dumps(line), flush=True)

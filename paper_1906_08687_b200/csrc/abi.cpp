@@ -1065,6 +1065,12 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
   // combine across GPUs (domain parallelism)
   if (c->world > 1) {
     int e = 0;
+    cudaEvent_t ca = nullptr, cb = nullptr;
+    if (c->prof) {  // the collective's own time (lmfao_profile), reported by lmfao_plan_info
+      cudaEventCreate(&ca);
+      cudaEventCreate(&cb);
+      cudaEventRecord(ca, st);
+    }
     if (!c->scalar_queries.empty()) {
       e |= nccl_allreduce_f64(c->comm, c->scalar_out.as<double>(), c->scalar_prog.nout, st);
       e |= nccl_allreduce_u64(c->comm, c->scalar_count.as<unsigned long long>(), 1, st);
@@ -1072,6 +1078,10 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
     for (auto& gp : c->groups) {
       e |= nccl_allreduce_f64(c->comm, gp.table.as<double>(), gp.ncells * gp.nudaf, st);
       e |= nccl_allreduce_u64(c->comm, gp.counts.as<unsigned long long>(), gp.ncells, st);
+    }
+    if (ca) {
+      cudaEventRecord(cb, st);
+      c->coll_events.push_back({ca, cb});
     }
     if (e) return fail(c, LMFAO_ERR_NCCL, "NCCL all-reduce failed: %s", nccl_error(e));
   }
@@ -1253,7 +1263,13 @@ extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   }
   o << "], \"scalar_outputs\": " << c->scalar_prog.nout << ", \"group_queries\": " << c->groups.size();
   o << ", \"fast_path\": " << (c->fast ? c->fast->describe() : std::string("null"));
-  o << ", \"launches_last_run\": " << c->launches_last_run << "}";
+  o << ", \"launches_last_run\": " << c->launches_last_run;
+  if (c->coll_n > 0) {  // profiled multi-GPU runs: the all-reduce of the partial results
+    int64_t bytes = c->scalar_queries.empty() ? 0 : (int64_t)c->scalar_prog.nout * 8 + 8;
+    for (auto& gp : c->groups) bytes += gp.ncells * (gp.nudaf * 8 + 8);
+    o << ", \"collective_ms\": " << c->coll_ms / c->coll_n << ", \"collective_bytes\": " << bytes;
+  }
+  o << "}";
   std::string s = o.str();
   if ((int64_t)s.size() + 1 > cap) return fail(c, LMFAO_ERR_INVALID_ARG, "plan_info buffer too small");
   std::memcpy(out, s.c_str(), s.size() + 1);
@@ -1284,6 +1300,12 @@ extern "C" lmfao_status lmfao_profile(lmfao_ctx* c, int enable) {
     cudaEventDestroy(e.second);
   }
   c->prof_events.clear();
+  for (auto& e : c->coll_events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->coll_events.clear();
+  if (enable) c->coll_ms = 0.0, c->coll_n = 0;
   c->prof = enable != 0;
   return LMFAO_OK;
 }
@@ -1301,5 +1323,15 @@ extern "C" lmfao_status lmfao_profile_read(lmfao_ctx* c, double* total_ms, int64
   }
   *total_ms = t;
   *launches = (int64_t)c->prof_events.size();
+  for (auto& e : c->coll_events) {  // the collectives of the same runs
+    if (cudaEventSynchronize(e.second) != cudaSuccess) return fail(c, LMFAO_ERR_CUDA, "profile: event sync failed");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    c->coll_ms += ms;
+    c->coll_n++;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  c->coll_events.clear();
   return LMFAO_OK;
 }

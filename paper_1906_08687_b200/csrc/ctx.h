@@ -179,6 +179,9 @@ struct lmfao_ctx {
   // optional timer around the dominant root-scan kernel (lmfao_profile)
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> coll_events;  // multi-GPU all-reduce (profiled runs)
+  double coll_ms = 0.0;
+  int64_t coll_n = 0;
   std::string prof_kernel;
   // CUDA Graph of lmfao_run (see abi.cpp)
   cudaGraphExec_t graph_exec = nullptr;
