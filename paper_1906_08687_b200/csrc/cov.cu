@@ -13,10 +13,10 @@
 //    features per dimension level (C1, C2, C5's covariance), so the hot loop has
 //    no runtime shape logic (the v12 kernel spent 45 warp-instructions per row);
 //  * every warp runs its own TMA pipeline: `cp.async.bulk` of the fact columns and
-//    keys of a 32-row block into a CF-deep shared-memory ring, and one
-//    `cp.async.bulk.tensor.2d ... tile::gather4` per 4 rows for the view rows
-//    s_L[k_L] (96-byte rows, L2-resident), issued one block ahead — no operand
-//    prefetch lives in registers;
+//    keys of a 32-row block into a CF-deep shared-memory ring, and 16-byte
+//    `cp.async` gathers of the view rows s_L[k_L] (96-byte rows, L2-resident),
+//    issued one block ahead — no operand prefetch lives in registers (a TMA
+//    `tile::gather4` per 4 rows instead was measured at 0.60 vs 0.367 ms per scan);
 //  * level-A run records are stored unreduced (per lane) in shared memory and
 //    reduced four at a time straight into the DMMA A-operand layout;
 //  * level-B records go to a device list and are finished by a small kernel;
