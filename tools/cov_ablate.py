@@ -20,8 +20,9 @@ lmfao.load(e, w.db, w.batch)
 e.plan()
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
-for wv, mode in [(16, 0), (12, 0), (16, 1), (16, 2), (16, 8), (16, 11), (16, 16), (16, 17), (12, 17), (16, 32), (16, 43),
-                 (16, 64), (12, 64), (12, 0)]:
+modes = [(12, int(m)) for m in os.environ["MODES"].split(",")] if "MODES" in os.environ else \
+    [(12, 0), (12, 1), (12, 2), (12, 8), (12, 16), (12, 32), (12, 33), (12, 64), (12, 96), (12, 0)]
+for wv, mode in modes:
     os.environ["LMFAO_COV_ABLATE"] = str(mode)
     os.environ["LMFAO_COV_W"] = str(wv)
     for _ in range(3):

@@ -15,8 +15,11 @@ units = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", obj], cwd=d, capture_output=True)
 import glob
-cub = glob.glob(d + "/*.cubin")[0]
-sass = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout.split("\n")
+sass = []
+for cub in glob.glob(d + "/*.cubin"):  # the cubin holding the kernel (a .so carries one per source file)
+    sass = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout.split("\n")
+    if any(f".text.{kern}:" in l for l in sass):
+        break
 start = next(i for i, l in enumerate(sass) if f".text.{kern}:" in l)
 cur, a2l = None, {}
 for l in sass[start + 1:]:
