@@ -24,6 +24,13 @@ namespace {
 constexpr int CN_ATTR = 24;   // attributes with codes
 constexpr int CN_LEV = 8;     // root children
 constexpr unsigned CFULL = 0xffffffffu;
+#ifndef CNT_UNROLL_SMALL
+#define CNT_UNROLL_SMALL 4
+#endif
+#ifndef CNT_UNROLL_BIG
+#define CNT_UNROLL_BIG 1
+#endif
+constexpr int kUnrollSmall = CNT_UNROLL_SMALL, kUnrollBig = CNT_UNROLL_BIG;
 
 struct CntQuery {
   int8_t a, b;      // attribute slots (b = -1: one attribute)
@@ -32,7 +39,8 @@ struct CntQuery {
   int32_t soff;     // >= 0: counted in the CTA's shared table at this offset (small tables)
   int32_t ncell;
 };
-constexpr int CN_SMEM_CELLS = 12288;  // shared counters per CTA (48 KB) for the smallest tables
+constexpr int CN_SMEM_CELLS = 32768;  // shared counters per CTA (128 KB) for the smallest tables
+constexpr int CN_THREADS = 1024;      // k_cnt_rows block (one CTA per SM with the counters above)
 struct CntArgs {
   int64_t nrows;
   int nattr, nlev, nq;
@@ -42,19 +50,32 @@ struct CntArgs {
   unsigned* H[CN_LEV];           // rows per key of the children with dimension-only queries (null: none)
   const CntQuery* q;             // [nq] per-row queries
   int nsmall;                    // shared counters of the small tables
+  int nsq;                       // queries [0, nsq) count in shared memory
   unsigned long long* total;     // COUNT
 };
 
-// Per root row: the codes of every attribute, then each per-row query's cell.
-__global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArgs a) {
+// Per root row: the codes of every attribute, then each per-row query's cell.  Queries come
+// sorted: the nsmall_q shared-counter tables first, then the global ones, so both loops are
+// branch-free; a one-attribute query reads the all-zero code row (slot nattr) as its second code.
+__global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntArgs a) {
   extern __shared__ __align__(16) unsigned char cnsm[];
-  CntQuery* sq = reinterpret_cast<CntQuery*>(cnsm);
-  unsigned* stab = reinterpret_cast<unsigned*>(cnsm + ((a.nq * sizeof(CntQuery) + 15) / 16) * 16);
-  __shared__ int scode[8][CN_ATTR][32];  // this warp's codes (attribute x lane)
-  for (int i = threadIdx.x; i < a.nq; i += blockDim.x) sq[i] = a.q[i];
+  int4* sq = reinterpret_cast<int4*>(cnsm);  // {a, b, sa, soff}
+  unsigned long long** sp = reinterpret_cast<unsigned long long**>(cnsm + (size_t)a.nq * 16);
+  // per warp: codes [nattr + 1][32] (row nattr = 0), then dense keys [nlev][32]
+  const int wrows = a.nattr + 1 + a.nlev;
+  int* wsm = reinterpret_cast<int*>(cnsm + (size_t)a.nq * 24 + ((a.nq & 1) ? 8 : 0));
+  unsigned* stab = reinterpret_cast<unsigned*>(wsm + (blockDim.x >> 5) * 32 * wrows);
+  for (int i = threadIdx.x; i < a.nq; i += blockDim.x) {
+    const CntQuery q = a.q[i];
+    sq[i] = make_int4(q.a, q.b >= 0 ? q.b : a.nattr, q.sa, q.soff);
+    sp[i] = q.counts;
+  }
   for (int i = threadIdx.x; i < a.nsmall; i += blockDim.x) stab[i] = 0u;
-  __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* scode = wsm + wib * 32 * wrows + lane;  // scode[32 i] = code of attribute i
+  int* skey = scode + 32 * (a.nattr + 1);      // skey[32 l] = dense key at level l
+  scode[32 * a.nattr] = 0;
+  __syncthreads();
   unsigned long long tot = 0;
   for (int64_t base = (blockIdx.x * (int64_t)blockDim.x) & ~31ll; base < a.nrows;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -64,16 +85,17 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
     int key[CN_LEV];
 #pragma unroll
     for (int l = 0; l < CN_LEV; l++)
-      if (l < a.nlev) key[l] = v ? a.fk[l][row] : 0;
+      if (l < a.nlev) {
+        key[l] = v ? a.fk[l][row] : 0;
+        skey[32 * l] = key[l];
+      }
+    __syncwarp();
 #pragma unroll
     for (int i = 0; i < CN_ATTR; i++) {
       if (i >= a.nattr) break;
       const int l = a.lev[i];
-      int kk = 0;
-#pragma unroll
-      for (int j = 0; j < CN_LEV; j++)
-        if (j == l) kk = key[j];
-      scode[wib][i][lane] = v ? (l < 0 ? a.code[i][row] : a.code[i][kk]) : 0;
+      const int64_t idx = l < 0 ? row : (int64_t)skey[32 * l];
+      scode[32 * i] = v ? a.code[i][idx] : 0;
     }
     __syncwarp();
     // rows per key of the children that have dimension-only queries
@@ -85,16 +107,21 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
       const unsigned peers = __match_any_sync(CFULL, k);
       if (v && (__ffs(peers) - 1) == lane) atomicAdd(&a.H[l][k], (unsigned)__popc(peers));
     }
-    for (int qi = 0; qi < a.nq; qi++) {
-      const CntQuery q = sq[qi];
-      const int ca = scode[wib][q.a][lane], cb = q.b >= 0 ? scode[wib][q.b][lane] : 0;
-      if (q.soff >= 0) {  // a small table: the CTA's shared counters (native shared atomics)
-        if (v) atomicAdd(&stab[q.soff + ca * q.sa + cb], 1u);
-        continue;
-      }
-      const int cell = v ? ca * q.sa + cb : -1 - lane;
+    // small tables: the CTA's shared counters (native shared atomics)
+#pragma unroll kUnrollSmall
+    for (int qi = 0; qi < a.nsq; qi++) {
+      const int4 d = sq[qi];
+      const int ca = scode[32 * d.x], cb = scode[32 * d.y];
+      if (v) atomicAdd(&stab[d.w + ca * d.z + cb], 1u);
+    }
+    // the others: lanes holding the same cell merged, one global atomic per distinct cell
+#pragma unroll kUnrollBig
+    for (int qi = a.nsq; qi < a.nq; qi++) {
+      const int4 d = sq[qi];
+      const int ca = scode[32 * d.x], cb = scode[32 * d.y];
+      const int cell = v ? ca * d.z + cb : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, cell);
-      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&q.counts[cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
+      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&sp[qi][cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
     }
     __syncwarp();
   }
@@ -103,12 +130,12 @@ __global__ void __launch_bounds__(256) k_cnt_rows(const __grid_constant__ CntArg
   if (lane == 0 && a.total) atomicAdd(a.total, tot);
   if (a.nsmall == 0) return;
   __syncthreads();
-  for (int qi = 0; qi < a.nq; qi++) {  // the shared counters -> the global tables
-    const CntQuery q = sq[qi];
-    if (q.soff < 0) continue;
-    for (int c = threadIdx.x; c < q.ncell; c += blockDim.x) {
-      const unsigned n = stab[q.soff + c];
-      if (n) gred_add(&q.counts[c], (unsigned long long)n);
+  for (int qi = 0; qi < a.nsq; qi++) {  // the shared counters -> the global tables
+    const int4 d = sq[qi];
+    const int ncell = a.q[qi].ncell;
+    for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+      const unsigned n = stab[d.w + c];
+      if (n) gred_add(&sp[qi][c], (unsigned long long)n);
     }
   }
 }
@@ -152,7 +179,7 @@ struct FastCounts : FastPaths {
   DevBuf dq, ddq, Hbuf, scoef;
   int nscalar = 0;
   int64_t hwords = 0;
-  int nrowq = 0, ndimq = 0, grid = 148 * 8;
+  int nrowq = 0, ndimq = 0, grid = 148 * 8, threads = 256, cell_cap = 0;
   size_t smem = 0;
   bool scalar = false;
   std::string describe() const override {
@@ -179,7 +206,7 @@ int FastCounts::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar
   }
   scan_timer_begin(c, st);
   if (a.nrows > 0) {
-    k_cnt_rows<<<grid, 256, std::max<size_t>(smem, 16), st>>>(a);
+    k_cnt_rows<<<grid, threads, std::max<size_t>(smem, 16), st>>>(a);
     launches_add(1);
   }
   scan_timer_end(c, st);
@@ -277,9 +304,22 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   }
   a.nattr = (int)slot.size();
   a.nq = (int)rq.size();
+  {
+    // one CTA of CN_THREADS per SM: the per-warp code rows plus as many small tables as fit the
+    // shared budget (C4: 38 of its 60 per-row tables; 256 threads with 12288 cells: 30 tables,
+    // 6.39 ms -> 4.33 ms).  LMFAO_CNT_THREADS / LMFAO_CNT_SMEM_CELLS: A/B knobs.
+    const char* th = std::getenv("LMFAO_CNT_THREADS");
+    fc->threads = th ? std::max(32, std::min(1024, std::atoi(th) / 32 * 32)) : CN_THREADS;
+    int optin = 232448;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const int64_t avail = (int64_t)optin - 2048 - (int64_t)rq.size() * 24;
+    const int64_t rows = a.nattr + 1 + a.nlev;
+    while (fc->threads > 64 && fc->threads * 4 * rows > avail / 2) fc->threads /= 2;
+    fc->cell_cap = (int)std::max<int64_t>(0, (avail - fc->threads * 4 * rows) / 4);
+  }
   {  // the smallest per-row tables get shared counters (no warp matching, no global atomics per row)
     const char* sc = std::getenv("LMFAO_CNT_SMEM_CELLS");
-    const int budget = sc ? std::atoi(sc) : CN_SMEM_CELLS;
+    const int budget = std::min(sc ? std::atoi(sc) : CN_SMEM_CELLS, fc->cell_cap);
     std::vector<int> order(rq.size());
     for (size_t i = 0; i < rq.size(); i++) order[i] = (int)i;
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rq[x].ncell < rq[y].ncell; });
@@ -290,6 +330,10 @@ FastPaths* plan_counts(lmfao_ctx* c) {
         used += rq[i].ncell;
       }
     a.nsmall = used;
+    // shared-counter queries first (k_cnt_rows loops over the two kinds separately)
+    std::stable_partition(rq.begin(), rq.end(), [](const CntQuery& q) { return q.soff >= 0; });
+    a.nsq = 0;
+    for (auto& q : rq) a.nsq += q.soff >= 0 ? 1 : 0;
   }
   fc->nrowq = (int)rq.size();
   fc->ndimq = (int)dq.size();
@@ -337,7 +381,8 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   fc->da.nq = (int)dq.size();
   fc->da.q = fc->ddq.as<CntDimQuery>();
   if (cudaStreamSynchronize(st)) return nullptr;
-  fc->smem = ((rq.size() * sizeof(CntQuery) + 15) / 16) * 16 + (size_t)a.nsmall * 4;
+  fc->smem = rq.size() * 24 + ((rq.size() & 1) ? 8 : 0) + (size_t)fc->threads * 4 * (a.nattr + 1 + a.nlev) +
+             (size_t)a.nsmall * 4;
   // (static scode + dynamic above 48 KB needs the opt-in; the attribute is process-wide: keep the max)
   static int set_smem = 0;
   if ((int)fc->smem > set_smem) {
@@ -346,9 +391,10 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   }
   {
     int per_sm = 0, nsm = 148;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cnt_rows, 256, fc->smem) || per_sm < 1) per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cnt_rows, fc->threads, fc->smem) || per_sm < 1)
+      per_sm = 1;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-    fc->grid = nsm * std::min(per_sm, 8);
+    fc->grid = nsm * std::min(per_sm, 2048 / fc->threads);
   }
   return fc.release();
 }
