@@ -58,3 +58,32 @@ def test_counts_sharded(nparts):
         for kk, cc in zip(map(tuple, k.astype(np.int64)), c):
             tot[kk] = tot.get(kk, 0) + int(cc)
     assert tot == {tuple(kk): int(cc) for kk, cc in zip(ref[qi].keys, ref[qi].counts)}
+
+
+def _wide_star(n, ndims, attrs_per_rel, seed=5):
+    """A star with `ndims` primary-key leaves and `attrs_per_rel` Zipf categoricals in the root
+    and in every dimension (wider than C4: the per-warp code rows of k_cnt_rows no longer fit
+    beside 1024 threads, so the planner takes fewer threads and a smaller shared budget)."""
+    db = synth._snowflake(seed, n, tuple(20 + 37 * r for r in range(ndims)), (0,) * ndims, [], tag="W")
+    names = []
+    for ri, rel in enumerate(["F"] + [f"D{r}" for r in range(1, ndims + 1)]):
+        R = db.rel(rel)
+        for j in range(attrs_per_rel):
+            a = f"c{ri}_{j}"
+            R.cols[a] = synth.zipf_ranks(synth._rng(seed, rel, a), 3 + 11 * j + 5 * ri, 1.0, R.nrows).astype(np.int32)
+            names.append(a)
+    return db, names
+
+
+@pytest.mark.parametrize("cells", [None, "0", "700"])
+def test_counts_wide_batch_smem_budgets(monkeypatch, cells):
+    """24 attributes over 8 relations (the kernel's maxima): every pair, single and COUNT,
+    with the default shared budget (capped by the planner), none, and a small one."""
+    if cells is not None:
+        monkeypatch.setenv("LMFAO_CNT_SMEM_CELLS", cells)
+    db, names = _wide_star(9_001, 7, 3)
+    assert len(names) == 24
+    batch = synth.mi_batch(names)  # 276 pairs, 24 singles, COUNT
+    gpu, info = run_gpu(db, batch, info=True)
+    assert info["fast_path"]["kind"] == "counts", info
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
