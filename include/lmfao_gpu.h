@@ -198,7 +198,10 @@ LMFAO_API lmfao_status lmfao_result_device(lmfao_ctx* ctx, int32_t query_id, con
 
 /* Diagnostics: fills `out` (up to `cap` bytes) with a JSON object describing
  * the plan (kernel path per query group, view widths, run counts per level after
- * the last run, kernel launches per run). */
+ * the last run, kernel launches per run; with world > 1, after profiled runs
+ * (lmfao_profile + lmfao_profile_read): "collective_ms", the mean device time of
+ * a run's NCCL all-reduce of the partial results, and "collective_bytes", the
+ * bytes it reduces per rank). */
 LMFAO_API lmfao_status lmfao_plan_info(lmfao_ctx* ctx, char* out, int64_t cap);
 
 /* Measurement: when enabled, lmfao_run records CUDA events on its stream around
