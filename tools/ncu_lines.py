@@ -57,7 +57,7 @@ for l in sass:
         break
 src = open(src_file).read().split("\n") if src_file else []
 print(f"total {tot:.0f} warp-instr, {tot / units:.1f} per unit")
-for ln, n in sorted(agg.items(), key=lambda x: -x[1])[:35]:
+for ln, n in sorted(agg.items(), key=lambda x: -x[1])[:int(os.environ.get("TOP", "35"))]:
     s = src[ln - 1].strip()[:95] if ln and ln <= len(src) else "?"
     print(f"{n / units:7.1f}  stall {sm[ln]:6d}  L{ln}  {s}")
 print("top opcodes:", ", ".join(f"{o} {n / units:.1f}" for o, n in ops.most_common(12)))
