@@ -93,6 +93,9 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+__device__ __forceinline__ void cp16full(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -113,6 +116,7 @@ __device__ __forceinline__ double red4(double v) {
 struct LayoutArgs {
   const double* x[8];
   const int32_t* key[3];
+  int pad[3];  // key of rows >= N per level: the zero row appended to the level's view (0: no level)
   int nx, nlev;
   int64_t N, nblk;
   unsigned char* out;
@@ -131,8 +135,8 @@ __global__ void k_cov_layout(LayoutArgs a) {
       int2 v = make_int2(0, 0);
       const int64_t row = 32 * b + r;
       if (lv < a.nlev) {
-        if (row < a.N) v.x = a.key[lv][row];
-        if (row + 1 < a.N) v.y = a.key[lv][row + 1];
+        v.x = row < a.N ? a.key[lv][row] : a.pad[lv];
+        v.y = row + 1 < a.N ? a.key[lv][row + 1] : a.pad[lv];
       }
       reinterpret_cast<int2*>(a.out)[i] = v;
     }
@@ -258,15 +262,14 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   }
   auto issue_gather = [&](const Cur& c, int fslot, int gslot) {
     if (c.item < nitems && !(g.ablate & 1)) {
+      // every block is full: rows past N carry the zero row's key (no per-chunk bounds)
       const int* kls = reinterpret_cast<const int*>(wbase + fslot * SBLK + 2048);
-      const int left = c.rows - c.b * 32;
       const char* vl = reinterpret_cast<const char*>(g.VL);
       const uint32_t dst = sa(gbase + gslot * STG_G) + 16 * lane;
 #pragma unroll
       for (int i = 0; i < 6; i++) {
-        const bool v = ch_row[i] < left;
         const unsigned off = (unsigned)kls[ch_row[i]] * (unsigned)(GP * 8) + (unsigned)ch_off[i];
-        cp16(dst + 512 * i, vl + (v ? off : 0u), v ? 16u : 0u);
+        cp16full(dst + 512 * i, vl + off);
       }
     }
     cp_commit();
@@ -361,9 +364,10 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     const double* xs = reinterpret_cast<const double*>(st);
     const int* ks = reinterpret_cast<const int*>(st + 2048);
     const double* gs = reinterpret_cast<const double*>(gbase + (blk & 1) * STG_G);
-    const int rleft = cc.rows - cc.b * 32;
-    const int nv = rleft < 32 ? rleft : 32;
-    const bool vr = lane < nv;
+    // rows past N (the last block's tail) are padding in the scan layout: x = 0 and the keys of
+    // the zero rows appended to the views, in runs of their own — they add exact zeros
+    constexpr int nv = 32;
+    constexpr bool vr = true;
     const int kl = vr ? ks[lane] : -1;
     const int ka = vr ? (NS >= 1 ? ks[32 + lane] : 0) : -1;
     const int kb = vr ? (NS == 2 ? ks[64 + lane] : 0) : -1;
@@ -1073,7 +1077,9 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   for (int i = 0; i < 3; i++) {
     CovLevel& l = *lv[i];
     if (l.rel < 0) continue;
-    if (l.V.alloc((size_t)std::max<int64_t>(l.nk, 1) * GP * 8)) return nullptr;
+    // + one zero row (index nk): the key of the scan layout's padding rows
+    if (l.V.alloc((size_t)(l.nk + 1) * GP * 8)) return nullptr;
+    if (cudaMemsetAsync(l.V.p, 0, l.V.bytes, c->stream)) return nullptr;
     std::vector<const double*> cp;
     std::vector<const int32_t*> ip;
     std::map<int, const int32_t*> chain;  // relation -> row per dimension key (composed foreign keys)
@@ -1116,8 +1122,8 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   }
   const int64_t nkA = fc->NS >= 1 ? fc->A.nk : 0;
   fc->off_HA = 16;
-  fc->off_HL = (fc->off_HA + (size_t)nkA * 4 + 15) / 16 * 16;
-  fc->zbytes = fc->off_HL + (size_t)std::max<int64_t>(fc->L.nk, 1) * 4;
+  fc->off_HL = (fc->off_HA + (size_t)(nkA + 1) * 4 + 15) / 16 * 16;  // + the padding rows' key
+  fc->zbytes = fc->off_HL + (size_t)(fc->L.nk + 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
   tr.mark("terms + buffers", c->stream);
   fc->nblk = (R.nrows + 31) / 32;
@@ -1141,6 +1147,9 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     la.nlev = 1 + fc->NS;
     la.N = R.nrows;
     la.nblk = fc->nblk;
+    la.pad[0] = (int)fc->L.nk;
+    la.pad[1] = fc->NS >= 1 ? (int)fc->A.nk : 0;
+    la.pad[2] = fc->NS == 2 ? (int)fc->B.nk : 0;
     la.out = fc->scan.as<unsigned char>();
     if (fc->nblk > 0) {
       k_cov_layout<<<148 * 8, 256, 0, c->stream>>>(la);
