@@ -4,7 +4,7 @@
 // aggregate is an entry of G = Σ_f u(f) u(f)^T with u = [1, x, s_L, s_A, s_B]),
 // evaluated over the root sorted by its foreign keys in increasing domain size
 // with the multi-output trie registration of P:1020-1214:
-//   per row          x⊗x, x⊗s_L                (FP64 DMMA m8n8k4 on 4-row groups + 2 DFMA)
+//   per row          x⊗x, x⊗s_L                (FP64 DMMA m8n8k4 on 4-row groups)
 //   per level-A run  R_A⊗s_A, R_A = Σ_run [x, s_L, 1]  (4 runs per DMMA, "intermediate aggregates")
 //   per level-B run  R_B⊗s_B, R_B = Σ_{A-runs} [R_A, n·s_A]  (record list, finished off-scan)
 //   dimension side   Σ_k H_r[k] s_r(k) s_r(k)^T  ("each aggregate to its own root")
@@ -160,7 +160,7 @@ struct CovCfg {
 // NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L); W warps per CTA.
 //
 // Per 32-row block (lane = row for keys; DMMA layout lane = 4m + k for values):
-//  * x⊗x and x⊗s_L on the FP64 tensor pipe (DMMA m8n8k4 per 4-row group), x⊗s_L8/9 by DFMA;
+//  * x⊗x, x⊗s_L0..7 and x⊗[s_L8, s_L9, 1] (B = the t tile) as three DMMA m8n8k4 per 4-row group;
 //  * the open level-A run's sums of v = [x, s_L0..7, (s_L8, s_L9, 1)] are carried per lane (C,
 //    DADD) across blocks in which no run ends (62% of C2's blocks: Zipf-hot keys make long runs);
 //  * in a block where runs end, the run ("segment") sums come from DMMA against a 0/1
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   };
 
   // ---- accumulators
-  double aXX[2] = {0, 0}, aXL[2] = {0, 0}, a8 = 0, a9 = 0;
+  double aXX[2] = {0, 0}, aXL[2] = {0, 0}, aXT[2] = {0, 0};
   double aRA[3][2] = {{0, 0}, {0, 0}, {0, 0}}, r8[3] = {0, 0, 0}, r9[3] = {0, 0, 0};
   double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;
   double C0 = 0, C1 = 0, C2 = 0;  // this lane's rows of the open level-A run (since its last fold)
@@ -412,11 +412,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         const double* gr = gl + j * 4 * GP;
         const double sv = gr[m];
         const double tv = gr[tcol];
-        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        a8 = fma(xa, s89.x, a8);
-        a9 = fma(xa, s89.y, a9);
+        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
         C0 += xa;
         C1 += sv;
         C2 += tv;
@@ -479,11 +477,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         const double* gr = gl + j * 4 * GP;
         const double sv = gr[m];
         const double tv = gr[tcol];
-        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        a8 = fma(xa, s89.x, a8);
-        a9 = fma(xa, s89.y, a9);
+        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
         dmma(aRA[0], xa, sam[jj]);
         dmma(aRA[1], sv, sam[jj]);
         dmma(aRA[2], tv, sam[jj]);
@@ -593,11 +589,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
         const double* gr = gl + j * 4 * GP;
         const double sv = gr[m];
         const double tv = gr[tcol];
-        const double2 s89 = *reinterpret_cast<const double2*>(gr + 8);
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        a8 = fma(xa, s89.x, a8);
-        a9 = fma(xa, s89.y, a9);
+        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
         const int slast = __popc(mAx & ((2u << (4 * j + 3)) - 1u));
         if (slast - sb >= 8) {  // the group reaches past the window: flush it, restart at the group's first segment
           const int s4j = __popc(mAx & ((2u << (4 * j)) - 1u));
@@ -647,8 +641,6 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   asm volatile("cp.async.wait_all;" ::: "memory");
 
   // ---- this warp's partial -> partials[CTA * W + warp] (no CTA barrier: warps finish unevenly)
-  a8 = red4(a8);
-  a9 = red4(a9);
 #pragma unroll
   for (int t = 0; t < 3; t++) {
     r8[t] = red4(r8[t]);
@@ -660,8 +652,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   out[64 + m * 10 + 2 * k] = aXL[0];
   out[64 + m * 10 + 2 * k + 1] = aXL[1];
   if (k == 0) {
-    out[64 + m * 10 + 8] = a8;
-    out[64 + m * 10 + 9] = a9;
+    out[64 + m * 10 + 8] = aXT[0];
+    out[64 + m * 10 + 9] = aXT[1];
   }
 #pragma unroll
   for (int t = 0; t < 3; t++) {
