@@ -39,7 +39,10 @@ namespace {
 
 constexpr int IB = 16;       // 32-row blocks per dynamically scheduled item
 constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
-constexpr int HT = 1024;     // per-CTA H_L hash slots
+#ifndef COV_HT_BITS  // per-CTA H_L slots: only the Zipf-hottest keys need them, the rest go to global
+#define COV_HT_BITS 6   // REDs over many addresses (C2 scan: 2^12 0.355, 2^10 0.346, 2^8 0.343, 2^6 0.342,
+#endif                  // 2^5 0.345 ms)
+constexpr int HT = 1 << COV_HT_BITS;
 constexpr int SBLK = 256 * 8 + 3 * 32 * 4;     // scan-layout bytes per 32-row block: x in DMMA order + 3 key rows
 constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows per block (2 slots)
 constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][10]
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
   auto hl_add = [&](int key, unsigned len) {  // two probes, straight-line; full: global RED
-    unsigned h = ((unsigned)key * 2654435761u) >> (32 - 10);
+    unsigned h = ((unsigned)key * 2654435761u) >> (32 - COV_HT_BITS);
     int t = hkey[h];
     if (t == -1) {
       const int old = atomicCAS(&hkey[h], -1, key);
@@ -888,11 +891,7 @@ struct FastCov : FastPaths {
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
 };
 
-int cov_warps() {  // LMFAO_COV_W (diagnostics): 12 or 16 warps per CTA
-  const char* e = std::getenv("LMFAO_COV_W");
-  if (e) return std::atoi(e) == 12 ? 12 : 16;
-  return COV_W;
-}
+int cov_warps() { return COV_W; }  // (16 warps per CTA spilled at 128 registers; measured slower)
 
 template <int W>
 cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
@@ -911,7 +910,7 @@ cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
   return go(k_cov<2, W>);
 }
 cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
-  return cov_warps() == 12 ? launch_cov_w<12>(NS, g, grid, st) : launch_cov_w<16>(NS, g, grid, st);
+  return launch_cov_w<COV_W>(NS, g, grid, st);
 }
 
 }  // namespace

@@ -1,7 +1,7 @@
 """Diagnostics for the k_cov scan: time lmfao_run on C2 with parts of the kernel
 switched off (LMFAO_COV_ABLATE bitmask: 1 no gathers, 2 no record DMMA, 8 no H_L; results are
 invalid in those modes; 16 pipeline only, 32 all blocks on the fast path, 64 no wait for the
-gathers) and with 12 or 16 warps per CTA (LMFAO_COV_W; 12 is the default, 16 spills).
+gathers).  MODES=a,b,... picks the masks.
 usage: LMFAO_NO_GRAPH=1 python tools/cov_ablate.py [fact_rows]"""
 import json
 import os
@@ -24,7 +24,6 @@ modes = [(12, int(m)) for m in os.environ["MODES"].split(",")] if "MODES" in os.
     [(12, 0), (12, 1), (12, 2), (12, 8), (12, 16), (12, 32), (12, 33), (12, 64), (12, 96), (12, 0)]
 for wv, mode in modes:
     os.environ["LMFAO_COV_ABLATE"] = str(mode)
-    os.environ["LMFAO_COV_W"] = str(wv)
     for _ in range(3):
         e.run(st.cuda_stream)
     e.profile(True)
