@@ -31,7 +31,10 @@ constexpr unsigned RFULL = 0xffffffffu;
 constexpr int RT_MAX_FACT = 24;   // root attributes with histograms (predicates + small group-bys)
 constexpr int RT_MAX_DIM = 64;    // dimension attributes with histograms
 constexpr int RT_MAX_LEVELS = 8;  // root children with views
-constexpr int RT_HT = 1024;       // per-CTA hash slots per view level (Zipf-hot keys)
+#ifndef RT_HT_BITS  // C3: 2^10 slots 1.233 ms, 2^8 1.211, 2^6 1.50 (too many misses to global REDs)
+#define RT_HT_BITS 8
+#endif
+constexpr int RT_HT = 1 << RT_HT_BITS;  // per-CTA hash slots per view level (Zipf-hot keys)
 
 // A histogram over the root rows: predicate cells of a column, or the codes of a group-by.
 struct FactHist {
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
   }
   __syncthreads();
   auto add = [&](int l, int key, double v0, double v1, double v2) {
-    unsigned h = ((unsigned)key * 2654435761u) >> 22;  // 10 bits
+    unsigned h = ((unsigned)key * 2654435761u) >> (32 - RT_HT_BITS);
 #pragma unroll 1
     for (int probe = 0; probe < 2; probe++) {
       int* slot = hkey + l * RT_HT + h;
