@@ -37,7 +37,10 @@
 namespace lmfao {
 namespace {
 
-constexpr int IB = 16;       // 32-row blocks per dynamically scheduled item
+#ifndef COV_IB  // C2 scan by item size: 8 0.359, 16 0.342, 24 0.335, 32 0.335, 40 0.342, 48 0.358, 64 0.373 ms
+#define COV_IB 24
+#endif
+constexpr int IB = COV_IB;   // 32-row blocks per dynamically scheduled item
 constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
 #ifndef COV_HT_BITS  // per-CTA H_L slots: only the Zipf-hottest keys need them, the rest go to global
 #define COV_HT_BITS 6   // REDs over many addresses (C2 scan: 2^12 0.355, 2^10 0.346, 2^8 0.343, 2^6 0.342,
