@@ -41,6 +41,9 @@ namespace {
 #define COV_IB 24
 #endif
 constexpr int IB = COV_IB;   // 32-row blocks per dynamically scheduled item
+#ifndef COV_TAIL_PCT  // the last COV_TAIL_PCT % of the blocks go in 2-block items (C2: 4 % 0.348, 10 % 0.335, 20 % 0.348 ms)
+#define COV_TAIL_PCT 10
+#endif
 constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
 #ifndef COV_HT_BITS  // per-CTA H_L slots: only the Zipf-hottest keys need them, the rest go to global
 #define COV_HT_BITS 6   // REDs over many addresses (C2 scan: 2^12 0.355, 2^10 0.346, 2^8 0.343, 2^6 0.342,
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   // work items: blocks [0, NB) in items of IB blocks, the last ~10% in items of 2 blocks (a
   // short tail for the dynamic schedule)
   const int64_t N = g.nrows, NB = g.nblk;
-  const int nbig = (int)(NB * 9 / 10 / IB);
+  const int nbig = (int)(NB * (100 - COV_TAIL_PCT) / 100 / IB);
   const int nitems = nbig + (int)((NB - (int64_t)nbig * IB + 1) / 2);
   auto item_first = [&](int it) { return it < nbig ? (int64_t)it * IB : (int64_t)nbig * IB + 2 * (int64_t)(it - nbig); };
   auto item_blocks = [&](int it) {
@@ -1122,7 +1125,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   tr.mark("terms + buffers", c->stream);
   fc->nblk = (R.nrows + 31) / 32;
   // work items as k_cov defines them: IB-block items, then 2-block items for the last ~10 %
-  const int64_t nbig = fc->nblk * 9 / 10 / IB;
+  const int64_t nbig = fc->nblk * (100 - COV_TAIL_PCT) / 100 / IB;
   const int64_t nitems = nbig + (fc->nblk - nbig * IB + 1) / 2;
   // level-B records: one per (B run, item) pair <= B runs + items
   fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + nitems + 64, INT32_MAX / BRW);
