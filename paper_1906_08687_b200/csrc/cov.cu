@@ -40,7 +40,7 @@ namespace {
 #ifndef COV_IB  // C2 scan by item size: 8 0.359, 16 0.342, 24 0.335, 32 0.335, 40 0.342, 48 0.358, 64 0.373 ms
 #define COV_IB 24
 #endif
-constexpr int IB = COV_IB;   // 32-row blocks per dynamically scheduled item
+constexpr int IB = COV_IB;   // 32-row blocks per dynamically scheduled item (at most; fewer for small roots)
 #ifndef COV_TAIL_PCT  // the last COV_TAIL_PCT % of the blocks go in 2-block items (C2: 4 % 0.348, 10 % 0.335, 20 % 0.348 ms)
 #define COV_TAIL_PCT 10
 #endif
@@ -76,6 +76,7 @@ struct CovArgs {
                // 16 no compute at all (pipeline only), 32 every block on the fast path, 64 no wait for gathers
   int cold;    // blocks with at least this many level-A run starts (and no level-B start inside) take
                // the per-row level-A path; 0: never (LMFAO_COV_COLD)
+  int ib;      // blocks per work item before the 2-block tail: IB, or 2 for small roots (template IBK)
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -178,7 +179,7 @@ struct CovCfg {
 //    against the s_A rows (lane (m,k) holds segments 2k and 2k+1), DFMA for s_A8/9 and n·s_A,
 //    and H_A;
 //  * level-B records (run totals and Σ n·s_A) go to the device record list at B-run ends.
-template <int NS, int W>
+template <int NS, int W, int IBK>
 __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
   using Cfg = CovCfg<W>;
   constexpr int CF = Cfg::CF;
@@ -208,12 +209,13 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   // work items: blocks [0, NB) in items of IB blocks, the last ~10% in items of 2 blocks (a
   // short tail for the dynamic schedule)
   const int64_t N = g.nrows, NB = g.nblk;
-  const int nbig = (int)(NB * (100 - COV_TAIL_PCT) / 100 / IB);
-  const int nitems = nbig + (int)((NB - (int64_t)nbig * IB + 1) / 2);
-  auto item_first = [&](int it) { return it < nbig ? (int64_t)it * IB : (int64_t)nbig * IB + 2 * (int64_t)(it - nbig); };
+  constexpr int ib = IBK;
+  const int nbig = (int)(NB * (100 - COV_TAIL_PCT) / 100 / ib);
+  const int nitems = nbig + (int)((NB - (int64_t)nbig * ib + 1) / 2);
+  auto item_first = [&](int it) { return it < nbig ? (int64_t)it * ib : (int64_t)nbig * ib + 2 * (int64_t)(it - nbig); };
   auto item_blocks = [&](int it) {
     const int64_t f = item_first(it), r = NB - f;
-    const int64_t cap = it < nbig ? IB : 2;
+    const int64_t cap = it < nbig ? ib : 2;
     return (int)(r < cap ? r : cap);
   };
 
@@ -882,7 +884,7 @@ struct FastCov : FastPaths {
   DevBuf brec, partials, finp, src, toff, tidx, tcoef;
   DevBuf scan;  // scan layout of the root (k_cov_layout), built at plan time
   int64_t nblk = 0;
-  int bcap = 0, grid = 148, nout = 0;
+  int bcap = 0, grid = 148, nout = 0, ib = IB;
   bool only_scalar = true;
 
   std::string describe() const override {
@@ -890,7 +892,7 @@ struct FastCov : FastPaths {
     std::snprintf(b, sizeof b,
                   "{\"kind\": \"cov\", \"NS\": %d, \"nF\": %d, \"nL\": %zu, \"nA\": %zu, \"nB\": %zu, \"grid\": %d, "
                   "\"threads\": %d, \"stages\": %d, \"item\": %d}",
-                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, COV_W * 32, CovCfg<COV_W>::CF, 32 * IB);
+                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, COV_W * 32, CovCfg<COV_W>::CF, 32 * ib);
     return b;
   }
   bool skip_generic_views() const override { return only_scalar; }
@@ -899,7 +901,7 @@ struct FastCov : FastPaths {
 
 int cov_warps() { return COV_W; }  // (16 warps per CTA spilled at 128 registers; measured slower)
 
-template <int W>
+template <int W, int IBK>
 cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
   static bool attr[3] = {false, false, false};
   auto go = [&](auto kern) -> cudaError_t {
@@ -911,12 +913,12 @@ cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
     kern<<<grid, W * 32, smem, st>>>(g);
     return cudaGetLastError();
   };
-  if (NS == 0) return go(k_cov<0, W>);
-  if (NS == 1) return go(k_cov<1, W>);
-  return go(k_cov<2, W>);
+  if (NS == 0) return go(k_cov<0, W, IBK>);
+  if (NS == 1) return go(k_cov<1, W, IBK>);
+  return go(k_cov<2, W, IBK>);
 }
 cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
-  return launch_cov_w<COV_W>(NS, g, grid, st);
+  return g.ib == IB ? launch_cov_w<COV_W, IB>(NS, g, grid, st) : launch_cov_w<COV_W, 2>(NS, g, grid, st);
 }
 
 }  // namespace
@@ -960,6 +962,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   }
   g.brec = brec.as<double>();
   g.bcap = bcap;
+  g.ib = ib;
   g.partials = partials.as<double>();
   scan_timer_begin(c, st);
   cudaError_t e = launch_cov(NS, g, grid, st);
@@ -1124,9 +1127,12 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
   tr.mark("terms + buffers", c->stream);
   fc->nblk = (R.nrows + 31) / 32;
-  // work items as k_cov defines them: IB-block items, then 2-block items for the last ~10 %
-  const int64_t nbig = fc->nblk * (100 - COV_TAIL_PCT) / 100 / IB;
-  const int64_t nitems = nbig + (fc->nblk - nbig * IB + 1) / 2;
+  // work items as k_cov defines them: ib-block items, then 2-block items for the last ~10 %;
+  // ib = IB unless the root has fewer than 2 such items per warp; then 2 (C1, 625 blocks:
+  // 0.057 ms in 24-block items, 0.045 in 16, 0.030 in 2)
+  fc->ib = fc->nblk >= (int64_t)fc->grid * COV_W * 2 * IB ? IB : 2;
+  const int64_t nbig = fc->nblk * (100 - COV_TAIL_PCT) / 100 / fc->ib;
+  const int64_t nitems = nbig + (fc->nblk - nbig * fc->ib + 1) / 2;
   // level-B records: one per (B run, item) pair <= B runs + items
   fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + nitems + 64, INT32_MAX / BRW);
   if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
