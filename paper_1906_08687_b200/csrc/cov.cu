@@ -154,7 +154,7 @@ __global__ void k_cov_layout(LayoutArgs a) {
 }
 
 constexpr int COV_W = 12;     // warps per CTA of the scan (one CTA per SM; 168 registers with the per-row path)
-constexpr int COV_COLD = 2;  // level-A run starts from which a block takes the per-row path (measured 2..6 alike)
+constexpr int COV_COLD = 1;  // level-A run starts from which a block takes the per-row path (C2 scan: 1 0.333, 2 0.335, 3 0.338, 4 0.339, never 0.383 ms)
 
 template <int W>
 #ifndef COV_CF12  // 3: a smaller carve-out leaves 60 KB of L1 for the view-row gathers (0.359 -> 0.357 ms vs 4)
