@@ -28,9 +28,9 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile oracle.cpp with g++ (no FP contraction, so products round exactly
-    as written)."""
+    as written; OpenMP for the THREADS fact-row chunks)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-std=c++17", "-shared", "-fPIC",
+        subprocess.check_call(["g++", "-O2", "-ffp-contract=off", "-fopenmp", "-std=c++17", "-shared", "-fPIC",
                                "-o", _LIB, _SRC])
     return _LIB
 
@@ -59,7 +59,15 @@ class OracleResult:
     absmass: np.ndarray   # [n_groups, n_udafs] Σ|term| (tolerance fallback, R14)
 
 
-def _spec(db, batch, root_range=None):
+def host_cores() -> int:
+    """Threads the oracle may use on this host (its CPU affinity)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _spec(db, batch, root_range=None, threads=1, acc="longdouble"):
     lines, ptrs, keep = [], [], []
     for r in db.relations:
         lines.append(f"REL {r.name} {r.nrows} {len(r.cols)}")
@@ -75,6 +83,8 @@ def _spec(db, batch, root_range=None):
     lines.append(f"ROOT {db.root}")
     if root_range is not None:
         lines.append(f"RANGE {int(root_range[0])} {int(root_range[1])}")
+    lines.append(f"THREADS {int(threads)}")
+    lines.append("ACC " + {"longdouble": "LONGDOUBLE", "neumaier": "NEUMAIER"}[acc])
     for p, c in db.edges:
         lines.append(f"EDGE {p} {c}")
     for q in batch:
@@ -90,11 +100,16 @@ def _spec(db, batch, root_range=None):
     return "\n".join(lines) + "\n", ptrs, keep
 
 
-def evaluate(db, batch, root_range=None) -> list:
+def evaluate(db, batch, root_range=None, threads=1, acc="longdouble") -> list:
     """Evaluate every query of `batch` over the natural join of `db`.
-    root_range=(lo, hi) restricts the root relation to rows [lo, hi)."""
+    root_range=(lo, hi) restricts the root relation to rows [lo, hi).
+    threads: contiguous root-row chunks enumerated in parallel with private group
+    tables merged in chunk order (0 = every host core).  acc: "longdouble" (default)
+    or "neumaier" (compensated double)."""
     lib = _load()
-    spec, ptrs, keep = _spec(db, batch, root_range)
+    if threads == 0:
+        threads = host_cores()
+    spec, ptrs, keep = _spec(db, batch, root_range, threads, acc)
     arr = (ctypes.c_void_p * max(1, len(ptrs)))(*ptrs)
     err = ctypes.create_string_buffer(512)
     h = lib.oracle_eval(spec.encode(), arr, err, 512)

@@ -26,10 +26,23 @@
 // mantissa).  Counts (the hidden join multiplicity of a group) are uint64.  The
 // absolute mass A = Σ|term| is accumulated too (for the tolerance fallback).
 //
+// Accumulation modes ("long double (x87, 64-bit mantissa) or
+// Neumaier-compensated double"): the default is long double as above; `ACC NEUMAIER`
+// in the spec sums the terms of a tuple and the tuples of a group in double with
+// Neumaier's compensation instead (used only to bound the oracle's own rounding error,
+// tests/test_oracle_pins.py).
+//
+// Threads (SURVEY.md §8(d)(ii) "the same source built with OpenMP over fact-row chunks:
+// private accumulators, merged in thread order"): `THREADS T` splits the root rows into
+// T contiguous chunks, each enumerated by its own worker into private group tables;
+// the tables are then added in chunk order (deterministic).  T = 1 is the plain loop.
+//
 // Input: a line-oriented text spec (see oracle/__init__.py, which writes it)
 // plus one pointer per column (int32 or double arrays).
 //
-// Build: g++ -O2 -ffp-contract=off -shared -fPIC -o liboracle.so oracle.cpp
+// Build: g++ -O2 -ffp-contract=off -fopenmp -shared -fPIC -o liboracle.so oracle.cpp
+#include <omp.h>
+
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -89,7 +102,16 @@ struct Acc {
   uint64_t count = 0;
   std::vector<long double> sum;
   std::vector<long double> absmass;
+  std::vector<double> nsum, ncomp;  // ACC NEUMAIER: running double sum and its compensation
 };
+
+// Neumaier's compensated addition: s + c carries the exact sum's rounding residue
+inline void neumaier_add(double& s, double& c, double v) {
+  const double t = s + v;
+  if (std::fabs(s) >= std::fabs(v)) c += (s - t) + v;
+  else c += (v - t) + s;
+  s = t;
+}
 
 struct Result {
   int ngb = 0, nudaf = 0;
@@ -101,6 +123,8 @@ struct Oracle {
   std::vector<std::pair<std::string, std::string>> edges;  // parent, child
   std::string root;
   int64_t root_lo = 0, root_hi = -1;
+  int threads = 1;
+  bool neumaier = false;
   std::vector<QuerySpec> queries;
   std::vector<Result> results;
 
@@ -111,7 +135,11 @@ struct Oracle {
   // per position (non-root): multimap key -> rows
   std::vector<std::map<std::vector<int64_t>, std::vector<int64_t>>> index;
 
-  std::vector<int64_t> binding;  // row bound at each position
+  // one enumeration worker: its own tuple binding and private group tables
+  struct Worker {
+    std::vector<int64_t> binding;  // row bound at each position
+    std::vector<Result> results;
+  };
 
   // resolved queries
   struct RFactor { int kind; AttrRef ref; double param; };
@@ -125,16 +153,16 @@ struct Oracle {
     throw std::runtime_error("unknown relation " + n);
   }
 
-  double value(const AttrRef& r) const {
+  double value(const Worker& w, const AttrRef& r) const {
     const Relation& R = rels[order[r.pos]];
     const Column& c = R.cols[r.col];
-    int64_t row = binding[r.pos];
+    int64_t row = w.binding[r.pos];
     return c.is_int ? (double)c.ip[row] : c.dp[row];
   }
-  int64_t ivalue(const AttrRef& r) const {
+  int64_t ivalue(const Worker& w, const AttrRef& r) const {
     const Relation& R = rels[order[r.pos]];
     const Column& c = R.cols[r.col];
-    return (int64_t)c.ip[binding[r.pos]];
+    return (int64_t)c.ip[w.binding[r.pos]];
   }
 
   AttrRef resolve(const std::string& a) const {
@@ -248,9 +276,9 @@ struct Oracle {
     }
   }
 
-  double eval_factor(const RFactor& f) const {
+  double eval_factor(const Worker& w, const RFactor& f) const {
     if (f.kind == F_CONST) return f.param;
-    double x = value(f.ref);
+    double x = value(w, f.ref);
     switch (f.kind) {
       case F_IDENT: return x;
       case F_LT: return x < f.param ? 1.0 : 0.0;
@@ -268,60 +296,103 @@ struct Oracle {
     throw std::runtime_error("bad factor kind");
   }
 
-  // one joined tuple t is bound in `binding`
-  void emit() {
+  // one joined tuple t is bound in w.binding
+  void emit(Worker& w) const {
     for (size_t qi = 0; qi < rq.size(); qi++) {
       const RQuery& q = rq[qi];
       std::vector<int64_t> key;
       key.reserve(q.gb.size());
-      for (auto& g : q.gb) key.push_back(ivalue(g));
-      Acc& acc = results[qi].groups[key];
+      for (auto& g : q.gb) key.push_back(ivalue(w, g));
+      Acc& acc = w.results[qi].groups[key];
       if (acc.sum.empty()) {
         acc.sum.assign(q.udafs.size(), 0.0L);
         acc.absmass.assign(q.udafs.size(), 0.0L);
+        if (neumaier) {
+          acc.nsum.assign(q.udafs.size(), 0.0);
+          acc.ncomp.assign(q.udafs.size(), 0.0);
+        }
       }
       acc.count += 1;
       for (size_t j = 0; j < q.udafs.size(); j++) {
         long double s = 0.0L, a = 0.0L;
+        double ns = 0.0, nc = 0.0;
         for (auto& p : q.udafs[j]) {
           double v = p.coeff;
-          for (auto& f : p.f) v = v * eval_factor(f);
-          s += (long double)v;
+          for (auto& f : p.f) v = v * eval_factor(w, f);
+          if (neumaier) neumaier_add(ns, nc, v);
+          else s += (long double)v;
           a += (long double)std::fabs(v);
         }
-        acc.sum[j] += s;
+        if (neumaier) {
+          neumaier_add(acc.nsum[j], acc.ncomp[j], ns);
+          neumaier_add(acc.nsum[j], acc.ncomp[j], nc);
+        } else {
+          acc.sum[j] += s;
+        }
         acc.absmass[j] += a;
       }
     }
   }
 
-  void enumerate(size_t pos) {
+  void enumerate(Worker& w, size_t pos) const {
     if (pos == order.size()) {
-      emit();
+      emit(w);
       return;
     }
     int pp = parent_pos[pos];
     const Relation& P = rels[order[pp]];
     std::vector<int64_t> k;
-    for (auto& kc : keycols[pos]) k.push_back(P.cols[kc.second].ip[binding[pp]]);
+    for (auto& kc : keycols[pos]) k.push_back(P.cols[kc.second].ip[w.binding[pp]]);
     auto it = index[pos].find(k);
     if (it == index[pos].end()) return;  // dangling: the tuple vanishes
     for (int64_t row : it->second) {
-      binding[pos] = row;
-      enumerate(pos + 1);
+      w.binding[pos] = row;
+      enumerate(w, pos + 1);
     }
   }
 
   void run() {
     build_tree();
     resolve_queries();
-    binding.assign(order.size(), -1);
     const Relation& R = rels[order[0]];
     int64_t hi = root_hi < 0 ? R.nrows : std::min(root_hi, R.nrows);
-    for (int64_t row = root_lo; row < hi; row++) {
-      binding[0] = row;
-      enumerate(1);
+    const int64_t lo = std::min(root_lo, hi);
+    const int T = threads < 1 ? 1 : threads;
+    std::vector<Worker> ws(T);
+    for (auto& w : ws) {
+      w.binding.assign(order.size(), -1);
+      w.results = results;  // empty tables of the right shape
     }
+    // chunk t = root rows [lo + (hi-lo)·t/T, lo + (hi-lo)·(t+1)/T)
+#pragma omp parallel for num_threads(T) schedule(static, 1)
+    for (int t = 0; t < T; t++) {
+      Worker& w = ws[t];
+      const int64_t a = lo + (hi - lo) * t / T, b = lo + (hi - lo) * (t + 1) / T;
+      for (int64_t row = a; row < b; row++) {
+        w.binding[0] = row;
+        enumerate(w, 1);
+      }
+    }
+    // merge the private tables in chunk order
+    for (int t = 0; t < T; t++)
+      for (size_t qi = 0; qi < rq.size(); qi++)
+        for (auto& kv : ws[t].results[qi].groups) {
+          Acc& acc = results[qi].groups[kv.first];
+          const Acc& part = kv.second;
+          if (acc.sum.empty()) {
+            acc = part;
+            continue;
+          }
+          acc.count += part.count;
+          for (size_t j = 0; j < acc.sum.size(); j++) {
+            acc.sum[j] += part.sum[j];
+            acc.absmass[j] += part.absmass[j];
+            if (neumaier) {
+              neumaier_add(acc.nsum[j], acc.ncomp[j], part.nsum[j]);
+              neumaier_add(acc.nsum[j], acc.ncomp[j], part.ncomp[j]);
+            }
+          }
+        }
     // P:134-139 SQL GROUP BY: with no group-by attribute the single output row
     // exists even over an empty join (value 0, count 0; reading R1).
     for (size_t qi = 0; qi < rq.size(); qi++) {
@@ -329,6 +400,10 @@ struct Oracle {
         Acc& acc = results[qi].groups[{}];
         acc.sum.assign(rq[qi].udafs.size(), 0.0L);
         acc.absmass.assign(rq[qi].udafs.size(), 0.0L);
+        if (neumaier) {
+          acc.nsum.assign(rq[qi].udafs.size(), 0.0);
+          acc.ncomp.assign(rq[qi].udafs.size(), 0.0);
+        }
       }
     }
   }
@@ -360,6 +435,13 @@ void parse(Oracle& o, const char* spec, const void* const* colptrs) {
       in >> o.root;
     } else if (tok == "RANGE") {
       in >> o.root_lo >> o.root_hi;
+    } else if (tok == "THREADS") {
+      in >> o.threads;
+    } else if (tok == "ACC") {
+      std::string mode;
+      in >> mode;
+      if (mode == "NEUMAIER") o.neumaier = true;
+      else if (mode != "LONGDOUBLE") throw std::runtime_error("bad ACC mode " + mode);
     } else if (tok == "EDGE") {
       std::string p, c;
       in >> p >> c;
@@ -439,7 +521,7 @@ void oracle_fetch(void* h, int q, int64_t* keys, double* vals, uint64_t* counts,
   for (auto& kv : r.groups) {  // std::map: ascending lexicographic key order
     for (int i = 0; i < r.ngb; i++) keys[g * r.ngb + i] = kv.first[i];
     for (int j = 0; j < r.nudaf; j++) {
-      vals[g * r.nudaf + j] = (double)kv.second.sum[j];
+      vals[g * r.nudaf + j] = o->neumaier ? kv.second.nsum[j] + kv.second.ncomp[j] : (double)kv.second.sum[j];
       absmass[g * r.nudaf + j] = (double)kv.second.absmass[j];
     }
     counts[g] = kv.second.count;

@@ -419,3 +419,52 @@ def test_set_inclusion_factor_vs_pandas(seed):
     ref = _brute(db, batch)
     for r, (k, v, n) in zip(res, ref):
         assert np.allclose(r.vals, v, rtol=1e-12, atol=1e-9), (r.vals, v)
+
+
+@pytest.mark.parametrize("name", ["h1", "h2", "h3", "h4", "h5"])
+@pytest.mark.parametrize("threads,acc", [(3, "longdouble"), (1, "neumaier"), (4, "neumaier")])
+def test_hand_databases_threads_and_neumaier(name, threads, acc):
+    """The OpenMP fact-row chunks (private tables merged in chunk order) and the Neumaier
+    accumulation mode reproduce the literal hand values
+    (all dyadic: every mode must be exact)."""
+    g = json.load(open(os.path.join(GOLD, f"{name}.json")))
+    qs = g["queries"]
+    if qs == "same-as-h2":
+        qs = json.load(open(os.path.join(GOLD, "h2.json")))["queries"]
+    batch = [query(q["groupby"], q["udafs"]) for q in qs]
+    res = oracle.evaluate(_db(name), batch, threads=threads, acc=acc)
+    for q, r in zip(qs, res):
+        assert r.keys.tolist() == q["keys"] or (len(q["keys"]) == 0 and r.keys.shape[0] == 0)
+        assert r.counts.tolist() == q["counts"]
+        assert np.array_equal(r.vals, np.array(q["vals"], dtype=np.float64).reshape(r.vals.shape))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_threads_vs_pandas_materialisation(seed):
+    """Chunked enumeration (including chunks with no joined tuple and more threads than
+    root rows) against the brute-force pandas materialisation."""
+    db = synth.random_db(200 + seed, max_rows=40 if seed % 2 else 300)
+    batch = synth.random_batch(seed, db, n_queries=3)
+    ref = _brute(db, batch)
+    for t in (2, 7, 64):
+        for r, (k, v, n) in zip(oracle.evaluate(db, batch, threads=t), ref):
+            assert r.keys.tolist() == k.tolist()
+            assert r.counts.tolist() == [int(x) for x in n]
+            assert np.allclose(r.vals, v, rtol=1e-12, atol=1e-9)
+
+
+def test_oracle_self_bound_longdouble_vs_neumaier():
+    """SURVEY.md §8(c) "GPU acceptance": the oracle's own rounding error, bounded by running
+    it in its two accumulation modes (long double vs Neumaier-compensated double) on a
+    covariance and a cube batch: |ld - neumaier| <= 1e-13·A (A = Σ|term|) everywhere, far
+    inside the 1e-9 / 1e-12·A acceptance band the GPU is held to (reading R14)."""
+    w = synth.config5(fact_rows=60_000, dim_rows=(50, 300, 2_000, 10_000))
+    a = oracle.evaluate(w.db, w.batch, threads=0)
+    b = oracle.evaluate(w.db, w.batch, threads=0, acc="neumaier")
+    worst = 0.0
+    for ra, rb in zip(a, b):
+        assert np.array_equal(ra.keys, rb.keys) and np.array_equal(ra.counts, rb.counts)
+        d = np.abs(ra.vals - rb.vals)
+        assert (d <= 1e-13 * ra.absmass).all()
+        worst = max(worst, float(np.max(d / np.maximum(ra.absmass, 1e-300))))
+    assert worst < 1e-13
