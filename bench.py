@@ -1,7 +1,8 @@
 """bench.py — fact rows/s of the covariance batch (BASELINE.json configs[1]) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
-  (N > 1: launched by torch.distributed.run, one process per GPU, NCCL)
+  (N > 1: one process per GPU over NCCL — either launched by torch.distributed.run, or,
+  when WORLD_SIZE is unset, bench.py launches N ranks itself the same way)
 
 A step is one lmfao_run over the whole batch (view build (b), fused root scan
 (c)+(d), dimension-side finishing, NCCL all-reduce when N > 1) with the
@@ -128,18 +129,33 @@ def committed_traffic(config):
     return None
 
 
-def cpu_baseline(w, max_rows, seconds=20.0):
-    """The oracle as it stands, on the first `max_rows` fact rows (bounded sample)."""
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(w, max_rows, threads=0):
+    """The oracle as it stands (oracle/, OpenMP over contiguous fact-row chunks with private
+    accumulators merged in chunk order) on the first `max_rows` fact rows,
+    on every host core (threads=0)."""
     import oracle
     db = w.db
     F = db.rel(db.root)
     n = min(max_rows, F.nrows)
+    cores = oracle.host_cores() if threads == 0 else threads
     t0 = time.perf_counter()
-    oracle.evaluate(db, w.batch, root_range=(0, n))
+    oracle.evaluate(db, w.batch, root_range=(0, n), threads=cores)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {n} of {F.nrows} sorted-order-agnostic fact rows of {w.name} (all dims), "
-                      f"single-threaded, {dt:.1f} s"}
+    return {"value": n / dt, "unit": "rows/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "nproc": os.cpu_count(), "wall_s": round(dt, 3),
+            "sample": f"first {n} of {F.nrows} fact rows of {w.name} (all dims, whole batch), "
+                      f"{cores} OpenMP threads, {dt:.1f} s"}
 
 
 def run_reference(args, rank, world):
@@ -152,6 +168,7 @@ def run_reference(args, rank, world):
         b = cpu_baseline(w, rows)
         if i >= args.warmup:
             per_step.append(rows / b["value"])
+    cores = b["cores"]
     t = sum(per_step)
     value = rows * args.steps / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
@@ -159,8 +176,9 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.config, "fact_rows": rows,
                                            "sample": f"first {rows} fact rows"},
-            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {rows} fact rows of {args.config} per step"},
+            "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle",
+                             "cpu_model": b.get("cpu_model"),
+                             "sample": f"first {rows} fact rows of {args.config} per step, {cores} OpenMP threads"},
             "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -173,16 +191,28 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-rows", type=int, default=150_000)
-    ap.add_argument("--ref-rows", type=int, default=50_000)
+    ap.add_argument("--cpu-rows", type=int, default=4_000_000)
+    ap.add_argument("--ref-rows", type=int, default=400_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch the N ranks the way the driver does (torch.distributed.run)
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
 
     if args.impl == "reference":
         run_reference(args, rank, world)
@@ -212,9 +242,12 @@ def main():
     eng = new_engine()
     t_load = time.perf_counter()
     qids = lmfao.load(eng, w.db, w.batch)
+    torch.cuda.synchronize()
+    t_plan = time.perf_counter()
     eng.plan()
     torch.cuda.synchronize()
     load_s = time.perf_counter() - t_load
+    plan_s = time.perf_counter() - t_plan
     info = eng.plan_info()
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
@@ -338,7 +371,11 @@ def main():
                          "alg_bytes_per_launch": alg_bytes, "kernel_ms_avg": scan_avg_s * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches_per_run) * args.steps,
             **({"collective": collective} if collective else {}),
-            "clocks": clk.summary(), "load_s": load_s, "plan": info.get("fast_path"),
+            "clocks": clk.summary(), "load_s": load_s,
+            # plan time (not in value): the planner incl. the scan layout of the root (a second,
+            # re-laid-out copy of the fact: x in DMMA lane order + run-flagged keys, 76 B/row) and
+            # the static cost-balanced chunking
+            "plan_s": plan_s, "plan": info.get("fast_path"),
         }
         print(json.dumps(line), flush=True)
     eng.close()

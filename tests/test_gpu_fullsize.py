@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import synth
-from _parity import run_gpu
+from _parity import assert_parity, run_gpu
 from _udaf import float_close
 
 pytestmark = pytest.mark.gpu
@@ -31,9 +31,14 @@ def _check_sampled(w, qi, n, seed=0):
     return gpu
 
 
-def test_c2_full_sampled_outputs():
+def test_c2_full_all_780_outputs():
+    """BASELINE.json configs[1] at its full size, in the launch configuration bench.py times:
+    every one of the 780 aggregates against the oracle over the whole 10M-row join
+    (OpenMP chunks on the host cores; SURVEY.md §8(c) "GPU acceptance")."""
     w = synth.config2()
-    gpu = _check_sampled(w, 0, 24)
+    gpu = run_gpu(w.db, w.batch)
+    ref = oracle.evaluate(w.db, w.batch, threads=0)
+    assert_parity(gpu, ref, w.batch)
     assert int(gpu[0][2][0]) == 10_000_000
 
 
