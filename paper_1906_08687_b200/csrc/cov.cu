@@ -1,82 +1,100 @@
-// cov.cu — the covariance batch's fused root scan, B200 version 2 (k_cov).
+// cov.cu — the covariance batch's fused root scan, B200 version 3 (k_cov).
 //
 // Same mathematics as gram.cu (§3 "covariance matrix" P:397-402: every
 // aggregate is an entry of G = Σ_f u(f) u(f)^T with u = [1, x, s_L, s_A, s_B]),
 // evaluated over the root sorted by its foreign keys in increasing domain size
 // with the multi-output trie registration of P:1020-1214:
-//   per row          x⊗x, x⊗s_L                (FP64 DMMA m8n8k4 on 4-row groups)
-//   per level-A run  R_A⊗s_A, R_A = Σ_run [x, s_L, 1]  (4 runs per DMMA, "intermediate aggregates")
+//   per row          x⊗x, x⊗s_L                 (DMMA m8n8k4 for x⊗s_L0..7, DFMA for the rest)
+//   per level-A run  R_A⊗s_A, R_A = Σ_run [x, s_L, 1]   ("intermediate aggregates": run sums
+//                    carried per lane, one DMMA per tile per run) — or, in blocks where many
+//                    short runs end (the Zipf tail), the same sum row by row (linearity)
 //   per level-B run  R_B⊗s_B, R_B = Σ_{A-runs} [R_A, n·s_A]  (record list, finished off-scan)
 //   dimension side   Σ_k H_r[k] s_r(k) s_r(k)^T  ("each aggregate to its own root")
-// What changed against gram.cu, and why (all measured on B200):
-//  * the kernel is specialised at compile time for ≤ 8 fact features and ≤ 10
-//    features per dimension level (C1, C2, C5's covariance), so the hot loop has
-//    no runtime shape logic (the v12 kernel spent 45 warp-instructions per row);
-//  * every warp runs its own TMA pipeline: `cp.async.bulk` of the fact columns and
-//    keys of a 32-row block into a CF-deep shared-memory ring, and 16-byte
-//    `cp.async` gathers of the view rows s_L[k_L] (96-byte rows, L2-resident),
-//    issued one block ahead — no operand prefetch lives in registers (a TMA
-//    `tile::gather4` per 4 rows instead was measured at 0.60 vs 0.367 ms per scan);
-//  * level-A run records are stored unreduced (per lane) in shared memory and
-//    reduced four at a time straight into the DMMA A-operand layout;
-//  * level-B records go to a device list and are finished by a small kernel;
-//  * H_L (root rows per L key, for s_L⊗s_L) is counted in a per-CTA open-
-//    addressing table in shared memory (Zipf-hot keys would serialise global
-//    atomics), spilling to global atomics when a probe misses twice.
-// Runs split at block / item boundaries are exact (every update is linear in the
-// run sums), so any row order is correct; the sort only makes runs long.
+// Design on B200 (measurements in DESIGN.md §2):
+//  * the FP64 pipe (DMMA and DFMA share it: 18.5 T FMA/s) is the scarce unit, so products
+//    go to DMMA only where a tile is fully used (x⊗s_L0..7: 64 of 64 products); the
+//    symmetric x⊗x (36 of 64) and the thin x⊗[s_L8, s_L9] are DFMA, lane (m, k) forming
+//    x_m·x_{m+d} (d = 0..4) for its row — 30 % fewer FP64 pipe cycles per row;
+//  * run boundaries are structural (like the trie): the scan layout built at plan
+//    time carries a run-start flag in bit 31 of every dense key, so a block's boundary masks
+//    are one ballot per level;
+//  * work is static: each warp scans a contiguous chunk of 32-row blocks, chunks of equal
+//    estimated cost (plan time, from the flags), and writes its partial sums and its level-B
+//    records to fixed slots — the result is bit-identical from run to run;
+//  * each warp streams its chunk with `cp.async.bulk` (one 2432-byte block per copy into a
+//    3-deep shared ring) and gathers the view rows s_L[k_L] (96-byte rows, L2-resident) one
+//    block ahead with 16-byte `cp.async` (a TMA `tile::gather4` measured 0.60 vs 0.367 ms);
+//  * H_L (root rows per L key, for s_L⊗s_L) is counted in a per-CTA open-addressing table in
+//    shared memory (Zipf-hot keys would serialise global atomics), spilling to global REDs.
+// Runs split at block / chunk boundaries are exact (every update is linear in the run sums).
 #include <cuda.h>
 
 #include <cstdlib>
 #include <set>
 
 #include <functional>
+#include <type_traits>
 
 #include "ctx.h"
 
 namespace lmfao {
 namespace {
 
-#ifndef COV_IB  // C2 scan by item size: 8 0.359, 16 0.342, 24 0.335, 32 0.335, 40 0.342, 48 0.358, 64 0.373 ms
-#define COV_IB 24
-#endif
-constexpr int IB = COV_IB;   // 32-row blocks per dynamically scheduled item (at most; fewer for small roots)
-#ifndef COV_TAIL_PCT  // the last COV_TAIL_PCT % of the blocks go in 2-block items (C2: 4 % 0.348, 10 % 0.335, 20 % 0.348 ms)
-#define COV_TAIL_PCT 10
-#endif
-constexpr int GP = 12;       // doubles per view row (cols >= n are 0)
+constexpr int GP = 12;       // doubles per view row (cols >= n are 0; col 10 = 1.0)
 #ifndef COV_HT_BITS  // per-CTA H_L slots: only the Zipf-hottest keys need them, the rest go to global
 #define COV_HT_BITS 6   // REDs over many addresses (C2 scan: 2^12 0.355, 2^10 0.346, 2^8 0.343, 2^6 0.342,
-#endif                  // 2^5 0.345 ms)
+#endif                  // 2^5 0.345 ms, round 1)
 constexpr int HT = 1 << COV_HT_BITS;
 constexpr int SBLK = 256 * 8 + 3 * 32 * 4;     // scan-layout bytes per 32-row block: x in DMMA order + 3 key rows
 constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows per block (2 slots)
-constexpr int NPART = 384;   // per-CTA partial: XX[8][8] | XL[8][10] | RA[24][10]
+constexpr int NPART = 384;   // per-warp partial: XX[8][8] | XL[8][10] | RA[24][10]
 constexpr int BRW = 36;      // doubles per B record
 constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
 constexpr int FIN_BLOCKS = 296;
 constexpr int SUM_SPLIT = 8;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int KEYMASK = 0x7fffffff;  // dense key; bit 31 = a run starts at this row (at this level)
+#ifndef COV_W
+#define COV_W 12  // warps per CTA of the scan (one CTA per SM)
+#endif
+#ifndef COV_XX_DMMA  // 1: x⊗x and x⊗[s_L8, s_L9, 1] as two more DMMA per 4-row group; 0: 7 DFMA (x_m·x_{m+d})
+#define COV_XX_DMMA 1   // (C2 scan: DFMA 0.334, DMMA 0.296 ms with the same static split: issue-bound)
+#endif
+// Work split (plan time): one static chunk per warp over the first (100 - COV_TAIL) % of the
+// estimated cost, chunks of equal cost (a block with level-A run starts inside costs COV_COST_COLD,
+// others COST_FAST), then COV_TB-block items grabbed dynamically — the dynamic tail absorbs what
+// the cost model gets wrong, per-item partials keep the sums in a fixed order.
+constexpr int COST_FAST = 3;
+#ifndef COV_COST_COLD
+#define COV_COST_COLD 6  // (C2, static chunks only: 3 0.395, 4 0.358, 5 0.334, 6 0.296, 7 0.391 ms)
+#endif
+#ifndef COV_TB
+#define COV_TB 8
+#endif
+#ifndef COV_TAIL
+#define COV_TAIL 10
+#endif
 
 static_assert(SBLK % 128 == 0 && STG_G % 128 == 0, "TMA / cp.async alignment");
 
 struct CovArgs {
-  int64_t nrows, nblk;
+  int64_t nblk;
   const unsigned char* scan;  // [nblk][SBLK] scan layout of the root
-  const double* VL;           // [nkL x GP]
-  const double* VA;           // [nkA x GP] (a zero row if absent)
+  const double* VL;           // [nkL + 1 x GP]
+  const double* VA;           // [nkA + 1 x GP] (a zero row if absent)
   unsigned* HL;
   unsigned* HA;
-  double* brec;
-  int* bcount;
-  int bcap;
-  double* partials;  // [grid * W][NPART] per-warp partials
-  int* work;
-  int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 2 no record DMMA, 8 no H_L,
-               // 16 no compute at all (pipeline only), 32 every block on the fast path, 64 no wait for gathers
-  int cold;    // blocks with at least this many level-A run starts (and no level-B start inside) take
-               // the per-row level-A path; 0: never (LMFAO_COV_COLD)
-  int ib;      // blocks per work item before the 2-block tail: IB, or 2 for small roots (template IBK)
+  double* brec;               // level-B records, [rec_base[NW]][BRW]
+  const int* item;            // [nitems + 1] first block of each work item (plan time)
+  int nitems;
+  int nstatic;                // items [0, nstatic): warp gw's first item is item gw (cost-balanced
+                              // static chunks); the rest are grabbed dynamically
+  int* work;                  // item counter (dynamic schedule), cleared every run
+  const int* rec_base;        // [nitems + 1] first level-B record slot of each item
+  double* partials;           // [nitems][NPART] per-item partials (summed in item order: deterministic)
+  int ablate;  // diagnostics only (LMFAO_COV_ABLATE, results invalid): 1 no gathers, 8 no H_L,
+               // 16 no compute at all (pipeline only), 32 every block on the fast path
+  int cold_all;  // LMFAO_COV_COLD_ALL=1 (tests): every block on the per-row level-A path (exact)
 };
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -99,10 +117,6 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                "l"(src), "r"(bytes), "r"(sa(b))
                : "memory");
 }
-// 16-byte L1-allocating async copy; src_bytes = 0 writes zeros (ragged tail rows)
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
 __device__ __forceinline__ void cp16full(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -118,10 +132,15 @@ __device__ __forceinline__ double red4(double v) {
   v += __shfl_xor_sync(FULL, v, 2);
   return v;
 }
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
-// Scan layout of the root (built once at plan time, like the sort at prepare):
-// per 32-row block b, x in the DMMA lane order [group j][lane 4m+k] = x_m[32b+4j+k]
-// (0 for m >= nx or rows >= N), then the dense keys [level][32] of L, A, B.  One
+// Scan layout of the root (built once at plan time, like the sort at prepare): per
+// 32-row block b, x in the DMMA lane order [group j][lane 4m+k] = x_m[32b+4j+k] (0 for
+// m >= nx or rows >= N), then the dense keys [level][32] of L, A, B.  Bit 31 of a key is
+// the run-start flag of its level in the sorted root: a B run starts where the B key
+// changes, an A run where the A or B key changes, an L run where any of them changes
+// (so A runs nest in B runs and L runs in A runs), and every level starts at row 0 and at
+// row N (the padding rows past N carry the key of a zero row appended to each view).  One
 // contiguous bulk copy per block; conflict-free shared reads.
 struct LayoutArgs {
   const double* x[8];
@@ -142,48 +161,64 @@ __global__ void k_cov_layout(LayoutArgs a) {
       reinterpret_cast<double*>(a.out)[i] = (m < a.nx && row < a.N) ? a.x[m][row] : 0.0;
     } else {
       const int e = 2 * (o - 256), lv = e >> 5, r = e & 31;
-      int2 v = make_int2(0, 0);
-      const int64_t row = 32 * b + r;
+      int v[2] = {0, 0};
       if (lv < a.nlev) {
-        v.x = row < a.N ? a.key[lv][row] : a.pad[lv];
-        v.y = row + 1 < a.N ? a.key[lv][row + 1] : a.pad[lv];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t row = 32 * b + r + h;
+          if (row < a.N) {
+            bool start = row == 0;
+            for (int l = lv; l < a.nlev && !start; l++) start = a.key[l][row] != a.key[l][row - 1];
+            v[h] = a.key[lv][row] | (start ? (int)0x80000000u : 0);
+          } else {
+            v[h] = a.pad[lv] | (row == a.N ? (int)0x80000000u : 0);
+          }
+        }
       }
-      reinterpret_cast<int2*>(a.out)[i] = v;
+      reinterpret_cast<int2*>(a.out)[i] = make_int2(v[0], v[1]);
     }
   }
 }
 
-constexpr int COV_W = 12;     // warps per CTA of the scan (one CTA per SM; 168 registers with the per-row path)
-constexpr int COV_COLD = 1;  // level-A run starts from which a block takes the per-row path (C2 scan: 1 0.333, 2 0.335, 3 0.338, 4 0.339, never 0.383 ms)
+// Plan time, per block (one warp per block): bits 0..5 the number of level-B run starts in it, bit
+// 6 its row 0 starts a B run, bit 7 level-A runs start inside it (the per-row path).
+__global__ void k_cov_bstats(const unsigned char* __restrict__ scan, int64_t nblk, int NS, uint32_t* __restrict__ st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t b = w0; b < nblk; b += nw) {
+    const int* ks = reinterpret_cast<const int*>(scan + b * SBLK + 2048);
+    const unsigned mA = NS >= 1 ? __ballot_sync(FULL, ks[32 + lane] < 0) : 0u;
+    const unsigned mB = NS == 2 ? __ballot_sync(FULL, ks[64 + lane] < 0) : 0u;
+    if (lane == 0) st[b] = (uint32_t)__popc(mB) | ((mB & 1u) << 6) | ((mA & ~1u) ? 128u : 0u);
+  }
+}
 
 template <int W>
-#ifndef COV_CF12  // 3: a smaller carve-out leaves 60 KB of L1 for the view-row gathers (0.359 -> 0.357 ms vs 4)
-#define COV_CF12 3
-#endif
 struct CovCfg {
-  static constexpr int CF = W >= 16 ? 3 : (W >= 12 ? COV_CF12 : 7);  // fact-block ring slots per warp
-  static constexpr int WB = CF * SBLK + 2 * STG_G + 512;       // + barriers, item ring, segment table
-  static constexpr int SMEM = 128 + HT * 8 + W * WB;  // [CTA counters | H_L table | warps]
+  static constexpr int CF = 3;                           // fact-block ring slots per warp
+  static constexpr int WB = CF * SBLK + 2 * STG_G + 128;  // + barriers
+  static constexpr int SMEM = 128 + HT * 8 + W * WB;      // [CTA counters | H_L table | warps]
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 // NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L); W warps per CTA.
 //
-// Per 32-row block (lane = row for keys; DMMA layout lane = 4m + k for values):
-//  * x⊗x, x⊗s_L0..7 and x⊗[s_L8, s_L9, 1] (B = the t tile) as three DMMA m8n8k4 per 4-row group;
-//  * the open level-A run's sums of v = [x, s_L0..7, (s_L8, s_L9, 1)] are carried per lane (C,
-//    DADD) across blocks in which no run ends (62% of C2's blocks: Zipf-hot keys make long runs);
-//  * in a block where runs end, the run ("segment") sums come from DMMA against a 0/1
-//    segment-indicator operand, D_t[f][s] += Σ_k v_t[f](row k) [seg(row k) = s], in windows of 8
-//    segments; each window's records (partial runs are exact by linearity) are two DMMA passes
-//    against the s_A rows (lane (m,k) holds segments 2k and 2k+1), DFMA for s_A8/9 and n·s_A,
-//    and H_A;
-//  * level-B records (run totals and Σ n·s_A) go to the device record list at B-run ends.
-template <int NS, int W, int IBK>
+// Per 32-row block, lane (m, k) = (lane / 4, lane % 4) holds, for DMMA group j (rows 4j..4j+3),
+// feature m of row 4j + k.  Paths by the block's level-A / level-B run starts (flags):
+//  * fast (no A run starts inside): per-row products; v = [x, s_L0..7, (s_L8, s_L9, 1)] is
+//    summed per lane into the open A run's carry C; when the run ends (at a block end) the
+//    carry times the run's s_A row is one DMMA per tile (the DMMA's k = 4 sums the lanes'
+//    rows) plus DFMA for s_A8/9;
+//  * cold (A run starts inside, no B start): every row's v times its own s_A row (the same
+//    sum by linearity: Σ_run (Σ_rows v) ⊗ s_A = Σ_rows v ⊗ s_A(row)), no segments;
+//  * slow (B run starts inside; rare): the cold product once per B segment, masked to its rows.
+template <int NS, int W>
 __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
   using Cfg = CovCfg<W>;
   constexpr int CF = Cfg::CF;
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * W + wib;
   extern __shared__ __align__(1024) unsigned char sm[];
   int* cta_done = reinterpret_cast<int*>(sm);
   int* hkey = reinterpret_cast<int*>(sm + 128);
@@ -191,9 +226,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   unsigned char* wbase = sm + 128 + HT * 8 + wib * Cfg::WB;
   unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
   uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
-  int* ring = reinterpret_cast<int*>(bar_f + 8);  // 8 grabbed item ids
-  int* segst = ring + 8;                          // [34] segment start rows of the current block
-  int* segkey = segst + 40;                       // [33] their A keys
+  int* ring = reinterpret_cast<int*>(bar_f + 4);  // [8] item ids grabbed by this warp, in order
 
   for (int i = threadIdx.x; i < HT; i += blockDim.x) {
     hkey[i] = -1;
@@ -206,60 +239,26 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   }
   __syncthreads();
 
-  // work items: blocks [0, NB) in items of IB blocks, the last ~10% in items of 2 blocks (a
-  // short tail for the dynamic schedule)
-  const int64_t N = g.nrows, NB = g.nblk;
-  constexpr int ib = IBK;
-  const int nbig = (int)(NB * (100 - COV_TAIL_PCT) / 100 / ib);
-  const int nitems = nbig + (int)((NB - (int64_t)nbig * ib + 1) / 2);
-  auto item_first = [&](int it) { return it < nbig ? (int64_t)it * ib : (int64_t)nbig * ib + 2 * (int64_t)(it - nbig); };
-  auto item_blocks = [&](int it) {
-    const int64_t f = item_first(it), r = NB - f;
-    const int64_t cap = it < nbig ? ib : 2;
-    return (int)(r < cap ? r : cap);
-  };
-
-  // cursors over this warp's block sequence (items grabbed dynamically, in order)
+  // ---- schedule: item gw (a static chunk), then items grabbed dynamically; this warp's items in
+  // grab order in a ring.  Every item has at least CF blocks (plan), so the fact look-ahead (CF
+  // blocks) is never more than one item ahead of the block being processed.
+  const int nitems = g.nitems;
   int nring = 0;
-  int next_item = lane == 0 ? atomicAdd(g.work, 1) : 0;  // one grab in flight ahead of use
-  auto grab = [&]() {
-    const int it = __shfl_sync(FULL, next_item, 0);
-    if (lane == 0) {
-      ring[nring & 7] = it;
-      next_item = atomicAdd(g.work, 1);
-    }
+  auto grab = [&]() {  // the static chunk first; dynamic items when needed (no grab ahead: a
+                       // prefetched tail item would wait behind the warp's current one)
+    int it = 0;
+    if (lane == 0) it = nring == 0 && gw < g.nstatic ? gw : g.nstatic + atomicAdd(g.work, 1);
+    it = __shfl_sync(FULL, it, 0);
+    if (lane == 0) ring[nring & 7] = it;
     nring++;
     __syncwarp();
   };
-  struct Cur {
-    int slot, b, item, nb;  // nb: blocks of the item
-    int64_t gb0;            // its first block
-    int rows;               // rows of the item
-  };
-  auto set_item = [&](Cur& c) {
-    c.item = ring[c.slot & 7];
-    if (c.item < nitems) {
-      c.gb0 = item_first(c.item);
-      c.nb = item_blocks(c.item);
-      const int64_t r = N - c.gb0 * 32;
-      c.rows = (int)(r < 32 * c.nb ? r : 32 * c.nb);
-    }
-  };
-  auto advance = [&](Cur& c, bool may_grab) {
-    if (c.item >= nitems) return;
-    if (++c.b < c.nb) return;
-    c.b = 0;
-    c.slot++;
-    if (may_grab && c.slot >= nring) grab();
-    set_item(c);
-  };
-  auto gblock = [&](const Cur& c) { return c.gb0 + c.b; };
-  auto issue_fact = [&](const Cur& c, int stage) {
-    __syncwarp();
-    if (c.item >= nitems) return;
+  int rec = 0;  // the current item's next level-B record slot
+
+  auto issue_fact = [&](int64_t b, int stage) {
     if (lane == 0) {  // the slot was only read (generic proxy) since its last fill: no proxy fence needed
       mbar_expect(&bar_f[stage], SBLK);
-      bulk_load(wbase + stage * SBLK, g.scan + gblock(c) * SBLK, SBLK, &bar_f[stage]);
+      bulk_load(wbase + stage * SBLK, g.scan + b * SBLK, SBLK, &bar_f[stage]);
     }
   };
   // view rows s_L[k_L(row)] of a landed fact block -> gather slot [32 rows x 96 B]; 16-byte
@@ -271,29 +270,29 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     ch_row[i] = c / 6;
     ch_off[i] = (c % 6) * 16;
   }
-  auto issue_gather = [&](const Cur& c, int fslot, int gslot) {
-    if (c.item < nitems && !(g.ablate & 1)) {
-      // every block is full: rows past N carry the zero row's key (no per-chunk bounds)
-      const int* kls = reinterpret_cast<const int*>(wbase + fslot * SBLK + 2048);
+  auto issue_gather = [&](int stage, int gslot) {
+    if (!(g.ablate & 1)) {
+      const int kl = reinterpret_cast<const int*>(wbase + stage * SBLK + 2048)[lane] & KEYMASK;
       const char* vl = reinterpret_cast<const char*>(g.VL);
       const uint32_t dst = sa(gbase + gslot * STG_G) + 16 * lane;
 #pragma unroll
       for (int i = 0; i < 6; i++) {
-        const unsigned off = (unsigned)kls[ch_row[i]] * (unsigned)(GP * 8) + (unsigned)ch_off[i];
-        cp16full(dst + 512 * i, vl + off);
+        const unsigned key = (unsigned)__shfl_sync(FULL, kl, ch_row[i]);
+        cp16full(dst + 512 * i, vl + key * (unsigned)(GP * 8) + (unsigned)ch_off[i]);
       }
     }
-    cp_commit();
   };
 
-  // ---- accumulators
-  double aXX[2] = {0, 0}, aXL[2] = {0, 0}, aXT[2] = {0, 0};
-  double aRA[3][2] = {{0, 0}, {0, 0}, {0, 0}}, r8[3] = {0, 0, 0}, r9[3] = {0, 0, 0};
-  double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;
-  double C0 = 0, C1 = 0, C2 = 0;  // this lane's rows of the open level-A run (since its last fold)
-  bool openB = false;
-  int curB = 0;
-  int prevL = -1, prevA = -1, prevB = -1;
+  // ---- accumulators (lane (m, k): feature m, rows 4j + k)
+  double aXL[2] = {0, 0};                              // x ⊗ s_L0..7 (DMMA)
+  double aXX[2] = {0, 0}, aXT[2] = {0, 0};             // COV_XX_DMMA: x ⊗ x, x ⊗ [s_L8, s_L9, 1] (DMMA)
+  double xx0 = 0, xx1 = 0, xx2 = 0, xx3 = 0, xx4 = 0;  // x_m · x_{(m+d)%8}, d = 0..4
+  double x8 = 0, x9 = 0;                               // x_m · s_L8, x_m · s_L9
+  double C0 = 0, C1 = 0, C2 = 0;                       // open A run: Σ x_m, Σ s_L_m, Σ t_m (this lane's rows)
+  double aRA0[2] = {0, 0}, aRA1[2] = {0, 0}, aRA2[2] = {0, 0};  // [x | s_L0..7 | t] ⊗ s_A0..7 (DMMA)
+  double r8x = 0, r9x = 0, r8l = 0, r9l = 0, r8t = 0, r9t = 0;   // ... ⊗ s_A8, s_A9
+  double tA8 = 0, tA9 = 0;                                       // s_L8 · s_A_m, s_L9 · s_A_m (per row)
+  double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;  // open B run: Σ v, Σ s_A
   const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
   auto hl_add = [&](int key, unsigned len) {  // two probes, straight-line; full: global RED
@@ -314,367 +313,343 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     if (t == key) atomicAdd(&hcnt[h], len);
     else gred_add(&g.HL[key], len);
   };
-  auto push_B = [&](int keyB) {
+  auto push_B = [&](int keyB) {  // the open B run's record -> this warp's next slot
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
-    int slot = 0;
-    if (lane == 0) slot = atomicAdd(g.bcount, 1);
-    slot = __shfl_sync(FULL, slot, 0);
-    if (slot < g.bcap) {
-      double* rec = g.brec + (size_t)slot * BRW;
-      if (k == 0) {
-        rec[m] = v0;
-        rec[8 + m] = v1;
-        rec[16 + m] = v2;
-        rec[24 + m] = v3;
-      }
-      if (lane == 0) {
-        rec[32] = v4;
-        rec[33] = v5;
-        rec[34] = (double)keyB;
-        rec[35] = 0.0;
-      }
+    double* r = g.brec + (size_t)rec * BRW;
+    if (k == 0) {
+      r[m] = v0;
+      r[8 + m] = v1;
+      r[16 + m] = v2;
+      r[24 + m] = v3;
     }
+    if (lane == 0) {
+      r[32] = v4;
+      r[33] = v5;
+      r[34] = (double)keyB;
+      r[35] = 0.0;
+    }
+    rec++;
     SB0 = SB1 = SB2 = SBn = SBn8 = SBn9 = 0.0;
   };
+  // the carried rows of the A run with key keyA: C ⊗ s_A(keyA), into the B sums, H_A
+  auto flush_carry = [&](int keyA) {
+    const double* ar = g.VA + (size_t)(unsigned)keyA * GP;
+    const double b0v = ar[m];
+    const double2 b89 = ld2(ar + 8);
+    dmma(aRA0, C0, b0v);
+    dmma(aRA1, C1, b0v);
+    dmma(aRA2, C2, b0v);
+    r8x = fma(C0, b89.x, r8x);
+    r9x = fma(C0, b89.y, r9x);
+    r8l = fma(C1, b89.x, r8l);
+    r9l = fma(C1, b89.y, r9l);
+    r8t = fma(C2, b89.x, r8t);
+    r9t = fma(C2, b89.y, r9t);
+    SB0 += C0;
+    SB1 += C1;
+    SB2 += C2;
+    const double n = __shfl_sync(FULL, red4(C2), 8);  // the carried rows: the "1" row (m == 2) of t
+    const double nq = k == 0 ? n : 0.0;               // once per quad (SBn* are summed over k at push_B)
+    SBn = fma(nq, b0v, SBn);
+    SBn8 = fma(nq, b89.x, SBn8);
+    SBn9 = fma(nq, b89.y, SBn9);
+    if (NS >= 1 && lane == 0 && n > 0.0) gred_add(&g.HA[keyA], (unsigned)n);
+    C0 = C1 = C2 = 0.0;
+  };
 
-  // ---- pipeline prologue: fact blocks 0..CF-1 in flight, gathers of block 0
-  grab();
-  Cur cc{0, 0, 0, 0, 0, 0};
-  set_item(cc);
-  Cur cf = cc;
-  for (int s = 0; s < CF; s++) {
-    issue_fact(cf, s);
-    advance(cf, true);
-  }
-  if (cc.item < nitems) mbar_wait(&bar_f[0], 0);
-  issue_gather(cc, 0, 0);
-  int blk = 0, fs = 0, fph = 0;  // fs = blk % CF, fph = (blk / CF) & 1
-  while (cc.item < nitems) {
-    Cur cn = cc;
-    advance(cn, false);
-    const bool has_next = cn.item < nitems;
-    const int fs1 = fs + 1 == CF ? 0 : fs + 1;
-    {  // gathers of the next block (its keys have landed)
-      const int fph1 = fs + 1 == CF ? fph ^ 1 : fph;
-      if (has_next) mbar_wait(&bar_f[fs1], (uint32_t)fph1);
-      issue_gather(cn, fs1, (blk + 1) & 1);
+  // the item's partial (every entry written; both triangles of XX); then the accumulators restart
+  auto store_partial = [&](int item) {
+    const double q0 = red4(xx0), q1 = red4(xx1), q2 = red4(xx2), q3 = red4(xx3), q4 = red4(xx4);
+    const double q8 = red4(x8), q9 = red4(x9);
+    const double s8x = red4(r8x), s9x = red4(r9x), s8l = red4(r8l), s9l = red4(r9l), s8t = red4(r8t), s9t = red4(r9t);
+    const double a8 = red4(tA8), a9 = red4(tA9);
+    double* out = g.partials + (size_t)item * NPART;
+    if (k == 0) {
+      const double qd[5] = {q0, q1, q2, q3, q4};
+  #pragma unroll
+      for (int d = 0; d < 5; d++) {
+        const int n = (m + d) & 7;
+        if (d < 4 || m < 4) {
+          out[m * 8 + n] = qd[d];
+          out[n * 8 + m] = qd[d];
+        }
+      }
+      out[64 + m * 10 + 8] = q8;
+      out[64 + m * 10 + 9] = q9;
+      out[144 + m * 10 + 8] = s8x;
+      out[144 + m * 10 + 9] = s9x;
+      out[144 + (8 + m) * 10 + 8] = s8l;
+      out[144 + (8 + m) * 10 + 9] = s9l;
+      out[144 + (16 + m) * 10 + 8] = s8t;
+      out[144 + (16 + m) * 10 + 9] = s9t;
     }
-    if (cc.b == 0) prevL = prevA = prevB = -1;  // a new item: row 0 starts runs at every level
-    if (!(g.ablate & 64)) cp_wait1();
+    out[64 + m * 10 + 2 * k] = aXL[0];
+    out[64 + m * 10 + 2 * k + 1] = aXL[1];
+    if (COV_XX_DMMA) {
+      __syncwarp();
+      out[m * 8 + 2 * k] = aXX[0];
+      out[m * 8 + 2 * k + 1] = aXX[1];
+      if (k == 0) {
+        out[64 + m * 10 + 8] = aXT[0];
+        out[64 + m * 10 + 9] = aXT[1];
+      }
+    }
+    // t rows 0, 1 (s_L8, s_L9) of RA: the carried DMMA part plus the per-row DFMA part (on lane m
+    // for column m: moved to the fragment's owner, lane (row, column / 2))
+    const double a8c0 = __shfl_sync(FULL, a8, 8 * k), a8c1 = __shfl_sync(FULL, a8, 8 * k + 4);
+    const double a9c0 = __shfl_sync(FULL, a9, 8 * k), a9c1 = __shfl_sync(FULL, a9, 8 * k + 4);
+    const double e0 = m == 0 ? a8c0 : (m == 1 ? a9c0 : 0.0), e1 = m == 0 ? a8c1 : (m == 1 ? a9c1 : 0.0);
+    out[144 + m * 10 + 2 * k] = aRA0[0];
+    out[144 + m * 10 + 2 * k + 1] = aRA0[1];
+    out[144 + (8 + m) * 10 + 2 * k] = aRA1[0];
+    out[144 + (8 + m) * 10 + 2 * k + 1] = aRA1[1];
+    out[144 + (16 + m) * 10 + 2 * k] = aRA2[0] + e0;
+    out[144 + (16 + m) * 10 + 2 * k + 1] = aRA2[1] + e1;
+    aXL[0] = aXL[1] = aXX[0] = aXX[1] = aXT[0] = aXT[1] = 0.0;
+    xx0 = xx1 = xx2 = xx3 = xx4 = x8 = x9 = 0.0;
+    aRA0[0] = aRA0[1] = aRA1[0] = aRA1[1] = aRA2[0] = aRA2[1] = 0.0;
+    r8x = r9x = r8l = r9l = r8t = r9t = tA8 = tA9 = 0.0;
     __syncwarp();
-    if (g.ablate & 16) {
-      issue_fact(cf, fs);
-      advance(cf, true);
-      cc = cn;
-      blk++;
-      fs = fs1;
-      if (fs == 0) fph ^= 1;
-      continue;
+  };
+
+  // ---- pipeline prologue: the first CF blocks of the sequence in flight, gathers of block 0
+  grab();
+  int pslot = 0, pitem = ring[0];  // the block being processed: pb of item pitem = [pbeg, pend)
+  int pb = 0, pbeg = 0, pend = 0;
+  if (pitem < nitems) {
+    pb = pbeg = g.item[pitem];
+    pend = g.item[pitem + 1];
+    rec = g.rec_base[pitem];
+  }
+  int fslot = 0, fitem = pitem, fb = pb, fend = pend;  // the next block to load (look-ahead)
+  auto f_advance = [&]() {
+    if (fitem >= nitems) return;
+    if (++fb < fend) return;
+    if (++fslot >= nring) grab();
+    fitem = ring[fslot & 7];
+    if (fitem < nitems) {
+      fb = g.item[fitem];
+      fend = g.item[fitem + 1];
     }
+  };
+  for (int s = 0; s < CF; s++) {
+    if (fitem < nitems) issue_fact(fb, s);
+    f_advance();
+  }
+  if (pitem < nitems) {
+    mbar_wait(&bar_f[0], 0);
+    issue_gather(0, 0);
+  }
+  cp_commit();
+  int fs = 0;  // position in the sequence % CF
+  uint32_t fph = 0;
+  bool carried = false;  // C holds rows of the open level-A run
+  for (int i = 0; pitem < nitems; i++) {
+    const bool next_in_item = pb + 1 < pend;
+    const int nitem = next_in_item ? pitem : ring[(pslot + 1) & 7];  // (grabbed by the look-ahead)
+    const bool has_next = nitem < nitems;
+    const bool first_of_item = pb == pbeg;
+    const int fs1 = fs + 1 == CF ? 0 : fs + 1;
+    const uint32_t fph1 = fs + 1 == CF ? fph ^ 1u : fph;
+    if (has_next) {  // gathers of the next block (its keys land first)
+      mbar_wait(&bar_f[fs1], fph1);
+      issue_gather(fs1, (i + 1) & 1);
+    }
+    cp_commit();
+    cp_wait1();  // this block's gathers have landed
+    __syncwarp();
     const unsigned char* st = wbase + fs * SBLK;
     const double* xs = reinterpret_cast<const double*>(st);
     const int* ks = reinterpret_cast<const int*>(st + 2048);
-    const double* gs = reinterpret_cast<const double*>(gbase + (blk & 1) * STG_G);
-    // rows past N (the last block's tail) are padding in the scan layout: x = 0 and the keys of
-    // the zero rows appended to the views, in runs of their own — they add exact zeros
-    constexpr int nv = 32;
-    constexpr bool vr = true;
-    const int kl = vr ? ks[lane] : -1;
-    const int ka = vr ? (NS >= 1 ? ks[32 + lane] : 0) : -1;
-    const int kb = vr ? (NS == 2 ? ks[64 + lane] : 0) : -1;
-    int pl = __shfl_up_sync(FULL, kl, 1), pa = __shfl_up_sync(FULL, ka, 1), pb = __shfl_up_sync(FULL, kb, 1);
-    if (lane == 0) {
-      pl = prevL;
-      pa = prevA;
-      pb = prevB;
-    }
-    const bool dB = vr && kb != pb;
-    const bool dA = vr && (dB || ka != pa);
-    const bool lead = vr && (dA || kl != pl || lane == 0);
-    const unsigned mB = __ballot_sync(FULL, dB), mA = __ballot_sync(FULL, dA), mLd = __ballot_sync(FULL, lead);
-    prevL = __shfl_sync(FULL, kl, nv - 1);
-    prevA = __shfl_sync(FULL, ka, nv - 1);
-    prevB = __shfl_sync(FULL, kb, nv - 1);
-    // does the run open at this block's end end here? (the next block is another item, or
-    // its row 0 has other A / B keys)
-    bool endA = true, endB = true;
-    if (has_next && cn.b != 0) {
-      const int* kn = reinterpret_cast<const int*>(wbase + fs1 * SBLK + 2048);
-      const int na = NS >= 1 ? kn[32] : 0, nb2 = NS == 2 ? kn[64] : 0;
-      endB = nb2 != prevB;
-      endA = endB || na != prevA;
-    }
-    if (lead && !(g.ablate & 8)) {
-      const unsigned above = mLd & ~((2u << lane) - 1u);
-      const int end = above ? __ffs(above) - 1 : nv;
-      hl_add(kl, (unsigned)(end - lane));
-    }
-    if (mB & 1u) {  // a level-B run starts at row 0
-      openB = true;
-      curB = __shfl_sync(FULL, kb, 0);
-    }
-    const unsigned mAx = mA & ~1u;  // run starts inside the block (row 0 always opens segment 0)
-    const double* gl = gs + k * GP;
-    if ((mAx == 0 && !endA) || (g.ablate & 32)) {
-      // fast path: the open run continues through the block
-#pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const double xa = xs[32 * j + lane];
+    const double* gs = reinterpret_cast<const double*>(gbase + (i & 1) * STG_G);
+    if (!(g.ablate & 16)) {
+      const int klr = ks[lane];
+      const int kar = NS >= 1 ? ks[32 + lane] : 0;
+      const int kbr = NS == 2 ? ks[64 + lane] : 0;
+      const int kl = klr & KEYMASK, ka = kar & KEYMASK, kb = kbr & KEYMASK;
+      const unsigned first = first_of_item ? 1u : 0u;  // an item's first row starts runs at every level
+      const unsigned mL = __ballot_sync(FULL, klr < 0) | first;
+      const unsigned mA = (NS >= 1 ? __ballot_sync(FULL, kar < 0) : 0u) | first;
+      const unsigned mB = (NS == 2 ? __ballot_sync(FULL, kbr < 0) : 0u) | first;
+      // does the run open at this block's end end here? (item end, or the next block's row 0
+      // starts a run at that level)
+      bool endA = true, endB = true;
+      if (next_in_item) {
+        const int* kn = reinterpret_cast<const int*>(wbase + fs1 * SBLK + 2048);
+        endB = NS == 2 ? kn[64] < 0 : false;
+        endA = NS >= 1 ? kn[32] < 0 : false;
+      }
+      if (!(g.ablate & 8) && (((mL >> lane) & 1u) || lane == 0)) {  // H_L: each L run's rows in the block
+        const unsigned above = mL & ~((2u << lane) - 1u);
+        hl_add(kl, (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
+      }
+      const double* gl = gs + k * GP;
+      // per-row products of group j; returns the lane's operands for the run-level work
+      auto rowpart = [&](int j, double& xa, double& sv, double2& s89, double& tv) {
+        xa = xs[32 * j + lane];
         const double* gr = gl + j * 4 * GP;
-        const double sv = gr[m];
-        const double tv = gr[tcol];
-        dmma(aXX, xa, xa);
-        dmma(aXL, xa, sv);
-        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
-        C0 += xa;
-        C1 += sv;
-        C2 += tv;
-      }
-    } else if (NS >= 1 && g.cold > 0 && __popc(mAx) >= g.cold && !(mB & ~1u)) {
-      // cold block (many short level-A runs, no level-B run starting inside): instead of run
-      // ("segment") sums times the run's s_A row, every row's v = [x, s_L, (s_L8, s_L9, 1)]
-      // times its own s_A row — the same sum by linearity, Σ_run (Σ_rows v) ⊗ s_A =
-      // Σ_rows v ⊗ s_A(row) — without segment windows, records or their s_A loads.
-      const int* kas = ks + 32;
-      double nc = 0.0;
-      if (!(mA & 1u)) {  // row 0 continues the run open at the previous block's end: its rows from
-                         // earlier blocks (carried in C) with the run's s_A row (row 0's key)
-        const int key0 = __shfl_sync(FULL, ka, 0);
-        const double* ar = g.VA + (size_t)(unsigned)key0 * GP;
-        const double b0 = ar[m];
-        const double2 b89 = *reinterpret_cast<const double2*>(ar + 8);
-        dmma(aRA[0], C0, b0);
-        dmma(aRA[1], C1, b0);
-        dmma(aRA[2], C2, b0);
-        r8[0] = fma(C0, b89.x, r8[0]);
-        r9[0] = fma(C0, b89.y, r9[0]);
-        r8[1] = fma(C1, b89.x, r8[1]);
-        r9[1] = fma(C1, b89.y, r9[1]);
-        r8[2] = fma(C2, b89.x, r8[2]);
-        r9[2] = fma(C2, b89.y, r9[2]);
-        SB0 += C0;
-        SB1 += C1;
-        SB2 += C2;
-        // carried rows: their count is the constant row (m == 2) of the t tile
-        nc = __shfl_sync(FULL, red4(C2), 8);
-        const double nq = k == 0 ? nc : 0.0;  // once per quad (SBn* are summed over k at push_B)
-        SBn = fma(nq, b0, SBn);
-        SBn8 = fma(nq, b89.x, SBn8);
-        SBn9 = fma(nq, b89.y, SBn9);
-        C0 = C1 = C2 = 0.0;
-      }
-      // H_A: each run's rows in this block (and the carried rows for row 0's run)
-      if (vr && (dA || lane == 0) && !(g.ablate & 2)) {
-        const unsigned above = mA & ~((2u << lane) - 1u);
-        const int end = above ? __ffs(above) - 1 : nv;
-        gred_add(&g.HA[ka], (unsigned)(end - lane) + (lane == 0 ? (unsigned)nc : 0u));
-      }
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        double sam[4], s8[4], s9[4];  // the s_A rows of this lane's next 4 rows, loads in flight together
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const int r = 4 * (4 * h + jj) + k;
-          const double* ar = g.VA + (size_t)(unsigned)(r < nv ? kas[r] : 0) * GP;
-          const double2 a89 = *reinterpret_cast<const double2*>(ar + 8);
-          sam[jj] = r < nv ? ar[m] : 0.0;
-          s8[jj] = r < nv ? a89.x : 0.0;
-          s9[jj] = r < nv ? a89.y : 0.0;
+        sv = gr[m];
+        tv = gr[tcol];
+        if (COV_XX_DMMA) {
+          dmma(aXX, xa, xa);
+          dmma(aXL, xa, sv);
+          dmma(aXT, xa, tv);
+          s89 = make_double2(0.0, 0.0);
+          return;
         }
-#pragma unroll
-      for (int jj = 0; jj < 4; jj++) {
-        const int j = 4 * h + jj;
-        const double xa = xs[32 * j + lane];
-        const double* gr = gl + j * 4 * GP;
-        const double sv = gr[m];
-        const double tv = gr[tcol];
-        dmma(aXX, xa, xa);
+        s89 = ld2(gr + 8);
+        const double xd1 = xs[32 * j + ((lane + 4) & 31)];
+        const double xd2 = xs[32 * j + ((lane + 8) & 31)];
+        const double xd3 = xs[32 * j + ((lane + 12) & 31)];
+        const double xd4 = xs[32 * j + ((lane + 16) & 31)];
         dmma(aXL, xa, sv);
-        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
-        dmma(aRA[0], xa, sam[jj]);
-        dmma(aRA[1], sv, sam[jj]);
-        dmma(aRA[2], tv, sam[jj]);
-        r8[0] = fma(xa, s8[jj], r8[0]);
-        r9[0] = fma(xa, s9[jj], r9[0]);
-        r8[1] = fma(sv, s8[jj], r8[1]);
-        r9[1] = fma(sv, s9[jj], r9[1]);
-        r8[2] = fma(tv, s8[jj], r8[2]);
-        r9[2] = fma(tv, s9[jj], r9[2]);
+        xx0 = fma(xa, xa, xx0);
+        xx1 = fma(xa, xd1, xx1);
+        xx2 = fma(xa, xd2, xx2);
+        xx3 = fma(xa, xd3, xx3);
+        xx4 = fma(xa, xd4, xx4);
+        x8 = fma(xa, s89.x, x8);
+        x9 = fma(xa, s89.y, x9);
+      };
+      // row-level A products of group j (rows masked to [lo, hi) when MASK)
+      auto cold_group = [&](auto mask_tag, int j, double xa, double sv, double2 s89, double tv, double sam,
+                            double2 sa89, int lo, int hi) {
+        constexpr bool MASK = decltype(mask_tag)::value;
+        if (MASK) {
+          const int r = 4 * j + k;
+          const double mk = (r >= lo && r < hi) ? 1.0 : 0.0;
+          xa *= mk;
+          sv *= mk;
+          tv *= mk;
+          s89.x *= mk;
+          s89.y *= mk;
+          sa89.x *= mk;
+          sa89.y *= mk;
+          sam *= mk;
+        }
+        if (COV_XX_DMMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
+        dmma(aRA0, xa, sam);
+        dmma(aRA1, sv, sam);
+        tA8 = fma(s89.x, sam, tA8);
+        tA9 = fma(s89.y, sam, tA9);
+        r8x = fma(xa, sa89.x, r8x);
+        r9x = fma(xa, sa89.y, r9x);
+        r8l = fma(sv, sa89.x, r8l);
+        r9l = fma(sv, sa89.y, r9l);
+        r8t = fma(tv, sa89.x, r8t);
+        r9t = fma(tv, sa89.y, r9t);
         SB0 += xa;
         SB1 += sv;
         SB2 += tv;
-        SBn += sam[jj];
-        SBn8 += s8[jj];
-        SBn9 += s9[jj];
-      }
-      }
-    } else {
-      // segments of the block: segment 0 starts at row 0, segment s >= 1 at the s-th run start
-      const int R = __popc(mAx);
-      {
-        const int sr = __popc(mAx & ((2u << lane) - 1u));
-        if (lane == 0 || ((mAx >> lane) & 1u)) {
-          segst[sr] = lane;
-          segkey[sr] = ka;
-        }
-        if (lane == 0) segst[R + 1] = nv;
-        __syncwarp();
-      }
-      int sb = 0;  // first segment of the current window of 8
-      double D[3][2] = {{0, 0}, {0, 0}, {0, 0}};
-      // this lane's record slots: segments s0 = sb + 2k (pass 0) and s0 + 1 (pass 1)
-      int key0 = 0, key1 = 0;
-      double b0 = 0, b1 = 0;
-      double2 b089 = make_double2(0, 0), b189 = make_double2(0, 0);
-      auto load_window = [&]() {  // keys and s_A rows of the window's segments
-        const int s0 = sb + 2 * k, s1 = s0 + 1;
-        const bool v0 = s0 <= R, v1 = s1 <= R;
-        key0 = v0 ? segkey[s0] : 0;
-        key1 = v1 ? segkey[s1] : 0;
-        const double* row0 = g.VA + (size_t)(unsigned)key0 * GP;
-        const double* row1 = g.VA + (size_t)(unsigned)key1 * GP;
-        b0 = v0 ? row0[m] : 0.0;
-        b1 = v1 ? row1[m] : 0.0;
-        b089 = v0 ? *reinterpret_cast<const double2*>(row0 + 8) : make_double2(0, 0);
-        b189 = v1 ? *reinterpret_cast<const double2*>(row1 + 8) : make_double2(0, 0);
+        SBn += sam;
+        SBn8 += sa89.x;
+        SBn9 += sa89.y;
       };
-      // the window's (partial) level-A records ⊗ s_A, and level B; segments before s_end are
-      // complete here (s_end itself may continue into the next window)
-      auto flush_window = [&](int s_end) {
-        const int s0 = sb + 2 * k, s1 = s0 + 1;
-        // row counts of the slots (incl. rows carried from earlier blocks) = the t tile's "1" row
-        const double n0 = __shfl_sync(FULL, D[2][0], 8 + k), n1 = __shfl_sync(FULL, D[2][1], 8 + k);
-        if (!(g.ablate & 2)) {
+      // s_A rows of this lane's rows in groups 4h .. 4h+3 (loads in flight together)
+      auto load_sa = [&](int h, double (&sam)[4], double2 (&sa89)[4]) {
 #pragma unroll
-          for (int t = 0; t < 3; t++) {
-            dmma(aRA[t], D[t][0], b0);
-            dmma(aRA[t], D[t][1], b1);
-            r8[t] = fma(D[t][0], b089.x, fma(D[t][1], b189.x, r8[t]));
-            r9[t] = fma(D[t][0], b089.y, fma(D[t][1], b189.y, r9[t]));
-          }
-          if (NS >= 1 && m == 0) {
-            if (n0 > 0.0) gred_add(&g.HA[key0], (unsigned)n0);
-            if (n1 > 0.0) gred_add(&g.HA[key1], (unsigned)n1);
-          }
+        for (int jj = 0; jj < 4; jj++) {
+          const unsigned key = (unsigned)__shfl_sync(FULL, ka, 4 * (4 * h + jj) + k);
+          const double* ar = g.VA + (size_t)key * GP;
+          sam[jj] = ar[m];
+          sa89[jj] = ld2(ar + 8);
         }
-        auto add_segs = [&](int lo, int hi) {  // segments [lo, hi) of the window -> the open B run
-          const bool u0 = s0 >= lo && s0 < hi, u1 = s1 >= lo && s1 < hi;
-          const double d0 = u0 ? 1.0 : 0.0, d1 = u1 ? 1.0 : 0.0;
-          SB0 = fma(d0, D[0][0], fma(d1, D[0][1], SB0));
-          SB1 = fma(d0, D[1][0], fma(d1, D[1][1], SB1));
-          SB2 = fma(d0, D[2][0], fma(d1, D[2][1], SB2));
-          const double w0 = u0 ? n0 : 0.0, w1 = u1 ? n1 : 0.0;
-          SBn = fma(w0, b0, fma(w1, b1, SBn));
-          SBn8 = fma(w0, b089.x, fma(w1, b189.x, SBn8));
-          SBn9 = fma(w0, b089.y, fma(w1, b189.y, SBn9));
-        };
-        int lo = sb;
-        unsigned bb = mB & ~1u;
-        while (bb) {  // level-B run starts inside the block (rare)
-          const int p = __ffs(bb) - 1;
-          bb &= bb - 1;
-          const int sp = __popc(mAx & ((2u << p) - 1u));
-          if (sp <= sb || sp > s_end) continue;  // handled by the window that completes segment sp - 1
-          add_segs(lo, sp);
-          push_B(curB);
-          curB = __shfl_sync(FULL, kb, p);
-          lo = sp;
-        }
-        add_segs(lo, sb + 8);
-#pragma unroll
-        for (int t = 0; t < 3; t++) D[t][0] = D[t][1] = 0.0;
       };
-      load_window();
-      {  // the carried part of segment 0 (rows of earlier blocks) -> slot 0
-        const double f0 = red4(C0), f1 = red4(C1), f2 = red4(C2);
-        if (k == 0) {
-          D[0][0] = f0;
-          D[1][0] = f1;
-          D[2][0] = f2;
+      // H_A: each A run's rows in this block (the carried rows were added by flush_carry)
+      auto ha_runs = [&]() {
+        if (((mA >> lane) & 1u) || lane == 0) {
+          const unsigned above = mA & ~((2u << lane) - 1u);
+          gred_add(&g.HA[ka], (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
         }
-        C0 = C1 = C2 = 0.0;
-      }
+      };
+      const unsigned mBi = NS == 2 ? (mB & ~1u) : 0u;
+      if (NS >= 1 && mBi) {
+        // slow: level-B runs start inside the block
+        if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
+        carried = false;
+        ha_runs();
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        const double xa = xs[32 * j + lane];
-        const double* gr = gl + j * 4 * GP;
-        const double sv = gr[m];
-        const double tv = gr[tcol];
-        dmma(aXX, xa, xa);
-        dmma(aXL, xa, sv);
-        dmma(aXT, xa, tv);  // x ⊗ [s_L8, s_L9, 1]: B[k][n] = t_n(row k) from lane 4n + k
-        const int slast = __popc(mAx & ((2u << (4 * j + 3)) - 1u));
-        if (slast - sb >= 8) {  // the group reaches past the window: flush it, restart at the group's first segment
-          const int s4j = __popc(mAx & ((2u << (4 * j)) - 1u));
-          flush_window(s4j);
-          sb = s4j;
-          load_window();
+        for (int j = 0; j < 8; j++) {
+          double xa, sv, tv;
+          double2 s89;
+          rowpart(j, xa, sv, s89, tv);
         }
-        const int sr = __popc(mAx & ((2u << (4 * j + k)) - 1u));
-        const double ind = (sr - sb == m) ? 1.0 : 0.0;
-        dmma(D[0], xa, ind);
-        dmma(D[1], sv, ind);
-        dmma(D[2], tv, ind);
-      }
-      if (endA) {
-        flush_window(64);
-      } else {  // the last segment continues into the next block: keep it open (carried in C)
-        const int sl = R - sb;  // its slot
-        {
-          // take it out of D before the flush: its value moves to lane (m, 0) of C
-          double e0 = 0, e1 = 0, e2 = 0;
-          if (k == (sl >> 1)) {
-            e0 = (sl & 1) ? D[0][1] : D[0][0];
-            e1 = (sl & 1) ? D[1][1] : D[1][0];
-            e2 = (sl & 1) ? D[2][1] : D[2][0];
-            if (sl & 1) D[0][1] = D[1][1] = D[2][1] = 0.0;
-            else D[0][0] = D[1][0] = D[2][0] = 0.0;
+        unsigned bits = mBi;
+        int lo = 0;
+        while (true) {
+          const int hi = bits ? __ffs(bits) - 1 : 32;
+#pragma unroll 1
+          for (int h = 0; h < 2; h++) {
+            double sam[4];
+            double2 sa89[4];
+            load_sa(h, sam, sa89);
+#pragma unroll
+            for (int jj = 0; jj < 4; jj++) {
+              const int j = 4 * h + jj;
+              const double* gr = gl + j * 4 * GP;
+              cold_group(std::true_type{}, j, xs[32 * j + lane], gr[m], ld2(gr + 8), gr[tcol], sam[jj], sa89[jj], lo,
+                         hi);
+            }
           }
-          C0 = __shfl_sync(FULL, e0, 4 * m + (sl >> 1));
-          C1 = __shfl_sync(FULL, e1, 4 * m + (sl >> 1));
-          C2 = __shfl_sync(FULL, e2, 4 * m + (sl >> 1));
-          if (k != 0) C0 = C1 = C2 = 0.0;
+          if (hi == 32) break;
+          push_B(__shfl_sync(FULL, kb, hi - 1));
+          lo = hi;
+          bits &= bits - 1;
         }
-        flush_window(64);
+      } else if (NS >= 1 && ((mA & ~1u) || g.cold_all) && !(g.ablate & 32)) {
+        // cold: level-A runs start inside the block; every row times its own s_A row
+        if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
+        carried = false;
+        ha_runs();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          double sam[4];
+          double2 sa89[4];
+          load_sa(h, sam, sa89);
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            double xa, sv, tv;
+            double2 s89;
+            rowpart(4 * h + jj, xa, sv, s89, tv);
+            cold_group(std::false_type{}, 4 * h + jj, xa, sv, s89, tv, sam[jj], sa89[jj], 0, 32);
+          }
+        }
+      } else {
+        // fast: the open A run goes on through the block
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          double xa, sv, tv;
+          double2 s89;
+          rowpart(j, xa, sv, s89, tv);
+          C0 += xa;
+          C1 += sv;
+          C2 += tv;
+        }
+        carried = !endA;
+        if (endA) flush_carry(__shfl_sync(FULL, ka, 31));
+      }
+      if (endB) push_B(__shfl_sync(FULL, kb, 31));
+    }
+    __syncwarp();
+    if (fitem < nitems) issue_fact(fb, fs);  // the slot just consumed takes the block CF ahead
+    f_advance();
+    if (next_in_item) {
+      pb++;
+    } else {  // the item is done: its partial -> partials[item], accumulators cleared
+      store_partial(pitem);
+      pslot++;
+      pitem = nitem;
+      if (has_next) {
+        pb = pbeg = g.item[pitem];
+        pend = g.item[pitem + 1];
+        rec = g.rec_base[pitem];
       }
     }
-    if (endB && openB) {  // the level-B run ends with this block
-      push_B(curB);
-      openB = false;
-    }
-    issue_fact(cf, fs);  // the slot just consumed takes the block CF ahead
-    advance(cf, true);
-    cc = cn;
-    blk++;
     fs = fs1;
-    if (fs == 0) fph ^= 1;
+    fph = fph1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
 
-  // ---- this warp's partial -> partials[CTA * W + warp] (no CTA barrier: warps finish unevenly)
-#pragma unroll
-  for (int t = 0; t < 3; t++) {
-    r8[t] = red4(r8[t]);
-    r9[t] = red4(r9[t]);
-  }
-  double* out = g.partials + ((size_t)blockIdx.x * W + wib) * NPART;
-  out[m * 8 + 2 * k] = aXX[0];
-  out[m * 8 + 2 * k + 1] = aXX[1];
-  out[64 + m * 10 + 2 * k] = aXL[0];
-  out[64 + m * 10 + 2 * k + 1] = aXL[1];
-  if (k == 0) {
-    out[64 + m * 10 + 8] = aXT[0];
-    out[64 + m * 10 + 9] = aXT[1];
-  }
-#pragma unroll
-  for (int t = 0; t < 3; t++) {
-    out[144 + (8 * t + m) * 10 + 2 * k] = aRA[t][0];
-    out[144 + (8 * t + m) * 10 + 2 * k + 1] = aRA[t][1];
-    if (k == 0) {
-      out[144 + (8 * t + m) * 10 + 8] = r8[t];
-      out[144 + (8 * t + m) * 10 + 9] = r9[t];
-    }
-  }
   // ---- the CTA's last warp to finish moves the H_L table to global
   __threadfence_block();
   int ticket = 0;
@@ -879,47 +854,48 @@ struct FastCov : FastPaths {
   std::vector<int> fattrs;
   CovLevel L, A, B;
   DevBuf zeros;  // one zero view row (absent levels)
-  DevBuf zbuf;   // [work | bcount | pad] [HA] [HL], cleared every run
+  DevBuf zbuf;   // [pad] [HA] [HL], cleared every run
   size_t off_HA = 0, off_HL = 0, zbytes = 0;
   DevBuf brec, partials, finp, src, toff, tidx, tcoef;
-  DevBuf scan;  // scan layout of the root (k_cov_layout), built at plan time
-  int64_t nblk = 0;
-  int bcap = 0, grid = 148, nout = 0, ib = IB;
+  DevBuf scan;   // scan layout of the root (k_cov_layout), built at plan time
+  DevBuf items;  // [nitems + 1] first block of each work item (plan time)
+  DevBuf rbase;  // [nitems + 1] first level-B record slot of each item; rbase[nitems] = records
+  int64_t nblk = 0, nrec = 0;
+  int nitems = 0, nstatic = 0;
+  int grid = 148, nout = 0;
   bool only_scalar = true;
 
   std::string describe() const override {
-    char b[256];
+    char b[320];
     std::snprintf(b, sizeof b,
                   "{\"kind\": \"cov\", \"NS\": %d, \"nF\": %d, \"nL\": %zu, \"nA\": %zu, \"nB\": %zu, \"grid\": %d, "
-                  "\"threads\": %d, \"stages\": %d, \"item\": %d}",
-                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, COV_W * 32, CovCfg<COV_W>::CF, 32 * ib);
+                  "\"threads\": %d, \"stages\": %d, \"static_chunks\": %d, \"items\": %d, \"b_records\": %lld}",
+                  NS, nF, L.attrs.size(), A.attrs.size(), B.attrs.size(), grid, COV_W * 32, CovCfg<COV_W>::CF,
+                  nstatic, nitems, (long long)nrec);
     return b;
   }
   bool skip_generic_views() const override { return only_scalar; }
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
 };
 
-int cov_warps() { return COV_W; }  // (16 warps per CTA spilled at 128 registers; measured slower)
+int cov_warps() { return COV_W; }
 
-template <int W, int IBK>
+template <int W>
+cudaError_t cov_kernel_attr(int NS) {  // per device: called at plan time on the ctx's device
+  constexpr int smem = CovCfg<W>::SMEM;
+  if (NS == 0) return cudaFuncSetAttribute(k_cov<0, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (NS == 1) return cudaFuncSetAttribute(k_cov<1, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return cudaFuncSetAttribute(k_cov<2, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+template <int W>
 cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
-  static bool attr[3] = {false, false, false};
-  auto go = [&](auto kern) -> cudaError_t {
-    constexpr int smem = CovCfg<W>::SMEM;
-    if (!attr[NS]) {
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      attr[NS] = true;
-    }
-    kern<<<grid, W * 32, smem, st>>>(g);
-    return cudaGetLastError();
-  };
-  if (NS == 0) return go(k_cov<0, W, IBK>);
-  if (NS == 1) return go(k_cov<1, W, IBK>);
-  return go(k_cov<2, W, IBK>);
+  constexpr int smem = CovCfg<W>::SMEM;
+  if (NS == 0) k_cov<0, W><<<grid, W * 32, smem, st>>>(g);
+  else if (NS == 1) k_cov<1, W><<<grid, W * 32, smem, st>>>(g);
+  else k_cov<2, W><<<grid, W * 32, smem, st>>>(g);
+  return cudaGetLastError();
 }
-cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) {
-  return g.ib == IB ? launch_cov_w<COV_W, IB>(NS, g, grid, st) : launch_cov_w<COV_W, 2>(NS, g, grid, st);
-}
+cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) { return launch_cov_w<COV_W>(NS, g, grid, st); }
 
 }  // namespace
 
@@ -944,25 +920,25 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
     }
   }
   CovArgs g{};
-  g.nrows = R.nrows;
   g.nblk = nblk;
   g.scan = scan.as<unsigned char>();
   g.VL = L.V.as<double>();
   g.VA = NS >= 1 ? A.V.as<double>() : zeros.as<double>();
   char* z = zbuf.as<char>();
-  g.work = reinterpret_cast<int*>(z);
-  g.bcount = reinterpret_cast<int*>(z + 4);
   g.HA = reinterpret_cast<unsigned*>(z + off_HA);
   g.HL = reinterpret_cast<unsigned*>(z + off_HL);
   {
     const char* ab = std::getenv("LMFAO_COV_ABLATE");
     g.ablate = ab ? std::atoi(ab) : 0;
-    const char* cd = std::getenv("LMFAO_COV_COLD");
-    g.cold = cd ? std::atoi(cd) : COV_COLD;
+    const char* cd = std::getenv("LMFAO_COV_COLD_ALL");
+    g.cold_all = cd && cd[0] == '1';
   }
   g.brec = brec.as<double>();
-  g.bcap = bcap;
-  g.ib = ib;
+  g.item = items.as<int>();
+  g.nitems = nitems;
+  g.nstatic = nstatic;
+  g.work = reinterpret_cast<int*>(z);
+  g.rec_base = rbase.as<int>();
   g.partials = partials.as<double>();
   scan_timer_begin(c, st);
   cudaError_t e = launch_cov(NS, g, grid, st);
@@ -971,8 +947,8 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   launches_add(1);
   FinArgs f{};
   f.brec = brec.as<double>();
-  f.bcount = g.bcount;
-  f.bcap = bcap;
+  f.bcount = g.rec_base + nitems;
+  f.bcap = (int)nrec;
   f.VB = NS == 2 ? B.V.as<double>() : zeros.as<double>();
   f.HL = g.HL;
   f.VL = L.V.as<double>();
@@ -982,7 +958,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
   k_cov_fin<<<FIN_BLOCKS, 256, 8 * NFIN * 8, st>>>(f);
-  k_cov_sum<<<dim3((NPART + NFIN + 31) / 32, SUM_SPLIT), 1024, 0, st>>>(partials.as<double>(), grid * cov_warps(), finp.as<double>(),
+  k_cov_sum<<<dim3((NPART + NFIN + 31) / 32, SUM_SPLIT), 1024, 0, st>>>(partials.as<double>(), nitems, finp.as<double>(),
                                                       FIN_BLOCKS, src.as<double>());
   k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                          tcoef.as<double>(), nout, c->scalar_out.as<double>(),
@@ -1126,20 +1102,16 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   fc->zbytes = fc->off_HL + (size_t)(fc->L.nk + 1) * 4;
   if (fc->zbuf.alloc(fc->zbytes)) return nullptr;
   tr.mark("terms + buffers", c->stream);
+  {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0) fc->grid = sms;
+  }
+  const int NW = fc->grid * COV_W;
   fc->nblk = (R.nrows + 31) / 32;
-  // work items as k_cov defines them: ib-block items, then 2-block items for the last ~10 %;
-  // ib = IB unless the root has fewer than 2 such items per warp; then 2 (C1, 625 blocks:
-  // 0.057 ms in 24-block items, 0.045 in 16, 0.030 in 2)
-  fc->ib = fc->nblk >= (int64_t)fc->grid * COV_W * 2 * IB ? IB : 2;
-  const int64_t nbig = fc->nblk * (100 - COV_TAIL_PCT) / 100 / fc->ib;
-  const int64_t nitems = nbig + (fc->nblk - nbig * fc->ib + 1) / 2;
-  // level-B records: one per (B run, item) pair <= B runs + items
-  fc->bcap = (int)std::min<int64_t>((fc->NS == 2 ? fc->B.nk : 0) + nitems + 64, INT32_MAX / BRW);
-  if (fc->brec.alloc((size_t)fc->bcap * BRW * 8)) return nullptr;
-  if (fc->partials.alloc((size_t)fc->grid * 16 * NPART * 8)) return nullptr;  // one partial per warp
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
   if (fc->src.alloc((size_t)SUM_SPLIT * (NPART + NFIN) * 8)) return nullptr;
-  {  // scan layout of the root: x in DMMA lane order + dense keys, one 2432-byte block per 32 rows
+  {  // scan layout of the root: x in DMMA lane order + dense keys with run-start flags, one
+     // 2432-byte block per 32 rows
     if (fc->scan.alloc((size_t)std::max<int64_t>(fc->nblk, 1) * SBLK)) return nullptr;
     LayoutArgs la{};
     for (int i = 0; i < 8; i++) la.x[i] = i < fc->nF ? (const double*)R.cols[R.find_attr(fc->fattrs[i])].buf.p : nullptr;
@@ -1156,8 +1128,66 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     la.out = fc->scan.as<unsigned char>();
     if (fc->nblk > 0) {
       k_cov_layout<<<148 * 8, 256, 0, c->stream>>>(la);
-      if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(c->stream) != cudaSuccess) return nullptr;
+      if (cudaGetLastError() != cudaSuccess) return nullptr;
     }
+  }
+  tr.mark("scan layout", c->stream);
+  {  // work items and their level-B record slots (see COV_TAIL)
+    const int64_t n = fc->nblk;
+    DevBuf bst;
+    if (bst.alloc((size_t)std::max<int64_t>(n, 1) * 4)) return nullptr;
+    if (n > 0)
+      k_cov_bstats<<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, c->stream>>>(
+          fc->scan.as<unsigned char>(), n, fc->NS, bst.as<uint32_t>());
+    std::vector<uint32_t> h((size_t)n);
+    if (n > 0 && (cudaMemcpyAsync(h.data(), bst.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream) ||
+                  cudaStreamSynchronize(c->stream) || cudaGetLastError()))
+      return nullptr;
+    int cold = COV_COST_COLD, tb = COV_TB, tail = COV_TAIL;
+    if (const char* e = std::getenv("LMFAO_COV_COST_COLD")) cold = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LMFAO_COV_TB")) tb = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("LMFAO_COV_TAIL")) tail = std::min(100, std::max(0, std::atoi(e)));
+    std::vector<uint64_t> cc((size_t)n + 1, 0);  // cost prefix
+    for (int64_t b = 0; b < n; b++) cc[b + 1] = cc[b] + ((h[b] & 128u) ? (uint64_t)cold : (uint64_t)COST_FAST);
+    const uint64_t stat = cc[n] * (uint64_t)(100 - tail) / 100;  // cost of the static part
+    std::vector<int32_t> it{0};
+    fc->nstatic = 0;
+    if (n >= 8 * (int64_t)NW) {  // every static chunk non-empty (>= 3 blocks)
+      for (int w = 1; w <= NW; w++) {  // chunk w-1 = [it[w-1], first b with cc[b] >= stat·w/NW)
+        const uint64_t target = stat * (uint64_t)w / (uint64_t)NW;
+        it.push_back((int32_t)(std::lower_bound(cc.begin(), cc.end(), target) - cc.begin()));
+      }
+      fc->nstatic = NW;
+    } else {  // a small root: dynamic items only, about two per warp
+      tb = (int)std::min<int64_t>(tb, n / (2 * (int64_t)NW));
+    }
+    constexpr int CFb = CovCfg<COV_W>::CF;  // k_cov needs items of at least CF blocks
+    tb = std::max(tb, CFb);
+    while (it.back() < n) {
+      const int64_t e = std::min<int64_t>(it.back() + tb, n);
+      if (n - e < CFb) {  // the remainder is too short for an item of its own
+        it.push_back((int32_t)n);
+        break;
+      }
+      it.push_back((int32_t)e);
+    }
+    fc->nitems = (int)it.size() - 1;
+    std::vector<int32_t> rb((size_t)fc->nitems + 1, 0);
+    for (int i = 0; i < fc->nitems; i++) {  // an item's records: its B run starts, its row 0 starting one
+      int32_t r = 0;
+      for (int64_t b = it[i]; b < it[i + 1]; b++) r += (int32_t)(h[b] & 63u);
+      if (it[i + 1] > it[i] && !(h[it[i]] & 64u)) r += 1;
+      rb[i + 1] = rb[i] + r;
+    }
+    if (fc->items.alloc(it.size() * 4) || fc->rbase.alloc(rb.size() * 4) ||
+        cudaMemcpyAsync(fc->items.p, it.data(), it.size() * 4, cudaMemcpyHostToDevice, c->stream) ||
+        cudaMemcpyAsync(fc->rbase.p, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice, c->stream) ||
+        cudaStreamSynchronize(c->stream))
+      return nullptr;
+    const uint32_t tot = (uint32_t)rb.back();
+    fc->nrec = tot;
+    if (fc->partials.alloc((size_t)std::max(fc->nitems, 1) * NPART * 8)) return nullptr;  // one partial per item
+    if (fc->brec.alloc((size_t)std::max<uint32_t>(tot, 1) * BRW * 8)) return nullptr;
   }
   tr.mark("scan layout", c->stream);
   // source index of G[a][b] (a, b: attr id or -1 = "1"); see the layout above k_cov_sum
@@ -1235,6 +1265,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   }
   if (cudaStreamSynchronize(st)) return nullptr;
   if (cudaFuncSetAttribute(k_cov_fin, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * NFIN * 8)) return nullptr;
+  if (cov_kernel_attr<COV_W>(fc->NS)) return nullptr;
   return fc.release();
 }
 

@@ -43,18 +43,23 @@ CASES = [
     (1, [2, 2, 2], [5, 7, 11]),              # tiny domains: very long runs
     (8, [4, 0, 6, 0], [30, 60, 600, 5000]),  # featureless dims interleaved in the sort order
     (0, [3, 4], [50, 400]),                  # no fact features
+    (8, [0, 4, 4, 4], [30, 100, 1000, 5000]),  # a featureless dim sorts first: B runs nest in its runs
 ]
 
 
 FAST = ("cov", "gram")
 
 
-@pytest.fixture(params=["cov", "gram"])
+@pytest.fixture(params=["cov", "cov_cold", "gram"])
 def kernel(request, monkeypatch):
-    """Run each case through the compile-time-specialised k_cov kernel (cov.cu) and,
-    with LMFAO_NO_COV=1, through the general gram.cu kernel."""
+    """Run each case through the compile-time-specialised k_cov kernel (cov.cu) — as planned,
+    and with LMFAO_COV_COLD_ALL=1, which sends every block down the per-row level-A path
+    (exact by linearity) — and, with LMFAO_NO_COV=1, through the general gram.cu kernel."""
     if request.param == "gram":
         monkeypatch.setenv("LMFAO_NO_COV", "1")
+    if request.param == "cov_cold":
+        monkeypatch.setenv("LMFAO_COV_COLD_ALL", "1")
+        return "cov"
     return request.param
 
 
