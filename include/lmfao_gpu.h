@@ -25,11 +25,18 @@
  *  - Inputs are copied (the caller keeps ownership).  Host output buffers are
  *    caller-owned; device views returned by lmfao_result_device are
  *    library-owned and valid until the next run/destroy.
- *  - Multi-GPU (world > 1): each rank passes the whole root relation; after the
- *    global sort in lmfao_prepare the rank keeps its contiguous shard of the
- *    sorted root (domain parallelism), dimension relations are
- *    replicated, and lmfao_run combines the partial aggregates with an NCCL
- *    all-reduce over NVLink, so every rank holds the full results.
+ *  - Multi-GPU (world > 1, one process per GPU): each rank passes the whole root
+ *    relation; after the global sort in lmfao_prepare the rank keeps its
+ *    contiguous shard of the sorted root (domain parallelism, "partition
+ *    the largest relation"), dimension relations are replicated, and lmfao_run
+ *    merges the partial aggregates over NVLink / NVSwitch: scalar queries and
+ *    group-by tables below LMFAO_DIST_CELLS cells (default 65536) by an NCCL
+ *    all-reduce (complete on every rank); larger dense tables by a
+ *    reduce-scatter, and sparse data-cube cuboids by an exchange through peer
+ *    memory (CUDA IPC), after which each rank holds the groups of its own
+ *    contiguous range of cells (lmfao_owner_range) — lmfao_result_shape /
+ *    lmfao_fetch return that range, lmfao_gather_result assembles the whole
+ *    table on one rank.  lmfao_plan_info lists each query's placement.
  *  - There is no CPU fallback: without a usable CUDA device every call that
  *    needs one returns LMFAO_ERR_CUDA.
  */
@@ -107,6 +114,22 @@ LMFAO_API lmfao_status lmfao_unique_id(void* out);
 /* Creates a context on CUDA device `device`.  world >= 1, 0 <= rank < world;
  * unique_id must be non-NULL iff world > 1 (collective call across ranks). */
 LMFAO_API lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id, lmfao_ctx** out);
+
+/* Testing the multi-GPU path on one GPU: `world` contexts of ONE process on one device form
+ * the in-process group named `group` (rank 0 .. world-1), each driven by its own host thread
+ * (every call that is collective for NCCL ranks — prepare's sharding, plan, run,
+ * gather_result — must be made by all of them).  The data path is the one of NCCL ranks —
+ * sharded root, the same kernels, reduce-scatter / exchange / gather — with the collectives
+ * done by device copies and the phases of a run separated by host barriers (no kernel waits
+ * for another rank's kernel; no CUDA Graph).  Not for production. */
+LMFAO_API lmfao_status lmfao_create_loopback(int device, int rank, int world, const char* group, lmfao_ctx** out);
+
+/* Host-only (no device needed): the contiguous shard [lo, hi) of a root of nrows sorted rows
+ * kept by `part` of `nparts` ([n·part/nparts, n·(part+1)/nparts)), and the range of cells
+ * [lo, hi) of a distributed output with ncells cells owned by `rank` of `world` (equal chunks
+ * of ceil(ncells / world) cells; the last ranks' may be short or empty). */
+LMFAO_API lmfao_status lmfao_shard_range(int64_t nrows, int32_t part, int32_t nparts, int64_t* lo, int64_t* hi);
+LMFAO_API lmfao_status lmfao_owner_range(int64_t ncells, int32_t rank, int32_t world, int64_t* lo, int64_t* hi);
 LMFAO_API lmfao_status lmfao_destroy(lmfao_ctx* ctx);
 LMFAO_API const char* lmfao_last_error(const lmfao_ctx* ctx);
 
@@ -177,8 +200,12 @@ LMFAO_API lmfao_status lmfao_reset_batch(lmfao_ctx* ctx);
 
 /* Runs the planned batch asynchronously on `cuda_stream` (cudaStream_t; NULL =
  * the ctx's own stream): view builds (b), the fused root scan (c) with its FP64
- * Gram tiles (d) and histograms (e), dimension-side finishing, the NCCL
- * all-reduce when world > 1, and compaction.  No host synchronisation. */
+ * Gram tiles (d) and histograms (e), dimension-side finishing, and when world > 1
+ * the collectives (see "Multi-GPU").  No host synchronisation (sizes that depend on
+ * the data stay on the device; compaction of dense tables happens at the first
+ * result_shape / fetch); the second run of a plan is captured in a CUDA Graph
+ * (NCCL collectives included) and later runs replay it.  LMFAO_ERR_NCCL if the
+ * communicator reported an asynchronous error. */
 LMFAO_API lmfao_status lmfao_run(lmfao_ctx* ctx, void* cuda_stream);
 
 /* Result shape of query_id after the last run (synchronises the stream). */
@@ -191,6 +218,14 @@ LMFAO_API lmfao_status lmfao_result_shape(lmfao_ctx* ctx, int32_t query_id, int6
  * join multiplicity of each group (nullable). Groups in ascending key order. */
 LMFAO_API lmfao_status lmfao_fetch(lmfao_ctx* ctx, int32_t query_id, int32_t* keys_out, double* vals_out,
                          uint64_t* counts_out);
+
+/* Collective (every rank calls it, world > 1): assembles a distributed result (see
+ * "Multi-GPU" above) on root_rank — the ranks' groups in rank order, which is the canonical
+ * ascending key order since the ranges ascend with the rank; afterwards result_shape / fetch /
+ * result_device on root_rank return the whole table (until the next run), the other ranks keep
+ * their own range.  Synchronises.  A no-op for results complete on every rank (scalar queries,
+ * all-reduced tables) and for world == 1.  LMFAO_ERR_NCCL if a transfer fails. */
+LMFAO_API lmfao_status lmfao_gather_result(lmfao_ctx* ctx, int32_t query_id, int32_t root_rank);
 
 /* Library-owned device views of query_id's result (same layout as fetch). */
 LMFAO_API lmfao_status lmfao_result_device(lmfao_ctx* ctx, int32_t query_id, const int32_t** keys,

@@ -131,6 +131,8 @@ lmfao_status lmfao_unique_id(void* out) {
   return nccl_unique_id(out) == 0 ? LMFAO_OK : LMFAO_ERR_NCCL;
 }
 
+lmfao_status lmfao_destroy(lmfao_ctx* c);
+
 lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id, lmfao_ctx** out) {
   if (!out || world < 1 || rank < 0 || rank >= world) return LMFAO_ERR_INVALID_ARG;
   if ((world > 1) != (unique_id != nullptr)) return LMFAO_ERR_INVALID_ARG;
@@ -159,8 +161,9 @@ lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id
     return LMFAO_ERR_CUDA;
   }
   if (world > 1) {
-    int e = nccl_init(&c->comm, world, unique_id, rank);
-    if (e != 0) {
+    int e = 0;
+    c->comm.reset(make_nccl_comm(rank, world, unique_id, e));
+    if (!c->comm) {
       cudaStreamDestroy(c->stream);
       delete c;
       return LMFAO_ERR_NCCL;
@@ -170,12 +173,46 @@ lmfao_status lmfao_create(int device, int rank, int world, const void* unique_id
   return LMFAO_OK;
 }
 
+lmfao_status lmfao_create_loopback(int device, int rank, int world, const char* group, lmfao_ctx** out) {
+  if (!out || !group || world < 1 || rank < 0 || rank >= world) return LMFAO_ERR_INVALID_ARG;
+  *out = nullptr;
+  lmfao_status s = lmfao_create(device, 0, 1, nullptr, out);
+  if (s != LMFAO_OK) return s;
+  lmfao_ctx* c = *out;
+  c->rank = rank;
+  c->world = world;
+  c->shard_part = rank;
+  c->shard_nparts = world;
+  if (world > 1) {
+    c->comm.reset(make_loopback_comm(group, rank, world, device));
+    if (!c->comm) {
+      lmfao_destroy(c);
+      *out = nullptr;
+      return LMFAO_ERR_INVALID_ARG;
+    }
+  }
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_shard_range(int64_t nrows, int32_t part, int32_t nparts, int64_t* lo, int64_t* hi) {
+  if (nrows < 0 || nparts < 1 || part < 0 || part >= nparts || !lo || !hi) return LMFAO_ERR_INVALID_ARG;
+  shard_range(nrows, part, nparts, *lo, *hi);
+  return LMFAO_OK;
+}
+
+lmfao_status lmfao_owner_range(int64_t ncells, int32_t rank, int32_t world, int64_t* lo, int64_t* hi) {
+  if (ncells < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return LMFAO_ERR_INVALID_ARG;
+  owner_range(ncells, rank, world, *lo, *hi);
+  return LMFAO_OK;
+}
+
 lmfao_status lmfao_destroy(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   cudaSetDevice(c->device);
   StreamScope scope_(c->stream);
   cudaStreamSynchronize(c->stream);
-  if (c->comm) nccl_destroy(c->comm);
+  c->fast.reset();  // peer mappings before the communicator
+  c->comm.reset();
   cudaStream_t st = c->stream;
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
@@ -492,6 +529,7 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
   for (auto& r : c->rels)  // columns no permutation consumed
     for (auto& col : r.cols) CTX_CUDA(c, column_ready(col, st), "prepare copy");
   if (c->copy_stream) CTX_CUDA(c, cudaStreamSynchronize(c->copy_stream), "prepare copy");  // host buffers released
+  c->root_rows_global = R.nrows;
   if (c->shard_nparts > 1) {
     for (size_t i = 0; i < R.cols.size(); i++) {
       if (R.cols[i].dt != LMFAO_INT32) continue;
@@ -501,8 +539,8 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       R.full_dict_n[R.cols[i].attr] = nd;
       R.full_dict[R.cols[i].attr] = std::move(d);
     }
-    int64_t N = R.nrows;
-    int64_t lo = N * c->shard_part / c->shard_nparts, hi = N * (c->shard_part + 1) / c->shard_nparts;
+    int64_t lo = 0, hi = 0;
+    shard_range(R.nrows, c->shard_part, c->shard_nparts, lo, hi);
     CTX_CUDA(c, slice_rel(R, lo, hi, st), "prepare shard");
   }
   // owners: the top-most relation holding each attribute (unique by P:720)
@@ -916,10 +954,24 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     gp.ncells = cells;
     if ((double)cells * (gp.nudaf + 1) * 8 > 40e9)
       return fail(c, LMFAO_ERR_UNSUPPORTED, "dense group-by table too large (%lld cells)", (long long)cells);
+    // world > 1: tables of at least LMFAO_DIST_CELLS cells (default 2^16) are distributed —
+    // reduce-scattered by cell range; smaller ones are all-reduced (complete on every rank)
+    {
+      static const int64_t dist_min = [] {
+        const char* e = std::getenv("LMFAO_DIST_CELLS");
+        return e ? std::atoll(e) : ((int64_t)1 << 16);
+      }();
+      gp.dist = c->world > 1 && cells >= dist_min;
+      gp.ncells_alloc = gp.dist ? (cells + c->world - 1) / c->world * c->world : cells;
+      owner_range(cells, c->rank, c->world, gp.cell_lo, gp.cell_hi);
+      if (!gp.dist) gp.cell_lo = 0, gp.cell_hi = cells;
+    }
     {
       StreamScope ts(st, !(plain_sites & 1));
-      CTX_CUDA(c, gp.table.alloc(cells * std::max(gp.nudaf, 1) * 8), "plan group table");
-      CTX_CUDA(c, gp.counts.alloc(cells * 8), "plan group counts");
+      CTX_CUDA(c, gp.table.alloc(gp.ncells_alloc * std::max(gp.nudaf, 1) * 8), "plan group table");
+      CTX_CUDA(c, gp.counts.alloc(gp.ncells_alloc * 8), "plan group counts");
+      CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "plan group table");
+      CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "plan group counts");
     }
     CTX_CUDA(c, gp.prog.upload(gprogs[c->query_slot[q]], st), "plan upload group");
   }
@@ -1062,7 +1114,8 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
                "run groups at a child");
     }
   }
-  // combine across GPUs (domain parallelism)
+  // combine across GPUs (domain parallelism): small outputs all-reduced, distributed
+  // tables reduce-scattered by cell range (sparse cuboids were exchanged by their fast path)
   if (c->world > 1) {
     int e = 0;
     cudaEvent_t ca = nullptr, cb = nullptr;
@@ -1071,20 +1124,29 @@ static lmfao_status run_body(lmfao_ctx* c, cudaStream_t st) {
       cudaEventCreate(&cb);
       cudaEventRecord(ca, st);
     }
+    Comm& cm = *c->comm;
     if (!c->scalar_queries.empty()) {
-      e |= nccl_allreduce_f64(c->comm, c->scalar_out.as<double>(), c->scalar_prog.nout, st);
-      e |= nccl_allreduce_u64(c->comm, c->scalar_count.as<unsigned long long>(), 1, st);
+      e = e ? e : cm.allreduce_sum(c->scalar_out.p, c->scalar_prog.nout, COMM_F64, st);
+      e = e ? e : cm.allreduce_sum(c->scalar_count.p, 1, COMM_U64, st);
     }
     for (auto& gp : c->groups) {
-      e |= nccl_allreduce_f64(c->comm, gp.table.as<double>(), gp.ncells * gp.nudaf, st);
-      e |= nccl_allreduce_u64(c->comm, gp.counts.as<unsigned long long>(), gp.ncells, st);
+      if (gp.direct) continue;
+      if (gp.dist) {
+        const size_t chunk = (size_t)(gp.ncells_alloc / c->world);
+        e = e ? e : cm.reduce_scatter_sum(gp.table.p, chunk * gp.nudaf, COMM_F64, st);
+        e = e ? e : cm.reduce_scatter_sum(gp.counts.p, chunk, COMM_U64, st);
+      } else {
+        e = e ? e : cm.allreduce_sum(gp.table.p, gp.ncells * gp.nudaf, COMM_F64, st);
+        e = e ? e : cm.allreduce_sum(gp.counts.p, gp.ncells, COMM_U64, st);
+      }
     }
     if (ca) {
       cudaEventRecord(cb, st);
       c->coll_events.push_back({ca, cb});
     }
-    if (e) return fail(c, LMFAO_ERR_NCCL, "NCCL all-reduce failed: %s", nccl_error(e));
+    if (e) return fail(c, LMFAO_ERR_NCCL, "%s collective failed: %s", cm.backend(), cm.error_string(e).c_str());
   }
+  for (auto& gp : c->groups) gp.gathered = false;
   for (auto& gp : c->groups) gp.compacted = false;
   c->ran = true;
   c->launches_last_run = launches_counter_reset();
@@ -1128,8 +1190,14 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   cudaSetDevice(c->device);
   StreamScope scope_(c->stream);
   cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
+  if (c->comm)
+    if (int e = c->comm->async_error())
+      return fail(c, LMFAO_ERR_NCCL, "%s asynchronous error: %s", c->comm->backend(), c->comm->error_string(e).c_str());
   const char* ng = std::getenv("LMFAO_NO_GRAPH");
-  bool use_graph = !c->prof && c->world == 1 && !(ng && ng[0] == '1') && !(c->fast && !c->fast->graph_ok());
+  // CUDA Graph: one capture of the whole run, NCCL collectives included (a loopback group
+  // synchronises the host between phases and stays eager)
+  bool use_graph = !c->prof && (c->world == 1 || c->comm->capturable()) && !(ng && ng[0] == '1') &&
+                   !(c->fast && !c->fast->graph_ok());
   if (!use_graph || c->graph_runs == 0) {
     c->graph_runs++;
     return run_body(c, st);
@@ -1159,7 +1227,7 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
     c->graph_launches = c->launches_last_run;
   }
   CTX_CUDA(c, cudaGraphLaunch(c->graph_exec, st), "graph launch");
-  for (auto& gp : c->groups) gp.compacted = false;
+  for (auto& gp : c->groups) gp.compacted = gp.gathered = false;
   c->launches_last_run = c->graph_launches;
   c->graph_runs++;
   return LMFAO_OK;
@@ -1167,12 +1235,31 @@ extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
 
 namespace {
 lmfao_status ensure_compacted(lmfao_ctx* c, GroupPlan& gp) {
-  if (gp.compacted || gp.direct) return LMFAO_OK;
+  if (gp.compacted) return LMFAO_OK;
   CTX_CUDA(c, cudaStreamSynchronize(c->stream), "sync");
   CTX_CUDA(c, cudaDeviceSynchronize(), "sync");
-  CTX_CUDA(c, launch_compact(gp.table.as<double>(), gp.counts.as<unsigned long long>(), gp.ncells, gp.nudaf, gp.d,
-                             gp.rkeys, gp.rvals, gp.rcnts, gp.ngroups, c->stream),
-           "compaction");
+  if (c->comm)
+    if (int e = c->comm->async_error())
+      return fail(c, LMFAO_ERR_NCCL, "%s asynchronous error: %s", c->comm->backend(), c->comm->error_string(e).c_str());
+  if (gp.direct) {  // written by a fast path; the group count on the device
+    if (gp.ngroups_on_device) {
+      unsigned long long n = 0;
+      CTX_CUDA(c, cudaMemcpy(&n, gp.ngroups_dev.p, 8, cudaMemcpyDeviceToHost), "group count");
+      gp.ngroups = (int64_t)n;
+    }
+    gp.compacted = true;
+    return LMFAO_OK;
+  }
+  DecodeArgs d = gp.d;  // this rank's range of the cells (all of them unless distributed)
+  d.cell0 = gp.cell_lo;
+  const int64_t n = gp.cell_hi - gp.cell_lo;
+  if (n <= 0) {
+    gp.ngroups = 0;
+  } else {
+    CTX_CUDA(c, launch_compact(gp.table.as<double>() + gp.cell_lo * gp.nudaf, gp.counts.as<unsigned long long>() + gp.cell_lo,
+                               n, gp.nudaf, d, gp.rkeys, gp.rvals, gp.rcnts, gp.ngroups, c->stream),
+             "compaction");
+  }
   gp.compacted = true;
   return LMFAO_OK;
 }
@@ -1195,7 +1282,7 @@ extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_g
   GroupPlan& gp = c->groups[c->query_slot[q]];
   lmfao_status s = ensure_compacted(c, gp);
   if (s != LMFAO_OK) return s;
-  if (n_groups) *n_groups = gp.ngroups;
+  if (n_groups) *n_groups = gp.gathered ? gp.gngroups : gp.ngroups;
   return LMFAO_OK;
 }
 
@@ -1216,9 +1303,9 @@ extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32
   GroupPlan& gp = c->groups[c->query_slot[q]];
   lmfao_status s = ensure_compacted(c, gp);
   if (s != LMFAO_OK) return s;
-  if (keys) *keys = gp.rkeys.as<int32_t>();
-  if (vals) *vals = gp.rvals.as<double>();
-  if (counts) *counts = (const uint64_t*)gp.rcnts.p;
+  if (keys) *keys = (gp.gathered ? gp.gkeys : gp.rkeys).as<int32_t>();
+  if (vals) *vals = (gp.gathered ? gp.gvals : gp.rvals).as<double>();
+  if (counts) *counts = (const uint64_t*)(gp.gathered ? gp.gcnts : gp.rcnts).p;
   return LMFAO_OK;
 }
 
@@ -1244,6 +1331,74 @@ extern "C" lmfao_status lmfao_fetch(lmfao_ctx* c, int32_t q, int32_t* keys_out, 
   return LMFAO_OK;
 }
 
+// Collective (every rank calls it with the same arguments).  A distributed output holds one
+// range of cells per rank, the ranges ascending with the rank, so the full table in canonical
+// order is the ranks' groups concatenated in rank order: every rank sends its compacted groups to
+// root_rank (counts first, all-gathered), which keeps the result next to its own range.
+extern "C" lmfao_status lmfao_gather_result(lmfao_ctx* c, int32_t q, int32_t root_rank) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
+  if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
+  if (root_rank < 0 || root_rank >= c->world) return fail(c, LMFAO_ERR_INVALID_ARG, "bad root rank");
+  if (c->world == 1 || c->query_kind[q] == 0) return LMFAO_OK;  // complete on every rank
+  cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
+  GroupPlan& gp = c->groups[c->query_slot[q]];
+  if (!gp.dist && !gp.direct) return LMFAO_OK;  // all-reduced: complete on every rank
+  lmfao_status s = ensure_compacted(c, gp);
+  if (s != LMFAO_OK) return s;
+  Comm& cm = *c->comm;
+  cudaStream_t st = c->stream;
+  const int G = c->world, ngb = gp.d.ngb, nu = gp.nudaf;
+  DevBuf cnt;
+  CTX_CUDA(c, cnt.alloc(8 * (G + 1)), "gather");
+  unsigned long long mine = (unsigned long long)gp.ngroups;
+  CTX_CUDA(c, cudaMemcpyAsync(cnt.as<unsigned long long>() + G, &mine, 8, cudaMemcpyHostToDevice, st), "gather");
+  int e = cm.allgather(cnt.as<unsigned long long>() + G, cnt.p, 8, st);
+  if (e) return fail(c, LMFAO_ERR_NCCL, "gather counts: %s", cm.error_string(e).c_str());
+  std::vector<unsigned long long> n(G);
+  CTX_CUDA(c, cudaMemcpyAsync(n.data(), cnt.p, 8 * G, cudaMemcpyDeviceToHost, st), "gather");
+  CTX_CUDA(c, cudaStreamSynchronize(st), "gather");
+  std::vector<int64_t> off(G + 1, 0);
+  for (int r = 0; r < G; r++) off[r + 1] = off[r] + (int64_t)n[r];
+  const int64_t tot = off[G];
+  const bool root = c->rank == root_rank;
+  if (root) {
+    CTX_CUDA(c, gp.gkeys.alloc(std::max<int64_t>(tot * ngb * 4, 16)), "gather");
+    CTX_CUDA(c, gp.gvals.alloc(std::max<int64_t>(tot * nu * 8, 16)), "gather");
+    CTX_CUDA(c, gp.gcnts.alloc(std::max<int64_t>(tot * 8, 16)), "gather");
+    const int64_t o = off[c->rank], m = (int64_t)n[c->rank];
+    if (m > 0) {
+      if (ngb) CTX_CUDA(c, cudaMemcpyAsync(gp.gkeys.as<int32_t>() + o * ngb, gp.rkeys.p, m * ngb * 4, cudaMemcpyDeviceToDevice, st), "gather");
+      if (nu) CTX_CUDA(c, cudaMemcpyAsync(gp.gvals.as<double>() + o * nu, gp.rvals.p, m * nu * 8, cudaMemcpyDeviceToDevice, st), "gather");
+      CTX_CUDA(c, cudaMemcpyAsync(gp.gcnts.as<unsigned long long>() + o, gp.rcnts.p, m * 8, cudaMemcpyDeviceToDevice, st), "gather");
+    }
+  }
+  e = cm.group_start();
+  for (int r = 0; r < G && !e; r++) {
+    if (r == root_rank) continue;
+    const int64_t m = (int64_t)n[r];
+    if (root) {
+      e = e ? e : cm.recv(gp.gkeys.as<int32_t>() + off[r] * ngb, m * ngb * 4, r, st);
+      e = e ? e : cm.recv(gp.gvals.as<double>() + off[r] * nu, m * nu * 8, r, st);
+      e = e ? e : cm.recv(gp.gcnts.as<unsigned long long>() + off[r], m * 8, r, st);
+    } else if (r == c->rank) {
+      e = e ? e : cm.send(gp.rkeys.p, m * ngb * 4, root_rank, st);
+      e = e ? e : cm.send(gp.rvals.p, m * nu * 8, root_rank, st);
+      e = e ? e : cm.send(gp.rcnts.p, m * 8, root_rank, st);
+    }
+  }
+  const int e2 = cm.group_end(st);
+  e = e ? e : e2;
+  if (e) return fail(c, LMFAO_ERR_NCCL, "gather: %s", cm.error_string(e).c_str());
+  CTX_CUDA(c, cudaStreamSynchronize(st), "gather");
+  if (root) {
+    gp.gngroups = tot;
+    gp.gathered = true;
+  }
+  return LMFAO_OK;
+}
+
 extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   if (!c || !out || cap <= 0) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "plan_info needs plan");
@@ -1264,9 +1419,24 @@ extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   o << "], \"scalar_outputs\": " << c->scalar_prog.nout << ", \"group_queries\": " << c->groups.size();
   o << ", \"fast_path\": " << (c->fast ? c->fast->describe() : std::string("null"));
   o << ", \"launches_last_run\": " << c->launches_last_run;
-  if (c->coll_n > 0) {  // profiled multi-GPU runs: the all-reduce of the partial results
+  o << ", \"world\": " << c->world << ", \"rank\": " << c->rank
+    << ", \"comm\": \"" << (c->comm ? c->comm->backend() : "none") << "\", \"outputs\": [";
+  for (size_t q = 0; q < c->queries.size(); q++) {  // where each query's result lives
+    const char* where = "replicated";
+    int64_t lo = 0, hi = 1;
+    if (c->query_kind[q] == 1) {
+      const GroupPlan& gp = c->groups[c->query_slot[q]];
+      hi = gp.ncells;
+      if (c->world > 1 && gp.direct) where = "exchanged", lo = gp.cell_lo, hi = gp.cell_hi;
+      else if (gp.dist) where = "reduce_scattered", lo = gp.cell_lo, hi = gp.cell_hi;
+    }
+    o << (q ? ", " : "") << "{\"placement\": \"" << where << "\", \"cells\": [" << lo << ", " << hi << "]}";
+  }
+  o << "]";
+  if (c->coll_n > 0) {  // profiled multi-GPU runs: the collectives of the partial results
     int64_t bytes = c->scalar_queries.empty() ? 0 : (int64_t)c->scalar_prog.nout * 8 + 8;
-    for (auto& gp : c->groups) bytes += gp.ncells * (gp.nudaf * 8 + 8);
+    for (auto& gp : c->groups)
+      if (!gp.direct) bytes += gp.ncells_alloc * (gp.nudaf * 8 + 8);
     o << ", \"collective_ms\": " << c->coll_ms / c->coll_n << ", \"collective_bytes\": " << bytes;
   }
   o << "}";

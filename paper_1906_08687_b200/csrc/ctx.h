@@ -2,6 +2,7 @@
 #pragma once
 #include <tuple>
 
+#include "comm.h"
 #include "internal.h"
 #include "paths.h"
 
@@ -125,6 +126,17 @@ struct GroupPlan {
   DevBuf rkeys, rvals, rcnts;
   DevBuf countcoef;
   int64_t ngroups = 0;
+  DevBuf ngroups_dev;              // direct outputs: the group count, written on the device
+  bool ngroups_on_device = false;
+  // world > 1: a distributed output — dense tables reduce-scattered (each rank keeps the sums of
+  // its own range of cells), sparse cuboids exchanged by cell owner — holds only [cell_lo,
+  // cell_hi) on this rank until lmfao_gather_result assembles it on one rank
+  bool dist = false;
+  int64_t ncells_alloc = 0;        // cells of the dense table (a multiple of world when dist)
+  int64_t cell_lo = 0, cell_hi = 0;
+  bool gathered = false;
+  DevBuf gkeys, gvals, gcnts;      // the gathered full table (gather_result's root)
+  int64_t gngroups = 0;
   int rev = -1;  // index into lmfao_ctx::revs: finished at a non-unique-keyed root child
 };
 
@@ -146,7 +158,8 @@ struct lmfao_ctx {
   int shard_part = 0, shard_nparts = 1;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // deferred host->device column copies (prepare)
-  void* comm = nullptr;
+  std::unique_ptr<Comm> comm;  // world > 1: NCCL, or an in-process loopback group (tests)
+  int64_t root_rows_global = 0;  // the root's rows before sharding
   std::string err;
   State state = S_CREATED;
   std::vector<Rel> rels;

@@ -18,6 +18,7 @@
 #include <map>
 #include <set>
 
+#include "comm.h"
 #include "ctx.h"
 
 namespace lmfao {
@@ -302,19 +303,104 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
   }
 }
 
-// sorted records of a sparse cuboid -> its groups in canonical (ascending cell) order
-__global__ void k_rec_heads(const unsigned* __restrict__ key, int64_t n, uint32_t* __restrict__ head) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    head[i] = (i == 0 || key[i] != key[i - 1]) ? 1u : 0u;
+// ---- sparse cuboids: run records -> sorted -> reduced groups, sizes on the device only
+//
+// World > 1: the cells are owned by the ranks in contiguous ranges
+// (owner_range); each rank reduces its own records, and the reduce kernel writes every local
+// group straight into its owner's receive buffer in peer memory (NVLink P2P stores, slot by a
+// remote atomic on the owner's counter) — compute and exchange fused, no host round trip — then
+// the owner sorts and reduces what it received: its range of the output, in canonical order.
+// Two receive buffers (by run parity) and epoch flags order successive runs: a sender waits
+// until the owner released the buffer of its parity, the owner until every sender signalled.
+struct XHdr {                  // a rank's exchange header (mapped by every rank)
+  unsigned long long cnt[2];   // records received, per run parity
+  unsigned long long done[2];  // senders finished (cumulative over the runs of that parity)
+  long long freed[2];          // the parity's buffer may be written by runs >= freed[b]
+  long long epoch;             // runs started (identical on every rank: runs are collective)
+  int err;                     // a wait timed out / a buffer overflowed
+  int pad_;
+};
+static_assert(sizeof(XHdr) == 64, "exchange header layout");
+struct XArgs {
+  XHdr* const* hdr;            // [world] every rank's header
+  unsigned* const* keys;       // [world] every rank's keys [2][capr]
+  double* const* vals;         // [world] every rank's vals [2][capr][M1]
+  long long capr;
+  long long chunk;             // owner of a cell: cell / chunk
+  int rank, world;
+};
+__device__ __forceinline__ long long x_epoch(const XHdr* h) { return *(volatile const long long*)&h->epoch - 1; }
+__device__ bool x_spin(const volatile long long* p, long long target, XHdr* own) {  // *p >= target, 60 s at most
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (*p < target) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 60ull * 1000000000ull) {
+      atomicExch(&own->err, 1);
+      return false;
+    }
+    __nanosleep(200);
+  }
+  return true;
+}
+__global__ void k_x_begin(XArgs x) {  // a new run; wait until every owner released this parity
+  XHdr* own = x.hdr[x.rank];
+  own->epoch += 1;
+  __threadfence_system();
+  const long long e = own->epoch - 1;
+  for (int p = 0; p < x.world; p++) x_spin(&x.hdr[p]->freed[e & 1], e, own);
+  __threadfence_system();
+}
+__global__ void k_x_signal(XArgs x) {  // this rank's groups are all in their owners' buffers
+  const long long e = x_epoch(x.hdr[x.rank]);
+  __threadfence_system();
+  for (int p = 0; p < x.world; p++) atomicAdd(&x.hdr[p]->done[e & 1], 1ull);
+}
+__global__ void k_x_wait(XArgs x, unsigned long long* nrecv) {  // every sender of this run has signalled
+  XHdr* own = x.hdr[x.rank];
+  const long long e = x_epoch(own);
+  const int b = (int)(e & 1);
+  x_spin((const volatile long long*)&own->done[b], (long long)x.world * ((e >> 1) + 1), own);
+  __threadfence_system();
+  *nrecv = min(*(volatile unsigned long long*)&own->cnt[b], (unsigned long long)x.capr);
+}
+__global__ void k_x_take(XArgs x, const unsigned long long* nrecv, unsigned* __restrict__ rkey,
+                         uint32_t* __restrict__ perm) {
+  const long long n = (long long)*nrecv;
+  const unsigned* src = x.keys[x.rank] + (size_t)(x_epoch(x.hdr[x.rank]) & 1) * x.capr;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    rkey[i] = src[i];
+    perm[i] = (uint32_t)i;
+  }
+}
+__global__ void k_x_release(XArgs x) {  // the received records are consumed: free the parity
+  XHdr* own = x.hdr[x.rank];
+  const long long e = x_epoch(own);
+  own->cnt[e & 1] = 0;
+  __threadfence_system();
+  *(volatile long long*)&own->freed[e & 1] = e + 2;
+}
+
+__global__ void k_rec_heads(const unsigned* __restrict__ key, int64_t cap, const unsigned long long* n_dev,
+                            uint32_t* __restrict__ head) {
+  const int64_t n = min(cap, (int64_t)*n_dev);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i < n && (i == 0 || key[i] != key[i - 1])) ? 1u : 0u;
+}
+__global__ void k_rec_ngroups(const uint32_t* head, const uint32_t* excl, const unsigned long long* n_dev,
+                              int64_t cap, unsigned long long* ngroups) {
+  const int64_t n = min(cap, (int64_t)*n_dev);
+  *ngroups = n > 0 ? (unsigned long long)excl[n - 1] + head[n - 1] : 0ull;
 }
 struct RecReduce {
   const unsigned* key;
   const uint32_t* perm;
   const uint32_t* head;
   const uint32_t* excl;
-  const double* rval;
+  const double* rval;  // records' sums [.][M1] (merge: the own receive buffer, both parities)
   long long rcap;
-  int64_t n;
+  int64_t cap;
+  const unsigned long long* n_dev;
   int M1, nudaf;
   const double* coef;  // [nudaf][M1]
   DecodeArgs d;
@@ -323,6 +409,9 @@ struct RecReduce {
   unsigned long long* ocnts;
   int nder;
   const struct Rollup* der;
+  int send;            // world > 1, local groups: to their owners (x), not decoded
+  int merge;           // world > 1, received groups: rval = own vals, parity from the epoch
+  XArgs x;
 };
 // A dense cuboid X at the sparse cuboid Y's level whose attributes are a subset of Y's: its
 // cells are sums of Y's groups (X = Σ over Y's other attributes), added per reduced group of Y
@@ -337,29 +426,44 @@ struct Rollup {
   unsigned long long cmask;
 };
 __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r.n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t n = min(r.cap, (int64_t)*r.n_dev);
+  const double* rval = r.rval;
+  int b = 0;
+  if (r.send || r.merge) b = (int)(x_epoch(r.x.hdr[r.x.rank]) & 1);
+  if (r.merge) rval += (size_t)b * r.x.capr * r.M1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (!r.head[i]) continue;
     double S[CB_MEAS + 1];
     for (int j = 0; j < r.M1; j++) S[j] = 0.0;
     int64_t t = i;
     do {
       const uint32_t p = r.perm[t];
-      for (int j = 0; j < r.M1; j++) S[j] += r.rval[(int64_t)p * r.M1 + j];
+      for (int j = 0; j < r.M1; j++) S[j] += rval[(int64_t)p * r.M1 + j];
       t++;
-    } while (t < r.n && !r.head[t]);
-    const int64_t g = r.excl[i];
+    } while (t < n && !r.head[t]);
     const unsigned cell = r.key[i];  // sparse cuboids have < 2^32 cells: 32-bit decode
     unsigned code[CB_GB];
-    for (int a = 0; a < r.d.ngb; a++) {
-      code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
-      r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
+    for (int a = 0; a < r.d.ngb; a++) code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
+    if (r.send) {  // fused exchange: the group goes straight to its owner's buffer (peer memory)
+      const int o = (int)(cell / (unsigned long long)r.x.chunk);
+      const unsigned long long slot = atomicAdd(&r.x.hdr[o]->cnt[b], 1ull);
+      if (slot < (unsigned long long)r.x.capr) {
+        const size_t at = (size_t)b * r.x.capr + slot;
+        r.x.keys[o][at] = cell;
+        for (int j = 0; j < r.M1; j++) r.x.vals[o][at * r.M1 + j] = S[j];
+      } else {
+        atomicExch(&r.x.hdr[r.x.rank]->err, 2);
+      }
+    } else {
+      const int64_t g = r.excl[i];
+      for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
+      for (int u = 0; u < r.nudaf; u++) {
+        double v = 0.0;
+        for (int j = 0; j < r.M1; j++) v = fma(r.coef[u * r.M1 + j], S[j], v);
+        r.ovals[g * r.nudaf + u] = v;
+      }
+      r.ocnts[g] = (unsigned long long)S[0];
     }
-    for (int u = 0; u < r.nudaf; u++) {
-      double v = 0.0;
-      for (int j = 0; j < r.M1; j++) v = fma(r.coef[u * r.M1 + j], S[j], v);
-      r.ovals[g * r.nudaf + u] = v;
-    }
-    r.ocnts[g] = (unsigned long long)S[0];
     for (int x = 0; x < r.nder; x++) {
       const Rollup& X = r.der[x];
       long long xc = 0;
@@ -375,12 +479,30 @@ __global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
   }
 }
 
+// exchange buffer layout: [XHdr | keys [2][capr] (u32) | vals [2][capr][M1] (f64)]
+inline size_t xoff_keys() { return 256; }
+inline size_t xoff_vals(long long capr) { return (256 + (size_t)2 * capr * 4 + 255) / 256 * 256; }
+inline size_t xbytes(long long capr, int M1) { return xoff_vals(capr) + (size_t)2 * capr * M1 * 8; }
+
 struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
   int gi = -1, coff = 0, bits = 1;
   long long cap = 0;
   DevBuf key, val, n, perm, head, excl;
   std::vector<Rollup> der;  // dense cuboids rolled up from this one's groups
   DevBuf dder;
+  // world > 1: the exchange
+  long long capr = 0;
+  DevBuf xbuf;                 // [XHdr | keys [2][capr] | vals [2][capr][M1]], mapped by every rank
+  std::vector<void*> peers;    // every rank's xbuf
+  DevBuf xptrs;                // [3][world] device pointers: headers, keys, vals
+  DevBuf rkey, rperm, rhead, rexcl, nrecv;
+  XArgs x{};
+  Comm* comm = nullptr;
+  SparseOut() = default;
+  SparseOut(SparseOut&&) = default;
+  ~SparseOut() {
+    if (comm && !peers.empty()) comm->unmap_peers(peers);
+  }
 };
 
 struct FastCube : FastPaths {
@@ -391,7 +513,7 @@ struct FastCube : FastPaths {
   std::vector<SparseOut> sparse;
   int nq = 0, grid = 148;
   size_t smem = 0;
-  bool graph_ok() const override { return sparse.empty(); }
+  bool graph_ok() const override { return true; }  // device-side sizes: no host synchronisation
   std::string describe() const override {
     char b[160];
     int m = 0;
@@ -427,52 +549,80 @@ struct FastCube : FastPaths {
     for (auto& sp : sparse) CUDA_TRY(finish_sparse(c, sp, st));
     return cudaSuccess;
   }
-  // sort the records by cell, reduce equal cells, decode: the groups in canonical order
+  // sort the records by cell, reduce equal cells: the groups in canonical order (world 1), or,
+  // world > 1, every local group to its owner (peer memory) and the owner's merge of what it
+  // received.  Sizes stay on the device (record count, groups): no host synchronisation.
   cudaError_t finish_sparse(lmfao_ctx* c, SparseOut& sp, cudaStream_t st) {
     GroupPlan& gp = c->groups[sp.gi];
-    unsigned long long n = 0;
-    CUDA_TRY(cudaMemcpyAsync(&n, sp.n.p, 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    if ((long long)n > sp.cap) return cudaErrorIllegalAddress;  // cannot happen: records <= runs + chunks
-    gp.ngroups = 0;
-    if (n > 0) {
-      CUDA_TRY(iota_u32(sp.perm.as<uint32_t>(), (int64_t)n, st));
-      CUDA_TRY(radix_sort_pairs(sp.key.as<uint32_t>(), sp.perm.as<uint32_t>(), (int64_t)n, sp.bits, st));
-      k_rec_heads<<<cgrid((int64_t)n), 256, 0, st>>>(sp.key.as<unsigned>(), (int64_t)n, sp.head.as<uint32_t>());
-      CUDA_TRY(exclusive_scan_u32(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), (int64_t)n, st));
-      uint32_t le = 0, lf = 0;
-      CUDA_TRY(cudaMemcpyAsync(&le, sp.excl.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaMemcpyAsync(&lf, sp.head.as<uint32_t>() + n - 1, 4, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      gp.ngroups = (int64_t)le + lf;
+    const bool dist = c->world > 1;
+    if (dist) {
+      k_x_begin<<<1, 1, 0, st>>>(sp.x);
+      launches_add(1);
     }
-    const int64_t ng = gp.ngroups;
-    if (gp.rkeys.bytes < (size_t)std::max<int64_t>(ng * gp.d.ngb * 4, 16)) CUDA_TRY(gp.rkeys.alloc(ng * gp.d.ngb * 4));
-    if (gp.rvals.bytes < (size_t)std::max<int64_t>(ng * gp.nudaf * 8, 16)) CUDA_TRY(gp.rvals.alloc(ng * gp.nudaf * 8));
-    if (gp.rcnts.bytes < (size_t)std::max<int64_t>(ng * 8, 16)) CUDA_TRY(gp.rcnts.alloc(ng * 8));
-    if (n > 0) {
-      RecReduce r{};
-      r.key = sp.key.as<unsigned>();
-      r.perm = sp.perm.as<uint32_t>();
-      r.head = sp.head.as<uint32_t>();
-      r.excl = sp.excl.as<uint32_t>();
-      r.rval = sp.val.as<double>();
-      r.rcap = sp.cap;
-      r.n = (int64_t)n;
-      r.M1 = ca.M + 1;
-      r.nudaf = gp.nudaf;
-      r.coef = dcoef.as<double>() + sp.coff;
-      r.d = gp.d;
-      r.okeys = gp.rkeys.as<int32_t>();
-      r.ovals = gp.rvals.as<double>();
-      r.ocnts = gp.rcnts.as<unsigned long long>();
-      r.nder = (int)sp.der.size();
-      r.der = sp.dder.as<Rollup>();
-      k_rec_reduce<<<cgrid((int64_t)n), 256, 0, st>>>(r);
-      launches_add(3);
-      CUDA_TRY(cudaGetLastError());
+    const int64_t cap = sp.cap;
+    CUDA_TRY(iota_u32(sp.perm.as<uint32_t>(), cap, st));
+    CUDA_TRY(radix_sort_pairs(sp.key.as<uint32_t>(), sp.perm.as<uint32_t>(), cap, sp.bits, st,
+                              sp.n.as<unsigned long long>()));
+    k_rec_heads<<<cgrid(cap), 256, 0, st>>>(sp.key.as<unsigned>(), cap, sp.n.as<unsigned long long>(),
+                                            sp.head.as<uint32_t>());
+    CUDA_TRY(exclusive_scan_u32(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), cap, st));
+    RecReduce r{};
+    r.key = sp.key.as<unsigned>();
+    r.perm = sp.perm.as<uint32_t>();
+    r.head = sp.head.as<uint32_t>();
+    r.excl = sp.excl.as<uint32_t>();
+    r.rval = sp.val.as<double>();
+    r.rcap = sp.cap;
+    r.cap = cap;
+    r.n_dev = sp.n.as<unsigned long long>();
+    r.M1 = ca.M + 1;
+    r.nudaf = gp.nudaf;
+    r.coef = dcoef.as<double>() + sp.coff;
+    r.d = gp.d;
+    r.okeys = gp.rkeys.as<int32_t>();
+    r.ovals = gp.rvals.as<double>();
+    r.ocnts = gp.rcnts.as<unsigned long long>();
+    r.nder = (int)sp.der.size();
+    r.der = sp.dder.as<Rollup>();
+    r.send = dist;
+    r.x = sp.x;
+    k_rec_reduce<<<cgrid(cap), 256, 0, st>>>(r);
+    launches_add(5);
+    CUDA_TRY(cudaGetLastError());
+    if (!dist) {
+      k_rec_ngroups<<<1, 1, 0, st>>>(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), sp.n.as<unsigned long long>(), cap,
+                                     gp.ngroups_dev.as<unsigned long long>());
+      launches_add(1);
+      return cudaGetLastError();
     }
-    return cudaSuccess;
+    // world > 1: signal the owners, then merge what this rank received
+    k_x_signal<<<1, 1, 0, st>>>(sp.x);
+    if (c->comm->phase(st)) return cudaErrorUnknown;  // loopback: every rank has sent
+    const int64_t capr = sp.capr;
+    unsigned long long* nrecv = sp.nrecv.as<unsigned long long>();
+    k_x_wait<<<1, 1, 0, st>>>(sp.x, nrecv);
+    k_x_take<<<cgrid(capr), 256, 0, st>>>(sp.x, nrecv, sp.rkey.as<unsigned>(), sp.rperm.as<uint32_t>());
+    CUDA_TRY(radix_sort_pairs(sp.rkey.as<uint32_t>(), sp.rperm.as<uint32_t>(), capr, sp.bits, st, nrecv));
+    k_rec_heads<<<cgrid(capr), 256, 0, st>>>(sp.rkey.as<unsigned>(), capr, nrecv, sp.rhead.as<uint32_t>());
+    CUDA_TRY(exclusive_scan_u32(sp.rhead.as<uint32_t>(), sp.rexcl.as<uint32_t>(), capr, st));
+    RecReduce m = r;
+    m.key = sp.rkey.as<unsigned>();
+    m.perm = sp.rperm.as<uint32_t>();
+    m.head = sp.rhead.as<uint32_t>();
+    m.excl = sp.rexcl.as<uint32_t>();
+    m.rval = reinterpret_cast<const double*>(sp.xbuf.as<char>() + xoff_vals(sp.capr));
+    m.rcap = capr;
+    m.cap = capr;
+    m.n_dev = nrecv;
+    m.nder = 0;  // the rollups were added from the local groups
+    m.send = 0;
+    m.merge = 1;
+    k_rec_reduce<<<cgrid(capr), 256, 0, st>>>(m);
+    k_rec_ngroups<<<1, 1, 0, st>>>(sp.rhead.as<uint32_t>(), sp.rexcl.as<uint32_t>(), nrecv, capr,
+                                   gp.ngroups_dev.as<unsigned long long>());
+    k_x_release<<<1, 1, 0, st>>>(sp.x);
+    launches_add(9);
+    return cudaGetLastError();
   }
 };
 
@@ -602,7 +752,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   // cuboids with more cells than 2^25 (C5's {A,B,C}: 5·10^8) keep no dense table: their
   // run records are sorted and reduced after the scan (single GPU; LMFAO_CUBE_DENSE=1: off)
   const char* dn = std::getenv("LMFAO_CUBE_DENSE");
-  const bool allow_sparse = c->world == 1 && nparts == 1 && !(dn && dn[0] == '1');
+  const bool allow_sparse = nparts == 1 && !(dn && dn[0] == '1') && (c->world == 1 || c->comm);
   const int64_t nrows = R.nrows, nchunks = (nrows + a.chunk - 1) / a.chunk;
   const char* smin = std::getenv("LMFAO_CUBE_SPARSE_CELLS");  // tests: lower the threshold
   const int64_t sparse_min = smin ? std::atoll(smin) : ((int64_t)1 << 25);
@@ -622,8 +772,53 @@ FastPaths* plan_cube(lmfao_ctx* c) {
     sp.cap = nrows + nchunks + 64;
     while (sp.bits < 32 && ((int64_t)1 << sp.bits) < gp.ncells) sp.bits++;
     if (sp.key.alloc(sp.cap * 4) || sp.val.alloc((size_t)sp.cap * M1 * 8) || sp.n.alloc(8) || sp.perm.alloc(sp.cap * 4) ||
-        sp.head.alloc(sp.cap * 4) || sp.excl.alloc(sp.cap * 4))
+        sp.head.alloc(sp.cap * 4) || sp.excl.alloc(sp.cap * 4) || gp.ngroups_dev.alloc(8))
       return nullptr;
+    int64_t ocap = std::min<int64_t>(sp.cap, gp.ncells);  // groups this rank outputs
+    if (c->world > 1) {
+      // receive capacity: every rank's groups are distinct cells, so at most world x (own
+      // cells), and at most the records of the whole root
+      const int64_t G = c->world, chunk = (gp.ncells + G - 1) / G;
+      const int64_t nch_all = (c->root_rows_global + a.chunk - 1) / a.chunk;
+      sp.capr = std::min<int64_t>(c->root_rows_global + G * (nch_all + 64), G * chunk);
+      ocap = std::min<int64_t>(sp.capr, chunk);
+      {
+        StreamScope plain(nullptr, false);  // CUDA IPC needs cudaMalloc memory (not the stream-ordered pool)
+        if (sp.xbuf.alloc(xbytes(sp.capr, M1))) return nullptr;
+      }
+      XHdr h{};
+      h.freed[0] = 0;
+      h.freed[1] = 1;
+      if (cudaMemsetAsync(sp.xbuf.p, 0, 256, c->stream) ||
+          cudaMemcpyAsync(sp.xbuf.p, &h, sizeof h, cudaMemcpyHostToDevice, c->stream) ||
+          cudaStreamSynchronize(c->stream))
+        return nullptr;
+      if (c->comm->map_peers(sp.xbuf.p, sp.peers, c->stream)) return nullptr;  // collective
+      std::vector<void*> ptr(3 * G);
+      for (int r = 0; r < G; r++) {
+        ptr[r] = sp.peers[r];
+        ptr[G + r] = (char*)sp.peers[r] + xoff_keys();
+        ptr[2 * G + r] = (char*)sp.peers[r] + xoff_vals(sp.capr);
+      }
+      if (sp.xptrs.alloc(ptr.size() * sizeof(void*)) ||
+          cudaMemcpyAsync(sp.xptrs.p, ptr.data(), ptr.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream))
+        return nullptr;
+      sp.x.hdr = (XHdr* const*)sp.xptrs.p;
+      sp.x.keys = (unsigned* const*)(sp.xptrs.as<void*>() + G);
+      sp.x.vals = (double* const*)(sp.xptrs.as<void*>() + 2 * G);
+      sp.x.capr = sp.capr;
+      sp.x.chunk = chunk;
+      sp.x.rank = c->rank;
+      sp.x.world = (int)G;
+      sp.comm = c->comm.get();
+      if (sp.rkey.alloc(sp.capr * 4) || sp.rperm.alloc(sp.capr * 4) || sp.rhead.alloc(sp.capr * 4) ||
+          sp.rexcl.alloc(sp.capr * 4) || sp.nrecv.alloc(8))
+        return nullptr;
+    }
+    if (gp.rkeys.alloc(std::max<int64_t>(ocap, 1) * gp.d.ngb * 4) || gp.rvals.alloc(std::max<int64_t>(ocap, 1) * gp.nudaf * 8) ||
+        gp.rcnts.alloc(std::max<int64_t>(ocap, 1) * 8))
+      return nullptr;
+    gp.ngroups_on_device = true;
     Cuboid& q = hq[k];
     q.sparse = 1;
     q.rkey = sp.key.as<unsigned>();

@@ -565,7 +565,7 @@ __global__ void k_scatter_groups(const double* __restrict__ table, const unsigne
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (!flags[i]) continue;
     int64_t g = excl[i];
-    for (int a = 0; a < d.ngb; a++) keys[g * d.ngb + a] = d.dict[a][(i / d.stride[a]) % d.radix[a]];
+    for (int a = 0; a < d.ngb; a++) keys[g * d.ngb + a] = d.dict[a][((i + d.cell0) / d.stride[a]) % d.radix[a]];
     for (int j = 0; j < nudaf; j++)
       vals[g * nudaf + j] = d.countcoef ? (isnan(d.countcoef[j]) ? table[i * nudaf + j] : d.countcoef[j] * (double)counts[i])
                                         : table[i * nudaf + j];

@@ -133,7 +133,8 @@ struct DevBuf {
 // ---- device primitives (prims.cu), all on stream st ----
 cudaError_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t st);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t st);
-cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st);
+cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st,
+                             const unsigned long long* n_dev = nullptr);
 cudaError_t iota_u32(uint32_t* a, int64_t n, cudaStream_t st);
 cudaError_t gather_bytes(const void* in, const uint32_t* perm, void* out, int64_t n, int elem_bytes, cudaStream_t st);
 cudaError_t dict_encode_i32(const int32_t* col, int64_t n, DevBuf& dict, int64_t& ndict, DevBuf* codes,
@@ -239,6 +240,7 @@ cudaError_t launch_rev(const NodeArgs& root, const int32_t* fkT, const ProgPtrs&
 // Compaction of a dense cell table: present cells (count > 0) in ascending order.
 struct DecodeArgs {
   int32_t ngb;
+  int64_t cell0;  // the table's first cell (a rank's range of a distributed table)
   const int32_t* dict[8];
   int64_t radix[8];
   int64_t stride[8];

@@ -20,9 +20,10 @@ constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 // Pass layout: hist[digit * nblocks + block] (digit-major) so one exclusive
 // scan over the whole array gives each (digit, block) its output offset and the
 // sort is stable across blocks.
-__global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, int shift, int bits,
-                             uint32_t* __restrict__ hist, int nblocks) {
+__global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, const unsigned long long* n_dev, int shift,
+                             int bits, uint32_t* __restrict__ hist, int nblocks) {
   __shared__ uint32_t h[256];
+  if (n_dev) n = min(n, (int64_t)*n_dev);  // device-side size (n = capacity)
   int nd = 1 << bits;
   for (int i = threadIdx.x; i < nd; i += blockDim.x) h[i] = 0;
   __syncthreads();
@@ -40,7 +41,9 @@ __global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, int s
 // (earlier chunks) + (earlier warps in this chunk) + (earlier lanes in warp).
 __global__ void k_radix_scatter(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                                 uint32_t* __restrict__ okeys, uint32_t* __restrict__ ovals, int64_t n,
-                                int shift, int bits, const uint32_t* __restrict__ offs, int nblocks) {
+                                const unsigned long long* n_dev, int shift, int bits,
+                                const uint32_t* __restrict__ offs, int nblocks) {
+  if (n_dev) n = min(n, (int64_t)*n_dev);
   __shared__ uint32_t base[256];
   __shared__ uint32_t wcnt[SORT_THREADS / 32][256];
   int nd = 1 << bits;
@@ -190,7 +193,10 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaS
   return exclusive_scan_t<int64_t>(in, out, n, st);
 }
 
-cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st) {
+// n_dev (optional): the number of pairs is *n_dev <= n, known on the device only (n is then the
+// capacity; launches are sized by it, so the sort needs no host synchronisation)
+cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_bits, cudaStream_t st,
+                             const unsigned long long* n_dev) {
   if (n <= 1 || key_bits <= 0) return cudaSuccess;
   int64_t nblocks = (n + SORT_TILE - 1) / SORT_TILE;
   uint32_t* k2 = (uint32_t*)g_arena.get(0, n * 4);
@@ -202,10 +208,11 @@ cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_
   int passes = 0;
   for (int shift = 0; shift < key_bits; shift += 8) {
     int bits = std::min(8, key_bits - shift);
-    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, shift, bits, hist, (int)nblocks);
+    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, n_dev, shift, bits, hist, (int)nblocks);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(exclusive_scan_t<uint32_t>(hist, offs, (int64_t)(1 << bits) * nblocks, st, 4));
-    k_radix_scatter<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, va, kb, vb, n, shift, bits, offs, (int)nblocks);
+    k_radix_scatter<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, va, kb, vb, n, n_dev, shift, bits, offs,
+                                                                 (int)nblocks);
     CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb);
     std::swap(va, vb);

@@ -68,6 +68,12 @@ _SIGS = {
     "lmfao_plan_info": [_P, ctypes.c_char_p, ctypes.c_int64],
     "lmfao_profile": [_P, ctypes.c_int],
     "lmfao_profile_read": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)],
+    "lmfao_create_loopback": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_P)],
+    "lmfao_gather_result": [_P, ctypes.c_int32, ctypes.c_int32],
+    "lmfao_shard_range": [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                          ctypes.POINTER(ctypes.c_int64)],
+    "lmfao_owner_range": [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                          ctypes.POINTER(ctypes.c_int64)],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -143,13 +149,36 @@ def _udaf_structs(udafs, attr_id):
     return ctypes.cast(U.ctypes.data, ctypes.POINTER(lmfao_udaf)), (F, P, U)
 
 
-class Engine:
-    """One lmfao_ctx (one process, one GPU)."""
+def shard_range(nrows: int, part: int, nparts: int):
+    """lmfao_shard_range (host only): the rows [lo, hi) of the sorted root kept by `part`."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    s = _lib.lmfao_shard_range(nrows, part, nparts, ctypes.byref(lo), ctypes.byref(hi))
+    if s:
+        raise LmfaoError(s, "lmfao_shard_range")
+    return lo.value, hi.value
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+
+def owner_range(ncells: int, rank: int, world: int):
+    """lmfao_owner_range (host only): the cells [lo, hi) of a distributed output owned by `rank`."""
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    s = _lib.lmfao_owner_range(ncells, rank, world, ctypes.byref(lo), ctypes.byref(hi))
+    if s:
+        raise LmfaoError(s, "lmfao_owner_range")
+    return lo.value, hi.value
+
+
+class Engine:
+    """One lmfao_ctx (one process, one GPU).  loopback=group name: a rank of an in-process
+    group of contexts on one device (lmfao_create_loopback; tests of the multi-GPU path)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+                 loopback: str | None = None):
         h = _P()
-        uid = ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES) if unique_id is not None else None
-        s = _lib.lmfao_create(device, rank, world, uid, ctypes.byref(h))
+        if loopback is not None:
+            s = _lib.lmfao_create_loopback(device, rank, world, loopback.encode(), ctypes.byref(h))
+        else:
+            uid = ctypes.create_string_buffer(unique_id, UNIQUE_ID_BYTES) if unique_id is not None else None
+            s = _lib.lmfao_create(device, rank, world, uid, ctypes.byref(h))
         if s:
             raise LmfaoError(s, "lmfao_create failed (no CUDA device?)")
         self.h = h
@@ -268,6 +297,10 @@ class Engine:
         self._check(_lib.lmfao_fetch(self.h, q, keys.ctypes.data if keys.size else None,
                                      vals.ctypes.data if vals.size else None, counts.ctypes.data if ng else None))
         return keys, vals, counts
+
+    def gather_result(self, q: int, root: int = 0):
+        """Collective: assemble a distributed result on rank `root` (lmfao_gather_result)."""
+        self._check(_lib.lmfao_gather_result(self.h, q, root))
 
     def result_device(self, q: int):
         k, v, c = _P(), _P(), _P()

@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_b.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_multirank.py -x -q > gpurun_out/r2_t7.log 2>&1; echo rc=$? >> gpurun_out/r2_t7.log
+timeout 900 python -m pytest tests/test_gpu_cube.py tests/test_gpu_counts.py tests/test_gpu_parity.py tests/test_gpu_gram.py -x -q > gpurun_out/r2_t8.log 2>&1; echo rc=$? >> gpurun_out/r2_t8.log
