@@ -897,6 +897,10 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   CTX_CUDA(c, c->scalar_out.alloc((size_t)std::max(nout, 1) * 8), "plan");
   CTX_CUDA(c, c->scalar_count.alloc(8), "plan");
   // group-by queries: dictionaries, codes, dense cell tables
+  const int64_t sparse_cells = [] {  // cube.cu's threshold for sparse cuboids (LMFAO_CUBE_SPARSE_CELLS)
+    const char* e = std::getenv("LMFAO_CUBE_SPARSE_CELLS");
+    return e ? std::atoll(e) : ((int64_t)1 << 25);
+  }();
   for (size_t q = 0; q < c->queries.size(); q++) {
     if (c->query_kind[q] != 1) continue;
     GroupPlan& gp = c->groups[c->query_slot[q]];
@@ -957,7 +961,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     // world > 1: tables of at least LMFAO_DIST_CELLS cells (default 2^16) are distributed —
     // reduce-scattered by cell range; smaller ones are all-reduced (complete on every rank)
     {
-      static const int64_t dist_min = [] {
+      const int64_t dist_min = [] {
         const char* e = std::getenv("LMFAO_DIST_CELLS");
         return e ? std::atoll(e) : ((int64_t)1 << 16);
       }();
@@ -966,7 +970,9 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
       owner_range(cells, c->rank, c->world, gp.cell_lo, gp.cell_hi);
       if (!gp.dist) gp.cell_lo = 0, gp.cell_hi = cells;
     }
-    {
+    // tables the data-cube path keeps sparse (no dense table: run records sorted by cell) are
+    // allocated only if no specialised path takes them (below)
+    if (cells <= sparse_cells || cells > ((int64_t)1 << 32)) {
       StreamScope ts(st, !(plain_sites & 1));
       CTX_CUDA(c, gp.table.alloc(gp.ncells_alloc * std::max(gp.nudaf, 1) * 8), "plan group table");
       CTX_CUDA(c, gp.counts.alloc(gp.ncells_alloc * 8), "plan group counts");
@@ -976,9 +982,10 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
     CTX_CUDA(c, gp.prog.upload(gprogs[c->query_slot[q]], st), "plan upload group");
   }
   // fused group-by scan: one combined program, one descriptor per group-by query
+  std::vector<GroupDesc> descs;
+  std::vector<int> desc_group;  // group index of each descriptor
   {
     Program all;
-    std::vector<GroupDesc> descs;
     for (size_t gi = 0; gi < c->groups.size(); gi++) {
       GroupPlan& gp = c->groups[gi];
       const Query& Q = c->queries[gp.q];
@@ -1034,6 +1041,7 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
         continue;
       }
       descs.push_back(d);
+      desc_group.push_back((int)gi);
     }
     CTX_CUDA(c, c->group_prog.upload(all, st), "plan upload groups");
     c->ndescs = (int)descs.size();
@@ -1047,6 +1055,35 @@ extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   {
     StreamScope fs(st, !(plain_sites & 4));
     c->fast.reset(plan_fast_paths(c));
+  }
+  {  // deferred tables that no specialised path took sparse: allocate them now, re-plan
+    bool late = false;
+    for (auto& gp : c->groups) {
+      if (gp.table.p || gp.direct) continue;
+      StreamScope ts(st, !(plain_sites & 1));
+      CTX_CUDA(c, gp.table.alloc(gp.ncells_alloc * std::max(gp.nudaf, 1) * 8), "plan group table");
+      CTX_CUDA(c, gp.counts.alloc(gp.ncells_alloc * 8), "plan group counts");
+      CTX_CUDA(c, cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st), "plan group table");
+      CTX_CUDA(c, cudaMemsetAsync(gp.counts.p, 0, gp.counts.bytes, st), "plan group counts");
+      late = true;
+    }
+    if (late) {
+      for (size_t i = 0; i < descs.size(); i++) {
+        descs[i].table = c->groups[desc_group[i]].table.as<double>();
+        descs[i].counts = c->groups[desc_group[i]].counts.as<unsigned long long>();
+      }
+      for (auto& rv : c->revs) {
+        rv.d.table = c->groups[rv.gi].table.as<double>();
+        rv.d.counts = c->groups[rv.gi].counts.as<unsigned long long>();
+      }
+      if (!descs.empty())
+        CTX_CUDA(c, cudaMemcpyAsync(c->group_descs.p, descs.data(), descs.size() * sizeof(GroupDesc),
+                                    cudaMemcpyHostToDevice, st),
+                 "plan");
+      c->fast.reset();
+      StreamScope fs(st, !(plain_sites & 4));
+      c->fast.reset(plan_fast_paths(c));
+    }
   }
   tr.mark("fast paths", st);
   c->state = S_PLANNED;

@@ -383,12 +383,9 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   if (cudaStreamSynchronize(st)) return nullptr;
   fc->smem = rq.size() * 24 + ((rq.size() & 1) ? 8 : 0) + (size_t)fc->threads * 4 * (a.nattr + 1 + a.nlev) +
              (size_t)a.nsmall * 4;
-  // (static scode + dynamic above 48 KB needs the opt-in; the attribute is process-wide: keep the max)
-  static int set_smem = 0;
-  if ((int)fc->smem > set_smem) {
-    if (cudaFuncSetAttribute(k_cnt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc->smem)) return nullptr;
-    set_smem = (int)fc->smem;
-  }
+  // (static scode + dynamic above 48 KB needs the opt-in; the attribute is per device and
+  // process-wide there: keep each device's max)
+  if (ensure_smem_attr((const void*)k_cnt_rows, fc->smem)) return nullptr;
   {
     int per_sm = 0, nsm = 148;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cnt_rows, fc->threads, fc->smem) || per_sm < 1)

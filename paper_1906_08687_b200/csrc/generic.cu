@@ -219,11 +219,7 @@ cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, doub
   if (a.nslots > VB_MAXSLOT) return cudaErrorInvalidValue;
   const size_t smem = (size_t)VB_WARPS * a.nslots * 8 * 33;
   if (smem > 48 * 1024) {
-    static size_t set = 0;
-    if (smem > set) {
-      CUDA_TRY(cudaFuncSetAttribute(k_view_lin, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      set = smem;
-    }
+    CUDA_TRY(ensure_smem_attr((const void*)k_view_lin, smem));
   }
   k_view_lin<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, V);
   launches_add(1);
@@ -241,11 +237,7 @@ cudaError_t launch_view_build(const NodeArgs& a, const int32_t* dense_key, const
   }
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
-    static size_t set = 0;
-    if (smem > set) {
-      CUDA_TRY(cudaFuncSetAttribute(k_view_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      set = smem;
-    }
+    CUDA_TRY(ensure_smem_attr((const void*)k_view_build, smem));
   }
   k_view_build<<<grid_rows(a.nrows), VB_WARPS * 32, smem, st>>>(a, dense_key, prog_i, prog_d, ioff, doff, nslots, V,
                                                                 use_lacc);
@@ -307,11 +299,7 @@ cudaError_t launch_root_scalar(const NodeArgs& a, const int32_t* prog_i, const d
                                const int32_t* doff, int nout, double* partials, unsigned long long* count_partials,
                                int grid, cudaStream_t st) {
   const int threads = 256, chunk = 1024;  // 8 warps x 1024 x 8 B = 64 KB smem per launch
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(k_root_scalar, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * chunk * 8));
-    attr_set = true;
-  }
+  CUDA_TRY(ensure_smem_attr((const void*)k_root_scalar, 8 * chunk * 8));
   if (nout == 0) {
     k_root_scalar<<<grid, threads, 0, st>>>(a, prog_i, prog_d, ioff, doff, 0, 0, 1, partials, count_partials);
     launches_add(1);
@@ -464,11 +452,7 @@ cudaError_t launch_groups_fused(const NodeArgs& a, const GroupDesc* descs, int n
   if (a.nrows <= 0 || nq == 0) return cudaSuccess;
   const size_t smem = ((size_t)nq * sizeof(GroupDesc) + 15) / 16 * 16;
   if (smem > 48 * 1024) {
-    static size_t set = 0;
-    if (smem > set) {
-      CUDA_TRY(cudaFuncSetAttribute(k_groups_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      set = smem;
-    }
+    CUDA_TRY(ensure_smem_attr((const void*)k_groups_fused, smem));
   }
   k_groups_fused<<<grid_rows(a.nrows, 16), 256, smem, st>>>(a, descs, nq, prog_i, prog_d, ioff, doff);
   launches_add(1);

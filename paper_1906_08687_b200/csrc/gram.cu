@@ -636,11 +636,7 @@ int tiles_for(int nb, int ns, int nts) {
 template <int NB, int NS, int NTS>
 cudaError_t launch_gram_t(const GramArgs& g, int grid, int threads, cudaStream_t st) {
   size_t smem = (size_t)(threads / 32) * (24 * 16 * 8 + g.smem_per_warp);
-  static size_t set = 0;
-  if (smem > set) {
-    CUDA_TRY(cudaFuncSetAttribute(k_gram<NB, NS, NTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    set = smem;
-  }
+  CUDA_TRY(ensure_smem_attr((const void*)k_gram<NB, NS, NTS>, smem));
   k_gram<NB, NS, NTS><<<grid, threads, smem, st>>>(g);
   return cudaGetLastError();
 }

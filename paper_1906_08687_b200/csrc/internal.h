@@ -130,6 +130,10 @@ struct DevBuf {
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// The dynamic shared-memory opt-in of a kernel (cudaFuncAttributeMaxDynamicSharedMemorySize) is
+// per device: raise it on the current device when a launch needs more than set there so far.
+cudaError_t ensure_smem_attr(const void* func, size_t smem);
+
 // ---- device primitives (prims.cu), all on stream st ----
 cudaError_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, cudaStream_t st);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t st);

@@ -5,6 +5,8 @@
 // P:42 "We sort the relations once"; "We choose the order that is the
 // increasing order in the domain sizes of these attributes ... We sort S in this
 // order."  These run at load time (lmfao_prepare) and plan time, never in lmfao_run.
+#include <mutex>
+
 #include "internal.h"
 
 namespace lmfao {
@@ -532,6 +534,20 @@ cudaError_t segment_offsets(const int32_t* dkey, int64_t n, int64_t nkeys, DevBu
 }  // namespace lmfao
 
 namespace lmfao {
+cudaError_t ensure_smem_attr(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{dev, func}];
+  if (smem > cur) {
+    CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  return cudaSuccess;
+}
+
 static int64_t g_launches = 0;
 int launches_counter_reset() {
   int r = (int)g_launches;
