@@ -198,6 +198,17 @@ LMFAO_API lmfao_status lmfao_plan(lmfao_ctx* ctx);
  * query ids restart at 0.  LMFAO_ERR_STATE otherwise. */
 LMFAO_API lmfao_status lmfao_reset_batch(lmfao_ctx* ctx);
 
+/* Dynamic functions ("Dynamic Functions": a decision tree recomputes
+ * the same aggregates at every node, the only difference being the node's threshold
+ * functions).  Replaces the path condition of the planned batch — the Kronecker-delta factors
+ * (LMFAO_F_LT .. LMFAO_F_IN) that every product of the batch carries, as planned — by
+ * factors[0 .. n_factors), for the following runs, without re-planning: every result is then
+ * that of the batch with the new condition in place of the old.  The attributes must belong to
+ * the root or to a root child with a primary key; at most 8 factors.  Valid after lmfao_plan;
+ * LMFAO_ERR_UNSUPPORTED when the planned kernels took no path condition (plan the batch with a
+ * placeholder condition, e.g. y >= -inf, to make it dynamic).  Synchronises the ctx stream. */
+LMFAO_API lmfao_status lmfao_set_condition(lmfao_ctx* ctx, int32_t n_factors, const lmfao_factor* factors);
+
 /* Runs the planned batch asynchronously on `cuda_stream` (cudaStream_t; NULL =
  * the ctx's own stream): view builds (b), the fused root scan (c) with its FP64
  * Gram tiles (d) and histograms (e), dimension-side finishing, and when world > 1

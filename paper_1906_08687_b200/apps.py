@@ -164,30 +164,33 @@ def chow_liu_tree(M):
 
 
 # ------------------------------------------------------------------ CART regression tree
-F_LE, F_GT, F_IDENT, F_IN = 3, 4, 1, 8  # lmfao_fkind
+F_LE, F_GT, F_GE, F_IDENT, F_IN = 3, 4, 5, 1, 8  # lmfao_fkind
 
 
 def _mask(values):
     return float(sum(1 << int(v) for v in values))
 
 
-def regression_tree(engine, features, target, thresholds, max_depth=4, min_split=1000, categoricals=()):
+def regression_tree(engine, features, target, thresholds, max_depth=4, min_split=1000, categoricals=(),
+                    dynamic=True):
     """A CART regression tree (§3 "Decision trees" P:480-555; §6: depth 4, min split
     1000, 20 buckets) grown over the prepared relations of `engine`.
 
-    Each node runs one batch (lmfao_reset_batch + add_query + plan + run): with α the node's
-    path condition, RT(α, y·α, y²·α) for the node and for every candidate condition A ≤ t
-    (the rt.cu path takes α as a row filter), and Q(X; α·y^p) for every categorical X.  The
-    split with the largest variance reduction SSE(node) − SSE(left) − SSE(right),
-    SSE = Σy² − (Σy)²/n, is taken; the right side's sums are the node's minus the left's.
-    A categorical X splits by set inclusion (LMFAO_F_IN; values in [0, 52]): its
-    categories in increasing order of mean y (then value), cut after each prefix.  A node
-    with fewer than `min_split` rows, at `max_depth`, or without a split that reduces SSE is a
-    leaf.  Returns nested dicts."""
+    Every node computes one batch: with α the node's path condition, RT(α, y·α, y²·α) for the
+    node and for every candidate condition A ≤ t (the rt.cu path takes α as a row filter), and
+    Q(X; α·y^p) for every categorical X.  dynamic=True ("dynamic
+    functions"): the batch is planned once, with a placeholder condition y ≥ -inf, and each
+    node only rebinds α (lmfao_set_condition) before its run; dynamic=False re-plans the batch
+    per node (lmfao_reset_batch + add_query + plan).  The split with the largest variance
+    reduction SSE(node) − SSE(left) − SSE(right), SSE = Σy² − (Σy)²/n, is taken; the right
+    side's sums are the node's minus the left's.  A categorical X splits by set inclusion (P:484,
+    LMFAO_F_IN; values in [0, 52]): its categories in increasing order of mean y (then value),
+    cut after each prefix.  A node with fewer than `min_split` rows, at `max_depth`, or without a
+    split that reduces SSE is a leaf.  Returns nested dicts."""
     y = [(F_IDENT, target, 0.0)]
+    placeholder = [(F_GE, target, float("-inf"))]
 
-    def node(path, depth):
-        engine.reset_batch()
+    def batch(path):
         udafs = [[(1.0, path + y * p)] for p in range(3)]
         for a in features:
             for t in thresholds:
@@ -195,7 +198,21 @@ def regression_tree(engine, features, target, thresholds, max_depth=4, min_split
                 udafs += [[(1.0, cond + y * p)] for p in range(3)]
         q = engine.add_query([], udafs)
         qc = [engine.add_query([x], [[(1.0, path + y * p)] for p in range(3)]) for x in categoricals]
+        return q, qc
+
+    if dynamic:
+        engine.reset_batch()
+        q_dyn, qc_dyn = batch(placeholder)
         engine.plan()
+
+    def node(path, depth):
+        if dynamic:
+            engine.set_condition(path if path else placeholder)
+            q, qc = q_dyn, qc_dyn
+        else:
+            engine.reset_batch()
+            q, qc = batch(path)
+            engine.plan()
         engine.run()
         v = engine.fetch(q)[1][0]
         n, s, s2 = v[0], v[1], v[2]

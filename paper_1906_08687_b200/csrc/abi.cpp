@@ -1221,6 +1221,29 @@ extern "C" lmfao_status lmfao_reset_batch(lmfao_ctx* c) {
   return LMFAO_OK;
 }
 
+// Dynamic functions: the next node of a decision tree differs from the
+// planned batch only in its path condition; the planned kernels take the new one as is.
+extern "C" lmfao_status lmfao_set_condition(lmfao_ctx* c, int32_t n_factors, const lmfao_factor* factors) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "set_condition needs plan");
+  if (n_factors < 0 || (n_factors > 0 && !factors)) return fail(c, LMFAO_ERR_INVALID_ARG, "bad condition");
+  for (int i = 0; i < n_factors; i++) {
+    const lmfao_factor& f = factors[i];
+    if (f.kind < LMFAO_F_LT || f.kind > LMFAO_F_IN) return fail(c, LMFAO_ERR_INVALID_ARG, "condition factor %d is not a predicate", i);
+    if (f.attr < 0 || f.attr >= (int)c->attrs.size()) return fail(c, LMFAO_ERR_UNKNOWN_ATTR, "condition factor %d: unknown attribute", i);
+  }
+  cudaSetDevice(c->device);
+  StreamScope scope_(c->stream);
+  CTX_CUDA(c, cudaStreamSynchronize(c->stream), "set_condition");
+  if (!c->fast || c->fast->set_condition(c, n_factors, factors) != 0)
+    return fail(c, LMFAO_ERR_UNSUPPORTED, "the planned batch has no path condition the kernels can rebind "
+                                         "(regression-tree batches whose products all carry the same predicates)");
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);  // the captured kernel arguments are stale
+  c->graph_exec = nullptr;
+  c->graph_runs = 0;
+  return LMFAO_OK;
+}
+
 extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");

@@ -21,6 +21,10 @@ struct FastPaths {
   // false if run() synchronises with the host (data-dependent sizes): no CUDA Graph capture
   virtual bool graph_ok() const { return true; }
   virtual std::string describe() const = 0;
+  // Dynamic functions: replace the planned batch's path condition (the
+  // predicates every product carries) by factors[0..n), without re-planning.  0 = ok, else
+  // unsupported (the path took no path condition, or an attribute it cannot evaluate).
+  virtual int set_condition(lmfao_ctx* c, int n, const lmfao_factor* factors) { return -1; }
 };
 // Returns nullptr when no specialised path applies (the generic path runs).
 FastPaths* plan_fast_paths(lmfao_ctx* c);

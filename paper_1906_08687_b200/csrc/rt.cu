@@ -717,6 +717,34 @@ struct FastRT : FastPaths {
   bool handles_all_groups() const override { return true; }
   bool skip_generic_views() const override { return true; }
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
+  // the row filter takes its predicates from phi at every run: a new path condition needs no
+  // re-planning (the unconditioned pass for the join multiplicities is planned with any φ)
+  int set_condition(lmfao_ctx* c, int n, const lmfao_factor* f) override {
+    if (nphi == 0 || n < 0 || n + (ncls > 0 ? 1 : 0) > RT_MAX_PHI) return -1;
+    const Rel& R = c->rels[c->root];
+    RtFilterArgs np = phi;
+    np.n = n;
+    for (int i = 0; i < n; i++) {
+      const int a = f[i].attr, kind = f[i].kind;
+      if (a < 0 || a >= (int)c->attrs.size() || kind < LMFAO_F_LT || kind > LMFAO_F_IN) return -1;
+      const int o = c->owner[a];
+      int lv = -1;
+      if (o != c->root) {
+        for (size_t j = 0; j < R.children.size(); j++)
+          if (R.children[j] == o) lv = (int)j;
+        if (lv < 0 || !c->rels[o].unique_key) return -1;  // deeper than a root child, or not a primary key
+      }
+      const Rel& O = lv < 0 ? R : c->rels[o];
+      RtPhi& q = np.p[i];
+      q.col = O.cols[O.find_attr(a)].buf.p;
+      q.fk = lv < 0 ? nullptr : R.fk_dense[lv].as<int32_t>();
+      q.is_int = c->attrs[a].dt == LMFAO_INT32;
+      q.kind = kind;
+      q.t = f[i].param;
+    }
+    phi = np;
+    return 0;
+  }
   cudaError_t pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const double* yp, double* accp, double* Vp,
                    const std::vector<FactHist>& fhl, const std::vector<DimHist>& dhl, bool timed);
 };
@@ -742,9 +770,9 @@ int FastRT::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_don
   if (ncls > 0 && R.nrows > 0) {  // classification: the node's condition and X = class, per class
     for (int k = 0; k < ncls; k++) {
       RtFilterArgs f = phi;
-      f.n = nphi + 1;
-      f.p[nphi] = ct_code;
-      f.p[nphi].t = (double)k;
+      f.n = phi.n + 1;
+      f.p[phi.n] = ct_code;
+      f.p[phi.n].t = (double)k;
       f.nrows = R.nrows;
       f.out = filt.as<uint8_t>();
       k_rt_filter<<<148 * 8, 256, 0, st>>>(f);

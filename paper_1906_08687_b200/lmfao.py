@@ -70,6 +70,7 @@ _SIGS = {
     "lmfao_profile_read": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)],
     "lmfao_create_loopback": [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_P)],
     "lmfao_gather_result": [_P, ctypes.c_int32, ctypes.c_int32],
+    "lmfao_set_condition": [_P, ctypes.c_int32, ctypes.POINTER(lmfao_factor)],
     "lmfao_shard_range": [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                           ctypes.POINTER(ctypes.c_int64)],
     "lmfao_owner_range": [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
@@ -297,6 +298,16 @@ class Engine:
         self._check(_lib.lmfao_fetch(self.h, q, keys.ctypes.data if keys.size else None,
                                      vals.ctypes.data if vals.size else None, counts.ctypes.data if ng else None))
         return keys, vals, counts
+
+    def set_condition(self, factors):
+        """Dynamic path condition (lmfao_set_condition): factors = [(kind, attr name, param)] or
+        synth.Factor objects, all predicates; replaces the planned batch's condition."""
+        fs = []
+        for f in factors:
+            kind, attr, param = (f.kind, f.attr, f.param) if hasattr(f, "kind") else f
+            fs.append(lmfao_factor(int(kind), self.attr_id(attr), float(param)))
+        arr = (lmfao_factor * max(1, len(fs)))(*fs)
+        self._check(_lib.lmfao_set_condition(self.h, len(fs), arr))
 
     def gather_result(self, q: int, root: int = 0):
         """Collective: assemble a distributed result on rank `root` (lmfao_gather_result)."""

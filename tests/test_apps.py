@@ -229,7 +229,10 @@ def _same_tree(g, r):
 
 
 @pytest.mark.gpu
-def test_regression_tree_matches_numpy_cart():
+@pytest.mark.parametrize("dynamic", [True, False])
+def test_regression_tree_matches_numpy_cart(dynamic):
+    """dynamic=True: one plan, the node's path condition rebound per node (lmfao_set_condition,
+    PAPER.md P:2086-2092); dynamic=False: one plan per node."""
     from paper_1906_08687_b200 import lmfao
     w = synth.config3(seed=2, fact_rows=30_000, dim_rows=(40, 300, 2000))
     feats = ["x1", "x2", "x5", "d1_1", "d2_3", "d3_2"]
@@ -237,7 +240,7 @@ def test_regression_tree_matches_numpy_cart():
     e = lmfao.Engine()
     try:
         lmfao.load(e, w.db, [])
-        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=2_000)
+        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=2_000, dynamic=dynamic)
     finally:
         e.close()
     ref = _cart_numpy(_join(w.db), feats, "y", ts, 3, 2_000)
@@ -292,7 +295,8 @@ def test_batch_over_assigned_roots_matches_oracle():
 
 
 @pytest.mark.gpu
-def test_regression_tree_with_categorical_splits():
+@pytest.mark.parametrize("dynamic", [True, False])
+def test_regression_tree_with_categorical_splits(dynamic):
     """Categorical features split by set inclusion: node paths carry LMFAO_F_IN."""
     from paper_1906_08687_b200 import lmfao
     w = synth.config3(seed=3, fact_rows=30_000, dim_rows=(40, 300, 2000))
@@ -308,7 +312,8 @@ def test_regression_tree_with_categorical_splits():
     e = lmfao.Engine()
     try:
         lmfao.load(e, w.db, [])
-        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=1_000, categoricals=["cat", "dc"])
+        tree = apps.regression_tree(e, feats, "y", ts, max_depth=3, min_split=1_000, categoricals=["cat", "dc"],
+                                    dynamic=dynamic)
     finally:
         e.close()
     ref = _cart_numpy(_join(w.db), feats, "y", ts, 3, 1_000, categoricals=["cat", "dc"])

@@ -163,3 +163,39 @@ def test_set_inclusion_in_products_interpreted():
     batch = [Query(["c1"], [[Product(1.0, (Factor(F_IN, "g3", m),))], [Product(1.0, (Factor(F_IN, "e1", m), ident("x2")))]]),
              Query([], [[Product(1.0, (Factor(F_IN, "i1", m), ident("y"), ident("x1")))]])]
     assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
+
+
+def test_set_condition_rebinds_the_path_without_replanning():
+    """Dynamic functions: a batch planned under path condition φ1, rebound
+    to φ2, φ3 (root, dimension and set-inclusion predicates, a different number of them, and
+    the empty condition) by lmfao_set_condition, equals the oracle of the batch written with φ2,
+    φ3 in place of φ1 — counts of the group-by queries included (join multiplicities)."""
+    from paper_1906_08687_b200 import lmfao
+    w = synth.config3(fact_rows=40_011, dim_rows=(30, 200, 1500))
+    F = synth.Factor
+    phi1 = [F(synth.F_GE, "y", float("-inf"))]
+    phi2 = [F(synth.F_LE, "x1", 0.25), F(synth.F_GT, "d2_3", -0.5)]
+    phi3 = [F(synth.F_GT, "d1_2", 0.0), F(synth.F_IN, "c1", float((1 << 2) | (1 << 5) | (1 << 7))),
+            F(synth.F_LE, "d3_1", 1.0)]
+
+    def batch(phi):
+        y = synth.ident("y")
+        u = [[synth.Product(1.0, tuple(phi) + (y,) * p)] for p in range(3)]
+        for a in ("x2", "d1_1", "d3_4"):
+            for t in (-0.5, 0.0, 0.75):
+                u += [[synth.Product(1.0, tuple(phi) + (F(synth.F_LE, a, t),) + (y,) * p)] for p in range(3)]
+        g = [synth.Query([x], [[synth.Product(1.0, tuple(phi) + (y,) * p)] for p in range(3)]) for x in ("c1", "c3")]
+        return [synth.Query([], u)] + g
+
+    e = lmfao.Engine()
+    try:
+        qids = lmfao.load(e, w.db, batch(phi1))
+        e.plan()
+        assert e.plan_info()["fast_path"]["kind"] == "rt"
+        for phi in (phi2, phi3, [], phi2):
+            e.set_condition(phi)
+            e.run()
+            got = [e.fetch(q) for q in qids]
+            assert_parity(got, oracle.evaluate(w.db, batch(phi)), batch(phi))
+    finally:
+        e.close()

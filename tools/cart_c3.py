@@ -20,18 +20,30 @@ cols = {r.name: {c: torch.from_numpy(v).cuda() for c, v in r.cols.items()} for r
 e = lmfao.Engine()
 lmfao.load(e, w.db, [], columns=cols)
 torch.cuda.synchronize()
-t0 = time.perf_counter()
-tree = apps.regression_tree(e, feats, "y", synth.thresholds_c3(), max_depth=4, min_split=1000)
-dt = time.perf_counter() - t0
 
 
 def count(n):
     return 1 + (count(n["left"]) + count(n["right"]) if "feature" in n else 0)
 
 
-nodes = count(tree)
-print(json.dumps({"config": "C3 CART", "fact_rows": rows, "features": len(feats), "thresholds": 20, "depth": 4,
-                  "nodes": nodes, "wall_s": dt, "ms_per_node": 1e3 * dt / nodes,
-                  "aggregates_per_node": 3 + 3 * 20 * len(feats), "root_split": [tree.get("feature"), tree.get("threshold")],
-                  "plan": e.plan_info().get("fast_path")}))
+trees = {}
+for dynamic in (True, False, True):  # dynamic path conditions (one plan) vs one plan per node
+    t0 = time.perf_counter()
+    tree = apps.regression_tree(e, feats, "y", synth.thresholds_c3(), max_depth=4, min_split=1000, dynamic=dynamic)
+    dt = time.perf_counter() - t0
+    trees[dynamic] = tree
+    nodes = count(tree)
+    print(json.dumps({"config": "C3 CART", "dynamic": dynamic, "fact_rows": rows, "features": len(feats),
+                      "thresholds": 20, "depth": 4, "nodes": nodes, "wall_s": dt, "ms_per_node": 1e3 * dt / nodes,
+                      "aggregates_per_node": 3 + 3 * 20 * len(feats),
+                      "root_split": [tree.get("feature"), tree.get("threshold")],
+                      "plan": e.plan_info().get("fast_path")}), flush=True)
+
+
+def shape(n):  # the splits and node sizes (means may differ in the last bits between the two plans)
+    return (n["n"], n.get("feature"), n.get("threshold"), n.get("categories"),
+            shape(n["left"]) if "left" in n else None, shape(n["right"]) if "right" in n else None)
+
+
+assert shape(trees[True]) == shape(trees[False])
 e.close()
