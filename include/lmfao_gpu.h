@@ -175,7 +175,13 @@ LMFAO_API lmfao_status lmfao_set_root_shard(lmfao_ctx* ctx, int32_t part, int32_
  * (the MOO attribute order). Then sharding (see above). */
 LMFAO_API lmfao_status lmfao_prepare(lmfao_ctx* ctx);
 
-/* Adds Q(F; α_1..α_n) += R_1..R_m.  groupby_attrs: int32 attributes
+/* Adds Q(F; α_1..α_n) += R_1..R_m.  Multi-root ("each aggregate to its
+ * own root"): a query whose group-by attributes the user's root cannot place (below a root
+ * child, or mixing a child with a non-unique key with other relations) is computed at another
+ * root of the same join tree — tried in the order of P:958's heuristic (the relations holding
+ * the query's group-by attributes, by how many they hold, then by size) — inside this context
+ * (a re-rooted copy of the relations, prepared once, run on its own stream concurrently with the
+ * main root); results and query ids are the same as for any query.  Single GPU only (world 1).  groupby_attrs: int32 attributes
  * (LMFAO_ERR_TYPE otherwise) owned by the root or by children of the root; when a
  * child's join key is not unique in it (a root row joins several of its rows) all the
  * query's group-by attributes must belong to that child — the query is then finished
@@ -186,7 +192,7 @@ LMFAO_API lmfao_status lmfao_prepare(lmfao_ctx* ctx);
 LMFAO_API lmfao_status lmfao_add_query(lmfao_ctx* ctx, int32_t n_groupby, const int32_t* groupby_attrs,
                              int32_t n_udafs, const lmfao_udaf* udafs, int32_t* query_id);
 
-/* Host planner: pushes every product down the join tree, dedups
+/* Host planner (and the plans of the queries placed at other roots): pushes every product down the join tree, dedups
  * view slots across the batch (view merging), picks the kernels and
  * allocates all device buffers.  Freezes the batch. */
 LMFAO_API lmfao_status lmfao_plan(lmfao_ctx* ctx);

@@ -122,6 +122,14 @@ NodeArgs node_args(const lmfao_ctx* c, int n) {
 
 }  // namespace
 
+namespace {
+lmfao_status relay(lmfao_ctx* c, lmfao_ctx* t, lmfao_status s);
+}
+
+lmfao_ctx::~lmfao_ctx() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+}
+
 // =====================================================================  ABI
 extern "C" {
 
@@ -208,6 +216,14 @@ lmfao_status lmfao_owner_range(int64_t ncells, int32_t rank, int32_t world, int6
 
 lmfao_status lmfao_destroy(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
+  for (auto& sc : c->secs) {
+    if (sc.ctx) lmfao_destroy(sc.ctx);
+    cudaSetDevice(c->device);
+    if (sc.ev_in) cudaEventDestroy(sc.ev_in);
+    if (sc.ev_out) cudaEventDestroy(sc.ev_out);
+    if (sc.stream) cudaStreamDestroy(sc.stream);
+  }
+  c->secs.clear();
   cudaSetDevice(c->device);
   StreamScope scope_(c->stream);
   cudaStreamSynchronize(c->stream);
@@ -561,6 +577,91 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
   return LMFAO_OK;
 }
 
+namespace {
+// Can the query's group-by attributes be placed at this context's root?  The root, a
+// unique-keyed child (determined by a root row), or a child with a non-unique key (the query is
+// then finished at that child: all its group-by attributes must belong to it).
+lmfao_status gb_placement(lmfao_ctx* c, const std::vector<int>& gb) {
+  for (int a : gb) {
+    const int o = c->owner[a];
+    if (!(o == c->root || c->rels[o].parent == c->root))
+      return fail(c, LMFAO_ERR_UNSUPPORTED, "group-by attribute %s belongs to neither the root nor a child of the root",
+                  c->attrs[a].name.c_str());
+  }
+  int T = -1;
+  bool mixed = false;
+  for (int a : gb) {
+    const int o = c->owner[a];
+    if (o != c->root && !c->rels[o].unique_key) T = o;
+  }
+  if (T >= 0)
+    for (int a : gb) mixed |= c->owner[a] != T;
+  if (mixed)
+    return fail(c, LMFAO_ERR_UNSUPPORTED, "group-by attributes of %s (a non-unique key) mixed with attributes of other relations",
+                c->rels[T].name.c_str());
+  return LMFAO_OK;
+}
+
+// The secondary context rooted at relation `root` (created on first use): every relation copied
+// from this context's device columns, the join tree re-oriented from `root`, prepared.
+int secondary_for(lmfao_ctx* c, int root) {
+  for (size_t i = 0; i < c->secs.size(); i++)
+    if (c->secs[i].root == root) return (int)i;
+  lmfao_ctx* s = nullptr;
+  if (lmfao_create(c->device, 0, 1, nullptr, &s) != LMFAO_OK) return -1;
+  s->is_secondary = true;
+  lmfao_ctx::Secondary sc;
+  sc.ctx = s;
+  sc.root = root;
+  auto bad = [&]() {
+    lmfao_destroy(s);
+    return -1;
+  };
+  for (auto& r : c->rels) {
+    std::vector<const char*> names;
+    std::vector<lmfao_dtype> dts;
+    std::vector<const void*> ptrs;
+    for (auto& col : r.cols) {
+      names.push_back(col.name.c_str());
+      dts.push_back(col.dt);
+      ptrs.push_back(col.buf.p);
+    }
+    int32_t rid = -1;
+    if (lmfao_add_relation(s, r.name.c_str(), r.nrows, (int32_t)r.cols.size(), names.data(), dts.data(), ptrs.data(),
+                           LMFAO_COLS_DEVICE, &rid) != LMFAO_OK)
+      return bad();
+  }
+  // re-orient the tree: breadth first from `root` over the undirected edges
+  const int m = (int)c->rels.size();
+  std::vector<std::vector<int>> adj(m);
+  for (int u = 0; u < m; u++)
+    if (c->rels[u].parent >= 0) {
+      adj[u].push_back(c->rels[u].parent);
+      adj[c->rels[u].parent].push_back(u);
+    }
+  std::vector<int32_t> par, chi;
+  std::vector<int> seen(m, 0), queue{root};
+  seen[root] = 1;
+  for (size_t i = 0; i < queue.size(); i++)
+    for (int v : adj[queue[i]])
+      if (!seen[v]) {
+        seen[v] = 1;
+        par.push_back(queue[i]);
+        chi.push_back(v);
+        queue.push_back(v);
+      }
+  if (lmfao_set_join_tree(s, root, (int32_t)par.size(), par.data(), chi.data()) != LMFAO_OK || lmfao_prepare(s) != LMFAO_OK)
+    return bad();
+  cudaSetDevice(c->device);
+  if (cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking) ||
+      cudaEventCreateWithFlags(&sc.ev_in, cudaEventDisableTiming) ||
+      cudaEventCreateWithFlags(&sc.ev_out, cudaEventDisableTiming))
+    return bad();
+  c->secs.push_back(sc);
+  return (int)c->secs.size() - 1;
+}
+}  // namespace
+
 lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* groupby_attrs, int32_t n_udafs,
                              const lmfao_udaf* udafs, int32_t* query_id) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
@@ -577,29 +678,31 @@ lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* gro
     if (c->attrs[a].dt != LMFAO_INT32)
       return fail(c, LMFAO_ERR_TYPE, "group-by attribute %s must be int32", c->attrs[a].name.c_str());
     if (!gbs.insert(a).second) return fail(c, LMFAO_ERR_INVALID_ARG, "duplicate group-by attribute");
-    int o = c->owner[a];
-    // the root, a unique-keyed child (determined by a root row), or a child with a
-    // non-unique key (the query is then finished at that child: all its group-by
-    // attributes must belong to it, checked below)
-    bool ok = o == c->root || c->rels[o].parent == c->root;
-    if (!ok)
-      return fail(c, LMFAO_ERR_UNSUPPORTED,
-                  "group-by attribute %s belongs to neither the root nor a child of the root", c->attrs[a].name.c_str());
     q.gb.push_back(a);
   }
-  {
-    int T = -1;
-    bool mixed = false;
-    for (int a : q.gb) {
-      const int o = c->owner[a];
-      if (o != c->root && !c->rels[o].unique_key) T = o;
+  if (lmfao_status ps = gb_placement(c, q.gb)) {
+    // each aggregate to its own root: another root of the same join tree, chosen
+    // as P:958 does — the relations holding the query's group-by attributes, by the number of
+    // them they hold, then by size — where the query can be placed
+    if (c->is_secondary || c->world > 1) return ps;
+    std::vector<std::pair<std::pair<int, int64_t>, int>> cand;  // ((held, rows), relation)
+    for (size_t u = 0; u < c->rels.size(); u++) {
+      int held = 0;
+      for (int a : q.gb) held += c->rels[u].find_attr(a) >= 0;
+      if (held > 0 && (int)u != c->root) cand.push_back({{held, c->rels[u].nrows}, (int)u});
     }
-    if (T >= 0)
-      for (int a : q.gb) mixed |= c->owner[a] != T;
-    if (mixed)
-      return fail(c, LMFAO_ERR_UNSUPPORTED,
-                  "group-by attributes of %s (a non-unique key) mixed with attributes of other relations",
-                  c->rels[T].name.c_str());
+    std::sort(cand.rbegin(), cand.rend());
+    const std::string why = c->err;
+    for (auto& cd : cand) {
+      const int si = secondary_for(c, cd.second);
+      if (si < 0) continue;
+      int32_t sq = -1;
+      if (lmfao_add_query(c->secs[si].ctx, n_groupby, groupby_attrs, n_udafs, udafs, &sq) != LMFAO_OK) continue;
+      c->qmap.push_back({si, sq});
+      if (query_id) *query_id = (int)c->qmap.size() - 1;
+      return LMFAO_OK;
+    }
+    return fail(c, ps, "%s (and no other root of the join tree places it)", why.c_str());
   }
   for (int j = 0; j < n_udafs; j++) {
     const lmfao_udaf& u = udafs[j];
@@ -628,7 +731,8 @@ lmfao_status lmfao_add_query(lmfao_ctx* c, int32_t n_groupby, const int32_t* gro
     q.udafs.push_back(ps);
   }
   c->queries.push_back(std::move(q));
-  if (query_id) *query_id = (int)c->queries.size() - 1;
+  c->qmap.push_back({-1, (int)c->queries.size() - 1});
+  if (query_id) *query_id = (int)c->qmap.size() - 1;
   return LMFAO_OK;
 }
 
@@ -787,7 +891,7 @@ void build_rev(lmfao_ctx* c, const Query& Q, int T, RevPlan& rv, Program& rp, Pr
 
 }  // namespace
 
-extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
+static lmfao_status plan_local(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PREPARED) return fail(c, LMFAO_ERR_STATE, "plan needs prepare (and runs once)");
   cudaSetDevice(c->device);
@@ -1216,8 +1320,11 @@ extern "C" lmfao_status lmfao_reset_batch(lmfao_ctx* c) {
   c->code_cache.clear();
   c->query_kind.clear();
   c->query_slot.clear();
+  c->qmap.clear();
   c->ran = false;
   c->state = S_PREPARED;
+  for (auto& sc : c->secs)  // keep the secondary roots prepared for the next batch
+    if (lmfao_status e = lmfao_reset_batch(sc.ctx)) return fail(c, e, "secondary root: %s", sc.ctx->err.c_str());
   return LMFAO_OK;
 }
 
@@ -1241,10 +1348,12 @@ extern "C" lmfao_status lmfao_set_condition(lmfao_ctx* c, int32_t n_factors, con
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);  // the captured kernel arguments are stale
   c->graph_exec = nullptr;
   c->graph_runs = 0;
+  for (auto& sc : c->secs)
+    if (lmfao_status s = lmfao_set_condition(sc.ctx, n_factors, factors)) return relay(c, sc.ctx, s);
   return LMFAO_OK;
 }
 
-extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
+static lmfao_status run_local(lmfao_ctx* c, void* cuda_stream) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
   cudaSetDevice(c->device);
@@ -1325,7 +1434,7 @@ lmfao_status ensure_compacted(lmfao_ctx* c, GroupPlan& gp) {
 }
 }  // namespace
 
-extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_groups, int32_t* n_groupby,
+static lmfao_status result_shape_local(lmfao_ctx* c, int32_t q, int64_t* n_groups, int32_t* n_groupby,
                                            int32_t* n_udafs) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
@@ -1346,7 +1455,7 @@ extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_g
   return LMFAO_OK;
 }
 
-extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32_t** keys, const double** vals,
+static lmfao_status result_device_local(lmfao_ctx* c, int32_t q, const int32_t** keys, const double** vals,
                                             const uint64_t** counts) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
@@ -1369,16 +1478,16 @@ extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32
   return LMFAO_OK;
 }
 
-extern "C" lmfao_status lmfao_fetch(lmfao_ctx* c, int32_t q, int32_t* keys_out, double* vals_out,
+static lmfao_status fetch_local(lmfao_ctx* c, int32_t q, int32_t* keys_out, double* vals_out,
                                     uint64_t* counts_out) {
   int64_t ng = 0;
   int32_t ngb = 0, nu = 0;
-  lmfao_status s = lmfao_result_shape(c, q, &ng, &ngb, &nu);
+  lmfao_status s = result_shape_local(c, q, &ng, &ngb, &nu);
   if (s != LMFAO_OK) return s;
   const int32_t* dk = nullptr;
   const double* dv = nullptr;
   const uint64_t* dc = nullptr;
-  s = lmfao_result_device(c, q, &dk, &dv, &dc);
+  s = result_device_local(c, q, &dk, &dv, &dc);
   if (s != LMFAO_OK) return s;
   if (ng > 0 && nu > 0 && !vals_out) return fail(c, LMFAO_ERR_INVALID_ARG, "vals_out is NULL");
   if (ng > 0 && ngb > 0 && !keys_out) return fail(c, LMFAO_ERR_INVALID_ARG, "keys_out is NULL");
@@ -1395,7 +1504,7 @@ extern "C" lmfao_status lmfao_fetch(lmfao_ctx* c, int32_t q, int32_t* keys_out, 
 // range of cells per rank, the ranges ascending with the rank, so the full table in canonical
 // order is the ranks' groups concatenated in rank order: every rank sends its compacted groups to
 // root_rank (counts first, all-gathered), which keeps the result next to its own range.
-extern "C" lmfao_status lmfao_gather_result(lmfao_ctx* c, int32_t q, int32_t root_rank) {
+static lmfao_status gather_local(lmfao_ctx* c, int32_t q, int32_t root_rank) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED || !c->ran) return fail(c, LMFAO_ERR_STATE, "no results: run first");
   if (q < 0 || q >= (int)c->queries.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
@@ -1459,6 +1568,83 @@ extern "C" lmfao_status lmfao_gather_result(lmfao_ctx* c, int32_t q, int32_t roo
   return LMFAO_OK;
 }
 
+// ---- public entry points over the multi-root query map (see lmfao_ctx::secs)
+namespace {
+lmfao_status resolve(lmfao_ctx* c, int32_t q, lmfao_ctx*& t, int32_t& lq) {
+  if (q < 0 || q >= (int32_t)c->qmap.size()) return fail(c, LMFAO_ERR_INVALID_ARG, "bad query id");
+  const auto& m = c->qmap[q];
+  t = m.first < 0 ? c : c->secs[m.first].ctx;
+  lq = m.second;
+  return LMFAO_OK;
+}
+lmfao_status relay(lmfao_ctx* c, lmfao_ctx* t, lmfao_status s) {  // a secondary's error, reported on c
+  if (s != LMFAO_OK && t != c) return fail(c, s, "at root %s: %s", t->rels[t->root].name.c_str(), t->err.c_str());
+  return s;
+}
+}  // namespace
+
+extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (lmfao_status s = plan_local(c)) return s;
+  for (auto& sc : c->secs)
+    if (lmfao_status s = lmfao_plan(sc.ctx)) return relay(c, sc.ctx, s);
+  return LMFAO_OK;
+}
+
+// The secondary roots run on their own streams, ordered after the caller's work and joined
+// back before lmfao_run's work on `cuda_stream` completes (they overlap the main root's run).
+extern "C" lmfao_status lmfao_run(lmfao_ctx* c, void* cuda_stream) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  if (c->secs.empty()) return run_local(c, cuda_stream);
+  if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "run needs plan");
+  cudaSetDevice(c->device);
+  cudaStream_t st = cuda_stream ? (cudaStream_t)cuda_stream : c->stream;
+  CTX_CUDA(c, cudaEventRecord(c->secs[0].ev_in, st), "run");
+  for (auto& sc : c->secs) {
+    CTX_CUDA(c, cudaStreamWaitEvent(sc.stream, c->secs[0].ev_in, 0), "run");
+    if (lmfao_status s = lmfao_run(sc.ctx, sc.stream)) return relay(c, sc.ctx, s);
+    cudaSetDevice(c->device);
+    CTX_CUDA(c, cudaEventRecord(sc.ev_out, sc.stream), "run");
+  }
+  if (!c->queries.empty())
+    if (lmfao_status s = run_local(c, cuda_stream)) return s;
+  for (auto& sc : c->secs) CTX_CUDA(c, cudaStreamWaitEvent(st, sc.ev_out, 0), "run");
+  c->ran = true;
+  return LMFAO_OK;
+}
+
+extern "C" lmfao_status lmfao_result_shape(lmfao_ctx* c, int32_t q, int64_t* n_groups, int32_t* n_groupby,
+                                           int32_t* n_udafs) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  lmfao_ctx* t;
+  int32_t lq;
+  if (lmfao_status s = resolve(c, q, t, lq)) return s;
+  return relay(c, t, result_shape_local(t, lq, n_groups, n_groupby, n_udafs));
+}
+extern "C" lmfao_status lmfao_result_device(lmfao_ctx* c, int32_t q, const int32_t** keys, const double** vals,
+                                            const uint64_t** counts) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  lmfao_ctx* t;
+  int32_t lq;
+  if (lmfao_status s = resolve(c, q, t, lq)) return s;
+  return relay(c, t, result_device_local(t, lq, keys, vals, counts));
+}
+extern "C" lmfao_status lmfao_fetch(lmfao_ctx* c, int32_t q, int32_t* keys_out, double* vals_out,
+                                    uint64_t* counts_out) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  lmfao_ctx* t;
+  int32_t lq;
+  if (lmfao_status s = resolve(c, q, t, lq)) return s;
+  return relay(c, t, fetch_local(t, lq, keys_out, vals_out, counts_out));
+}
+extern "C" lmfao_status lmfao_gather_result(lmfao_ctx* c, int32_t q, int32_t root_rank) {
+  if (!c) return LMFAO_ERR_INVALID_ARG;
+  lmfao_ctx* t;
+  int32_t lq;
+  if (lmfao_status s = resolve(c, q, t, lq)) return s;
+  return relay(c, t, gather_local(t, lq, root_rank));
+}
+
 extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   if (!c || !out || cap <= 0) return LMFAO_ERR_INVALID_ARG;
   if (c->state != S_PLANNED) return fail(c, LMFAO_ERR_STATE, "plan_info needs plan");
@@ -1481,17 +1667,22 @@ extern "C" lmfao_status lmfao_plan_info(lmfao_ctx* c, char* out, int64_t cap) {
   o << ", \"launches_last_run\": " << c->launches_last_run;
   o << ", \"world\": " << c->world << ", \"rank\": " << c->rank
     << ", \"comm\": \"" << (c->comm ? c->comm->backend() : "none") << "\", \"outputs\": [";
-  for (size_t q = 0; q < c->queries.size(); q++) {  // where each query's result lives
+  for (size_t pq = 0; pq < c->qmap.size(); pq++) {  // where each query's result lives
+    const lmfao_ctx* t = c->qmap[pq].first < 0 ? c : c->secs[c->qmap[pq].first].ctx;
+    const int q = c->qmap[pq].second;
     const char* where = "replicated";
     int64_t lo = 0, hi = 1;
-    if (c->query_kind[q] == 1) {
-      const GroupPlan& gp = c->groups[c->query_slot[q]];
+    if (t->query_kind[q] == 1) {
+      const GroupPlan& gp = t->groups[t->query_slot[q]];
       hi = gp.ncells;
-      if (c->world > 1 && gp.direct) where = "exchanged", lo = gp.cell_lo, hi = gp.cell_hi;
+      if (t->world > 1 && gp.direct) where = "exchanged", lo = gp.cell_lo, hi = gp.cell_hi;
       else if (gp.dist) where = "reduce_scattered", lo = gp.cell_lo, hi = gp.cell_hi;
     }
-    o << (q ? ", " : "") << "{\"placement\": \"" << where << "\", \"cells\": [" << lo << ", " << hi << "]}";
+    o << (pq ? ", " : "") << "{\"placement\": \"" << where << "\", \"cells\": [" << lo << ", " << hi
+      << "], \"root\": \"" << t->rels[t->root].name << "\"}";
   }
+  o << "], \"roots\": [\"" << c->rels[c->root].name << "\"";
+  for (auto& sc : c->secs) o << ", \"" << c->rels[sc.root].name << "\"";
   o << "]";
   if (c->coll_n > 0) {  // profiled multi-GPU runs: the collectives of the partial results
     int64_t bytes = c->scalar_queries.empty() ? 0 : (int64_t)c->scalar_prog.nout * 8 + 8;

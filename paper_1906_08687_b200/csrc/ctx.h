@@ -199,9 +199,20 @@ struct lmfao_ctx {
   // CUDA Graph of lmfao_run (see abi.cpp)
   cudaGraphExec_t graph_exec = nullptr;
   int64_t graph_runs = 0, graph_launches = 0;
-  ~lmfao_ctx() {
-    if (graph_exec) cudaGraphExecDestroy(graph_exec);
-  }
+  // Multi-root plans (§4.3 "each aggregate to its own root"): a query the
+  // user's root cannot place is computed at another root — a secondary context over the same
+  // relations (device copies), its join tree re-rooted, prepared for that root — and its run
+  // overlaps the main one on its own stream (task parallelism).
+  struct Secondary {
+    lmfao_ctx* ctx = nullptr;
+    int root = -1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  };
+  std::vector<Secondary> secs;
+  std::vector<std::pair<int, int>> qmap;  // public query id -> (secondary index or -1, its local id)
+  bool is_secondary = false;
+  ~lmfao_ctx();
 };
 
 namespace lmfao {

@@ -31,11 +31,12 @@ def test_hand_databases_golden(name):
         qs = json.load(open(os.path.join(GOLD, "h2.json")))["queries"]
     db = {"h1": synth.hand_h1, "h2": synth.hand_h2, "h4": synth.hand_h4, "h5": lambda: synth.hand_h2("S")}[name]()
     batch = [query(q["groupby"], q["udafs"]) for q in qs]
-    if name == "h5":  # rooted at S: g is owned by the root; (g,b) needs b from F (non-unique child) -> skip
-        keep = [i for i, q in enumerate(qs) if "b" not in q["groupby"]]
-        qs = [qs[i] for i in keep]
-        batch = [batch[i] for i in keep]
-    gpu = run_gpu(db, batch)
+    # h5 is rooted at S: the (g,b) query mixes the root with F, a child with a non-unique key,
+    # so the context computes it at another root (F: g from a primary-key child, b at the root)
+    gpu, info = run_gpu(db, batch, info=True)
+    if name == "h5":
+        roots = {o["root"] for o in info["outputs"]}
+        assert info["roots"][0] == "S" and "F" in roots, info
     for q, (k, v, c) in zip(qs, gpu):
         assert k.tolist() == q["keys"] or (len(q["keys"]) == 0 and k.shape[0] == 0)
         assert c.tolist() == q["counts"]
@@ -48,6 +49,52 @@ def test_chain_each_query_at_its_own_root(root, gbs):
     db = synth.hand_h3(root)
     batch = [query([g], ["1"]) for g in gbs] + [query([], ["1"])]
     _check(db, batch)
+
+
+def _multi_root_case(seed):
+    """Each aggregate to its own root inside one context: group-bys over attributes
+    anywhere in a random acyclic tree — deeper than the root's children, or mixing a non-unique
+    child with other relations — are placed by the context at another root of the same tree
+    (a secondary context, re-rooted and prepared, run on its own stream); every query the
+    engine accepts matches the oracle at the user's root."""
+    from paper_1906_08687_b200 import lmfao
+    db = synth.random_db(300 + seed, max_rels=5, max_rows=500, unique_child_keys=seed % 2 == 0)
+    ints = {a for r in db.relations for a, v in r.cols.items() if v.dtype == np.int32}
+    batch = synth.random_batch(seed, db, n_queries=5, groupby_ok=lambda a: a in ints)
+    ref = oracle.evaluate(db, batch)
+    e = lmfao.Engine()
+    try:
+        for r in db.relations:
+            e.add_relation(r.name, r.cols)
+        e.set_join_tree(db.root, db.edges)
+        e.prepare()
+        kept = []
+        for qi, q in enumerate(batch):
+            try:
+                kept.append((qi, e.add_query(q.groupby, q.udafs)))
+            except lmfao.LmfaoError as ex:
+                assert ex.name == "LMFAO_ERR_UNSUPPORTED", ex
+        e.plan()
+        e.run()
+        info = e.plan_info()
+        got = [e.fetch(q) for _, q in kept]
+    finally:
+        e.close()
+    assert_parity(got, [ref[qi] for qi, _ in kept], [batch[qi] for qi, _ in kept])
+    return info
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_multi_root_plans_random_trees(seed):
+    _multi_root_case(seed)
+
+
+def test_multi_root_used():
+    """The random trees above do route queries to other roots (not only the user's)."""
+    roots = set()
+    for seed in range(10):
+        roots |= {o["root"] for o in _multi_root_case(seed)["outputs"]}
+    assert len(roots) >= 2, roots
 
 
 @pytest.mark.parametrize("seed", range(12))
