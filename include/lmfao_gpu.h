@@ -64,8 +64,8 @@ typedef enum {
   LMFAO_ERR_CYCLIC_TREE = 5,        /* join tree has a cycle */
   LMFAO_ERR_DISCONNECTED_TREE = 6,  /* join tree does not span all relations */
   LMFAO_ERR_RUNNING_INTERSECTION = 7, /* ω_i ∩ ω_j ⊄ ω_k for some R_k on the path */
-  LMFAO_ERR_UNSUPPORTED = 8,        /* limits: join keys of more than two attributes, group-by
-                                       attributes the engine cannot place (see lmfao_add_query) */
+  LMFAO_ERR_UNSUPPORTED = 8,        /* limits: join keys of more than eight attributes, group-by
+                                       attributes no root can place (see lmfao_add_query) */
   LMFAO_ERR_OOM = 9,                /* device allocation failed */
   LMFAO_ERR_CUDA = 10,              /* CUDA runtime error / no device */
   LMFAO_ERR_NCCL = 11               /* NCCL error (multi-GPU) */
@@ -156,9 +156,10 @@ LMFAO_API lmfao_status lmfao_attr_id(lmfao_ctx* ctx, const char* attr_name, int3
 
 /* Registers the rooted join tree: n_edges = m-1 edges parent->child.
  * Validates: connected, acyclic, each relation has at most one parent, the
- * running-intersection property, and that every edge shares one or two
- * attributes, of type int32 (a two-attribute key such as Favorita's (date, store),
- * P:1408-1411, is matched as the pair); otherwise LMFAO_ERR_UNSUPPORTED / _TYPE. */
+ * running-intersection property, and that every edge shares one to eight
+ * attributes, of type int32 (a multi-attribute key such as Favorita's (date, store),
+ * P:1408-1411, is matched as the tuple: a chain of pair dictionaries at prepare);
+ * otherwise LMFAO_ERR_UNSUPPORTED / _TYPE. */
 LMFAO_API lmfao_status lmfao_set_join_tree(lmfao_ctx* ctx, int32_t root_rel, int32_t n_edges,
                                  const int32_t* parent_rel, const int32_t* child_rel);
 

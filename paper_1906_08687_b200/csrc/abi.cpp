@@ -390,8 +390,8 @@ lmfao_status lmfao_set_join_tree(lmfao_ctx* c, int32_t root_rel, int32_t n_edges
     for (auto& col : C.cols)
       if (P.find_attr(col.attr) >= 0) keys.push_back(col.attr);
     std::sort(keys.begin(), keys.end());
-    if (keys.empty() || keys.size() > 2)
-      return fail(c, LMFAO_ERR_UNSUPPORTED, "edge %s-%s shares %zu attributes (one or two supported)",
+    if (keys.empty() || keys.size() > 8)
+      return fail(c, LMFAO_ERR_UNSUPPORTED, "edge %s-%s shares %zu attributes (one to eight supported)",
                   P.name.c_str(), C.name.c_str(), keys.size());
     for (int key : keys)
       if (c->attrs[key].dt != LMFAO_INT32)
@@ -400,15 +400,21 @@ lmfao_status lmfao_set_join_tree(lmfao_ctx* c, int32_t root_rel, int32_t n_edges
     C.key_col = C.find_attr(keys[0]);
     C.key_attr2 = keys.size() > 1 ? keys[1] : -1;
     C.key_col2 = keys.size() > 1 ? C.find_attr(keys[1]) : -1;
+    C.key_cols_more.clear();
+    for (size_t i = 2; i < keys.size(); i++) C.key_cols_more.push_back(C.find_attr(keys[i]));
   }
   for (int u = 0; u < m; u++) {
     c->rels[u].parent = parent[u];
     c->rels[u].children = children[u];
     c->rels[u].fk_col.clear();
     c->rels[u].fk_col2.clear();
+    c->rels[u].fk_cols_more.clear();
     for (int ch : children[u]) {
       c->rels[u].fk_col.push_back(c->rels[u].find_attr(c->rels[ch].key_attr));
       c->rels[u].fk_col2.push_back(c->rels[ch].key_attr2 >= 0 ? c->rels[u].find_attr(c->rels[ch].key_attr2) : -1);
+      std::vector<int> more;
+      for (int kc : c->rels[ch].key_cols_more) more.push_back(c->rels[u].find_attr(c->rels[ch].cols[kc].attr));
+      c->rels[u].fk_cols_more.push_back(more);
     }
   }
   c->root = root_rel;
@@ -445,8 +451,11 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       for (int j : r.fk_col) order.push_back({&r, &r.cols[j]});
       for (int j : r.fk_col2)
         if (j >= 0) order.push_back({&r, &r.cols[j]});
+      for (auto& more : r.fk_cols_more)
+        for (int j : more) order.push_back({&r, &r.cols[j]});
       if (r.key_col >= 0) order.push_back({&r, &r.cols[r.key_col]});
       if (r.key_col2 >= 0) order.push_back({&r, &r.cols[r.key_col2]});
+      for (int j : r.key_cols_more) order.push_back({&r, &r.cols[j]});
     }
     for (int u : post)
       for (auto& col : c->rels[u].cols) order.push_back({&c->rels[u], &col});
@@ -481,7 +490,23 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       CTX_CUDA(c, column_ready(r.cols[r.fk_col[j]], st), "prepare copy");
       DevBuf d;
       CTX_CUDA(c, d.alloc(std::max<int64_t>(r.nrows, 1) * 4), "prepare");
-      if (r.fk_col2[j] >= 0) {  // two-attribute key
+      if (!ch.key_cols_more.empty()) {  // a key of three or more attributes: the chain of pair lookups
+        CTX_CUDA(c, column_ready(r.cols[r.fk_col2[j]], st), "prepare copy");
+        DevBuf t;
+        CTX_CUDA(c, t.alloc(std::max<int64_t>(r.nrows, 1) * 4), "prepare");
+        CTX_CUDA(c, lookup_dense_pair(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.cols[r.fk_col2[j]].buf.as<int32_t>(),
+                                      r.nrows, ch.kdict[0].as<uint64_t>(), ch.kdn[0], t.as<int32_t>(), st),
+                 "prepare remap");
+        for (size_t i = 0; i < ch.key_cols_more.size(); i++) {  // (code of the prefix, next attribute); -1 stays dangling
+          const int fc = r.fk_cols_more[j][i];
+          CTX_CUDA(c, column_ready(r.cols[fc], st), "prepare copy");
+          CTX_CUDA(c, lookup_dense_pair(t.as<int32_t>(), r.cols[fc].buf.as<int32_t>(), r.nrows, ch.kdict[i + 1].as<uint64_t>(),
+                                        ch.kdn[i + 1], d.as<int32_t>(), st),
+                   "prepare remap");
+          std::swap(t, d);
+        }
+        std::swap(t, d);
+      } else if (r.fk_col2[j] >= 0) {  // two-attribute key
         CTX_CUDA(c, column_ready(r.cols[r.fk_col2[j]], st), "prepare copy");
         CTX_CUDA(c, lookup_dense_pair(r.cols[r.fk_col[j]].buf.as<int32_t>(), r.cols[r.fk_col2[j]].buf.as<int32_t>(),
                                       r.nrows, ch.dict.as<uint64_t>(), ch.nkeys, d.as<int32_t>(), st),
@@ -504,7 +529,28 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
       // (3) dictionary of the key to the parent, dense ids, sort by them
       CTX_CUDA(c, column_ready(r.cols[r.key_col], st), "prepare copy");
       DevBuf codes;
-      if (r.key_col2 >= 0) {
+      if (!r.key_cols_more.empty()) {  // three or more attributes: the chain of pair dictionaries
+        CTX_CUDA(c, column_ready(r.cols[r.key_col2], st), "prepare copy");
+        r.kdict.clear();
+        r.kdn.clear();
+        DevBuf dct;
+        int64_t nd = 0;
+        CTX_CUDA(c, dict_encode_pair(r.cols[r.key_col].buf.as<int32_t>(), r.cols[r.key_col2].buf.as<int32_t>(), r.nrows,
+                                     dct, nd, &codes, st),
+                 "prepare dict");
+        r.kdict.push_back(std::move(dct));
+        r.kdn.push_back(nd);
+        for (int kc : r.key_cols_more) {
+          CTX_CUDA(c, column_ready(r.cols[kc], st), "prepare copy");
+          DevBuf next, d2;
+          CTX_CUDA(c, dict_encode_pair(codes.as<int32_t>(), r.cols[kc].buf.as<int32_t>(), r.nrows, d2, nd, &next, st),
+                   "prepare dict");
+          r.kdict.push_back(std::move(d2));
+          r.kdn.push_back(nd);
+          codes = std::move(next);
+        }
+        r.nkeys = nd;
+      } else if (r.key_col2 >= 0) {
         CTX_CUDA(c, column_ready(r.cols[r.key_col2], st), "prepare copy");
         CTX_CUDA(c, dict_encode_pair(r.cols[r.key_col].buf.as<int32_t>(), r.cols[r.key_col2].buf.as<int32_t>(), r.nrows,
                                      r.dict, r.nkeys, &codes, st),

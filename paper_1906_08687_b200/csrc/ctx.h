@@ -29,6 +29,14 @@ struct Rel {
   int key_attr2 = -1, key_col2 = -1;  // second attribute of a two-attribute join key (-1: one attribute)
   std::vector<int> fk_col;   // per child: column of this relation holding the child's key
   std::vector<int> fk_col2;  // per child: the second key column (-1: one attribute)
+  // keys of more than two attributes: the third and later key columns (as a child), and per
+  // child the matching foreign-key columns; the key is dictionary-encoded pairwise in a chain,
+  // (a0, a1) -> c1, (c1, a2) -> c2, ..., each code the rank of its prefix tuple, so the last
+  // code is the rank of the whole tuple (lexicographic)
+  std::vector<int> key_cols_more;
+  std::vector<std::vector<int>> fk_cols_more;
+  std::vector<DevBuf> kdict;     // the chain's pair dictionaries (u64 images), first pair first
+  std::vector<int64_t> kdn;
   // prepared
   int64_t nkeys = 0;
   DevBuf dict;       // sorted distinct key values [nkeys] (int32; u64 pair images for two-attribute keys)

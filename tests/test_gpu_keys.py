@@ -79,3 +79,43 @@ def test_pair_key_many_to_many():
     db = favorita_like(3, 20_000, dup=True)
     batch = cov_batch() + group_batch()[1:]  # (group-bys on T's own attributes need a unique key, v1)
     assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
+
+
+def three_attr_db(seed, n, dangle=0.0, dup=False):
+    """Sales(date, store, item, units) with an inventory child Inv(date, store, item, stock, cat)
+    joined on the three attributes (keys of more than two attributes: a chain of pair
+    dictionaries at prepare), plus Oil(date) and Items(item) on one attribute each."""
+    rng = np.random.default_rng(seed)
+    dates = np.arange(20, dtype=np.int32) * 7 - 30
+    stores = np.arange(6, dtype=np.int32) + 100
+    items = np.arange(40, dtype=np.int32) * 2
+    d, s, i = np.meshgrid(dates, stores, items, indexing="ij")
+    trip = np.stack([d.ravel(), s.ravel(), i.ravel()], 1)
+    trip = trip[rng.random(len(trip)) > 0.3]  # not every triple stocked
+    if dup:
+        trip = np.concatenate([trip, trip[rng.random(len(trip)) > 0.9]])
+    trip = trip[rng.permutation(len(trip))]
+    inv = synth.Relation("V", {"date": trip[:, 0].astype(np.int32), "store": trip[:, 1].astype(np.int32),
+                               "item": trip[:, 2].astype(np.int32), "stock": rng.standard_normal(len(trip)),
+                               "vcat": rng.integers(0, 3, len(trip)).astype(np.int32)})
+    oil = synth.Relation("O", {"date": dates, "price": rng.standard_normal(len(dates))})
+    it = synth.Relation("I", {"item": items, "perish": rng.standard_normal(len(items))})
+    sales = {"date": dates[rng.integers(0, len(dates), n)], "store": stores[rng.integers(0, len(stores), n)],
+             "item": items[rng.integers(0, len(items), n)]}
+    if dangle:
+        sales["item"] = np.where(rng.random(n) < dangle, 7, sales["item"]).astype(np.int32)  # odd: no such item
+    sales["units"] = rng.standard_normal(n)
+    F = synth.Relation("F", sales)
+    return synth.Database([F, inv, oil, it], "F", [("F", "V"), ("F", "O"), ("F", "I")])
+
+
+@pytest.mark.parametrize("n,dangle,dup", [(1, 0.0, False), (3_000, 0.0, False), (40_000, 0.05, False),
+                                          (20_000, 0.0, True)])
+def test_three_attribute_key(n, dangle, dup):
+    db = three_attr_db(4, n, dangle, dup)
+    P, I = synth.Product, synth.ident
+    batch = [synth.covar_batch(["units", "stock", "price", "perish"]),
+             synth.Query(["date"], [[P(1.0, (I("stock"),))], [P(1.0, ())]])]
+    if not dup:  # a group-by on the child's own attribute needs its key unique at this root
+        batch.append(synth.Query(["vcat", "store"], [[P(1.0, (I("units"), I("stock")))]]))
+    assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
