@@ -53,7 +53,8 @@ constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | 
 constexpr int FIN_BLOCKS = 296;
 constexpr int SUM_SPLIT = 8;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int KEYMASK = 0x7fffffff;  // dense key; bit 31 = a run starts at this row (at this level)
+constexpr int KEYMASK = 0x3fffffff;  // dense key; bit 31 = a run starts at this row (at this level),
+constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends after this row
 #ifndef COV_W
 #define COV_W 12  // warps per CTA of the scan (one CTA per SM)
 #endif
@@ -163,15 +164,19 @@ __global__ void k_cov_layout(LayoutArgs a) {
       const int e = 2 * (o - 256), lv = e >> 5, r = e & 31;
       int v[2] = {0, 0};
       if (lv < a.nlev) {
+        auto starts = [&](int64_t row) {  // a run starts at `row` at level lv
+          if (row == 0 || row >= a.N) return true;
+          for (int l = lv; l < a.nlev; l++)
+            if (a.key[l][row] != a.key[l][row - 1]) return true;
+          return false;
+        };
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const int64_t row = 32 * b + r + h;
           if (row < a.N) {
-            bool start = row == 0;
-            for (int l = lv; l < a.nlev && !start; l++) start = a.key[l][row] != a.key[l][row - 1];
-            v[h] = a.key[lv][row] | (start ? (int)0x80000000u : 0);
+            v[h] = a.key[lv][row] | (starts(row) ? (int)0x80000000u : 0) | (starts(row + 1) ? RUN_END : 0);
           } else {
-            v[h] = a.pad[lv] | (row == a.N ? (int)0x80000000u : 0);
+            v[h] = a.pad[lv] | (row == a.N ? (int)0x80000000u : 0) | (row == 32 * a.nblk - 1 ? RUN_END : 0);
           }
         }
       }
@@ -203,9 +208,9 @@ struct CovCfg {
 };
 
 // NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L); W warps per CTA.
-//
-// Per 32-row block, lane (m, k) = (lane / 4, lane % 4) holds, for DMMA group j (rows 4j..4j+3),
-// feature m of row 4j + k.  Paths by the block's level-A / level-B run starts (flags):
+// The per-warp state and per-block work of the scan (shared by k_cov and k_cov_ws): lane (m, k)
+// = (lane / 4, lane % 4) holds, for DMMA group j (rows 4j..4j+3), feature m of row 4j + k.
+// Paths by the block's level-A / level-B run starts (flags of the scan layout):
 //  * fast (no A run starts inside): per-row products; v = [x, s_L0..7, (s_L8, s_L9, 1)] is
 //    summed per lane into the open A run's carry C; when the run ends (at a block end) the
 //    carry times the run's s_A row is one DMMA per tile (the DMMA's k = 4 sums the lanes'
@@ -213,89 +218,30 @@ struct CovCfg {
 //  * cold (A run starts inside, no B start): every row's v times its own s_A row (the same
 //    sum by linearity: Σ_run (Σ_rows v) ⊗ s_A = Σ_rows v ⊗ s_A(row)), no segments;
 //  * slow (B run starts inside; rare): the cold product once per B segment, masked to its rows.
-template <int NS, int W>
-__global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
-  using Cfg = CovCfg<W>;
-  constexpr int CF = Cfg::CF;
-  const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, wib = threadIdx.x >> 5;
-  const int gw = blockIdx.x * W + wib;
-  extern __shared__ __align__(1024) unsigned char sm[];
-  int* cta_done = reinterpret_cast<int*>(sm);
-  int* hkey = reinterpret_cast<int*>(sm + 128);
-  unsigned* hcnt = reinterpret_cast<unsigned*>(sm + 128 + HT * 4);
-  unsigned char* wbase = sm + 128 + HT * 8 + wib * Cfg::WB;
-  unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
-  uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
-  int* ring = reinterpret_cast<int*>(bar_f + 4);  // [8] item ids grabbed by this warp, in order
-
-  for (int i = threadIdx.x; i < HT; i += blockDim.x) {
-    hkey[i] = -1;
-    hcnt[i] = 0;
-  }
-  if (threadIdx.x == 0) *cta_done = 0;
-  if (lane == 0) {
-    for (int s = 0; s < CF; s++) mbar_init(&bar_f[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  // ---- schedule: item gw (a static chunk), then items grabbed dynamically; this warp's items in
-  // grab order in a ring.  Every item has at least CF blocks (plan), so the fact look-ahead (CF
-  // blocks) is never more than one item ahead of the block being processed.
-  const int nitems = g.nitems;
-  int nring = 0;
-  auto grab = [&]() {  // the static chunk first; dynamic items when needed (no grab ahead: a
-                       // prefetched tail item would wait behind the warp's current one)
-    int it = 0;
-    if (lane == 0) it = nring == 0 && gw < g.nstatic ? gw : g.nstatic + atomicAdd(g.work, 1);
-    it = __shfl_sync(FULL, it, 0);
-    if (lane == 0) ring[nring & 7] = it;
-    nring++;
-    __syncwarp();
-  };
-  int rec = 0;  // the current item's next level-B record slot
-
-  auto issue_fact = [&](int64_t b, int stage) {
-    if (lane == 0) {  // the slot was only read (generic proxy) since its last fill: no proxy fence needed
-      mbar_expect(&bar_f[stage], SBLK);
-      bulk_load(wbase + stage * SBLK, g.scan + b * SBLK, SBLK, &bar_f[stage]);
-    }
-  };
-  // view rows s_L[k_L(row)] of a landed fact block -> gather slot [32 rows x 96 B]; 16-byte
-  // chunk c = 32 i + lane (row c / 6), so each instruction covers ~5 whole rows (coalesced)
-  int ch_row[6], ch_off[6];
-#pragma unroll
-  for (int i = 0; i < 6; i++) {
-    const int c = 32 * i + lane;
-    ch_row[i] = c / 6;
-    ch_off[i] = (c % 6) * 16;
-  }
-  auto issue_gather = [&](int stage, int gslot) {
-    if (!(g.ablate & 1)) {
-      const int kl = reinterpret_cast<const int*>(wbase + stage * SBLK + 2048)[lane] & KEYMASK;
-      const char* vl = reinterpret_cast<const char*>(g.VL);
-      const uint32_t dst = sa(gbase + gslot * STG_G) + 16 * lane;
-#pragma unroll
-      for (int i = 0; i < 6; i++) {
-        const unsigned key = (unsigned)__shfl_sync(FULL, kl, ch_row[i]);
-        cp16full(dst + 512 * i, vl + key * (unsigned)(GP * 8) + (unsigned)ch_off[i]);
-      }
-    }
-  };
-
-  // ---- accumulators (lane (m, k): feature m, rows 4j + k)
+template <int NS>
+struct CovWarp {
+  const CovArgs& g;
+  const int lane, k, m, tcol;
+  int* hkey;
+  unsigned* hcnt;
+  int rec = 0;           // the current item's next level-B record slot
+  bool carried = false;  // C holds rows of the open level-A run
+  // accumulators
   double aXL[2] = {0, 0};                              // x ⊗ s_L0..7 (DMMA)
   double aXX[2] = {0, 0}, aXT[2] = {0, 0};             // COV_XX_DMMA: x ⊗ x, x ⊗ [s_L8, s_L9, 1] (DMMA)
-  double xx0 = 0, xx1 = 0, xx2 = 0, xx3 = 0, xx4 = 0;  // x_m · x_{(m+d)%8}, d = 0..4
-  double x8 = 0, x9 = 0;                               // x_m · s_L8, x_m · s_L9
+  double xx0 = 0, xx1 = 0, xx2 = 0, xx3 = 0, xx4 = 0;  // x_m · x_{(m+d)%8}, d = 0..4 (COV_XX_DMMA=0)
+  double x8 = 0, x9 = 0;                               // x_m · s_L8, x_m · s_L9 (COV_XX_DMMA=0)
   double C0 = 0, C1 = 0, C2 = 0;                       // open A run: Σ x_m, Σ s_L_m, Σ t_m (this lane's rows)
   double aRA0[2] = {0, 0}, aRA1[2] = {0, 0}, aRA2[2] = {0, 0};  // [x | s_L0..7 | t] ⊗ s_A0..7 (DMMA)
   double r8x = 0, r9x = 0, r8l = 0, r9l = 0, r8t = 0, r9t = 0;   // ... ⊗ s_A8, s_A9
   double tA8 = 0, tA9 = 0;                                       // s_L8 · s_A_m, s_L9 · s_A_m (per row)
   double SB0 = 0, SB1 = 0, SB2 = 0, SBn = 0, SBn8 = 0, SBn9 = 0;  // open B run: Σ v, Σ s_A
-  const int tcol = m < 3 ? 8 + m : 11;  // t tile: s_L8, s_L9, 1 (view column 10 holds 1.0), 0
 
-  auto hl_add = [&](int key, unsigned len) {  // two probes, straight-line; full: global RED
+  __device__ __forceinline__ CovWarp(const CovArgs& g_, int lane_, int* hk, unsigned* hc)
+      : g(g_), lane(lane_), k(lane_ & 3), m(lane_ >> 2), tcol((lane_ >> 2) < 3 ? 8 + (lane_ >> 2) : 11), hkey(hk),
+        hcnt(hc) {}
+
+  __device__ __forceinline__ void hl_add(int key, unsigned len) {  // two probes, straight-line; full: global RED
     unsigned h = ((unsigned)key * 2654435761u) >> (32 - COV_HT_BITS);
     int t = hkey[h];
     if (t == -1) {
@@ -312,8 +258,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     }
     if (t == key) atomicAdd(&hcnt[h], len);
     else gred_add(&g.HL[key], len);
-  };
-  auto push_B = [&](int keyB) {  // the open B run's record -> this warp's next slot
+  }
+  __device__ __forceinline__ void push_B(int keyB) {  // the open B run's record -> the item's next slot
     const double v0 = red4(SB0), v1 = red4(SB1), v2 = red4(SB2), v3 = red4(SBn), v4 = red4(SBn8), v5 = red4(SBn9);
     double* r = g.brec + (size_t)rec * BRW;
     if (k == 0) {
@@ -330,9 +276,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     }
     rec++;
     SB0 = SB1 = SB2 = SBn = SBn8 = SBn9 = 0.0;
-  };
+  }
   // the carried rows of the A run with key keyA: C ⊗ s_A(keyA), into the B sums, H_A
-  auto flush_carry = [&](int keyA) {
+  __device__ __forceinline__ void flush_carry(int keyA) {
     const double* ar = g.VA + (size_t)(unsigned)keyA * GP;
     const double b0v = ar[m];
     const double2 b89 = ld2(ar + 8);
@@ -355,10 +301,9 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     SBn9 = fma(nq, b89.y, SBn9);
     if (NS >= 1 && lane == 0 && n > 0.0) gred_add(&g.HA[keyA], (unsigned)n);
     C0 = C1 = C2 = 0.0;
-  };
-
+  }
   // the item's partial (every entry written; both triangles of XX); then the accumulators restart
-  auto store_partial = [&](int item) {
+  __device__ __forceinline__ void store_partial(int item) {
     const double q0 = red4(xx0), q1 = red4(xx1), q2 = red4(xx2), q3 = red4(xx3), q4 = red4(xx4);
     const double q8 = red4(x8), q9 = red4(x9);
     const double s8x = red4(r8x), s9x = red4(r9x), s8l = red4(r8l), s9l = red4(r9l), s8t = red4(r8t), s9t = red4(r9t);
@@ -366,7 +311,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     double* out = g.partials + (size_t)item * NPART;
     if (k == 0) {
       const double qd[5] = {q0, q1, q2, q3, q4};
-  #pragma unroll
+#pragma unroll
       for (int d = 0; d < 5; d++) {
         const int n = (m + d) & 7;
         if (d < 4 || m < 4) {
@@ -410,6 +355,244 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     aRA0[0] = aRA0[1] = aRA1[0] = aRA1[1] = aRA2[0] = aRA2[1] = 0.0;
     r8x = r9x = r8l = r9l = r8t = r9t = tA8 = tA9 = 0.0;
     __syncwarp();
+  }
+
+  // One 32-row block: st = its scan-layout block, gs = its gathered view rows [32][GP].  An item's
+  // first row starts runs at every level, its last row ends them.
+  __device__ __forceinline__ void block(const unsigned char* st, const double* gs, bool first_of_item,
+                                        bool last_of_item) {
+    const double* xs = reinterpret_cast<const double*>(st);
+    const int* ks = reinterpret_cast<const int*>(st + 2048);
+    const int klr = ks[lane];
+    const int kar = NS >= 1 ? ks[32 + lane] : 0;
+    const int kbr = NS == 2 ? ks[64 + lane] : 0;
+    const int kl = klr & KEYMASK, ka = kar & KEYMASK, kb = kbr & KEYMASK;
+    const unsigned first = first_of_item ? 1u : 0u;
+    const unsigned mL = __ballot_sync(FULL, klr < 0) | first;
+    const unsigned mA = (NS >= 1 ? __ballot_sync(FULL, kar < 0) : 0u) | first;
+    const unsigned mB = (NS == 2 ? __ballot_sync(FULL, kbr < 0) : 0u) | first;
+    // does the run open at this block's end end here? (the row-31 end flags, or the item's end)
+    const int ends = __shfl_sync(FULL, (kar & RUN_END ? 1 : 0) | (kbr & RUN_END ? 2 : 0), 31);
+    const bool endA = last_of_item || (NS >= 1 && (ends & 1));
+    const bool endB = last_of_item || (NS == 2 && (ends & 2));
+    if (!(g.ablate & 8) && (((mL >> lane) & 1u) || lane == 0)) {  // H_L: each L run's rows in the block
+      const unsigned above = mL & ~((2u << lane) - 1u);
+      hl_add(kl, (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
+    }
+    const double* gl = gs + k * GP;
+    // per-row products of group j; returns the lane's operands for the run-level work
+    auto rowpart = [&](int j, double& xa, double& sv, double2& s89, double& tv) {
+      xa = xs[32 * j + lane];
+      const double* gr = gl + j * 4 * GP;
+      sv = gr[m];
+      tv = gr[tcol];
+      if (COV_XX_DMMA) {
+        dmma(aXX, xa, xa);
+        dmma(aXL, xa, sv);
+        dmma(aXT, xa, tv);
+        s89 = make_double2(0.0, 0.0);
+        return;
+      }
+      s89 = ld2(gr + 8);
+      const double xd1 = xs[32 * j + ((lane + 4) & 31)];
+      const double xd2 = xs[32 * j + ((lane + 8) & 31)];
+      const double xd3 = xs[32 * j + ((lane + 12) & 31)];
+      const double xd4 = xs[32 * j + ((lane + 16) & 31)];
+      dmma(aXL, xa, sv);
+      xx0 = fma(xa, xa, xx0);
+      xx1 = fma(xa, xd1, xx1);
+      xx2 = fma(xa, xd2, xx2);
+      xx3 = fma(xa, xd3, xx3);
+      xx4 = fma(xa, xd4, xx4);
+      x8 = fma(xa, s89.x, x8);
+      x9 = fma(xa, s89.y, x9);
+    };
+    // row-level A products of group j (rows masked to [lo, hi) when MASK)
+    auto cold_group = [&](auto mask_tag, int j, double xa, double sv, double2 s89, double tv, double sam,
+                          double2 sa89, int lo, int hi) {
+      constexpr bool MASK = decltype(mask_tag)::value;
+      if (MASK) {
+        const int r = 4 * j + k;
+        const double mk = (r >= lo && r < hi) ? 1.0 : 0.0;
+        xa *= mk;
+        sv *= mk;
+        tv *= mk;
+        s89.x *= mk;
+        s89.y *= mk;
+        sa89.x *= mk;
+        sa89.y *= mk;
+        sam *= mk;
+      }
+      if (COV_XX_DMMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
+      dmma(aRA0, xa, sam);
+      dmma(aRA1, sv, sam);
+      tA8 = fma(s89.x, sam, tA8);
+      tA9 = fma(s89.y, sam, tA9);
+      r8x = fma(xa, sa89.x, r8x);
+      r9x = fma(xa, sa89.y, r9x);
+      r8l = fma(sv, sa89.x, r8l);
+      r9l = fma(sv, sa89.y, r9l);
+      r8t = fma(tv, sa89.x, r8t);
+      r9t = fma(tv, sa89.y, r9t);
+      SB0 += xa;
+      SB1 += sv;
+      SB2 += tv;
+      SBn += sam;
+      SBn8 += sa89.x;
+      SBn9 += sa89.y;
+    };
+    // s_A rows of this lane's rows in groups 4h .. 4h+3 (loads in flight together)
+    auto load_sa = [&](int h, double (&sam)[4], double2 (&sa89)[4]) {
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        const unsigned key = (unsigned)__shfl_sync(FULL, ka, 4 * (4 * h + jj) + k);
+        const double* ar = g.VA + (size_t)key * GP;
+        sam[jj] = ar[m];
+        sa89[jj] = ld2(ar + 8);
+      }
+    };
+    // H_A: each A run's rows in this block (the carried rows were added by flush_carry)
+    auto ha_runs = [&]() {
+      if (((mA >> lane) & 1u) || lane == 0) {
+        const unsigned above = mA & ~((2u << lane) - 1u);
+        gred_add(&g.HA[ka], (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
+      }
+    };
+    const unsigned mBi = NS == 2 ? (mB & ~1u) : 0u;
+    if (NS >= 1 && mBi) {
+      // slow: level-B runs start inside the block
+      if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
+      carried = false;
+      ha_runs();
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        double xa, sv, tv;
+        double2 s89;
+        rowpart(j, xa, sv, s89, tv);
+      }
+      unsigned bits = mBi;
+      int lo = 0;
+      while (true) {
+        const int hi = bits ? __ffs(bits) - 1 : 32;
+#pragma unroll 1
+        for (int h = 0; h < 2; h++) {
+          double sam[4];
+          double2 sa89[4];
+          load_sa(h, sam, sa89);
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            const int j = 4 * h + jj;
+            const double* gr = gl + j * 4 * GP;
+            cold_group(std::true_type{}, j, xs[32 * j + lane], gr[m], ld2(gr + 8), gr[tcol], sam[jj], sa89[jj], lo, hi);
+          }
+        }
+        if (hi == 32) break;
+        push_B(__shfl_sync(FULL, kb, hi - 1));
+        lo = hi;
+        bits &= bits - 1;
+      }
+    } else if (NS >= 1 && ((mA & ~1u) || g.cold_all) && !(g.ablate & 32)) {
+      // cold: level-A runs start inside the block; every row times its own s_A row
+      if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
+      carried = false;
+      ha_runs();
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        double sam[4];
+        double2 sa89[4];
+        load_sa(h, sam, sa89);
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) {
+          double xa, sv, tv;
+          double2 s89;
+          rowpart(4 * h + jj, xa, sv, s89, tv);
+          cold_group(std::false_type{}, 4 * h + jj, xa, sv, s89, tv, sam[jj], sa89[jj], 0, 32);
+        }
+      }
+    } else {
+      // fast: the open A run goes on through the block
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        double xa, sv, tv;
+        double2 s89;
+        rowpart(j, xa, sv, s89, tv);
+        C0 += xa;
+        C1 += sv;
+        C2 += tv;
+      }
+      carried = !endA;
+      if (endA) flush_carry(__shfl_sync(FULL, ka, 31));
+    }
+    if (endB) push_B(__shfl_sync(FULL, kb, 31));
+  }
+};
+
+// view rows s_L[k_L(row)] of a landed fact block -> a gather slot [32 rows x 96 B]; 16-byte chunk
+// c = 32 i + lane (row c / 6), so each instruction covers ~5 whole rows (coalesced)
+__device__ __forceinline__ void gather_rows(const CovArgs& g, const unsigned char* fact, uint32_t dst_slot, int lane) {
+  const int kl = reinterpret_cast<const int*>(fact + 2048)[lane] & KEYMASK;
+  const char* vl = reinterpret_cast<const char*>(g.VL);
+  const uint32_t dst = dst_slot + 16 * lane;
+#pragma unroll
+  for (int i = 0; i < 6; i++) {
+    const int c = 32 * i + lane;
+    const unsigned key = (unsigned)__shfl_sync(FULL, kl, c / 6);
+    cp16full(dst + 512 * i, vl + key * (unsigned)(GP * 8) + (unsigned)((c % 6) * 16));
+  }
+}
+
+// The scan, every warp its own pipeline: the CF-deep fact ring (bulk copies), the view-row
+// gathers one block ahead (cp.async), and the work schedule — item gw (a static chunk), then
+// items grabbed dynamically — all in the computing warp.
+template <int NS, int W>
+__global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovArgs g) {
+  using Cfg = CovCfg<W>;
+  constexpr int CF = Cfg::CF;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gw = blockIdx.x * W + wib;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  int* cta_done = reinterpret_cast<int*>(sm);
+  int* hkey = reinterpret_cast<int*>(sm + 128);
+  unsigned* hcnt = reinterpret_cast<unsigned*>(sm + 128 + HT * 4);
+  unsigned char* wbase = sm + 128 + HT * 8 + wib * Cfg::WB;
+  unsigned char* gbase = wbase + CF * SBLK;  // 2 gather slots
+  uint64_t* bar_f = reinterpret_cast<uint64_t*>(gbase + 2 * STG_G);
+  int* ring = reinterpret_cast<int*>(bar_f + 4);  // [8] item ids grabbed by this warp, in order
+
+  for (int i = threadIdx.x; i < HT; i += blockDim.x) {
+    hkey[i] = -1;
+    hcnt[i] = 0;
+  }
+  if (threadIdx.x == 0) *cta_done = 0;
+  if (lane == 0) {
+    for (int s = 0; s < CF; s++) mbar_init(&bar_f[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  CovWarp<NS> w(g, lane, hkey, hcnt);
+
+  // ---- schedule: item gw (a static chunk), then items grabbed dynamically; this warp's items in
+  // grab order in a ring.  Every item has at least CF blocks (plan), so the fact look-ahead (CF
+  // blocks) is never more than one item ahead of the block being processed.
+  const int nitems = g.nitems;
+  int nring = 0;
+  auto grab = [&]() {  // the static chunk first; dynamic items when needed (no grab ahead: a
+                       // prefetched tail item would wait behind the warp's current one)
+    int it = 0;
+    if (lane == 0) it = nring == 0 && gw < g.nstatic ? gw : g.nstatic + atomicAdd(g.work, 1);
+    it = __shfl_sync(FULL, it, 0);
+    if (lane == 0) ring[nring & 7] = it;
+    nring++;
+    __syncwarp();
+  };
+  auto issue_fact = [&](int64_t b, int stage) {
+    if (lane == 0) {  // the slot was only read (generic proxy) since its last fill: no proxy fence needed
+      mbar_expect(&bar_f[stage], SBLK);
+      bulk_load(wbase + stage * SBLK, g.scan + b * SBLK, SBLK, &bar_f[stage]);
+    }
+  };
+  auto issue_gather = [&](int stage, int gslot) {
+    if (!(g.ablate & 1)) gather_rows(g, wbase + stage * SBLK, sa(gbase + gslot * STG_G), lane);
   };
 
   // ---- pipeline prologue: the first CF blocks of the sequence in flight, gathers of block 0
@@ -419,7 +602,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   if (pitem < nitems) {
     pb = pbeg = g.item[pitem];
     pend = g.item[pitem + 1];
-    rec = g.rec_base[pitem];
+    w.rec = g.rec_base[pitem];
   }
   int fslot = 0, fitem = pitem, fb = pb, fend = pend;  // the next block to load (look-ahead)
   auto f_advance = [&]() {
@@ -443,12 +626,10 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
   cp_commit();
   int fs = 0;  // position in the sequence % CF
   uint32_t fph = 0;
-  bool carried = false;  // C holds rows of the open level-A run
   for (int i = 0; pitem < nitems; i++) {
     const bool next_in_item = pb + 1 < pend;
     const int nitem = next_in_item ? pitem : ring[(pslot + 1) & 7];  // (grabbed by the look-ahead)
     const bool has_next = nitem < nitems;
-    const bool first_of_item = pb == pbeg;
     const int fs1 = fs + 1 == CF ? 0 : fs + 1;
     const uint32_t fph1 = fs + 1 == CF ? fph ^ 1u : fph;
     if (has_next) {  // gathers of the next block (its keys land first)
@@ -458,191 +639,21 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     cp_commit();
     cp_wait1();  // this block's gathers have landed
     __syncwarp();
-    const unsigned char* st = wbase + fs * SBLK;
-    const double* xs = reinterpret_cast<const double*>(st);
-    const int* ks = reinterpret_cast<const int*>(st + 2048);
-    const double* gs = reinterpret_cast<const double*>(gbase + (i & 1) * STG_G);
-    if (!(g.ablate & 16)) {
-      const int klr = ks[lane];
-      const int kar = NS >= 1 ? ks[32 + lane] : 0;
-      const int kbr = NS == 2 ? ks[64 + lane] : 0;
-      const int kl = klr & KEYMASK, ka = kar & KEYMASK, kb = kbr & KEYMASK;
-      const unsigned first = first_of_item ? 1u : 0u;  // an item's first row starts runs at every level
-      const unsigned mL = __ballot_sync(FULL, klr < 0) | first;
-      const unsigned mA = (NS >= 1 ? __ballot_sync(FULL, kar < 0) : 0u) | first;
-      const unsigned mB = (NS == 2 ? __ballot_sync(FULL, kbr < 0) : 0u) | first;
-      // does the run open at this block's end end here? (item end, or the next block's row 0
-      // starts a run at that level)
-      bool endA = true, endB = true;
-      if (next_in_item) {
-        const int* kn = reinterpret_cast<const int*>(wbase + fs1 * SBLK + 2048);
-        endB = NS == 2 ? kn[64] < 0 : false;
-        endA = NS >= 1 ? kn[32] < 0 : false;
-      }
-      if (!(g.ablate & 8) && (((mL >> lane) & 1u) || lane == 0)) {  // H_L: each L run's rows in the block
-        const unsigned above = mL & ~((2u << lane) - 1u);
-        hl_add(kl, (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
-      }
-      const double* gl = gs + k * GP;
-      // per-row products of group j; returns the lane's operands for the run-level work
-      auto rowpart = [&](int j, double& xa, double& sv, double2& s89, double& tv) {
-        xa = xs[32 * j + lane];
-        const double* gr = gl + j * 4 * GP;
-        sv = gr[m];
-        tv = gr[tcol];
-        if (COV_XX_DMMA) {
-          dmma(aXX, xa, xa);
-          dmma(aXL, xa, sv);
-          dmma(aXT, xa, tv);
-          s89 = make_double2(0.0, 0.0);
-          return;
-        }
-        s89 = ld2(gr + 8);
-        const double xd1 = xs[32 * j + ((lane + 4) & 31)];
-        const double xd2 = xs[32 * j + ((lane + 8) & 31)];
-        const double xd3 = xs[32 * j + ((lane + 12) & 31)];
-        const double xd4 = xs[32 * j + ((lane + 16) & 31)];
-        dmma(aXL, xa, sv);
-        xx0 = fma(xa, xa, xx0);
-        xx1 = fma(xa, xd1, xx1);
-        xx2 = fma(xa, xd2, xx2);
-        xx3 = fma(xa, xd3, xx3);
-        xx4 = fma(xa, xd4, xx4);
-        x8 = fma(xa, s89.x, x8);
-        x9 = fma(xa, s89.y, x9);
-      };
-      // row-level A products of group j (rows masked to [lo, hi) when MASK)
-      auto cold_group = [&](auto mask_tag, int j, double xa, double sv, double2 s89, double tv, double sam,
-                            double2 sa89, int lo, int hi) {
-        constexpr bool MASK = decltype(mask_tag)::value;
-        if (MASK) {
-          const int r = 4 * j + k;
-          const double mk = (r >= lo && r < hi) ? 1.0 : 0.0;
-          xa *= mk;
-          sv *= mk;
-          tv *= mk;
-          s89.x *= mk;
-          s89.y *= mk;
-          sa89.x *= mk;
-          sa89.y *= mk;
-          sam *= mk;
-        }
-        if (COV_XX_DMMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
-        dmma(aRA0, xa, sam);
-        dmma(aRA1, sv, sam);
-        tA8 = fma(s89.x, sam, tA8);
-        tA9 = fma(s89.y, sam, tA9);
-        r8x = fma(xa, sa89.x, r8x);
-        r9x = fma(xa, sa89.y, r9x);
-        r8l = fma(sv, sa89.x, r8l);
-        r9l = fma(sv, sa89.y, r9l);
-        r8t = fma(tv, sa89.x, r8t);
-        r9t = fma(tv, sa89.y, r9t);
-        SB0 += xa;
-        SB1 += sv;
-        SB2 += tv;
-        SBn += sam;
-        SBn8 += sa89.x;
-        SBn9 += sa89.y;
-      };
-      // s_A rows of this lane's rows in groups 4h .. 4h+3 (loads in flight together)
-      auto load_sa = [&](int h, double (&sam)[4], double2 (&sa89)[4]) {
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          const unsigned key = (unsigned)__shfl_sync(FULL, ka, 4 * (4 * h + jj) + k);
-          const double* ar = g.VA + (size_t)key * GP;
-          sam[jj] = ar[m];
-          sa89[jj] = ld2(ar + 8);
-        }
-      };
-      // H_A: each A run's rows in this block (the carried rows were added by flush_carry)
-      auto ha_runs = [&]() {
-        if (((mA >> lane) & 1u) || lane == 0) {
-          const unsigned above = mA & ~((2u << lane) - 1u);
-          gred_add(&g.HA[ka], (unsigned)((above ? __ffs(above) - 1 : 32) - lane));
-        }
-      };
-      const unsigned mBi = NS == 2 ? (mB & ~1u) : 0u;
-      if (NS >= 1 && mBi) {
-        // slow: level-B runs start inside the block
-        if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
-        carried = false;
-        ha_runs();
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-          double xa, sv, tv;
-          double2 s89;
-          rowpart(j, xa, sv, s89, tv);
-        }
-        unsigned bits = mBi;
-        int lo = 0;
-        while (true) {
-          const int hi = bits ? __ffs(bits) - 1 : 32;
-#pragma unroll 1
-          for (int h = 0; h < 2; h++) {
-            double sam[4];
-            double2 sa89[4];
-            load_sa(h, sam, sa89);
-#pragma unroll
-            for (int jj = 0; jj < 4; jj++) {
-              const int j = 4 * h + jj;
-              const double* gr = gl + j * 4 * GP;
-              cold_group(std::true_type{}, j, xs[32 * j + lane], gr[m], ld2(gr + 8), gr[tcol], sam[jj], sa89[jj], lo,
-                         hi);
-            }
-          }
-          if (hi == 32) break;
-          push_B(__shfl_sync(FULL, kb, hi - 1));
-          lo = hi;
-          bits &= bits - 1;
-        }
-      } else if (NS >= 1 && ((mA & ~1u) || g.cold_all) && !(g.ablate & 32)) {
-        // cold: level-A runs start inside the block; every row times its own s_A row
-        if (carried) flush_carry(__shfl_sync(FULL, ka, 0));
-        carried = false;
-        ha_runs();
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          double sam[4];
-          double2 sa89[4];
-          load_sa(h, sam, sa89);
-#pragma unroll
-          for (int jj = 0; jj < 4; jj++) {
-            double xa, sv, tv;
-            double2 s89;
-            rowpart(4 * h + jj, xa, sv, s89, tv);
-            cold_group(std::false_type{}, 4 * h + jj, xa, sv, s89, tv, sam[jj], sa89[jj], 0, 32);
-          }
-        }
-      } else {
-        // fast: the open A run goes on through the block
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-          double xa, sv, tv;
-          double2 s89;
-          rowpart(j, xa, sv, s89, tv);
-          C0 += xa;
-          C1 += sv;
-          C2 += tv;
-        }
-        carried = !endA;
-        if (endA) flush_carry(__shfl_sync(FULL, ka, 31));
-      }
-      if (endB) push_B(__shfl_sync(FULL, kb, 31));
-    }
+    if (!(g.ablate & 16))
+      w.block(wbase + fs * SBLK, reinterpret_cast<const double*>(gbase + (i & 1) * STG_G), pb == pbeg, !next_in_item);
     __syncwarp();
     if (fitem < nitems) issue_fact(fb, fs);  // the slot just consumed takes the block CF ahead
     f_advance();
     if (next_in_item) {
       pb++;
     } else {  // the item is done: its partial -> partials[item], accumulators cleared
-      store_partial(pitem);
+      w.store_partial(pitem);
       pslot++;
       pitem = nitem;
       if (has_next) {
         pb = pbeg = g.item[pitem];
         pend = g.item[pitem + 1];
-        rec = g.rec_base[pitem];
+        w.rec = g.rec_base[pitem];
       }
     }
     fs = fs1;
@@ -663,6 +674,8 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     }
   }
 }
+
+
 
 // V[k][f] = col_f[k] for f < n, 0 for n <= f < GP, except V[k][10] = 1 (the constant of the
 // scan's t tile; primary-key leaf: row k has dense key k).
@@ -878,7 +891,7 @@ struct FastCov : FastPaths {
   int run(lmfao_ctx* c, const NodeArgs& ra, cudaStream_t st, bool& scalar_done) override;
 };
 
-int cov_warps() { return COV_W; }
+
 
 template <int W>
 cudaError_t cov_kernel_attr(int NS) {  // per device: called at plan time on the ctx's device
