@@ -34,6 +34,9 @@ constexpr int kUnrollSmall = CNT_UNROLL_SMALL, kUnrollBig = CNT_UNROLL_BIG;
 
 struct CntQuery {
   int8_t a, b;      // attribute slots (b = -1: one attribute)
+  int8_t run;       // >= 0: both attributes belong to dimensions, the deeper at sort position
+                    // `run`: the cell is constant over a run at that level, counted once per run
+                    // (segment) with the run's length; -1: per row
   int32_t sa;       // cell = code_a * sa + code_b
   unsigned long long* counts;
   int32_t soff;     // >= 0: counted in the CTA's shared table at this offset (small tables)
@@ -51,6 +54,9 @@ struct CntArgs {
   const CntQuery* q;             // [nq] per-row queries
   int nsmall;                    // shared counters of the small tables
   int nsq;                       // queries [0, nsq) count in shared memory
+  int nsq_row, ngq_row;          // ... of which [0, nsq_row) per row; global ones [nsq, ngq_row) per row
+  int8_t pos[CN_LEV];            // sort position (P:1052 order) of each child
+  int8_t at[CN_LEV];             // child at each sort position
   unsigned long long* total;     // COUNT
 };
 
@@ -59,7 +65,7 @@ struct CntArgs {
 // branch-free; a one-attribute query reads the all-zero code row (slot nattr) as its second code.
 __global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntArgs a) {
   extern __shared__ __align__(16) unsigned char cnsm[];
-  int4* sq = reinterpret_cast<int4*>(cnsm);  // {a, b, sa, soff}
+  int4* sq = reinterpret_cast<int4*>(cnsm);  // {a, b, sa, soff}; the run level in soff's top byte
   unsigned long long** sp = reinterpret_cast<unsigned long long**>(cnsm + (size_t)a.nq * 16);
   // per warp: codes [nattr + 1][32] (row nattr = 0), then dense keys [nlev][32]
   const int wrows = a.nattr + 1 + a.nlev;
@@ -67,7 +73,7 @@ __global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntAr
   unsigned* stab = reinterpret_cast<unsigned*>(wsm + (blockDim.x >> 5) * 32 * wrows);
   for (int i = threadIdx.x; i < a.nq; i += blockDim.x) {
     const CntQuery q = a.q[i];
-    sq[i] = make_int4(q.a, q.b >= 0 ? q.b : a.nattr, q.sa, q.soff);
+    sq[i] = make_int4(q.a | ((int)(q.run + 1) << 8), q.b >= 0 ? q.b : a.nattr, q.sa, q.soff);
     sp[i] = q.counts;
   }
   for (int i = threadIdx.x; i < a.nsmall; i += blockDim.x) stab[i] = 0u;
@@ -89,6 +95,26 @@ __global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntAr
         key[l] = v ? a.fk[l][row] : 0;
         skey[32 * l] = key[l];
       }
+    // run starts per sort position p: a key at a position <= p differs from the previous row's
+    // (the block's first row always starts; runs split at block edges are counted in parts)
+    unsigned smask[CN_LEV];
+    {
+      bool chg = lane == 0;
+      const int64_t rem = a.nrows - base - (threadIdx.x & ~31);
+      const int nvb = rem < 32 ? (int)rem : 32;
+#pragma unroll
+      for (int p = 0; p < CN_LEV; p++) {
+        if (p >= a.nlev) break;
+        const int l = a.at[p];
+        int kl = 0;
+#pragma unroll
+        for (int t = 0; t < CN_LEV; t++)
+          if (t == l) kl = key[t];
+        const int kp = __shfl_up_sync(CFULL, kl, 1);
+        chg = chg || kp != kl;
+        smask[p] = __ballot_sync(CFULL, v && chg) | (nvb < 32 ? (~0u << (nvb > 0 ? nvb : 0)) : 0u);
+      }
+    }
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < CN_ATTR; i++) {
@@ -107,21 +133,43 @@ __global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntAr
       const unsigned peers = __match_any_sync(CFULL, k);
       if (v && (__ffs(peers) - 1) == lane) atomicAdd(&a.H[l][k], (unsigned)__popc(peers));
     }
+    // a lane starting a run segment at position p: the segment's rows in this block
+    auto seg_len = [&](int p, bool& start) -> unsigned {
+      unsigned m = 0;
+#pragma unroll
+      for (int t = 0; t < CN_LEV; t++)
+        if (t == p) m = smask[t];
+      start = v && ((m >> lane) & 1u);
+      const unsigned above = m & ~((2u << lane) - 1u);
+      return (unsigned)((above ? __ffs(above) - 1 : 32) - lane);
+    };
     // small tables: the CTA's shared counters (native shared atomics)
 #pragma unroll kUnrollSmall
-    for (int qi = 0; qi < a.nsq; qi++) {
+    for (int qi = 0; qi < a.nsq_row; qi++) {
       const int4 d = sq[qi];
-      const int ca = scode[32 * d.x], cb = scode[32 * d.y];
+      const int ca = scode[32 * (d.x & 255)], cb = scode[32 * d.y];
       if (v) atomicAdd(&stab[d.w + ca * d.z + cb], 1u);
+    }
+    for (int qi = a.nsq_row; qi < a.nsq; qi++) {  // per run segment
+      const int4 d = sq[qi];
+      bool start;
+      const unsigned len = seg_len((d.x >> 8) - 1, start);
+      if (start) atomicAdd(&stab[d.w + scode[32 * (d.x & 255)] * d.z + scode[32 * d.y]], len);
     }
     // the others: lanes holding the same cell merged, one global atomic per distinct cell
 #pragma unroll kUnrollBig
-    for (int qi = a.nsq; qi < a.nq; qi++) {
+    for (int qi = a.nsq; qi < a.ngq_row; qi++) {
       const int4 d = sq[qi];
-      const int ca = scode[32 * d.x], cb = scode[32 * d.y];
+      const int ca = scode[32 * (d.x & 255)], cb = scode[32 * d.y];
       const int cell = v ? ca * d.z + cb : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, cell);
       if (v && (__ffs(peers) - 1) == lane) atomicAdd(&sp[qi][cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
+    }
+    for (int qi = a.ngq_row; qi < a.nq; qi++) {  // per run segment
+      const int4 d = sq[qi];
+      bool start;
+      const unsigned len = seg_len((d.x >> 8) - 1, start);
+      if (start) gred_add(&sp[qi][scode[32 * (d.x & 255)] * d.z + scode[32 * d.y]], (unsigned long long)len);
     }
     __syncwarp();
   }
@@ -184,8 +232,9 @@ struct FastCounts : FastPaths {
   bool scalar = false;
   std::string describe() const override {
     char b[160];
-    std::snprintf(b, sizeof b, "{\"kind\": \"counts\", \"attrs\": %d, \"row_queries\": %d, \"dim_queries\": %d}",
-                  ra.nattr, nrowq, ndimq);
+    std::snprintf(b, sizeof b,
+                  "{\"kind\": \"counts\", \"attrs\": %d, \"row_queries\": %d, \"run_queries\": %d, \"dim_queries\": %d}",
+                  ra.nattr, nrowq, (ra.nsq - ra.nsq_row) + (ra.nq - ra.ngq_row), ndimq);
     return b;
   }
   bool handles_group(int) const override { return true; }
@@ -254,6 +303,15 @@ FastPaths* plan_counts(lmfao_ctx* c) {
   std::unique_ptr<FastCounts> fc(new FastCounts());
   CntArgs& a = fc->ra;
   a.nlev = (int)R.children.size();
+  // Cross-dimension pair tables per run measured slower on C4 than per row with
+  // warp-merged atomics (4.42-4.76 vs 4.24 ms: __match_any_sync already merges a run's rows);
+  // off by default, LMFAO_CNT_RUNS=1 turns it on (A/B)
+  const char* ro = std::getenv("LMFAO_CNT_RUNS");
+  const bool run_off = !(ro && ro[0] == '1');
+  for (size_t p = 0; p < c->levels.size(); p++) {
+    a.at[p] = (int8_t)c->levels[p];
+    a.pos[c->levels[p]] = (int8_t)p;
+  }
   for (int j = 0; j < a.nlev; j++) a.fk[j] = R.fk_dense[j].as<int32_t>();
   std::map<int, int> slot;  // attr -> code slot
   std::vector<CntQuery> rq;
@@ -296,6 +354,15 @@ FastPaths* plan_counts(lmfao_ctx* c) {
       else q.b = (int8_t)it->second;
     }
     if (Q.gb.size() == 1) q.b = -1;
+    q.run = -1;
+    if (Q.gb.size() == 2 && lv[0] >= 0 && lv[1] >= 0 && !run_off) {  // two dimensions: per run at the deeper one
+      int p0 = 0, p1 = 0;
+      for (size_t p = 0; p < c->levels.size(); p++) {
+        if (c->levels[p] == lv[0]) p0 = (int)p;
+        if (c->levels[p] == lv[1]) p1 = (int)p;
+      }
+      q.run = (int8_t)std::max(p0, p1);
+    }
     q.sa = (int32_t)gp.g.stride[0];
     q.counts = gp.counts.as<unsigned long long>();
     q.soff = -1;
@@ -330,10 +397,22 @@ FastPaths* plan_counts(lmfao_ctx* c) {
         used += rq[i].ncell;
       }
     a.nsmall = used;
-    // shared-counter queries first (k_cnt_rows loops over the two kinds separately)
+    // shared-counter queries first (k_cnt_rows loops over the kinds separately), per-row before
+    // per-run in each
     std::stable_partition(rq.begin(), rq.end(), [](const CntQuery& q) { return q.soff >= 0; });
     a.nsq = 0;
     for (auto& q : rq) a.nsq += q.soff >= 0 ? 1 : 0;
+    // global tables stay per row: warp-merged atomics there beat per-run ones (C4: 4.25 vs 4.76 ms
+    // with every cross-dimension table per run); LMFAO_CNT_RUN_GLOBAL=1 keeps them per run
+    const char* rg = std::getenv("LMFAO_CNT_RUN_GLOBAL");
+    if (!(rg && rg[0] == '1'))
+      for (size_t i = a.nsq; i < rq.size(); i++) rq[i].run = -1;
+    std::stable_partition(rq.begin(), rq.begin() + a.nsq, [](const CntQuery& q) { return q.run < 0; });
+    std::stable_partition(rq.begin() + a.nsq, rq.end(), [](const CntQuery& q) { return q.run < 0; });
+    a.nsq_row = a.ngq_row = 0;
+    for (int i = 0; i < a.nsq; i++) a.nsq_row += rq[i].run < 0 ? 1 : 0;
+    a.ngq_row = a.nsq;
+    for (size_t i = a.nsq; i < rq.size(); i++) a.ngq_row += rq[i].run < 0 ? 1 : 0;
   }
   fc->nrowq = (int)rq.size();
   fc->ndimq = (int)dq.size();

@@ -208,7 +208,7 @@ struct CovCfg {
 };
 
 // NS = number of featured levels above L (0: L only, 1: A and L, 2: B, A and L); W warps per CTA.
-// The per-warp state and per-block work of the scan (shared by k_cov and k_cov_ws): lane (m, k)
+// The per-warp state and per-block work of the scan: lane (m, k)
 // = (lane / 4, lane % 4) holds, for DMMA group j (rows 4j..4j+3), feature m of row 4j + k.
 // Paths by the block's level-A / level-B run starts (flags of the scan layout):
 //  * fast (no A run starts inside): per-row products; v = [x, s_L0..7, (s_L8, s_L9, 1)] is

@@ -13,8 +13,13 @@ from synth import Product, Query
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("runs", ["0", "1"])
 @pytest.mark.parametrize("n", [1, 31, 33, 5000, 40_011])
-def test_counts_config4_shape(n):
+def test_counts_config4_shape(n, runs, monkeypatch):
+    """runs=1: cross-dimension pair tables counted once per run segment (LMFAO_CNT_RUNS; the
+    slower alternative, kept exact)."""
+    monkeypatch.setenv("LMFAO_CNT_RUNS", runs)
+    monkeypatch.setenv("LMFAO_CNT_RUN_GLOBAL", runs)
     w = synth.config4(fact_rows=n, dim_rows=(40, 300, 2000))
     gpu, info = run_gpu(w.db, w.batch, info=True)
     assert info["fast_path"] and info["fast_path"]["kind"] == "counts", info
