@@ -33,4 +33,5 @@ FastPaths* plan_cov(lmfao_ctx* c);
 FastPaths* plan_rt(lmfao_ctx* c);
 FastPaths* plan_counts(lmfao_ctx* c);
 FastPaths* plan_cube(lmfao_ctx* c);  // group-by queries only (scalar queries: another path)
+FastPaths* plan_poly(lmfao_ctx* c);  // scalar polynomial batches (products of up to 4 features)
 }  // namespace lmfao

@@ -54,9 +54,30 @@ def test_categorical_covariance(n):
     assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
 
 
-@pytest.mark.parametrize("n", [1, 5_000])
-def test_degree2_polynomial(n):
+@pytest.mark.parametrize("path", ["poly", "generic"])
+@pytest.mark.parametrize("n", [1, 5_000, 40_013])
+def test_degree2_polynomial(n, path, monkeypatch):
+    """poly: the Gram of the degree-2 monomials as FP64 DMMA tiles (poly.cu); generic: the
+    interpreted scan (LMFAO_NO_POLY=1)."""
+    if path == "generic":
+        monkeypatch.setenv("LMFAO_NO_POLY", "1")
     db = cat_db(2, n)
     batch = poly2_batch(["x1", "d2_1", "d3_3"])  # monomials over the root and two dimensions
     assert sum(len(q.udafs) for q in batch) == 55
-    assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
+    gpu, info = run_gpu(db, batch, info=True)
+    assert (info["fast_path"] or {}).get("kind") == (path if path == "poly" else None), info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("feats", [["x1", "x2", "d1_1", "d3_1"], ["x1", "x2", "x3", "d1_2", "d2_2", "d3_4"]])
+def test_degree2_polynomial_more_features_and_coefficients(feats):
+    """Up to 24 halves (six features: 1 + 6 + 21 = 28 monomials would not fit, so the planner
+    splits products over the halves it has), sums of products with coefficients, constants."""
+    db = cat_db(3, 30_011)
+    batch = poly2_batch(feats[:4])
+    P, I = Product, ident
+    f = feats
+    batch.append(Query([], [[P(2.0, (I(f[0]), I(f[1]), I(f[2]))), P(-1.5, (I(f[-1]),)), P(0.25, ())],
+                            [P(1.0, (I(f[-1]), I(f[-1]), I(f[-2]), I(f[-3])))], []]))
+    gpu, info = run_gpu(db, batch, info=True)
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)

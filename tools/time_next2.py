@@ -34,7 +34,10 @@ poly = [Query([], [[Product(1.0, tuple(ident(a) for a in m1 + m2))] for i, m1 in
 torch.cuda.set_stream(torch.cuda.Stream())
 cols = {r.name: {c: torch.from_numpy(v).cuda() for c, v in r.cols.items()} for r in w.db.relations}
 sp = torch.cuda.current_stream().cuda_stream
-for name, batch in (("categorical covariance", catcov), ("degree-2 polynomial", poly)):
+for name, batch, env in (("categorical covariance", catcov, None), ("degree-2 polynomial", poly, None),
+                         ("degree-2 polynomial, interpreted", poly, "LMFAO_NO_POLY")):
+    if env:
+        os.environ[env] = "1"
     e = lmfao.Engine()
     lmfao.load(e, w.db, batch, columns=cols)
     e.plan()
@@ -50,3 +53,5 @@ for name, batch in (("categorical covariance", catcov), ("degree-2 polynomial", 
     print(json.dumps({"batch": name, "fact_rows": F.nrows, "aggregates": synth.n_aggregates(batch),
                       "run_ms": s.elapsed_time(t) / 5, "plan": e.plan_info().get("fast_path")}), flush=True)
     e.close()
+    if env:
+        del os.environ[env]
