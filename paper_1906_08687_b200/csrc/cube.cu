@@ -43,10 +43,12 @@ struct Cuboid {
   double* table;                // [cells][nudaf]; constant UDAFs are left to the compaction (countcoef)
   unsigned long long* counts;
   // sparse cuboid (too many cells for a dense table): one record per run end, sorted and
-  // reduced after the scan: rkey[slot] = cell, rval[slot * (M + 1) + j] = S_j (a record's sums contiguous)
+  // reduced after the scan: rkey[slot] = cell, rval[slot * (M + 1) + j] = S_j (a record's sums
+  // contiguous); a work chunk's records start at rbase[chunk] (counted at plan time: the run
+  // ends depend on the sorted keys only), so slots need no atomics and their order is fixed
   unsigned* rkey;
   double* rval;
-  unsigned long long* rn;
+  const long long* rbase;
   long long rcap;
   long long pad_;
 };
@@ -64,6 +66,7 @@ struct CubeArgs {
   int64_t nrows;
   int R, M, nattr, nq, nterm, nitem;
   unsigned dmask;               // levels (0..R) with cuboids
+  int nkey;                     // dense keys read per row (levels 0..nkey-1)
   int64_t chunk;                // rows per work unit (multiple of 32), taken dynamically
   int* work;                    // chunk counter (zeroed per run)
   const int32_t* key[CB_LEV];   // dense keys, level order
@@ -80,6 +83,22 @@ struct CubeArgs {
   const double* tc;             // [nterm] coefficient
   int ablate;                   // LMFAO_CUBE_ABLATE (profiling): 1 no flush, 2 counts only
   int nocount;                  // a later measure group's scan: the counts come from the first
+  int slevel;                   // the sparse cuboids' level (-1: none)
+  int count_only;               // plan time: count each chunk's run ends at slevel into tails[chunk]
+  long long* tails;
+  // k_cube_rec (the scan keeps only the sparse cuboids' level: C5's {A,B,C}, every other cuboid
+  // rolled up from it): the records' cuboids
+  int nrec;
+  const long long* rbase;
+  struct RecOut {
+    unsigned* rkey;
+    double* rval;
+    const unsigned* part[CB_LEV];  // per level: the cell's part from that level's key (null: none)
+    int ngb;                       // root group-by attributes (level R): slot, stride
+    int8_t aslot[CB_GB];
+    long long stride[CB_GB];
+  } rec[4];
+  int meas_plain;               // every measure an fp64 root column, no root group-by attribute
 };
 
 unsigned cgrid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
@@ -143,6 +162,9 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
     const int64_t r1 = r0 + a.chunk < a.nrows ? r0 + a.chunk : a.nrows;
     for (int i = lane; i < (CB_LEV + 1) * (CB_MEAS + 1); i += 32) carry[i] = 0.0;
     __syncwarp();
+    long long rdone = 0;  // this chunk's records so far (run ends at slevel)
+    long long rb = 0;
+    if (a.slevel >= 0 && !a.count_only) rb = sq[a.qbeg[a.slevel]].rbase[ch];
     for (int64_t base = r0; base < r1; base += 32) {
       const int64_t row = base + lane;
       const bool v = row < r1;
@@ -155,7 +177,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
         bool chg = false, chgn = false;
 #pragma unroll
         for (int l = 0; l < CB_LEV; l++) {
-          if (l >= a.R) break;
+          if (l >= a.nkey) break;
           const int k = v ? a.key[l][row] : -1;
           key[l] = k;
           int kp = __shfl_up_sync(BFULL, k, 1);
@@ -191,7 +213,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
 #pragma unroll
       for (int j = 0; j < CB_MEAS; j++) {
         xm[j + 1] = 0.0;
-        if (j < a.M && v) {
+        if (j < a.M && v && !a.count_only) {
           const int64_t mr = a.midx[j] ? (int64_t)a.midx[j][row] : row;
           xm[j + 1] = a.meas_i32[j] ? (double)reinterpret_cast<const int32_t*>(a.meas[j])[mr]
                                     : reinterpret_cast<const double*>(a.meas[j])[mr];
@@ -206,6 +228,10 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
         const bool carry_out = !__shfl_sync(BFULL, (int)(stn >> d & 1u), 31);
         const unsigned T = __ballot_sync(BFULL, tail);  // run ends, compacted by rank
         const int nt = __popc(T), rank = __popc(T & ((1u << lane) - 1u));
+        if (a.count_only) {
+          if (d == a.slevel) rdone += nt;
+          continue;
+        }
         double* cd = carry + d * (CB_MEAS + 1);
 #pragma unroll
         for (int j = 0; j <= CB_MEAS; j++) {
@@ -250,15 +276,9 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                 cells[t * CB_QD + qk] = cell;
                 if (!q.sparse && !a.nocount) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
               }
-              const bool rec = act && q.sparse;
-              if (__any_sync(BFULL, rec)) {  // warp-aggregated record slots per cuboid
-                const unsigned grp = __match_any_sync(BFULL, rec ? qk : -1);
-                const int leader = __ffs(grp) - 1;
-                unsigned long long b0 = 0;
-                if (rec && lane == leader) b0 = atomicAdd(q.rn, (unsigned long long)__popc(grp));
-                b0 = __shfl_sync(BFULL, b0, leader);
-                const long long slot = (long long)b0 + __popc(grp & ((1u << lane) - 1u));
-                if (rec && slot < q.rcap) {
+              if (act && q.sparse) {  // the t-th run end of this block: slot fixed at plan time
+                const long long slot = rb + rdone + t;
+                if (slot < q.rcap) {
                   q.rkey[slot] = (unsigned)cell;
                   for (int j = 0; j < M1; j++) q.rval[slot * M1 + j] = S[t * (CB_MEAS + 1) + j];
                 }
@@ -297,10 +317,162 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
             }
           }
         }
+        if (d == a.slevel) rdone += nt;
         __syncwarp();
       }
     }
+    if (a.count_only && lane == 0) a.tails[ch] = rdone;
   }
+}
+
+// The scan when only the sparse cuboids' level is left (every dense cuboid rolled up from a
+// sparse one's groups; C5): per 32-row block, the run starts at that level from the keys
+// (the previous row's keys carried in registers), segmented sums of the M1 values, and at each
+// run end one record per sparse cuboid — its cell from the run's group-by codes and its sums —
+// in the slot fixed at plan time.  Same chunks and run ends as k_cube's count mode.  The next
+// block's keys, codes and measures are loaded before this block is processed (its row 0's
+// keys are also this block's row 31's successors).
+constexpr int REC_LEV = 4;   // k_cube_rec: key levels read
+constexpr int REC_ATTR = 4;  // ... and root group-by attributes (level R)
+// a record's cell = Σ_l part_l[key_l] (+ the root group-by codes × strides at level R), the
+// per-level parts tabulated at plan time (k_cell_part): no per-attribute code lookups per row
+// PLAIN: every measure an fp64 root column and no root group-by attribute
+template <int M1, bool PLAIN>
+struct RecRow {
+  int k[REC_LEV], c[REC_ATTR];  // dense keys; root group-by codes
+  unsigned cell;                // rec[0]'s cell (the parts from the keys)
+  double x[M1];
+  __device__ __forceinline__ void load(const CubeArgs& a, int64_t row, bool v) {
+#pragma unroll
+    for (int l = 0; l < REC_LEV; l++) k[l] = (l < a.nkey && v) ? a.key[l][row] : -1;
+#pragma unroll
+    for (int i = 0; i < REC_ATTR; i++) c[i] = (!PLAIN && a.slevel == a.R && i < a.nattr && a.alvl[i] == a.R && v) ? a.acode[i][row] : -1;
+    cell = 0;
+#pragma unroll
+    for (int l = 0; l < REC_LEV; l++)
+      if (l < a.nkey && a.rec[0].part[l] && v) cell += a.rec[0].part[l][k[l]];
+    x[0] = v ? 1.0 : 0.0;
+#pragma unroll
+    for (int j = 1; j < M1; j++) {
+      x[j] = 0.0;
+      if (PLAIN) {
+        if (v) x[j] = reinterpret_cast<const double*>(a.meas[j - 1])[row];
+      } else if (v) {
+        const int64_t mr = a.midx[j - 1] ? (int64_t)a.midx[j - 1][row] : row;
+        x[j] = a.meas_i32[j - 1] ? (double)reinterpret_cast<const int32_t*>(a.meas[j - 1])[mr]
+                                 : reinterpret_cast<const double*>(a.meas[j - 1])[mr];
+      }
+    }
+  }
+};
+#ifndef REC_MINB
+#define REC_MINB 3
+#endif
+template <int M1, bool PLAIN>
+__global__ void __launch_bounds__(256, REC_MINB) k_cube_rec(const __grid_constant__ CubeArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int d = a.slevel;
+  const int64_t nchunks = (a.nrows + a.chunk - 1) / a.chunk;
+  for (;;) {
+    int ch = 0;
+    if (lane == 0) ch = atomicAdd(a.work, 1);
+    ch = __shfl_sync(BFULL, ch, 0);
+    if (ch >= nchunks) break;
+    const int64_t r0 = (int64_t)ch * a.chunk;
+    const int64_t r1 = r0 + a.chunk < a.nrows ? r0 + a.chunk : a.nrows;
+    long long slot0 = a.rbase[ch];
+    double carry[M1];
+#pragma unroll
+    for (int j = 0; j < M1; j++) carry[j] = 0.0;
+    int pk[REC_LEV], pc[REC_ATTR];  // the previous block's last row: keys, root group-by codes
+#pragma unroll
+    for (int l = 0; l < REC_LEV; l++) pk[l] = -2;
+#pragma unroll
+    for (int i = 0; i < REC_ATTR; i++) pc[i] = -2;
+    RecRow<M1, PLAIN> cur, nxt;
+    cur.load(a, r0 + lane, r0 + lane < r1);
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int64_t row = base + lane;
+      const bool v = row < r1;
+      const bool vn = row + 1 < r1;
+      if (base + 32 < r1) nxt.load(a, row + 32, row + 32 < r1);
+      bool chg = false, chgn = false;
+#pragma unroll
+      for (int l = 0; l < REC_LEV; l++) {
+        if (l >= a.nkey) continue;
+        const int k = cur.k[l];
+        int kp = __shfl_up_sync(BFULL, k, 1);
+        if (lane == 0) kp = pk[l];
+        int kn = __shfl_down_sync(BFULL, k, 1);
+        const int k0n = __shfl_sync(BFULL, nxt.k[l], 0);
+        if (lane == 31) kn = vn ? k0n : -3;
+        pk[l] = __shfl_sync(BFULL, k, 31);
+        chg |= kp != k;
+        chgn |= !vn || kn != k;
+      }
+      if (!PLAIN && d == a.R) {  // level R: equal keys and equal root group-by codes
+#pragma unroll
+        for (int i = 0; i < REC_ATTR; i++) {
+          if (i >= a.nattr || a.alvl[i] != a.R) continue;
+          const int c = cur.c[i];
+          int cp = __shfl_up_sync(BFULL, c, 1);
+          if (lane == 0) cp = pc[i];
+          int cn = __shfl_down_sync(BFULL, c, 1);
+          const int c0n = __shfl_sync(BFULL, nxt.c[i], 0);
+          if (lane == 31) cn = vn ? c0n : -3;
+          pc[i] = __shfl_sync(BFULL, c, 31);
+          chg |= cp != c;
+          chgn |= !vn || cn != c;
+        }
+      }
+      if (!v) chg = chgn = true;
+      const bool tail = v && chgn;
+      const unsigned starts = __ballot_sync(BFULL, chg) | 1u;
+      const int s0 = 31 - __clz(starts & ((2u << lane) - 1u));
+      const bool end31 = __shfl_sync(BFULL, (int)chgn, 31);  // lane 31 closes its run: no carry
+      double x[M1];
+#pragma unroll
+      for (int j = 0; j < M1; j++) {
+        x[j] = cur.x[j];
+        if (lane == 0 && !chg) x[j] += carry[j];
+        x[j] = seg_scan(x[j], lane, s0);
+        const double c31 = __shfl_sync(BFULL, x[j], 31);
+        carry[j] = end31 ? 0.0 : c31;
+      }
+      const unsigned T = __ballot_sync(BFULL, tail);
+      if (tail) {
+        const long long slot = slot0 + __popc(T & ((1u << lane) - 1u));
+        for (int r = 0; r < a.nrec; r++) {
+          const CubeArgs::RecOut& o = a.rec[r];
+          unsigned cell = cur.cell;
+          if (r > 0) {
+            cell = 0;
+#pragma unroll
+            for (int l = 0; l < REC_LEV; l++)
+              if (l < a.nkey && o.part[l]) cell += o.part[l][cur.k[l]];
+          }
+          for (int i = 0; i < (PLAIN ? 0 : o.ngb); i++) {  // root group-by attributes (level R)
+            int code = 0;
+#pragma unroll
+            for (int t = 0; t < REC_ATTR; t++)
+              if (t == o.aslot[i]) code = cur.c[t];
+            cell += (unsigned)((long long)code * o.stride[i]);
+          }
+          o.rkey[slot] = cell;
+          double* rv = o.rval + slot * M1;
+#pragma unroll
+          for (int j = 0; j < M1; j++) rv[j] = x[j];
+        }
+      }
+      slot0 += __popc(T);
+      cur = nxt;
+    }
+  }
+}
+// part[k] += code_i[k] * stride_i over a level's group-by attributes (plan time)
+__global__ void k_cell_part(unsigned* part, const int32_t* code, long long stride, int64_t nkeys) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nkeys; k += (int64_t)gridDim.x * blockDim.x)
+    part[k] += (unsigned)((long long)code[k] * stride);
 }
 
 // ---- sparse cuboids: run records -> sorted -> reduced groups, sizes on the device only
@@ -387,16 +559,29 @@ __global__ void k_rec_heads(const unsigned* __restrict__ key, int64_t cap, const
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x)
     head[i] = (i < n && (i == 0 || key[i] != key[i - 1])) ? 1u : 0u;
 }
-__global__ void k_rec_ngroups(const uint32_t* head, const uint32_t* excl, const unsigned long long* n_dev,
-                              int64_t cap, unsigned long long* ngroups) {
+// group g's records are [gstart[g], gstart[g + 1]); *ng = the number of groups
+__global__ void k_rec_starts(const uint32_t* __restrict__ head, const uint32_t* __restrict__ excl,
+                             const unsigned long long* n_dev, int64_t cap, uint32_t* __restrict__ gstart,
+                             unsigned long long* __restrict__ ng) {
   const int64_t n = min(cap, (int64_t)*n_dev);
-  *ngroups = n > 0 ? (unsigned long long)excl[n - 1] + head[n - 1] : 0ull;
+  if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    gstart[0] = 0;
+    *ng = 0;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (head[i]) gstart[excl[i]] = (uint32_t)i;
+    if (i == n - 1) {
+      const uint32_t tot = excl[i] + head[i];
+      gstart[tot] = (uint32_t)n;
+      *ng = tot;
+    }
+  }
 }
 struct RecReduce {
   const unsigned* key;
   const uint32_t* perm;
-  const uint32_t* head;
-  const uint32_t* excl;
+  const uint32_t* gstart;  // [groups + 1] first record of each group (k_rec_starts)
+  const unsigned long long* ng;  // groups (device)
   const double* rval;  // records' sums [.][M1] (merge: the own receive buffer, both parities)
   long long rcap;
   int64_t cap;
@@ -412,6 +597,7 @@ struct RecReduce {
   int send;            // world > 1, local groups: to their owners (x), not decoded
   int merge;           // world > 1, received groups: rval = own vals, parity from the epoch
   int sorted;          // rval is already in sorted order (k_rec_gather): perm not used
+  unsigned* gcell;     // (merge rollups) the groups' cells
   XArgs x;
 };
 // A dense cuboid X at the sparse cuboid Y's level whose attributes are a subset of Y's: its
@@ -425,6 +611,8 @@ struct Rollup {
   int pos[CB_GB];      // X's attribute i is Y's attribute pos[i]
   long long stride[CB_GB];
   unsigned long long cmask;
+  int prefix;          // X's attributes are the first ngb of Y's: X's cells are runs of consecutive groups
+  int pad_;
 };
 // The records' sums in sorted order: sval[i][j] = rval[perm[i]][j], one thread per (i, j), so the
 // M1 threads of a record read its M1 doubles together (a record per two 32-byte sectors instead
@@ -486,55 +674,247 @@ __global__ void k_dense_rollup(const __grid_constant__ DenseRollup d) {
     }
   }
 }
-__global__ void k_rec_reduce(const __grid_constant__ RecReduce r) {
-  const int64_t n = min(r.cap, (int64_t)*r.n_dev);
+// One lane per group (consecutive lanes: consecutive groups, in canonical order): the group's
+// sums over its records, its output row (or, world > 1, its owner's buffer), and its share of
+// the cuboids rolled up from it.  A rolled-up cuboid X whose attributes are the first of Y's
+// (C5: {A,B} of {A,B,C}) has its cells on runs of consecutive groups: summed over the run by
+// a segmented warp scan, one RED per run and warp instead of one per group.
+// X = Σ of the sparse cuboid Y's groups over the attributes X drops, without atomics to global
+// memory (world 1; X's UDAFs = Y's).  Y's groups are sorted by Y's cell; let p be the position
+// of the last attribute X drops.  Groups with equal Y-attributes 0..p form a segment, sorted
+// within by the suffix (Y's attributes after p, all kept by X); X's other attributes (kept,
+// before p) are constant in a segment.  A tile = one value P of those kept prefix attributes and
+// a range [lo, hi) of the suffix: its groups are, in every segment consistent with P (one per
+// combination of the dropped attributes), the contiguous run with suffix in [lo, hi) — found by
+// binary search — summed into a shared-memory table of the tile's cells and written once.
+// C5: {B,C} (drop A: 50 segments per tile) and {A,C} (drop B: 1000) from {A,B,C}.
+constexpr int MR_W = 1024;     // suffix cells per tile
+constexpr int MR_SEG = 1024;   // segments per tile (more: per-group REDs instead)
+struct MergeRollup {
+  const unsigned* gcell;       // Y's groups' cells, ascending
+  const unsigned long long* ng;
+  const double* yvals;         // [g][nudaf]
+  const unsigned long long* ycnt;
+  double* xtab;
+  unsigned long long* xcnt;
+  int nudaf;
+  int nseg;                    // combinations of the dropped attributes
+  long long npre;              // values P of the kept prefix attributes
+  long long suffix;            // suffix cells (Y's stride of attribute p)
+  long long ntile_s;           // tiles per P
+  // Y's attributes 0..p: radix, Y stride, role (0 dropped, 1 kept prefix), X stride (kept)
+  int np;
+  int role[CB_GB];
+  long long radix[CB_GB], ystr[CB_GB], xstr[CB_GB];
+  // suffix attributes (Y's after p): radix, Y stride, X stride
+  int ns;
+  long long sradix[CB_GB], systr[CB_GB], sxstr[CB_GB];
+};
+__device__ __forceinline__ int64_t lower_bound_u32(const unsigned* a, int64_t n, unsigned long long v) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((unsigned long long)a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void __launch_bounds__(256) k_merge_rollup(const __grid_constant__ MergeRollup m) {
+  extern __shared__ __align__(16) unsigned char msm[];
+  double* tv = reinterpret_cast<double*>(msm);                                        // [MR_W][nudaf]
+  unsigned long long* tc = reinterpret_cast<unsigned long long*>(tv + (size_t)MR_W * m.nudaf);  // [MR_W]
+  uint32_t* sbeg = reinterpret_cast<uint32_t*>(tc + MR_W);                            // [MR_SEG]
+  uint32_t* soff = sbeg + MR_SEG;                                                     // [MR_SEG + 1]
+  unsigned long long* sbase = reinterpret_cast<unsigned long long*>(soff + MR_SEG + 2);  // [MR_SEG]
+  __shared__ uint32_t wsum[8];
+  const int64_t ng = (int64_t)*m.ng;
+  const int64_t ntiles = m.npre * m.ntile_s;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long P = tile / m.ntile_s;
+    const long long lo = (tile - P * m.ntile_s) * MR_W;
+    const long long hi = min(lo + MR_W, m.suffix);
+    for (int i = threadIdx.x; i < MR_W * m.nudaf; i += blockDim.x) tv[i] = 0.0;
+    for (int i = threadIdx.x; i < MR_W; i += blockDim.x) tc[i] = 0ull;
+    // segment s: Y's prefix cell from P (kept attributes) and s (dropped ones)
+    for (int sg = threadIdx.x; sg < m.nseg; sg += blockDim.x) {
+      unsigned long long base = 0;
+      long long rp = P, rs = sg;
+      for (int i = m.np - 1; i >= 0; i--) {
+        long long code;
+        if (m.role[i]) {
+          code = rp % m.radix[i];
+          rp /= m.radix[i];
+        } else {
+          code = rs % m.radix[i];
+          rs /= m.radix[i];
+        }
+        base += (unsigned long long)code * m.ystr[i];
+      }
+      const int64_t b = lower_bound_u32(m.gcell, ng, base + lo);
+      const int64_t e = lower_bound_u32(m.gcell + b, ng - b, base + hi) + b;
+      sbeg[sg] = (uint32_t)b;
+      soff[sg] = (uint32_t)(e - b);
+      sbase[sg] = base + lo;
+    }
+    __syncthreads();
+    // exclusive scan of the slice lengths (one thread per segment chunk)
+    {
+      const int per = (m.nseg + blockDim.x - 1) / blockDim.x;
+      const int s0 = threadIdx.x * per, s1 = min(m.nseg, s0 + per);
+      uint32_t loc = 0;
+      for (int sg = s0; sg < s1; sg++) loc += soff[sg];
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      uint32_t x = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(BFULL, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      uint32_t pre = x - loc;
+      for (int w = 0; w < warp; w++) pre += wsum[w];
+      __syncthreads();
+      for (int sg = s0; sg < s1; sg++) {
+        const uint32_t l = soff[sg];
+        soff[sg] = pre;
+        pre += l;
+      }
+      if (threadIdx.x == blockDim.x - 1) soff[m.nseg] = pre;
+    }
+    __syncthreads();
+    const uint32_t total = soff[m.nseg];
+    for (uint32_t it = threadIdx.x; it < total; it += blockDim.x) {
+      int a = 0, b = m.nseg;  // the segment: last s with soff[s] <= it
+      while (b - a > 1) {
+        const int mid = (a + b) >> 1;
+        if (soff[mid] <= it) a = mid;
+        else b = mid;
+      }
+      const int64_t g = (int64_t)sbeg[a] + (it - soff[a]);
+      const int r = (int)(m.gcell[g] - sbase[a]);
+      const double* yv = m.yvals + g * m.nudaf;
+      for (int u = 0; u < m.nudaf; u++) sred_add(&tv[r * m.nudaf + u], yv[u]);
+      atomicAdd(&tc[r], m.ycnt[g]);
+    }
+    __syncthreads();
+    // write the tile's cells (each X cell belongs to one tile: plain stores)
+    for (int r = threadIdx.x; r < hi - lo; r += blockDim.x) {
+      const unsigned long long cnt = tc[r];
+      if (!cnt) continue;
+      long long xc = 0, rp = P, rr = lo + r;
+      for (int i = m.np - 1; i >= 0; i--)
+        if (m.role[i]) {
+          xc += (rp % m.radix[i]) * m.xstr[i];
+          rp /= m.radix[i];
+        }
+      for (int i = 0; i < m.ns; i++) xc += (rr / m.systr[i] % m.sradix[i]) * m.sxstr[i];
+      m.xcnt[xc] = cnt;
+      for (int u = 0; u < m.nudaf; u++) m.xtab[xc * m.nudaf + u] = tv[r * m.nudaf + u];
+    }
+    __syncthreads();
+  }
+}
+inline size_t merge_smem(int nudaf) { return (size_t)MR_W * nudaf * 8 + MR_W * 8 + MR_SEG * 4 + (MR_SEG + 2) * 4 + MR_SEG * 8; }
+
+__global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecReduce r) {
+  const int64_t ng = (int64_t)*r.ng;
   const double* rval = r.rval;
   int b = 0;
   if (r.send || r.merge) b = (int)(x_epoch(r.x.hdr[r.x.rank]) & 1);
   if (r.merge && !r.sorted) rval += (size_t)b * r.x.capr * r.M1;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    if (!r.head[i]) continue;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g0 = wid * 32; g0 < ng; g0 += nw * 32) {
+    const int64_t g = g0 + lane;
+    const bool act = g < ng;
     double S[CB_MEAS + 1];
-    for (int j = 0; j < r.M1; j++) S[j] = 0.0;
-    int64_t t = i;
-    do {
-      const int64_t p = r.sorted ? t : (int64_t)r.perm[t];
-      for (int j = 0; j < r.M1; j++) S[j] += rval[p * r.M1 + j];
-      t++;
-    } while (t < n && !r.head[t]);
-    const unsigned cell = r.key[i];  // sparse cuboids have < 2^32 cells: 32-bit decode
+#pragma unroll
+    for (int j = 0; j <= CB_MEAS; j++) S[j] = 0.0;
+    unsigned cell = 0;
     unsigned code[CB_GB];
-    for (int a = 0; a < r.d.ngb; a++) code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
-    if (r.send) {  // fused exchange: the group goes straight to its owner's buffer (peer memory)
-      const int o = (int)(cell / (unsigned long long)r.x.chunk);
-      const unsigned long long slot = atomicAdd(&r.x.hdr[o]->cnt[b], 1ull);
-      if (slot < (unsigned long long)r.x.capr) {
-        const size_t at = (size_t)b * r.x.capr + slot;
-        r.x.keys[o][at] = cell;
-        for (int j = 0; j < r.M1; j++) r.x.vals[o][at * r.M1 + j] = S[j];
+    if (act) {
+      const int64_t t0 = r.gstart[g], t1 = r.gstart[g + 1];
+      for (int64_t t = t0; t < t1; t++) {
+        const int64_t p = r.sorted ? t : (int64_t)r.perm[t];
+        const double* rv = rval + p * r.M1;
+        if (!(r.M1 & 1)) {  // 16-byte aligned record: pairs
+#pragma unroll
+          for (int j = 0; j < CB_MEAS; j += 2)
+            if (j < r.M1) {
+              const double2 w = *reinterpret_cast<const double2*>(rv + j);
+              S[j] += w.x;
+              S[j + 1] += w.y;
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j <= CB_MEAS; j++)
+            if (j < r.M1) S[j] += rv[j];
+        }
+      }
+      cell = r.key[t0];  // sparse cuboids have < 2^32 cells: 32-bit decode
+#pragma unroll
+      for (int a = 0; a < CB_GB; a++)
+        if (a < r.d.ngb) code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
+      if (r.send) {  // fused exchange: the group goes straight to its owner's buffer (peer memory)
+        const int o = (int)(cell / (unsigned long long)r.x.chunk);
+        const unsigned long long slot = atomicAdd(&r.x.hdr[o]->cnt[b], 1ull);
+        if (slot < (unsigned long long)r.x.capr) {
+          const size_t at = (size_t)b * r.x.capr + slot;
+          r.x.keys[o][at] = cell;
+#pragma unroll
+          for (int j = 0; j <= CB_MEAS; j++)
+            if (j < r.M1) r.x.vals[o][at * r.M1 + j] = S[j];
+        } else {
+          atomicExch(&r.x.hdr[r.x.rank]->err, 2);
+        }
       } else {
-        atomicExch(&r.x.hdr[r.x.rank]->err, 2);
+        for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
+        for (int u = 0; u < r.nudaf; u++) {
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j <= CB_MEAS; j++)
+            if (j < r.M1) v = fma(r.coef[u * r.M1 + j], S[j], v);
+          r.ovals[g * r.nudaf + u] = v;
+        }
+        r.ocnts[g] = (unsigned long long)S[0];
+        if (r.gcell) r.gcell[g] = cell;
       }
-    } else {
-      const int64_t g = r.excl[i];
-      for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
-      for (int u = 0; u < r.nudaf; u++) {
-        double v = 0.0;
-        for (int j = 0; j < r.M1; j++) v = fma(r.coef[u * r.M1 + j], S[j], v);
-        r.ovals[g * r.nudaf + u] = v;
-      }
-      r.ocnts[g] = (unsigned long long)S[0];
     }
     for (int x = 0; x < r.nder; x++) {
       const Rollup& X = r.der[x];
-      long long xc = 0;
-      for (int i = 0; i < X.ngb; i++) xc += (long long)code[X.pos[i]] * X.stride[i];
-      gred_add(&X.counts[xc], (unsigned long long)S[0]);
-      for (int u = 0; u < X.nudaf; u++) {
-        if (X.cmask >> u & 1ull) continue;
-        double v = 0.0;
-        for (int j = 0; j < r.M1; j++) v = fma(X.coef[u * r.M1 + j], S[j], v);
-        if (v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
+      long long xc = -1 - lane;  // idle lanes: cells of their own
+      if (act) {
+        xc = 0;
+        for (int i = 0; i < X.ngb; i++) xc += (long long)code[X.pos[i]] * X.stride[i];
+      }
+      if (X.prefix) {
+        const long long xp = __shfl_up_sync(BFULL, xc, 1), xn = __shfl_down_sync(BFULL, xc, 1);
+        const unsigned starts = __ballot_sync(BFULL, lane == 0 || xp != xc) | 1u;
+        const int s0 = 31 - __clz(starts & ((2u << lane) - 1u));
+        const bool tail = act && (lane == 31 || xn != xc);
+        const double cnt = seg_scan(S[0], lane, s0);
+        if (tail) gred_add(&X.counts[xc], (unsigned long long)cnt);
+        for (int u = 0; u < X.nudaf; u++) {
+          if (X.cmask >> u & 1ull) continue;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j <= CB_MEAS; j++)
+            if (j < r.M1) v = fma(X.coef[u * r.M1 + j], S[j], v);
+          v = seg_scan(v, lane, s0);
+          if (tail && v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
+        }
+      } else if (act) {
+        gred_add(&X.counts[xc], (unsigned long long)S[0]);
+        for (int u = 0; u < X.nudaf; u++) {
+          if (X.cmask >> u & 1ull) continue;
+          double v = 0.0;
+#pragma unroll
+          for (int j = 0; j <= CB_MEAS; j++)
+            if (j < r.M1) v = fma(X.coef[u * r.M1 + j], S[j], v);
+          if (v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
+        }
       }
     }
   }
@@ -548,7 +928,7 @@ inline size_t xbytes(long long capr, int M1) { return xoff_vals(capr) + (size_t)
 struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
   int gi = -1, coff = 0, bits = 1;
   long long cap = 0;
-  DevBuf key, val, n, perm, head, excl;
+  DevBuf key, val, n, perm, head, excl, gstart, ngl;
   std::vector<Rollup> der;  // dense cuboids rolled up from this one's groups
   DevBuf dder;
   // world > 1: the exchange
@@ -556,9 +936,10 @@ struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
   DevBuf xbuf;                 // [XHdr | keys [2][capr] | vals [2][capr][M1]], mapped by every rank
   std::vector<void*> peers;    // every rank's xbuf
   DevBuf xptrs;                // [3][world] device pointers: headers, keys, vals
-  DevBuf rkey, rperm, rhead, rexcl, nrecv;
+  DevBuf rkey, rperm, rhead, rexcl, rgstart, nrecv;
   DevBuf sval;                 // records' sums in sorted order (k_rec_gather), local then received
   std::vector<DenseRollup> dense_rollups;  // derived cuboids summed from a larger derived one, after the reduce
+  std::vector<MergeRollup> merges;        // derived cuboids merged from the sorted groups (world 1), after the reduce
   XArgs x{};
   Comm* comm = nullptr;
   SparseOut() = default;
@@ -572,9 +953,12 @@ struct FastCube : FastPaths {
   CubeArgs ca{};
   std::vector<CubeArgs> parts;  // one scan per group of up to CB_MEAS measures
   std::vector<DevBuf> pbuf;     // per part: items, tj, tc
-  DevBuf dq, dcoef, ditems, dtj, dtc, dwork;
+  DevBuf dq, dcoef, ditems, dtj, dtc, dwork, rbase;
   std::vector<SparseOut> sparse;
-  int nq = 0, grid = 148;
+  int nq = 0, grid = 148, rec_grid = 148;
+  DevBuf parts_tab[4 * CB_LEV];  // k_cube_rec: per record cuboid and level, the cell parts
+  bool rec_only = false;  // k_cube_rec
+  bool gather_first = false;
   size_t smem = 0;
   bool graph_ok() const override { return true; }  // device-side sizes: no host synchronisation
   std::string describe() const override {
@@ -582,8 +966,9 @@ struct FastCube : FastPaths {
     int m = 0;
     for (auto& p : parts) m += p.M;
     std::snprintf(b, sizeof b,
-                  "{\"kind\": \"cube\", \"cuboids\": %d, \"sparse\": %d, \"measures\": %d, \"scans\": %d, \"levels\": %d}",
-                  nq, (int)sparse.size(), m, (int)parts.size(), ca.R);
+                  "{\"kind\": \"cube\", \"cuboids\": %d, \"sparse\": %d, \"measures\": %d, \"scans\": %d, \"levels\": %d, "
+                  "\"scan\": \"%s\"}",
+                  nq, (int)sparse.size(), m, (int)parts.size(), ca.R, rec_only ? "records" : "levels");
     return b;
   }
   bool handles_group(int) const override { return true; }
@@ -595,7 +980,6 @@ struct FastCube : FastPaths {
       CUDA_TRY(cudaMemsetAsync(gp.counts.p, 0, gp.ncells * 8, st));
       CUDA_TRY(cudaMemsetAsync(gp.table.p, 0, gp.table.bytes, st));
     }
-    for (auto& sp : sparse) CUDA_TRY(cudaMemsetAsync(sp.n.p, 0, 8, st));
     for (size_t pi = 0; pi < parts.size(); pi++) {
       CUDA_TRY(cudaMemsetAsync(dwork.as<int>() + pi, 0, 4, st));
       CubeArgs a = parts[pi];
@@ -603,14 +987,32 @@ struct FastCube : FastPaths {
       a.work = dwork.as<int>() + pi;
       if (a.nrows > 0) {
         const int64_t nch = (a.nrows + a.chunk - 1) / a.chunk;
-        const int64_t g = std::min<int64_t>((nch + CB_WARPS - 1) / CB_WARPS, grid);
-        k_cube<<<(unsigned)g, CB_WARPS * 32, smem, st>>>(a);
+        if (rec_only) {
+          const int64_t g = std::min<int64_t>((nch + 7) / 8, rec_grid);
+          CUDA_TRY(launch_rec(a, (unsigned)g, st));
+        } else {
+          const int64_t g = std::min<int64_t>((nch + CB_WARPS - 1) / CB_WARPS, grid);
+          k_cube<<<(unsigned)g, CB_WARPS * 32, smem, st>>>(a);
+        }
         launches_add(1);
       }
     }
     CUDA_TRY(cudaGetLastError());
     for (auto& sp : sparse) CUDA_TRY(finish_sparse(c, sp, st));
     return cudaSuccess;
+  }
+  static cudaError_t launch_rec(const CubeArgs& a, unsigned g, cudaStream_t st) {
+    switch (a.M + 1) {
+#define LMFAO_REC(m)                                       \
+  case m:                                                  \
+    if (a.meas_plain) k_cube_rec<m, true><<<g, 256, 0, st>>>(a); \
+    else k_cube_rec<m, false><<<g, 256, 0, st>>>(a);       \
+    break;
+      LMFAO_REC(1) LMFAO_REC(2) LMFAO_REC(3) LMFAO_REC(4) LMFAO_REC(5) LMFAO_REC(6) LMFAO_REC(7) LMFAO_REC(8) LMFAO_REC(9)
+#undef LMFAO_REC
+      default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
   }
   // sort the records by cell, reduce equal cells: the groups in canonical order (world 1), or,
   // world > 1, every local group to its owner (peer memory) and the owner's merge of what it
@@ -632,8 +1034,11 @@ struct FastCube : FastPaths {
     RecReduce r{};
     r.key = sp.key.as<unsigned>();
     r.perm = sp.perm.as<uint32_t>();
-    r.head = sp.head.as<uint32_t>();
-    r.excl = sp.excl.as<uint32_t>();
+    k_rec_starts<<<cgrid(cap), 256, 0, st>>>(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), sp.n.as<unsigned long long>(),
+                                             cap, sp.gstart.as<uint32_t>(),
+                                             dist ? sp.ngl.as<unsigned long long>() : gp.ngroups_dev.as<unsigned long long>());
+    r.gstart = sp.gstart.as<uint32_t>();
+    r.ng = dist ? sp.ngl.as<unsigned long long>() : gp.ngroups_dev.as<unsigned long long>();
     r.rval = sp.val.as<double>();
     r.rcap = sp.cap;
     r.cap = cap;
@@ -649,22 +1054,28 @@ struct FastCube : FastPaths {
     r.der = sp.dder.as<Rollup>();
     r.send = dist;
     r.x = sp.x;
-    k_rec_gather<<<cgrid(cap * r.M1), 256, 0, st>>>(r, sp.sval.as<double>());
-    r.rval = sp.sval.as<double>();
-    r.sorted = 1;
+    if (gather_first) {  // LMFAO_CUBE_GATHER=1: the records' sums permuted first (round-2 A/B)
+      k_rec_gather<<<cgrid(cap * r.M1), 256, 0, st>>>(r, sp.sval.as<double>());
+      r.rval = sp.sval.as<double>();
+      r.sorted = 1;
+    }
+    r.gcell = sp.merges.empty() || dist ? nullptr : sp.excl.as<unsigned>();  // excl is free after k_rec_starts
     k_rec_reduce<<<cgrid(cap), 256, 0, st>>>(r);
+    for (auto& mr : sp.merges) {
+      MergeRollup m = mr;
+      m.gcell = sp.excl.as<unsigned>();
+      m.ng = gp.ngroups_dev.as<unsigned long long>();
+      const long long nt = m.npre * m.ntile_s;
+      k_merge_rollup<<<(unsigned)std::max<long long>(1, std::min<long long>(nt, 148 * 4)), 256, merge_smem(m.nudaf), st>>>(m);
+    }
+    launches_add((int)sp.merges.size());
     for (auto& dr : sp.dense_rollups) {
       const long long tot = dr.xcells * (dr.nudaf + 1) * dr.split;
       k_dense_rollup<<<(unsigned)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 148 * 16)), 256, 0, st>>>(dr);
     }
-    launches_add(6 + (int)sp.dense_rollups.size());
+    launches_add(7 + (int)sp.dense_rollups.size());
     CUDA_TRY(cudaGetLastError());
-    if (!dist) {
-      k_rec_ngroups<<<1, 1, 0, st>>>(sp.head.as<uint32_t>(), sp.excl.as<uint32_t>(), sp.n.as<unsigned long long>(), cap,
-                                     gp.ngroups_dev.as<unsigned long long>());
-      launches_add(1);
-      return cudaGetLastError();
-    }
+    if (!dist) return cudaSuccess;
     // world > 1: signal the owners, then merge what this rank received
     k_x_signal<<<1, 1, 0, st>>>(sp.x);
     if (c->comm->phase(st)) return cudaErrorUnknown;  // loopback: every rank has sent
@@ -678,8 +1089,10 @@ struct FastCube : FastPaths {
     RecReduce m = r;
     m.key = sp.rkey.as<unsigned>();
     m.perm = sp.rperm.as<uint32_t>();
-    m.head = sp.rhead.as<uint32_t>();
-    m.excl = sp.rexcl.as<uint32_t>();
+    k_rec_starts<<<cgrid(capr), 256, 0, st>>>(sp.rhead.as<uint32_t>(), sp.rexcl.as<uint32_t>(), nrecv, capr,
+                                              sp.rgstart.as<uint32_t>(), gp.ngroups_dev.as<unsigned long long>());
+    m.gstart = sp.rgstart.as<uint32_t>();
+    m.ng = gp.ngroups_dev.as<unsigned long long>();
     m.rval = reinterpret_cast<const double*>(sp.xbuf.as<char>() + xoff_vals(sp.capr));
     m.rcap = capr;
     m.cap = capr;
@@ -692,8 +1105,6 @@ struct FastCube : FastPaths {
     m.rval = sp.sval.as<double>();
     m.sorted = 1;
     k_rec_reduce<<<cgrid(capr), 256, 0, st>>>(m);
-    k_rec_ngroups<<<1, 1, 0, st>>>(sp.rhead.as<uint32_t>(), sp.rexcl.as<uint32_t>(), nrecv, capr,
-                                   gp.ngroups_dev.as<unsigned long long>());
     k_x_release<<<1, 1, 0, st>>>(sp.x);
     launches_add(9);
     return cudaGetLastError();
@@ -832,6 +1243,8 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   const int64_t sparse_min = smin ? std::atoll(smin) : ((int64_t)1 << 25);
   std::vector<Cuboid> hq;
   std::vector<double> dense;
+  a.slevel = -1;
+  if (const char* gf = std::getenv("LMFAO_CUBE_GATHER")) fc->gather_first = gf[0] == '1';
   std::vector<int> coffs, sparse_of(qs.size(), -1);
   for (size_t k = 0; k < qs.size(); k++) {
     hq.push_back(qs[k].q);
@@ -840,13 +1253,16 @@ FastPaths* plan_cube(lmfao_ctx* c) {
     dense.insert(dense.end(), qs[k].dense.begin(), qs[k].dense.end());
     GroupPlan& gp = c->groups[qs[k].gi];
     if (!allow_sparse || gp.ncells <= sparse_min || gp.ncells > ((int64_t)1 << 32)) continue;
+    if (a.slevel >= 0 && qs[k].depth != a.slevel) continue;  // one level's run ends give the slots
+    a.slevel = qs[k].depth;
     SparseOut sp;
     sp.gi = qs[k].gi;
     sp.coff = coff;
     sp.cap = nrows + nchunks + 64;
     while (sp.bits < 32 && ((int64_t)1 << sp.bits) < gp.ncells) sp.bits++;
     if (sp.key.alloc(sp.cap * 4) || sp.val.alloc((size_t)sp.cap * M1 * 8) || sp.n.alloc(8) || sp.perm.alloc(sp.cap * 4) ||
-        sp.head.alloc(sp.cap * 4) || sp.excl.alloc(sp.cap * 4) || gp.ngroups_dev.alloc(8))
+        sp.head.alloc(sp.cap * 4) || sp.excl.alloc(sp.cap * 4) || sp.gstart.alloc((sp.cap + 1) * 4) || sp.ngl.alloc(8) ||
+        gp.ngroups_dev.alloc(8))
       return nullptr;
     int64_t ocap = std::min<int64_t>(sp.cap, gp.ncells);  // groups this rank outputs
     if (c->world > 1) {
@@ -886,26 +1302,26 @@ FastPaths* plan_cube(lmfao_ctx* c) {
       sp.x.world = (int)G;
       sp.comm = c->comm.get();
       if (sp.rkey.alloc(sp.capr * 4) || sp.rperm.alloc(sp.capr * 4) || sp.rhead.alloc(sp.capr * 4) ||
-          sp.rexcl.alloc(sp.capr * 4) || sp.nrecv.alloc(8))
+          sp.rexcl.alloc(sp.capr * 4) || sp.rgstart.alloc((sp.capr + 1) * 4) || sp.nrecv.alloc(8))
         return nullptr;
     }
     if (gp.rkeys.alloc(std::max<int64_t>(ocap, 1) * gp.d.ngb * 4) || gp.rvals.alloc(std::max<int64_t>(ocap, 1) * gp.nudaf * 8) ||
         gp.rcnts.alloc(std::max<int64_t>(ocap, 1) * 8) ||
-        sp.sval.alloc((size_t)std::max<int64_t>(sp.cap, sp.capr) * M1 * 8))
+        ((c->world > 1 || fc->gather_first) && sp.sval.alloc((size_t)std::max<int64_t>(sp.cap, sp.capr) * M1 * 8)))
       return nullptr;
     gp.ngroups_on_device = true;
     Cuboid& q = hq[k];
     q.sparse = 1;
     q.rkey = sp.key.as<unsigned>();
     q.rval = sp.val.as<double>();
-    q.rn = sp.n.as<unsigned long long>();
     q.rcap = sp.cap;
     sparse_of[k] = (int)fc->sparse.size();
     fc->sparse.push_back(std::move(sp));
   }
-  // dense cuboids at a sparse cuboid's level over a subset of its attributes: rolled up from
-  // its reduced groups (one update per group, not per run end; C5's {A,C}, {B,C}, {C} from
-  // {A,B,C}).  LMFAO_CUBE_ROLLUP=0: off.
+  // dense cuboids over a subset of a sparse cuboid's attributes: rolled up from its reduced
+  // groups (one update per group, not per run end), at any level — every join row falls in
+  // exactly one of Y's groups, so X's cells are sums of Y's.  C5: all seven cuboids from
+  // {A,B,C}, so the scan keeps only {A,B,C}'s level.  LMFAO_CUBE_ROLLUP=0: off.
   std::vector<std::vector<int>> der_coff(fc->sparse.size()), der_k(fc->sparse.size());
   const char* ru = std::getenv("LMFAO_CUBE_ROLLUP");
   const char* rmin = std::getenv("LMFAO_CUBE_ROLLUP_MIN");  // cuboids with fewer cells stay on the scan
@@ -914,7 +1330,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
     for (size_t k = 0; k < qs.size(); k++) {
       if (hq[k].sparse || c->groups[qs[k].gi].ncells < rollup_min) continue;
       for (size_t y = 0; y < qs.size(); y++) {
-        if (sparse_of[y] < 0 || qs[y].depth != qs[k].depth) continue;
+        if (sparse_of[y] < 0) continue;
         Rollup ro{};
         bool sub = true;
         for (int i = 0; i < hq[k].ngb && sub; i++) {
@@ -926,6 +1342,8 @@ FastPaths* plan_cube(lmfao_ctx* c) {
           ro.stride[i] = hq[k].stride[i];
         }
         if (!sub) continue;
+        ro.prefix = 1;  // X's attributes = Y's first ngb (as a set)
+        for (int i = 0; i < hq[k].ngb; i++) ro.prefix &= ro.pos[i] < hq[k].ngb;
         ro.table = hq[k].table;
         ro.counts = hq[k].counts;
         ro.nudaf = hq[k].nudaf;
@@ -1009,7 +1427,76 @@ FastPaths* plan_cube(lmfao_ctx* c) {
       der_coff[y] = keep_coff;
       der_k[y] = keep_k;
     }
+    // world 1: a non-prefix rollup with Y's UDAFs and few segments per tile can be merged from
+    // the sorted groups (k_merge_rollup) instead of per-group REDs.  Opt-in (LMFAO_CUBE_MERGE=1):
+    // on C5 it measured 4.1 ms for {A,C} + {B,C} against ~1.1 ms of REDs (the per-tile binary
+    // searches and the latency-bound slice walks dominate).
+    const char* mg = std::getenv("LMFAO_CUBE_MERGE");
+    int ky = -1;
+    for (size_t k = 0; k < qs.size(); k++)
+      if (sparse_of[k] == (int)y) ky = (int)k;
+    if (c->world == 1 && ky >= 0 && mg && mg[0] == '1') {
+      const GroupPlan& gy = c->groups[qs[ky].gi];
+      std::vector<Rollup> left;
+      std::vector<int> left_coff, left_k;
+      for (size_t xi = 0; xi < sp.der.size(); xi++) {
+        const Rollup& ro = sp.der[xi];
+        const int kx = der_k[y][xi];
+        const int ngy = hq[ky].ngb;
+        std::vector<int> xpos_of(ngy, -1);  // Y position -> X attribute index
+        for (int i = 0; i < ro.ngb; i++) xpos_of[ro.pos[i]] = i;
+        int p = -1;
+        for (int t = 0; t < ngy; t++)
+          if (xpos_of[t] < 0) p = t;
+        MergeRollup m{};
+        m.nudaf = ro.nudaf;
+        m.nseg = 1;
+        m.npre = 1;
+        bool ok = !ro.prefix && p >= 0 && qs[kx].dense == qs[ky].dense && ro.nudaf == gy.nudaf;
+        if (ok) {
+          m.suffix = hq[ky].stride[p];
+          m.np = p + 1;
+          for (int t = 0; t <= p; t++) {
+            m.role[t] = xpos_of[t] >= 0;
+            m.radix[t] = gy.d.radix[t];
+            m.ystr[t] = hq[ky].stride[t];
+            m.xstr[t] = m.role[t] ? hq[kx].stride[xpos_of[t]] : 0;
+            if (m.role[t]) m.npre *= gy.d.radix[t];
+            else m.nseg = (int)std::min<long long>((long long)m.nseg * gy.d.radix[t], 1 << 30);
+          }
+          for (int t = p + 1; t < ngy; t++) {
+            m.sradix[m.ns] = gy.d.radix[t];
+            m.systr[m.ns] = hq[ky].stride[t];
+            m.sxstr[m.ns] = hq[kx].stride[xpos_of[t]];
+            m.ns++;
+          }
+          m.ntile_s = (m.suffix + MR_W - 1) / MR_W;
+          const char* mm = std::getenv("LMFAO_CUBE_MERGE_MIN");  // tests: small suffix spaces too
+          ok = m.nseg <= MR_SEG && m.suffix >= (mm ? std::atoll(mm) : 256) && merge_smem(m.nudaf) <= 160 * 1024;
+        }
+        if (!ok) {
+          left.push_back(ro);
+          left_coff.push_back(der_coff[y][xi]);
+          left_k.push_back(kx);
+          continue;
+        }
+        m.yvals = gy.rvals.as<double>();
+        m.ycnt = gy.rcnts.as<unsigned long long>();
+        m.xtab = ro.table;
+        m.xcnt = ro.counts;
+        sp.merges.push_back(m);
+      }
+      sp.der = left;
+      der_coff[y] = left_coff;
+      der_k[y] = left_k;
+    }
   }
+  // the scan's levels: those of the cuboids it still updates (derived ones are not), and the
+  // dense keys it needs to find their runs
+  a.dmask = 0;
+  for (size_t k = 0; k < qs.size(); k++)
+    if (!hq[k].derived) a.dmask |= 1u << qs[k].depth;
+  a.nkey = (a.dmask >> a.R & 1u) ? a.R : std::min(a.R, 32 - __builtin_clz(a.dmask | 1u));
   // items: (cuboid, non-constant UDAF) pairs of the dense cuboids, by level, with their terms;
   // with more than CB_MEAS measures one scan per group of CB_MEAS, each with the terms of its
   // measures (the count term and the counts with the first)
@@ -1112,6 +1599,77 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
   fc->grid = nsm * per_sm;
+  for (auto& sp : fc->sparse)
+    for (auto& m : sp.merges)
+      if (ensure_smem_attr((const void*)k_merge_rollup, merge_smem(m.nudaf)))
+        return nullptr;
+  if (!fc->sparse.empty()) {
+    // the sparse cuboids' record slots: each work chunk's run ends at slevel, counted by the
+    // scan itself in count mode (keys only), then an exclusive scan gives the chunks' bases
+    // and the total the sort and reduce read
+    if (fc->rbase.alloc((nchunks + 1) * 8) || fc->dwork.alloc(16 * 4)) return nullptr;
+    CubeArgs ca = fc->parts[0];
+    ca.count_only = 1;
+    ca.tails = fc->rbase.as<long long>();
+    ca.nrows = nrows;
+    ca.work = fc->dwork.as<int>();
+    if (cudaMemsetAsync(fc->dwork.p, 0, 4, st) || cudaMemsetAsync(fc->rbase.p, 0, (nchunks + 1) * 8, st)) return nullptr;
+    if (nrows > 0) {
+      const int64_t g = std::min<int64_t>((nchunks + CB_WARPS - 1) / CB_WARPS, fc->grid);
+      k_cube<<<(unsigned)g, CB_WARPS * 32, fc->smem, st>>>(ca);
+    }
+    if (exclusive_scan_i64(fc->rbase.as<int64_t>(), fc->rbase.as<int64_t>(), nchunks + 1, st)) return nullptr;
+    for (auto& sp : fc->sparse)
+      if (cudaMemcpyAsync(sp.n.p, fc->rbase.as<long long>() + nchunks, 8, cudaMemcpyDeviceToDevice, st)) return nullptr;
+    for (int k = a.qbeg[a.slevel]; k < a.qbeg[a.slevel + 1]; k++) hq[k].rbase = fc->rbase.as<long long>();
+    if (cudaMemcpyAsync(fc->dq.p, hq.data(), hq.size() * sizeof(Cuboid), cudaMemcpyHostToDevice, st)) return nullptr;
+    // only the sparse level left to scan, no dense cuboid updated by the scan: k_cube_rec
+    CubeArgs& p0 = fc->parts[0];
+    bool rec = fc->parts.size() == 1 && p0.dmask == (1u << p0.slevel) && p0.nitem == 0 && p0.nkey <= REC_LEV &&
+               p0.nattr <= REC_ATTR &&
+               !(std::getenv("LMFAO_CUBE_REC") && std::getenv("LMFAO_CUBE_REC")[0] == '0');
+    for (int k = a.qbeg[a.slevel]; k < a.qbeg[a.slevel + 1] && rec; k++) rec = hq[k].sparse || hq[k].derived;
+    int nr = 0;
+    for (int k = a.qbeg[a.slevel]; k < a.qbeg[a.slevel + 1] && rec; k++) {
+      if (!hq[k].sparse) continue;
+      if (nr == 4) {
+        rec = false;
+        break;
+      }
+      CubeArgs::RecOut& o = p0.rec[nr++];
+      o.rkey = hq[k].rkey;
+      o.rval = hq[k].rval;
+      // per level: the part of the cell its key determines (the codes of the level's
+      // attributes × strides), tabulated over the level's dense keys
+      for (int i = 0; i < hq[k].ngb && rec; i++) {
+        const int sl = hq[k].aslot[i], l = p0.alvl[sl];
+        if (l >= p0.R) {
+          o.aslot[o.ngb] = (int8_t)sl;
+          o.stride[o.ngb++] = hq[k].stride[i];
+          continue;
+        }
+        const int64_t nk = c->rels[R.children[c->levels[l]]].nrows;
+        DevBuf& pb = fc->parts_tab[(nr - 1) * CB_LEV + l];
+        if (!pb.p) {
+          if (pb.alloc(std::max<int64_t>(nk, 1) * 4) || cudaMemsetAsync(pb.p, 0, std::max<int64_t>(nk, 1) * 4, st)) return nullptr;
+        }
+        if (nk > 0)
+          k_cell_part<<<cgrid(nk), 256, 0, st>>>(pb.as<unsigned>(), p0.acode[sl], hq[k].stride[i], nk);
+        o.part[l] = pb.as<unsigned>();
+      }
+    }
+    if (rec) {
+      p0.nrec = nr;
+      p0.meas_plain = 1;
+      for (int j = 0; j < p0.M; j++) p0.meas_plain &= !p0.midx[j] && !p0.meas_i32[j];
+      if (p0.slevel == p0.R) p0.meas_plain = 0;
+      p0.rbase = fc->rbase.as<long long>();
+      fc->rec_only = true;
+      int per = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_cube_rec<CB_MEAS + 1, false>, 256, 0) || per < 1) per = 1;
+      fc->rec_grid = nsm * per;
+    }
+  }
   if (cudaStreamSynchronize(st)) return nullptr;
   for (auto& sp : fc->sparse) {  // no dense table for these
     GroupPlan& gp = c->groups[sp.gi];

@@ -133,6 +133,34 @@ def test_cube_sparse_records(n, monkeypatch):
         assert np.allclose(v1, v2, rtol=1e-11, atol=1e-9)
 
 
+@pytest.mark.parametrize("n", [1, 4097, 40_000])
+def test_cube_rollups_from_sparse(n, monkeypatch):
+    """Every cuboid over a subset of a sparse cuboid's attributes is rolled up from its sorted
+    groups: prefix subsets by segmented warp sums, others merged per tile from the segments of
+    the dropped attributes (k_merge_rollup, opt-in: LMFAO_CUBE_MERGE=1; LMFAO_CUBE_MERGE_MIN
+    lowers its size threshold) or by per-group REDs, the smaller ones from those tables; the scan keeps only the sparse
+    level (k_cube_rec).  All three rollup routes against the oracle."""
+    db = cube_db(11, n)
+    batch = [Query(["a1", "a2", "a3"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a2", "a3"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a1", "a3"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a3", "a1"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a1", "a2"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a3"], [S((1, "m1")), S((1, "m2"), (2, None))]),
+             Query(["a2"], [S((1, "m2"))]),
+             Query([], [S((1, "m1")), S((1, None))])]
+    ref = oracle.evaluate(db, batch)
+    monkeypatch.setenv("LMFAO_CUBE_SPARSE_CELLS", "500")  # {a1,a2,a3}: 910 cells; the others dense
+    for merge, gather in (("1", "0"), ("0", "0"), ("0", "1")):  # merged / RED rollups; records gathered first
+        monkeypatch.setenv("LMFAO_CUBE_MERGE", merge)
+        monkeypatch.setenv("LMFAO_CUBE_MERGE_MIN", "1")
+        monkeypatch.setenv("LMFAO_CUBE_GATHER", gather)
+        gpu, info = run_gpu(db, batch, info=True, runs=2)
+        g = info["fast_path"]["groups"]
+        assert g["sparse"] == 1 and g["scan"] == "records", g
+        assert_parity(gpu, ref, batch)
+
+
 def test_c5_cube_sparse_abc():
     """C5's {A,B,C} cuboid at its full 5·10^8-cell domain takes the sparse path."""
     w = synth.config5(fact_rows=200_000, dim_rows=(1_000, 10_000, 100_000, 1_000_000))
