@@ -158,12 +158,19 @@ def cpu_baseline(w, max_rows, threads=0):
                       f"{cores} OpenMP threads, {dt:.1f} s"}
 
 
+REF_BUDGET_S = 150.0  # --impl reference: CPU seconds the timed steps may take in total
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
     w = workload(args.config)
     per_step = []
     rows = args.ref_rows
+    if rows <= 0:  # auto: size each step's sample so the whole run takes about REF_BUDGET_S of CPU
+        probe = cpu_baseline(w, 50_000)
+        rows = int(probe["value"] * REF_BUDGET_S / (args.warmup + args.steps))
+        rows = max(2_000, min(400_000, rows))
     for i in range(args.warmup + args.steps):
         b = cpu_baseline(w, rows)
         if i >= args.warmup:
@@ -192,7 +199,7 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C5"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-rows", type=int, default=4_000_000)
-    ap.add_argument("--ref-rows", type=int, default=400_000)
+    ap.add_argument("--ref-rows", type=int, default=0, help="rows per reference step (0: sized to the run)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

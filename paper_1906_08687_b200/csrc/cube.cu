@@ -1073,7 +1073,7 @@ struct FastCube : FastPaths {
       const long long tot = dr.xcells * (dr.nudaf + 1) * dr.split;
       k_dense_rollup<<<(unsigned)std::max<long long>(1, std::min<long long>((tot + 255) / 256, 148 * 16)), 256, 0, st>>>(dr);
     }
-    launches_add(7 + (int)sp.dense_rollups.size());
+    launches_add(3 + (gather_first ? 1 : 0) + (int)sp.dense_rollups.size());  // heads, starts, (gather), reduce, rollups
     CUDA_TRY(cudaGetLastError());
     if (!dist) return cudaSuccess;
     // world > 1: signal the owners, then merge what this rank received
@@ -1106,7 +1106,7 @@ struct FastCube : FastPaths {
     m.sorted = 1;
     k_rec_reduce<<<cgrid(capr), 256, 0, st>>>(m);
     k_x_release<<<1, 1, 0, st>>>(sp.x);
-    launches_add(9);
+    launches_add(8);
     return cudaGetLastError();
   }
 };

@@ -245,15 +245,15 @@ cudaError_t exclusive_scan_rec(const T* in, T* out, int64_t n, T* scratch, cudaS
   if (n <= 0) return cudaSuccess;
   int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles == 1) {
-    k_scan_tiles<T><<<1, SCAN_THREADS, 0, st>>>(in, out, n, nullptr);
+    k_scan_tiles<T><<<1, SCAN_THREADS, 0, st>>>(in, out, n, nullptr); launches_add(1);
     return cudaGetLastError();
   }
   T* sums = scratch;
   T* offs = scratch + tiles;
-  k_scan_tiles<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums);
+  k_scan_tiles<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(in, out, n, sums); launches_add(1);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(exclusive_scan_rec<T>(sums, offs, tiles, scratch + 2 * tiles, st));
-  k_scan_add<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(out, n, offs);
+  k_scan_add<T><<<(unsigned)tiles, SCAN_THREADS, 0, st>>>(out, n, offs); launches_add(1);
   return cudaGetLastError();
 }
 
@@ -287,11 +287,11 @@ cudaError_t radix_sort_pairs(uint32_t* keys, uint32_t* vals, int64_t n, int key_
   int passes = 0;
   for (int shift = 0; shift < key_bits; shift += 8) {
     int bits = std::min(8, key_bits - shift);
-    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, n_dev, shift, bits, hist, (int)nblocks);
+    k_radix_hist<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, n, n_dev, shift, bits, hist, (int)nblocks); launches_add(1);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(exclusive_scan_t<uint32_t>(hist, offs, (int64_t)(1 << bits) * nblocks, st, 4));
     k_radix_scatter<<<(unsigned)nblocks, SORT_THREADS, 0, st>>>(ka, va, kb, vb, n, n_dev, shift, bits, offs,
-                                                                 (int)nblocks);
+                                                                 (int)nblocks); launches_add(1);
     CUDA_TRY(cudaGetLastError());
     std::swap(ka, kb);
     std::swap(va, vb);
@@ -396,7 +396,7 @@ static unsigned grid_for(int64_t n) {
 
 cudaError_t iota_u32(uint32_t* a, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  k_iota<<<grid_for(n), 256, 0, st>>>(a, n);
+  k_iota<<<grid_for(n), 256, 0, st>>>(a, n); launches_add(1);
   return cudaGetLastError();
 }
 

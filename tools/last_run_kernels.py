@@ -1,6 +1,7 @@
 """Per-kernel device time of the last N launches of an ncu launch list (--metrics
 gpu__time_duration.sum --csv), grouped by kernel name.
-usage: python tools/last_run_kernels.py LAUNCHES.csv N"""
+usage: python tools/last_run_kernels.py LAUNCHES.csv N [SKIP]   (SKIP: ignore the last SKIP launches,
+e.g. the compaction of a fetch after the last run)"""
 import csv
 import re
 import sys
@@ -11,7 +12,9 @@ h = rows[0]
 ik, iv, iid = h.index("Kernel Name"), h.index("Metric Value"), h.index("ID")
 ks = [(int(r[iid]), re.sub(r"\(.*", "", r[ik]), float(r[iv].replace(",", ""))) for r in rows[1:]]
 agg = OrderedDict()
-for _, n, v in ks[-int(sys.argv[2]):]:
+skip = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+sel = ks[len(ks) - skip - int(sys.argv[2]):len(ks) - skip]
+for _, n, v in sel:
     a = agg.setdefault(n, [0, 0.0])
     a[0] += 1
     a[1] += v
