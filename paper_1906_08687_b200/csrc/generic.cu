@@ -208,6 +208,128 @@ __global__ void __launch_bounds__(VB_WARPS * 32) k_view_lin(const __grid_constan
   });
 }
 
+// k_view_lin for the common shape — every slot the count or one fp64 column, at most 16
+// slots (the (b) view bench; many-to-many children of covariance batches): the same segmented
+// pass and the same store/RED rule, with the run sums and lane-private sums in registers, the
+// next block's key and values loaded before this block is processed, and no per-slot branches.
+constexpr int VLF_CHUNK = 16;  // 32-row blocks per range
+template <int NS>
+__global__ void __launch_bounds__(256) k_view_lin_fast(const __grid_constant__ ViewLinArgs a,
+                                                       const int32_t* __restrict__ dense_key,
+                                                       double* __restrict__ V) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nrows = a.nrows, nblk = (nrows + 31) / 32;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // ranges of VLF_CHUNK blocks dealt round-robin to the warps (Zipf-hot keys make some ranges
+  // cheap, all lane-private sums, and others expensive, many short runs: interleaving balances)
+  const int64_t nch = (nblk + VLF_CHUNK - 1) / VLF_CHUNK;
+  for (int64_t ch = gw; ch < nch; ch += nw) {
+  const int64_t b0 = ch * VLF_CHUNK, b1 = min(nblk, b0 + VLF_CHUNK);
+  const int64_t rend = min(nrows, 32 * b1);
+  const int after = rend < nrows ? dense_key[rend] : -3;  // the row after this warp's range
+  int last = b0 > 0 ? dense_key[32 * b0 - 1] : -2;       // the row before the current block
+  double carry[NS], acc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; s++) carry[s] = acc[s] = 0.0;
+  bool cstart = false, ldirty = false;
+  auto load = [&](int64_t b, int& k, double (&x)[NS]) {
+    const int64_t row = 32 * b + lane;
+    const bool v = row < rend;
+    k = v ? dense_key[row] : -1;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+      const double* c = reinterpret_cast<const double*>(a.ca[s]);
+      x[s] = v ? (c ? c[row] : 1.0) : 0.0;
+    }
+  };
+  auto wsum = [](double x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  };
+  int nk;
+  double nx[NS];
+  load(b0, nk, nx);
+  for (int64_t b = b0; b < b1; b++) {
+    const int key = nk;
+    double x[NS];
+#pragma unroll
+    for (int s = 0; s < NS; s++) x[s] = nx[s];
+    if (b + 1 < b1) load(b + 1, nk, nx);
+    const int64_t row = 32 * b + lane;
+    const bool v = row < rend;
+    const int64_t nrem = rend - 32 * b;
+    const int nv = nrem < 32 ? (int)nrem : 32;
+    int prev = __shfl_up_sync(0xffffffffu, key, 1);
+    if (lane == 0) prev = last;
+    int next = __shfl_down_sync(0xffffffffu, key, 1);
+    const int k0n = __shfl_sync(0xffffffffu, nk, 0);
+    if (lane == 31) next = b + 1 < b1 ? k0n : after;
+    const unsigned heads = __ballot_sync(0xffffffffu, v && key != prev);
+    const bool lastlane = lane == nv - 1;
+    const bool tail = v && (lastlane || next != key);
+    const bool cont = tail && lastlane && row + 1 < nrows && next == key;  // the block's last run goes on
+    const bool carry_on = cont && row + 1 < rend;                           // ... inside this range
+    const bool c_on = __shfl_sync(0xffffffffu, (int)carry_on, nv - 1);
+    const bool c_any = __shfl_sync(0xffffffffu, (int)cont, nv - 1);
+    if (heads == 0) {  // the carried run goes on through the block: lane-private sums
+#pragma unroll
+      for (int s = 0; s < NS; s++) acc[s] += x[s];
+      ldirty = true;
+      if (!c_on) {  // the run ends with this block (or leaves the range): emit it
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+          const double t = wsum(acc[s]) + carry[s];
+          acc[s] = 0.0;
+          carry[s] = 0.0;
+          if (lastlane) {
+            double* dst = &V[(int64_t)key * NS + s];
+            if (cstart && !c_any) *dst = t;
+            else gred_add(dst, t);
+          }
+        }
+        ldirty = false;
+        cstart = false;
+      }
+      last = __shfl_sync(0xffffffffu, key, nv - 1);
+      continue;
+    }
+    if (ldirty) {  // a run starts in this block: fold the lane-private sums into the carry
+#pragma unroll
+      for (int s = 0; s < NS; s++) {
+        carry[s] += wsum(acc[s]);
+        acc[s] = 0.0;
+      }
+      ldirty = false;
+    }
+    const unsigned upto = heads & ((2u << lane) - 1u);
+    const int s0 = upto ? 31 - __clz(upto) : 0;
+    const bool first_seg = upto == 0;
+    const bool started_in = first_seg ? cstart : true;
+#pragma unroll
+    for (int s = 0; s < NS; s++) {
+      double y = x[s];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double u = __shfl_up_sync(0xffffffffu, y, d);
+        if (lane - d >= s0) y += u;
+      }
+      if (first_seg) y += carry[s];
+      if (tail && !carry_on) {
+        double* dst = &V[(int64_t)key * NS + s];
+        if (started_in && !cont) *dst = y;  // the run lies inside this warp's range
+        else gred_add(dst, y);
+      }
+      carry[s] = c_on ? __shfl_sync(0xffffffffu, y, nv - 1) : 0.0;
+    }
+    const unsigned up_l = __shfl_sync(0xffffffffu, upto, nv - 1);
+    cstart = c_on ? (up_l ? true : cstart) : false;
+    last = __shfl_sync(0xffffffffu, key, nv - 1);
+  }
+  }
+}
+
 static unsigned grid_rows(int64_t n, int per_sm = 8) {
   int64_t g = (n + 255) / 256;
   g = std::min<int64_t>(g, 148 * per_sm);
@@ -217,6 +339,27 @@ static unsigned grid_rows(int64_t n, int per_sm = 8) {
 cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, double* V, cudaStream_t st) {
   if (a.nrows <= 0) return cudaSuccess;
   if (a.nslots > VB_MAXSLOT) return cudaErrorInvalidValue;
+  bool fast = a.nslots >= 1 && a.nslots <= 16 && !(std::getenv("LMFAO_VIEW_FAST") && std::getenv("LMFAO_VIEW_FAST")[0] == '0');
+  for (int s = 0; s < a.nslots && fast; s++) fast = !a.cb[s] && (!a.ca[s] || !a.ia[s]);
+  if (fast) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    auto grid = [&](const void* f) {  // one wave of resident CTAs (each warp owns a static range)
+      int per = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, 256, 0) || per < 1) per = 1;
+      return (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.nrows + 255) / 256, (int64_t)nsm * per));
+    };
+    switch (a.nslots) {
+#define LMFAO_VLF(n) \
+  case n: k_view_lin_fast<n><<<grid((const void*)k_view_lin_fast<n>), 256, 0, st>>>(a, dense_key, V); break;
+      LMFAO_VLF(1) LMFAO_VLF(2) LMFAO_VLF(3) LMFAO_VLF(4) LMFAO_VLF(5) LMFAO_VLF(6) LMFAO_VLF(7) LMFAO_VLF(8)
+      LMFAO_VLF(9) LMFAO_VLF(10) LMFAO_VLF(11) LMFAO_VLF(12) LMFAO_VLF(13) LMFAO_VLF(14) LMFAO_VLF(15) LMFAO_VLF(16)
+#undef LMFAO_VLF
+    }
+    launches_add(1);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)VB_WARPS * a.nslots * 8 * 33;
   if (smem > 48 * 1024) {
     CUDA_TRY(ensure_smem_attr((const void*)k_view_lin, smem));

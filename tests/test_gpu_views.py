@@ -49,3 +49,24 @@ def test_view_interpreted_predicates(grandchild):
         udafs.append([Product(1.0, (ident("gv"), ident("d0")))])
     batch = [Query([], udafs), Query(["g"], udafs[:2])]
     assert_parity(run_gpu(db, batch), oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("fast", ["1", "0"])
+@pytest.mark.parametrize("n_child,n_keys,s,nfeat", [(300_007, 2_000, 1.1, 10), (90_000, 30_000, 1.1, 15),
+                                                     (50_000, 3, 0.0, 2), (64, 5, 1.0, 1), (1, 1, 0.0, 4)])
+def test_view_lin_fast_count_and_columns(fast, n_child, n_keys, s, nfeat, monkeypatch):
+    """The register path of k_view_lin (every slot the count or one fp64 column, <= 16 slots:
+    the (b) view bench's shape) and the generic one (LMFAO_VIEW_FAST=0) against the oracle:
+    runs through many blocks and warp ranges, runs inside a block, ragged ends."""
+    rng = np.random.default_rng(7)
+    keys = np.arange(n_keys, dtype=np.int32)
+    D = {"k": keys[synth.zipf_ranks(rng, n_keys, s, n_child)].astype(np.int32)}
+    for j in range(nfeat):
+        D[f"d{j}"] = rng.standard_normal(n_child)
+    F = {"k": rng.integers(0, n_keys + 2, 2_000).astype(np.int32), "x": rng.standard_normal(2_000),
+         "g": rng.integers(0, 4, 2_000).astype(np.int32)}
+    db = synth.Database([synth.Relation("F", F), synth.Relation("D", D)], "F", [("F", "D")])
+    sums = [[Product(1.0, (ident(f"d{j}"),))] for j in range(nfeat)]
+    batch = [Query([], [[Product(1.0, ())]] + sums), Query(["g"], sums[:2] + [[Product(1.0, (ident("x"),))]])]
+    monkeypatch.setenv("LMFAO_VIEW_FAST", fast)
+    assert_parity(run_gpu(db, batch, runs=2), oracle.evaluate(db, batch), batch)

@@ -1,0 +1,8 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_b.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_views.py -x -q > gpurun_out/r2_t25.log 2>&1; echo rc=$? >> gpurun_out/r2_t25.log
+for i in 1 2; do
+timeout 300 python tools/view_bench.py >> gpurun_out/r2_view3.log 2>&1
+LMFAO_VIEW_FAST=0 timeout 300 python tools/view_bench.py >> gpurun_out/r2_view3.log 2>&1
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_vb_launch2.csv python tools/view_bench.py > /dev/null 2>&1
+LMFAO_VIEW_FAST=0 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_vb_launch3.csv python tools/view_bench.py > /dev/null 2>&1
