@@ -208,125 +208,199 @@ __global__ void __launch_bounds__(VB_WARPS * 32) k_view_lin(const __grid_constan
   });
 }
 
-// k_view_lin for the common shape — every slot the count or one fp64 column, at most 16
-// slots (the (b) view bench; many-to-many children of covariance batches): the same segmented
-// pass and the same store/RED rule, with the run sums and lane-private sums in registers, the
-// next block's key and values loaded before this block is processed, and no per-slot branches.
+// k_view_lin for the common shape — every slot the count or one fp64 column (at most 16
+// column slots, at most one count: the (b) view bench; many-to-many children of covariance
+// batches): the same segmented pass and the same store/RED rule, in registers, without
+// per-slot branches.  Ranges of VLF_CHUNK blocks are dealt round-robin to the warps (Zipf-
+// hot keys make some ranges cheap and others expensive: interleaving balances them).  The
+// child is sorted by key, so a range whose first and last rows have the same key is one run
+// segment: its columns are summed as a stream (16-byte loads, no per-block key logic) — most
+// rows of a Zipf-skewed child are in such ranges.  Other ranges go block by block (segmented
+// warp sums over the runs of equal keys, lane-private sums while no run starts), the next
+// block's key and values loaded before this one is processed.
 constexpr int VLF_CHUNK = 16;  // 32-row blocks per range
+struct ViewFastArgs {
+  int64_t nrows;
+  const double* col[16];  // the column slots' columns, in kernel order
+  int8_t vslot[17];       // kernel slot s -> V column (the count, if any, is kernel slot NC)
+  int nslots;             // V's row width
+};
+// Sums over the warp of NS <= 16 lane values at once by recursive halving (16 shuffles instead
+// of 5 per value): afterwards lanes l and l ^ 1 hold the total of value vl_index(l).
+__device__ __forceinline__ int vl_index(int l) { return ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1); }
 template <int NS>
-__global__ void __launch_bounds__(256) k_view_lin_fast(const __grid_constant__ ViewLinArgs a,
+__device__ __forceinline__ double warp_sums16(const double (&x)[NS], int lane) {
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = i < NS ? x[i] : 0.0;
+#pragma unroll
+  for (int h = 8, o = 16; h >= 1; h >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < h; i++) {
+      const double send = up ? v[i] : v[h + i];
+      const double keep = up ? v[h + i] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+template <int NC, bool CNT>
+__global__ void __launch_bounds__(256) k_view_lin_fast(const __grid_constant__ ViewFastArgs a,
                                                        const int32_t* __restrict__ dense_key,
                                                        double* __restrict__ V) {
+  constexpr int NS = NC + (CNT ? 1 : 0);
   const int lane = threadIdx.x & 31;
   const int64_t nrows = a.nrows, nblk = (nrows + 31) / 32;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // ranges of VLF_CHUNK blocks dealt round-robin to the warps (Zipf-hot keys make some ranges
-  // cheap, all lane-private sums, and others expensive, many short runs: interleaving balances)
   const int64_t nch = (nblk + VLF_CHUNK - 1) / VLF_CHUNK;
-  for (int64_t ch = gw; ch < nch; ch += nw) {
-  const int64_t b0 = ch * VLF_CHUNK, b1 = min(nblk, b0 + VLF_CHUNK);
-  const int64_t rend = min(nrows, 32 * b1);
-  const int after = rend < nrows ? dense_key[rend] : -3;  // the row after this warp's range
-  int last = b0 > 0 ? dense_key[32 * b0 - 1] : -2;       // the row before the current block
-  double carry[NS], acc[NS];
-#pragma unroll
-  for (int s = 0; s < NS; s++) carry[s] = acc[s] = 0.0;
-  bool cstart = false, ldirty = false;
-  auto load = [&](int64_t b, int& k, double (&x)[NS]) {
-    const int64_t row = 32 * b + lane;
-    const bool v = row < rend;
-    k = v ? dense_key[row] : -1;
-#pragma unroll
-    for (int s = 0; s < NS; s++) {
-      const double* c = reinterpret_cast<const double*>(a.ca[s]);
-      x[s] = v ? (c ? c[row] : 1.0) : 0.0;
-    }
-  };
   auto wsum = [](double x) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
   };
-  int nk;
-  double nx[NS];
-  load(b0, nk, nx);
-  for (int64_t b = b0; b < b1; b++) {
-    const int key = nk;
-    double x[NS];
+  auto emit = [&](int key, int s, double t, bool store) {
+    double* dst = &V[(int64_t)key * a.nslots + a.vslot[s]];
+    if (store) *dst = t;
+    else gred_add(dst, t);
+  };
+  // a range's edge keys (lanes 0-3): the row before it, its first and last rows, the row
+  // after it; loaded one range ahead
+  auto edge = [&](int64_t ch) -> int {
+    if (ch >= nch || lane >= 4) return -4;
+    const int64_t e0 = ch * VLF_CHUNK, e1 = min(nblk, e0 + VLF_CHUNK), r0 = 32 * e0, re = min(nrows, 32 * e1);
+    if (lane == 0) return r0 > 0 ? dense_key[r0 - 1] : -2;
+    if (lane == 1) return dense_key[r0];
+    if (lane == 2) return dense_key[re - 1];
+    return re < nrows ? dense_key[re] : -3;
+  };
+  int en = edge(gw);
+  for (int64_t ch = gw; ch < nch; ch += nw) {
+    const int before = __shfl_sync(0xffffffffu, en, 0), first = __shfl_sync(0xffffffffu, en, 1);
+    const int lastk = __shfl_sync(0xffffffffu, en, 2), after = __shfl_sync(0xffffffffu, en, 3);
+    en = edge(ch + nw);
+    const int64_t b0 = ch * VLF_CHUNK, b1 = min(nblk, b0 + VLF_CHUNK);
+    const int64_t r0 = 32 * b0, rend = min(nrows, 32 * b1);
+    if (first == lastk) {  // one run segment: stream the columns
+      const bool store = before != first && after != first;  // the whole run lies in this range
+      const int64_t n = rend - r0;
+      double xs[NS];  // lane-private sums of every column over the range, then one warp reduction
 #pragma unroll
-    for (int s = 0; s < NS; s++) x[s] = nx[s];
-    if (b + 1 < b1) load(b + 1, nk, nx);
-    const int64_t row = 32 * b + lane;
-    const bool v = row < rend;
-    const int64_t nrem = rend - 32 * b;
-    const int nv = nrem < 32 ? (int)nrem : 32;
-    int prev = __shfl_up_sync(0xffffffffu, key, 1);
-    if (lane == 0) prev = last;
-    int next = __shfl_down_sync(0xffffffffu, key, 1);
-    const int k0n = __shfl_sync(0xffffffffu, nk, 0);
-    if (lane == 31) next = b + 1 < b1 ? k0n : after;
-    const unsigned heads = __ballot_sync(0xffffffffu, v && key != prev);
-    const bool lastlane = lane == nv - 1;
-    const bool tail = v && (lastlane || next != key);
-    const bool cont = tail && lastlane && row + 1 < nrows && next == key;  // the block's last run goes on
-    const bool carry_on = cont && row + 1 < rend;                           // ... inside this range
-    const bool c_on = __shfl_sync(0xffffffffu, (int)carry_on, nv - 1);
-    const bool c_any = __shfl_sync(0xffffffffu, (int)cont, nv - 1);
-    if (heads == 0) {  // the carried run goes on through the block: lane-private sums
+      for (int s = 0; s < NC; s++) {
+        const double* c = a.col[s] + r0;
+        double x = 0.0, y = 0.0;
+        if (n == 32 * VLF_CHUNK) {
 #pragma unroll
-      for (int s = 0; s < NS; s++) acc[s] += x[s];
-      ldirty = true;
-      if (!c_on) {  // the run ends with this block (or leaves the range): emit it
-#pragma unroll
-        for (int s = 0; s < NS; s++) {
-          const double t = wsum(acc[s]) + carry[s];
-          acc[s] = 0.0;
-          carry[s] = 0.0;
-          if (lastlane) {
-            double* dst = &V[(int64_t)key * NS + s];
-            if (cstart && !c_any) *dst = t;
-            else gred_add(dst, t);
+          for (int j = 0; j < VLF_CHUNK / 2; j++) {
+            const double2 w = reinterpret_cast<const double2*>(c)[lane + 32 * j];
+            x += w.x;
+            y += w.y;
           }
+        } else {
+          for (int64_t i = lane; i < n; i += 32) x += c[i];
         }
-        ldirty = false;
-        cstart = false;
+        xs[s] = x + y;
       }
-      last = __shfl_sync(0xffffffffu, key, nv - 1);
+      if (CNT) xs[NS - 1] = lane == 0 ? (double)n : 0.0;
+      const double t = warp_sums16<NS>(xs, lane);
+      const int si = vl_index(lane);
+      if (!(lane & 1) && si < NS) emit(first, si, t, store);
       continue;
     }
-    if (ldirty) {  // a run starts in this block: fold the lane-private sums into the carry
+    int last = before;
+    double carry[NS], acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; s++) carry[s] = acc[s] = 0.0;
+    bool cstart = false, ldirty = false;
+    auto load = [&](int64_t b, int& k, double (&x)[NS]) {
+      const int64_t row = 32 * b + lane;
+      const bool v = row < rend;
+      k = -1;
+      if (v) k = dense_key[row];
+#pragma unroll
+      for (int s = 0; s < NC; s++) {
+        x[s] = 0.0;
+        if (v) x[s] = a.col[s][row];
+      }
+      if (CNT) x[NS - 1] = v ? 1.0 : 0.0;
+    };
+    int nk;
+    double nx[NS];
+    load(b0, nk, nx);
+    for (int64_t b = b0; b < b1; b++) {
+      const int key = nk;
+      double x[NS];
+#pragma unroll
+      for (int s = 0; s < NS; s++) x[s] = nx[s];
+      if (b + 1 < b1) load(b + 1, nk, nx);
+      const int64_t row = 32 * b + lane;
+      const bool v = row < rend;
+      const int64_t nrem = rend - 32 * b;
+      const int nv = nrem < 32 ? (int)nrem : 32;
+      int prev = __shfl_up_sync(0xffffffffu, key, 1);
+      if (lane == 0) prev = last;
+      int next = __shfl_down_sync(0xffffffffu, key, 1);
+      const int k0n = __shfl_sync(0xffffffffu, nk, 0);
+      if (lane == 31) next = b + 1 < b1 ? k0n : after;
+      const unsigned heads = __ballot_sync(0xffffffffu, v && key != prev);
+      const bool lastlane = lane == nv - 1;
+      const bool tail = v && (lastlane || next != key);
+      const bool cont = tail && lastlane && row + 1 < nrows && next == key;  // the block's last run goes on
+      const bool carry_on = cont && row + 1 < rend;                           // ... inside this range
+      const bool c_on = __shfl_sync(0xffffffffu, (int)carry_on, nv - 1);
+      const bool c_any = __shfl_sync(0xffffffffu, (int)cont, nv - 1);
+      if (heads == 0) {  // the carried run goes on through the block: lane-private sums
+#pragma unroll
+        for (int s = 0; s < NS; s++) acc[s] += x[s];
+        ldirty = true;
+        if (!c_on) {  // the run ends with this block (or leaves the range): emit it
+          const double tt = warp_sums16<NS>(acc, lane);
+          const int si = vl_index(lane);
+          double cs = 0.0;
+#pragma unroll
+          for (int s = 0; s < NS; s++) {
+            if (s == si) cs = carry[s];
+            acc[s] = 0.0;
+            carry[s] = 0.0;
+          }
+          const int k0 = __shfl_sync(0xffffffffu, key, 0);  // the block's key (lanes past the end hold -1)
+          if (!(lane & 1) && si < NS) emit(k0, si, tt + cs, cstart && !c_any);
+          ldirty = false;
+          cstart = false;
+        }
+        last = __shfl_sync(0xffffffffu, key, nv - 1);
+        continue;
+      }
+      if (ldirty) {  // a run starts in this block: fold the lane-private sums into the carry
+        const double tt = warp_sums16<NS>(acc, lane);
+#pragma unroll
+        for (int s = 0; s < NS; s++) {
+          carry[s] += __shfl_sync(0xffffffffu, tt, (s >> 3 & 1) * 16 + (s >> 2 & 1) * 8 + (s >> 1 & 1) * 4 + (s & 1) * 2);
+          acc[s] = 0.0;
+        }
+        ldirty = false;
+      }
+      const unsigned upto = heads & ((2u << lane) - 1u);
+      const int s0 = upto ? 31 - __clz(upto) : 0;
+      const bool first_seg = upto == 0;
+      const bool started_in = first_seg ? cstart : true;
 #pragma unroll
       for (int s = 0; s < NS; s++) {
-        carry[s] += wsum(acc[s]);
-        acc[s] = 0.0;
-      }
-      ldirty = false;
-    }
-    const unsigned upto = heads & ((2u << lane) - 1u);
-    const int s0 = upto ? 31 - __clz(upto) : 0;
-    const bool first_seg = upto == 0;
-    const bool started_in = first_seg ? cstart : true;
+        double y = x[s];
 #pragma unroll
-    for (int s = 0; s < NS; s++) {
-      double y = x[s];
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const double u = __shfl_up_sync(0xffffffffu, y, d);
-        if (lane - d >= s0) y += u;
+        for (int d = 1; d < 32; d <<= 1) {
+          const double u = __shfl_up_sync(0xffffffffu, y, d);
+          if (lane - d >= s0) y += u;
+        }
+        if (first_seg) y += carry[s];
+        if (tail && !carry_on) emit(key, s, y, started_in && !cont);  // store: the run lies inside this range
+        carry[s] = c_on ? __shfl_sync(0xffffffffu, y, nv - 1) : 0.0;
       }
-      if (first_seg) y += carry[s];
-      if (tail && !carry_on) {
-        double* dst = &V[(int64_t)key * NS + s];
-        if (started_in && !cont) *dst = y;  // the run lies inside this warp's range
-        else gred_add(dst, y);
-      }
-      carry[s] = c_on ? __shfl_sync(0xffffffffu, y, nv - 1) : 0.0;
+      const unsigned up_l = __shfl_sync(0xffffffffu, upto, nv - 1);
+      cstart = c_on ? (up_l ? true : cstart) : false;
+      last = __shfl_sync(0xffffffffu, key, nv - 1);
     }
-    const unsigned up_l = __shfl_sync(0xffffffffu, upto, nv - 1);
-    cstart = c_on ? (up_l ? true : cstart) : false;
-    last = __shfl_sync(0xffffffffu, key, nv - 1);
-  }
   }
 }
 
@@ -340,22 +414,42 @@ cudaError_t launch_view_lin(const ViewLinArgs& a, const int32_t* dense_key, doub
   if (a.nrows <= 0) return cudaSuccess;
   if (a.nslots > VB_MAXSLOT) return cudaErrorInvalidValue;
   bool fast = a.nslots >= 1 && a.nslots <= 16 && !(std::getenv("LMFAO_VIEW_FAST") && std::getenv("LMFAO_VIEW_FAST")[0] == '0');
-  for (int s = 0; s < a.nslots && fast; s++) fast = !a.cb[s] && (!a.ca[s] || !a.ia[s]);
+  int ncnt = 0;
+  for (int s = 0; s < a.nslots && fast; s++) {
+    fast = !a.cb[s] && (!a.ca[s] || !a.ia[s]) && (reinterpret_cast<uintptr_t>(a.ca[s]) & 15) == 0;  // 16-byte loads
+    ncnt += !a.ca[s];
+  }
+  fast = fast && ncnt <= 1;
   if (fast) {
+    ViewFastArgs f{};
+    f.nrows = a.nrows;
+    f.nslots = a.nslots;
+    int nc = 0;
+    for (int s = 0; s < a.nslots; s++)
+      if (a.ca[s]) {
+        f.col[nc] = reinterpret_cast<const double*>(a.ca[s]);
+        f.vslot[nc++] = (int8_t)s;
+      }
+    for (int s = 0; s < a.nslots; s++)
+      if (!a.ca[s]) f.vslot[nc] = (int8_t)s;  // the count: kernel slot nc
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    auto grid = [&](const void* f) {  // one wave of resident CTAs (each warp owns a static range)
+    auto grid = [&](const void* fn) {  // one wave of resident CTAs
       int per = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, f, 256, 0) || per < 1) per = 1;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, 0) || per < 1) per = 1;
       return (unsigned)std::max<int64_t>(1, std::min<int64_t>((a.nrows + 255) / 256, (int64_t)nsm * per));
     };
-    switch (a.nslots) {
-#define LMFAO_VLF(n) \
-  case n: k_view_lin_fast<n><<<grid((const void*)k_view_lin_fast<n>), 256, 0, st>>>(a, dense_key, V); break;
+    switch (nc * 2 + (ncnt ? 1 : 0)) {
+#define LMFAO_VLF(n)                                                                                            \
+  case 2 * n: k_view_lin_fast<n, false><<<grid((const void*)k_view_lin_fast<n, false>), 256, 0, st>>>(f, dense_key, V); break; \
+  case 2 * n + 1: k_view_lin_fast<n, true><<<grid((const void*)k_view_lin_fast<n, true>), 256, 0, st>>>(f, dense_key, V); break;
       LMFAO_VLF(1) LMFAO_VLF(2) LMFAO_VLF(3) LMFAO_VLF(4) LMFAO_VLF(5) LMFAO_VLF(6) LMFAO_VLF(7) LMFAO_VLF(8)
-      LMFAO_VLF(9) LMFAO_VLF(10) LMFAO_VLF(11) LMFAO_VLF(12) LMFAO_VLF(13) LMFAO_VLF(14) LMFAO_VLF(15) LMFAO_VLF(16)
+      LMFAO_VLF(9) LMFAO_VLF(10) LMFAO_VLF(11) LMFAO_VLF(12) LMFAO_VLF(13) LMFAO_VLF(14) LMFAO_VLF(15)
 #undef LMFAO_VLF
+      case 1: k_view_lin_fast<0, true><<<grid((const void*)k_view_lin_fast<0, true>), 256, 0, st>>>(f, dense_key, V); break;
+      case 32: k_view_lin_fast<16, false><<<grid((const void*)k_view_lin_fast<16, false>), 256, 0, st>>>(f, dense_key, V); break;
+      default: return cudaErrorInvalidValue;
     }
     launches_add(1);
     return cudaGetLastError();
