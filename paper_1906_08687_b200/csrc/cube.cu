@@ -598,6 +598,8 @@ struct RecReduce {
   int merge;           // world > 1, received groups: rval = own vals, parity from the epoch
   int sorted;          // rval is already in sorted order (k_rec_gather): perm not used
   unsigned* gcell;     // (merge rollups) the groups' cells
+  double rinv[CB_GB];  // 1 / radix of Y's attributes (decode by reciprocal, corrected)
+  size_t smem;         // dynamic shared memory: the coefficients and the rollups (0: read from global)
   XArgs x;
 };
 // A dense cuboid X at the sparse cuboid Y's level whose attributes are a subset of Y's: its
@@ -612,7 +614,8 @@ struct Rollup {
   long long stride[CB_GB];
   unsigned long long cmask;
   int prefix;          // X's attributes are the first ngb of Y's: X's cells are runs of consecutive groups
-  int pad_;
+  int same;            // X's UDAFs are Y's (same coefficient rows): X's values are the group's
+  long long xstr_y[CB_GB];  // X's stride of Y's attribute t (0: X drops it)
 };
 // The records' sums in sorted order: sval[i][j] = rval[perm[i]][j], one thread per (i, j), so the
 // M1 threads of a record read its M1 doubles together (a record per two 32-byte sectors instead
@@ -817,7 +820,40 @@ __global__ void __launch_bounds__(256) k_merge_rollup(const __grid_constant__ Me
 }
 inline size_t merge_smem(int nudaf) { return (size_t)MR_W * nudaf * 8 + MR_W * 8 + MR_SEG * 4 + (MR_SEG + 2) * 4 + MR_SEG * 8; }
 
+__device__ __forceinline__ unsigned div_rinv(unsigned n, unsigned d, double rinv, unsigned& rem) {
+  unsigned q = (unsigned)((double)n * rinv);  // within one of the quotient
+  long long r = (long long)n - (long long)q * d;
+  if (r < 0) {
+    q--;
+    r += d;
+  } else if (r >= (long long)d) {
+    q++;
+    r -= d;
+  }
+  rem = (unsigned)r;
+  return q;
+}
 __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecReduce r) {
+  // the UDAF coefficients and the rollups in shared memory (read by every group)
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const Rollup* der = r.der;
+  const double* ycoef = r.coef;
+  if (r.smem) {
+    Rollup* sd = reinterpret_cast<Rollup*>(rsm);
+    double* sc = reinterpret_cast<double*>(rsm + r.nder * sizeof(Rollup));
+    for (int i = threadIdx.x; i < r.nudaf * r.M1; i += blockDim.x) sc[i] = r.coef[i];
+    double* xc0 = sc + r.nudaf * r.M1;
+    for (int x = 0; x < r.nder; x++) {
+      if (threadIdx.x == 0) sd[x] = r.der[x];
+      for (int i = threadIdx.x; i < r.der[x].nudaf * r.M1; i += blockDim.x) xc0[i] = r.der[x].coef[i];
+      __syncthreads();
+      if (threadIdx.x == 0) sd[x].coef = xc0;
+      xc0 += r.der[x].nudaf * r.M1;
+    }
+    __syncthreads();
+    der = sd;
+    ycoef = sc;
+  }
   const int64_t ng = (int64_t)*r.ng;
   const double* rval = r.rval;
   int b = 0;
@@ -834,6 +870,8 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
     for (int j = 0; j <= CB_MEAS; j++) S[j] = 0.0;
     unsigned cell = 0;
     unsigned code[CB_GB];
+#pragma unroll
+    for (int a = 0; a < CB_GB; a++) code[a] = 0;
     if (act) {
       const int64_t t0 = r.gstart[g], t1 = r.gstart[g + 1];
       for (int64_t t = t0; t < t1; t++) {
@@ -854,9 +892,10 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
         }
       }
       cell = r.key[t0];  // sparse cuboids have < 2^32 cells: 32-bit decode
+      unsigned rest = cell;  // row-major: the last attribute varies fastest
 #pragma unroll
-      for (int a = 0; a < CB_GB; a++)
-        if (a < r.d.ngb) code[a] = (cell / (unsigned)r.d.stride[a]) % (unsigned)r.d.radix[a];
+      for (int a = CB_GB - 1; a >= 0; a--)
+        if (a < r.d.ngb) rest = div_rinv(rest, (unsigned)r.d.radix[a], r.rinv[a], code[a]);
       if (r.send) {  // fused exchange: the group goes straight to its owner's buffer (peer memory)
         const int o = (int)(cell / (unsigned long long)r.x.chunk);
         const unsigned long long slot = atomicAdd(&r.x.hdr[o]->cnt[b], 1ull);
@@ -870,12 +909,14 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
           atomicExch(&r.x.hdr[r.x.rank]->err, 2);
         }
       } else {
-        for (int a = 0; a < r.d.ngb; a++) r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
+#pragma unroll
+        for (int a = 0; a < CB_GB; a++)
+          if (a < r.d.ngb) r.okeys[g * r.d.ngb + a] = r.d.dict[a][code[a]];
         for (int u = 0; u < r.nudaf; u++) {
           double v = 0.0;
 #pragma unroll
           for (int j = 0; j <= CB_MEAS; j++)
-            if (j < r.M1) v = fma(r.coef[u * r.M1 + j], S[j], v);
+            if (j < r.M1) v = fma(ycoef[u * r.M1 + j], S[j], v);
           r.ovals[g * r.nudaf + u] = v;
         }
         r.ocnts[g] = (unsigned long long)S[0];
@@ -883,12 +924,15 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
       }
     }
     for (int x = 0; x < r.nder; x++) {
-      const Rollup& X = r.der[x];
+      const Rollup& X = der[x];
       long long xc = -1 - lane;  // idle lanes: cells of their own
       if (act) {
         xc = 0;
-        for (int i = 0; i < X.ngb; i++) xc += (long long)code[X.pos[i]] * X.stride[i];
+#pragma unroll
+        for (int t = 0; t < CB_GB; t++)
+          if (t < r.d.ngb) xc += (long long)code[t] * X.xstr_y[t];
       }
+      const double* xcoef = X.same ? ycoef : X.coef;
       if (X.prefix) {
         const long long xp = __shfl_up_sync(BFULL, xc, 1), xn = __shfl_down_sync(BFULL, xc, 1);
         const unsigned starts = __ballot_sync(BFULL, lane == 0 || xp != xc) | 1u;
@@ -901,7 +945,7 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
           double v = 0.0;
 #pragma unroll
           for (int j = 0; j <= CB_MEAS; j++)
-            if (j < r.M1) v = fma(X.coef[u * r.M1 + j], S[j], v);
+            if (j < r.M1) v = fma(xcoef[u * r.M1 + j], S[j], v);
           v = seg_scan(v, lane, s0);
           if (tail && v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
         }
@@ -912,7 +956,7 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
           double v = 0.0;
 #pragma unroll
           for (int j = 0; j <= CB_MEAS; j++)
-            if (j < r.M1) v = fma(X.coef[u * r.M1 + j], S[j], v);
+            if (j < r.M1) v = fma(xcoef[u * r.M1 + j], S[j], v);
           if (v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
         }
       }
@@ -940,6 +984,7 @@ struct SparseOut {  // per sparse cuboid: record buffers and sort temporaries
   DevBuf sval;                 // records' sums in sorted order (k_rec_gather), local then received
   std::vector<DenseRollup> dense_rollups;  // derived cuboids summed from a larger derived one, after the reduce
   std::vector<MergeRollup> merges;        // derived cuboids merged from the sorted groups (world 1), after the reduce
+  size_t reduce_smem = 0;                 // k_rec_reduce's shared memory (coefficients and rollups)
   XArgs x{};
   Comm* comm = nullptr;
   SparseOut() = default;
@@ -1046,6 +1091,8 @@ struct FastCube : FastPaths {
     r.M1 = ca.M + 1;
     r.nudaf = gp.nudaf;
     r.coef = dcoef.as<double>() + sp.coff;
+    for (int a = 0; a < gp.d.ngb; a++) r.rinv[a] = 1.0 / (double)gp.d.radix[a];
+    r.smem = sp.reduce_smem;
     r.d = gp.d;
     r.okeys = gp.rkeys.as<int32_t>();
     r.ovals = gp.rvals.as<double>();
@@ -1060,7 +1107,7 @@ struct FastCube : FastPaths {
       r.sorted = 1;
     }
     r.gcell = sp.merges.empty() || dist ? nullptr : sp.excl.as<unsigned>();  // excl is free after k_rec_starts
-    k_rec_reduce<<<cgrid(cap), 256, 0, st>>>(r);
+    k_rec_reduce<<<cgrid(cap), 256, r.smem, st>>>(r);
     for (auto& mr : sp.merges) {
       MergeRollup m = mr;
       m.gcell = sp.excl.as<unsigned>();
@@ -1104,6 +1151,7 @@ struct FastCube : FastPaths {
     k_rec_gather<<<cgrid(capr * m.M1), 256, 0, st>>>(m, sp.sval.as<double>());
     m.rval = sp.sval.as<double>();
     m.sorted = 1;
+    m.smem = 0;
     k_rec_reduce<<<cgrid(capr), 256, 0, st>>>(m);
     k_x_release<<<1, 1, 0, st>>>(sp.x);
     launches_add(8);
@@ -1583,6 +1631,23 @@ FastPaths* plan_cube(lmfao_ctx* c) {
   for (size_t y = 0; y < fc->sparse.size(); y++) {
     SparseOut& sp = fc->sparse[y];
     for (size_t x = 0; x < sp.der.size(); x++) sp.der[x].coef = fc->dcoef.as<double>() + der_coff[y][x];
+    {  // rollup cells from Y's codes; X's UDAFs identical to Y's; the reduce's shared memory
+      int ky = -1;
+      for (size_t k = 0; k < qs.size(); k++)
+        if (sparse_of[k] == (int)y) ky = (int)k;
+      const GroupPlan& gy = c->groups[qs[ky].gi];
+      size_t sm = (size_t)gy.nudaf * M1 * 8;
+      for (size_t x = 0; x < sp.der.size(); x++) {
+        Rollup& ro = sp.der[x];
+        const int kx = der_k[y][x];
+        for (int t = 0; t < CB_GB; t++) ro.xstr_y[t] = 0;
+        for (int i = 0; i < ro.ngb; i++) ro.xstr_y[ro.pos[i]] = ro.stride[i];
+        ro.same = qs[kx].dense == qs[ky].dense;
+        sm += sizeof(Rollup) + (size_t)ro.nudaf * M1 * 8;
+      }
+      sp.reduce_smem = sm <= 96 * 1024 ? sm : 0;
+      if (sp.reduce_smem > 48 * 1024 && ensure_smem_attr((const void*)k_rec_reduce, sp.reduce_smem)) return nullptr;
+    }
     if (sp.dder.alloc(std::max<size_t>(sp.der.size(), 1) * sizeof(Rollup))) return nullptr;
     if (!sp.der.empty() &&
         cudaMemcpyAsync(sp.dder.p, sp.der.data(), sp.der.size() * sizeof(Rollup), cudaMemcpyHostToDevice, st))
