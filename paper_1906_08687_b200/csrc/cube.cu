@@ -50,7 +50,8 @@ struct Cuboid {
   double* rval;
   const long long* rbase;
   long long rcap;
-  long long pad_;
+  int smoff;                    // >= 0: a small table kept per CTA in shared memory at smoff (doubles):
+  int sncell;                   //   [sncell][nudaf] doubles, then the counts [sncell] (u64)
 };
 static_assert(sizeof(Cuboid) % 16 == 0, "cuboids are copied to shared memory in 16-byte units");
 // (cuboid, UDAF) pair of a level: value = Σ_{t in [t0, t1)} tc[t] · S_{tj[t]}
@@ -83,6 +84,7 @@ struct CubeArgs {
   const double* tc;             // [nterm] coefficient
   int ablate;                   // LMFAO_CUBE_ABLATE (profiling): 1 no flush, 2 counts only
   int nocount;                  // a later measure group's scan: the counts come from the first
+  int nsmall;                   // doubles of the per-CTA small tables (shared memory)
   int slevel;                   // the sparse cuboids' level (-1: none)
   int count_only;               // plan time: count each chunk's run ends at slevel into tails[chunk]
   long long* tails;
@@ -115,21 +117,26 @@ __device__ __forceinline__ double seg_scan(double v, int lane, int s0) {
 // shared memory: [cuboids | items | tj | tc | per warp: S[32][CB_MEAS+1], carry[CB_LEV+1][CB_MEAS+1],
 // cells[32][CB_QD], codes[32][CB_ATTR]]
 struct CubeSmem {
-  size_t q, items, tj, tc, warps, per_warp;
-  __host__ __device__ CubeSmem(int nq, int nitem, int nterm) {
+  size_t q, items, tj, tc, warps, per_warp, small;
+  __host__ __device__ CubeSmem(int nq, int nitem, int nterm, int nsmall = 0) {
     q = 0;
     items = (nq * sizeof(Cuboid) + 15) / 16 * 16;
     tj = items + (nitem * sizeof(CubeItem) + 15) / 16 * 16;
     tc = tj + (nterm + 15) / 16 * 16;
     warps = tc + (size_t)nterm * 8;
     per_warp = (32 * (CB_MEAS + 1) + (CB_LEV + 1) * (CB_MEAS + 1) + 32 * CB_QD) * 8 + 32 * CB_ATTR * 4;
+    small = warps + CB_WARPS * per_warp;
+    nsm = nsmall;
   }
-  size_t total() const { return warps + CB_WARPS * per_warp; }
+  int nsm;
+  size_t total() const { return small + (size_t)nsm * 8; }
 };
 
 __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ CubeArgs a) {
   extern __shared__ __align__(16) unsigned char csm[];
-  const CubeSmem L(a.nq, a.nitem, a.nterm);
+  const CubeSmem L(a.nq, a.nitem, a.nterm, a.nsmall);
+  double* stab = reinterpret_cast<double*>(csm + L.small);  // the small tables of this CTA
+  for (int i = threadIdx.x; i < a.nsmall; i += blockDim.x) stab[i] = 0.0;
   const Cuboid* sq = reinterpret_cast<const Cuboid*>(csm + L.q);
   const CubeItem* items = reinterpret_cast<const CubeItem*>(csm + L.items);
   const int8_t* tj = reinterpret_cast<const int8_t*>(csm + L.tj);
@@ -274,7 +281,12 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
               if (act && !q.derived) {
                 for (int i = 0; i < q.ngb; i++) cell += (long long)codes[t * CB_ATTR + q.aslot[i]] * q.stride[i];
                 cells[t * CB_QD + qk] = cell;
-                if (!q.sparse && !a.nocount) gred_add(&q.counts[cell], (unsigned long long)S[t * (CB_MEAS + 1)]);
+                if (!q.sparse && !a.nocount) {
+                  const unsigned long long n = (unsigned long long)S[t * (CB_MEAS + 1)];
+                  if (q.smoff >= 0)
+                    atomicAdd(reinterpret_cast<unsigned long long*>(stab + q.smoff + q.sncell * q.nudaf) + cell, n);
+                  else gred_add(&q.counts[cell], n);
+                }
               }
               if (act && q.sparse) {  // the t-th run end of this block: slot fixed at plan time
                 const long long slot = rb + rdone + t;
@@ -300,7 +312,11 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                   if (e.t1 == e.t0 + 1) val = e.c1 * S[t * (CB_MEAS + 1) + e.j1];
                   else
                     for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
-                  if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
+                  if (val != 0.0) {
+                    const long long at = cells[t * CB_QD + e.qk] * q.nudaf + e.u;
+                    if (q.smoff >= 0) sred_add(stab + q.smoff + at, val);
+                    else gred_add(q.table + at, val);
+                  }
                 }
               }
             } else if (nid > 32) {
@@ -312,7 +328,11 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
                   if (e.t1 == e.t0 + 1) val = e.c1 * S[t * (CB_MEAS + 1) + e.j1];
                   else
                     for (int k = e.t0; k < e.t1; k++) val = fma(tc[k], S[t * (CB_MEAS + 1) + tj[k]], val);
-                  if (val != 0.0) gred_add(q.table + cells[t * CB_QD + e.qk] * q.nudaf + e.u, val);
+                  if (val != 0.0) {
+                    const long long at = cells[t * CB_QD + e.qk] * q.nudaf + e.u;
+                    if (q.smoff >= 0) sred_add(stab + q.smoff + at, val);
+                    else gred_add(q.table + at, val);
+                  }
                 }
             }
           }
@@ -322,6 +342,18 @@ __global__ void __launch_bounds__(CB_WARPS * 32) k_cube(const __grid_constant__ 
       }
     }
     if (a.count_only && lane == 0) a.tails[ch] = rdone;
+  }
+  if (a.nsmall == 0) return;
+  __syncthreads();  // the CTA's small tables -> the global ones, nonzero entries only
+  for (int k = 0; k < a.nq; k++) {
+    const Cuboid& q = sq[k];
+    if (q.smoff < 0) continue;
+    const int nd = q.sncell * q.nudaf;  // [cells][nudaf] doubles, then the counts
+    for (int i = threadIdx.x; i < nd; i += blockDim.x)
+      if (stab[q.smoff + i] != 0.0) gred_add(q.table + i, stab[q.smoff + i]);
+    const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(stab + q.smoff + nd);
+    for (int i = threadIdx.x; i < q.sncell; i += blockDim.x)
+      if (sc[i]) gred_add(&q.counts[i], sc[i]);
   }
 }
 
@@ -1539,6 +1571,25 @@ FastPaths* plan_cube(lmfao_ctx* c) {
       der_k[y] = left_k;
     }
   }
+  // small dense tables (C5-like cubes over tiny domains; a root categorical's group-bys, whose
+  // runs end at nearly every row): one copy per CTA in shared memory, flushed once at the end —
+  // REDs from every SM on a handful of global addresses serialise in L2.  LMFAO_CUBE_SMALL=0: off.
+  {
+    const char* sm = std::getenv("LMFAO_CUBE_SMALL");
+    const bool on = !(sm && sm[0] == '0');
+    int used = 0;
+    for (size_t k = 0; k < hq.size(); k++) {
+      hq[k].smoff = -1;
+      hq[k].sncell = 0;
+      const GroupPlan& g = c->groups[qs[k].gi];
+      const int64_t need = g.ncells * (hq[k].nudaf + 1);
+      if (!on || hq[k].sparse || hq[k].derived || need > 1024 || used + need > 4096) continue;
+      hq[k].smoff = used;
+      hq[k].sncell = (int)g.ncells;
+      used += (int)need;
+    }
+    a.nsmall = used;
+  }
   // the scan's levels: those of the cuboids it still updates (derived ones are not), and the
   // dense keys it needs to find their runs
   a.dmask = 0;
@@ -1654,7 +1705,7 @@ FastPaths* plan_cube(lmfao_ctx* c) {
       return nullptr;
   }
   fc->ca = fc->parts[0];
-  fc->smem = CubeSmem(a.nq, max_item, max_term).total();
+  fc->smem = CubeSmem(a.nq, max_item, max_term, a.nsmall).total();
   if (fc->smem > 227 * 1024) return nullptr;
   if (fc->smem > 48 * 1024 &&
       cudaFuncSetAttribute(k_cube, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc->smem))

@@ -70,6 +70,19 @@ def test_cube_ragged(n):
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
 
 
+@pytest.mark.parametrize("small", ["1", "0"])
+def test_cube_small_tables_in_shared_memory(small, monkeypatch):
+    """Dense cuboids of at most 1024 values (cells x (UDAFs + 1)) accumulate in a per-CTA copy in
+    shared memory, flushed once (LMFAO_CUBE_SMALL=0: global REDs throughout); a root group-by
+    attribute makes nearly every row a run end, the case the copies are for."""
+    db = cube_db(12, 30_011)
+    monkeypatch.setenv("LMFAO_CUBE_SMALL", small)
+    batch = rich_batch()
+    gpu, info = run_gpu(db, batch, info=True, runs=2)
+    assert info["fast_path"]["groups"]["kind"] == "cube", info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
 @pytest.mark.parametrize("s", [0.0, 2.5])
 def test_cube_skew_matches_generic(s, monkeypatch):
     db = cube_db(2, 50_000)
