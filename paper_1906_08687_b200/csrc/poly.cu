@@ -3,7 +3,7 @@
 // monomials, i.e. sums of products of up to four features).
 //
 // Every product of the batch is split into two "halves", monomials of at most two features,
-// from a small set H = {h_1 .. h_n} (n <= 24) chosen at plan time; the batch is then entries of
+// from a small set H = {1, h_1 .. h_n} (n <= 24) chosen at plan time; the batch is then entries of
 // the Gram matrix G = Σ_rows u u^T with u = [h_1(row) .. h_n(row)] — a dense contraction with K =
 // the rows, as FP64 DMMA m8n8k4 tiles: per 4-row group one DMMA per (t, s) tile pair, t <= s.
 // The features are root columns or columns of primary-key children of the root (one joined row
@@ -32,8 +32,11 @@ struct PolyArgs {
   const int32_t* fk[PL_ATTR];   // null: root column
   int isint[PL_ATTR];
   int8_t ha[PL_MAXT * 8], hb[PL_MAXT * 8];  // half h = feature ha (or 1 if -1) × feature hb (or 1)
-  double* partials;             // [warps][PL_MAXT*PL_MAXT][64]
+  double* partials;             // [warps][tile pairs × 64 | NT × 8 linear sums]
 };
+// The constant half 1 is not a tile column: its Gram row is the linear sums Σ h (lane sums, one
+// DADD per half and group) and its corner the row count.  So C2-like covariance batches over 8
+// features (halves 1, x_1..x_8) need one tile, one DMMA per 4-row group.
 
 __device__ __forceinline__ void pdmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -48,23 +51,31 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_poly(const __grid_constant__ 
   const int64_t nblk = (a.nrows + 31) / 32;
   const int64_t gw = (int64_t)blockIdx.x * PL_WARPS + wib, NW = (int64_t)gridDim.x * PL_WARPS;
   const int64_t b0 = nblk * gw / NW, b1 = nblk * (gw + 1) / NW;
-  double acc[NT * (NT + 1) / 2][2];
+  double acc[NT * (NT + 1) / 2][2], lin[NT];
 #pragma unroll
   for (int t = 0; t < NT * (NT + 1) / 2; t++) acc[t][0] = acc[t][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; t++) lin[t] = 0.0;
   double (*f)[33] = fv[wib];
-  for (int64_t b = b0; b < b1; b++) {
+  // the block's feature values, loaded one block ahead
+  auto load = [&](int64_t b, double (&x)[PL_ATTR]) {
     const int64_t row = 32 * b + lane;
     const bool v = row < a.nrows;
 #pragma unroll
     for (int i = 0; i < PL_ATTR; i++) {
-      if (i >= a.nattr) break;
-      double x = 0.0;
-      if (v) {
+      x[i] = 0.0;
+      if (i < a.nattr && v) {
         const int64_t r = a.fk[i] ? (int64_t)a.fk[i][row] : row;
-        x = a.isint[i] ? (double)reinterpret_cast<const int32_t*>(a.col[i])[r] : reinterpret_cast<const double*>(a.col[i])[r];
+        x[i] = a.isint[i] ? (double)reinterpret_cast<const int32_t*>(a.col[i])[r] : reinterpret_cast<const double*>(a.col[i])[r];
       }
-      f[i][lane] = x;
     }
+  };
+  double nx[PL_ATTR];
+  if (b0 < b1) load(b0, nx);
+  for (int64_t b = b0; b < b1; b++) {
+#pragma unroll
+    for (int i = 0; i < PL_ATTR; i++) f[i][lane] = nx[i];
+    if (b + 1 < b1) load(b + 1, nx);
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < 8; j++) {
@@ -78,6 +89,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_poly(const __grid_constant__ 
         if (ia >= 0) x *= f[ia][r];
         if (ib >= 0) x *= f[ib][r];
         h[t] = x;
+        lin[t] += x;
       }
       int p = 0;
 #pragma unroll
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_poly(const __grid_constant__ 
     }
     __syncwarp();
   }
-  double* out = a.partials + (size_t)gw * (NT * (NT + 1) / 2) * 64;
+  double* out = a.partials + (size_t)gw * (NT * (NT + 1) / 2 * 64 + NT * 8);
   int p = 0;
 #pragma unroll
   for (int t = 0; t < NT; t++)
@@ -96,15 +108,32 @@ __global__ void __launch_bounds__(PL_WARPS * 32) k_poly(const __grid_constant__ 
       out[p * 64 + m * 8 + 2 * k] = acc[p][0];  // tile (t, s): D[m][n] = Σ h_{8t+m} h_{8s+n}
       out[p * 64 + m * 8 + 2 * k + 1] = acc[p][1];
     }
+#pragma unroll
+  for (int t = 0; t < NT; t++) {  // Σ h_{8t+m} over the warp's rows: the 4 lanes k of half m
+    double l = lin[t];
+    l += __shfl_xor_sync(PFULL, l, 1);
+    l += __shfl_xor_sync(PFULL, l, 2);
+    if (k == 0) out[NT * (NT + 1) / 2 * 64 + t * 8 + m] = l;
+  }
 }
 
-// src[e] = Σ_w partials[w][e], fixed order
-__global__ void k_poly_sum(const double* __restrict__ partials, int nw, int n, double* __restrict__ src) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+// src[e] = Σ_w partials[w][e] in a fixed order: one CTA per element, its threads over strided
+// warps, then a fixed tree; src[n] = the row count (the constant half's corner)
+__global__ void k_poly_sum(const double* __restrict__ partials, int nw, int n, double* __restrict__ src, int64_t nrows) {
+  __shared__ double red[256];
+  for (int e = blockIdx.x; e < n; e += gridDim.x) {
     double s = 0.0;
-    for (int w = 0; w < nw; w++) s += partials[(size_t)w * n + e];
-    src[e] = s;
+    for (int w = threadIdx.x; w < nw; w += blockDim.x) s += partials[(size_t)w * n + e];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) src[e] = red[0];
+    __syncthreads();
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) src[n] = (double)nrows;
 }
 __global__ void k_poly_assemble(const double* __restrict__ src, const int32_t* __restrict__ toff,
                                 const int32_t* __restrict__ tidx, const double* __restrict__ tcoef, int nout,
@@ -137,7 +166,7 @@ struct FastPoly : FastPaths {
     else if (pa.nt == 2) k_poly<2><<<grid, PL_WARPS * 32, 0, st>>>(a);
     else k_poly<3><<<grid, PL_WARPS * 32, 0, st>>>(a);
     scan_timer_end(c, st);
-    k_poly_sum<<<(npart + 127) / 128, 128, 0, st>>>(partials.as<double>(), nw, npart, src.as<double>());
+    k_poly_sum<<<std::min(npart, 1024), 256, 0, st>>>(partials.as<double>(), nw, npart, src.as<double>(), a.nrows);
     k_poly_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
                                                             tcoef.as<double>(), nout, c->scalar_out.as<double>(),
                                                             count_idx, c->scalar_count.as<unsigned long long>());
@@ -189,19 +218,19 @@ FastPaths* plan_poly(lmfao_ctx* c) {
   auto half_of = [&](std::pair<int, int> h) -> int {
     auto it = half.find(h);
     if (it != half.end()) return it->second;
-    if ((int)halves.size() == PL_MAXT * 8) return -1;
+    if ((int)halves.size() == PL_MAXT * 8 + 1) return -1;  // the constant + 24 tile columns
     half[h] = (int)halves.size();
     halves.push_back(h);
     return (int)halves.size() - 1;
   };
   auto mono = [](int x, int y) { return x <= y ? std::make_pair(x, y) : std::make_pair(y, x); };
-  half_of({-1, -1});  // h_0 = 1: the count is G[0][0]
+  half_of({-1, -1});  // h_0 = 1: not a tile column (linear sums and the count)
   struct T {
     double coef;
     int a, b;
   };
   std::vector<std::vector<T>> outs;
-  bool higher = false;  // a product with more than two factors (otherwise cov.cu / gram.cu serve)
+  bool higher = false;  // a product with more than two factors
   for (int q : c->scalar_queries)
     for (auto& u : c->queries[q].udafs) {
       std::vector<T> ts;
@@ -242,22 +271,28 @@ FastPaths* plan_poly(lmfao_ctx* c) {
       }
       outs.push_back(ts);
     }
-  if (!higher) return nullptr;
-  const int n = (int)halves.size();
+  // batches of products of at most two factors reach here only when cov.cu and gram.cu
+  // declined them (e.g. a relation without children: the fact-only Gram)
+  (void)higher;
+  const int n = (int)halves.size() - 1;  // tile columns: halves 1..n (half 0 is the constant)
+  if (n > PL_MAXT * 8) return nullptr;
   a.nattr = (int)feat.size();
-  a.nt = (n + 7) / 8;
+  a.nt = std::max(1, (n + 7) / 8);
   for (int i = 0; i < PL_MAXT * 8; i++) {
-    a.ha[i] = i < n ? (int8_t)halves[i].first : (int8_t)-1;
-    a.hb[i] = i < n ? (int8_t)halves[i].second : (int8_t)-1;
+    a.ha[i] = i < n ? (int8_t)halves[i + 1].first : (int8_t)-1;
+    a.hb[i] = i < n ? (int8_t)halves[i + 1].second : (int8_t)-1;
   }
-  // padded halves (i >= n) are 1 too: harmless, their entries are never read
-  // G entry (x, y), x <= y: tile pair (t, s) = (x / 8, y / 8), t <= s, element [x % 8][y % 8]
+  // padded columns (i >= n) are the constant: harmless, their entries are never read
+  // G entry (x, y), x <= y over the halves: (0, 0) the count; (0, y) the linear sum of column
+  // y - 1; else tile pair (t, s) = ((x-1) / 8, (y-1) / 8), element [(x-1) % 8][(y-1) % 8]
+  const int npairs = a.nt * (a.nt + 1) / 2;
   auto gidx = [&](int x, int y) {
-    const int t = x / 8, s = y / 8;
+    if (x == 0) return y == 0 ? npairs * 64 + a.nt * 8 : npairs * 64 + (y - 1);
+    const int xx = x - 1, yy = y - 1, t = xx / 8, s = yy / 8;
     int p = 0;
     for (int tt = 0; tt < a.nt; tt++)
       for (int ss = tt; ss < a.nt; ss++, p++)
-        if (tt == t && ss == s) return p * 64 + (x % 8) * 8 + (y % 8);
+        if (tt == t && ss == s) return p * 64 + (xx % 8) * 8 + (yy % 8);
     return -1;
   };
   std::vector<int32_t> toff{0}, tidx;
@@ -273,11 +308,14 @@ FastPaths* plan_poly(lmfao_ctx* c) {
   fp->count_idx = gidx(0, 0);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  fp->grid = sms * 4;
+  int per = 0;  // one wave of resident CTAs (static per-warp ranges)
+  const void* kfn = a.nt == 1 ? (const void*)k_poly<1> : a.nt == 2 ? (const void*)k_poly<2> : (const void*)k_poly<3>;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kfn, PL_WARPS * 32, 0) || per < 1) per = 1;
+  fp->grid = sms * per;
   fp->nw = fp->grid * PL_WARPS;
-  fp->npart = a.nt * (a.nt + 1) / 2 * 64;
+  fp->npart = npairs * 64 + a.nt * 8;  // + the count at src[npart]
   cudaStream_t st = c->stream;
-  if (fp->partials.alloc((size_t)fp->nw * fp->npart * 8) || fp->src.alloc((size_t)fp->npart * 8) ||
+  if (fp->partials.alloc((size_t)fp->nw * fp->npart * 8) || fp->src.alloc((size_t)(fp->npart + 1) * 8) ||
       fp->toff.alloc(toff.size() * 4) || fp->tidx.alloc(std::max<size_t>(tidx.size(), 1) * 4) ||
       fp->tcoef.alloc(std::max<size_t>(tcoef.size(), 1) * 8))
     return nullptr;

@@ -81,3 +81,17 @@ def test_degree2_polynomial_more_features_and_coefficients(feats):
                             [P(1.0, (I(f[-1]), I(f[-1]), I(f[-2]), I(f[-3])))], []]))
     gpu, info = run_gpu(db, batch, info=True)
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("n", [1, 31, 4097, 60_013])
+def test_fact_only_covariance_on_the_gram_kernel(n):
+    """A relation without children (the fact-only Gram of SURVEY §8(d)): cov.cu and gram.cu need
+    root children, so poly.cu's Gram of halves [1, x_1..x_8] takes it (45 distinct entries)."""
+    rng = np.random.default_rng(n)
+    cols = {f"x{j}": rng.standard_normal(n) for j in range(7)}
+    cols["i"] = rng.integers(-5, 6, n).astype(np.int32)  # eight features: poly.cu's limit
+    db = synth.Database([synth.Relation("F", cols)], "F", [])
+    batch = [synth.covar_batch(list(cols))]
+    gpu, info = run_gpu(db, batch, info=True)
+    assert info["fast_path"]["kind"] == "poly", info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
