@@ -199,6 +199,39 @@ __global__ void k_cov_bstats(const unsigned char* __restrict__ scan, int64_t nbl
   }
 }
 
+// Plan time, the work split on the device (no per-block data to the host): a block's cost
+// (COST_FAST, or `cold` when level-A runs start inside it); the static chunk boundaries, chunk w
+// ending at the first block whose cost prefix reaches stat·w/NW; the level-B records of each work
+// item (its blocks' B run starts, plus one if its row 0 does not start a B run).
+__global__ void k_cov_cost(const uint32_t* __restrict__ st, int64_t n, uint32_t cold, uint32_t* __restrict__ cost) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= n; b += (int64_t)gridDim.x * blockDim.x)
+    cost[b] = b < n ? ((st[b] & 128u) ? cold : (uint32_t)COST_FAST) : 0u;
+}
+__global__ void k_cov_static(const uint32_t* __restrict__ cc, int64_t n, int NW, int tail, int32_t* __restrict__ it) {
+  const uint64_t stat = (uint64_t)cc[n] * (uint64_t)(100 - tail) / 100;  // cost of the static part
+  for (int w = blockIdx.x * blockDim.x + threadIdx.x; w <= NW; w += gridDim.x * blockDim.x) {
+    const uint64_t target = stat * (uint64_t)w / (uint64_t)NW;
+    int64_t lo = 0, hi = n + 1;  // first b with cc[b] >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((uint64_t)cc[mid] < target) lo = mid + 1;
+      else hi = mid;
+    }
+    it[w] = w == 0 ? 0 : (int32_t)lo;
+  }
+}
+__global__ void k_cov_recs(const uint32_t* __restrict__ st, const int32_t* __restrict__ it, int nitems,
+                           uint32_t* __restrict__ rc) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nitems; i += gridDim.x * blockDim.x) {
+    uint32_t r = 0;
+    if (i < nitems) {
+      for (int64_t b = it[i]; b < it[i + 1]; b++) r += st[b] & 63u;
+      if (it[i + 1] > it[i] && !(st[it[i]] & 64u)) r += 1;
+    }
+    rc[i] = r;
+  }
+}
+
 template <int W>
 struct CovCfg {
   static constexpr int CF = 3;                           // fact-block ring slots per warp
@@ -1152,52 +1185,59 @@ FastPaths* plan_cov(lmfao_ctx* c) {
     if (n > 0)
       k_cov_bstats<<<(unsigned)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, c->stream>>>(
           fc->scan.as<unsigned char>(), n, fc->NS, bst.as<uint32_t>());
-    std::vector<uint32_t> h((size_t)n);
-    if (n > 0 && (cudaMemcpyAsync(h.data(), bst.p, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream) ||
-                  cudaStreamSynchronize(c->stream) || cudaGetLastError()))
-      return nullptr;
     int cold = COV_COST_COLD, tb = COV_TB, tail = COV_TAIL;
     if (const char* e = std::getenv("LMFAO_COV_COST_COLD")) cold = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("LMFAO_COV_TB")) tb = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("LMFAO_COV_TAIL")) tail = std::min(100, std::max(0, std::atoi(e)));
-    std::vector<uint64_t> cc((size_t)n + 1, 0);  // cost prefix
-    for (int64_t b = 0; b < n; b++) cc[b + 1] = cc[b] + ((h[b] & 128u) ? (uint64_t)cold : (uint64_t)COST_FAST);
-    const uint64_t stat = cc[n] * (uint64_t)(100 - tail) / 100;  // cost of the static part
-    std::vector<int32_t> it{0};
-    fc->nstatic = 0;
-    if (n >= 8 * (int64_t)NW) {  // every static chunk non-empty (>= 3 blocks)
-      for (int w = 1; w <= NW; w++) {  // chunk w-1 = [it[w-1], first b with cc[b] >= stat·w/NW)
-        const uint64_t target = stat * (uint64_t)w / (uint64_t)NW;
-        it.push_back((int32_t)(std::lower_bound(cc.begin(), cc.end(), target) - cc.begin()));
-      }
-      fc->nstatic = NW;
-    } else {  // a small root: dynamic items only, about two per warp
-      tb = (int)std::min<int64_t>(tb, n / (2 * (int64_t)NW));
-    }
+    cudaStream_t st = c->stream;
+    const bool stat_chunks = n >= 8 * (int64_t)NW;  // every static chunk non-empty (>= 3 blocks)
+    if (!stat_chunks) tb = (int)std::min<int64_t>(tb, n / (2 * (int64_t)NW));  // dynamic items only, ~two per warp
     constexpr int CFb = CovCfg<COV_W>::CF;  // k_cov needs items of at least CF blocks
     tb = std::max(tb, CFb);
-    while (it.back() < n) {
-      const int64_t e = std::min<int64_t>(it.back() + tb, n);
+    // the static chunks' boundaries on the device; the host reads back where they end
+    int32_t static_end = 0;
+    DevBuf cost, cc;
+    if (stat_chunks) {
+      if (cost.alloc((size_t)(n + 1) * 4) || cc.alloc((size_t)(n + 1) * 4) || fc->items.alloc((size_t)(NW + 1) * 4 + 4))
+        return nullptr;
+      k_cov_cost<<<(unsigned)std::min<int64_t>((n + 256) / 256, 148 * 8), 256, 0, st>>>(bst.as<uint32_t>(), n,
+                                                                                       (uint32_t)cold, cost.as<uint32_t>());
+      if (exclusive_scan_u32(cost.as<uint32_t>(), cc.as<uint32_t>(), n + 1, st)) return nullptr;
+      k_cov_static<<<(NW + 256) / 256, 256, 0, st>>>(cc.as<uint32_t>(), n, NW, tail, fc->items.as<int32_t>());
+      if (cudaMemcpyAsync(&static_end, fc->items.as<int32_t>() + NW, 4, cudaMemcpyDeviceToHost, st) ||
+          cudaStreamSynchronize(st) || cudaGetLastError())
+        return nullptr;
+      fc->nstatic = NW;
+    } else {
+      fc->nstatic = 0;
+    }
+    std::vector<int32_t> tl{static_end};  // the dynamic items after the static part
+    while (tl.back() < n) {
+      const int64_t e = std::min<int64_t>(tl.back() + tb, n);
       if (n - e < CFb) {  // the remainder is too short for an item of its own
-        it.push_back((int32_t)n);
+        tl.push_back((int32_t)n);
         break;
       }
-      it.push_back((int32_t)e);
+      tl.push_back((int32_t)e);
     }
-    fc->nitems = (int)it.size() - 1;
-    std::vector<int32_t> rb((size_t)fc->nitems + 1, 0);
-    for (int i = 0; i < fc->nitems; i++) {  // an item's records: its B run starts, its row 0 starting one
-      int32_t r = 0;
-      for (int64_t b = it[i]; b < it[i + 1]; b++) r += (int32_t)(h[b] & 63u);
-      if (it[i + 1] > it[i] && !(h[it[i]] & 64u)) r += 1;
-      rb[i + 1] = rb[i] + r;
-    }
-    if (fc->items.alloc(it.size() * 4) || fc->rbase.alloc(rb.size() * 4) ||
-        cudaMemcpyAsync(fc->items.p, it.data(), it.size() * 4, cudaMemcpyHostToDevice, c->stream) ||
-        cudaMemcpyAsync(fc->rbase.p, rb.data(), rb.size() * 4, cudaMemcpyHostToDevice, c->stream) ||
-        cudaStreamSynchronize(c->stream))
+    const int nst = fc->nstatic;
+    fc->nitems = nst + (int)tl.size() - 1;
+    DevBuf items_all, rc;
+    if (items_all.alloc((size_t)(fc->nitems + 1) * 4) || rc.alloc((size_t)(fc->nitems + 1) * 4) ||
+        fc->rbase.alloc((size_t)(fc->nitems + 1) * 4))
       return nullptr;
-    const uint32_t tot = (uint32_t)rb.back();
+    if ((nst && cudaMemcpyAsync(items_all.p, fc->items.p, (size_t)nst * 4, cudaMemcpyDeviceToDevice, st)) ||
+        cudaMemcpyAsync(items_all.as<int32_t>() + nst, tl.data(), tl.size() * 4, cudaMemcpyHostToDevice, st))
+      return nullptr;
+    fc->items = std::move(items_all);
+    k_cov_recs<<<(fc->nitems + 256) / 256, 256, 0, st>>>(bst.as<uint32_t>(), fc->items.as<int32_t>(), fc->nitems,
+                                                         rc.as<uint32_t>());
+    if (exclusive_scan_u32(rc.as<uint32_t>(), fc->rbase.as<uint32_t>(), fc->nitems + 1, st)) return nullptr;
+    uint32_t tot = 0;
+    if (cudaMemcpyAsync(&tot, fc->rbase.as<uint32_t>() + fc->nitems, 4, cudaMemcpyDeviceToHost, st) ||
+        cudaStreamSynchronize(st) || cudaGetLastError())
+      return nullptr;
+
     fc->nrec = tot;
     if (fc->partials.alloc((size_t)std::max(fc->nitems, 1) * NPART * 8)) return nullptr;  // one partial per item
     if (fc->brec.alloc((size_t)std::max<uint32_t>(tot, 1) * BRW * 8)) return nullptr;
