@@ -99,6 +99,79 @@ __device__ __forceinline__ int rt_cell_fast(double x, const double* t, int n, do
   return rt_cell_uniform(x, t, n, t0, inv_h);
 }
 
+// k_rt_fact's row loop for one histogram piece.  KIND: 0 fp64 predicate column, 1 group-by
+// codes, 2 int32 predicate column; FILT: a path condition filters the rows.
+template <int KIND, bool FILT>
+__device__ __forceinline__ void rt_fact_rows(const RtFactArgs& a, const FactHist& h, int64_t r0, int64_t r1,
+                                             const double* thr, double* eqt, unsigned* tc, double2* ty, int nc,
+                                             double& t0, double& t1, double& t2) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  constexpr int U = 16;  // rows per lane per step: all loads issued before the table updates
+  for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
+    double yv[U], xv[U];
+    int cv[U];
+    bool pv[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t row = base + 32 * u;
+      const bool v = row < r1;
+      const bool pass = v && (!FILT || a.filt[row]);
+      yv[u] = 0.0;
+      if (pass && a.y) yv[u] = a.y[row];
+      pv[u] = pass;
+      cv[u] = -1;
+      xv[u] = 0.0;
+      if (v) {
+        if (KIND == 1) cv[u] = reinterpret_cast<const int32_t*>(h.col)[row];
+        else if (KIND == 2) xv[u] = (double)reinterpret_cast<const int32_t*>(h.col)[row];
+        else xv[u] = reinterpret_cast<const double*>(h.col)[row];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u += 2) {
+      int e[2];
+      double n[2], yy[2], q[2];
+#pragma unroll
+      for (int z = 0; z < 2; z++) {
+        const bool v = base + 32 * (u + z) < r1;
+        int c = cv[u + z];
+        bool eq = false;
+        if (KIND != 1 && v) {
+          c = h.uniform ? rt_cell_fast(xv[u + z], thr, h.nthr, h.t0, h.inv_h, h.margin) : rt_cell(xv[u + z], thr, h.nthr);
+          eq = (c & 1) && pv[u + z];
+          c >>= 1;
+        }
+        n[z] = pv[u + z] ? 1.0 : 0.0;  // rows failing the path condition weigh 0
+        yy[z] = yv[u + z];
+        q[z] = yy[z] * yy[z];
+        t0 += n[z];
+        t1 += yy[z];
+        t2 += q[z];
+        if (KIND != 1 && eq) {  // x equals threshold c: rare for continuous data
+          double* et = eqt + 3 * c;
+          sred_add(et, 1.0);
+          sred_add(et + 1, yy[z]);
+          sred_add(et + 2, q[z]);
+          n[z] = yy[z] = q[z] = 0.0;
+        }
+        e[z] = (v && !eq ? c : nc) * 32 + lane;
+      }
+      if (e[0] == e[1]) {  // merge into the first; the second writes its old value back
+        n[0] += n[1];
+        yy[0] += yy[1];
+        q[0] += q[1];
+        n[1] = yy[1] = q[1] = 0.0;
+      }
+      const unsigned c0 = tc[e[0]], c1 = tc[e[1]];
+      const double2 w0 = ty[e[0]], w1 = ty[e[1]];
+      tc[e[1]] = c1 + (unsigned)n[1];
+      ty[e[1]] = make_double2(w1.x + yy[1], w1.y + q[1]);
+      tc[e[0]] = c0 + (unsigned)n[0];
+      ty[e[0]] = make_double2(w0.x + yy[0], w0.y + q[0]);
+    }
+  }
+}
+
 // Root rows, all histograms: the (histogram, row) space is cut into equal contiguous pieces,
 // one per CTA (so every CTA has the same work and at most a few histogram switches, each a
 // flush of its tables).  Small histograms (<= RT_SMALL cells) use per-lane private tables in
@@ -141,68 +214,16 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
     }
     __syncthreads();
     double t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    constexpr int U = 16;  // rows per lane per step: all loads issued before the table updates
-    for (int64_t base = r0 + wib * 32 * U + lane; base < r1; base += (int64_t)nw * 32 * U) {
-      double yv[U], xv[U];
-      int cv[U];
-      bool pv[U];
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t row = base + 32 * u;
-        const bool v = row < r1;
-        const bool pass = v && (!a.filt || a.filt[row]);
-        yv[u] = (pass && a.y) ? a.y[row] : 0.0;
-        pv[u] = pass;
-        cv[u] = -1;
-        xv[u] = 0.0;
-        if (v) {
-          if (h.is_code) cv[u] = reinterpret_cast<const int32_t*>(h.col)[row];
-          else xv[u] = h.is_int ? (double)reinterpret_cast<const int32_t*>(h.col)[row]
-                                : reinterpret_cast<const double*>(h.col)[row];
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; u += 2) {
-        int e[2];
-        double n[2], yy[2], q[2];
-#pragma unroll
-        for (int z = 0; z < 2; z++) {
-          const bool v = base + 32 * (u + z) < r1;
-          int c = cv[u + z];
-          bool eq = false;
-          if (v && !h.is_code) {
-            c = h.uniform ? rt_cell_fast(xv[u + z], thr, h.nthr, h.t0, h.inv_h, h.margin) : rt_cell(xv[u + z], thr, h.nthr);
-            eq = (c & 1) && pv[u + z];
-            c >>= 1;
-          }
-          n[z] = pv[u + z] ? 1.0 : 0.0;  // rows failing the path condition weigh 0
-          yy[z] = yv[u + z];
-          q[z] = yy[z] * yy[z];
-          t0 += n[z];
-          t1 += yy[z];
-          t2 += q[z];
-          if (eq) {  // x equals threshold c: rare for continuous data
-            double* et = eqt + 3 * c;
-            sred_add(et, 1.0);
-            sred_add(et + 1, yy[z]);
-            sred_add(et + 2, q[z]);
-            n[z] = yy[z] = q[z] = 0.0;
-          }
-          e[z] = (v && !eq ? c : nc) * 32 + lane;
-        }
-        if (e[0] == e[1]) {  // merge into the first; the second writes its old value back
-          n[0] += n[1];
-          yy[0] += yy[1];
-          q[0] += q[1];
-          n[1] = yy[1] = q[1] = 0.0;
-        }
-        const unsigned c0 = tc[e[0]], c1 = tc[e[1]];
-        const double2 w0 = ty[e[0]], w1 = ty[e[1]];
-        tc[e[1]] = c1 + (unsigned)n[1];
-        ty[e[1]] = make_double2(w1.x + yy[1], w1.y + q[1]);
-        tc[e[0]] = c0 + (unsigned)n[0];
-        ty[e[0]] = make_double2(w0.x + yy[0], w0.y + q[0]);
-      }
+    // the row loop, specialised by the column kind and the path condition (no per-row checks)
+    if (h.is_code) {
+      if (a.filt) rt_fact_rows<1, true>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
+      else rt_fact_rows<1, false>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
+    } else if (h.is_int) {
+      if (a.filt) rt_fact_rows<2, true>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
+      else rt_fact_rows<2, false>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
+    } else {
+      if (a.filt) rt_fact_rows<0, true>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
+      else rt_fact_rows<0, false>(a, h, r0, r1, thr, eqt, tc, ty, nc, t0, t1, t2);
     }
     if (hi == 0) {
 #pragma unroll
