@@ -212,3 +212,19 @@ def test_cube_many_measures():
     fp = info["fast_path"]["groups"]
     assert fp["kind"] == "cube" and fp["scans"] == 2 and fp["measures"] == 14, fp
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("n", [257, 3001, 40_009])  # enough rows for {a1,g,a2}'s ~420 present cells
+def test_cube_records_at_the_root_level(n, monkeypatch):
+    """k_cube_rec when the sparse cuboid groups by a root attribute (its runs at level R: equal
+    keys and equal root codes) and the measures are not all fp64 root columns (the general
+    load path), every other cuboid a rollup of it."""
+    db = cube_db(13, n)
+    sums = [S((1, "m1")), S((1, "i1")), S((2, "m2"), (1, None)), S((1, "x2"))]  # x2: a dimension measure
+    batch = [Query(["a1", "g", "a2"], sums), Query(["g"], sums), Query(["a1", "g"], sums),
+             Query(["a2"], sums), Query([], sums)]
+    monkeypatch.setenv("LMFAO_CUBE_SPARSE_CELLS", "100")
+    gpu, info = run_gpu(db, batch, info=True, runs=2)
+    g = info["fast_path"]["groups"] if "groups" in info["fast_path"] else info["fast_path"]
+    assert g["kind"] == "cube" and g["sparse"] == 1 and g["scan"] == "records", info["fast_path"]
+    assert_parity(gpu, oracle.evaluate(db, batch), batch)
