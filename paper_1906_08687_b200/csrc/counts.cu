@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(1024) k_cnt_rows(const __grid_constant__ CntAr
       const int ca = scode[32 * (d.x & 255)], cb = scode[32 * d.y];
       const int cell = v ? ca * d.z + cb : -1 - lane;
       const unsigned peers = __match_any_sync(CFULL, cell);
-      if (v && (__ffs(peers) - 1) == lane) atomicAdd(&sp[qi][cell], (unsigned long long)__popc(peers));  // ATOM: throttles hot cells
+      if (v && (__ffs(peers) - 1) == lane) gred_add(&sp[qi][cell], (unsigned long long)__popc(peers));
     }
     for (int qi = a.ngq_row; qi < a.nq; qi++) {  // per run segment
       const int4 d = sq[qi];
