@@ -58,6 +58,9 @@ constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends af
 #ifndef COV_W
 #define COV_W 12  // warps per CTA of the scan (one CTA per SM)
 #endif
+#ifndef COV_XT_DFMA  // 1 (with COV_XX_DMMA): x⊗[s_L8, s_L9] as 2 DFMA per group instead of the third DMMA
+#define COV_XT_DFMA 0   // (the tile's column "1" is not needed: Σx comes from the level-B records)
+#endif
 #ifndef COV_XX_DMMA  // 1: x⊗x and x⊗[s_L8, s_L9, 1] as two more DMMA per 4-row group; 0: 7 DFMA (x_m·x_{m+d})
 #define COV_XX_DMMA 1   // (C2 scan: DFMA 0.334, DMMA 0.296 ms with the same static split: issue-bound)
 #endif
@@ -367,7 +370,7 @@ struct CovWarp {
       __syncwarp();
       out[m * 8 + 2 * k] = aXX[0];
       out[m * 8 + 2 * k + 1] = aXX[1];
-      if (k == 0) {
+      if (k == 0 && !COV_XT_DFMA) {
         out[64 + m * 10 + 8] = aXT[0];
         out[64 + m * 10 + 9] = aXT[1];
       }
@@ -422,8 +425,14 @@ struct CovWarp {
       if (COV_XX_DMMA) {
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        dmma(aXT, xa, tv);
-        s89 = make_double2(0.0, 0.0);
+        if (COV_XT_DFMA) {
+          s89 = ld2(gr + 8);
+          x8 = fma(xa, s89.x, x8);
+          x9 = fma(xa, s89.y, x9);
+        } else {
+          dmma(aXT, xa, tv);
+          s89 = make_double2(0.0, 0.0);
+        }
         return;
       }
       s89 = ld2(gr + 8);
@@ -456,7 +465,7 @@ struct CovWarp {
         sa89.y *= mk;
         sam *= mk;
       }
-      if (COV_XX_DMMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
+      if (COV_XX_DMMA && !COV_XT_DFMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
       dmma(aRA0, xa, sam);
       dmma(aRA1, sv, sam);
       tA8 = fma(s89.x, sam, tA8);

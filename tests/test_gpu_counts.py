@@ -13,13 +13,15 @@ from synth import Product, Query
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("runs", ["0", "1"])
+@pytest.mark.parametrize("runs,pack", [(None, "1"), ("0", "1"), ("1", "1"), (None, "0")])
 @pytest.mark.parametrize("n", [1, 31, 33, 5000, 40_011])
-def test_counts_config4_shape(n, runs, monkeypatch):
-    """runs=1: cross-dimension pair tables counted once per run segment (LMFAO_CNT_RUNS; the
-    slower alternative, kept exact)."""
-    monkeypatch.setenv("LMFAO_CNT_RUNS", runs)
-    monkeypatch.setenv("LMFAO_CNT_RUN_GLOBAL", runs)
+def test_counts_config4_shape(n, runs, pack, monkeypatch):
+    """runs: cross-dimension tables counted once per run segment at the first two sort positions
+    (default), never ("0"), or at every position ("1"; LMFAO_CNT_RUNS); pack=0: dimension codes
+    gathered one attribute at a time (LMFAO_CNT_PACK)."""
+    if runs is not None:
+        monkeypatch.setenv("LMFAO_CNT_RUNS", runs)
+    monkeypatch.setenv("LMFAO_CNT_PACK", pack)
     w = synth.config4(fact_rows=n, dim_rows=(40, 300, 2000))
     gpu, info = run_gpu(w.db, w.batch, info=True)
     assert info["fast_path"] and info["fast_path"]["kind"] == "counts", info
@@ -92,3 +94,28 @@ def test_counts_wide_batch_smem_budgets(monkeypatch, cells):
     gpu, info = run_gpu(db, batch, info=True)
     assert info["fast_path"]["kind"] == "counts", info
     assert_parity(gpu, oracle.evaluate(db, batch), batch)
+
+
+@pytest.mark.parametrize("views,cap,every", [("0", None, False), ("1", None, False), ("1", "2000", False),
+                                             ("1", None, True)])
+def test_counts_views(monkeypatch, views, cap, every):
+    """Pair queries finished from shared views V_D[k][b] (LMFAO_CNT_VIEWS):
+    none, the default choice, only the small views (LMFAO_CNT_VIEW_CELLS: the rest per row), and
+    every candidate (any table size, views keyed by any level)."""
+    monkeypatch.setenv("LMFAO_CNT_VIEWS", views)
+    if cap is not None:
+        monkeypatch.setenv("LMFAO_CNT_VIEW_CELLS", cap)
+        monkeypatch.setenv("LMFAO_CNT_VIEW_MIN", "0")
+    if every:
+        monkeypatch.setenv("LMFAO_CNT_VIEW_MIN", "0")
+        monkeypatch.setenv("LMFAO_CNT_VIEW_POS", "8")
+    w = synth.config4(fact_rows=50_003, dim_rows=(40, 300, 2000))
+    gpu, info = run_gpu(w.db, w.batch, info=True)
+    fp = info["fast_path"]
+    assert fp["kind"] == "counts", info
+    if views == "0":
+        assert fp["views"] == 0
+    else:
+        assert fp["views"] > 0 and fp["view_queries"] >= 2 * fp["views"], fp
+        assert fp["row_queries"] == 60 - fp["view_queries"] + fp["views"], fp
+    assert_parity(gpu, oracle.evaluate(w.db, w.batch), w.batch)
