@@ -62,7 +62,12 @@ struct RtFactArgs {
   double* out;        // global accumulators (TOT at 0)
   int eq_off, tab_off;  // shared memory (doubles): thresholds | equality cells | lane tables
   int wgt[RT_MAX_FACT];   // relative cost per row of each histogram (work split)
+  int npieces;            // equal-cost pieces of the (histogram, row) space, taken dynamically
+  int* work;              // piece counter (zeroed per pass)
 };
+#ifndef RT_PIECES_PER_CTA
+#define RT_PIECES_PER_CTA 2  // (C3: one static piece per CTA left SM active cycles 32 % apart; 2: 1.053, 4: 1.060, 8: 1.121 ms)
+#endif
 
 __device__ __forceinline__ int rt_cell(double x, const double* t, int n) {
   int lo = 0, hi = n;  // lower bound: first t >= x
@@ -184,12 +189,21 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double* thr = rsm;
   double* eqt = rsm + a.eq_off;  // [nthr][3] rows equal to a threshold (rare: shared atomics)
-  // this CTA's equal-cost piece of the (histogram, row) space, histogram h weighing wgt[h]
+  // equal-cost pieces of the (histogram, row) space, histogram h weighing wgt[h], taken
+  // dynamically (the weights are estimates)
   const int64_t N = a.nrows;
   int64_t T = 0;
   for (int i = 0; i < a.nh; i++) T += (int64_t)a.wgt[i] * N;
-  const int64_t W0 = T / gridDim.x * blockIdx.x + (T % gridDim.x) * blockIdx.x / gridDim.x;
-  const int64_t W1 = T / gridDim.x * (blockIdx.x + 1) + (T % gridDim.x) * (blockIdx.x + 1) / gridDim.x;
+  __shared__ int piece_sh;
+  const int64_t P = a.npieces;
+  for (;;) {
+  if (threadIdx.x == 0) piece_sh = atomicAdd(a.work, 1);
+  __syncthreads();
+  const int64_t pc = piece_sh;
+  __syncthreads();
+  if (pc >= P) break;
+  const int64_t W0 = T / P * pc + (T % P) * pc / P;
+  const int64_t W1 = T / P * (pc + 1) + (T % P) * (pc + 1) / P;
   int64_t hb = 0;  // weighted start of histogram hi
   for (int hi = 0; hi < a.nh; hb += (int64_t)a.wgt[hi] * N, hi++) {
     const int64_t he = hb + (int64_t)a.wgt[hi] * N;
@@ -261,6 +275,7 @@ __global__ void __launch_bounds__(RT_FACT_WARPS * 32) k_rt_fact(const __grid_con
       if (sum != 0.0) gred_add(a.out + h.goff + 3 * oc + v, sum);
     }
   }
+  }
 }
 
 // Root histograms with more than RT_SMALL cells (group-bys on large root domains): one
@@ -286,11 +301,27 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
     }
     __syncthreads();
   }
-  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < a.nrows;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    if (a.filt && !a.filt[row]) continue;
-    const double y = a.y ? a.y[row] : 0.0;
-    const int c = a.code[row];
+  // RT_BIG_U rows per thread per step, their loads issued together (one CTA of 16 warps per SM:
+  // one row at a time left the warps waiting on their loads, 62 % long-scoreboard stalls)
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r0 < a.nrows; r0 += U * stride) {
+    double yv[U];
+    int cv[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t row = r0 + u * stride;
+      ok[u] = row < a.nrows;
+      cv[u] = ok[u] ? a.code[row] : 0;
+      yv[u] = (ok[u] && a.y) ? a.y[row] : 0.0;
+      if (ok[u] && a.filt) ok[u] = a.filt[row] != 0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+    if (!ok[u]) continue;
+    const double y = yv[u];
+    const int c = cv[u];
     if (a.in_smem) {
       atomicAdd(&cnt[c], 1u);
       if (a.y) {
@@ -303,6 +334,7 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
         gred_add(a.out + 3 * (int64_t)c + 1, y);
         gred_add(a.out + 3 * (int64_t)c + 2, y * y);
       }
+    }
     }
   }
   if (!a.in_smem) return;
@@ -842,6 +874,9 @@ cudaError_t FastRT::pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const
   fa.eq_off = eq_off;
   fa.tab_off = tab_off;
   fa.out = accp;
+  fa.npieces = nparts * RT_PIECES_PER_CTA;
+  fa.work = vwork.as<int>() + 1;
+  CUDA_TRY(cudaMemsetAsync(vwork.p, 0, 16, st));
   if (timed) scan_timer_begin(c, st);
   if (R.nrows > 0 && fa.nh > 0) {
     k_rt_fact<<<nparts, RT_FACT_WARPS * 32, fact_smem, st>>>(fa);

@@ -1,0 +1,10 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2_b.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_rt.py tests/test_gpu_rt_path.py -q -x > gpurun_out/r2s3_t8.log 2>&1; echo rc=$? >> gpurun_out/r2s3_t8.log
+o=gpurun_out/r2s3_c3a.log
+B=paper_1906_08687_b200/build
+for r in 1 2; do
+echo p4 >> $o; timeout 600 python tools/time_configs.py C3 >> $o 2>&1
+echo p8 >> $o; LMFAO_LIB=$B/var_rtp8/lib.so timeout 600 python tools/time_configs.py C3 >> $o 2>&1
+echo p2 >> $o; LMFAO_LIB=$B/var_rtp2/lib.so timeout 600 python tools/time_configs.py C3 >> $o 2>&1
+done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2s3_launch_C3b.csv python tools/run_config.py C3 2 > /dev/null 2>&1

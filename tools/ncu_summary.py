@@ -33,5 +33,12 @@ st = [(k, f(k)) for k in h if "pcsamp_warps_issue_stalled" in k and not k.endswi
 tot = sum(x for _, x in st if x)
 for k, x in sorted(st, key=lambda z: -(z[1] or 0))[:8]:
     print(f"  stall {100 * x / tot:5.1f}%  {k.replace('smsp__pcsamp_warps_issue_stalled_', '')}")
+atom = [k for k in h if k.endswith(".sum") and not k.startswith("sys") and "aperture" not in k and "lookup" not in k
+        and any(t in k for t in ("op_atom", "op_red", "shared_atom", "global_red", "global_atom"))]
+if atom:
+    print("-- atomics / reductions")
+    for k in sorted(atom):
+        if f(k):
+            print(f"{k:80s} {f(k):.0f}")
 if "--json" in sys.argv:
     json.dump({k: val for k, (val, unit) in res.items()}, open(sys.argv[sys.argv.index("--json") + 1], "w"), indent=1)
