@@ -4,17 +4,18 @@
 // aggregate is an entry of G = Σ_f u(f) u(f)^T with u = [1, x, s_L, s_A, s_B]),
 // evaluated over the root sorted by its foreign keys in increasing domain size
 // with the multi-output trie registration of P:1020-1214:
-//   per row          x⊗x, x⊗s_L                 (DMMA m8n8k4 for x⊗s_L0..7, DFMA for the rest)
+//   per row          x⊗x, x⊗s_L                 (DMMA m8n8k4 for x⊗x and x⊗s_L0..7, DFMA for s_L8/9)
 //   per level-A run  R_A⊗s_A, R_A = Σ_run [x, s_L, 1]   ("intermediate aggregates": run sums
 //                    carried per lane, one DMMA per tile per run) — or, in blocks where many
 //                    short runs end (the Zipf tail), the same sum row by row (linearity)
 //   per level-B run  R_B⊗s_B, R_B = Σ_{A-runs} [R_A, n·s_A]  (record list, finished off-scan)
 //   dimension side   Σ_k H_r[k] s_r(k) s_r(k)^T  ("each aggregate to its own root")
 // Design on B200 (measurements in DESIGN.md §2):
-//  * the FP64 pipe (DMMA and DFMA share it: 18.5 T FMA/s) is the scarce unit, so products
-//    go to DMMA only where a tile is fully used (x⊗s_L0..7: 64 of 64 products); the
-//    symmetric x⊗x (36 of 64) and the thin x⊗[s_L8, s_L9] are DFMA, lane (m, k) forming
-//    x_m·x_{m+d} (d = 0..4) for its row — 30 % fewer FP64 pipe cycles per row;
+//  * the FP64 pipe (DMMA and DFMA share it: 18.5 T FMA/s) is the scarce unit next to issue:
+//    x⊗x and x⊗s_L0..7 are one DMMA m8n8k4 each per 4 rows (the k = 4 sums the rows), the
+//    thin x⊗[s_L8, s_L9] two DFMA per lane and group (a third DMMA would use 2 of its 8
+//    columns; COV_XT_DFMA); x⊗x as DFMA (lane (m, k) forming x_m·x_{m+d}, COV_XX_DMMA=0)
+//    saves FP64 pipe cycles but measured slower (issue);
 //  * run boundaries are structural (like the trie): the scan layout built at plan
 //    time carries a run-start flag in bit 31 of every dense key, so a block's boundary masks
 //    are one ballot per level;
@@ -59,7 +60,7 @@ constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends af
 #define COV_W 12  // warps per CTA of the scan (one CTA per SM)
 #endif
 #ifndef COV_XT_DFMA  // 1 (with COV_XX_DMMA): x⊗[s_L8, s_L9] as 2 DFMA per group instead of the third DMMA
-#define COV_XT_DFMA 0   // (the tile's column "1" is not needed: Σx comes from the level-B records)
+#define COV_XT_DFMA 1   // (the tile's column "1" is not needed: Σx comes from the level-B records; C2 scan 0.3035 vs 0.3064 ms)
 #endif
 #ifndef COV_XX_DMMA  // 1: x⊗x and x⊗[s_L8, s_L9, 1] as two more DMMA per 4-row group; 0: 7 DFMA (x_m·x_{m+d})
 #define COV_XX_DMMA 1   // (C2 scan: DFMA 0.334, DMMA 0.296 ms with the same static split: issue-bound)
