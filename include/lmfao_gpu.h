@@ -138,10 +138,12 @@ LMFAO_API const char* lmfao_last_error(const lmfao_ctx* ctx);
  *   LMFAO_COLS_HOST   (0) host memory, copied before the call returns;
  *   LMFAO_COLS_DEVICE (1) device memory on this ctx's device, copied before return;
  *   LMFAO_COLS_HOST_DEFERRED (2) host memory (pinned for full speed) that the caller
- *       keeps valid and unchanged until lmfao_prepare returns: prepare streams the
- *       columns in on a copy stream in the order it consumes them (dimension
- *       relations, then the root's foreign keys, then its other columns), so the
- *       host->device transfer overlaps the remap, the sort and the root permutation.
+ *       keeps valid and unchanged until lmfao_plan returns (or lmfao_prepare fails, or
+ *       lmfao_destroy returns): prepare streams the columns in on a copy stream in the
+ *       order it consumes them (dimension relations, then the root's foreign keys, then
+ *       its other columns), so the host->device transfer overlaps the remap, the sort
+ *       and the root permutation; prepare may return while the last columns are still in
+ *       flight (plan's host work then overlaps them) and plan waits for them.
  * Attributes with the same name in different relations are the natural-join
  * attributes (X = ∪ω).  *rel_id receives the relation id. */
 #define LMFAO_COLS_HOST 0
@@ -173,7 +175,9 @@ LMFAO_API lmfao_status lmfao_set_root_shard(lmfao_ctx* ctx, int32_t part, int32_
  * among the child's distinct key values; dangling foreign keys drop the row,
  * inner-join semantics), sort of each child by its key, and one composite LSD
  * radix sort of the root by its foreign keys in increasing domain-size order
- * (the MOO attribute order). Then sharding (see above). */
+ * (the MOO attribute order). Then sharding (see above).  With deferred
+ * host columns the work is stream-ordered behind their copies and may still be in
+ * flight on return; lmfao_plan waits for the copies (host buffers released there). */
 LMFAO_API lmfao_status lmfao_prepare(lmfao_ctx* ctx);
 
 /* Adds Q(F; α_1..α_n) += R_1..R_m.  Multi-root ("each aggregate to its

@@ -430,8 +430,22 @@ lmfao_status lmfao_set_root_shard(lmfao_ctx* c, int32_t part, int32_t nparts) {
   return LMFAO_OK;
 }
 
+// Deferred host columns (LMFAO_COLS_HOST_DEFERRED) stay the caller's until this returns: the
+// copies prepare issued may still be in flight when prepare returns (the root's non-key
+// columns arrive last), so plan's host work overlaps the transfer; plan (whatever its
+// outcome), a failed prepare, secondary-root creation and destroy wait for them here.
+void copies_wait(lmfao_ctx* c) {
+  if (c->copy_stream && c->copies_pending) cudaStreamSynchronize(c->copy_stream);
+  c->copies_pending = false;
+}
+lmfao_status prepare_impl(lmfao_ctx* c);
 lmfao_status lmfao_prepare(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
+  const lmfao_status s = prepare_impl(c);
+  if (s != LMFAO_OK) copies_wait(c);
+  return s;
+}
+lmfao_status prepare_impl(lmfao_ctx* c) {
   if (c->state != S_TREE) return fail(c, LMFAO_ERR_STATE, "prepare needs a join tree (and runs once)");
   cudaSetDevice(c->device);
   StreamScope scope_(c->stream);
@@ -590,7 +604,7 @@ lmfao_status lmfao_prepare(lmfao_ctx* c) {
   }
   for (auto& r : c->rels)  // columns no permutation consumed
     for (auto& col : r.cols) CTX_CUDA(c, column_ready(col, st), "prepare copy");
-  if (c->copy_stream) CTX_CUDA(c, cudaStreamSynchronize(c->copy_stream), "prepare copy");  // host buffers released
+  if (c->copy_stream) c->copies_pending = true;  // host buffers released by plan (copies_wait)
   c->root_rows_global = R.nrows;
   if (c->shard_nparts > 1) {
     for (size_t i = 0; i < R.cols.size(); i++) {
@@ -653,6 +667,8 @@ lmfao_status gb_placement(lmfao_ctx* c, const std::vector<int>& gb) {
 int secondary_for(lmfao_ctx* c, int root) {
   for (size_t i = 0; i < c->secs.size(); i++)
     if (c->secs[i].root == root) return (int)i;
+  copies_wait(c);  // the columns are copied from this context's device buffers
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return -1;
   lmfao_ctx* s = nullptr;
   if (lmfao_create(c->device, 0, 1, nullptr, &s) != LMFAO_OK) return -1;
   s->is_secondary = true;
@@ -1631,7 +1647,9 @@ lmfao_status relay(lmfao_ctx* c, lmfao_ctx* t, lmfao_status s) {  // a secondary
 
 extern "C" lmfao_status lmfao_plan(lmfao_ctx* c) {
   if (!c) return LMFAO_ERR_INVALID_ARG;
-  if (lmfao_status s = plan_local(c)) return s;
+  const lmfao_status s0 = plan_local(c);
+  copies_wait(c);
+  if (s0) return s0;
   for (auto& sc : c->secs)
     if (lmfao_status s = lmfao_plan(sc.ctx)) return relay(c, sc.ctx, s);
   return LMFAO_OK;

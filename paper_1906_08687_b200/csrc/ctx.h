@@ -166,6 +166,7 @@ struct lmfao_ctx {
   int shard_part = 0, shard_nparts = 1;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // deferred host->device column copies (prepare)
+  bool copies_pending = false;          // ... possibly in flight until plan (copies_wait)
   std::unique_ptr<Comm> comm;  // world > 1: NCCL, or an in-process loopback group (tests)
   int64_t root_rows_global = 0;  // the root's rows before sharding
   std::string err;

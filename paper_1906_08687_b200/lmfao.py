@@ -185,7 +185,7 @@ class Engine:
         self.h = h
         self.rel_ids = {}
         self.query_ids = []
-        self._deferred = []  # host buffers of LMFAO_COLS_HOST_DEFERRED relations, until prepare
+        self._deferred = []  # host buffers of LMFAO_COLS_HOST_DEFERRED relations, until plan
 
     def _check(self, s):
         if s:
@@ -263,7 +263,6 @@ class Engine:
 
     def prepare(self):
         self._check(_lib.lmfao_prepare(self.h))
-        self._deferred = []  # prepare has consumed the deferred host columns (else close() drops them)
 
     def add_query(self, groupby, udafs) -> int:
         gb = (ctypes.c_int32 * max(1, len(groupby)))(*[self.attr_id(g) for g in groupby])
@@ -275,7 +274,10 @@ class Engine:
         return q.value
 
     def plan(self):
-        self._check(_lib.lmfao_plan(self.h))
+        try:
+            self._check(_lib.lmfao_plan(self.h))
+        finally:
+            self._deferred = []  # plan has waited for the deferred host columns (else close() drops them)
 
     def reset_batch(self):
         """Drop the batch and plan, keep the prepared relations (lmfao_reset_batch)."""
