@@ -51,8 +51,14 @@ constexpr int STG_G = 32 * GP * 8;             // 3072 B of gathered view rows p
 constexpr int NPART = 384;   // per-warp partial: XX[8][8] | XL[8][10] | RA[24][10]
 constexpr int BRW = 36;      // doubles per B record
 constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | MB[16][16]
-constexpr int FIN_BLOCKS = 296;
-constexpr int SUM_SPLIT = 8;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
+#ifndef COV_FIN_BLOCKS
+#define COV_FIN_BLOCKS 296
+#endif
+#ifndef COV_SUM_SPLIT
+#define COV_SUM_SPLIT 8
+#endif
+constexpr int FIN_BLOCKS = COV_FIN_BLOCKS;
+constexpr int SUM_SPLIT = COV_SUM_SPLIT;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int KEYMASK = 0x3fffffff;  // dense key; bit 31 = a run starts at this row (at this level),
 constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends after this row

@@ -633,6 +633,7 @@ struct RecReduce {
   double rinv[CB_GB];  // 1 / radix of Y's attributes (decode by reciprocal, corrected)
   size_t smem;         // dynamic shared memory: the coefficients and the rollups (0: read from global)
   XArgs x;
+  int ablate;          // diagnostics only (LMFAO_CUBE_ABLATE=1, results invalid): no non-prefix rollup REDs
 };
 // A dense cuboid X at the sparse cuboid Y's level whose attributes are a subset of Y's: its
 // cells are sums of Y's groups (X = Σ over Y's other attributes), added per reduced group of Y
@@ -981,7 +982,7 @@ __global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecR
           v = seg_scan(v, lane, s0);
           if (tail && v != 0.0) gred_add(&X.table[xc * X.nudaf + u], v);
         }
-      } else if (act) {
+      } else if (act && !r.ablate) {
         gred_add(&X.counts[xc], (unsigned long long)S[0]);
         for (int u = 0; u < X.nudaf; u++) {
           if (X.cmask >> u & 1ull) continue;
@@ -1133,6 +1134,10 @@ struct FastCube : FastPaths {
     r.der = sp.dder.as<Rollup>();
     r.send = dist;
     r.x = sp.x;
+    r.ablate = [] {
+      const char* e = std::getenv("LMFAO_CUBE_ABLATE");
+      return e && e[0] == '1' ? 1 : 0;
+    }();
     if (gather_first) {  // LMFAO_CUBE_GATHER=1: the records' sums permuted first (round-2 A/B)
       k_rec_gather<<<cgrid(cap * r.M1), 256, 0, st>>>(r, sp.sval.as<double>());
       r.rval = sp.sval.as<double>();

@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
     for (int l = 0; l < NLEV; l++) keys[l] = nkey[l];
     load(b + 1);
     const double w0 = rp ? 1.0 : 0.0, w1 = y, w2 = y * y;
+    const unsigned pm = __ballot_sync(RFULL, rp);  // rows counted (w0 = 1): counts by popc, not scanned
 #pragma unroll
     for (int l = 0; l < NLEV; l++) {
       const int key = keys[l];
@@ -488,12 +489,11 @@ __global__ void __launch_bounds__(256) k_rt_views(const __grid_constant__ RtView
       // segmented inclusive scan; segment s0 = the run containing the lane
       const unsigned upto = heads & ((2u << lane) - 1u);
       const int s0 = upto ? 31 - __clz(upto) : 0;
+      v0 = (double)__popc(pm & ((2u << lane) - 1u) & ~((1u << s0) - 1u));
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
-        const double o0 = __shfl_up_sync(RFULL, v0, d), o1 = __shfl_up_sync(RFULL, v1, d),
-                     o2 = __shfl_up_sync(RFULL, v2, d);
+        const double o1 = __shfl_up_sync(RFULL, v1, d), o2 = __shfl_up_sync(RFULL, v2, d);
         if (lane - d >= s0) {
-          v0 += o0;
           v1 += o1;
           v2 += o2;
         }
