@@ -4,7 +4,7 @@
 // aggregate is an entry of G = Σ_f u(f) u(f)^T with u = [1, x, s_L, s_A, s_B]),
 // evaluated over the root sorted by its foreign keys in increasing domain size
 // with the multi-output trie registration of P:1020-1214:
-//   per row          x⊗x, x⊗s_L                 (DMMA m8n8k4 for x⊗x and x⊗s_L0..7, DFMA for s_L8/9)
+//   per row          x⊗x, x⊗s_L                 (DMMA m8n8k4; x⊗s_L8/9 by DFMA in cold blocks)
 //   per level-A run  R_A⊗s_A, R_A = Σ_run [x, s_L, 1]   ("intermediate aggregates": run sums
 //                    carried per lane, one DMMA per tile per run) — or, in blocks where many
 //                    short runs end (the Zipf tail), the same sum row by row (linearity)
@@ -13,9 +13,9 @@
 // Design on B200 (measurements in DESIGN.md §2):
 //  * the FP64 pipe (DMMA and DFMA share it: 18.5 T FMA/s) is the scarce unit next to issue:
 //    x⊗x and x⊗s_L0..7 are one DMMA m8n8k4 each per 4 rows (the k = 4 sums the rows), the
-//    thin x⊗[s_L8, s_L9] two DFMA per lane and group (a third DMMA would use 2 of its 8
-//    columns; COV_XT_DFMA); x⊗x as DFMA (lane (m, k) forming x_m·x_{m+d}, COV_XX_DMMA=0)
-//    saves FP64 pipe cycles but measured slower (issue);
+//    thin x⊗[s_L8, s_L9] a third DMMA in fast blocks and two DFMA per lane and group in cold
+//    blocks, where s_L8/9 are loaded anyway (COV_XT_DFMA); x⊗x as DFMA (lane (m, k) forming
+//    x_m·x_{m+d}, COV_XX_DMMA=0) saves FP64 pipe cycles but measured slower (issue);
 //  * run boundaries are structural (like the trie): the scan layout built at plan
 //    time carries a run-start flag in bit 31 of every dense key, so a block's boundary masks
 //    are one ballot per level;
@@ -65,9 +65,9 @@ constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends af
 #ifndef COV_W
 #define COV_W 12  // warps per CTA of the scan (one CTA per SM)
 #endif
-#ifndef COV_XT_DFMA  // 1 (with COV_XX_DMMA): x⊗[s_L8, s_L9] as 2 DFMA per group instead of the third DMMA
-#define COV_XT_DFMA 1   // (the tile's column "1" is not needed: Σx comes from the level-B records; C2 scan 0.3035 vs 0.3064 ms)
-#endif
+#ifndef COV_XT_DFMA  // x⊗[s_L8, s_L9] (with COV_XX_DMMA): 0 a third DMMA per group (B = [s_L8, s_L9, 1, 0..]),
+#define COV_XT_DFMA 2   // 1 two DFMA per lane and group, 2 DFMA in cold blocks (which load s_L8/9 anyway) and
+#endif                  // the DMMA elsewhere (C2 scan: 0 0.3072, 1 0.3044, 2 0.3032 ms)
 #ifndef COV_XX_DMMA  // 1: x⊗x and x⊗[s_L8, s_L9, 1] as two more DMMA per 4-row group; 0: 7 DFMA (x_m·x_{m+d})
 #define COV_XX_DMMA 1   // (C2 scan: DFMA 0.334, DMMA 0.296 ms with the same static split: issue-bound)
 #endif
@@ -377,9 +377,13 @@ struct CovWarp {
       __syncwarp();
       out[m * 8 + 2 * k] = aXX[0];
       out[m * 8 + 2 * k + 1] = aXX[1];
-      if (k == 0 && !COV_XT_DFMA) {
+      if (k == 0 && COV_XT_DFMA == 0) {
         out[64 + m * 10 + 8] = aXT[0];
         out[64 + m * 10 + 9] = aXT[1];
+      }
+      if (k == 0 && COV_XT_DFMA == 2) {  // the DMMA part (fast and slow blocks) + the DFMA part (cold)
+        out[64 + m * 10 + 8] = aXT[0] + q8;
+        out[64 + m * 10 + 9] = aXT[1] + q9;
       }
     }
     // t rows 0, 1 (s_L8, s_L9) of RA: the carried DMMA part plus the per-row DFMA part (on lane m
@@ -424,7 +428,7 @@ struct CovWarp {
     }
     const double* gl = gs + k * GP;
     // per-row products of group j; returns the lane's operands for the run-level work
-    auto rowpart = [&](int j, double& xa, double& sv, double2& s89, double& tv) {
+    auto rowpart = [&](int j, double& xa, double& sv, double2& s89, double& tv, bool cold) {
       xa = xs[32 * j + lane];
       const double* gr = gl + j * 4 * GP;
       sv = gr[m];
@@ -432,7 +436,7 @@ struct CovWarp {
       if (COV_XX_DMMA) {
         dmma(aXX, xa, xa);
         dmma(aXL, xa, sv);
-        if (COV_XT_DFMA) {
+        if (COV_XT_DFMA == 1 || (COV_XT_DFMA == 2 && cold)) {  // (2: DFMA where the cold path loads s89 anyway)
           s89 = ld2(gr + 8);
           x8 = fma(xa, s89.x, x8);
           x9 = fma(xa, s89.y, x9);
@@ -472,7 +476,7 @@ struct CovWarp {
         sa89.y *= mk;
         sam *= mk;
       }
-      if (COV_XX_DMMA && !COV_XT_DFMA && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
+      if (COV_XX_DMMA && COV_XT_DFMA == 0 && !MASK) s89 = ld2(gl + j * 4 * GP + 8);
       dmma(aRA0, xa, sam);
       dmma(aRA1, sv, sam);
       tA8 = fma(s89.x, sam, tA8);
@@ -517,7 +521,7 @@ struct CovWarp {
       for (int j = 0; j < 8; j++) {
         double xa, sv, tv;
         double2 s89;
-        rowpart(j, xa, sv, s89, tv);
+        rowpart(j, xa, sv, s89, tv, false);
       }
       unsigned bits = mBi;
       int lo = 0;
@@ -554,7 +558,7 @@ struct CovWarp {
         for (int jj = 0; jj < 4; jj++) {
           double xa, sv, tv;
           double2 s89;
-          rowpart(4 * h + jj, xa, sv, s89, tv);
+          rowpart(4 * h + jj, xa, sv, s89, tv, true);
           cold_group(std::false_type{}, 4 * h + jj, xa, sv, s89, tv, sam[jj], sa89[jj], 0, 32);
         }
       }
@@ -564,7 +568,7 @@ struct CovWarp {
       for (int j = 0; j < 8; j++) {
         double xa, sv, tv;
         double2 s89;
-        rowpart(j, xa, sv, s89, tv);
+        rowpart(j, xa, sv, s89, tv, false);
         C0 += xa;
         C1 += sv;
         C2 += tv;
