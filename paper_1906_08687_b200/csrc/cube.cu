@@ -866,7 +866,10 @@ __device__ __forceinline__ unsigned div_rinv(unsigned n, unsigned d, double rinv
   rem = (unsigned)r;
   return q;
 }
-__global__ void __launch_bounds__(256) k_rec_reduce(const __grid_constant__ RecReduce r) {
+#ifndef REC_RED_MINB
+#define REC_RED_MINB 1  // resident CTAs per SM the register budget is sized for
+#endif
+__global__ void __launch_bounds__(256, REC_RED_MINB) k_rec_reduce(const __grid_constant__ RecReduce r) {
   // the UDAF coefficients and the rollups in shared memory (read by every group)
   extern __shared__ __align__(16) unsigned char rsm[];
   const Rollup* der = r.der;
