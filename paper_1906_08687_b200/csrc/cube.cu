@@ -867,7 +867,7 @@ __device__ __forceinline__ unsigned div_rinv(unsigned n, unsigned d, double rinv
   return q;
 }
 #ifndef REC_RED_MINB
-#define REC_RED_MINB 1  // resident CTAs per SM the register budget is sized for
+#define REC_RED_MINB 5  // resident CTAs per SM the register budget is sized for (C5 run, same box: 1 9.59, 5 9.21, 6 9.37 ms)
 #endif
 __global__ void __launch_bounds__(256, REC_RED_MINB) k_rec_reduce(const __grid_constant__ RecReduce r) {
   // the UDAF coefficients and the rollups in shared memory (read by every group)

@@ -66,3 +66,36 @@ def test_bad_load_mode_rejected():
         assert lmfao.STATUS[s] == "LMFAO_ERR_INVALID_ARG"
     finally:
         e.close()
+
+
+@pytest.mark.parametrize("seed", [0, 2, 4, 6])
+def test_deferred_load_multi_root(seed):
+    """Deferred columns may still be in flight when prepare returns (plan waits for them); a
+    query placed at another root copies every relation into a secondary context inside
+    add_query, which must wait for the copies first.  Pinned (deferred) columns vs the oracle,
+    on random trees whose batches use other roots."""
+    from paper_1906_08687_b200 import lmfao
+    db = synth.random_db(300 + seed, max_rels=5, max_rows=60_000, unique_child_keys=True)
+    ints = {a for r in db.relations for a, v in r.cols.items() if v.dtype == np.int32}
+    batch = synth.random_batch(seed, db, n_queries=5, groupby_ok=lambda a: a in ints)
+    ref = oracle.evaluate(db, batch)
+    cols = pinned(db)
+    e = lmfao.Engine()
+    try:
+        for r in db.relations:
+            e.add_relation(r.name, cols[r.name])
+        e.set_join_tree(db.root, db.edges)
+        e.prepare()
+        kept = []
+        for qi, q in enumerate(batch):
+            try:
+                kept.append((qi, e.add_query(q.groupby, q.udafs)))
+            except lmfao.LmfaoError as ex:
+                assert ex.name == "LMFAO_ERR_UNSUPPORTED", ex
+        e.plan()
+        e.run()
+        got = [e.fetch(q) for _, q in kept]
+    finally:
+        e.close()
+    assert kept
+    assert_parity(got, [ref[qi] for qi, _ in kept], [batch[qi] for qi, _ in kept])
