@@ -290,7 +290,13 @@ struct RtBigArgs {
   int in_smem;
   double* out;  // [ncell][3] at its goff
 };
-__global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArgs a) {
+#ifndef RT_BIG_THREADS
+#define RT_BIG_THREADS 512
+#endif
+#ifndef RT_BIG_U
+#define RT_BIG_U 4
+#endif
+__global__ void __launch_bounds__(RT_BIG_THREADS) k_rt_big(const __grid_constant__ RtBigArgs a) {
   extern __shared__ unsigned char bsm[];
   unsigned* cnt = reinterpret_cast<unsigned*>(bsm);
   double* sums = reinterpret_cast<double*>(bsm + ((a.ncell * 4 + 15) & ~15));
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(512) k_rt_big(const __grid_constant__ RtBigArg
   }
   // RT_BIG_U rows per thread per step, their loads issued together (one CTA of 16 warps per SM:
   // one row at a time left the warps waiting on their loads, 62 % long-scoreboard stalls)
-  constexpr int U = 4;
+  constexpr int U = RT_BIG_U;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r0 < a.nrows; r0 += U * stride) {
     double yv[U];
@@ -894,7 +900,7 @@ cudaError_t FastRT::pass(lmfao_ctx* c, cudaStream_t st, const uint8_t* fp, const
     const size_t smem = (size_t)((h.ncell * 4 + 15) & ~15) + (size_t)h.ncell * 16;
     ba.in_smem = smem <= 200 * 1024;
     ba.out = accp + h.goff;
-    k_rt_big<<<148, 512, ba.in_smem ? smem : 0, st>>>(ba);
+    k_rt_big<<<148, RT_BIG_THREADS, ba.in_smem ? smem : 0, st>>>(ba);
     launches_add(1);
   }
   if (nlev > 0 && R.nrows > 0 && !dhl.empty()) {
