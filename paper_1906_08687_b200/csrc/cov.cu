@@ -54,11 +54,17 @@ constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | 
 #ifndef COV_FIN_BLOCKS
 #define COV_FIN_BLOCKS 296
 #endif
-#ifndef COV_SUM_SPLIT
-#define COV_SUM_SPLIT 8
+#ifndef COV_SUM_SP  // k_cov_sum: the scan's per-item partial rows in SUM_SP chunks, the fin partials in
+#define COV_SUM_SP 16  // SUM_SF chunks (one CTA per chunk and 32 elements; 12 x 16 + 44 x 2 = 280 CTAs, one
+#endif                 // wave), the chunk sums added again by k_cov_assemble (was 8 and 8: 57 x 8 CTAs)
+#ifndef COV_SUM_SF
+#define COV_SUM_SF 2
 #endif
 constexpr int FIN_BLOCKS = COV_FIN_BLOCKS;
-constexpr int SUM_SPLIT = COV_SUM_SPLIT;  // k_cov_sum: partial rows in SUM_SPLIT chunks (grid y), summed again by k_cov_assemble
+constexpr int SUM_SP = COV_SUM_SP, SUM_SF = COV_SUM_SF;
+constexpr int SUM_CTAS = (NPART / 32) * SUM_SP + (NFIN / 32) * SUM_SF;
+constexpr int SRC_N = SUM_SP * NPART + SUM_SF * NFIN;  // src: [SUM_SP][NPART] | [SUM_SF][NFIN]
+static_assert(NPART % 32 == 0 && NFIN % 32 == 0, "k_cov_sum: whole 32-element columns");
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int KEYMASK = 0x3fffffff;  // dense key; bit 31 = a run starts at this row (at this level),
 constexpr int RUN_END = 0x40000000;  // bit 30 = the run (at this level) ends after this row
@@ -144,6 +150,12 @@ __device__ __forceinline__ double red4(double v) {
   return v;
 }
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+// Programmatic dependent launch (the run's kernel chain dims -> scan -> fin -> sum -> assemble):
+// a kernel launched with the PDL attribute may start while its predecessor drains; it runs only
+// work on plan-time data before pdl_wait(), which returns once the predecessor grid has completed
+// and its writes are visible.  Without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Scan layout of the root (built once at plan time, like the sort at prepare): per
 // 32-row block b, x in the DMMA lane order [group j][lane 4m+k] = x_m[32b+4j+k] (0 for
@@ -648,7 +660,11 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     if (!(g.ablate & 1)) gather_rows(g, wbase + stage * SBLK, sa(gbase + gslot * STG_G), lane);
   };
 
-  // ---- pipeline prologue: the first CF blocks of the sequence in flight, gathers of block 0
+  // ---- pipeline prologue: the first CF blocks of the sequence in flight, gathers of block 0.
+  // A warp without a static chunk takes its first item from the work counter, which k_cov_dims
+  // clears: it waits for that grid first; the others issue their first fact loads before.
+  const bool dyn_first = gw >= g.nstatic;
+  if (dyn_first) pdl_wait();
   grab();
   int pslot = 0, pitem = ring[0];  // the block being processed: pb of item pitem = [pbeg, pend)
   int pb = 0, pbeg = 0, pend = 0;
@@ -672,6 +688,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     if (fitem < nitems) issue_fact(fb, s);
     f_advance();
   }
+  if (!dyn_first) pdl_wait();  // the view rows (k_cov_dims) and the cleared H / work buffers
   if (pitem < nitems) {
     mbar_wait(&bar_f[0], 0);
     issue_gather(0, 0);
@@ -713,6 +730,7 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
     fph = fph1;
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  pdl_trigger();
 
   // ---- the CTA's last warp to finish moves the H_L table to global
   __threadfence_block();
@@ -738,8 +756,13 @@ struct DimTables {
   int n[3];
   int64_t nk[3];
   double* V[3];
+  unsigned* z;  // the run's cleared words (work counter, H_A, H_L): zeroed here instead of a memset node
+  int64_t nz;
 };
 __global__ void k_cov_dims(DimTables d) {
+  pdl_trigger();  // k_cov's prologue (fact loads) may start on SMs this grid frees
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.nz; i += (int64_t)gridDim.x * blockDim.x)
+    d.z[i] = 0u;
   const int64_t n0 = d.nk[0], n1 = d.nk[1], n2 = d.nk[2];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n0 + n1 + n2;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -783,6 +806,8 @@ struct FinArgs {
 __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
   const int lane = threadIdx.x & 31, k = lane & 3, m = lane >> 2, w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * 8 + w, GW = (int64_t)gridDim.x * 8;
+  pdl_wait();
+  pdl_trigger();
   double mL[4][2] = {}, mA[4][2] = {}, mB[4][2] = {}, rb[5][2][2] = {};
   auto srow = [&](const double* V, int64_t kk, bool v, double& s0, double& s1) {
     const double* row = V + (size_t)kk * GP;
@@ -865,39 +890,60 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
 // src[0:NPART] = Σ_warp scan partials; src[NPART:NPART+NFIN] = Σ_b fin partials.  A CTA per 32
 // consecutive outputs: lane = output (coalesced rows), warp r of 32 sums rows r, r + 32, ...;
 // then a fixed-order sum over the warps (deterministic).
-// src[g][e] = Σ of chunk g (of SUM_SPLIT) of the partial rows of element e, fixed order
+// src = chunk sums of the partial rows, per element e: the scan's (e < NPART) in SUM_SP chunks,
+// the fin's in SUM_SF chunks.  A CTA per (chunk, 32 consecutive elements): lane = element
+// (coalesced rows), warp r of 32 sums rows r, r + 32, ... of the chunk, then a fixed-order sum
+// over the warps (deterministic).
 __global__ void __launch_bounds__(1024) k_cov_sum(const double* __restrict__ p1, int n1, const double* __restrict__ p2,
                                                   int n2, double* __restrict__ src) {
-  const int e = blockIdx.x * 32 + (threadIdx.x & 31), r = threadIdx.x >> 5, g = blockIdx.y;
-  double s = 0.0;
-  if (e < NPART) {
-    const int b0 = n1 * g / SUM_SPLIT, b1 = n1 * (g + 1) / SUM_SPLIT;
-#pragma unroll 4
-    for (int b = b0 + r; b < b1; b += 32) s += p1[(size_t)b * NPART + e];
-  } else if (e < NPART + NFIN) {
-    const int b0 = n2 * g / SUM_SPLIT, b1 = n2 * (g + 1) / SUM_SPLIT;
-#pragma unroll 4
-    for (int b = b0 + r; b < b1; b += 32) s += p2[(size_t)b * NFIN + e - NPART];
+  pdl_wait();
+  pdl_trigger();
+  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;
+  int b = blockIdx.x;
+  const double* p;
+  int n, w, split, g, e;
+  double* dst;
+  if (b < (NPART / 32) * SUM_SP) {  // the heavy part first (scheduled first)
+    g = b / (NPART / 32);
+    e = (b % (NPART / 32)) * 32 + lane;
+    p = p1, n = n1, w = NPART, split = SUM_SP;
+    dst = src + (size_t)g * NPART + e;
+  } else {
+    b -= (NPART / 32) * SUM_SP;
+    g = b / (NFIN / 32);
+    e = (b % (NFIN / 32)) * 32 + lane;
+    p = p2, n = n2, w = NFIN, split = SUM_SF;
+    dst = src + (size_t)SUM_SP * NPART + (size_t)g * NFIN + e;
   }
+  const int b0 = (int)((int64_t)n * g / split), b1 = (int)((int64_t)n * (g + 1) / split);
+  double s = 0.0;
+#pragma unroll 4
+  for (int i = b0 + r; i < b1; i += 32) s += p[(size_t)i * w + e];
   __shared__ double red[32][33];
-  red[r][threadIdx.x & 31] = s;
+  red[r][lane] = s;
   __syncthreads();
-  if (r == 0 && e < NPART + NFIN) {
+  if (r == 0) {
     double t = 0.0;
-    for (int i = 0; i < 32; i++) t += red[i][threadIdx.x];
-    src[(size_t)g * (NPART + NFIN) + e] = t;
+    for (int i = 0; i < 32; i++) t += red[i][lane];
+    *dst = t;
   }
 }
 __device__ __forceinline__ double cov_src(const double* __restrict__ src, int e) {
   double t = 0.0;
+  if (e < NPART) {
 #pragma unroll
-  for (int g = 0; g < SUM_SPLIT; g++) t += src[(size_t)g * (NPART + NFIN) + e];
+    for (int g = 0; g < SUM_SP; g++) t += src[(size_t)g * NPART + e];
+  } else {
+#pragma unroll
+    for (int g = 0; g < SUM_SF; g++) t += src[(size_t)SUM_SP * NPART + (size_t)g * NFIN + e - NPART];
+  }
   return t;
 }
 
 __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __restrict__ toff,
                                const int32_t* __restrict__ tidx, const double* __restrict__ tcoef, int nout,
                                double* __restrict__ out, int count_idx, unsigned long long* __restrict__ count) {
+  pdl_wait();
   for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * cov_src(src, tidx[t]);
@@ -953,13 +999,34 @@ cudaError_t cov_kernel_attr(int NS) {  // per device: called at plan time on the
   if (NS == 1) return cudaFuncSetAttribute(k_cov<1, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return cudaFuncSetAttribute(k_cov<2, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
+// launch with the programmatic-stream-serialization attribute (LMFAO_PDL=0: plain launches)
+bool pdl_on() {
+  static const int on = [] {
+    const char* e = std::getenv("LMFAO_PDL");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on;
+}
+template <typename... KA, typename... A>
+cudaError_t launch_pdl(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
 template <int W>
 cudaError_t launch_cov_w(int NS, const CovArgs& g, int grid, cudaStream_t st) {
   constexpr int smem = CovCfg<W>::SMEM;
-  if (NS == 0) k_cov<0, W><<<grid, W * 32, smem, st>>>(g);
-  else if (NS == 1) k_cov<1, W><<<grid, W * 32, smem, st>>>(g);
-  else k_cov<2, W><<<grid, W * 32, smem, st>>>(g);
-  return cudaGetLastError();
+  if (NS == 0) return launch_pdl(k_cov<0, W>, grid, W * 32, smem, st, g);
+  if (NS == 1) return launch_pdl(k_cov<1, W>, grid, W * 32, smem, st, g);
+  return launch_pdl(k_cov<2, W>, grid, W * 32, smem, st, g);
 }
 cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) { return launch_cov_w<COV_W>(NS, g, grid, st); }
 
@@ -967,9 +1034,10 @@ cudaError_t launch_cov(int NS, const CovArgs& g, int grid, cudaStream_t st) { re
 
 int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_done) {
   const Rel& R = c->rels[c->root];
-  CUDA_TRY(cudaMemsetAsync(zbuf.p, 0, zbytes, st));
   {  // (b) dimension views of the featured PK leaves
     DimTables d{};
+    d.z = zbuf.as<unsigned>();
+    d.nz = (int64_t)(zbytes / 4);
     CovLevel* lv[3] = {&L, &A, &B};
     int64_t tot = 0;
     for (int i = 0; i < 3; i++) {
@@ -980,10 +1048,9 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
       d.V[i] = lv[i]->V.as<double>();
       tot += d.nk[i] * GP;
     }
-    if (tot > 0) {
-      k_cov_dims<<<(unsigned)std::min<int64_t>((tot / GP + 255) / 256, 148 * 16), 256, 0, st>>>(d);
-      launches_add(1);
-    }
+    const int64_t nth = std::max<int64_t>(tot / GP, d.nz);
+    k_cov_dims<<<(unsigned)std::min<int64_t>((nth + 255) / 256, 148 * 16), 256, 0, st>>>(d);
+    launches_add(1);
   }
   CovArgs g{};
   g.nblk = nblk;
@@ -1023,12 +1090,14 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   f.VA = g.VA;
   f.nkA = NS >= 1 ? A.nk : 0;
   f.partials = finp.as<double>();
-  k_cov_fin<<<FIN_BLOCKS, 256, 8 * NFIN * 8, st>>>(f);
-  k_cov_sum<<<dim3((NPART + NFIN + 31) / 32, SUM_SPLIT), 1024, 0, st>>>(partials.as<double>(), nitems, finp.as<double>(),
-                                                      FIN_BLOCKS, src.as<double>());
-  k_cov_assemble<<<(nout + 127) / 128 + 1, 128, 0, st>>>(src.as<double>(), toff.as<int32_t>(), tidx.as<int32_t>(),
-                                                         tcoef.as<double>(), nout, c->scalar_out.as<double>(),
-                                                         NPART + 18 * 16 + 10, c->scalar_count.as<unsigned long long>());
+  CUDA_TRY(launch_pdl(k_cov_fin, FIN_BLOCKS, 256, 8 * NFIN * 8, st, f));
+  CUDA_TRY(launch_pdl(k_cov_sum, SUM_CTAS, 1024, 0, st,
+                      (const double*)partials.as<double>(), (int)nitems, (const double*)finp.as<double>(),
+                      (int)FIN_BLOCKS, src.as<double>()));
+  CUDA_TRY(launch_pdl(k_cov_assemble, (nout + 127) / 128 + 1, 128, 0, st, (const double*)src.as<double>(),
+                      (const int32_t*)toff.as<int32_t>(), (const int32_t*)tidx.as<int32_t>(),
+                      (const double*)tcoef.as<double>(), (int)nout, c->scalar_out.as<double>(),
+                      (int)(NPART + 18 * 16 + 10), c->scalar_count.as<unsigned long long>()));
   launches_add(3);
   scalar_done = true;
   return cudaGetLastError();
@@ -1175,7 +1244,7 @@ FastPaths* plan_cov(lmfao_ctx* c) {
   const int NW = fc->grid * COV_W;
   fc->nblk = (R.nrows + 31) / 32;
   if (fc->finp.alloc((size_t)FIN_BLOCKS * NFIN * 8)) return nullptr;
-  if (fc->src.alloc((size_t)SUM_SPLIT * (NPART + NFIN) * 8)) return nullptr;
+  if (fc->src.alloc((size_t)SRC_N * 8)) return nullptr;
   {  // scan layout of the root: x in DMMA lane order + dense keys with run-start flags, one
      // 2432-byte block per 32 rows
     if (fc->scan.alloc((size_t)std::max<int64_t>(fc->nblk, 1) * SBLK)) return nullptr;
