@@ -176,3 +176,24 @@ def test_empty_root_and_empty_child():
     F = synth.Relation("F", {"a": np.zeros(0, np.int32), "x": np.zeros(0)})
     S = synth.Relation("S", {"a": np.array([1], np.int32), "y": np.array([2.0])})
     _check(synth.Database([F, S], "F", [("F", "S")]), [query([], ["1", "x*y"]), query(["a"], ["y"])])
+
+
+def test_pdl_off_bit_identical(tmp_path):
+    """The C2 run chain (dims -> scan -> fin -> sum -> assemble) is launched with programmatic
+    dependent launch; every kernel waits for its predecessor before its first dependent read,
+    so plain launches (LMFAO_PDL=0, read once per process: a subprocess) give the same bits."""
+    import subprocess
+    import sys
+    rows, dims = 400_003, (30, 200, 1500)
+    w = synth.config2(fact_rows=rows, dim_rows=dims)
+    a = run_gpu(w.db, w.batch, runs=3)
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (f"import sys, numpy as np; sys.path[:0] = [{here!r}, {os.path.dirname(here)!r}]\n"
+            "import synth\nfrom _parity import run_gpu\n"
+            f"w = synth.config2(fact_rows={rows}, dim_rows={dims!r})\n"
+            "o = run_gpu(w.db, w.batch, runs=3)\n"
+            f"np.save({str(tmp_path / 'v.npy')!r}, o[0][1]); np.save({str(tmp_path / 'c.npy')!r}, o[0][2])\n")
+    env = dict(os.environ, LMFAO_PDL="0")
+    subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+    assert np.array_equal(np.load(tmp_path / "c.npy"), a[0][2])
+    assert np.array_equal(np.load(tmp_path / "v.npy").view(np.uint64), a[0][1].view(np.uint64))
