@@ -54,6 +54,9 @@ constexpr int NFIN = 640 + 3 * 256;  // RBM[40][16] | ML[16][16] | MA[16][16] | 
 #ifndef COV_FIN_BLOCKS
 #define COV_FIN_BLOCKS 296
 #endif
+#ifndef COV_FIN_U
+#define COV_FIN_U 4  // k_cov_fin: key groups (4 keys each) whose loads are in flight together per warp
+#endif
 #ifndef COV_SUM_SP  // k_cov_sum: the scan's per-item partial rows in SUM_SP chunks, the fin partials in
 #define COV_SUM_SP 16  // SUM_SF chunks (one CTA per chunk and 32 elements; 12 x 16 + 44 x 2 = 280 CTAs, one
 #endif                 // wave), the chunk sums added again by k_cov_assemble (was 8 and 8: 57 x 8 CTAs)
@@ -816,7 +819,7 @@ __global__ void __launch_bounds__(256) k_cov_fin(FinArgs a) {
   };
   auto moments = [&](const unsigned* H, const double* V, int64_t nk, double (&acc)[4][2]) {
     const int64_t ng = (nk + 3) / 4, g0 = gw * ng / GW, g1 = (gw + 1) * ng / GW;
-    constexpr int U = 4;  // groups whose loads are in flight together
+    constexpr int U = COV_FIN_U;  // groups whose loads are in flight together
     for (int64_t gb = g0; gb < g1; gb += U) {
       double h[U], s0[U], s1[U];
 #pragma unroll
