@@ -754,15 +754,15 @@ __global__ void __launch_bounds__(W * 32, 1) k_cov(const __grid_constant__ CovAr
 // V[k][f] = col_f[k] for f < n, 0 for n <= f < GP, except V[k][10] = 1 (the constant of the
 // scan's t tile; primary-key leaf: row k has dense key k).
 struct DimTables {
-  const double* const* cols[3];
-  const int32_t* const* idx[3];  // per feature: row of its relation per dimension key (null: the key's own row)
+  const double* cols[3][GP];   // by value in the parameter space: no dependent pointer loads
+  const int32_t* idx[3][GP];   // per feature: row of its relation per dimension key (null: the key's own row)
   int n[3];
   int64_t nk[3];
   double* V[3];
   unsigned* z;  // the run's cleared words (work counter, H_A, H_L): zeroed here instead of a memset node
   int64_t nz;
 };
-__global__ void k_cov_dims(DimTables d) {
+__global__ void k_cov_dims(const __grid_constant__ DimTables d) {
   pdl_trigger();  // k_cov's prologue (fact loads) may start on SMs this grid frees
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.nz; i += (int64_t)gridDim.x * blockDim.x)
     d.z[i] = 0u;
@@ -960,7 +960,9 @@ struct CovLevel {
   int child = -1, rel = -1;
   std::vector<int> attrs;
   int64_t nk = 0;
-  DevBuf V, colptrs, idxptrs;
+  DevBuf V;
+  std::vector<const double*> hcols;  // the features' columns (k_cov_dims parameters)
+  std::vector<const int32_t*> hidx;
   std::vector<DevBuf> idx;  // composed foreign-key chains to the features of deeper relations
 };
 
@@ -1044,8 +1046,10 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
     CovLevel* lv[3] = {&L, &A, &B};
     int64_t tot = 0;
     for (int i = 0; i < 3; i++) {
-      d.cols[i] = (const double* const*)lv[i]->colptrs.p;
-      d.idx[i] = (const int32_t* const*)lv[i]->idxptrs.p;
+      for (size_t f = 0; f < lv[i]->hcols.size(); f++) {
+        d.cols[i][f] = lv[i]->hcols[f];
+        d.idx[i][f] = lv[i]->hidx[f];
+      }
       d.n[i] = (int)lv[i]->attrs.size();
       d.nk[i] = lv[i]->rel >= 0 ? lv[i]->nk : 0;
       d.V[i] = lv[i]->V.as<double>();
@@ -1226,13 +1230,9 @@ FastPaths* plan_cov(lmfao_ctx* c) {
       if (o != l.rel && !ix) return nullptr;
       ip.push_back(ix);
     }
-    if (l.colptrs.alloc(std::max<size_t>(cp.size(), 1) * sizeof(void*)) ||
-        l.idxptrs.alloc(std::max<size_t>(ip.size(), 1) * sizeof(void*)))
-      return nullptr;
-    if (!cp.empty() &&
-        (cudaMemcpyAsync(l.colptrs.p, cp.data(), cp.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream) ||
-         cudaMemcpyAsync(l.idxptrs.p, ip.data(), ip.size() * sizeof(void*), cudaMemcpyHostToDevice, c->stream)))
-      return nullptr;
+    if (cp.size() > (size_t)GP) return nullptr;
+    l.hcols = cp;
+    l.hidx = ip;
   }
   const int64_t nkA = fc->NS >= 1 ? fc->A.nk : 0;
   fc->off_HA = 16;
