@@ -947,10 +947,27 @@ __global__ void k_cov_assemble(const double* __restrict__ src, const int32_t* __
                                const int32_t* __restrict__ tidx, const double* __restrict__ tcoef, int nout,
                                double* __restrict__ out, int count_idx, unsigned long long* __restrict__ count) {
   pdl_wait();
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < nout; o += gridDim.x * blockDim.x) {
+  // a warp per output: lane (half, g) takes chunk g of every other term, then a fixed-order
+  // butterfly sum over the lanes (all loads of an output in flight together; deterministic)
+  static_assert(SUM_SP <= 16 && SUM_SF <= 16, "k_cov_assemble: one lane per chunk");
+  const int lane = threadIdx.x & 31, g = lane & 15, half = lane >> 4;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < nout; o += nw) {
     double s = 0.0;
-    for (int t = toff[o]; t < toff[o + 1]; t++) s += tcoef[t] * cov_src(src, tidx[t]);
-    out[o] = s;
+    const int t1 = toff[o + 1];
+    for (int t = toff[o] + half; t < t1; t += 2) {
+      const int e = tidx[t];
+      double v = 0.0;
+      if (e < NPART) {
+        if (g < SUM_SP) v = src[(size_t)g * NPART + e];
+      } else if (g < SUM_SF) {
+        v = src[(size_t)SUM_SP * NPART + (size_t)g * NFIN + e - NPART];
+      }
+      s = fma(tcoef[t], v, s);
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(FULL, s, d);
+    if (lane == 0) out[o] = s;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = (unsigned long long)cov_src(src, count_idx);
 }
@@ -1101,7 +1118,7 @@ int FastCov::run(lmfao_ctx* c, const NodeArgs&, cudaStream_t st, bool& scalar_do
   CUDA_TRY(launch_pdl(k_cov_sum, SUM_CTAS, 1024, 0, st,
                       (const double*)partials.as<double>(), (int)nitems, (const double*)finp.as<double>(),
                       (int)FIN_BLOCKS, src.as<double>()));
-  CUDA_TRY(launch_pdl(k_cov_assemble, (nout + 127) / 128 + 1, 128, 0, st, (const double*)src.as<double>(),
+  CUDA_TRY(launch_pdl(k_cov_assemble, (nout + 7) / 8 + 1, 256, 0, st, (const double*)src.as<double>(),
                       (const int32_t*)toff.as<int32_t>(), (const int32_t*)tidx.as<int32_t>(),
                       (const double*)tcoef.as<double>(), (int)nout, c->scalar_out.as<double>(),
                       (int)(NPART + 18 * 16 + 10), c->scalar_count.as<unsigned long long>()));
