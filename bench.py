@@ -176,13 +176,18 @@ def run_reference(args, rank, world):
         if i >= args.warmup:
             per_step.append(rows / b["value"])
     cores = b["cores"]
+    N = w.db.rel(w.db.root).nrows
     t = sum(per_step)
     value = rows * args.steps / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": args.config, "fact_rows": rows,
-                                           "sample": f"first {rows} fact rows"},
+            "data": "synthetic",
+            # the own arm's workload, named the same way; each step evaluates a bounded sample of it
+            "config": {"workload": f"{args.config}: {w.batch[0].name if w.batch else ''} batch, "
+                                   f"{N} fact rows, {synth.n_aggregates(w.batch)} aggregates",
+                       "fact_rows": N, "aggregates": synth.n_aggregates(w.batch),
+                       "sample": f"first {rows} of {N} fact rows per step"},
             "cpu_baseline": {"value": value, "unit": "rows/s", "cores": cores, "kind": "oracle",
                              "cpu_model": b.get("cpu_model"),
                              "sample": f"first {rows} fact rows of {args.config} per step, {cores} OpenMP threads"},
